@@ -1,0 +1,207 @@
+/*
+ * hgrd_gpu.h — C ABI of the B200 race-check stage (libhgrd_gpu.so).
+ *
+ * Drop-in for the data-parallel core of the reference's concrete oracle
+ * (arXiv 2604.02106 "HGRD"; reference /root/reference/proj):
+ *
+ *   reference                                   replaced by
+ *   ------------------------------------------  ------------------------------
+ *   Interpreter::execLaunch thread loop +       hgrd_gpu_check_launch
+ *     runThread/runThreadStmt                     (one lowered launch: expansion
+ *     src/oracle.cpp:440-646                       of every (blockIdx, threadIdx)
+ *   Interpreter::detectRaces                       instance + conflict detection
+ *     src/oracle.cpp:730-784                       on the GPU)
+ *   Interpreter buffers_ (vector<long long>)    hgrd_gpu_buffer_alloc/_write/_read
+ *     src/oracle.cpp:283, 789                     (device-resident int64 buffers)
+ *   hgrd::runConcrete                           hgrd_gpu_run_concrete_json
+ *     include/hgrd/oracle.hpp:57                  (host front end + GPU stage)
+ *   hgrd::enumerateVerdict                      hgrd_gpu_enumerate_verdict_json
+ *     include/hgrd/oracle.hpp:75
+ *   hgrd::countInputs  oracle.hpp:79            hgrd_gpu_count_inputs
+ *
+ * Conventions: plain pointers and sizes only; negative return codes are
+ * errors (no exceptions cross the ABI); the caller owns every descriptor and
+ * output array, a context owns its device memory; calls on one context are
+ * serialised on its CUDA stream, distinct contexts may be driven from
+ * distinct host threads.  There is no CPU fallback: on a machine without a
+ * usable sm_100 device hgrd_gpu_create fails with HGRD_GPU_ENODEV.
+ */
+#ifndef HGRD_GPU_H
+#define HGRD_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ------------------------------------------------------- */
+#define HGRD_GPU_OK 0
+#define HGRD_GPU_EINVAL (-22)   /* malformed descriptor */
+#define HGRD_GPU_E2BIG (-7)     /* an output array was too small */
+#define HGRD_GPU_ENODEV (-19)   /* no CUDA device / not sm_100 */
+#define HGRD_GPU_ENOMEM (-12)   /* device allocation failed */
+#define HGRD_GPU_ECUDA (-5)     /* CUDA runtime error (message: hgrd_gpu_last_error) */
+#define HGRD_GPU_ENOTSUP (-95)  /* launch outside the supported envelope */
+
+/* ---- lowered kernel bytecode (register machine over wrapping int64) ---- */
+/* One MiniCU kernel body (reference include/hgrd/ast.hpp:101-178) lowered by
+ * the host to straight-line code.  Evaluation order follows the reference
+ * interpreter exactly: binary operators evaluate their RIGHT operand first
+ * (src/oracle.cpp:500 as compiled by GCC), stores evaluate index then value
+ * (:569-570), atomics index, value, compare (:580-583), loops re-evaluate
+ * their bound every iteration (:629-631), and one STEP is charged per
+ * executed statement and per loop test (:561, :630). */
+enum hgrd_gpu_opcode {
+  HGRD_OP_END = 0,      /* thread done (falls off the body / return)      */
+  HGRD_OP_CONST = 1,    /* r[a] = imm                                      */
+  HGRD_OP_MOV = 2,      /* r[a] = r[b]                                     */
+  HGRD_OP_BUILTIN = 3,  /* r[a] = builtin[sub/3][sub%3] (tid,bid,bdim,gdim)*/
+  HGRD_OP_BIN = 4,      /* r[a] = r[b] <sub> r[c]   (enum hgrd_gpu_binop)  */
+  HGRD_OP_LOAD = 5,     /* r[a] = site imm [r[b]]; sub&1: value is needed  */
+  HGRD_OP_STORE = 6,    /* site imm [r[a]] = r[b]                          */
+  HGRD_OP_ATOMIC = 7,   /* site imm [r[a]] op= r[b] (cmp r[c] for CAS)     */
+  HGRD_OP_SYNCTHREADS = 8,
+  HGRD_OP_SYNCWARP = 9,
+  HGRD_OP_FENCE = 10,   /* sub = scope                                     */
+  HGRD_OP_STEP = 11,    /* charge one step; imm = statement id (trap loc)  */
+  HGRD_OP_JZ = 12,      /* if r[a] == 0 goto imm                           */
+  HGRD_OP_JMP = 13      /* goto imm                                        */
+};
+
+/* reference BinOp order, include/hgrd/ast.hpp:31-45 */
+enum hgrd_gpu_binop {
+  HGRD_ADD, HGRD_SUB, HGRD_MUL, HGRD_DIV, HGRD_MOD, HGRD_LT, HGRD_LE,
+  HGRD_GT, HGRD_GE, HGRD_EQ, HGRD_NE, HGRD_AND, HGRD_OR
+};
+
+typedef struct hgrd_gpu_insn {
+  uint8_t op;
+  uint8_t sub;
+  uint16_t a, b, c;
+  uint16_t pad;
+  int64_t imm;
+} hgrd_gpu_insn; /* 16 bytes */
+
+/* Access sites: one per ArrayLoad / ArrayStoreStmt / AtomicStmt node. */
+enum hgrd_gpu_site_kind { HGRD_SITE_LOAD = 0, HGRD_SITE_STORE = 1, HGRD_SITE_ATOMIC = 2 };
+enum hgrd_gpu_atomic_op { HGRD_ATOMIC_CAS = 0, HGRD_ATOMIC_EXCH = 1, HGRD_ATOMIC_ADD = 2 };
+enum hgrd_gpu_scope { HGRD_SCOPE_NONE = 0, HGRD_SCOPE_BLOCK = 1, HGRD_SCOPE_DEVICE = 2 };
+
+typedef struct hgrd_gpu_site {
+  int32_t loc;       /* source-location id; id order == SourceLoc order      */
+  int32_t param;     /* kernel parameter index the access goes through      */
+  uint8_t kind;      /* hgrd_gpu_site_kind                                  */
+  uint8_t atomic_op; /* hgrd_gpu_atomic_op (atomics only)                   */
+  uint8_t scope;     /* hgrd_gpu_scope (atomics only; reference Event.atomicScope) */
+  uint8_t pad0;
+  int32_t pad1;
+} hgrd_gpu_site; /* 16 bytes */
+
+/* ---- one launch after host analysis fixed its parameters --------------- */
+#define HGRD_LAUNCH_SEQUENTIAL 1u /* loaded values feed addresses/control:
+                                     run instances in canonical order with
+                                     memory effects (reference :440-465) */
+#define HGRD_LAUNCH_PAIRWISE 2u   /* force the exhaustive pairwise detector
+                                     (always used when the kernel holds
+                                     fence + CAS/Exch lock idioms) */
+#define HGRD_LAUNCH_NO_WITNESS 4u /* skip first-pair witness extraction */
+
+typedef struct hgrd_gpu_launch {
+  const hgrd_gpu_insn *code;
+  uint32_t n_code;
+  uint32_t n_regs;
+  const int64_t *reg_init;       /* n_regs initial values (scalar params)   */
+  const hgrd_gpu_site *sites;
+  uint32_t n_sites;
+  uint32_t n_locs;
+  const int32_t *param_handle;   /* per kernel param: buffer handle or -1    */
+  uint32_t n_params;
+  uint32_t flags;
+  int64_t grid[3];
+  int64_t block[3];
+  int64_t warp_size;
+  int64_t step_budget;           /* steps left before "step budget exhausted" */
+} hgrd_gpu_launch;
+
+/* One realised race key (locA, locB, kind) with the reference's
+ * first-found report fields (array = site_x's parameter name, address =
+ * index; src/oracle.cpp:766-780) and the witness pair: the first (x, y)
+ * in reference iteration order, i.e. the minimum (handle, index) element,
+ * then the lexicographically first event pair on it. */
+typedef struct hgrd_gpu_race {
+  int32_t loc_a, loc_b; /* loc_a <= loc_b */
+  int32_t kind;         /* 0 INTER-BLOCK, 1 INTRA-BLOCK, 2 INTRA-WARP */
+  int32_t site_x, site_y;
+  int32_t handle;
+  int64_t index;
+  int64_t thread_x, thread_y; /* dense launch thread numbers (:457-460) */
+  int32_t seq_x, seq_y;       /* per-thread event sequence numbers (:538) */
+} hgrd_gpu_race;
+
+enum hgrd_gpu_trap_kind { HGRD_TRAP_OOB = 0, HGRD_TRAP_UNALLOCATED = 1 };
+typedef struct hgrd_gpu_trap {
+  int32_t site;
+  int32_t kind;
+  int64_t thread;
+} hgrd_gpu_trap;
+
+typedef struct hgrd_gpu_result {
+  hgrd_gpu_race *races;  /* caller-owned */
+  uint32_t race_cap;
+  uint32_t n_races;      /* set; > race_cap with HGRD_GPU_E2BIG */
+  hgrd_gpu_trap *traps;  /* first trap_cap traps in canonical order */
+  uint32_t trap_cap;
+  uint32_t n_traps;      /* traps recorded (<= trap_cap)               */
+  uint64_t n_traps_total;/* traps raised before the end / abort        */
+  int64_t steps;         /* steps charged by this launch               */
+  uint64_t instances;    /* in-bounds accesses = reference Events      */
+  uint64_t records;      /* events kept for detection (written buffers)*/
+  int32_t aborted;       /* step budget ran out inside this launch     */
+  int32_t abort_stmt;    /* STEP imm at which it ran out               */
+  uint32_t mode;         /* flags actually used                        */
+  float device_ms;       /* device time of the check (CUDA events)     */
+} hgrd_gpu_result;
+
+/* ---- contexts and device-resident buffers ------------------------------ */
+typedef struct hgrd_gpu_ctx hgrd_gpu_ctx;
+
+int hgrd_gpu_create(int device, hgrd_gpu_ctx **out);
+void hgrd_gpu_destroy(hgrd_gpu_ctx *ctx);
+const char *hgrd_gpu_last_error(hgrd_gpu_ctx *ctx);
+
+/* Drop every buffer (start of a runConcrete). */
+int hgrd_gpu_buffers_reset(hgrd_gpu_ctx *ctx);
+/* Zero-filled int64 buffer (reference :282-285); handles are dense from 0. */
+int hgrd_gpu_buffer_alloc(hgrd_gpu_ctx *ctx, int64_t elems, int32_t *handle);
+int hgrd_gpu_buffer_write(hgrd_gpu_ctx *ctx, int32_t handle, int64_t offset,
+                          int64_t count, const int64_t *src);
+int hgrd_gpu_buffer_read(hgrd_gpu_ctx *ctx, int32_t handle, int64_t offset,
+                         int64_t count, int64_t *dst);
+
+/* The race-check stage for one launch. */
+int hgrd_gpu_check_launch(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
+                          hgrd_gpu_result *result);
+
+/* ---- reference-shaped entry points (JSON in / JSON out) ---------------- */
+/* cfg: {"gridCap":[3],"blockCap":[3],"warpSize":n,"inputs":[..],
+ *       "maxThreads":n,"maxArrayElems":n,"maxSteps":n}  (ExecConfig)
+ * out: {"races":[{kind,locA,locB,array,address}],"traps":[..],
+ *       "launchesRun","launchesSkipped","assertStopped","indirectIndexing",
+ *       "launchRecords":[..],"witnesses":[..],"stats":{..}}  (OracleResult)
+ * *out must be released with hgrd_gpu_free. */
+int hgrd_gpu_run_concrete_json(hgrd_gpu_ctx *ctx, const char *source,
+                               const char *file_name, const char *cfg_json,
+                               char **out);
+/* caps: {"gridCap","blockCap","inputSet","warpSizes","maxThreads","maxConfigs"}
+ * out: {"races":[{kind,locA,locB,warpSize}]} in discovery order. */
+int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
+                                    const char *file_name,
+                                    const char *caps_json, char **out);
+int hgrd_gpu_count_inputs(const char *source, const char *file_name);
+void hgrd_gpu_free(char *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGRD_GPU_H */

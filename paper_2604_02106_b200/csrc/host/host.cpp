@@ -1,0 +1,1241 @@
+// Host interpreter of the race-check stage.  Mirrors the reference's
+// Interpreter (reference src/oracle.cpp:55-437) so that every launch
+// reaches the backend with exactly the parameters, dimensions, buffer
+// contents, step budget and trap slots the reference would use, and folds
+// the backend's per-launch result back the way the reference does
+// (first-insert dedup across launches :776-780, final sort :76).
+//
+// Memory model.  The reference runs MiniCU threads to completion one after
+// another (:440-465), so loads observe earlier threads' stores.  A launch is
+// checked in one of two modes (chosen here, executed by the backend):
+//  * PARALLEL: no loaded value that can reach an index / condition / loop
+//    bound (LoweredKernel::siteValueNeeded) reads a buffer the launch
+//    writes, so every instance's accesses are independent of the order
+//    threads run in; the value-needed loads read the launch-entry buffers.
+//    The launch's own stores are not materialised: its written buffers
+//    become "stale".
+//  * SEQUENTIAL: instances run in canonical order with memory effects.
+// A stale buffer read by the host, or read by a later launch where the
+// value matters, restarts the run in conservative mode, where every launch
+// that writes memory runs SEQUENTIAL, so buffers are always exact.
+#include "host.hpp"
+
+#include <algorithm>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+#include <tuple>
+
+namespace hgrdgpu {
+
+const LoweredKernel &CompiledProgram::kernel(const Function *k) {
+  auto it = kernels.find(k);
+  if (it == kernels.end())
+    it = kernels.emplace(k, lowerKernel(*k)).first;
+  return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// static scans (reference src/oracle.cpp:86-123 and :805-861)
+
+bool hasIndirectIndexing(const Program &p) {
+  bool found = false;
+  std::function<void(const Expr &, bool)> scanE = [&](const Expr &e, bool inIndex) {
+    if (e.kind == EK::Load) {
+      if (inIndex)
+        found = true;
+      scanE(*e.index, true);
+    } else if (e.kind == EK::Binary) {
+      scanE(*e.lhs, inIndex);
+      scanE(*e.rhs, inIndex);
+    }
+  };
+  std::function<void(const Body &)> scanB = [&](const Body &b) {
+    for (const auto &s : b) {
+      switch (s->kind) {
+      case SK::Store:
+        scanE(*s->index, true);
+        scanE(*s->value, false);
+        break;
+      case SK::Atomic:
+        scanE(*s->index, true);
+        break;
+      case SK::Assign:
+        if (s->value)
+          scanE(*s->value, false);
+        break;
+      case SK::If:
+        scanB(s->body);
+        scanB(s->elseBody);
+        break;
+      case SK::For:
+        scanB(s->body);
+        break;
+      default:
+        break;
+      }
+    }
+  };
+  for (const auto &k : p.kernels)
+    scanB(k.body);
+  return found;
+}
+
+int countInputs(const Program &p) {
+  int n = 0;
+  std::function<void(const Expr &)> scanE = [&](const Expr &e) {
+    if (e.kind == EK::Input)
+      ++n;
+    else if (e.kind == EK::Binary) {
+      scanE(*e.lhs);
+      scanE(*e.rhs);
+    } else if (e.kind == EK::Load) {
+      scanE(*e.index);
+    }
+  };
+  std::function<void(const Body &)> scanB = [&](const Body &b) {
+    for (const auto &sp : b) {
+      const Stmt &s = *sp;
+      switch (s.kind) {
+      case SK::Assign:
+        if (s.value)
+          scanE(*s.value);
+        break;
+      case SK::Store:
+        scanE(*s.index);
+        scanE(*s.value);
+        break;
+      case SK::Assert:
+        scanE(*s.cond);
+        break;
+      case SK::Alloc:
+        scanE(*s.width);
+        if (s.height)
+          scanE(*s.height);
+        break;
+      case SK::If:
+        scanE(*s.cond);
+        scanB(s.body);
+        scanB(s.elseBody);
+        break;
+      case SK::For:
+        scanE(*s.init);
+        scanE(*s.bound);
+        scanB(s.body);
+        break;
+      case SK::Launch:
+        for (const auto &d : s.grid)
+          scanE(*d);
+        for (const auto &d : s.block)
+          scanE(*d);
+        for (const auto &a : s.args)
+          scanE(*a);
+        break;
+      case SK::Call:
+        for (const auto &a : s.args)
+          scanE(*a);
+        break;
+      case SK::Return:
+        if (s.value)
+          scanE(*s.value);
+        break;
+      default:
+        break;
+      }
+    }
+  };
+  for (const auto &f : p.hosts)
+    scanB(f.body);
+  return n;
+}
+
+std::unique_ptr<CompiledProgram> compileProgram(std::unique_ptr<Program> p) {
+  auto cp = std::make_unique<CompiledProgram>();
+  cp->indirectIndexing = hasIndirectIndexing(*p);
+  cp->inputs = countInputs(*p);
+  cp->program = std::move(p);
+  return cp;
+}
+
+const char *raceKindName(int kind) {
+  switch (kind) {
+  case 0:
+    return "INTER-BLOCK";
+  case 1:
+    return "INTRA-BLOCK";
+  case 2:
+    return "INTRA-WARP";
+  }
+  return "?";
+}
+
+// ---------------------------------------------------------------------------
+
+namespace {
+
+// names assigned anywhere in a body (reference src/host_facts.cpp:101-121)
+std::set<std::string> assignedNames(const Body &b) {
+  std::set<std::string> names;
+  std::function<void(const Body &)> walk = [&](const Body &body) {
+    for (const auto &s : body) {
+      if (s->kind == SK::Assign) {
+        names.insert(s->name);
+      } else if (s->kind == SK::If) {
+        walk(s->body);
+        walk(s->elseBody);
+      } else if (s->kind == SK::For) {
+        names.insert(s->aux);
+        walk(s->body);
+      } else if (s->kind == SK::Alloc) {
+        names.insert(s->name);
+        if (!s->aux.empty())
+          names.insert(s->aux);
+      }
+    }
+  };
+  walk(b);
+  return names;
+}
+
+int64_t wrapAdd(int64_t a, int64_t b) {
+  return static_cast<int64_t>(static_cast<uint64_t>(a) + static_cast<uint64_t>(b));
+}
+int64_t wrapSub(int64_t a, int64_t b) {
+  return static_cast<int64_t>(static_cast<uint64_t>(a) - static_cast<uint64_t>(b));
+}
+int64_t wrapMul(int64_t a, int64_t b) {
+  return static_cast<int64_t>(static_cast<uint64_t>(a) * static_cast<uint64_t>(b));
+}
+
+// reference applyBinOp, src/oracle.cpp:179-209 (wrapping int64)
+int64_t binop(Bin op, int64_t l, int64_t r) {
+  switch (op) {
+  case Bin::Add:
+    return wrapAdd(l, r);
+  case Bin::Sub:
+    return wrapSub(l, r);
+  case Bin::Mul:
+    return wrapMul(l, r);
+  case Bin::Div:
+    return r == 0 ? 0 : (r == -1 ? wrapSub(0, l) : l / r);
+  case Bin::Mod:
+    return r == 0 || r == -1 ? 0 : l % r;
+  case Bin::Lt:
+    return l < r;
+  case Bin::Le:
+    return l <= r;
+  case Bin::Gt:
+    return l > r;
+  case Bin::Ge:
+    return l >= r;
+  case Bin::Eq:
+    return l == r;
+  case Bin::Ne:
+    return l != r;
+  case Bin::And:
+    return (l != 0 && r != 0) ? 1 : 0;
+  case Bin::Or:
+    return (l != 0 || r != 0) ? 1 : 0;
+  }
+  return 0;
+}
+
+struct Abort {};            // TrapAbort / assert stop
+struct NeedConservative {}; // a stale buffer's value was needed
+struct BackendFail {
+  int code;
+  std::string msg;
+};
+
+class HostRun {
+public:
+  HostRun(CompiledProgram &cp, const ExecConfig &cfg, LaunchBackend &be,
+          bool conservative)
+      : cp_(cp), prog_(*cp.program), cfg_(cfg), be_(be),
+        conservative_(conservative) {}
+
+  RunResult run() {
+    res_.indirectIndexing = cp_.indirectIndexing;
+    int rc = be_.reset();
+    if (rc < 0)
+      return fail(rc, be_.lastError());
+    const Function *entry = prog_.findHost("main");
+    if (!entry) {
+      res_.traps.push_back("missing entry function");
+      return std::move(res_);
+    }
+    Frame f;
+    for (const auto &p : entry->params) {
+      if (p.type == VarType::Int) {
+        f.scalars[p.name] = 0;
+        setDef(-entry->loc.line, 0, p.name, 0);
+      } else {
+        f.arrays[p.name] = -1;
+      }
+    }
+    try {
+      execBody(entry->body, f);
+    } catch (const Abort &) {
+    } catch (const BackendFail &bf) {
+      return fail(bf.code, bf.msg);
+    }
+    std::sort(res_.races.begin(), res_.races.end(), [](const Race &a, const Race &b) {
+      if (!(a.locA == b.locA))
+        return a.locA < b.locA;
+      if (!(a.locB == b.locB))
+        return a.locB < b.locB;
+      if (a.kind != b.kind)
+        return a.kind < b.kind;
+      if (a.array != b.array)
+        return a.array < b.array;
+      return a.address < b.address;
+    });
+    return std::move(res_);
+  }
+
+private:
+  struct Frame {
+    std::map<std::string, int64_t> scalars;
+    std::map<std::string, int> arrays;
+  };
+  struct Buf {
+    int64_t elems = 0;
+    std::vector<int64_t> host; // lazily materialised mirror
+    bool hostValid = true;     // mirror (or implicit zeros) == device
+    int64_t dirtyLo = INT64_MAX, dirtyHi = -1;
+    bool stale = false;        // device content not exact (PARALLEL writes)
+  };
+
+  RunResult fail(int code, const std::string &msg) {
+    res_.error = code;
+    res_.errorMessage = msg;
+    return std::move(res_);
+  }
+
+  void setDef(int site, int aux, const std::string &name, int64_t v) {
+    auto key = std::make_pair(site, aux);
+    auto it = defs_.find(key);
+    if (it == defs_.end())
+      defs_.emplace(key, DefVal{name, v});
+    else
+      it->second.value = v; // DefKey identity ignores the name (host_facts.hpp:26-33)
+  }
+
+  void trap(const Loc &loc, const std::string &msg) {
+    if (res_.traps.size() < 256)
+      res_.traps.push_back(prog_.file + ":" + std::to_string(loc.line) + ": " + msg);
+  }
+
+  void step(const Loc &loc) {
+    if (++steps_ > cfg_.maxSteps) {
+      trap(loc, "step budget exhausted");
+      throw Abort{};
+    }
+  }
+
+  void ensureHost(Buf &b, int h) {
+    if (b.host.empty() && b.elems > 0 && b.hostValid) {
+      b.host.assign(static_cast<size_t>(b.elems), 0);
+      return;
+    }
+    if (!b.hostValid) {
+      if (b.host.size() != static_cast<size_t>(b.elems))
+        b.host.assign(static_cast<size_t>(b.elems), 0);
+      int rc = be_.read(h, 0, b.elems, b.host.data());
+      if (rc < 0)
+        throw BackendFail{rc, be_.lastError()};
+      b.hostValid = true;
+    }
+  }
+
+  int64_t evalHost(const Expr &e, Frame &f) {
+    switch (e.kind) {
+    case EK::Lit:
+      return e.value;
+    case EK::Var: {
+      auto it = f.scalars.find(e.name);
+      return it == f.scalars.end() ? 0 : it->second;
+    }
+    case EK::Input: {
+      int64_t v = 0;
+      if (inputCursor_ < cfg_.inputs.size())
+        v = cfg_.inputs[inputCursor_++];
+      else
+        trap(e.loc, "input exhausted; __input() defaults to 0");
+      setDef(e.id, 0, "__input", v);
+      return v;
+    }
+    case EK::Load: {
+      auto it = f.arrays.find(e.name);
+      int64_t idx = evalHost(*e.index, f);
+      if (it == f.arrays.end() || it->second < 0) {
+        trap(e.loc, "read from unallocated array " + e.name);
+        return 0;
+      }
+      Buf &b = bufs_[it->second];
+      if (idx < 0 || idx >= b.elems) {
+        trap(e.loc, "host read out of bounds on " + e.name);
+        return 0;
+      }
+      if (b.stale)
+        throw NeedConservative{};
+      ensureHost(b, it->second);
+      return b.host[static_cast<size_t>(idx)];
+    }
+    case EK::Binary: {
+      int64_t l = evalHost(*e.lhs, f); // host: left to right (:174-175)
+      int64_t r = evalHost(*e.rhs, f);
+      return binop(e.op, l, r);
+    }
+    default:
+      return 0;
+    }
+  }
+
+  bool execBody(const Body &b, Frame &f) {
+    for (const auto &s : b)
+      if (execStmt(*s, f))
+        return true;
+    return false;
+  }
+
+  void syncJoin(const Stmt &s, Frame &f) {
+    std::set<std::string> names = assignedNames(s.body);
+    std::set<std::string> e = assignedNames(s.elseBody);
+    names.insert(e.begin(), e.end());
+    for (const auto &n : names) {
+      auto it = f.scalars.find(n);
+      if (it != f.scalars.end())
+        setDef(s.id, 3, n, it->second);
+    }
+  }
+
+  bool execStmt(const Stmt &s, Frame &f) {
+    step(s.loc);
+    switch (s.kind) {
+    case SK::Assign: {
+      if (s.isDecl && isArray(s.declType)) {
+        f.arrays[s.name] = -1;
+        return false;
+      }
+      int64_t v = s.value ? evalHost(*s.value, f) : 0;
+      f.scalars[s.name] = v;
+      setDef(s.id, 0, s.name, v);
+      return false;
+    }
+    case SK::Store: {
+      int64_t idx = evalHost(*s.index, f);
+      int64_t val = evalHost(*s.value, f);
+      auto it = f.arrays.find(s.name);
+      if (it == f.arrays.end() || it->second < 0) {
+        trap(s.loc, "write to unallocated array " + s.name);
+        return false;
+      }
+      Buf &b = bufs_[it->second];
+      if (idx < 0 || idx >= b.elems) {
+        trap(s.loc, "host write out of bounds on " + s.name);
+        return false;
+      }
+      ensureHost(b, it->second);
+      b.host[static_cast<size_t>(idx)] = val;
+      b.dirtyLo = std::min(b.dirtyLo, idx);
+      b.dirtyHi = std::max(b.dirtyHi, idx);
+      return false;
+    }
+    case SK::Assert:
+      if (evalHost(*s.cond, f) == 0) {
+        res_.assertStopped = true;
+        throw Abort{};
+      }
+      return false;
+    case SK::Alloc: {
+      int64_t elems = 0;
+      if (!s.pitch) {
+        elems = evalHost(*s.width, f);
+      } else {
+        int64_t w = evalHost(*s.width, f);
+        int64_t h = evalHost(*s.height, f);
+        if (w <= 0 || h <= 0) {
+          trap(s.loc, "cudaMallocPitch with non-positive extent");
+          f.scalars[s.aux] = 0;
+          setDef(s.id, 1, s.aux, 0);
+          f.arrays[s.name] = -1;
+          return false;
+        }
+        int64_t pitch = wrapMul((w + 3) / 4, 4); // reference :271-275
+        f.scalars[s.aux] = pitch;
+        setDef(s.id, 1, s.aux, pitch);
+        elems = wrapMul(pitch, h);
+      }
+      if (elems <= 0 || elems > cfg_.maxArrayElems) {
+        trap(s.loc, "allocation size out of range for " + s.name);
+        f.arrays[s.name] = -1;
+        return false;
+      }
+      int32_t handle = -1;
+      int rc = be_.alloc(elems, &handle);
+      if (rc < 0)
+        throw BackendFail{rc, be_.lastError()};
+      if (handle != static_cast<int32_t>(bufs_.size()))
+        throw BackendFail{HGRD_GPU_EINVAL, "backend handle order"};
+      Buf b;
+      b.elems = elems;
+      bufs_.push_back(std::move(b));
+      f.arrays[s.name] = handle;
+      return false;
+    }
+    case SK::If: {
+      bool taken = evalHost(*s.cond, f) != 0;
+      bool returned = execBody(taken ? s.body : s.elseBody, f);
+      syncJoin(s, f);
+      return returned;
+    }
+    case SK::For: {
+      int64_t i = evalHost(*s.init, f);
+      std::set<std::string> assigned = assignedNames(s.body);
+      assigned.erase(s.aux);
+      for (;;) {
+        step(s.loc);
+        int64_t bound = evalHost(*s.bound, f);
+        bool cont = s.inclusive ? (i <= bound) : (i < bound);
+        if (!cont)
+          break;
+        f.scalars[s.aux] = i;
+        setDef(s.id, 0, s.aux, i);
+        for (const auto &n : assigned) {
+          auto it = f.scalars.find(n);
+          if (it != f.scalars.end())
+            setDef(s.id, 1, n, it->second);
+        }
+        if (execBody(s.body, f))
+          return true;
+        i = wrapAdd(i, s.step);
+      }
+      f.scalars[s.aux] = i;
+      setDef(s.id, 2, s.aux, i);
+      for (const auto &n : assigned) {
+        auto it = f.scalars.find(n);
+        if (it != f.scalars.end())
+          setDef(s.id, 2, n, it->second);
+      }
+      return false;
+    }
+    case SK::Launch:
+      execLaunch(s, f);
+      return false;
+    case SK::Call: {
+      const Function *callee = prog_.findHost(s.name);
+      if (!callee) {
+        trap(s.loc, "call to unknown function");
+        return false;
+      }
+      if (callDepth_ > 64) {
+        trap(s.loc, "host call depth exceeded");
+        throw Abort{};
+      }
+      Frame cf;
+      for (size_t i = 0; i < callee->params.size(); ++i) {
+        const Param &p = callee->params[i];
+        if (p.type == VarType::Int) {
+          int64_t v = evalHost(*s.args[i], f);
+          cf.scalars[p.name] = v;
+          setDef(s.id, static_cast<int>(i) + 10, p.name, v);
+        } else {
+          int handle = -1;
+          if (s.args[i]->kind == EK::Var) {
+            auto it = f.arrays.find(s.args[i]->name);
+            if (it != f.arrays.end())
+              handle = it->second;
+          }
+          cf.arrays[p.name] = handle;
+        }
+      }
+      ++callDepth_;
+      execBody(callee->body, cf);
+      --callDepth_;
+      return false;
+    }
+    case SK::Return:
+      return true;
+    default:
+      return false;
+    }
+  }
+
+  // reference Interpreter::execLaunch, src/oracle.cpp:378-467: the host part
+  // runs here; the thread loop and detectRaces run in the backend.
+  void execLaunch(const Stmt &s, Frame &f) {
+    const Function *kernel = prog_.findKernel(s.name);
+    if (!kernel) {
+      trap(s.loc, "launch of unknown kernel");
+      return;
+    }
+    std::array<int64_t, 3> grid{}, block{};
+    for (int d = 0; d < 3; ++d) {
+      grid[d] = evalHost(*s.grid[d], f);
+      block[d] = evalHost(*s.block[d], f);
+    }
+    for (int d = 0; d < 3; ++d) {
+      if (grid[d] <= 0 || block[d] <= 0) {
+        trap(s.loc, "non-positive launch dimension");
+        ++res_.launchesSkipped;
+        return;
+      }
+    }
+    bool fits = true;
+    for (int d = 0; d < 3; ++d)
+      fits = fits && grid[d] <= cfg_.gridCap[d] && block[d] <= cfg_.blockCap[d];
+    int64_t tpb = wrapMul(wrapMul(block[0], block[1]), block[2]);
+    int64_t total = wrapMul(wrapMul(wrapMul(grid[0], grid[1]), grid[2]), tpb);
+    if (!fits || total > cfg_.maxThreads) {
+      ++res_.launchesSkipped;
+      return;
+    }
+    LaunchRec rec;
+    rec.site = s.id;
+    rec.loc = s.loc;
+    rec.grid = grid;
+    rec.block = block;
+    rec.defValues = defs_;
+    std::vector<int32_t> paramHandle(kernel->params.size(), -1);
+    std::vector<int64_t> scalarVal(kernel->params.size(), 0);
+    for (size_t i = 0; i < kernel->params.size(); ++i) {
+      const Param &p = kernel->params[i];
+      if (p.type == VarType::Int) {
+        int64_t v = evalHost(*s.args[i], f);
+        scalarVal[i] = v;
+        rec.scalarArgs.push_back(v);
+        rec.isScalar.push_back(true);
+      } else {
+        int handle = -1;
+        if (s.args[i]->kind == EK::Var) {
+          auto it = f.arrays.find(s.args[i]->name);
+          if (it != f.arrays.end())
+            handle = it->second;
+        }
+        paramHandle[i] = handle;
+        rec.scalarArgs.push_back(-1);
+        rec.isScalar.push_back(false);
+      }
+    }
+    res_.launchRecords.push_back(std::move(rec));
+    ++res_.launchesRun;
+    const int launchIndex = static_cast<int>(res_.launchRecords.size() - 1);
+    checkLaunch(cp_.kernel(kernel), grid, block, paramHandle, scalarVal, launchIndex);
+  }
+
+  void checkLaunch(const LoweredKernel &lk, const std::array<int64_t, 3> &grid,
+                   const std::array<int64_t, 3> &block,
+                   const std::vector<int32_t> &paramHandle,
+                   const std::vector<int64_t> &scalarVal, int launchIndex) {
+    auto handleOf = [&](const hgrd_gpu_site &st) -> int32_t {
+      return st.param >= 0 ? paramHandle[static_cast<size_t>(st.param)] : -1;
+    };
+    // Buffers this launch writes (aliasing resolved through handles).
+    std::set<int32_t> written;
+    for (const auto &st : lk.sites)
+      if (st.kind != HGRD_SITE_LOAD && handleOf(st) >= 0)
+        written.insert(handleOf(st));
+    bool sequential = false;
+    for (size_t i = 0; i < lk.sites.size(); ++i) {
+      const auto &st = lk.sites[i];
+      int32_t h = handleOf(st);
+      if (st.kind != HGRD_SITE_LOAD || h < 0 || !lk.siteValueNeeded[i])
+        continue;
+      if (written.count(h))
+        sequential = true;
+      if (bufs_[static_cast<size_t>(h)].stale)
+        throw NeedConservative{};
+    }
+    if (conservative_ && !written.empty())
+      sequential = true;
+    if (sequential) {
+      for (const auto &st : lk.sites) {
+        int32_t h = handleOf(st);
+        if (st.kind == HGRD_SITE_LOAD && h >= 0 && bufs_[static_cast<size_t>(h)].stale)
+          throw NeedConservative{};
+      }
+    }
+    // Bring host-side writes to the device.
+    for (size_t h = 0; h < bufs_.size(); ++h) {
+      Buf &b = bufs_[h];
+      if (b.dirtyHi >= b.dirtyLo) {
+        int rc = be_.write(static_cast<int32_t>(h), b.dirtyLo, b.dirtyHi - b.dirtyLo + 1,
+                           b.host.data() + b.dirtyLo);
+        if (rc < 0)
+          throw BackendFail{rc, be_.lastError()};
+        b.dirtyLo = INT64_MAX;
+        b.dirtyHi = -1;
+      }
+    }
+    std::vector<int64_t> regInit(lk.nRegs, 0);
+    for (size_t i = 0; i < lk.paramReg.size(); ++i)
+      if (lk.paramReg[i] >= 0)
+        regInit[static_cast<size_t>(lk.paramReg[i])] = scalarVal[i];
+
+    hgrd_gpu_launch L{};
+    L.code = lk.code.data();
+    L.n_code = static_cast<uint32_t>(lk.code.size());
+    L.n_regs = lk.nRegs;
+    L.reg_init = regInit.data();
+    L.sites = lk.sites.data();
+    L.n_sites = static_cast<uint32_t>(lk.sites.size());
+    L.n_locs = static_cast<uint32_t>(lk.locs.size());
+    L.param_handle = paramHandle.data();
+    L.n_params = static_cast<uint32_t>(paramHandle.size());
+    L.flags = (sequential ? HGRD_LAUNCH_SEQUENTIAL : 0u) |
+              (lk.hasLocks ? HGRD_LAUNCH_PAIRWISE : 0u);
+    for (int d = 0; d < 3; ++d) {
+      L.grid[d] = grid[d];
+      L.block[d] = block[d];
+    }
+    L.warp_size = cfg_.warpSize;
+    L.step_budget = cfg_.maxSteps - steps_;
+
+    const size_t nl = std::max<size_t>(lk.locs.size(), 1);
+    std::vector<hgrd_gpu_race> races(3 * nl * nl);
+    const size_t trapCap = res_.traps.size() < 256 ? 256 - res_.traps.size() : 0;
+    std::vector<hgrd_gpu_trap> traps(std::max<size_t>(trapCap, 1));
+    hgrd_gpu_result R{};
+    R.races = races.data();
+    R.race_cap = static_cast<uint32_t>(races.size());
+    R.traps = traps.data();
+    R.trap_cap = static_cast<uint32_t>(trapCap);
+    int rc = be_.checkLaunch(L, R);
+    if (rc < 0)
+      throw BackendFail{rc, be_.lastError()};
+
+    res_.stats.instances += R.instances;
+    res_.stats.records += R.records;
+    res_.stats.kernelSteps += R.steps;
+    res_.stats.deviceMs += R.device_ms;
+    if (R.mode & HGRD_LAUNCH_SEQUENTIAL)
+      ++res_.stats.seqLaunches;
+    else
+      ++res_.stats.parLaunches;
+
+    for (uint32_t i = 0; i < R.n_traps && i < trapCap; ++i) {
+      const hgrd_gpu_trap &t = traps[i];
+      const auto si = static_cast<size_t>(t.site);
+      trap(lk.siteLoc[si], std::string(t.kind == HGRD_TRAP_OOB
+                                            ? "kernel access out of bounds on "
+                                            : "kernel access to unallocated array ") +
+                               lk.siteArray[si]);
+    }
+    steps_ += R.steps;
+    if (R.aborted) {
+      trap(lk.stmtLocs[static_cast<size_t>(R.abort_stmt)], "step budget exhausted");
+      throw Abort{};
+    }
+    // Memory state after the launch.
+    for (int32_t h : written) {
+      Buf &b = bufs_[static_cast<size_t>(h)];
+      if (sequential)
+        b.hostValid = false;
+      else
+        b.stale = true;
+    }
+    const int64_t tpb = block[0] * block[1] * block[2];
+    for (uint32_t i = 0; i < R.n_races; ++i) {
+      const hgrd_gpu_race &g = races[i];
+      Race r;
+      r.locA = lk.locs[static_cast<size_t>(g.loc_a)];
+      r.locB = lk.locs[static_cast<size_t>(g.loc_b)];
+      r.kind = g.kind;
+      r.array = lk.siteArray[static_cast<size_t>(g.site_x)];
+      r.address = g.index;
+      r.launch = launchIndex;
+      r.threadX = g.thread_x;
+      r.threadY = g.thread_y;
+      r.seqX = g.seq_x;
+      r.seqY = g.seq_y;
+      decompose(g.thread_x, grid, block, tpb, r.blockX, r.tidX);
+      decompose(g.thread_y, grid, block, tpb, r.blockY, r.tidY);
+      auto key = std::make_tuple(r.locA.line, r.locA.col, r.locB.line, r.locB.col, r.kind);
+      if (seen_.insert(key).second)
+        res_.races.push_back(std::move(r));
+    }
+  }
+
+  static void decompose(int64_t thread, const std::array<int64_t, 3> &grid,
+                        const std::array<int64_t, 3> &block, int64_t tpb,
+                        int64_t (&b)[3], int64_t (&t)[3]) {
+    int64_t bl = thread / tpb, tl = thread % tpb;
+    b[0] = bl % grid[0];
+    b[1] = (bl / grid[0]) % grid[1];
+    b[2] = bl / (grid[0] * grid[1]);
+    t[0] = tl % block[0];
+    t[1] = (tl / block[0]) % block[1];
+    t[2] = tl / (block[0] * block[1]);
+  }
+
+  CompiledProgram &cp_;
+  const Program &prog_;
+  const ExecConfig &cfg_;
+  LaunchBackend &be_;
+  const bool conservative_;
+  RunResult res_;
+  std::vector<Buf> bufs_;
+  std::map<std::pair<int, int>, DefVal> defs_;
+  std::set<std::tuple<int, int, int, int, int>> seen_;
+  size_t inputCursor_ = 0;
+  int64_t steps_ = 0;
+  int callDepth_ = 0;
+};
+
+} // namespace
+
+RunResult runConcrete(CompiledProgram &prog, const ExecConfig &cfg,
+                      LaunchBackend &backend) {
+  try {
+    return HostRun(prog, cfg, backend, false).run();
+  } catch (const NeedConservative &) {
+  }
+  RunResult r;
+  try {
+    r = HostRun(prog, cfg, backend, true).run();
+  } catch (const NeedConservative &) {
+    r.error = HGRD_GPU_EINVAL;
+    r.errorMessage = "stale buffer in conservative mode";
+  }
+  r.stats.restarts = 1;
+  return r;
+}
+
+// reference enumerateVerdict, src/oracle.cpp:863-903
+SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
+                             LaunchBackend &backend) {
+  SweepResult out;
+  const int inputs = prog.inputs;
+  std::set<std::tuple<int, int, int, int, int, int64_t>> seen;
+  uint64_t configs = 0;
+  std::vector<size_t> cursor(static_cast<size_t>(inputs), 0);
+  for (int64_t ws : caps.warpSizes) {
+    std::fill(cursor.begin(), cursor.end(), 0);
+    for (;;) {
+      if (configs++ > caps.maxConfigs) {
+        out.configs = configs - 1;
+        return out;
+      }
+      ExecConfig c;
+      c.gridCap = caps.gridCap;
+      c.blockCap = caps.blockCap;
+      c.warpSize = ws;
+      c.maxThreads = caps.maxThreads;
+      for (int i = 0; i < inputs; ++i)
+        c.inputs.push_back(caps.inputSet[cursor[static_cast<size_t>(i)]]);
+      RunResult r = runConcrete(prog, c, backend);
+      if (r.error) {
+        out.error = r.error;
+        out.errorMessage = r.errorMessage;
+        return out;
+      }
+      out.stats.instances += r.stats.instances;
+      out.stats.records += r.stats.records;
+      out.stats.deviceMs += r.stats.deviceMs;
+      out.stats.parLaunches += r.stats.parLaunches;
+      out.stats.seqLaunches += r.stats.seqLaunches;
+      out.stats.restarts += r.stats.restarts;
+      for (const auto &race : r.races) {
+        auto key = std::make_tuple(race.locA.line, race.locA.col, race.locB.line,
+                                   race.locB.col, race.kind, ws);
+        if (seen.insert(key).second)
+          out.races.push_back(SweepRace{race.locA, race.locB, race.kind, ws});
+      }
+      int pos = inputs - 1;
+      while (pos >= 0) {
+        if (++cursor[static_cast<size_t>(pos)] < caps.inputSet.size())
+          break;
+        cursor[static_cast<size_t>(pos)] = 0;
+        --pos;
+      }
+      if (pos < 0)
+        break;
+    }
+  }
+  out.configs = configs;
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// JSON
+
+namespace {
+
+struct JVal {
+  enum Kind { Null, Bool, Num, Str, Arr, Obj } kind = Null;
+  bool b = false;
+  int64_t i = 0;
+  double d = 0;
+  bool isInt = true;
+  std::string s;
+  std::vector<JVal> arr;
+  std::vector<std::pair<std::string, JVal>> obj;
+  const JVal *get(const char *k) const {
+    for (const auto &kv : obj)
+      if (kv.first == k)
+        return &kv.second;
+    return nullptr;
+  }
+};
+
+class JParse {
+public:
+  explicit JParse(const char *s) : p_(s) {}
+  JVal value() {
+    ws();
+    JVal v;
+    char c = *p_;
+    if (c == '{') {
+      ++p_;
+      v.kind = JVal::Obj;
+      ws();
+      if (*p_ == '}') {
+        ++p_;
+        return v;
+      }
+      for (;;) {
+        ws();
+        std::string k = str();
+        ws();
+        expect(':');
+        JVal x = value();
+        v.obj.emplace_back(std::move(k), std::move(x));
+        ws();
+        if (*p_ == ',') {
+          ++p_;
+          continue;
+        }
+        expect('}');
+        return v;
+      }
+    }
+    if (c == '[') {
+      ++p_;
+      v.kind = JVal::Arr;
+      ws();
+      if (*p_ == ']') {
+        ++p_;
+        return v;
+      }
+      for (;;) {
+        v.arr.push_back(value());
+        ws();
+        if (*p_ == ',') {
+          ++p_;
+          continue;
+        }
+        expect(']');
+        return v;
+      }
+    }
+    if (c == '"') {
+      v.kind = JVal::Str;
+      v.s = str();
+      return v;
+    }
+    if (!std::strncmp(p_, "true", 4)) {
+      p_ += 4;
+      v.kind = JVal::Bool;
+      v.b = true;
+      return v;
+    }
+    if (!std::strncmp(p_, "false", 5)) {
+      p_ += 5;
+      v.kind = JVal::Bool;
+      return v;
+    }
+    if (!std::strncmp(p_, "null", 4)) {
+      p_ += 4;
+      return v;
+    }
+    const char *start = p_;
+    if (*p_ == '-' || *p_ == '+')
+      ++p_;
+    bool isInt = true;
+    while ((*p_ >= '0' && *p_ <= '9') || *p_ == '.' || *p_ == 'e' || *p_ == 'E' ||
+           *p_ == '-' || *p_ == '+') {
+      if (*p_ == '.' || *p_ == 'e' || *p_ == 'E')
+        isInt = false;
+      ++p_;
+    }
+    if (p_ == start)
+      throw std::runtime_error("bad JSON value");
+    std::string num(start, p_);
+    v.kind = JVal::Num;
+    v.isInt = isInt;
+    if (isInt) {
+      v.i = std::stoll(num);
+      v.d = static_cast<double>(v.i);
+    } else {
+      v.d = std::stod(num);
+      v.i = static_cast<int64_t>(v.d);
+    }
+    return v;
+  }
+
+private:
+  void ws() {
+    while (*p_ == ' ' || *p_ == '\n' || *p_ == '\t' || *p_ == '\r')
+      ++p_;
+  }
+  void expect(char c) {
+    if (*p_ != c)
+      throw std::runtime_error(std::string("JSON: expected ") + c);
+    ++p_;
+  }
+  std::string str() {
+    expect('"');
+    std::string out;
+    while (*p_ && *p_ != '"') {
+      if (*p_ == '\\') {
+        ++p_;
+        char e = *p_++;
+        out.push_back(e == 'n' ? '\n' : e == 't' ? '\t' : e);
+      } else {
+        out.push_back(*p_++);
+      }
+    }
+    expect('"');
+    return out;
+  }
+  const char *p_;
+};
+
+bool readI64(const JVal &o, const char *k, int64_t &dst) {
+  const JVal *v = o.get(k);
+  if (!v || v->kind != JVal::Num)
+    return false;
+  dst = v->i;
+  return true;
+}
+void readArr3(const JVal &o, const char *k, std::array<int64_t, 3> &dst) {
+  const JVal *v = o.get(k);
+  if (!v || v->kind != JVal::Arr)
+    return;
+  for (size_t i = 0; i < 3 && i < v->arr.size(); ++i)
+    dst[i] = v->arr[i].i;
+}
+void readVec(const JVal &o, const char *k, std::vector<int64_t> &dst) {
+  const JVal *v = o.get(k);
+  if (!v || v->kind != JVal::Arr)
+    return;
+  dst.clear();
+  for (const auto &x : v->arr)
+    dst.push_back(x.i);
+}
+
+std::string esc(const std::string &s) {
+  std::string o = "\"";
+  for (char c : s) {
+    switch (c) {
+    case '"':
+      o += "\\\"";
+      break;
+    case '\\':
+      o += "\\\\";
+      break;
+    case '\n':
+      o += "\\n";
+      break;
+    case '\t':
+      o += "\\t";
+      break;
+    default:
+      if (static_cast<unsigned char>(c) < 0x20) {
+        char buf[8];
+        std::snprintf(buf, sizeof buf, "\\u%04x", c);
+        o += buf;
+      } else {
+        o.push_back(c);
+      }
+    }
+  }
+  return o + "\"";
+}
+
+std::string locJ(const Loc &l, const std::string &file) {
+  return "{\"file\":" + esc(file) + ",\"line\":" + std::to_string(l.line) +
+         ",\"column\":" + std::to_string(l.col) + "}";
+}
+
+template <class V> std::string arrJ(const V &v) {
+  std::string o = "[";
+  bool first = true;
+  for (const auto &x : v) {
+    if (!first)
+      o += ",";
+    first = false;
+    o += std::to_string(x);
+  }
+  return o + "]";
+}
+
+std::string statsJ(const RunStats &s) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "{\"instances\":%" PRIu64 ",\"records\":%" PRIu64
+                ",\"kernelSteps\":%" PRId64 ",\"deviceMs\":%.6f,\"parallelLaunches\":%d,"
+                "\"sequentialLaunches\":%d,\"restarts\":%d}",
+                s.instances, s.records, s.kernelSteps, s.deviceMs, s.parLaunches,
+                s.seqLaunches, s.restarts);
+  return buf;
+}
+
+} // namespace
+
+bool parseExecConfigJson(const char *json, ExecConfig &c, std::string &err) {
+  try {
+    JVal o = JParse(json && *json ? json : "{}").value();
+    readArr3(o, "gridCap", c.gridCap);
+    readArr3(o, "blockCap", c.blockCap);
+    readI64(o, "warpSize", c.warpSize);
+    readVec(o, "inputs", c.inputs);
+    readI64(o, "maxThreads", c.maxThreads);
+    readI64(o, "maxArrayElems", c.maxArrayElems);
+    readI64(o, "maxSteps", c.maxSteps);
+  } catch (const std::exception &e) {
+    err = e.what();
+    return false;
+  }
+  return true;
+}
+
+bool parseSweepCapsJson(const char *json, SweepCaps &c, std::string &err) {
+  try {
+    JVal o = JParse(json && *json ? json : "{}").value();
+    readArr3(o, "gridCap", c.gridCap);
+    readArr3(o, "blockCap", c.blockCap);
+    readVec(o, "inputSet", c.inputSet);
+    readVec(o, "warpSizes", c.warpSizes);
+    readI64(o, "maxThreads", c.maxThreads);
+    int64_t mc;
+    if (readI64(o, "maxConfigs", mc))
+      c.maxConfigs = static_cast<uint64_t>(mc);
+  } catch (const std::exception &e) {
+    err = e.what();
+    return false;
+  }
+  return true;
+}
+
+std::string errorJson(const std::vector<std::string> &diags) {
+  std::string o = "{\"error\":[";
+  for (size_t i = 0; i < diags.size(); ++i)
+    o += (i ? "," : "") + esc(diags[i]);
+  return o + "]}";
+}
+
+std::string runResultJson(const RunResult &r, const std::string &file) {
+  std::ostringstream o;
+  o << "{\"races\":[";
+  for (size_t i = 0; i < r.races.size(); ++i) {
+    const Race &x = r.races[i];
+    o << (i ? "," : "") << "{\"kind\":" << esc(raceKindName(x.kind))
+      << ",\"locA\":" << locJ(x.locA, file) << ",\"locB\":" << locJ(x.locB, file)
+      << ",\"array\":" << esc(x.array) << ",\"address\":" << x.address << "}";
+  }
+  o << "],\"traps\":[";
+  for (size_t i = 0; i < r.traps.size(); ++i)
+    o << (i ? "," : "") << esc(r.traps[i]);
+  o << "],\"launchesRun\":" << r.launchesRun
+    << ",\"launchesSkipped\":" << r.launchesSkipped
+    << ",\"assertStopped\":" << (r.assertStopped ? "true" : "false")
+    << ",\"indirectIndexing\":" << (r.indirectIndexing ? "true" : "false")
+    << ",\"launchRecords\":[";
+  for (size_t i = 0; i < r.launchRecords.size(); ++i) {
+    const LaunchRec &l = r.launchRecords[i];
+    o << (i ? "," : "") << "{\"site\":" << l.site << ",\"line\":" << l.loc.line
+      << ",\"column\":" << l.loc.col << ",\"grid\":" << arrJ(l.grid)
+      << ",\"block\":" << arrJ(l.block) << ",\"scalarArgs\":" << arrJ(l.scalarArgs)
+      << ",\"isScalar\":[";
+    for (size_t k = 0; k < l.isScalar.size(); ++k)
+      o << (k ? "," : "") << (l.isScalar[k] ? 1 : 0);
+    o << "],\"defValues\":[";
+    bool first = true;
+    for (const auto &[key, dv] : l.defValues) {
+      o << (first ? "" : ",") << "[" << key.first << "," << key.second << ","
+        << esc(dv.name) << "," << dv.value << "]";
+      first = false;
+    }
+    o << "]}";
+  }
+  o << "],\"witnesses\":[";
+  for (size_t i = 0; i < r.races.size(); ++i) {
+    const Race &x = r.races[i];
+    o << (i ? "," : "") << "{\"launch\":" << x.launch << ",\"threadA\":" << x.threadX
+      << ",\"seqA\":" << x.seqX << ",\"blockIdxA\":" << arrJ(x.blockX)
+      << ",\"threadIdxA\":" << arrJ(x.tidX) << ",\"threadB\":" << x.threadY
+      << ",\"seqB\":" << x.seqY << ",\"blockIdxB\":" << arrJ(x.blockY)
+      << ",\"threadIdxB\":" << arrJ(x.tidY) << "}";
+  }
+  o << "],\"stats\":" << statsJ(r.stats) << "}";
+  return o.str();
+}
+
+std::string sweepResultJson(const SweepResult &r, const std::string &file) {
+  std::ostringstream o;
+  o << "{\"races\":[";
+  for (size_t i = 0; i < r.races.size(); ++i) {
+    const SweepRace &x = r.races[i];
+    o << (i ? "," : "") << "{\"kind\":" << esc(raceKindName(x.kind))
+      << ",\"locA\":" << locJ(x.locA, file) << ",\"locB\":" << locJ(x.locB, file)
+      << ",\"warpSize\":" << x.warpSize << "}";
+  }
+  o << "],\"configs\":" << r.configs << ",\"stats\":" << statsJ(r.stats) << "}";
+  return o.str();
+}
+
+int runConcreteJson(LaunchBackend &be, const char *src, const char *file,
+                    const char *cfgJson, std::string &out) {
+  ExecConfig cfg;
+  std::string err;
+  if (!parseExecConfigJson(cfgJson, cfg, err)) {
+    out = errorJson({"config: " + err});
+    return HGRD_GPU_EINVAL;
+  }
+  ParseOutcome po = parseMiniCU(src ? src : "", file ? file : "");
+  if (!po.program) {
+    out = errorJson(po.diagnostics);
+    return HGRD_GPU_OK;
+  }
+  std::string fileName = po.program->file;
+  auto cp = compileProgram(std::move(po.program));
+  RunResult r = runConcrete(*cp, cfg, be);
+  if (r.error) {
+    out = errorJson({"backend: " + r.errorMessage});
+    return r.error;
+  }
+  out = runResultJson(r, fileName);
+  return HGRD_GPU_OK;
+}
+
+int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
+                         const char *capsJson, std::string &out) {
+  SweepCaps caps;
+  std::string err;
+  if (!parseSweepCapsJson(capsJson, caps, err)) {
+    out = errorJson({"caps: " + err});
+    return HGRD_GPU_EINVAL;
+  }
+  ParseOutcome po = parseMiniCU(src ? src : "", file ? file : "");
+  if (!po.program) {
+    out = errorJson(po.diagnostics);
+    return HGRD_GPU_OK;
+  }
+  std::string fileName = po.program->file;
+  auto cp = compileProgram(std::move(po.program));
+  SweepResult r = enumerateVerdict(*cp, caps, be);
+  if (r.error) {
+    out = errorJson({"backend: " + r.errorMessage});
+    return r.error;
+  }
+  out = sweepResultJson(r, fileName);
+  return HGRD_GPU_OK;
+}
+
+} // namespace hgrdgpu

@@ -1,0 +1,149 @@
+// Host side of the race-check stage: the reference's concrete host
+// interpreter (reference src/oracle.cpp:55-437), mirrored so that every
+// kernel launch is handed, fully parameterised, to a launch backend
+// (the B200 kernels in the product; the CPU restatement in oracle/).
+#pragma once
+
+#include "hgrd_gpu.h"
+#include "lower.hpp"
+#include "minicu.hpp"
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace hgrdgpu {
+
+// reference include/hgrd/oracle.hpp:17-25
+struct ExecConfig {
+  std::array<int64_t, 3> gridCap{2, 2, 1};
+  std::array<int64_t, 3> blockCap{4, 1, 1};
+  int64_t warpSize = 32;
+  std::vector<int64_t> inputs;
+  int64_t maxThreads = 64;
+  int64_t maxArrayElems = 1 << 20;
+  int64_t maxSteps = 1 << 20;
+};
+
+// reference include/hgrd/oracle.hpp:59-66
+struct SweepCaps {
+  std::array<int64_t, 3> gridCap{2, 2, 1};
+  std::array<int64_t, 3> blockCap{4, 1, 1};
+  std::vector<int64_t> inputSet{0, 1, 2, 3, 127};
+  std::vector<int64_t> warpSizes{2, 4};
+  int64_t maxThreads = 64;
+  uint64_t maxConfigs = 100000;
+};
+
+// reference ObservedRace (oracle.hpp:27-32) + witness pair
+struct Race {
+  Loc locA, locB;
+  int kind = 0;
+  std::string array;
+  int64_t address = 0;
+  int launch = 0;           // index into launchRecords
+  int64_t threadX = 0, threadY = 0;
+  int seqX = 0, seqY = 0;
+  int64_t blockX[3] = {0, 0, 0}, tidX[3] = {0, 0, 0};
+  int64_t blockY[3] = {0, 0, 0}, tidY[3] = {0, 0, 0};
+};
+
+struct DefVal {
+  std::string name;
+  int64_t value = 0;
+};
+
+// reference LaunchRecord (oracle.hpp:38-45)
+struct LaunchRec {
+  int site = -1;
+  Loc loc;
+  std::array<int64_t, 3> grid{1, 1, 1}, block{1, 1, 1};
+  std::vector<int64_t> scalarArgs;
+  std::vector<bool> isScalar;
+  std::map<std::pair<int, int>, DefVal> defValues;
+};
+
+struct RunStats {
+  uint64_t instances = 0, records = 0;
+  int64_t kernelSteps = 0;
+  double deviceMs = 0;
+  int parLaunches = 0, seqLaunches = 0, restarts = 0;
+};
+
+// reference OracleResult (oracle.hpp:47-55)
+struct RunResult {
+  std::vector<Race> races;
+  std::vector<std::string> traps;
+  int launchesRun = 0;
+  int launchesSkipped = 0;
+  bool assertStopped = false;
+  bool indirectIndexing = false;
+  std::vector<LaunchRec> launchRecords;
+  RunStats stats;
+  int error = 0; // backend failure (negative hgrd_gpu code)
+  std::string errorMessage;
+};
+
+struct SweepRace {
+  Loc locA, locB;
+  int kind = 0;
+  int64_t warpSize = 0;
+};
+
+struct SweepResult {
+  std::vector<SweepRace> races;
+  RunStats stats;
+  uint64_t configs = 0;
+  int error = 0;
+  std::string errorMessage;
+};
+
+// Device (or restated) execution of the race-check stage for one launch,
+// plus the int64 buffers it runs against.
+class LaunchBackend {
+public:
+  virtual ~LaunchBackend() = default;
+  virtual int reset() = 0;
+  virtual int alloc(int64_t elems, int32_t *handle) = 0;
+  virtual int write(int32_t h, int64_t off, int64_t n, const int64_t *src) = 0;
+  virtual int read(int32_t h, int64_t off, int64_t n, int64_t *dst) = 0;
+  virtual int checkLaunch(const hgrd_gpu_launch &launch, hgrd_gpu_result &res) = 0;
+  virtual std::string lastError() = 0;
+};
+
+// Lowered kernels are cached per program.
+struct CompiledProgram {
+  std::unique_ptr<Program> program;
+  std::map<const Function *, LoweredKernel> kernels;
+  bool indirectIndexing = false;
+  int inputs = 0;
+  const LoweredKernel &kernel(const Function *k);
+};
+
+std::unique_ptr<CompiledProgram> compileProgram(std::unique_ptr<Program> p);
+
+RunResult runConcrete(CompiledProgram &prog, const ExecConfig &cfg,
+                      LaunchBackend &backend);
+SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
+                             LaunchBackend &backend);
+int countInputs(const Program &p);                 // oracle.cpp:805-861
+bool hasIndirectIndexing(const Program &p);        // oracle.cpp:86-123
+
+// JSON bridges shared by the product C ABI and the oracle library.
+bool parseExecConfigJson(const char *json, ExecConfig &cfg, std::string &err);
+bool parseSweepCapsJson(const char *json, SweepCaps &caps, std::string &err);
+std::string runResultJson(const RunResult &r, const std::string &file);
+std::string sweepResultJson(const SweepResult &r, const std::string &file);
+std::string errorJson(const std::vector<std::string> &diags);
+const char *raceKindName(int kind);
+
+// Full pipeline from source text (parse -> run), used by both C ABIs.
+int runConcreteJson(LaunchBackend &be, const char *src, const char *file,
+                    const char *cfgJson, std::string &out);
+int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
+                         const char *capsJson, std::string &out);
+
+} // namespace hgrdgpu

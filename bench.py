@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Race-check throughput on B200: access instances race-checked per second.
+
+Workload (BASELINE.json configs[1]): the synthetic 1D stencil with a
+per-block tile, 2^20 MiniCU threads in blocks of 256, warp size 32; one step
+checks BOTH variants of the config — the missing-barrier launch (4 racy keys)
+and the fixed one (clean) — i.e. 2 x 5 x 2^20 = 10,485,760 instances/step.
+
+* ``value``: instances / device time of hgrd_gpu_check_launch with the launch
+  buffers already resident in HBM (CUDA events on the context's stream),
+  L2 flushed (256 MiB write) between steps.
+* ``e2e``: the same checks through the C ABI from HOST buffers: every step
+  writes the launch's int64 buffers host->device and reads the race report
+  back; wall clock with the copies inside.
+* ``roofline``: dominant pipeline stage vs the measured HBM copy bandwidth,
+  algorithmic bytes = 32 B per instance.
+* ``cpu_baseline``: the unmodified reference (oracle/_ref/libhgrd_ref.so,
+  hgrd::runConcrete) on this host's cores on a bounded sample.
+
+--impl reference times that reference CPU implementation alone (rank 0).
+With --gpus N under torchrun every rank checks its own replica of the
+workload (weak scaling; the path has no cross-rank exchange for this config).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+
+import programs  # noqa: E402
+
+N_THREADS = 1 << 20
+BLOCK = 256
+WS = 32
+INST_PER_THREAD = 5
+B_ALG = 32  # algorithmic bytes per instance
+SAMPLE_THREADS = 1 << 16  # CPU reference sample (per host thread, per step)
+METRIC = "access instances race-checked/sec"
+UNIT = "instances/s"
+WORKLOAD = "stencil1d_2^20threads_block256_ws32_missing+fixed"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (clock / throttle record)."""
+
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def reference_rate(threads: int, reps: int, sample: int):
+    """The unmodified reference runConcrete, `threads` host threads at once,
+    each running both variants of the stencil on a `sample`-thread launch."""
+    from oracles import RefOracle, REF_LIB, CpuOracle, ORACLE_LIB
+    cfg = programs.synthetic_config()
+    srcs = [programs.stencil(sample, barrier=b) for b in (False, True)]
+    if os.path.exists(REF_LIB):
+        ref, kind = RefOracle(), "reference"
+        secs = 0.0
+        for s in srcs:
+            t, _ = ref.time_parallel(s, cfg, threads, reps, "syn.mcu")
+            secs += t
+    else:
+        ora, kind = CpuOracle(ORACLE_LIB), "port"
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            for s in srcs:
+                ora.run_concrete(s, cfg, "syn.mcu")
+        secs = time.perf_counter() - t0
+        threads = 1
+    inst = threads * reps * len(srcs) * INST_PER_THREAD * sample
+    return inst / secs, kind, threads, secs, inst
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        reference_rate(threads, 1, SAMPLE_THREADS)
+    tot_inst, tot_secs = 0, 0.0
+    kind = "reference"
+    for _ in range(args.steps):
+        _, kind, threads, secs, inst = reference_rate(threads, 1, SAMPLE_THREADS)
+        tot_inst += inst
+        tot_secs += secs
+    v = tot_inst / tot_secs
+    sample = (f"{threads} host threads x both stencil variants at {SAMPLE_THREADS} MiniCU "
+              f"threads each per step (hgrd::runConcrete, caps raised)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_threads": SAMPLE_THREADS},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def build_specs(hg, ctx):
+    specs = []
+    for barrier in (False, True):
+        src = programs.stencil(N_THREADS, BLOCK, barrier)
+        low = hg.lower(src, "st")
+        sizes = {"in_": N_THREADS, "tile": N_THREADS // BLOCK * (BLOCK + 2), "out_": N_THREADS}
+        handles = {k: ctx.alloc(v) for k, v in sizes.items()}
+        spec = hg.LaunchSpec(low, (N_THREADS // BLOCK, 1, 1), (BLOCK, 1, 1), WS,
+                             handles=handles)
+        host = {k: np.zeros(v, np.int64) for k, v in sizes.items()}  # reference buffers_
+        specs.append((spec, handles, host))
+    return specs
+
+
+def run_gpu_arm(args):
+    import torch
+    import paper_2604_02106_b200 as hg
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = hg.GpuContext(local)
+    ctx.set_profiling(True)
+    specs = build_specs(hg, ctx)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        out = []
+        for spec, _, _ in specs:
+            res = ctx.check_launch(spec)
+            out.append((res, ctx.last_profile()))
+        return out
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    # correctness guard: the report must be the known one (tests pin it to the oracle)
+    got = step()
+    kinds = sorted(r["kind"] for r in got[0][0]["races"])
+    assert kinds == ["INTRA-BLOCK", "INTRA-BLOCK", "INTRA-WARP", "INTRA-WARP"], kinds
+    assert not got[1][0]["races"]
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    launches0 = ctx.kernel_launches()
+    barrier()
+    dev_ms = 0.0
+    stage_ms = {}
+    stage_n = {}
+    inst = 0
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        for res, prof in step():
+            dev_ms += res["deviceMs"]
+            inst += res["instances"]
+            for s in prof:
+                stage_ms[s["name"]] = stage_ms.get(s["name"], 0.0) + s["ms"]
+                stage_n[s["name"]] = stage_n.get(s["name"], 0) + 1
+    barrier()
+    wall = time.perf_counter() - wall0
+    launches = ctx.kernel_launches() - launches0
+    clk = clocks.stop()
+
+    # e2e: host buffers -> device, check, report back (wall clock)
+    h2d = sum(sum(a.nbytes for a in host.values()) for _, _, host in specs)
+    barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(args.steps):
+        for spec, handles, host in specs:
+            for name, arr in host.items():
+                ctx.write(handles[name], arr)
+            raw = ctx.check_launch(spec, raw=True)
+            d2h += raw.n_races * 56 + 88
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    d2h //= max(args.steps, 1)
+
+    if ws > 1:
+        t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms, e2e_s = float(t[0]), float(t[1])
+    total_inst = inst * ws
+    value = total_inst / (dev_ms / 1e3)
+    e2e_value = total_inst / e2e_s
+
+    peak, peak_kind = peaks()
+    dom = max(stage_ms, key=stage_ms.get)
+    per_launch_inst = INST_PER_THREAD * N_THREADS
+    dom_avg_ms = stage_ms[dom] / stage_n[dom]
+    achieved = B_ALG * per_launch_inst / (dom_avg_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "threads_per_launch": N_THREADS,
+                   "instances_per_step": 2 * per_launch_inst,
+                   "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"replicas{ws}"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": dom,
+                     "kernel_avg_ms": dom_avg_ms, "peak_source": peak_kind,
+                     "stage_share": {k: v / sum(stage_ms.values()) for k, v in stage_ms.items()}},
+        "clocks": clk,
+        "wall_s": wall,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, kind, threads, secs, n = reference_rate(threads, 2, SAMPLE_THREADS)
+        line["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{threads} host threads x 2 reps x both variants at {SAMPLE_THREADS} "
+                      f"threads ({n} instances, {secs:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

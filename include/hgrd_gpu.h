@@ -183,6 +183,14 @@ int hgrd_gpu_buffer_read(hgrd_gpu_ctx *ctx, int32_t handle, int64_t offset,
 int hgrd_gpu_check_launch(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
                           hgrd_gpu_result *result);
 
+/* ---- instrumentation --------------------------------------------------- */
+/* Per-stage CUDA-event timing of the next checks (off by default). */
+int hgrd_gpu_set_profiling(hgrd_gpu_ctx *ctx, int on);
+/* JSON [{"name":..., "ms":...}] of the last check's stages (ctx-owned). */
+const char *hgrd_gpu_last_profile(hgrd_gpu_ctx *ctx);
+/* Number of this library's own kernels launched by the context so far. */
+unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *ctx);
+
 /* ---- reference-shaped entry points (JSON in / JSON out) ---------------- */
 /* cfg: {"gridCap":[3],"blockCap":[3],"warpSize":n,"inputs":[..],
  *       "maxThreads":n,"maxArrayElems":n,"maxSteps":n}  (ExecConfig)

@@ -1,0 +1,346 @@
+"""hgrd-b200 — the race-check stage of arXiv 2604.02106 (HGRD) on B200.
+
+Python face of ``libhgrd_gpu.so`` (C ABI: ``include/hgrd_gpu.h``).  The names
+mirror the reference's oracle API (reference include/hgrd/oracle.hpp):
+
+* :class:`ExecConfig`, :class:`SweepCaps`   — oracle.hpp:17-25, :59-66
+* :meth:`GpuContext.run_concrete`            — ``hgrd::runConcrete``      (:57)
+* :meth:`GpuContext.enumerate_verdict`       — ``hgrd::enumerateVerdict`` (:75)
+* :func:`count_inputs`                       — ``hgrd::countInputs``      (:79)
+
+Results are the reference's ``OracleResult`` / ``SweepRace`` fields as JSON
+dicts (plus ``witnesses`` and ``stats``).  There is no CPU fallback: without
+the built library or without an sm_100 device these calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIBRARY_PATH = os.path.join(_HERE, "libhgrd_gpu.so")
+
+# ---------------------------------------------------------------- ABI types
+c_int32, c_int64, c_uint8, c_uint16, c_uint32, c_uint64 = (
+    ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8, ctypes.c_uint16,
+    ctypes.c_uint32, ctypes.c_uint64)
+
+LAUNCH_SEQUENTIAL = 1
+LAUNCH_PAIRWISE = 2
+LAUNCH_NO_WITNESS = 4
+RACE_KINDS = ("INTER-BLOCK", "INTRA-BLOCK", "INTRA-WARP")
+
+
+class Insn(ctypes.Structure):
+    _fields_ = [("op", c_uint8), ("sub", c_uint8), ("a", c_uint16), ("b", c_uint16),
+                ("c", c_uint16), ("pad", c_uint16), ("imm", c_int64)]
+
+
+class Site(ctypes.Structure):
+    _fields_ = [("loc", c_int32), ("param", c_int32), ("kind", c_uint8),
+                ("atomic_op", c_uint8), ("scope", c_uint8), ("pad0", c_uint8),
+                ("pad1", c_int32)]
+
+
+class Launch(ctypes.Structure):
+    _fields_ = [("code", ctypes.POINTER(Insn)), ("n_code", c_uint32), ("n_regs", c_uint32),
+                ("reg_init", ctypes.POINTER(c_int64)), ("sites", ctypes.POINTER(Site)),
+                ("n_sites", c_uint32), ("n_locs", c_uint32),
+                ("param_handle", ctypes.POINTER(c_int32)), ("n_params", c_uint32),
+                ("flags", c_uint32), ("grid", c_int64 * 3), ("block", c_int64 * 3),
+                ("warp_size", c_int64), ("step_budget", c_int64)]
+
+
+class Race(ctypes.Structure):
+    _fields_ = [("loc_a", c_int32), ("loc_b", c_int32), ("kind", c_int32),
+                ("site_x", c_int32), ("site_y", c_int32), ("handle", c_int32),
+                ("index", c_int64), ("thread_x", c_int64), ("thread_y", c_int64),
+                ("seq_x", c_int32), ("seq_y", c_int32)]
+
+
+class Trap(ctypes.Structure):
+    _fields_ = [("site", c_int32), ("kind", c_int32), ("thread", c_int64)]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [("races", ctypes.POINTER(Race)), ("race_cap", c_uint32), ("n_races", c_uint32),
+                ("traps", ctypes.POINTER(Trap)), ("trap_cap", c_uint32), ("n_traps", c_uint32),
+                ("n_traps_total", c_uint64), ("steps", c_int64), ("instances", c_uint64),
+                ("records", c_uint64), ("aborted", c_int32), ("abort_stmt", c_int32),
+                ("mode", c_uint32), ("device_ms", ctypes.c_float)]
+
+
+# ----------------------------------------------------------- configuration
+@dataclass
+class ExecConfig:
+    """reference ExecConfig, include/hgrd/oracle.hpp:17-25"""
+    gridCap: Sequence[int] = (2, 2, 1)
+    blockCap: Sequence[int] = (4, 1, 1)
+    warpSize: int = 32
+    inputs: Sequence[int] = ()
+    maxThreads: int = 64
+    maxArrayElems: int = 1 << 20
+    maxSteps: int = 1 << 20
+
+    def to_json(self) -> str:
+        d = {k: list(v) if isinstance(v, (list, tuple)) else v for k, v in self.__dict__.items()}
+        return json.dumps(d)
+
+
+@dataclass
+class SweepCaps:
+    """reference SweepCaps, include/hgrd/oracle.hpp:59-66"""
+    gridCap: Sequence[int] = (2, 2, 1)
+    blockCap: Sequence[int] = (4, 1, 1)
+    inputSet: Sequence[int] = (0, 1, 2, 3, 127)
+    warpSizes: Sequence[int] = (2, 4)
+    maxThreads: int = 64
+    maxConfigs: int = 100000
+
+    def to_json(self) -> str:
+        d = {k: list(v) if isinstance(v, (list, tuple)) else v for k, v in self.__dict__.items()}
+        return json.dumps(d)
+
+
+def _cfg_json(cfg) -> str:
+    if cfg is None:
+        return "{}"
+    if isinstance(cfg, str):
+        return cfg
+    if isinstance(cfg, dict):
+        return json.dumps(cfg)
+    return cfg.to_json()
+
+
+# ------------------------------------------------------------------ library
+_lib = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the in-tree libhgrd_gpu.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIBRARY_PATH):
+        raise ImportError(f"{LIBRARY_PATH} is missing: run __graft_entry__.build() "
+                          "(python paper_2604_02106_b200/build.py)")
+    lib = ctypes.CDLL(LIBRARY_PATH)
+    P = ctypes.c_void_p
+    lib.hgrd_gpu_create.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+    lib.hgrd_gpu_destroy.argtypes = [P]
+    lib.hgrd_gpu_last_error.argtypes = [P]
+    lib.hgrd_gpu_last_error.restype = ctypes.c_char_p
+    lib.hgrd_gpu_buffers_reset.argtypes = [P]
+    lib.hgrd_gpu_buffer_alloc.argtypes = [P, c_int64, ctypes.POINTER(c_int32)]
+    lib.hgrd_gpu_buffer_write.argtypes = [P, c_int32, c_int64, c_int64, P]
+    lib.hgrd_gpu_buffer_read.argtypes = [P, c_int32, c_int64, c_int64, P]
+    lib.hgrd_gpu_check_launch.argtypes = [P, ctypes.POINTER(Launch), ctypes.POINTER(Result)]
+    for fn in ("hgrd_gpu_run_concrete_json", "hgrd_gpu_enumerate_verdict_json"):
+        getattr(lib, fn).argtypes = [P, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                     ctypes.POINTER(P)]
+    lib.hgrd_gpu_lower_json.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                        ctypes.POINTER(P)]
+    lib.hgrd_gpu_count_inputs.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+    lib.hgrd_gpu_free.argtypes = [P]
+    lib.hgrd_gpu_set_profiling.argtypes = [P, ctypes.c_int]
+    lib.hgrd_gpu_last_profile.argtypes = [P]
+    lib.hgrd_gpu_last_profile.restype = ctypes.c_char_p
+    lib.hgrd_gpu_kernel_launches.argtypes = [P]
+    lib.hgrd_gpu_kernel_launches.restype = ctypes.c_ulonglong
+    _lib = lib
+    return lib
+
+
+def _take_string(lib, p: ctypes.c_void_p) -> str:
+    s = ctypes.string_at(p.value).decode() if p.value else ""
+    lib.hgrd_gpu_free(p)
+    return s
+
+
+def count_inputs(source: str, file_name: str = "prog.mcu") -> int:
+    """reference hgrd::countInputs (src/oracle.cpp:805-861)."""
+    return load_library().hgrd_gpu_count_inputs(source.encode(), file_name.encode())
+
+
+def lower(source: str, kernel: str, file_name: str = "prog.mcu") -> dict:
+    """Lowered bytecode + access sites of one kernel (no GPU needed)."""
+    lib = load_library()
+    out = ctypes.c_void_p()
+    rc = lib.hgrd_gpu_lower_json(source.encode(), file_name.encode(), kernel.encode(),
+                                 ctypes.byref(out))
+    d = json.loads(_take_string(lib, out))
+    if rc != 0:
+        raise ValueError(f"lowering failed: {d}")
+    return d
+
+
+class LaunchSpec:
+    """A fully parameterised launch (the C ABI's hgrd_gpu_launch) + keep-alives."""
+
+    def __init__(self, lowered: dict, grid, block, warp_size: int,
+                 scalars: Optional[Dict[str, int]] = None,
+                 handles: Optional[Dict[str, int]] = None,
+                 step_budget: int = 1 << 60, flags: Optional[int] = None):
+        self.lowered = lowered
+        code = lowered["code"]
+        self._code = (Insn * len(code))(*[Insn(op, sub, a, b, c, 0, imm)
+                                         for op, sub, a, b, c, imm in code])
+        sites = lowered["sites"]
+        self._sites = (Site * max(len(sites), 1))(*[
+            Site(s["loc"], s["param"], s["kind"], s["atomicOp"], s["scope"], 0, 0)
+            for s in sites])
+        regs = [0] * max(lowered["nRegs"], 1)
+        scalars = scalars or {}
+        handles = handles or {}
+        ph = []
+        for p in lowered["params"]:
+            if p["array"]:
+                ph.append(handles.get(p["name"], -1))
+            else:
+                ph.append(-1)
+                if p["reg"] >= 0:
+                    regs[p["reg"]] = int(scalars.get(p["name"], 0))
+        self._regs = (c_int64 * len(regs))(*regs)
+        self._ph = (c_int32 * max(len(ph), 1))(*ph)
+        if flags is None:
+            flags = LAUNCH_PAIRWISE if lowered["hasLocks"] else 0
+        self.launch = Launch(self._code, len(code), lowered["nRegs"], self._regs,
+                             self._sites, len(sites), len(lowered["locs"]), self._ph, len(ph),
+                             flags, (c_int64 * 3)(*grid), (c_int64 * 3)(*block), warp_size,
+                             step_budget)
+
+    @property
+    def n_threads(self) -> int:
+        g, b = self.launch.grid, self.launch.block
+        return g[0] * g[1] * g[2] * b[0] * b[1] * b[2]
+
+    def new_result(self, trap_cap: int = 256):
+        n = max(len(self.lowered["locs"]), 1)
+        races = (Race * (3 * n * n))()
+        traps = (Trap * max(trap_cap, 1))()
+        res = Result(races, 3 * n * n, 0, traps, trap_cap, 0, 0, 0, 0, 0, 0, -1, 0, 0.0)
+        return res, races, traps
+
+    def decode(self, res: Result) -> dict:
+        """Races as reference-shaped dicts (kind, locA, locB, array, address) + witness."""
+        locs = self.lowered["locs"]
+        sites = self.lowered["sites"]
+        races = []
+        for i in range(res.n_races):
+            r = res.races[i]
+            races.append({"kind": RACE_KINDS[r.kind], "locA": list(locs[r.loc_a]),
+                          "locB": list(locs[r.loc_b]), "array": sites[r.site_x]["array"],
+                          "handle": r.handle, "address": r.index,
+                          "threadA": r.thread_x, "seqA": r.seq_x,
+                          "threadB": r.thread_y, "seqB": r.seq_y})
+        races.sort(key=lambda d: (d["locA"], d["locB"], RACE_KINDS.index(d["kind"])))
+        traps = [(res.traps[i].site, res.traps[i].kind, res.traps[i].thread)
+                 for i in range(res.n_traps)]
+        return {"races": races, "traps": traps, "steps": res.steps,
+                "instances": res.instances, "records": res.records,
+                "aborted": bool(res.aborted), "abortStmt": res.abort_stmt,
+                "mode": res.mode, "deviceMs": res.device_ms}
+
+
+class GpuContext:
+    """One B200 context (hgrd_gpu_ctx): device buffers + race-check calls."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load_library()
+        self._ctx = ctypes.c_void_p()
+        rc = self._lib.hgrd_gpu_create(device, ctypes.byref(self._ctx))
+        if rc != 0:
+            raise RuntimeError(f"hgrd_gpu_create(device={device}) failed with {rc}: "
+                               "no usable sm_100 device (there is no CPU fallback)")
+
+    def close(self):
+        if self._ctx:
+            self._lib.hgrd_gpu_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _err(self, what: str, rc: int):
+        msg = self._lib.hgrd_gpu_last_error(self._ctx)
+        raise RuntimeError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+
+    # -- reference-shaped API --
+    def run_concrete(self, source: str, config=None, file_name: str = "prog.mcu") -> dict:
+        out = ctypes.c_void_p()
+        rc = self._lib.hgrd_gpu_run_concrete_json(self._ctx, source.encode(),
+                                                  file_name.encode(),
+                                                  _cfg_json(config).encode(),
+                                                  ctypes.byref(out))
+        s = _take_string(self._lib, out)
+        if rc != 0:
+            raise RuntimeError(f"run_concrete failed ({rc}): {s}")
+        return json.loads(s)
+
+    def enumerate_verdict(self, source: str, caps=None, file_name: str = "prog.mcu") -> dict:
+        out = ctypes.c_void_p()
+        rc = self._lib.hgrd_gpu_enumerate_verdict_json(self._ctx, source.encode(),
+                                                       file_name.encode(),
+                                                       _cfg_json(caps).encode(),
+                                                       ctypes.byref(out))
+        s = _take_string(self._lib, out)
+        if rc != 0:
+            raise RuntimeError(f"enumerate_verdict failed ({rc}): {s}")
+        return json.loads(s)
+
+    # -- instrumentation --
+    def set_profiling(self, on: bool = True):
+        self._lib.hgrd_gpu_set_profiling(self._ctx, 1 if on else 0)
+
+    def last_profile(self) -> List[dict]:
+        """[{name, ms}] per pipeline stage of the last check (CUDA events)."""
+        return json.loads(self._lib.hgrd_gpu_last_profile(self._ctx).decode() or "[]")
+
+    def kernel_launches(self) -> int:
+        return int(self._lib.hgrd_gpu_kernel_launches(self._ctx))
+
+    # -- device buffers --
+    def reset(self):
+        rc = self._lib.hgrd_gpu_buffers_reset(self._ctx)
+        if rc:
+            self._err("buffers_reset", rc)
+
+    def alloc(self, elems: int) -> int:
+        h = c_int32()
+        rc = self._lib.hgrd_gpu_buffer_alloc(self._ctx, elems, ctypes.byref(h))
+        if rc:
+            self._err("buffer_alloc", rc)
+        return h.value
+
+    def write(self, handle: int, array, offset: int = 0):
+        """array: contiguous int64 numpy array (host buffer)."""
+        rc = self._lib.hgrd_gpu_buffer_write(self._ctx, handle, offset, int(array.size),
+                                             array.ctypes.data)
+        if rc:
+            self._err("buffer_write", rc)
+
+    def read(self, handle: int, out, offset: int = 0):
+        rc = self._lib.hgrd_gpu_buffer_read(self._ctx, handle, offset, int(out.size),
+                                            out.ctypes.data)
+        if rc:
+            self._err("buffer_read", rc)
+        return out
+
+    def check_launch(self, spec: LaunchSpec, trap_cap: int = 256, raw: bool = False):
+        res, races, traps = spec.new_result(trap_cap)
+        rc = self._lib.hgrd_gpu_check_launch(self._ctx, ctypes.byref(spec.launch),
+                                             ctypes.byref(res))
+        if rc:
+            self._err("check_launch", rc)
+        return res if raw else spec.decode(res)
+
+
+__all__ = ["ExecConfig", "SweepCaps", "GpuContext", "LaunchSpec", "count_inputs", "lower",
+           "load_library", "LIBRARY_PATH", "RACE_KINDS", "LAUNCH_SEQUENTIAL",
+           "LAUNCH_PAIRWISE", "LAUNCH_NO_WITNESS"]

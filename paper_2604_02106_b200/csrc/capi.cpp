@@ -1,0 +1,135 @@
+// Reference-shaped C ABI entry points of libhgrd_gpu.so: the host front end
+// (csrc/host) driving the B200 race-check stage (csrc/gpu) through the
+// device-buffer / check-launch ABI of include/hgrd_gpu.h.
+#include "hgrd_gpu.h"
+#include "host.hpp"
+
+#include <cstdlib>
+#include <cstring>
+
+using namespace hgrdgpu;
+
+namespace {
+
+class GpuBackend final : public LaunchBackend {
+public:
+  explicit GpuBackend(hgrd_gpu_ctx *c) : c_(c) {}
+  int reset() override { return hgrd_gpu_buffers_reset(c_); }
+  int alloc(int64_t elems, int32_t *handle) override {
+    return hgrd_gpu_buffer_alloc(c_, elems, handle);
+  }
+  int write(int32_t h, int64_t off, int64_t n, const int64_t *src) override {
+    return hgrd_gpu_buffer_write(c_, h, off, n, src);
+  }
+  int read(int32_t h, int64_t off, int64_t n, int64_t *dst) override {
+    return hgrd_gpu_buffer_read(c_, h, off, n, dst);
+  }
+  int checkLaunch(const hgrd_gpu_launch &l, hgrd_gpu_result &r) override {
+    return hgrd_gpu_check_launch(c_, &l, &r);
+  }
+  std::string lastError() override { return hgrd_gpu_last_error(c_); }
+
+private:
+  hgrd_gpu_ctx *c_;
+};
+
+char *dup(const std::string &s) {
+  char *p = static_cast<char *>(std::malloc(s.size() + 1));
+  if (p)
+    std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+} // namespace
+
+extern "C" {
+
+int hgrd_gpu_run_concrete_json(hgrd_gpu_ctx *ctx, const char *source,
+                               const char *file_name, const char *cfg_json,
+                               char **out) {
+  if (!ctx || !out)
+    return HGRD_GPU_EINVAL;
+  GpuBackend be(ctx);
+  std::string s;
+  int rc = runConcreteJson(be, source, file_name, cfg_json, s);
+  *out = dup(s);
+  return rc;
+}
+
+int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
+                                    const char *file_name, const char *caps_json,
+                                    char **out) {
+  if (!ctx || !out)
+    return HGRD_GPU_EINVAL;
+  GpuBackend be(ctx);
+  std::string s;
+  int rc = enumerateVerdictJson(be, source, file_name, caps_json, s);
+  *out = dup(s);
+  return rc;
+}
+
+int hgrd_gpu_count_inputs(const char *source, const char *file_name) {
+  ParseOutcome po = parseMiniCU(source ? source : "", file_name ? file_name : "");
+  if (!po.program)
+    return HGRD_GPU_EINVAL;
+  return countInputs(*po.program);
+}
+
+void hgrd_gpu_free(char *p) { std::free(p); }
+
+} // extern "C"
+
+// Lowering only (no host interpretation): the bytecode, site table and
+// per-kernel facts of one kernel, as JSON.  Used by callers that fix the
+// launch parameters themselves (bench workloads, reference-side adapters).
+extern "C" int hgrd_gpu_lower_json(const char *source, const char *file_name,
+                                   const char *kernel, char **out) {
+  if (!out)
+    return HGRD_GPU_EINVAL;
+  ParseOutcome po = parseMiniCU(source ? source : "", file_name ? file_name : "");
+  if (!po.program) {
+    *out = dup(errorJson(po.diagnostics));
+    return HGRD_GPU_EINVAL;
+  }
+  const Function *k = po.program->findKernel(kernel ? kernel : "");
+  if (!k) {
+    *out = dup(errorJson({"unknown kernel"}));
+    return HGRD_GPU_EINVAL;
+  }
+  LoweredKernel lk = lowerKernel(*k);
+  std::string s = "{\"nRegs\":" + std::to_string(lk.nRegs) + ",\"hasLocks\":" +
+                  (lk.hasLocks ? "true" : "false") + ",\"code\":[";
+  for (size_t i = 0; i < lk.code.size(); ++i) {
+    const auto &I = lk.code[i];
+    s += (i ? ",[" : "[") + std::to_string(I.op) + "," + std::to_string(I.sub) + "," +
+         std::to_string(I.a) + "," + std::to_string(I.b) + "," + std::to_string(I.c) + "," +
+         std::to_string(I.imm) + "]";
+  }
+  s += "],\"sites\":[";
+  for (size_t i = 0; i < lk.sites.size(); ++i) {
+    const auto &S = lk.sites[i];
+    s += (i ? ",{" : "{") + std::string("\"loc\":") + std::to_string(S.loc) +
+         ",\"param\":" + std::to_string(S.param) + ",\"kind\":" + std::to_string(S.kind) +
+         ",\"atomicOp\":" + std::to_string(S.atomic_op) + ",\"scope\":" +
+         std::to_string(S.scope) + ",\"array\":\"" + lk.siteArray[i] + "\",\"valueNeeded\":" +
+         (lk.siteValueNeeded[i] ? "true" : "false") + ",\"line\":" +
+         std::to_string(lk.siteLoc[i].line) + ",\"column\":" + std::to_string(lk.siteLoc[i].col) +
+         "}";
+  }
+  s += "],\"locs\":[";
+  for (size_t i = 0; i < lk.locs.size(); ++i)
+    s += (i ? ",[" : "[") + std::to_string(lk.locs[i].line) + "," +
+         std::to_string(lk.locs[i].col) + "]";
+  s += "],\"stmtLocs\":[";
+  for (size_t i = 0; i < lk.stmtLocs.size(); ++i)
+    s += (i ? ",[" : "[") + std::to_string(lk.stmtLocs[i].line) + "," +
+         std::to_string(lk.stmtLocs[i].col) + "]";
+  s += "],\"params\":[";
+  for (size_t i = 0; i < k->params.size(); ++i)
+    s += (i ? ",{" : "{") + std::string("\"name\":\"") + k->params[i].name +
+         "\",\"array\":" + (isArray(k->params[i].type) ? "true" : "false") +
+         ",\"reg\":" + std::to_string(lk.paramReg[i]) + "}";
+  s += "]}";
+  *out = dup(s);
+  return 0;
+}

@@ -1,0 +1,979 @@
+// hgrd_gpu_ctx: device-resident buffers + the per-launch race-check
+// pipeline (include/hgrd_gpu.h).
+//
+//   blob H2D -> K1 expand (PARALLEL | SEQUENTIAL) -> counters D2H
+//     -> radix sort of packed records (CUB onesweep, bits = key width)
+//     -> K3 segment detector (summary | pairwise) -> K4 witness/decode
+//     -> races D2H
+#include "detect.cuh"
+#include "device.cuh"
+#include "expand.cuh"
+
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace hgrdgpu::dev;
+
+// element ids + identity permutation for the stable element sort
+__global__ void k_elem_keys(const uint64_t *keys, uint64_t n, int shE, uint64_t *elem,
+                            uint32_t *order) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    elem[i] = shE >= 64 ? 0 : keys[i] >> shE;
+    order[i] = static_cast<uint32_t>(i);
+  }
+}
+
+namespace {
+
+template <class T> struct DevVec {
+  T *p = nullptr;
+  size_t cap = 0;
+};
+
+struct BigBlock {
+  void *p;
+  size_t bytes;
+};
+
+int bitsFor(uint64_t n) { // bits to hold values 0 .. n-1
+  if (n <= 1)
+    return 0;
+  return 64 - __builtin_clzll(n - 1);
+}
+
+} // namespace
+
+struct hgrd_gpu_ctx {
+  int device = 0;
+  int nSM = 148;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::string err;
+
+  struct Buf {
+    int64_t *p;
+    int64_t elems;
+  };
+  std::vector<Buf> bufs;
+  // small allocations: bump arena over 256 MiB chunks; large: size-keyed cache
+  std::vector<char *> chunks;
+  size_t chunkBytes = size_t(256) << 20;
+  size_t chunkIdx = 0, chunkUsed = 0;
+  std::multimap<size_t, void *> bigFree;
+  std::vector<BigBlock> bigUsed;
+
+  DevVec<uint64_t> keys, keysAlt, elemK, elemKAlt;
+  DevVec<uint32_t> vals, valsAlt, order, orderAlt;
+  DevVec<unsigned char> cubTemp, blob, snapshot;
+  DevVec<uint32_t> keySeg;
+  DevVec<unsigned long long> keyPair;
+  DevVec<hgrd_gpu_race> races;
+  DevVec<Counters> ctr;
+  DevVec<int64_t> seqRegs, opIndex;
+  DevVec<int32_t> opMeta, opSeq;
+  DevVec<uint64_t> opStart;
+  DevVec<hgrd_gpu_trap> traps;
+
+  unsigned char *hStage = nullptr;
+  size_t hStageCap = 0;
+  Counters *hCtr = nullptr;
+  uint64_t capHint = 1 << 16;
+  uint64_t opHint = 1 << 12;
+
+  // optional per-stage timing (CUDA events on the launching stream)
+  bool profiling = false;
+  struct Stage {
+    const char *name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Stage> stages;      // recorded in the current check
+  std::vector<cudaEvent_t> evPool;
+  size_t evUsed = 0;
+  std::string profileJson;
+  unsigned long long kernelLaunches = 0; // own kernels launched (lifetime)
+};
+
+namespace {
+
+int cudaFail(hgrd_gpu_ctx *c, cudaError_t e, const char *what) {
+  c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return HGRD_GPU_ECUDA;
+}
+
+#define CK(expr)                                                                       \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return cudaFail(c, _e, #expr);                                                   \
+  } while (0)
+
+template <class T> int need(hgrd_gpu_ctx *c, DevVec<T> &v, size_t n) {
+  if (n == 0)
+    n = 1;
+  if (v.cap >= n)
+    return 0;
+  size_t want = std::max(n, v.cap + v.cap / 2);
+  if (v.p) {
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaFree(v.p));
+    v.p = nullptr;
+    v.cap = 0;
+  }
+  cudaError_t e = cudaMalloc(&v.p, want * sizeof(T));
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    e = cudaMalloc(&v.p, n * sizeof(T));
+    want = n;
+  }
+  if (e != cudaSuccess) {
+    v.p = nullptr;
+    c->err = "device allocation failed";
+    return HGRD_GPU_ENOMEM;
+  }
+  v.cap = want;
+  return 0;
+}
+
+#define NEED(v, n)                                                                     \
+  do {                                                                                 \
+    int _rc = need(c, v, n);                                                           \
+    if (_rc < 0)                                                                       \
+      return _rc;                                                                      \
+  } while (0)
+
+cudaEvent_t poolEvent(hgrd_gpu_ctx *c) {
+  if (c->evUsed == c->evPool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evPool.push_back(e);
+  }
+  return c->evPool[c->evUsed++];
+}
+
+// RAII marker around one pipeline stage when profiling is on.
+struct StageTimer {
+  hgrd_gpu_ctx *c;
+  size_t idx = SIZE_MAX;
+  StageTimer(hgrd_gpu_ctx *ctx, const char *name) : c(ctx) {
+    if (!c->profiling)
+      return;
+    hgrd_gpu_ctx::Stage s{name, poolEvent(c), poolEvent(c)};
+    cudaEventRecord(s.a, c->st);
+    c->stages.push_back(s);
+    idx = c->stages.size() - 1;
+  }
+  ~StageTimer() {
+    if (idx != SIZE_MAX)
+      cudaEventRecord(c->stages[idx].b, c->st);
+  }
+};
+
+int stage(hgrd_gpu_ctx *c, size_t bytes) {
+  if (c->hStageCap >= bytes)
+    return 0;
+  if (c->hStage) {
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaFreeHost(c->hStage));
+  }
+  size_t want = std::max(bytes, size_t(1) << 20);
+  CK(cudaMallocHost(&c->hStage, want));
+  c->hStageCap = want;
+  return 0;
+}
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Static bound on the barrier phases of one thread: straight-line code
+// executes each barrier at most once; a barrier inside a loop is unbounded.
+void phaseBounds(const hgrd_gpu_launch &L, int &bP, int &bQ, bool &bounded,
+                 uint32_t &recInsns, bool &loops) {
+  uint32_t nS = 0, nW = 0;
+  loops = false;
+  bounded = true;
+  recInsns = 0;
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    const auto &I = L.code[pc];
+    if (I.op == HGRD_OP_SYNCTHREADS)
+      ++nS;
+    if (I.op == HGRD_OP_SYNCWARP)
+      ++nW;
+    if (I.op == HGRD_OP_LOAD || I.op == HGRD_OP_STORE || I.op == HGRD_OP_ATOMIC)
+      ++recInsns;
+    if (I.op == HGRD_OP_JMP && I.imm <= static_cast<int64_t>(pc)) {
+      loops = true;
+      for (int64_t q = I.imm; q <= static_cast<int64_t>(pc); ++q) {
+        uint8_t op = L.code[q].op;
+        if (op == HGRD_OP_SYNCTHREADS || op == HGRD_OP_SYNCWARP)
+          bounded = false;
+      }
+    }
+  }
+  if (bounded) {
+    bP = bitsFor(uint64_t(nS) + 1);
+    bQ = bitsFor(uint64_t(nS) + nW + 1);
+  } else {
+    bP = 8;
+    bQ = 8;
+  }
+}
+
+bool makeLayout(KeyLayout &k, int bE, int bB, int bP, int bW, int bQ, int bL) {
+  k.bE = bE;
+  k.bB = bB;
+  k.bP = bP;
+  k.bW = bW;
+  k.bQ = bQ;
+  k.bL = bL;
+  k.shQ = bL;
+  k.shW = k.shQ + bQ;
+  k.shP = k.shW + bW;
+  k.shB = k.shP + bP;
+  k.shE = k.shB + bB;
+  k.total = k.shE + bE;
+  if (k.total > 64)
+    return false;
+  k.sentinel = k.total == 64 ? ~0ull : ((1ull << k.total) - 1);
+  return true;
+}
+
+struct Plan {
+  std::vector<ParamDev> params;
+  std::vector<SiteDev> sites;
+  std::vector<uint64_t> confInter, confIntra, locMask, wBase;
+  std::vector<int32_t> wHandle;
+  uint64_t totalW = 0;
+  bool summaryOk = true;
+};
+
+void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
+  std::vector<char> written(c->bufs.size(), 0);
+  auto handleOfParam = [&](int p) -> int32_t {
+    if (p < 0 || static_cast<uint32_t>(p) >= L.n_params)
+      return -1;
+    int32_t h = L.param_handle[p];
+    return (h >= 0 && static_cast<size_t>(h) < c->bufs.size()) ? h : -1;
+  };
+  for (uint32_t s = 0; s < L.n_sites; ++s)
+    if (L.sites[s].kind != HGRD_SITE_LOAD && handleOfParam(L.sites[s].param) >= 0)
+      written[static_cast<size_t>(handleOfParam(L.sites[s].param))] = 1;
+  std::vector<uint64_t> base(c->bufs.size(), 0);
+  for (size_t h = 0; h < c->bufs.size(); ++h)
+    if (written[h]) {
+      base[h] = P.totalW;
+      P.wBase.push_back(P.totalW);
+      P.wHandle.push_back(static_cast<int32_t>(h));
+      P.totalW += static_cast<uint64_t>(c->bufs[h].elems);
+    }
+  if (P.wBase.empty()) {
+    P.wBase.push_back(0);
+    P.wHandle.push_back(-1);
+  }
+  P.params.resize(std::max<uint32_t>(L.n_params, 1));
+  for (uint32_t p = 0; p < L.n_params; ++p) {
+    ParamDev d{};
+    int32_t h = handleOfParam(static_cast<int>(p));
+    d.handle = h;
+    if (h >= 0) {
+      d.ptr = c->bufs[static_cast<size_t>(h)].p;
+      d.size = c->bufs[static_cast<size_t>(h)].elems;
+      d.written = written[static_cast<size_t>(h)];
+      d.elemBase = base[static_cast<size_t>(h)];
+    }
+    P.params[p] = d;
+  }
+  P.sites.resize(std::max<uint32_t>(L.n_sites, 1));
+  for (uint32_t s = 0; s < L.n_sites; ++s) {
+    SiteDev d{};
+    d.param = L.sites[s].param;
+    d.loc = L.sites[s].loc;
+    d.kind = L.sites[s].kind;
+    d.aop = L.sites[s].atomic_op;
+    d.scope = L.sites[s].scope;
+    int32_t h = handleOfParam(d.param);
+    d.record = (h >= 0 && written[static_cast<size_t>(h)]) ? 1 : 0;
+    P.sites[s] = d;
+  }
+  P.summaryOk = L.n_sites <= static_cast<uint32_t>(kMaxSites);
+  const uint32_t ns = std::min<uint32_t>(L.n_sites, kMaxSites);
+  P.confInter.assign(std::max<uint32_t>(ns, 1), 0);
+  P.confIntra.assign(std::max<uint32_t>(ns, 1), 0);
+  P.locMask.assign(std::max<uint32_t>(L.n_locs, 1), 0);
+  // static pair rules (reference :752-758): a write, and not two atomics
+  // whose scopes both cover the pair
+  for (uint32_t a = 0; a < ns; ++a) {
+    const auto &A = L.sites[a];
+    P.locMask[static_cast<size_t>(A.loc)] |= 1ull << a;
+    for (uint32_t b = 0; b < ns; ++b) {
+      const auto &B = L.sites[b];
+      const bool write = A.kind != HGRD_SITE_LOAD || B.kind != HGRD_SITE_LOAD;
+      const bool bothAtomic = A.kind == HGRD_SITE_ATOMIC && B.kind == HGRD_SITE_ATOMIC;
+      const bool devBoth = A.scope == HGRD_SCOPE_DEVICE && B.scope == HGRD_SCOPE_DEVICE;
+      const bool blkBoth = A.scope != HGRD_SCOPE_NONE && B.scope != HGRD_SCOPE_NONE;
+      if (write && !(bothAtomic && devBoth))
+        P.confInter[a] |= 1ull << b;
+      if (write && !(bothAtomic && blkBoth))
+        P.confIntra[a] |= 1ull << b;
+    }
+  }
+}
+
+struct BlobOffsets {
+  size_t code, sites, params, regs, cInter, cIntra, locMask, wBase, wHandle, total;
+};
+
+int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOffsets &o) {
+  size_t off = 0;
+  auto put = [&](size_t bytes) {
+    size_t at = off;
+    off = align16(off + bytes);
+    return at;
+  };
+  o.code = put(sizeof(hgrd_gpu_insn) * L.n_code);
+  o.sites = put(sizeof(SiteDev) * P.sites.size());
+  o.params = put(sizeof(ParamDev) * P.params.size());
+  o.regs = put(sizeof(int64_t) * std::max<uint32_t>(L.n_regs, 1));
+  o.cInter = put(8 * P.confInter.size());
+  o.cIntra = put(8 * P.confIntra.size());
+  o.locMask = put(8 * P.locMask.size());
+  o.wBase = put(8 * P.wBase.size());
+  o.wHandle = put(4 * P.wHandle.size());
+  o.total = off;
+  int rc = stage(c, o.total);
+  if (rc < 0)
+    return rc;
+  CK(cudaStreamSynchronize(c->st)); // staging buffer reuse
+  NEED(c->blob, o.total);
+  unsigned char *h = c->hStage;
+  std::memcpy(h + o.code, L.code, sizeof(hgrd_gpu_insn) * L.n_code);
+  std::memcpy(h + o.sites, P.sites.data(), sizeof(SiteDev) * P.sites.size());
+  std::memcpy(h + o.params, P.params.data(), sizeof(ParamDev) * P.params.size());
+  if (L.n_regs)
+    std::memcpy(h + o.regs, L.reg_init, sizeof(int64_t) * L.n_regs);
+  std::memcpy(h + o.cInter, P.confInter.data(), 8 * P.confInter.size());
+  std::memcpy(h + o.cIntra, P.confIntra.data(), 8 * P.confIntra.size());
+  std::memcpy(h + o.locMask, P.locMask.data(), 8 * P.locMask.size());
+  std::memcpy(h + o.wBase, P.wBase.data(), 8 * P.wBase.size());
+  std::memcpy(h + o.wHandle, P.wHandle.data(), 4 * P.wHandle.size());
+  CK(cudaMemcpyAsync(c->blob.p, h, o.total, cudaMemcpyHostToDevice, c->st));
+  return 0;
+}
+
+int readCounters(hgrd_gpu_ctx *c) {
+  CK(cudaMemcpyAsync(c->hCtr, c->ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+// Sort + detect + witness over `n` records in c->keys/c->vals (layout kl).
+int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOffsets &o,
+           uint64_t n, bool pairwise, bool locks, hgrd_gpu_result *R) {
+  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+  const int nKeys = 3 * nLocs * nLocs;
+  NEED(c->races, static_cast<size_t>(nKeys));
+  CK(cudaMemsetAsync(&c->ctr.p->nRaces, 0, sizeof(unsigned), c->st));
+  DetectArgs A{};
+  A.n = n;
+  A.kl = D.kl;
+  A.sites = D.sites;
+  A.confInter = D.confInter;
+  A.confIntra = D.confIntra;
+  A.locMask = D.locMask;
+  A.nLocs = nLocs;
+  A.nSites = static_cast<int>(L.n_sites);
+  A.tpb = D.tpb;
+  A.ws = D.ws;
+  A.wBase = reinterpret_cast<const uint64_t *>(c->blob.p + o.wBase);
+  A.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
+  A.nW = static_cast<int>((o.wHandle - o.wBase) / 8 > 0 ? (o.wHandle - o.wBase) / 8 : 1);
+  if (n > 1) {
+    if (!pairwise) {
+      NEED(c->keysAlt, n);
+      NEED(c->valsAlt, n);
+      cub::DoubleBuffer<uint64_t> dk(c->keys.p, c->keysAlt.p);
+      cub::DoubleBuffer<uint32_t> dv(c->vals.p, c->valsAlt.p);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, static_cast<int64_t>(n), 0,
+                                         D.kl.total, c->st));
+      NEED(c->cubTemp, tb);
+      {
+        StageTimer t(c, "sort_records");
+        CK(cub::DeviceRadixSort::SortPairs(c->cubTemp.p, tb, dk, dv, static_cast<int64_t>(n),
+                                           0, D.kl.total, c->st));
+      }
+      A.keys = dk.Current();
+      A.vals = dv.Current();
+      NEED(c->keySeg, static_cast<size_t>(nKeys));
+      CK(cudaMemsetAsync(c->keySeg.p, 0xff, sizeof(uint32_t) * nKeys, c->st));
+      const unsigned g = static_cast<unsigned>((n + 255) / 256);
+      {
+        StageTimer t(c, "k_detect_summary");
+        k_detect_summary<<<g, 256, 0, c->st>>>(A, c->keySeg.p);
+      }
+      CK(cudaGetLastError());
+      {
+        StageTimer t(c, "k_witness");
+        k_witness<<<(nKeys + 127) / 128, 128, 0, c->st>>>(A, c->keySeg.p, nKeys, c->races.p,
+                                                           c->ctr.p);
+      }
+      CK(cudaGetLastError());
+      c->kernelLaunches += 2;
+    } else {
+      // canonical-order records, stable sort by element
+      A.keys = c->keys.p;
+      A.vals = c->vals.p;
+      NEED(c->elemK, n);
+      NEED(c->elemKAlt, n);
+      NEED(c->order, n);
+      NEED(c->orderAlt, n);
+      const unsigned g = static_cast<unsigned>((n + 255) / 256);
+      k_elem_keys<<<g, 256, 0, c->st>>>(c->keys.p, n, D.kl.shE, c->elemK.p, c->order.p);
+      CK(cudaGetLastError());
+      cub::DoubleBuffer<uint64_t> dk(c->elemK.p, c->elemKAlt.p);
+      cub::DoubleBuffer<uint32_t> dv(c->order.p, c->orderAlt.p);
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, static_cast<int64_t>(n), 0,
+                                         std::max(D.kl.bE, 1), c->st));
+      NEED(c->cubTemp, tb);
+      CK(cub::DeviceRadixSort::SortPairs(c->cubTemp.p, tb, dk, dv, static_cast<int64_t>(n), 0,
+                                         std::max(D.kl.bE, 1), c->st));
+      NEED(c->keyPair, static_cast<size_t>(nKeys));
+      CK(cudaMemsetAsync(c->keyPair.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
+      {
+        StageTimer t(c, "k_detect_pairwise");
+        k_detect_pairwise<<<g, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(), locks,
+                                                 c->keyPair.p);
+      }
+      CK(cudaGetLastError());
+      k_decode_pairwise<<<(nKeys + 127) / 128, 128, 0, c->st>>>(
+          A, dk.Current(), dv.Current(), c->keyPair.p, nKeys, c->races.p, c->ctr.p);
+      CK(cudaGetLastError());
+      c->kernelLaunches += 3;
+    }
+  }
+  int rc = readCounters(c);
+  if (rc < 0)
+    return rc;
+  if (c->hCtr->flags & (kFlagLockSet | kFlagSegment)) {
+    c->err = "pairwise detector limits exceeded (lock sets > 8 or element > 65535 events)";
+    return HGRD_GPU_ENOTSUP;
+  }
+  const unsigned nr = c->hCtr->nRaces;
+  R->n_races = nr;
+  if (nr > R->race_cap)
+    return HGRD_GPU_E2BIG;
+  if (nr) {
+    CK(cudaMemcpyAsync(R->races, c->races.p, sizeof(hgrd_gpu_race) * nr,
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  return 0;
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+namespace {
+
+bool validLaunch(const hgrd_gpu_launch &L, std::string &why) {
+  if (!L.code || L.n_code == 0) {
+    why = "empty code";
+    return false;
+  }
+  if (L.warp_size <= 0) {
+    why = "warp size must be positive";
+    return false;
+  }
+  for (int d = 0; d < 3; ++d)
+    if (L.grid[d] <= 0 || L.block[d] <= 0) {
+      why = "non-positive launch dimension";
+      return false;
+    }
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    const auto &I = L.code[pc];
+    if (I.op > HGRD_OP_JMP) {
+      why = "bad opcode";
+      return false;
+    }
+    if ((I.op == HGRD_OP_JZ || I.op == HGRD_OP_JMP) &&
+        (I.imm < 0 || I.imm >= static_cast<int64_t>(L.n_code))) {
+      why = "bad jump target";
+      return false;
+    }
+    if ((I.op == HGRD_OP_LOAD || I.op == HGRD_OP_STORE || I.op == HGRD_OP_ATOMIC) &&
+        (I.imm < 0 || I.imm >= static_cast<int64_t>(L.n_sites))) {
+      why = "bad site";
+      return false;
+    }
+    if (I.op != HGRD_OP_STEP && I.op != HGRD_OP_JMP && I.op != HGRD_OP_END &&
+        (I.a >= L.n_regs || I.b >= std::max<uint32_t>(L.n_regs, 1) ||
+         I.c >= std::max<uint32_t>(L.n_regs, 1)))
+      if (I.op != HGRD_OP_SYNCTHREADS && I.op != HGRD_OP_SYNCWARP && I.op != HGRD_OP_FENCE) {
+        why = "register out of range";
+        return false;
+      }
+    if (I.op == HGRD_OP_BUILTIN && I.sub >= 12) {
+      why = "bad builtin";
+      return false;
+    }
+  }
+  if (L.code[L.n_code - 1].op != HGRD_OP_END) {
+    why = "code must end with END";
+    return false;
+  }
+  for (uint32_t s = 0; s < L.n_sites; ++s)
+    if (L.sites[s].loc < 0 || static_cast<uint32_t>(L.sites[s].loc) >= L.n_locs ||
+        L.sites[s].param >= static_cast<int32_t>(L.n_params)) {
+      why = "bad site table";
+      return false;
+    }
+  return true;
+}
+
+int snapshot(hgrd_gpu_ctx *c, const Plan &P, bool restore) {
+  size_t off = 0;
+  for (int32_t h : P.wHandle) {
+    if (h < 0)
+      continue;
+    const auto &b = c->bufs[static_cast<size_t>(h)];
+    const size_t bytes = static_cast<size_t>(b.elems) * 8;
+    if (!restore) {
+      CK(cudaMemcpyAsync(c->snapshot.p + off, b.p, bytes, cudaMemcpyDeviceToDevice, c->st));
+    } else {
+      CK(cudaMemcpyAsync(b.p, c->snapshot.p + off, bytes, cudaMemcpyDeviceToDevice, c->st));
+    }
+    off += bytes;
+  }
+  return 0;
+}
+
+int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
+  R->n_races = 0;
+  R->n_traps = 0;
+  R->n_traps_total = 0;
+  R->steps = 0;
+  R->instances = 0;
+  R->records = 0;
+  R->aborted = 0;
+  R->abort_stmt = -1;
+  R->mode = 0;
+  R->device_ms = 0;
+  c->stages.clear();
+  c->evUsed = 0;
+  CK(cudaEventRecord(c->e0, c->st));
+
+  Plan P;
+  planLaunch(c, L, P);
+  BlobOffsets o{};
+  int rc = uploadBlob(c, L, P, o);
+  if (rc < 0)
+    return rc;
+  NEED(c->ctr, 1);
+
+  LaunchDev D{};
+  D.code = reinterpret_cast<const hgrd_gpu_insn *>(c->blob.p + o.code);
+  D.sites = reinterpret_cast<const SiteDev *>(c->blob.p + o.sites);
+  D.params = reinterpret_cast<const ParamDev *>(c->blob.p + o.params);
+  D.regInit = reinterpret_cast<const int64_t *>(c->blob.p + o.regs);
+  D.confInter = reinterpret_cast<const uint64_t *>(c->blob.p + o.cInter);
+  D.confIntra = reinterpret_cast<const uint64_t *>(c->blob.p + o.cIntra);
+  D.locMask = reinterpret_cast<const uint64_t *>(c->blob.p + o.locMask);
+  D.nCode = static_cast<int>(L.n_code);
+  D.nRegs = static_cast<int>(L.n_regs);
+  D.nSites = static_cast<int>(L.n_sites);
+  D.nParams = static_cast<int>(L.n_params);
+  D.nLocs = static_cast<int>(L.n_locs);
+  for (int d = 0; d < 3; ++d) {
+    D.grid[d] = L.grid[d];
+    D.block[d] = L.block[d];
+  }
+  D.ws = L.warp_size;
+  D.tpb = L.block[0] * L.block[1] * L.block[2];
+  D.nBlocks = L.grid[0] * L.grid[1] * L.grid[2];
+  D.nThreads = D.nBlocks * D.tpb;
+  D.stepBudget = L.step_budget;
+  D.ctr = c->ctr.p;
+
+  int bP, bQ;
+  bool bounded, loops;
+  uint32_t accessInsns;
+  phaseBounds(L, bP, bQ, bounded, accessInsns, loops);
+  uint32_t recInsns = 0;
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    const auto &I = L.code[pc];
+    if ((I.op == HGRD_OP_LOAD || I.op == HGRD_OP_STORE || I.op == HGRD_OP_ATOMIC) &&
+        P.sites[static_cast<size_t>(I.imm)].record)
+      ++recInsns;
+  }
+  const int bE = bitsFor(P.totalW + 1);
+  const int bB = bitsFor(static_cast<uint64_t>(D.nBlocks));
+  const int bW = bitsFor(static_cast<uint64_t>((D.tpb + D.ws - 1) / D.ws));
+  const int bL = bitsFor(static_cast<uint64_t>(std::min<int64_t>(D.ws, D.tpb)));
+
+  const bool locks = (L.flags & HGRD_LAUNCH_PAIRWISE) != 0;
+  const bool pairwise = locks || !P.summaryOk;
+  bool seq = (L.flags & HGRD_LAUNCH_SEQUENTIAL) || pairwise || L.n_regs > kMaxRegs;
+  const size_t smem = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
+                      sizeof(ParamDev) * P.params.size();
+  if (smem > 200 * 1024)
+    seq = true;
+  bool snapped = false;
+
+  for (int attempt = 0; attempt < 16; ++attempt) {
+    if (!makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
+      c->err = "packed record key wider than 64 bits";
+      return HGRD_GPU_ENOTSUP;
+    }
+    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(Counters), c->st));
+    if (!seq) {
+      const uint64_t nBatches = (static_cast<uint64_t>(D.nThreads) + 31) / 32;
+      const uint64_t blocks = std::min<uint64_t>((nBatches + 7) / 8, uint64_t(c->nSM) * 8);
+      const uint64_t warps = blocks * 8;
+      const uint64_t expected = static_cast<uint64_t>(D.nThreads) * recInsns;
+      uint64_t chunk = std::clamp<uint64_t>(expected / std::max<uint64_t>(warps, 1) / 4, 64, kChunk);
+      uint64_t cap = expected + warps * chunk + 4096;
+      if (loops)
+        cap = std::max(cap, c->capHint);
+      D.chunk = static_cast<uint32_t>(chunk);
+      NEED(c->keys, cap);
+      NEED(c->vals, cap);
+      D.keys = c->keys.p;
+      D.vals = c->vals.p;
+      D.capacity = cap;
+      if (smem > 48 * 1024)
+        CK(cudaFuncSetAttribute(k_expand_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+      {
+        StageTimer t(c, "k_expand_par");
+        k_expand_par<<<static_cast<unsigned>(blocks), 256, smem, c->st>>>(D);
+      }
+      CK(cudaGetLastError());
+      ++c->kernelLaunches;
+      rc = readCounters(c);
+      if (rc < 0)
+        return rc;
+      const Counters h = *c->hCtr;
+      if ((h.flags & kFlagAbort) || static_cast<int64_t>(h.steps) > L.step_budget ||
+          h.traps > 0) {
+        seq = true; // traps / budget need the canonical order
+        continue;
+      }
+      if (h.flags & kFlagCapacity) {
+        c->capHint = std::max<uint64_t>(c->capHint, h.cursor + warps * chunk + 4096) * 2;
+        continue;
+      }
+      if (h.flags & kFlagPhase) {
+        bP = std::max(bP, bitsFor(uint64_t(h.maxBp) + 1));
+        bQ = std::max(bQ, bitsFor(uint64_t(h.maxWp) + 1));
+        continue;
+      }
+      if (h.flags & kFlagSeqSite) {
+        c->err = "more than 2^20 accesses in one thread";
+        return HGRD_GPU_ENOTSUP;
+      }
+      R->steps = static_cast<int64_t>(h.steps);
+      R->instances = h.instances;
+      R->records = h.records;
+      R->mode = L.flags & ~HGRD_LAUNCH_SEQUENTIAL;
+      rc = detect(c, L, D, o, std::min<uint64_t>(h.cursor, cap), false, false, R);
+      if (rc < 0)
+        return rc;
+      break;
+    }
+    // SEQUENTIAL
+    if (!snapped) {
+      size_t bytes = 0;
+      for (int32_t hnd : P.wHandle)
+        if (hnd >= 0)
+          bytes += static_cast<size_t>(c->bufs[static_cast<size_t>(hnd)].elems) * 8;
+      NEED(c->snapshot, bytes);
+      rc = snapshot(c, P, false);
+      if (rc < 0)
+        return rc;
+      snapped = true;
+    } else {
+      rc = snapshot(c, P, true);
+      if (rc < 0)
+        return rc;
+    }
+    uint64_t cap = loops ? c->capHint : static_cast<uint64_t>(D.nThreads) * recInsns + 16;
+    cap = std::max<uint64_t>(cap, 16);
+    NEED(c->keys, cap);
+    NEED(c->vals, cap);
+    D.keys = c->keys.p;
+    D.vals = c->vals.p;
+    D.capacity = cap;
+    D.chunk = 0;
+    NEED(c->seqRegs, std::max<uint32_t>(L.n_regs, 1));
+    D.seqRegs = c->seqRegs.p;
+    NEED(c->traps, std::max<uint32_t>(R->trap_cap, 1));
+    D.traps = c->traps.p;
+    D.trapCap = R->trap_cap;
+    if (locks) {
+      NEED(c->opStart, static_cast<size_t>(D.nThreads) + 1);
+      uint64_t ocap = std::max<uint64_t>(c->opHint, 16);
+      NEED(c->opIndex, ocap);
+      NEED(c->opMeta, ocap);
+      NEED(c->opSeq, ocap);
+      D.opStart = c->opStart.p;
+      D.opIndex = c->opIndex.p;
+      D.opMeta = c->opMeta.p;
+      D.opSeq = c->opSeq.p;
+      D.opCap = ocap;
+    } else {
+      D.opStart = nullptr;
+      D.opCap = 0;
+    }
+    {
+      StageTimer t(c, "k_expand_seq");
+      k_expand_seq<<<1, 32, 0, c->st>>>(D);
+    }
+    CK(cudaGetLastError());
+    ++c->kernelLaunches;
+    rc = readCounters(c);
+    if (rc < 0)
+      return rc;
+    const Counters h = *c->hCtr;
+    const uint32_t nt = static_cast<uint32_t>(std::min<uint64_t>(h.traps, R->trap_cap));
+    if (!(h.flags & kFlagAbort)) {
+      bool retry = false;
+      if (h.flags & kFlagCapacity) {
+        c->capHint = std::max<uint64_t>(c->capHint, h.cursor) * 2;
+        retry = true;
+      }
+      if (h.flags & kFlagOps) {
+        c->opHint = std::max<uint64_t>(c->opHint, h.nOps) * 2;
+        retry = true;
+      }
+      if (h.flags & kFlagPhase) {
+        bP = std::max(bP, bitsFor(uint64_t(h.maxBp) + 1));
+        bQ = std::max(bQ, bitsFor(uint64_t(h.maxWp) + 1));
+        retry = true;
+      }
+      if (retry)
+        continue;
+      if (h.flags & kFlagSeqSite) {
+        c->err = "more than 2^20 accesses in one thread";
+        return HGRD_GPU_ENOTSUP;
+      }
+    }
+    if (nt) {
+      CK(cudaMemcpyAsync(R->traps, c->traps.p, sizeof(hgrd_gpu_trap) * nt,
+                         cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+    }
+    R->n_traps = nt;
+    R->n_traps_total = h.traps;
+    R->steps = static_cast<int64_t>(h.steps);
+    R->instances = h.instances;
+    R->records = h.records;
+    R->mode = L.flags | HGRD_LAUNCH_SEQUENTIAL;
+    if (h.flags & kFlagAbort) {
+      R->aborted = 1;
+      R->abort_stmt = h.abortStmt;
+      break;
+    }
+    rc = detect(c, L, D, o, h.cursor, pairwise, locks, R);
+    if (rc < 0)
+      return rc;
+    break;
+  }
+  CK(cudaEventRecord(c->e1, c->st));
+  CK(cudaEventSynchronize(c->e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  R->device_ms = ms;
+  if (c->profiling) {
+    std::string j = "[";
+    for (size_t i = 0; i < c->stages.size(); ++i) {
+      float sm = 0;
+      cudaEventElapsedTime(&sm, c->stages[i].a, c->stages[i].b);
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "%s{\"name\":\"%s\",\"ms\":%.6f}", i ? "," : "",
+                    c->stages[i].name, sm);
+      j += buf;
+    }
+    c->profileJson = j + "]";
+  }
+  return 0;
+}
+
+} // namespace
+
+extern "C" {
+
+int hgrd_gpu_create(int device, hgrd_gpu_ctx **out) {
+  if (!out)
+    return HGRD_GPU_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) {
+    (void)cudaGetLastError();
+    return HGRD_GPU_ENODEV;
+  }
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10)
+    return HGRD_GPU_ENODEV; // built for sm_100a only
+  auto *c = new hgrd_gpu_ctx();
+  c->device = device;
+  c->nSM = prop.multiProcessorCount;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->e0) != cudaSuccess || cudaEventCreate(&c->e1) != cudaSuccess ||
+      cudaMallocHost(&c->hCtr, sizeof(Counters)) != cudaSuccess) {
+    delete c;
+    return HGRD_GPU_ECUDA;
+  }
+  *out = c;
+  return 0;
+}
+
+void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
+  if (!c)
+    return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  auto f = [](auto &v) {
+    if (v.p)
+      cudaFree(v.p);
+  };
+  f(c->keys), f(c->keysAlt), f(c->elemK), f(c->elemKAlt), f(c->vals), f(c->valsAlt);
+  f(c->order), f(c->orderAlt), f(c->cubTemp), f(c->blob), f(c->snapshot), f(c->keySeg);
+  f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
+  f(c->opSeq), f(c->opStart), f(c->traps);
+  for (char *ch : c->chunks)
+    cudaFree(ch);
+  for (auto &b : c->bigUsed)
+    cudaFree(b.p);
+  for (auto &kv : c->bigFree)
+    cudaFree(kv.second);
+  if (c->hStage)
+    cudaFreeHost(c->hStage);
+  if (c->hCtr)
+    cudaFreeHost(c->hCtr);
+  for (cudaEvent_t e : c->evPool)
+    cudaEventDestroy(e);
+  cudaEventDestroy(c->e0);
+  cudaEventDestroy(c->e1);
+  cudaStreamDestroy(c->st);
+  delete c;
+}
+
+const char *hgrd_gpu_last_error(hgrd_gpu_ctx *c) { return c ? c->err.c_str() : "no context"; }
+
+int hgrd_gpu_set_profiling(hgrd_gpu_ctx *c, int on) {
+  if (!c)
+    return HGRD_GPU_EINVAL;
+  c->profiling = on != 0;
+  return 0;
+}
+
+const char *hgrd_gpu_last_profile(hgrd_gpu_ctx *c) { return c ? c->profileJson.c_str() : "[]"; }
+
+unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *c) { return c ? c->kernelLaunches : 0; }
+
+int hgrd_gpu_buffers_reset(hgrd_gpu_ctx *c) {
+  if (!c)
+    return HGRD_GPU_EINVAL;
+  c->bufs.clear();
+  c->chunkIdx = 0;
+  c->chunkUsed = 0;
+  for (auto &b : c->bigUsed)
+    c->bigFree.emplace(b.bytes, b.p);
+  c->bigUsed.clear();
+  return 0;
+}
+
+int hgrd_gpu_buffer_alloc(hgrd_gpu_ctx *c, int64_t elems, int32_t *handle) {
+  if (!c || !handle || elems <= 0)
+    return HGRD_GPU_EINVAL;
+  CK(cudaSetDevice(c->device));
+  const size_t bytes = (static_cast<size_t>(elems) * 8 + 255) & ~size_t(255);
+  char *p = nullptr;
+  if (bytes <= c->chunkBytes / 4) {
+    while (c->chunkIdx < c->chunks.size() && c->chunkUsed + bytes > c->chunkBytes) {
+      ++c->chunkIdx;
+      c->chunkUsed = 0;
+    }
+    if (c->chunkIdx == c->chunks.size()) {
+      char *ch = nullptr;
+      CK(cudaMalloc(&ch, c->chunkBytes));
+      c->chunks.push_back(ch);
+      c->chunkUsed = 0;
+    }
+    p = c->chunks[c->chunkIdx] + c->chunkUsed;
+    c->chunkUsed += bytes;
+  } else {
+    auto it = c->bigFree.find(bytes);
+    if (it != c->bigFree.end()) {
+      p = static_cast<char *>(it->second);
+      c->bigFree.erase(it);
+    } else {
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        for (auto &kv : c->bigFree)
+          cudaFree(kv.second);
+        c->bigFree.clear();
+        CK(cudaMalloc(&p, bytes));
+      }
+    }
+    c->bigUsed.push_back(BigBlock{p, bytes});
+  }
+  CK(cudaMemsetAsync(p, 0, static_cast<size_t>(elems) * 8, c->st));
+  c->bufs.push_back(hgrd_gpu_ctx::Buf{reinterpret_cast<int64_t *>(p), elems});
+  *handle = static_cast<int32_t>(c->bufs.size() - 1);
+  return 0;
+}
+
+int hgrd_gpu_buffer_write(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n,
+                          const int64_t *src) {
+  if (!c || h < 0 || static_cast<size_t>(h) >= c->bufs.size() || off < 0 || n < 0 ||
+      off + n > c->bufs[static_cast<size_t>(h)].elems || (n && !src))
+    return HGRD_GPU_EINVAL;
+  if (n == 0)
+    return 0;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->bufs[static_cast<size_t>(h)].p + off, src, static_cast<size_t>(n) * 8,
+                     cudaMemcpyHostToDevice, c->st));
+  return 0;
+}
+
+int hgrd_gpu_buffer_read(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n, int64_t *dst) {
+  if (!c || h < 0 || static_cast<size_t>(h) >= c->bufs.size() || off < 0 || n < 0 ||
+      off + n > c->bufs[static_cast<size_t>(h)].elems || (n && !dst))
+    return HGRD_GPU_EINVAL;
+  if (n == 0)
+    return 0;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(dst, c->bufs[static_cast<size_t>(h)].p + off, static_cast<size_t>(n) * 8,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+int hgrd_gpu_check_launch(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
+                          hgrd_gpu_result *result) {
+  if (!c || !launch || !result || (!result->races && result->race_cap) ||
+      (!result->traps && result->trap_cap))
+    return HGRD_GPU_EINVAL;
+  std::string why;
+  if (!validLaunch(*launch, why)) {
+    c->err = why;
+    return HGRD_GPU_EINVAL;
+  }
+  CK(cudaSetDevice(c->device));
+  return checkLaunch(c, *launch, result);
+}
+
+} // extern "C"

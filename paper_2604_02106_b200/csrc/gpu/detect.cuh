@@ -1,0 +1,447 @@
+// K3/K4: conflict detection over key-sorted records.
+//
+// Reference semantics (src/oracle.cpp:745-769): for events a, b on one
+// element from different threads, with at least one write, not both
+// atomics whose scopes cover the pair, and not ordered by a barrier phase
+// or a lock, the pair races with kind INTER-BLOCK (blocks differ),
+// INTRA-BLOCK (same block, warps differ) or INTRA-WARP.
+//
+// Summary detector (no lock idioms).  After sorting by
+//   element | block | blockPhase | warp | warpPhase | lane
+// the three kinds are "two distinct ids inside one group":
+//   INTER : group element,                             id block
+//   INTRA-BLOCK : group (element, block, blockPhase),   id warp
+//   INTRA-WARP  : group (element, block, bp, warp, wp), id lane
+// and the write / atomic-scope rules are static per site pair (conf masks).
+// So a site pair (s1, s2) realises a kind on an element iff the union of
+// their ids in some group has two values: min(min1,min2) < max(max1,max2).
+// One thread per element segment keeps per-site (min, max) at the three
+// levels — O(g·S) instead of the reference's O(g²) pair loop — and
+// publishes, per realised key, the minimum segment start (= minimum
+// (handle, index), the reference's first-found element, :745).
+//
+// Witness (first pair in reference order inside that element): x is the
+// earliest event (thread, seq) that has a later partner; "later" in event
+// order inside a group is exactly "larger id" at that level, so x
+// qualifies iff a partner site's max id in its group exceeds id(x); y is
+// the earliest partner event with a larger id in x's group.
+//
+// Pairwise detector (kernels with fence + CAS/Exch lock idioms, whose
+// lockInfo ordering (:678-728) is not a group property): records in
+// canonical event order, stably sorted by element, brute-force pairs in
+// the reference's x<y order, first pair per key via a packed atomicMin.
+#pragma once
+
+#include "device.cuh"
+
+namespace hgrdgpu {
+namespace dev {
+
+struct DetectArgs {
+  const uint64_t *keys;
+  const uint32_t *vals;
+  uint64_t n;
+  KeyLayout kl;
+  const SiteDev *sites;
+  const uint64_t *confInter, *confIntra, *locMask;
+  int nLocs, nSites;
+  int64_t tpb, ws;
+  // element -> (handle, index) over written buffers
+  const uint64_t *wBase;
+  const int32_t *wHandle;
+  int nW;
+};
+
+__device__ __forceinline__ void siteKey(const DetectArgs &A, int a, int b, int kind,
+                                        uint32_t segStart, uint32_t *keySeg) {
+  int la = A.sites[a].loc, lb = A.sites[b].loc;
+  if (lb < la) {
+    int t = la;
+    la = lb;
+    lb = t;
+  }
+  const int K = (la * A.nLocs + lb) * 3 + kind;
+  if (keySeg[K] > segStart)
+    atomicMin(&keySeg[K], segStart);
+}
+
+__device__ __forceinline__ void flushLevel(const DetectArgs &A, uint64_t pres,
+                                           const uint32_t *mn, const uint32_t *mx,
+                                           const uint64_t *conf, int kind,
+                                           uint32_t segStart, uint32_t *keySeg) {
+  uint64_t rem = pres;
+  while (rem) {
+    const int a = __ffsll(static_cast<long long>(rem)) - 1;
+    rem &= rem - 1;
+    uint64_t m = conf[a] & pres & ~((1ull << a) - 1);
+    while (m) {
+      const int b = __ffsll(static_cast<long long>(m)) - 1;
+      m &= m - 1;
+      const uint32_t lo = min(mn[a], mn[b]);
+      const uint32_t hi = max(mx[a], mx[b]);
+      if (lo < hi)
+        siteKey(A, a, b, kind, segStart, keySeg);
+    }
+  }
+}
+
+__device__ __forceinline__ void note(uint64_t &pres, uint32_t *mn, uint32_t *mx,
+                                     int s, uint32_t id) {
+  const uint64_t bit = 1ull << s;
+  if (!(pres & bit)) {
+    pres |= bit;
+    mn[s] = id;
+    mx[s] = id;
+  } else {
+    mn[s] = min(mn[s], id);
+    mx[s] = max(mx[s], id);
+  }
+}
+
+__global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= A.n)
+    return;
+  const KeyLayout kl = A.kl;
+  const uint64_t k0 = A.keys[i];
+  if (k0 == kl.sentinel)
+    return;
+  const uint64_t elem = k0 >> kl.shE;
+  if (i > 0 && (A.keys[i - 1] >> kl.shE) == elem)
+    return; // not the first record of its element
+  if (i + 1 >= A.n || (A.keys[i + 1] >> kl.shE) != elem)
+    return; // a lone access cannot race
+  const uint64_t mB = fieldMask(kl.bB), mW = fieldMask(kl.bW), mL = fieldMask(kl.bL);
+  uint32_t mn1[kMaxSites], mx1[kMaxSites], mn2[kMaxSites], mx2[kMaxSites],
+      mn3[kMaxSites], mx3[kMaxSites];
+  uint64_t p1 = 0, p2 = 0, p3 = 0;
+  uint64_t g2 = k0 >> kl.shP, g3 = k0 >> kl.shQ;
+  const uint32_t seg = static_cast<uint32_t>(i);
+  for (uint64_t j = i; j < A.n; ++j) {
+    const uint64_t k = A.keys[j];
+    if ((k >> kl.shE) != elem)
+      break;
+    if ((k >> kl.shP) != g2) {
+      flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
+      p2 = 0;
+      g2 = k >> kl.shP;
+    }
+    if ((k >> kl.shQ) != g3) {
+      flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
+      p3 = 0;
+      g3 = k >> kl.shQ;
+    }
+    const int s = static_cast<int>(A.vals[j] >> kSeqBits);
+    note(p1, mn1, mx1, s, static_cast<uint32_t>((k >> kl.shB) & mB));
+    note(p2, mn2, mx2, s, static_cast<uint32_t>((k >> kl.shW) & mW));
+    note(p3, mn3, mx3, s, static_cast<uint32_t>(k & mL));
+  }
+  flushLevel(A, p1, mn1, mx1, A.confInter, 0, seg, keySeg);
+  flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
+  flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
+}
+
+__device__ __forceinline__ void elementOf(const DetectArgs &A, uint64_t elem,
+                                          int32_t &handle, int64_t &index) {
+  int w = 0;
+  for (int q = 1; q < A.nW; ++q)
+    if (A.wBase[q] <= elem)
+      w = q;
+  handle = A.wHandle[w];
+  index = static_cast<int64_t>(elem - A.wBase[w]);
+}
+
+__device__ __forceinline__ uint64_t eventOrder(const DetectArgs &A, uint64_t k, uint32_t v) {
+  const KeyLayout &kl = A.kl;
+  const uint64_t block = (k >> kl.shB) & fieldMask(kl.bB);
+  const uint64_t warp = (k >> kl.shW) & fieldMask(kl.bW);
+  const uint64_t lane = k & fieldMask(kl.bL);
+  const uint64_t thread = block * static_cast<uint64_t>(A.tpb) +
+                          warp * static_cast<uint64_t>(A.ws) + lane;
+  return (thread << kSeqBits) | (v & kSeqMask);
+}
+
+__device__ __forceinline__ uint32_t levelId(const KeyLayout &kl, int kind, uint64_t k) {
+  if (kind == 0)
+    return static_cast<uint32_t>((k >> kl.shB) & fieldMask(kl.bB));
+  if (kind == 1)
+    return static_cast<uint32_t>((k >> kl.shW) & fieldMask(kl.bW));
+  return static_cast<uint32_t>(k & fieldMask(kl.bL));
+}
+
+// One thread per race key; realised keys extract their witness pair.
+__global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
+                          hgrd_gpu_race *races, Counters *ctr) {
+  const int K = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K >= nKeys)
+    return;
+  const uint32_t s = keySeg[K];
+  if (s == 0xffffffffu)
+    return;
+  const KeyLayout kl = A.kl;
+  const int kind = K % 3;
+  const int la = (K / 3) / A.nLocs, lb = (K / 3) % A.nLocs;
+  const uint64_t *conf = kind == 0 ? A.confInter : A.confIntra;
+  const int gsh = kind == 0 ? kl.shE : kind == 1 ? kl.shP : kl.shQ;
+  const uint64_t elem = A.keys[s] >> kl.shE;
+  uint64_t e = s;
+  while (e < A.n && (A.keys[e] >> kl.shE) == elem)
+    ++e;
+  uint32_t mx[kMaxSites];
+  uint64_t best = ~0ull, bestPm = 0;
+  uint64_t bestI = s, bestG0 = s, bestG1 = e;
+  for (uint64_t j = s; j < e;) {
+    const uint64_t g = A.keys[j] >> gsh;
+    uint64_t ge = j;
+    uint64_t pres = 0;
+    for (; ge < e && (A.keys[ge] >> gsh) == g; ++ge) {
+      const int st = static_cast<int>(A.vals[ge] >> kSeqBits);
+      const uint32_t id = levelId(kl, kind, A.keys[ge]);
+      const uint64_t bit = 1ull << st;
+      if (!(pres & bit)) {
+        pres |= bit;
+        mx[st] = id;
+      } else if (id > mx[st]) {
+        mx[st] = id;
+      }
+    }
+    for (uint64_t x = j; x < ge; ++x) {
+      const int st = static_cast<int>(A.vals[x] >> kSeqBits);
+      const int loc = A.sites[st].loc;
+      if (loc != la && loc != lb)
+        continue;
+      const int ploc = loc == la ? lb : la;
+      const uint64_t pm = conf[st] & A.locMask[ploc] & pres;
+      const uint32_t id = levelId(kl, kind, A.keys[x]);
+      bool later = false;
+      for (uint64_t m = pm; m && !later; m &= m - 1)
+        later = mx[__ffsll(static_cast<long long>(m)) - 1] > id;
+      if (!later)
+        continue;
+      const uint64_t ord = eventOrder(A, A.keys[x], A.vals[x]);
+      if (ord < best) {
+        best = ord;
+        bestI = x;
+        bestPm = pm;
+        bestG0 = j;
+        bestG1 = ge;
+      }
+    }
+    j = ge;
+  }
+  if (best == ~0ull)
+    return; // cannot happen for a realised key
+  const uint32_t idx = levelId(kl, kind, A.keys[bestI]);
+  uint64_t bestY = ~0ull, yI = bestI;
+  for (uint64_t y = bestG0; y < bestG1; ++y) {
+    const int st = static_cast<int>(A.vals[y] >> kSeqBits);
+    if (!((bestPm >> st) & 1ull) || levelId(kl, kind, A.keys[y]) <= idx)
+      continue;
+    const uint64_t ord = eventOrder(A, A.keys[y], A.vals[y]);
+    if (ord < bestY) {
+      bestY = ord;
+      yI = y;
+    }
+  }
+  const unsigned pos = atomicAdd(&ctr->nRaces, 1u);
+  hgrd_gpu_race &o = races[pos];
+  o.loc_a = la;
+  o.loc_b = lb;
+  o.kind = kind;
+  o.site_x = static_cast<int32_t>(A.vals[bestI] >> kSeqBits);
+  o.site_y = static_cast<int32_t>(A.vals[yI] >> kSeqBits);
+  elementOf(A, elem, o.handle, o.index);
+  o.thread_x = static_cast<int64_t>(best >> kSeqBits);
+  o.seq_x = static_cast<int32_t>(best & kSeqMask);
+  o.thread_y = static_cast<int64_t>(bestY >> kSeqBits);
+  o.seq_y = static_cast<int32_t>(bestY & kSeqMask);
+}
+
+// ---------------------------------------------------------------------------
+// Pairwise path (lock idioms).  Records are in canonical event order;
+// order[] is the stable sort of record indices by element.
+
+struct LockSet {
+  int n;
+  int32_t h[8];
+  int64_t idx[8];
+  int32_t scope[8];
+};
+
+__device__ __forceinline__ void lockInsert(LockSet &s, int32_t h, int64_t idx, int32_t sc,
+                                           unsigned &flags) {
+  for (int i = 0; i < s.n; ++i)
+    if (s.h[i] == h && s.idx[i] == idx) {
+      if (sc > s.scope[i])
+        s.scope[i] = sc;
+      return;
+    }
+  if (s.n < 8) {
+    s.h[s.n] = h;
+    s.idx[s.n] = idx;
+    s.scope[s.n] = sc;
+    ++s.n;
+  } else {
+    flags |= kFlagLockSet;
+  }
+}
+
+struct LockInfo {
+  LockSet acq, rel, cs;
+};
+
+// reference lockInfo, src/oracle.cpp:678-704
+__device__ void lockInfoOf(const LaunchDev &L, uint64_t thread, int32_t seq,
+                           LockInfo &li, unsigned &flags) {
+  li.acq.n = li.rel.n = li.cs.n = 0;
+  const uint64_t b = L.opStart[thread], e = L.opStart[thread + 1];
+  for (uint64_t f = b; f < e; ++f) {
+    const int32_t mf = L.opMeta[f];
+    if ((mf & 15) != 2)
+      continue;
+    const int32_t fs = L.opSeq[f], fsc = (mf >> 4) & 15;
+    for (uint64_t c = b; c < e; ++c) {
+      const int32_t mc = L.opMeta[c];
+      if ((mc & 15) != 0 || L.opSeq[c] >= fs)
+        continue;
+      if (fs < seq)
+        lockInsert(li.acq, (mc >> 8) - 1, L.opIndex[c], min((mc >> 4) & 15, fsc), flags);
+    }
+    for (uint64_t x = b; x < e; ++x) {
+      const int32_t mx = L.opMeta[x];
+      if ((mx & 15) != 1 || L.opSeq[x] <= fs)
+        continue;
+      if (fs > seq)
+        lockInsert(li.rel, (mx >> 8) - 1, L.opIndex[x], min((mx >> 4) & 15, fsc), flags);
+    }
+  }
+  for (int i = 0; i < li.acq.n; ++i)
+    for (int j = 0; j < li.rel.n; ++j)
+      if (li.acq.h[i] == li.rel.h[j] && li.acq.idx[i] == li.rel.idx[j])
+        lockInsert(li.cs, li.acq.h[i], li.acq.idx[i], min(li.acq.scope[i], li.rel.scope[j]),
+                   flags);
+}
+
+__device__ __forceinline__ bool covers(int32_t s, bool sameBlock) {
+  return s == HGRD_SCOPE_DEVICE || (s == HGRD_SCOPE_BLOCK && sameBlock);
+}
+__device__ __forceinline__ bool crossed(const LockSet &x, const LockSet &y, bool sameBlock) {
+  for (int i = 0; i < x.n; ++i)
+    for (int j = 0; j < y.n; ++j)
+      if (x.h[i] == y.h[j] && x.idx[i] == y.idx[j] && covers(min(x.scope[i], y.scope[j]), sameBlock))
+        return true;
+  return false;
+}
+
+struct Ev {
+  uint64_t block, warp, lane, bp, wp, thread;
+  int site, seq;
+};
+
+__device__ __forceinline__ Ev decodeEv(const DetectArgs &A, uint64_t k, uint32_t v) {
+  const KeyLayout &kl = A.kl;
+  Ev e;
+  e.block = (k >> kl.shB) & fieldMask(kl.bB);
+  e.bp = (k >> kl.shP) & fieldMask(kl.bP);
+  e.warp = (k >> kl.shW) & fieldMask(kl.bW);
+  e.wp = (k >> kl.shQ) & fieldMask(kl.bQ);
+  e.lane = k & fieldMask(kl.bL);
+  e.thread = e.block * static_cast<uint64_t>(A.tpb) + e.warp * static_cast<uint64_t>(A.ws) + e.lane;
+  e.site = static_cast<int>(v >> kSeqBits);
+  e.seq = static_cast<int>(v & kSeqMask);
+  return e;
+}
+
+__global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
+                                  const uint32_t *order, bool locks,
+                                  unsigned long long *keyPair) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= A.n)
+    return;
+  const uint64_t elem = elemSorted[i];
+  if (i > 0 && elemSorted[i - 1] == elem)
+    return;
+  uint64_t e = i + 1;
+  while (e < A.n && elemSorted[e] == elem)
+    ++e;
+  unsigned flags = 0;
+  if (e - i > 65535) {
+    atomicOr(&L.ctr->flags, static_cast<unsigned>(kFlagSegment));
+    return;
+  }
+  LockInfo la, lb;
+  for (uint64_t x = i; x < e; ++x) {
+    const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
+    const SiteDev sa = A.sites[a.site];
+    if (locks)
+      lockInfoOf(L, a.thread, a.seq, la, flags);
+    for (uint64_t y = x + 1; y < e; ++y) {
+      const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
+      if (a.thread == b.thread)
+        continue;
+      const SiteDev sb = A.sites[b.site];
+      if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
+        continue;
+      const bool sameBlock = a.block == b.block;
+      if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC &&
+          covers(sa.scope, sameBlock) && covers(sb.scope, sameBlock))
+        continue;
+      if (sameBlock && a.bp != b.bp)
+        continue;
+      const bool sameWarp = sameBlock && a.warp == b.warp;
+      if (sameWarp && a.wp != b.wp)
+        continue;
+      if (locks) {
+        lockInfoOf(L, b.thread, b.seq, lb, flags);
+        if (crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
+            crossed(lb.rel, la.acq, sameBlock))
+          continue;
+      }
+      const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
+      int l0 = sa.loc, l1 = sb.loc;
+      if (l1 < l0) {
+        int t = l0;
+        l0 = l1;
+        l1 = t;
+      }
+      const int K = (l0 * A.nLocs + l1) * 3 + kind;
+      const unsigned long long packed =
+          (static_cast<unsigned long long>(i) << 32) | ((x - i) << 16) | (y - i);
+      if (keyPair[K] > packed)
+        atomicMin(&keyPair[K], packed);
+    }
+  }
+  if (flags)
+    atomicOr(&L.ctr->flags, flags);
+}
+
+__global__ void k_decode_pairwise(DetectArgs A, const uint64_t *elemSorted,
+                                  const uint32_t *order,
+                                  const unsigned long long *keyPair, int nKeys,
+                                  hgrd_gpu_race *races, Counters *ctr) {
+  const int K = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K >= nKeys)
+    return;
+  const unsigned long long p = keyPair[K];
+  if (p == ~0ull)
+    return;
+  const uint64_t s = p >> 32;
+  const uint64_t x = s + ((p >> 16) & 0xffff), y = s + (p & 0xffff);
+  const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
+  const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
+  const unsigned pos = atomicAdd(&ctr->nRaces, 1u);
+  hgrd_gpu_race &o = races[pos];
+  o.kind = K % 3;
+  o.loc_a = (K / 3) / A.nLocs;
+  o.loc_b = (K / 3) % A.nLocs;
+  o.site_x = a.site;
+  o.site_y = b.site;
+  elementOf(A, elemSorted[s], o.handle, o.index);
+  o.thread_x = static_cast<int64_t>(a.thread);
+  o.thread_y = static_cast<int64_t>(b.thread);
+  o.seq_x = a.seq;
+  o.seq_y = b.seq;
+}
+
+} // namespace dev
+} // namespace hgrdgpu

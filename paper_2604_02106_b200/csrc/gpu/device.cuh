@@ -1,0 +1,161 @@
+// Device-side data layout of the race-check stage (sm_100a).
+//
+// HBM layout per launch (all device-resident, owned by hgrd_gpu_ctx):
+//   buffers      int64[elems] per allocation (reference buffers_, :789)
+//   blob         code | sites | params | reg_init | conflict masks  (one H2D)
+//   keys/vals    packed access records: u64 key + u32 (site,seq)
+//   keySeg       u32 per race key (locA, locB, kind): first segment start
+//   races        hgrd_gpu_race[] output
+//
+// Packed record key (high -> low bits), widths chosen per launch:
+//   element | block | blockPhase | warp | warpPhase | lane
+// element = flat index over the buffers the launch writes (handle order,
+// so element order == reference (handle, index) order).  Sorting by the
+// key makes the reference's element groups contiguous (:733-735) and,
+// inside them, the (block, blockPhase) and (block, blockPhase, warp,
+// warpPhase) groups on which the pair rule (:750-769) reduces to
+// "two distinct ids at the right level" — see detect.cuh.
+#pragma once
+
+#include "hgrd_gpu.h"
+
+#include <cstdint>
+
+namespace hgrdgpu {
+namespace dev {
+
+constexpr int kMaxRegs = 64;    // PARALLEL per-lane register file
+constexpr int kMaxSites = 64;   // summary detector site masks (u64)
+constexpr int kLaneBuf = 16;    // records buffered per lane per batch
+constexpr uint32_t kChunk = 4096; // records reserved per warp refill
+constexpr int kSeqBits = 20;    // val = site << 20 | seq
+constexpr uint32_t kSeqMask = (1u << kSeqBits) - 1;
+constexpr int kMaxSiteId = 4095;
+
+enum CounterFlags : uint32_t {
+  kFlagCapacity = 1u,   // record buffer too small
+  kFlagPhase = 2u,      // a phase counter exceeded its key field
+  kFlagSeqSite = 4u,    // seq >= 2^20
+  kFlagAbort = 8u,      // step budget exhausted
+  kFlagLockSet = 16u,   // lock-set scratch overflow (pairwise)
+  kFlagSegment = 32u,   // pairwise segment longer than 65535
+  kFlagOps = 64u        // sync-op buffer too small
+};
+
+struct ParamDev {
+  int64_t *ptr;      // device buffer base (nullptr: scalar / unallocated)
+  int64_t size;      // elements
+  int32_t handle;    // -1 when unbound
+  int32_t written;   // the launch stores/atomically updates this buffer
+  uint64_t elemBase; // flat element base (written buffers only)
+};
+
+struct SiteDev {
+  int32_t param;
+  int32_t loc;
+  uint8_t kind, aop, scope, record; // record: access lands in a written buffer
+  int32_t valueNeeded;
+};
+
+struct KeyLayout {
+  int bL, bQ, bW, bP, bB, bE;
+  int shQ, shW, shP, shB, shE;
+  int total;
+  uint64_t sentinel; // all-ones in `total` bits: never a valid key
+};
+
+struct Counters {
+  unsigned long long steps;
+  unsigned long long instances;
+  unsigned long long records;   // real records written (no sentinels)
+  unsigned long long traps;
+  unsigned long long cursor;    // record slots handed out (incl. padding)
+  unsigned long long nOps;
+  unsigned int maxBp, maxWp;
+  unsigned int flags;
+  int abortStmt;
+  unsigned int nRaces;
+  unsigned int pad;
+};
+
+struct LaunchDev {
+  const hgrd_gpu_insn *code;
+  const SiteDev *sites;
+  const ParamDev *params;
+  const int64_t *regInit;
+  const uint64_t *confInter; // per site: sites it can race with across blocks
+  const uint64_t *confIntra; // ... within a block
+  const uint64_t *locMask;   // per loc id: sites at that loc
+  int nCode, nRegs, nSites, nParams, nLocs;
+  int64_t grid[3], block[3];
+  int64_t ws, tpb, nThreads, nBlocks;
+  int64_t stepBudget;
+  KeyLayout kl;
+  uint64_t *keys;
+  uint32_t *vals;
+  uint64_t capacity;
+  uint32_t chunk;             // records reserved per warp refill
+  Counters *ctr;
+  // SEQUENTIAL extras
+  int64_t *seqRegs;          // nRegs scratch
+  hgrd_gpu_trap *traps;      // first trapCap traps
+  uint32_t trapCap;
+  // lock idioms (pairwise): per-thread sync ops
+  int64_t *opIndex;          // per op: element index
+  int32_t *opMeta;           // per op: kind | scope << 4 | handle << 8
+  int32_t *opSeq;
+  uint64_t opCap;
+  uint64_t *opStart;         // nThreads + 1
+};
+
+__host__ __device__ inline int64_t wrapAdd(int64_t a, int64_t b) {
+  return static_cast<int64_t>(static_cast<uint64_t>(a) + static_cast<uint64_t>(b));
+}
+
+// reference applyBinOp, src/oracle.cpp:179-209, over wrapping int64
+__device__ __forceinline__ int64_t applyBin(int op, int64_t l, int64_t r) {
+  switch (op) {
+  case HGRD_ADD:
+    return wrapAdd(l, r);
+  case HGRD_SUB:
+    return static_cast<int64_t>(static_cast<uint64_t>(l) - static_cast<uint64_t>(r));
+  case HGRD_MUL:
+    return static_cast<int64_t>(static_cast<uint64_t>(l) * static_cast<uint64_t>(r));
+  case HGRD_DIV:
+    return r == 0 ? 0 : (r == -1 ? -l : l / r);
+  case HGRD_MOD:
+    return (r == 0 || r == -1) ? 0 : l % r;
+  case HGRD_LT:
+    return l < r;
+  case HGRD_LE:
+    return l <= r;
+  case HGRD_GT:
+    return l > r;
+  case HGRD_GE:
+    return l >= r;
+  case HGRD_EQ:
+    return l == r;
+  case HGRD_NE:
+    return l != r;
+  case HGRD_AND:
+    return (l != 0 && r != 0) ? 1 : 0;
+  case HGRD_OR:
+    return (l != 0 || r != 0) ? 1 : 0;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ uint64_t packKey(const KeyLayout &k, uint64_t elem,
+                                            uint64_t block, uint64_t bp,
+                                            uint64_t warp, uint64_t wp,
+                                            uint64_t lane) {
+  return (elem << k.shE) | (block << k.shB) | (bp << k.shP) | (warp << k.shW) |
+         (wp << k.shQ) | lane;
+}
+
+__device__ __forceinline__ uint64_t fieldMask(int bits) {
+  return bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+}
+
+} // namespace dev
+} // namespace hgrdgpu

@@ -1,0 +1,174 @@
+"""GPU parity: the B200 race-check stage (libhgrd_gpu.so, through its C ABI)
+against the reference's recorded outputs (tests/golden, generated from the
+unmodified reference) on every field the reference reports, and against the
+CPU restatement (oracle/) on the witness pairs the reference does not
+report.  Bit-exact: integer / index work, no tolerance."""
+import numpy as np
+import pytest
+
+import paper_2604_02106_b200 as hg
+import programs
+from conftest import load_golden
+from oracles import strip_extras
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_run(gpu, cpu_oracle, src, cfg, file_name, want):
+    got = gpu.run_concrete(src, cfg, file_name)
+    assert strip_extras(got) == want, (cfg, got, want)
+    ora = cpu_oracle.run_concrete(src, cfg, file_name)
+    assert got["witnesses"] == ora["witnesses"], (cfg, got["witnesses"], ora["witnesses"])
+    assert got["stats"]["instances"] == ora["stats"]["instances"]
+    return got
+
+
+def test_corpus_runs(gpu, cpu_oracle):
+    for e in load_golden("corpus"):
+        for run in e["runs"]:
+            _check_run(gpu, cpu_oracle, e["source"], run["config"], e["file"], run["result"])
+
+
+def test_corpus_sweeps(gpu):
+    """Acceptance criterion 4 / corpus.cpp:203-237 on the GPU."""
+    for e in load_golden("corpus"):
+        got = strip_extras(gpu.enumerate_verdict(e["source"], e["caps"], e["file"]))
+        assert got == e["sweep_manifest"], e["name"]
+        got = strip_extras(gpu.enumerate_verdict(e["source"], {}, e["file"]))
+        assert got == e["sweep_default"], e["name"]
+
+
+def test_unit_cases(gpu, cpu_oracle):
+    for c in load_golden("unit_cases"):
+        _check_run(gpu, cpu_oracle, c["source"], c["config"], "oracle.mcu", c["result"])
+
+
+def test_fuzz(gpu, cpu_oracle):
+    """reference tests/test_soundness.cpp programs (mt19937(31337))."""
+    total = 0
+    for f in load_golden("fuzz"):
+        got = strip_extras(gpu.enumerate_verdict(f["source"], {}, "fuzz.mcu"))
+        assert got == f["sweep"], f["index"]
+        total += len(got["races"])
+        for run in f["runs"]:
+            _check_run(gpu, cpu_oracle, f["source"], run["config"], "fuzz.mcu", run["result"])
+    assert total > 500
+
+
+def test_edge_programs(gpu, cpu_oracle):
+    for c in load_golden("edge"):
+        _check_run(gpu, cpu_oracle, c["source"], c["config"], "edge.mcu", c["result"])
+
+
+def test_synthetic_small(gpu, cpu_oracle):
+    for c in load_golden("synthetic"):
+        got = _check_run(gpu, cpu_oracle, c["source"], c["config"], "syn.mcu", c["result"])
+        assert got["stats"]["parallelLaunches"] >= 1  # the data-parallel path ran
+
+
+# --------------------------------------------------------------- launch level
+def _spec_stencil(ctx, n, barrier, ws=32):
+    src = programs.stencil(n, barrier=barrier)
+    low = hg.lower(src, "st")
+    bufs = [np.zeros(n, np.int64), np.zeros(n // 256 * 258, np.int64), np.zeros(n, np.int64)]
+    handles = {}
+    if ctx is not None:
+        ctx.reset()
+        handles = {"in_": ctx.alloc(n), "tile": ctx.alloc(n // 256 * 258), "out_": ctx.alloc(n)}
+    else:
+        handles = {"in_": 0, "tile": 1, "out_": 2}
+    spec = hg.LaunchSpec(low, (n // 256, 1, 1), (256, 1, 1), ws, handles=handles)
+    return spec, bufs
+
+
+def _spec_hist(ctx, n, bins, update, ws=32):
+    src = programs.histogram(n, bins, update, host_init=False)
+    low = hg.lower(src, "h")
+    data = programs.histogram_data(n, bins)
+    bufs = [data, np.zeros(bins, np.int64)]
+    if ctx is not None:
+        ctx.reset()
+        h = {"data": ctx.alloc(n), "hist": ctx.alloc(bins)}
+        ctx.write(h["data"], data)
+    else:
+        h = {"data": 0, "hist": 1}
+    return hg.LaunchSpec(low, (n // 256, 1, 1), (256, 1, 1), ws, handles=h), bufs
+
+
+def _spec_transpose(ctx, n, barrier):
+    src = programs.transpose(n, barrier=barrier)
+    low = hg.lower(src, "tr")
+    ntile = (n // 32) * (n // 32) * 1056
+    bufs = [np.zeros(ntile, np.int64), np.zeros(n * n, np.int64)]
+    if ctx is not None:
+        ctx.reset()
+        h = {"tile": ctx.alloc(ntile), "out_": ctx.alloc(n * n)}
+    else:
+        h = {"tile": 0, "out_": 1}
+    return hg.LaunchSpec(low, (n // 32, n // 32, 1), (32, 32, 1), 32,
+                         scalars={"n": n}, handles=h), bufs
+
+
+def _same(a, b):
+    keys = ("races", "traps", "steps", "instances", "records", "aborted")
+    return {k: a[k] for k in keys} == {k: b[k] for k in keys}
+
+
+@pytest.mark.parametrize("barrier", [False, True])
+@pytest.mark.parametrize("ws", [32, 5])
+def test_launch_stencil(gpu, cpu_oracle, barrier, ws):
+    spec, bufs = _spec_stencil(gpu, 1 << 14, barrier, ws)
+    got = gpu.check_launch(spec)
+    ref_spec, _ = _spec_stencil(None, 1 << 14, barrier, ws)
+    want = cpu_oracle.check_launch(ref_spec, bufs)
+    assert _same(got, want), (got, want)
+    spec.launch.flags |= hg.LAUNCH_SEQUENTIAL  # ordered path must agree too
+    assert _same(gpu.check_launch(spec), want)
+
+
+@pytest.mark.parametrize("update", list(programs.HIST_UPDATES))
+@pytest.mark.parametrize("bins", [64, 1 << 10, 61])
+def test_launch_histogram(gpu, cpu_oracle, update, bins):
+    n = 1 << 13
+    spec, bufs = _spec_hist(gpu, n, bins, update)
+    got = gpu.check_launch(spec)
+    ref_spec, _ = _spec_hist(None, n, bins, update)
+    want = cpu_oracle.check_launch(ref_spec, bufs)
+    assert _same(got, want), (got, want)
+
+
+@pytest.mark.parametrize("barrier", [False, True])
+def test_launch_transpose(gpu, cpu_oracle, barrier):
+    spec, bufs = _spec_transpose(gpu, 128, barrier)
+    got = gpu.check_launch(spec)
+    ref_spec, _ = _spec_transpose(None, 128, barrier)
+    want = cpu_oracle.check_launch(ref_spec, bufs)
+    assert _same(got, want), (got, want)
+
+
+# ------------------------------------------------ full size, size-independent
+def test_full_stencil_2p20(gpu, cpu_oracle):
+    """configs[1]: 2^20 threads.  The first-found element of every key lies in
+    block 0, so the full-size report equals the 2^14 oracle report."""
+    for barrier in (False, True):
+        spec, _ = _spec_stencil(gpu, 1 << 20, barrier)
+        got = gpu.check_launch(spec)
+        small, bufs = _spec_stencil(None, 1 << 14, barrier)
+        want = cpu_oracle.check_launch(small, bufs)
+        assert got["races"] == want["races"]
+        assert got["instances"] == 5 << 20
+        assert got["records"] == 4 << 20
+
+
+def test_full_transpose_8192(gpu, cpu_oracle):
+    """configs[2]: 8192^2, 2^26 instances per interval."""
+    for barrier in (False, True):
+        spec, _ = _spec_transpose(gpu, 8192, barrier)
+        got = gpu.check_launch(spec)
+        small, bufs = _spec_transpose(None, 128, barrier)
+        want = cpu_oracle.check_launch(small, bufs)
+        assert [(r["kind"], r["locA"], r["locB"], r["address"], r["threadA"], r["seqA"],
+                 r["threadB"], r["seqB"]) for r in got["races"]] == \
+               [(r["kind"], r["locA"], r["locB"], r["address"], r["threadA"], r["seqA"],
+                 r["threadB"], r["seqB"]) for r in want["races"]]
+        assert got["instances"] == 3 << 26

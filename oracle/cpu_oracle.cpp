@@ -199,18 +199,21 @@ public:
     for (uint32_t s = 0; s < L.n_sites; ++s)
       if (L.sites[s].kind != HGRD_SITE_LOAD && handleOf(static_cast<int>(s)) >= 0)
         written_.insert(handleOf(static_cast<int>(s)));
+    bool aborted = false;
     try {
       expand();
     } catch (const AbortRun &) {
-      R.aborted = 1;
-      R.steps = steps_;
-      return 0; // the in-flight launch contributes no races (:71-76)
+      aborted = true;
     }
     R.steps = steps_;
-    R.instances = events_.size();
+    R.instances = events_.size(); // executed up to the end or the abort
     for (const auto &e : events_)
       if (written_.count(e.handle))
         ++R.records;
+    if (aborted) {
+      R.aborted = 1;
+      return 0; // the in-flight launch contributes no races (:71-76)
+    }
     return detectRaces();
   }
 

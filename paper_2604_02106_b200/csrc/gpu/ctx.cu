@@ -328,6 +328,7 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
 
 struct BlobOffsets {
   size_t code, sites, params, regs, cInter, cIntra, locMask, wBase, wHandle, total;
+  int nW;
 };
 
 int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOffsets &o) {
@@ -347,6 +348,7 @@ int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOff
   o.wBase = put(8 * P.wBase.size());
   o.wHandle = put(4 * P.wHandle.size());
   o.total = off;
+  o.nW = static_cast<int>(P.wBase.size());
   int rc = stage(c, o.total);
   if (rc < 0)
     return rc;
@@ -393,7 +395,7 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
   A.ws = D.ws;
   A.wBase = reinterpret_cast<const uint64_t *>(c->blob.p + o.wBase);
   A.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
-  A.nW = static_cast<int>((o.wHandle - o.wBase) / 8 > 0 ? (o.wHandle - o.wBase) / 8 : 1);
+  A.nW = o.nW;
   if (n > 1) {
     if (!pairwise) {
       NEED(c->keysAlt, n);

@@ -207,6 +207,10 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
                                     const char *file_name,
                                     const char *caps_json, char **out);
 int hgrd_gpu_count_inputs(const char *source, const char *file_name);
+/* Lowering only: bytecode, sites, locs and per-kernel facts of one kernel as
+ * JSON (for callers that fix launch parameters themselves). */
+int hgrd_gpu_lower_json(const char *source, const char *file_name,
+                        const char *kernel, char **out);
 void hgrd_gpu_free(char *p);
 
 #ifdef __cplusplus

@@ -44,7 +44,7 @@ def test_lowering_right_operand_first():
            "  k<<<1,4>>>(A, B); }\n")
     low = hg.lower(src, "k")
     loads = [s for s in low["sites"] if s["kind"] == 0]
-    assert [(s["line"], s["column"]) for s in loads] == [(3, 19), (3, 10)]
+    assert [(s["line"], s["column"]) for s in loads] == [(3, 17), (3, 10)]
     assert low["locs"] == sorted(low["locs"])
 
 

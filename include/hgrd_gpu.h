@@ -106,6 +106,7 @@ typedef struct hgrd_gpu_site {
                                      (always used when the kernel holds
                                      fence + CAS/Exch lock idioms) */
 #define HGRD_LAUNCH_NO_WITNESS 4u /* skip first-pair witness extraction */
+#define HGRD_LAUNCH_GENERAL 8u    /* bypass the fused block-local check (testing) */
 
 typedef struct hgrd_gpu_launch {
   const hgrd_gpu_insn *code;
@@ -188,6 +189,8 @@ int hgrd_gpu_check_launch(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
 int hgrd_gpu_set_profiling(hgrd_gpu_ctx *ctx, int on);
 /* JSON [{"name":..., "ms":...}] of the last check's stages (ctx-owned). */
 const char *hgrd_gpu_last_profile(hgrd_gpu_ctx *ctx);
+/* Enable (default) / disable the fused block-local check for PARALLEL launches. */
+int hgrd_gpu_set_fused(hgrd_gpu_ctx *ctx, int enabled);
 /* Number of this library's own kernels launched by the context so far. */
 unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *ctx);
 

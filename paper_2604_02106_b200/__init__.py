@@ -31,6 +31,7 @@ c_int32, c_int64, c_uint8, c_uint16, c_uint32, c_uint64 = (
 LAUNCH_SEQUENTIAL = 1
 LAUNCH_PAIRWISE = 2
 LAUNCH_NO_WITNESS = 4
+LAUNCH_GENERAL = 8
 RACE_KINDS = ("INTER-BLOCK", "INTRA-BLOCK", "INTRA-WARP")
 
 
@@ -148,6 +149,7 @@ def load_library() -> ctypes.CDLL:
     lib.hgrd_gpu_set_profiling.argtypes = [P, ctypes.c_int]
     lib.hgrd_gpu_last_profile.argtypes = [P]
     lib.hgrd_gpu_last_profile.restype = ctypes.c_char_p
+    lib.hgrd_gpu_set_fused.argtypes = [P, ctypes.c_int]
     lib.hgrd_gpu_kernel_launches.argtypes = [P]
     lib.hgrd_gpu_kernel_launches.restype = ctypes.c_ulonglong
     _lib = lib
@@ -302,6 +304,10 @@ class GpuContext:
         """[{name, ms}] per pipeline stage of the last check (CUDA events)."""
         return json.loads(self._lib.hgrd_gpu_last_profile(self._ctx).decode() or "[]")
 
+    def set_fused(self, on: bool = True):
+        """Enable (default) / disable the fused block-local check."""
+        self._lib.hgrd_gpu_set_fused(self._ctx, 1 if on else 0)
+
     def kernel_launches(self) -> int:
         return int(self._lib.hgrd_gpu_kernel_launches(self._ctx))
 
@@ -343,4 +349,4 @@ class GpuContext:
 
 __all__ = ["ExecConfig", "SweepCaps", "GpuContext", "LaunchSpec", "count_inputs", "lower",
            "load_library", "LIBRARY_PATH", "RACE_KINDS", "LAUNCH_SEQUENTIAL",
-           "LAUNCH_PAIRWISE", "LAUNCH_NO_WITNESS"]
+           "LAUNCH_PAIRWISE", "LAUNCH_NO_WITNESS", "LAUNCH_GENERAL"]

@@ -8,6 +8,7 @@
 #include "detect.cuh"
 #include "device.cuh"
 #include "expand.cuh"
+#include "fused.cuh"
 
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -82,6 +83,12 @@ struct hgrd_gpu_ctx {
   DevVec<int32_t> opMeta, opSeq;
   DevVec<uint64_t> opStart;
   DevVec<hgrd_gpu_trap> traps;
+  DevVec<uint32_t> owner;              // fused path: per-element ownership
+  uint32_t epoch = 0;
+  DevVec<unsigned long long> keyElem;  // fused path: per key minimum element
+  DevVec<Candidate> cand;
+  DevVec<Counters> ctr2;               // fused pass 2 counters
+  bool fusedEnabled = true;
 
   unsigned char *hStage = nullptr;
   size_t hStageCap = 0;
@@ -266,8 +273,10 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
     if (L.sites[s].kind != HGRD_SITE_LOAD && handleOfParam(L.sites[s].param) >= 0)
       written[static_cast<size_t>(handleOfParam(L.sites[s].param))] = 1;
   std::vector<uint64_t> base(c->bufs.size(), 0);
+  std::vector<int> windex(c->bufs.size(), 0);
   for (size_t h = 0; h < c->bufs.size(); ++h)
     if (written[h]) {
+      windex[h] = static_cast<int>(P.wBase.size()) + 1;
       base[h] = P.totalW;
       P.wBase.push_back(P.totalW);
       P.wHandle.push_back(static_cast<int32_t>(h));
@@ -285,7 +294,7 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
     if (h >= 0) {
       d.ptr = c->bufs[static_cast<size_t>(h)].p;
       d.size = c->bufs[static_cast<size_t>(h)].elems;
-      d.written = written[static_cast<size_t>(h)];
+      d.written = windex[static_cast<size_t>(h)];
       d.elemBase = base[static_cast<size_t>(h)];
     }
     P.params[p] = d;
@@ -376,12 +385,10 @@ int readCounters(hgrd_gpu_ctx *c) {
 }
 
 // Sort + detect + witness over `n` records in c->keys/c->vals (layout kl).
-int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOffsets &o,
-           uint64_t n, bool pairwise, bool locks, hgrd_gpu_result *R) {
-  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
-  const int nKeys = 3 * nLocs * nLocs;
-  NEED(c->races, static_cast<size_t>(nKeys));
-  CK(cudaMemsetAsync(&c->ctr.p->nRaces, 0, sizeof(unsigned), c->st));
+int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R);
+
+DetectArgs detectArgs(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const LaunchDev &D,
+                      const BlobOffsets &o, uint64_t n, int kindMask) {
   DetectArgs A{};
   A.n = n;
   A.kl = D.kl;
@@ -389,13 +396,29 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
   A.confInter = D.confInter;
   A.confIntra = D.confIntra;
   A.locMask = D.locMask;
-  A.nLocs = nLocs;
+  A.nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   A.nSites = static_cast<int>(L.n_sites);
   A.tpb = D.tpb;
   A.ws = D.ws;
   A.wBase = reinterpret_cast<const uint64_t *>(c->blob.p + o.wBase);
   A.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
   A.nW = o.nW;
+  A.kindMask = kindMask;
+  return A;
+}
+
+int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOffsets &o,
+           uint64_t n, bool pairwise, bool locks, hgrd_gpu_result *R, int kindMask = 7,
+           bool append = false) {
+  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+  const int nKeys = 3 * nLocs * nLocs;
+  NEED(c->races, static_cast<size_t>(nKeys));
+  if (!append)
+    CK(cudaMemsetAsync(&c->ctr.p->nRaces, 0, sizeof(unsigned), c->st));
+  DetectArgs A = detectArgs(c, L, D, o, n, kindMask);
+  (void)A;
+  {
+  }
   if (n > 1) {
     if (!pairwise) {
       NEED(c->keysAlt, n);
@@ -464,6 +487,10 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
   int rc = readCounters(c);
   if (rc < 0)
     return rc;
+  return fetchRaces(c, R);
+}
+
+int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
   if (c->hCtr->flags & (kFlagLockSet | kFlagSegment)) {
     c->err = "pairwise detector limits exceeded (lock sets > 8 or element > 65535 events)";
     return HGRD_GPU_ENOTSUP;
@@ -481,6 +508,162 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
 }
 
 } // namespace
+
+
+// ---------------------------------------------------------------------------
+// Fused block-local path (fused.cuh) + pass 2 for elements shared by blocks.
+
+template <int IPT> size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
+  const size_t nKeysPad = (static_cast<size_t>(nKeys) + 3) & ~size_t(3);
+  return align16(sizeof(FusedSmem<IPT>)) + 8 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
+         sizeof(SiteDev) * P.sites.size() + sizeof(ParamDev) * P.params.size() +
+         8 * P.sites.size();
+}
+
+int readCountersFrom(hgrd_gpu_ctx *c, Counters *dev) {
+  CK(cudaMemcpyAsync(c->hCtr, dev, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+template <int IPT>
+int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem) {
+  CK(cudaFuncSetAttribute(k_fused<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(smem)));
+  int perSM = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_fused<IPT>, kFusedThreads, smem));
+  const int64_t grid = std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1));
+  StageTimer t(c, "k_fused");
+  k_fused<IPT><<<static_cast<unsigned>(grid), kFusedThreads, smem, c->st>>>(F);
+  return 0;
+}
+
+// Returns 1 when the launch was fully checked, 0 to fall back to the
+// general pipeline, < 0 on error.  D.kl must hold the general key layout
+// (used by pass 2).
+int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobOffsets &o,
+             const Plan &P, hgrd_gpu_result *R, uint32_t recInsns, bool loops) {
+  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+  const int nKeys = 3 * nLocs * nLocs;
+  int64_t bpi = std::max<int64_t>(1, kFusedThreads / D.tpb);
+  const uint64_t per = std::max<uint32_t>(recInsns, 1);
+  while (bpi > 1 && static_cast<uint64_t>(bpi * D.tpb) * per > 4096)
+    bpi /= 2;
+  const uint64_t perIter = static_cast<uint64_t>(bpi * D.tpb) * per;
+  if (bpi * D.tpb > 65536 || (!loops && perIter > 4096))
+    return 0;
+  const int ipt = (!loops && perIter <= 1024) ? 4 : 16;
+  const size_t smem = ipt == 4 ? fusedSmemBytes<4>(L, P, nKeys) : fusedSmemBytes<16>(L, P, nKeys);
+  if (smem > 227 * 1024)
+    return 0;
+
+  const size_t ownerN = std::max<uint64_t>(P.totalW, 1);
+  const bool fresh = c->owner.cap < ownerN;
+  NEED(c->owner, ownerN);
+  if (fresh || c->epoch >= 4094) {
+    CK(cudaMemsetAsync(c->owner.p, 0, c->owner.cap * sizeof(uint32_t), c->st));
+    c->epoch = 0;
+  }
+  ++c->epoch;
+  NEED(c->keyElem, static_cast<size_t>(nKeys));
+  CK(cudaMemsetAsync(c->keyElem.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
+  const uint32_t candCap = 1u << 16;
+  NEED(c->cand, candCap);
+  NEED(c->races, static_cast<size_t>(nKeys));
+  CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(Counters), c->st));
+
+  FusedArgs F{};
+  F.L = D;
+  F.nLocs = nLocs;
+  F.nKeys = nKeys;
+  F.bpi = static_cast<int>(bpi);
+  F.nIters = (D.nBlocks + bpi - 1) / bpi;
+  F.owner = c->owner.p;
+  F.epoch = c->epoch;
+  F.keyElem = c->keyElem.p;
+  F.cand = c->cand.p;
+  F.candCap = candCap;
+  F.candCount = &c->ctr.p->candCount;
+  F.nW = o.nW;
+  int rc = ipt == 4 ? launchFused<4>(c, F, smem) : launchFused<16>(c, F, smem);
+  if (rc < 0)
+    return rc;
+  CK(cudaGetLastError());
+  ++c->kernelLaunches;
+  DetectArgs A = detectArgs(c, L, D, o, 0, 7);
+  {
+    StageTimer t(c, "k_fused_finalize");
+    k_fused_finalize<<<nKeys, 128, 0, c->st>>>(F, A, c->races.p);
+  }
+  CK(cudaGetLastError());
+  ++c->kernelLaunches;
+  rc = readCounters(c);
+  if (rc < 0)
+    return rc;
+  const Counters h = *c->hCtr;
+  if ((h.flags & (kFlagAbort | kFlagFusedOverflow)) || h.traps > 0 ||
+      static_cast<int64_t>(h.steps) > L.step_budget)
+    return 0;
+  R->steps = static_cast<int64_t>(h.steps);
+  R->instances = h.instances;
+  R->records = h.records;
+  R->mode = L.flags & ~HGRD_LAUNCH_SEQUENTIAL;
+  if (!(h.flags & kFlagShared))
+    return fetchRaces(c, R) < 0 ? -1 : 1;
+
+  // pass 2: INTER-BLOCK over the elements two or more blocks touched
+  NEED(c->ctr2, 1);
+  LaunchDev D2 = D;
+  D2.ctr = c->ctr2.p;
+  D2.ownerFilter = c->owner.p;
+  D2.ownerMultiTag = (c->epoch << 20) | kOwnerMulti;
+  int bP = D.kl.bP, bQ = D.kl.bQ;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    if (!makeLayout(D2.kl, D.kl.bE, D.kl.bB, bP, D.kl.bW, bQ, D.kl.bL)) {
+      c->err = "packed record key wider than 64 bits";
+      return HGRD_GPU_ENOTSUP;
+    }
+    const uint64_t nBatches = (static_cast<uint64_t>(D.nThreads) + 31) / 32;
+    const uint64_t blocks = std::min<uint64_t>((nBatches + 7) / 8, uint64_t(c->nSM) * 8);
+    const uint64_t warps = blocks * 8;
+    const uint64_t chunk = std::clamp<uint64_t>(h.records / std::max<uint64_t>(warps, 1) / 4, 64, kChunk);
+    uint64_t cap = std::max<uint64_t>(h.records + warps * chunk + 4096, c->capHint);
+    D2.chunk = static_cast<uint32_t>(chunk);
+    NEED(c->keys, cap);
+    NEED(c->vals, cap);
+    D2.keys = c->keys.p;
+    D2.vals = c->vals.p;
+    D2.capacity = cap;
+    CK(cudaMemsetAsync(c->ctr2.p, 0, sizeof(Counters), c->st));
+    const size_t sm = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
+                      sizeof(ParamDev) * P.params.size();
+    if (sm > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_expand_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(sm)));
+    {
+      StageTimer t(c, "k_expand_par_shared");
+      k_expand_par<<<static_cast<unsigned>(blocks), 256, sm, c->st>>>(D2);
+    }
+    CK(cudaGetLastError());
+    ++c->kernelLaunches;
+    rc = readCountersFrom(c, c->ctr2.p);
+    if (rc < 0)
+      return rc;
+    const Counters h2 = *c->hCtr;
+    if (h2.flags & kFlagCapacity) {
+      c->capHint = std::max<uint64_t>(c->capHint, h2.cursor + warps * chunk + 4096) * 2;
+      continue;
+    }
+    if (h2.flags & kFlagPhase) {
+      bP = std::max(bP, bitsFor(uint64_t(h2.maxBp) + 1));
+      bQ = std::max(bQ, bitsFor(uint64_t(h2.maxWp) + 1));
+      continue;
+    }
+    rc = detect(c, L, D2, o, std::min<uint64_t>(h2.cursor, cap), false, false, R, 1, true);
+    return rc < 0 ? rc : 1;
+  }
+  return 0;
+}
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -630,6 +813,17 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   if (smem > 200 * 1024)
     seq = true;
   bool snapped = false;
+
+  const bool fusedOk = c->fusedEnabled && !seq && !locks && P.summaryOk && L.n_locs <= 32 &&
+                       o.nW <= kMaxWritten && D.nBlocks < (1 << 20) - 2 &&
+                       !(L.flags & HGRD_LAUNCH_GENERAL);
+  if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
+    rc = runFused(c, L, D, o, P, R, recInsns, loops);
+    if (rc < 0)
+      return rc;
+    if (rc == 1)
+      goto finish;
+  }
 
   for (int attempt = 0; attempt < 16; ++attempt) {
     if (!makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
@@ -790,6 +984,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       return rc;
     break;
   }
+finish:
   CK(cudaEventRecord(c->e1, c->st));
   CK(cudaEventSynchronize(c->e1));
   float ms = 0;
@@ -852,7 +1047,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   f(c->keys), f(c->keysAlt), f(c->elemK), f(c->elemKAlt), f(c->vals), f(c->valsAlt);
   f(c->order), f(c->orderAlt), f(c->cubTemp), f(c->blob), f(c->snapshot), f(c->keySeg);
   f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
-  f(c->opSeq), f(c->opStart), f(c->traps);
+  f(c->opSeq), f(c->opStart), f(c->traps), f(c->owner), f(c->keyElem), f(c->cand), f(c->ctr2);
   for (char *ch : c->chunks)
     cudaFree(ch);
   for (auto &b : c->bigUsed)
@@ -881,6 +1076,13 @@ int hgrd_gpu_set_profiling(hgrd_gpu_ctx *c, int on) {
 }
 
 const char *hgrd_gpu_last_profile(hgrd_gpu_ctx *c) { return c ? c->profileJson.c_str() : "[]"; }
+
+int hgrd_gpu_set_fused(hgrd_gpu_ctx *c, int enabled) {
+  if (!c)
+    return HGRD_GPU_EINVAL;
+  c->fusedEnabled = enabled != 0;
+  return 0;
+}
 
 unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *c) { return c ? c->kernelLaunches : 0; }
 

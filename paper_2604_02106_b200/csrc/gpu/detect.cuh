@@ -50,6 +50,7 @@ struct DetectArgs {
   const uint64_t *wBase;
   const int32_t *wHandle;
   int nW;
+  int kindMask; // kinds to report: bit 0 INTER-BLOCK, 1 INTRA-BLOCK, 2 INTRA-WARP
 };
 
 __device__ __forceinline__ void siteKey(const DetectArgs &A, int a, int b, int kind,
@@ -122,12 +123,14 @@ __global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
     if ((k >> kl.shE) != elem)
       break;
     if ((k >> kl.shP) != g2) {
-      flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
+      if (A.kindMask & 2)
+        flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
       p2 = 0;
       g2 = k >> kl.shP;
     }
     if ((k >> kl.shQ) != g3) {
-      flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
+      if (A.kindMask & 4)
+        flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
       p3 = 0;
       g3 = k >> kl.shQ;
     }
@@ -136,9 +139,12 @@ __global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
     note(p2, mn2, mx2, s, static_cast<uint32_t>((k >> kl.shW) & mW));
     note(p3, mn3, mx3, s, static_cast<uint32_t>(k & mL));
   }
-  flushLevel(A, p1, mn1, mx1, A.confInter, 0, seg, keySeg);
-  flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
-  flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
+  if (A.kindMask & 1)
+    flushLevel(A, p1, mn1, mx1, A.confInter, 0, seg, keySeg);
+  if (A.kindMask & 2)
+    flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
+  if (A.kindMask & 4)
+    flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
 }
 
 __device__ __forceinline__ void elementOf(const DetectArgs &A, uint64_t elem,
@@ -180,6 +186,8 @@ __global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
     return;
   const KeyLayout kl = A.kl;
   const int kind = K % 3;
+  if (!((A.kindMask >> kind) & 1))
+    return;
   const int la = (K / 3) / A.nLocs, lb = (K / 3) % A.nLocs;
   const uint64_t *conf = kind == 0 ? A.confInter : A.confIntra;
   const int gsh = kind == 0 ? kl.shE : kind == 1 ? kl.shP : kl.shQ;

@@ -46,7 +46,7 @@ struct ParamDev {
   int64_t *ptr;      // device buffer base (nullptr: scalar / unallocated)
   int64_t size;      // elements
   int32_t handle;    // -1 when unbound
-  int32_t written;   // the launch stores/atomically updates this buffer
+  int32_t written;   // 1 + index among the buffers the launch writes, 0 if read-only
   uint64_t elemBase; // flat element base (written buffers only)
 };
 
@@ -75,7 +75,7 @@ struct Counters {
   unsigned int flags;
   int abortStmt;
   unsigned int nRaces;
-  unsigned int pad;
+  unsigned int candCount;
 };
 
 struct LaunchDev {
@@ -106,6 +106,9 @@ struct LaunchDev {
   int32_t *opSeq;
   uint64_t opCap;
   uint64_t *opStart;         // nThreads + 1
+  // pass 2 of the fused path: only elements the ownership table marks MULTI
+  const uint32_t *ownerFilter;
+  uint32_t ownerMultiTag;
 };
 
 __host__ __device__ inline int64_t wrapAdd(int64_t a, int64_t b) {
@@ -151,6 +154,10 @@ __device__ __forceinline__ uint64_t packKey(const KeyLayout &k, uint64_t elem,
                                             uint64_t lane) {
   return (elem << k.shE) | (block << k.shB) | (bp << k.shP) | (warp << k.shW) |
          (wp << k.shQ) | lane;
+}
+
+__device__ __forceinline__ int bitsForDev(uint64_t n) { // bits to hold 0 .. n-1
+  return n <= 1 ? 0 : 64 - __clzll(static_cast<long long>(n - 1));
 }
 
 __device__ __forceinline__ uint64_t fieldMask(int bits) {

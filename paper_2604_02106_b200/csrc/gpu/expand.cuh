@@ -112,7 +112,8 @@ __device__ __forceinline__ void runParallel(const LaunchDev &L,
         break;
       }
       ++tally.inst;
-      if (S.record) {
+      if (S.record && (!L.ownerFilter ||
+                       L.ownerFilter[P->elemBase + static_cast<uint64_t>(idx)] == L.ownerMultiTag)) {
         if (bp > maskP || wp > maskQ)
           tally.flags |= kFlagPhase;
         if (seq > kSeqMask)

@@ -1,0 +1,628 @@
+// K-fused: block-local race check (PARALLEL launches without lock idioms).
+//
+// One CTA iteration takes one or more whole MiniCU blocks.  Every
+// INTRA-BLOCK / INTRA-WARP pair lies inside one MiniCU block
+// (reference src/oracle.cpp:754-769), so they are found entirely on chip:
+//   1. expansion into shared memory (records: global element id + meta),
+//   2. CUB block radix sort by  w | element offset | block | bp | warp | wp | lane
+//      (element offsets relative to the iteration's minimum per buffer, so
+//      the key is short: 10 bits for the stencil tile),
+//   3. per element group: realised INTRA keys (pairwise for small groups,
+//      per-site min/max summaries for large ones), minimum element per key,
+//   4. per realised key: the first (x, y) pair of the reference's order
+//      inside that element, published as a candidate (global element via
+//      atomicMin, candidates filtered by it; k_fused_finalize keeps the
+//      lexicographically first pair of the minimum element).
+// INTER-BLOCK pairs need a second block: every (element, block) also does
+// one ownership update on a per-element table (epoch-tagged, no memset);
+// an element reached from two blocks becomes MULTI and only MULTI elements
+// go through the global record sort (pass 2 in ctx.cu).
+#pragma once
+
+#include "detect.cuh"
+#include "device.cuh"
+#include "expand.cuh"
+
+#include <cub/block/block_radix_sort.cuh>
+
+namespace hgrdgpu {
+namespace dev {
+
+constexpr int kFusedThreads = 256;
+constexpr int kMaxWritten = 8;
+constexpr uint32_t kOwnerMulti = 0xFFFFFu;
+constexpr int kSmallGroup = 24; // pairwise below, summaries above
+
+enum FusedFlags : uint32_t {
+  kFlagShared = 128u,   // an element is accessed by two blocks (pass 2 needed)
+  kFlagFusedOverflow = 256u, // records / key bits / candidates did not fit
+};
+
+struct Candidate {
+  int32_t key;
+  int32_t siteX, siteY;
+  int32_t pad;
+  uint64_t elem;
+  uint64_t xOrd, yOrd;
+};
+
+struct FusedArgs {
+  LaunchDev L;
+  int nLocs, nKeys;
+  int bpi;              // whole MiniCU blocks per iteration
+  int64_t nIters;
+  uint32_t *owner;
+  uint32_t epoch;
+  unsigned long long *keyElem;
+  Candidate *cand;
+  uint32_t candCap;
+  unsigned int *candCount;
+  int nW;
+};
+
+__device__ __forceinline__ void ownerUpdate(const FusedArgs &F, uint64_t e, uint64_t blk,
+                                            unsigned &flags) {
+  const uint32_t tag = F.epoch << 20;
+  const uint32_t want = tag | static_cast<uint32_t>(blk + 1);
+  const uint32_t multi = tag | kOwnerMulti;
+  uint32_t cur = F.owner[e];
+  for (;;) {
+    if ((cur >> 20) != F.epoch) { // empty for this launch
+      const uint32_t prev = atomicCAS(&F.owner[e], cur, want);
+      if (prev == cur)
+        return;
+      cur = prev;
+      continue;
+    }
+    const uint32_t f = cur & kOwnerMulti;
+    if (f == (want & kOwnerMulti) || f == kOwnerMulti) {
+      if (f == kOwnerMulti)
+        flags |= kFlagShared;
+      return;
+    }
+    const uint32_t prev = atomicCAS(&F.owner[e], cur, multi);
+    if (prev == cur) {
+      flags |= kFlagShared;
+      return;
+    }
+    cur = prev;
+  }
+}
+
+template <int IPT> struct FusedSmem {
+  static constexpr int kCap = kFusedThreads * IPT;
+  using Sort = cub::BlockRadixSort<uint64_t, kFusedThreads, IPT, uint32_t, 6>;
+  typename Sort::TempStorage sortTmp;
+  uint64_t elem[kCap];  // global element id, by record index
+  uint64_t meta[kCap];  // tli:16 | bp:8 | wp:8 | site:12 | seq:20
+  uint64_t key[kCap];   // sorted keys
+  uint32_t idx[kCap];   // sorted -> record index
+  unsigned long long minE[kMaxWritten], maxE[kMaxWritten];
+  unsigned int count, maxBp, maxWp, nReal, flags;
+  // field start bits of the block-local key  w|off|blk|bp|warp|wp|lane
+  int fWp, fWarp, fBp, fBlk, fOff, fW, total;
+};
+
+__device__ __forceinline__ uint64_t packMeta(uint32_t tli, uint32_t bp, uint32_t wp, int site,
+                                             uint32_t seq) {
+  return (static_cast<uint64_t>(tli) << 48) | (static_cast<uint64_t>(bp & 255) << 40) |
+         (static_cast<uint64_t>(wp & 255) << 32) | (static_cast<uint64_t>(site & 4095) << 20) |
+         (seq & kSeqMask);
+}
+__device__ __forceinline__ uint32_t metaTli(uint64_t m) { return static_cast<uint32_t>(m >> 48); }
+__device__ __forceinline__ uint32_t metaBp(uint64_t m) { return (m >> 40) & 255; }
+__device__ __forceinline__ uint32_t metaWp(uint64_t m) { return (m >> 32) & 255; }
+__device__ __forceinline__ int metaSite(uint64_t m) { return static_cast<int>((m >> 20) & 4095); }
+__device__ __forceinline__ uint32_t metaSeq(uint64_t m) { return static_cast<uint32_t>(m & kSeqMask); }
+
+// Expansion of one MiniCU thread into shared memory (PARALLEL semantics,
+// same interpreter as k_expand_par).
+template <int IPT>
+__device__ __forceinline__ void runIntoSmem(const LaunchDev &L, const hgrd_gpu_insn *code,
+                                            const SiteDev *sites, const ParamDev *params,
+                                            int64_t t, uint32_t tli, FusedSmem<IPT> &S,
+                                            LaneTally &tally) {
+  int64_t r[kMaxRegs];
+  for (int i = 0; i < L.nRegs; ++i)
+    r[i] = L.regInit[i];
+  Builtins bi;
+  int64_t block, warp, lane;
+  threadIdentity(L, t, bi, block, warp, lane);
+  uint32_t bp = 0, wp = 0, seq = 0;
+  int64_t steps = 0;
+  int pc = 0;
+  for (;;) {
+    const hgrd_gpu_insn I = code[pc];
+    switch (I.op) {
+    case HGRD_OP_END:
+      goto done;
+    case HGRD_OP_STEP:
+      if (++steps > L.stepBudget) {
+        tally.flags |= kFlagAbort;
+        goto done;
+      }
+      break;
+    case HGRD_OP_CONST:
+      r[I.a] = I.imm;
+      break;
+    case HGRD_OP_MOV:
+      r[I.a] = r[I.b];
+      break;
+    case HGRD_OP_BUILTIN:
+      r[I.a] = bi.v[I.sub];
+      break;
+    case HGRD_OP_BIN:
+      r[I.a] = applyBin(I.sub, r[I.b], r[I.c]);
+      break;
+    case HGRD_OP_LOAD:
+    case HGRD_OP_STORE:
+    case HGRD_OP_ATOMIC: {
+      const int site = static_cast<int>(I.imm);
+      const SiteDev Sd = sites[site];
+      const int64_t idx = I.op == HGRD_OP_LOAD ? r[I.b] : r[I.a];
+      const ParamDev *P = Sd.param >= 0 ? &params[Sd.param] : nullptr;
+      if (!P || P->handle < 0 || idx < 0 || idx >= P->size) {
+        ++tally.traps;
+        if (I.op == HGRD_OP_LOAD)
+          r[I.a] = 0;
+        break;
+      }
+      ++tally.inst;
+      if (Sd.record) {
+        if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
+          tally.flags |= kFlagFusedOverflow;
+        const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
+        const unsigned pos = atomicAdd(&S.count, 1u);
+        if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
+          S.elem[pos] = e;
+          S.meta[pos] = packMeta(tli, bp, wp, site, seq);
+          const int w = P->written - 1;
+          atomicMin(&S.minE[w], static_cast<unsigned long long>(e));
+          atomicMax(&S.maxE[w], static_cast<unsigned long long>(e));
+        } else {
+          tally.flags |= kFlagFusedOverflow;
+        }
+        ++tally.recs;
+      }
+      ++seq;
+      if (I.op == HGRD_OP_LOAD)
+        r[I.a] = (I.sub & 1) ? __ldg(P->ptr + idx) : 0;
+      break;
+    }
+    case HGRD_OP_SYNCTHREADS:
+      ++bp;
+      ++wp;
+      break;
+    case HGRD_OP_SYNCWARP:
+      ++wp;
+      break;
+    case HGRD_OP_FENCE:
+      ++seq;
+      break;
+    case HGRD_OP_JZ:
+      if (r[I.a] == 0) {
+        pc = static_cast<int>(I.imm);
+        continue;
+      }
+      break;
+    case HGRD_OP_JMP:
+      pc = static_cast<int>(I.imm);
+      continue;
+    default:
+      goto done;
+    }
+    ++pc;
+  }
+done:
+  tally.steps += static_cast<unsigned long long>(steps);
+  atomicMax(&S.maxBp, bp);
+  atomicMax(&S.maxWp, wp);
+}
+
+// Conditions of the reference pair rule for two records of one element
+// inside one MiniCU block (:750-769), INTRA kinds only.  Returns kind or -1.
+__device__ __forceinline__ int intraKind(const LaunchDev &L, const SiteDev *sites, uint64_t ma,
+                                         uint64_t mb, uint32_t tpb, int64_t ws) {
+  const uint32_t ta = metaTli(ma), tb = metaTli(mb);
+  if (ta == tb)
+    return -1;
+  if (ta / tpb != tb / tpb)
+    return -1; // different MiniCU blocks: INTER, handled by ownership
+  const SiteDev &sa = sites[metaSite(ma)], &sb = sites[metaSite(mb)];
+  if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
+    return -1;
+  if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC && sa.scope != HGRD_SCOPE_NONE &&
+      sb.scope != HGRD_SCOPE_NONE)
+    return -1;
+  if (metaBp(ma) != metaBp(mb))
+    return -1;
+  const uint32_t wa = (ta % tpb) / static_cast<uint32_t>(ws), wb = (tb % tpb) / static_cast<uint32_t>(ws);
+  if (wa == wb && metaWp(ma) != metaWp(mb))
+    return -1;
+  return wa != wb ? 1 : 2;
+}
+
+__device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa, int sb, int kind) {
+  int la = sites[sa].loc, lb = sites[sb].loc;
+  if (lb < la) {
+    int t = la;
+    la = lb;
+    lb = t;
+  }
+  return (la * nLocs + lb) * 3 + kind;
+}
+
+template <int IPT>
+__device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, uint32_t *sKeyMin, uint32_t *sReal,
+                                        int K, uint32_t pos) {
+  if (sKeyMin[K] <= pos)
+    return;
+  const uint32_t old = atomicMin(&sKeyMin[K], pos);
+  if (old == 0xffffffffu) {
+    const unsigned slot = atomicAdd(&S.nReal, 1u);
+    sReal[slot] = static_cast<uint32_t>(K);
+  }
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
+  using Smem = FusedSmem<IPT>;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  Smem &S = *reinterpret_cast<Smem *>(dyn);
+  unsigned char *after = dyn + ((sizeof(Smem) + 15) & ~size_t(15));
+  const int nKeysPad = (F.nKeys + 3) & ~3;
+  uint32_t *sKeyMin = reinterpret_cast<uint32_t *>(after);
+  uint32_t *sReal = sKeyMin + nKeysPad;
+  hgrd_gpu_insn *sCode = reinterpret_cast<hgrd_gpu_insn *>(sReal + nKeysPad);
+  SiteDev *sSites = reinterpret_cast<SiteDev *>(sCode + F.L.nCode);
+  ParamDev *sParams = reinterpret_cast<ParamDev *>(sSites + F.L.nSites);
+  uint64_t *sConf = reinterpret_cast<uint64_t *>(sParams + F.L.nParams);
+  // dynamic shared memory layout mirrored by fusedSmemBytes() in ctx.cu
+  const LaunchDev &L = F.L;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < L.nCode; i += kFusedThreads)
+    sCode[i] = L.code[i];
+  for (int i = tid; i < L.nSites; i += kFusedThreads) {
+    sSites[i] = L.sites[i];
+    sConf[i] = L.confIntra[i];
+  }
+  for (int i = tid; i < L.nParams; i += kFusedThreads)
+    sParams[i] = L.params[i];
+  for (int i = tid; i < F.nKeys; i += kFusedThreads)
+    sKeyMin[i] = 0xffffffffu;
+  if (tid == 0) {
+    S.nReal = 0;
+    S.flags = 0;
+  }
+  const uint32_t tpb = static_cast<uint32_t>(L.tpb);
+  const int64_t ws = L.ws;
+  LaneTally tally;
+  unsigned myFlags = 0;
+
+  for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x) {
+    const int64_t firstBlock = it * F.bpi;
+    const int64_t nb = min(static_cast<int64_t>(F.bpi), L.nBlocks - firstBlock);
+    __syncthreads();
+    if (tid == 0) {
+      S.count = 0;
+      S.maxBp = 0;
+      S.maxWp = 0;
+    }
+    if (tid < kMaxWritten) {
+      S.minE[tid] = ~0ull;
+      S.maxE[tid] = 0;
+    }
+    __syncthreads();
+    // 1. expansion of the iteration's whole MiniCU blocks
+    for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads)
+      runIntoSmem<IPT>(L, sCode, sSites, sParams, firstBlock * L.tpb + tl,
+                       static_cast<uint32_t>(tl), S, tally);
+    __syncthreads();
+    const unsigned n = min(S.count, static_cast<unsigned>(Smem::kCap));
+    if (S.count > static_cast<unsigned>(Smem::kCap))
+      myFlags |= kFlagFusedOverflow;
+    if (n == 0)
+      continue;
+    // 2. key layout for this iteration
+    if (tid == 0) {
+      uint64_t span = 1;
+      for (int w = 0; w < F.nW && w < kMaxWritten; ++w)
+        if (S.minE[w] <= S.maxE[w])
+          span = max(span, static_cast<uint64_t>(S.maxE[w] - S.minE[w] + 1));
+      const int bL = bitsForDev(static_cast<uint64_t>(ws < L.tpb ? ws : L.tpb));
+      const int bW = bitsForDev(static_cast<uint64_t>((L.tpb + ws - 1) / ws));
+      const int bQ = bitsForDev(uint64_t(S.maxWp) + 1);
+      const int bP = bitsForDev(uint64_t(S.maxBp) + 1);
+      const int bBk = bitsForDev(static_cast<uint64_t>(F.bpi));
+      const int bO = bitsForDev(span);
+      const int bWr = bitsForDev(static_cast<uint64_t>(F.nW));
+      S.fWp = bL;
+      S.fWarp = S.fWp + bQ;
+      S.fBp = S.fWarp + bW;
+      S.fBlk = S.fBp + bP;
+      S.fOff = S.fBlk + bBk;
+      S.fW = S.fOff + bO;
+      S.total = S.fW + bWr;
+      if (S.total > 64)
+        S.flags |= kFlagFusedOverflow;
+    }
+    __syncthreads();
+    if (S.total > 64)
+      continue;
+    // 3. block-local sort
+    {
+      uint64_t keys[IPT];
+      uint32_t vals[IPT];
+      const int wpShift = S.fWp, warpShift = S.fWarp, bpShift = S.fBp, blkShift = S.fBlk,
+                offShift = S.fOff, wShift = S.fW;
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        const unsigned i = static_cast<unsigned>(tid * IPT + j);
+        vals[j] = i;
+        if (i < n) {
+          const uint64_t m = S.meta[i];
+          const uint32_t tli = metaTli(m);
+          const uint32_t blk = tli / tpb, tl = tli % tpb;
+          const uint32_t warp = tl / static_cast<uint32_t>(ws), lane = tl % static_cast<uint32_t>(ws);
+          const SiteDev &sd = sSites[metaSite(m)];
+          const int w = sParams[sd.param].written - 1;
+          const uint64_t off = S.elem[i] - S.minE[w];
+          keys[j] = (static_cast<uint64_t>(w) << wShift) | (off << offShift) |
+                    (static_cast<uint64_t>(blk) << blkShift) |
+                    (static_cast<uint64_t>(metaBp(m)) << bpShift) |
+                    (static_cast<uint64_t>(warp) << warpShift) |
+                    (static_cast<uint64_t>(metaWp(m)) << wpShift) | lane;
+        } else {
+          keys[j] = ~0ull;
+        }
+      }
+      typename Smem::Sort(S.sortTmp).Sort(keys, vals, 0, S.total > 0 ? S.total : 1);
+#pragma unroll
+      for (int j = 0; j < IPT; ++j) {
+        S.key[tid * IPT + j] = keys[j];
+        S.idx[tid * IPT + j] = vals[j];
+      }
+    }
+    __syncthreads();
+    // group keys of the sorted key
+    const int shLane = S.fWp;  // key >> fWp  : element|blk|bp|warp|wp  (INTRA-WARP group)
+    const int shBpF = S.fBp;   // key >> fBp  : element|blk|bp          (INTRA-BLOCK group)
+    const int shBlkF = S.fBlk; // key >> fBlk : element|blk             (ownership unit)
+    const int shElem = S.fOff; // key >> fOff : element
+    // 4. per element group: ownership + INTRA keys
+    for (int j = 0; j < IPT; ++j) {
+      const int p = tid * IPT + j;
+      if (p >= static_cast<int>(n))
+        break;
+      const uint64_t g = S.key[p] >> shElem;
+      if (p > 0 && (S.key[p - 1] >> shElem) == g)
+        continue;
+      int e = p + 1;
+      while (e < static_cast<int>(n) && (S.key[e] >> shElem) == g)
+        ++e;
+      const uint64_t ge = S.elem[S.idx[p]];
+      // ownership per (element, block)
+      for (int q = p; q < e; ++q)
+        if (q == p || (S.key[q] >> shBlkF) != (S.key[q - 1] >> shBlkF))
+          ownerUpdate(F, ge, static_cast<uint64_t>(firstBlock + metaTli(S.meta[S.idx[q]]) / tpb),
+                      myFlags);
+      if (e - p < 2)
+        continue;
+      if (e - p <= kSmallGroup) {
+        for (int a = p; a < e; ++a) {
+          const uint64_t ma = S.meta[S.idx[a]];
+          for (int b = a + 1; b < e; ++b) {
+            const uint64_t mb = S.meta[S.idx[b]];
+            const int kind = intraKind(L, sSites, ma, mb, tpb, ws);
+            if (kind < 0)
+              continue;
+            const int sa = metaSite(ma), sb = metaSite(mb);
+            if (!((sConf[sa] >> sb) & 1ull))
+              continue;
+            noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, sa, sb, kind),
+                    static_cast<uint32_t>(p));
+          }
+        }
+      } else {
+        // summaries: per site (min,max) warp at (element,blk,bp), lane at (..,warp,wp)
+        uint32_t mn2[kMaxSites], mx2[kMaxSites], mn3[kMaxSites], mx3[kMaxSites];
+        uint64_t p2 = 0, p3 = 0;
+        uint64_t g2 = S.key[p] >> shBpF, g3 = S.key[p] >> shLane;
+        auto flush = [&](uint64_t pres, const uint32_t *mn, const uint32_t *mx, int kind) {
+          uint64_t rem = pres;
+          while (rem) {
+            const int a = __ffsll(static_cast<long long>(rem)) - 1;
+            rem &= rem - 1;
+            uint64_t m = sConf[a] & pres & ~((1ull << a) - 1);
+            while (m) {
+              const int b = __ffsll(static_cast<long long>(m)) - 1;
+              m &= m - 1;
+              if (min(mn[a], mn[b]) < max(mx[a], mx[b]))
+                noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, a, b, kind),
+                        static_cast<uint32_t>(p));
+            }
+          }
+        };
+        for (int q = p; q < e; ++q) {
+          const uint64_t k = S.key[q];
+          if ((k >> shBpF) != g2) {
+            flush(p2, mn2, mx2, 1);
+            p2 = 0;
+            g2 = k >> shBpF;
+          }
+          if ((k >> shLane) != g3) {
+            flush(p3, mn3, mx3, 2);
+            p3 = 0;
+            g3 = k >> shLane;
+          }
+          const uint64_t m = S.meta[S.idx[q]];
+          const int s = metaSite(m);
+          const uint32_t tl = metaTli(m) % tpb;
+          note(p2, mn2, mx2, s, tl / static_cast<uint32_t>(ws));
+          note(p3, mn3, mx3, s, tl % static_cast<uint32_t>(ws));
+        }
+        flush(p2, mn2, mx2, 1);
+        flush(p3, mn3, mx3, 2);
+      }
+    }
+    __syncthreads();
+    // 5. witnesses of the keys realised in this iteration
+    const unsigned nReal = S.nReal;
+    for (unsigned r = tid; r < nReal; r += kFusedThreads) {
+      const int K = static_cast<int>(sReal[r]);
+      const int kind = K % 3;
+      const int la = (K / 3) / F.nLocs, lb = (K / 3) % F.nLocs;
+      const int p = static_cast<int>(sKeyMin[K]);
+      sKeyMin[K] = 0xffffffffu; // reset for the next iteration
+      const uint64_t g = S.key[p] >> shElem;
+      int e = p + 1;
+      while (e < static_cast<int>(n) && (S.key[e] >> shElem) == g)
+        ++e;
+      uint64_t bestX = ~0ull, bestY = ~0ull;
+      int sX = 0, sY = 0;
+      auto order = [&](uint64_t m) {
+        const uint64_t thread = static_cast<uint64_t>(firstBlock * L.tpb) + metaTli(m);
+        return (thread << kSeqBits) | metaSeq(m);
+      };
+      // lexicographically first (x, y) over the group's racing pairs of K
+      for (int a = p; a < e; ++a) {
+        const uint64_t ma = S.meta[S.idx[a]];
+        const int sa = metaSite(ma);
+        const int loa = sSites[sa].loc;
+        if (loa != la && loa != lb)
+          continue;
+        const uint64_t oa = order(ma);
+        if (oa > bestX)
+          continue;
+        for (int b = p; b < e; ++b) {
+          if (b == a)
+            continue;
+          const uint64_t mb = S.meta[S.idx[b]];
+          const uint64_t ob = order(mb);
+          if (ob <= oa)
+            continue; // y must follow x in event order
+          const int sb = metaSite(mb);
+          const int lob = sSites[sb].loc;
+          if (!((loa == la && lob == lb) || (loa == lb && lob == la)))
+            continue;
+          if (!((sConf[sa] >> sb) & 1ull))
+            continue;
+          if (intraKind(L, sSites, ma, mb, tpb, ws) != kind)
+            continue;
+          if (oa < bestX || (oa == bestX && ob < bestY)) {
+            bestX = oa;
+            bestY = ob;
+            sX = sa;
+            sY = sb;
+          }
+        }
+      }
+      const uint64_t ge = S.elem[S.idx[p]];
+      const unsigned long long old = atomicMin(&F.keyElem[K], static_cast<unsigned long long>(ge));
+      if (ge <= old) {
+        const unsigned c = atomicAdd(F.candCount, 1u);
+        if (c < F.candCap)
+          F.cand[c] = Candidate{K, sX, sY, 0, ge, bestX, bestY};
+        else
+          myFlags |= kFlagFusedOverflow;
+      }
+    }
+    if (tid == 0)
+      S.nReal = 0;
+  }
+  // counters
+  __syncthreads();
+  const int lane = tid & 31;
+  tally.flags |= myFlags;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    tally.steps += __shfl_down_sync(0xffffffffu, tally.steps, o);
+    tally.inst += __shfl_down_sync(0xffffffffu, tally.inst, o);
+    tally.traps += __shfl_down_sync(0xffffffffu, tally.traps, o);
+    tally.recs += __shfl_down_sync(0xffffffffu, tally.recs, o);
+    tally.flags |= __shfl_down_sync(0xffffffffu, tally.flags, o);
+  }
+  if (lane == 0) {
+    if (tally.steps)
+      atomicAdd(&L.ctr->steps, tally.steps);
+    if (tally.inst)
+      atomicAdd(&L.ctr->instances, tally.inst);
+    if (tally.traps)
+      atomicAdd(&L.ctr->traps, tally.traps);
+    if (tally.recs)
+      atomicAdd(&L.ctr->records, tally.recs);
+    if (tally.flags)
+      atomicOr(&L.ctr->flags, tally.flags);
+  }
+  if (tid == 0 && S.flags)
+    atomicOr(&L.ctr->flags, S.flags);
+}
+
+// One block per key: the lexicographically first candidate pair of the
+// key's minimum element becomes the race record.
+__global__ void k_fused_finalize(FusedArgs F, DetectArgs A, hgrd_gpu_race *races) {
+  const int K = blockIdx.x;
+  const unsigned long long e = F.keyElem[K];
+  if (e == ~0ull)
+    return;
+  const unsigned nc = min(*F.candCount, F.candCap);
+  __shared__ uint64_t bx[32], by[32];
+  __shared__ int bs[32], bt[32];
+  uint64_t x = ~0ull, y = ~0ull;
+  int sx = 0, sy = 0;
+  for (unsigned c = threadIdx.x; c < nc; c += blockDim.x) {
+    const Candidate &cd = F.cand[c];
+    if (cd.key != K || cd.elem != e)
+      continue;
+    if (cd.xOrd < x || (cd.xOrd == x && cd.yOrd < y)) {
+      x = cd.xOrd;
+      y = cd.yOrd;
+      sx = cd.siteX;
+      sy = cd.siteY;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ox = __shfl_down_sync(0xffffffffu, x, o);
+    const uint64_t oy = __shfl_down_sync(0xffffffffu, y, o);
+    const int osx = __shfl_down_sync(0xffffffffu, sx, o);
+    const int osy = __shfl_down_sync(0xffffffffu, sy, o);
+    if (ox < x || (ox == x && oy < y)) {
+      x = ox;
+      y = oy;
+      sx = osx;
+      sy = osy;
+    }
+  }
+  if (lane == 0) {
+    bx[wid] = x;
+    by[wid] = y;
+    bs[wid] = sx;
+    bt[wid] = sy;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0)
+    return;
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+    if (bx[w] < x || (bx[w] == x && by[w] < y)) {
+      x = bx[w];
+      y = by[w];
+      sx = bs[w];
+      sy = bt[w];
+    }
+  const unsigned pos = atomicAdd(&F.L.ctr->nRaces, 1u);
+  hgrd_gpu_race &o = races[pos];
+  o.kind = K % 3;
+  o.loc_a = (K / 3) / F.nLocs;
+  o.loc_b = (K / 3) % F.nLocs;
+  o.site_x = sx;
+  o.site_y = sy;
+  elementOf(A, e, o.handle, o.index);
+  o.thread_x = static_cast<int64_t>(x >> kSeqBits);
+  o.seq_x = static_cast<int32_t>(x & kSeqMask);
+  o.thread_y = static_cast<int64_t>(y >> kSeqBits);
+  o.seq_y = static_cast<int32_t>(y & kSeqMask);
+}
+
+} // namespace dev
+} // namespace hgrdgpu

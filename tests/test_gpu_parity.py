@@ -23,7 +23,14 @@ def _check_run(gpu, cpu_oracle, src, cfg, file_name, want):
     return got
 
 
-def test_corpus_runs(gpu, cpu_oracle):
+@pytest.fixture(params=["fused", "general"])
+def mode(request, gpu):
+    gpu.set_fused(request.param == "fused")
+    yield request.param
+    gpu.set_fused(True)
+
+
+def test_corpus_runs(gpu, cpu_oracle, mode):
     for e in load_golden("corpus"):
         for run in e["runs"]:
             _check_run(gpu, cpu_oracle, e["source"], run["config"], e["file"], run["result"])
@@ -38,12 +45,12 @@ def test_corpus_sweeps(gpu):
         assert got == e["sweep_default"], e["name"]
 
 
-def test_unit_cases(gpu, cpu_oracle):
+def test_unit_cases(gpu, cpu_oracle, mode):
     for c in load_golden("unit_cases"):
         _check_run(gpu, cpu_oracle, c["source"], c["config"], "oracle.mcu", c["result"])
 
 
-def test_fuzz(gpu, cpu_oracle):
+def test_fuzz(gpu, cpu_oracle, mode):
     """reference tests/test_soundness.cpp programs (mt19937(31337))."""
     total = 0
     for f in load_golden("fuzz"):
@@ -55,12 +62,12 @@ def test_fuzz(gpu, cpu_oracle):
     assert total > 500
 
 
-def test_edge_programs(gpu, cpu_oracle):
+def test_edge_programs(gpu, cpu_oracle, mode):
     for c in load_golden("edge"):
         _check_run(gpu, cpu_oracle, c["source"], c["config"], "edge.mcu", c["result"])
 
 
-def test_synthetic_small(gpu, cpu_oracle):
+def test_synthetic_small(gpu, cpu_oracle, mode):
     for c in load_golden("synthetic"):
         got = _check_run(gpu, cpu_oracle, c["source"], c["config"], "syn.mcu", c["result"])
         assert got["stats"]["parallelLaunches"] >= 1  # the data-parallel path ran
@@ -122,7 +129,9 @@ def test_launch_stencil(gpu, cpu_oracle, barrier, ws):
     ref_spec, _ = _spec_stencil(None, 1 << 14, barrier, ws)
     want = cpu_oracle.check_launch(ref_spec, bufs)
     assert _same(got, want), (got, want)
-    spec.launch.flags |= hg.LAUNCH_SEQUENTIAL  # ordered path must agree too
+    spec.launch.flags |= hg.LAUNCH_GENERAL  # the general (global sort) pipeline too
+    assert _same(gpu.check_launch(spec), want)
+    spec.launch.flags |= hg.LAUNCH_SEQUENTIAL  # and the ordered path
     assert _same(gpu.check_launch(spec), want)
 
 
@@ -135,6 +144,8 @@ def test_launch_histogram(gpu, cpu_oracle, update, bins):
     ref_spec, _ = _spec_hist(None, n, bins, update)
     want = cpu_oracle.check_launch(ref_spec, bufs)
     assert _same(got, want), (got, want)
+    spec.launch.flags |= hg.LAUNCH_GENERAL
+    assert _same(gpu.check_launch(spec), want)
 
 
 @pytest.mark.parametrize("barrier", [False, True])
@@ -144,6 +155,8 @@ def test_launch_transpose(gpu, cpu_oracle, barrier):
     ref_spec, _ = _spec_transpose(None, 128, barrier)
     want = cpu_oracle.check_launch(ref_spec, bufs)
     assert _same(got, want), (got, want)
+    spec.launch.flags |= hg.LAUNCH_GENERAL
+    assert _same(gpu.check_launch(spec), want)
 
 
 # ------------------------------------------------ full size, size-independent

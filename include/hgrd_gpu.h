@@ -29,7 +29,11 @@
 #ifndef HGRD_GPU_H
 #define HGRD_GPU_H
 
+#if defined(__CUDACC_RTC__) /* NVRTC (JIT-compiled race-check kernels) */
+#include <cuda/std/cstdint>
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -167,6 +171,8 @@ typedef struct hgrd_gpu_result {
 /* ---- contexts and device-resident buffers ------------------------------ */
 typedef struct hgrd_gpu_ctx hgrd_gpu_ctx;
 
+#if !defined(__CUDACC_RTC__) /* host API (not visible to JIT-compiled kernels) */
+
 int hgrd_gpu_create(int device, hgrd_gpu_ctx **out);
 void hgrd_gpu_destroy(hgrd_gpu_ctx *ctx);
 const char *hgrd_gpu_last_error(hgrd_gpu_ctx *ctx);
@@ -191,6 +197,12 @@ int hgrd_gpu_set_profiling(hgrd_gpu_ctx *ctx, int on);
 const char *hgrd_gpu_last_profile(hgrd_gpu_ctx *ctx);
 /* Enable (default) / disable the fused block-local check for PARALLEL launches. */
 int hgrd_gpu_set_fused(hgrd_gpu_ctx *ctx, int enabled);
+/* NVRTC specialisation of the expansion for each MiniCU kernel:
+ * 0 off (bytecode interpreter), 1 auto (launches >= 2^14 threads, default),
+ * 2 always. */
+int hgrd_gpu_set_jit(hgrd_gpu_ctx *ctx, int mode);
+/* JSON {"mode","compiles","compileMs","failures","lastError"} (ctx-owned). */
+const char *hgrd_gpu_jit_info(hgrd_gpu_ctx *ctx);
 /* Number of this library's own kernels launched by the context so far. */
 unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *ctx);
 
@@ -215,6 +227,7 @@ int hgrd_gpu_count_inputs(const char *source, const char *file_name);
 int hgrd_gpu_lower_json(const char *source, const char *file_name,
                         const char *kernel, char **out);
 void hgrd_gpu_free(char *p);
+#endif /* !__CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

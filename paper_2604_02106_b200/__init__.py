@@ -150,6 +150,9 @@ def load_library() -> ctypes.CDLL:
     lib.hgrd_gpu_last_profile.argtypes = [P]
     lib.hgrd_gpu_last_profile.restype = ctypes.c_char_p
     lib.hgrd_gpu_set_fused.argtypes = [P, ctypes.c_int]
+    lib.hgrd_gpu_set_jit.argtypes = [P, ctypes.c_int]
+    lib.hgrd_gpu_jit_info.argtypes = [P]
+    lib.hgrd_gpu_jit_info.restype = ctypes.c_char_p
     lib.hgrd_gpu_kernel_launches.argtypes = [P]
     lib.hgrd_gpu_kernel_launches.restype = ctypes.c_ulonglong
     _lib = lib
@@ -307,6 +310,13 @@ class GpuContext:
     def set_fused(self, on: bool = True):
         """Enable (default) / disable the fused block-local check."""
         self._lib.hgrd_gpu_set_fused(self._ctx, 1 if on else 0)
+
+    def set_jit(self, mode: int = 1):
+        """NVRTC specialisation: 0 off, 1 auto (>= 2^14 threads), 2 always."""
+        self._lib.hgrd_gpu_set_jit(self._ctx, mode)
+
+    def jit_info(self) -> dict:
+        return json.loads(self._lib.hgrd_gpu_jit_info(self._ctx).decode())
 
     def kernel_launches(self) -> int:
         return int(self._lib.hgrd_gpu_kernel_launches(self._ctx))

@@ -1,0 +1,149 @@
+// Thread bodies: how one MiniCU thread's statements execute.
+//
+// A body runs the lowered kernel for one thread and reports every effect to
+// a Sink (the kernel-specific access semantics):
+//   bool    step(int stmt)                    one step charged (false: stop)
+//   int64_t load(int site, int64_t idx, bool valueNeeded)
+//   void    store(int site, int64_t idx, int64_t value)
+//   void    atomic(int site, int64_t idx, int64_t value, int64_t compare)
+//   void    syncthreads(); syncwarp(); fence(int scope);
+//
+// InterpBody interprets hgrd_gpu bytecode (any kernel, no compilation).
+// JIT bodies are the same bytecode translated to straight-line CUDA C++ by
+// csrc/gpu/jit.cpp and compiled with NVRTC for sm_100a: registers become
+// locals, jumps become gotos, launch constants fold.
+#pragma once
+
+#include "device.cuh"
+
+namespace hgrdgpu {
+namespace dev {
+
+struct Builtins {
+  int64_t v[12];
+};
+
+__device__ __forceinline__ void threadIdentity(const LaunchDev &L, int64_t t, Builtins &b,
+                                               int64_t &block, int64_t &warp, int64_t &lane) {
+  block = t / L.tpb;
+  const int64_t tl = t - block * L.tpb;
+  b.v[0] = tl % L.block[0];
+  b.v[1] = (tl / L.block[0]) % L.block[1];
+  b.v[2] = tl / (L.block[0] * L.block[1]);
+  b.v[3] = block % L.grid[0];
+  b.v[4] = (block / L.grid[0]) % L.grid[1];
+  b.v[5] = block / (L.grid[0] * L.grid[1]);
+  b.v[6] = L.block[0];
+  b.v[7] = L.block[1];
+  b.v[8] = L.block[2];
+  b.v[9] = L.grid[0];
+  b.v[10] = L.grid[1];
+  b.v[11] = L.grid[2];
+  warp = tl / L.ws;
+  lane = tl - warp * L.ws;
+}
+
+struct InterpBody {
+  // `r` holds nRegs registers (local array or global scratch).
+  template <class Sink>
+  __device__ static void run(const LaunchDev &L, const hgrd_gpu_insn *__restrict__ code,
+                             const Builtins &bi, Sink &s, int64_t *r) {
+    for (int i = 0; i < L.nRegs; ++i)
+      r[i] = L.regInit[i];
+    int pc = 0;
+    for (;;) {
+      const hgrd_gpu_insn I = code[pc];
+      switch (I.op) {
+      case HGRD_OP_END:
+        return;
+      case HGRD_OP_STEP:
+        if (!s.step(static_cast<int>(I.imm)))
+          return;
+        break;
+      case HGRD_OP_CONST:
+        r[I.a] = I.imm;
+        break;
+      case HGRD_OP_MOV:
+        r[I.a] = r[I.b];
+        break;
+      case HGRD_OP_BUILTIN:
+        r[I.a] = bi.v[I.sub];
+        break;
+      case HGRD_OP_BIN:
+        r[I.a] = applyBin(I.sub, r[I.b], r[I.c]);
+        break;
+      case HGRD_OP_LOAD:
+        r[I.a] = s.load(static_cast<int>(I.imm), r[I.b], (I.sub & 1) != 0);
+        break;
+      case HGRD_OP_STORE:
+        s.store(static_cast<int>(I.imm), r[I.a], r[I.b]);
+        break;
+      case HGRD_OP_ATOMIC:
+        s.atomic(static_cast<int>(I.imm), r[I.a], r[I.b], r[I.c]);
+        break;
+      case HGRD_OP_SYNCTHREADS:
+        s.syncthreads();
+        break;
+      case HGRD_OP_SYNCWARP:
+        s.syncwarp();
+        break;
+      case HGRD_OP_FENCE:
+        s.fence(I.sub);
+        break;
+      case HGRD_OP_JZ:
+        if (r[I.a] == 0) {
+          pc = static_cast<int>(I.imm);
+          continue;
+        }
+        break;
+      case HGRD_OP_JMP:
+        pc = static_cast<int>(I.imm);
+        continue;
+      default:
+        return;
+      }
+      ++pc;
+    }
+  }
+};
+
+// Shared bookkeeping of the PARALLEL sinks: identity, phases, sequence
+// numbers, step budget, bounds checks (reference checkBounds :508-519).
+struct ParState {
+  const LaunchDev *L;
+  const SiteDev *sites;
+  const ParamDev *params;
+  int64_t block, warp, lane;
+  uint32_t bp = 0, wp = 0, seq = 0;
+  int64_t steps = 0;
+  unsigned long long inst = 0, traps = 0, recs = 0;
+  unsigned flags = 0;
+
+  __device__ __forceinline__ bool step(int) {
+    if (++steps > L->stepBudget) {
+      flags |= kFlagAbort;
+      return false;
+    }
+    return true;
+  }
+  // Returns the parameter when the access is in bounds (an instance).
+  __device__ __forceinline__ const ParamDev *check(int site, int64_t idx) {
+    const SiteDev &S = sites[site];
+    const ParamDev *P = S.param >= 0 ? &params[S.param] : nullptr;
+    if (!P || P->handle < 0 || idx < 0 || idx >= P->size) {
+      ++traps; // any trap sends the launch to the ordered path
+      return nullptr;
+    }
+    ++inst;
+    return P;
+  }
+  __device__ __forceinline__ void syncthreads() {
+    ++bp;
+    ++wp;
+  }
+  __device__ __forceinline__ void syncwarp() { ++wp; }
+  __device__ __forceinline__ void fence(int) { ++seq; } // fences take a seq (:616-618)
+};
+
+} // namespace dev
+} // namespace hgrdgpu

@@ -9,6 +9,7 @@
 #include "device.cuh"
 #include "expand.cuh"
 #include "fused.cuh"
+#include "jit.hpp"
 
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -89,6 +90,12 @@ struct hgrd_gpu_ctx {
   DevVec<Candidate> cand;
   DevVec<Counters> ctr2;               // fused pass 2 counters
   bool fusedEnabled = true;
+  // NVRTC specialisation: 0 off, 1 auto (large launches), 2 always
+  int jitMode = 1;
+  hgrdgpu::jit::Cache *jit = nullptr;
+  std::string jitErr;
+  int jitFailures = 0;
+  std::string jitInfo;
 
   unsigned char *hStage = nullptr;
   size_t hStageCap = 0;
@@ -510,6 +517,40 @@ int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
 } // namespace
 
 
+// Lazily compiled specialised kernels of one launch.
+struct JitGetter {
+  hgrd_gpu_ctx *c;
+  const hgrd_gpu_launch *L;
+  bool enabled;
+  const void *get(hgrdgpu::jit::Variant v) {
+    if (!enabled)
+      return nullptr;
+    if (!c->jit)
+      c->jit = hgrdgpu::jit::create();
+    std::string err;
+    const void *k = hgrdgpu::jit::get(c->jit, *L, v, err);
+    if (!k && !err.empty()) {
+      c->jitErr = err;
+      ++c->jitFailures;
+    }
+    return k;
+  }
+};
+
+int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t smem,
+                    const void *jitKernel, const char *stage) {
+  const void *fn = jitKernel ? jitKernel : reinterpret_cast<const void *>(k_expand_par<InterpBody>);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  void *args[] = {const_cast<LaunchDev *>(&D)};
+  {
+    StageTimer t(c, stage);
+    CK(cudaLaunchKernel(fn, dim3(blocks), dim3(256), args, smem, c->st));
+  }
+  ++c->kernelLaunches;
+  return 0;
+}
+
 // ---------------------------------------------------------------------------
 // Fused block-local path (fused.cuh) + pass 2 for elements shared by blocks.
 
@@ -527,14 +568,18 @@ int readCountersFrom(hgrd_gpu_ctx *c, Counters *dev) {
 }
 
 template <int IPT>
-int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem) {
-  CK(cudaFuncSetAttribute(k_fused<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *jitKernel) {
+  const void *fn =
+      jitKernel ? jitKernel : reinterpret_cast<const void *>(k_fused<IPT, InterpBody>);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(smem)));
   int perSM = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, k_fused<IPT>, kFusedThreads, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, kFusedThreads, smem));
   const int64_t grid = std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1));
-  StageTimer t(c, "k_fused");
-  k_fused<IPT><<<static_cast<unsigned>(grid), kFusedThreads, smem, c->st>>>(F);
+  void *args[] = {const_cast<FusedArgs *>(&F)};
+  StageTimer t(c, jitKernel ? "k_fused[jit]" : "k_fused");
+  CK(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kFusedThreads), args, smem,
+                      c->st));
   return 0;
 }
 
@@ -542,7 +587,8 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem) {
 // general pipeline, < 0 on error.  D.kl must hold the general key layout
 // (used by pass 2).
 int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobOffsets &o,
-             const Plan &P, hgrd_gpu_result *R, uint32_t recInsns, bool loops) {
+             const Plan &P, hgrd_gpu_result *R, uint32_t recInsns, bool loops,
+             JitGetter &jk) {
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
   int64_t bpi = std::max<int64_t>(1, kFusedThreads / D.tpb);
@@ -585,7 +631,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.candCap = candCap;
   F.candCount = &c->ctr.p->candCount;
   F.nW = o.nW;
-  int rc = ipt == 4 ? launchFused<4>(c, F, smem) : launchFused<16>(c, F, smem);
+  int rc = ipt == 4 ? launchFused<4>(c, F, smem, jk.get(hgrdgpu::jit::kFused4))
+                    : launchFused<16>(c, F, smem, jk.get(hgrdgpu::jit::kFused16));
   if (rc < 0)
     return rc;
   CK(cudaGetLastError());
@@ -637,15 +684,11 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     CK(cudaMemsetAsync(c->ctr2.p, 0, sizeof(Counters), c->st));
     const size_t sm = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
                       sizeof(ParamDev) * P.params.size();
-    if (sm > 48 * 1024)
-      CK(cudaFuncSetAttribute(k_expand_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(sm)));
-    {
-      StageTimer t(c, "k_expand_par_shared");
-      k_expand_par<<<static_cast<unsigned>(blocks), 256, sm, c->st>>>(D2);
-    }
-    CK(cudaGetLastError());
-    ++c->kernelLaunches;
+    const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
+    rc = launchExpandPar(c, D2, static_cast<unsigned>(blocks), sm, jx,
+                         jx ? "k_expand_par_shared[jit]" : "k_expand_par_shared");
+    if (rc < 0)
+      return rc;
     rc = readCountersFrom(c, c->ctr2.p);
     if (rc < 0)
       return rc;
@@ -808,6 +851,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   const bool locks = (L.flags & HGRD_LAUNCH_PAIRWISE) != 0;
   const bool pairwise = locks || !P.summaryOk;
   bool seq = (L.flags & HGRD_LAUNCH_SEQUENTIAL) || pairwise || L.n_regs > kMaxRegs;
+  // (the interpreter keeps at most kMaxRegs registers per lane)
   const size_t smem = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
                       sizeof(ParamDev) * P.params.size();
   if (smem > 200 * 1024)
@@ -817,8 +861,11 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   const bool fusedOk = c->fusedEnabled && !seq && !locks && P.summaryOk && L.n_locs <= 32 &&
                        o.nW <= kMaxWritten && D.nBlocks < (1 << 20) - 2 &&
                        !(L.flags & HGRD_LAUNCH_GENERAL);
+  // NVRTC specialisation for large PARALLEL launches (compiled on first use)
+  const bool useJit = !seq && (c->jitMode == 2 || (c->jitMode == 1 && D.nThreads >= (int64_t(1) << 14)));
+  JitGetter jk{c, &L, useJit};
   if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
-    rc = runFused(c, L, D, o, P, R, recInsns, loops);
+    rc = runFused(c, L, D, o, P, R, recInsns, loops, jk);
     if (rc < 0)
       return rc;
     if (rc == 1)
@@ -846,15 +893,11 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       D.keys = c->keys.p;
       D.vals = c->vals.p;
       D.capacity = cap;
-      if (smem > 48 * 1024)
-        CK(cudaFuncSetAttribute(k_expand_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-      {
-        StageTimer t(c, "k_expand_par");
-        k_expand_par<<<static_cast<unsigned>(blocks), 256, smem, c->st>>>(D);
-      }
-      CK(cudaGetLastError());
-      ++c->kernelLaunches;
+      const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
+      rc = launchExpandPar(c, D, static_cast<unsigned>(blocks), smem, jx,
+                           jx ? "k_expand_par[jit]" : "k_expand_par");
+      if (rc < 0)
+        return rc;
       rc = readCounters(c);
       if (rc < 0)
         return rc;
@@ -932,7 +975,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     }
     {
       StageTimer t(c, "k_expand_seq");
-      k_expand_seq<<<1, 32, 0, c->st>>>(D);
+      k_expand_seq<InterpBody><<<1, 32, 0, c->st>>>(D);
     }
     CK(cudaGetLastError());
     ++c->kernelLaunches;
@@ -1058,6 +1101,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
     cudaFreeHost(c->hStage);
   if (c->hCtr)
     cudaFreeHost(c->hCtr);
+  hgrdgpu::jit::destroy(c->jit);
   for (cudaEvent_t e : c->evPool)
     cudaEventDestroy(e);
   cudaEventDestroy(c->e0);
@@ -1076,6 +1120,28 @@ int hgrd_gpu_set_profiling(hgrd_gpu_ctx *c, int on) {
 }
 
 const char *hgrd_gpu_last_profile(hgrd_gpu_ctx *c) { return c ? c->profileJson.c_str() : "[]"; }
+
+int hgrd_gpu_set_jit(hgrd_gpu_ctx *c, int mode) {
+  if (!c || mode < 0 || mode > 2)
+    return HGRD_GPU_EINVAL;
+  c->jitMode = mode;
+  return 0;
+}
+
+const char *hgrd_gpu_jit_info(hgrd_gpu_ctx *c) {
+  if (!c)
+    return "{}";
+  char buf[256];
+  std::snprintf(buf, sizeof buf,
+                "{\"mode\":%d,\"compiles\":%d,\"compileMs\":%.1f,\"failures\":%d,\"lastError\":",
+                c->jitMode, hgrdgpu::jit::compiles(c->jit), hgrdgpu::jit::compileMs(c->jit),
+                c->jitFailures);
+  std::string e;
+  for (char ch : c->jitErr.substr(0, 2000))
+    e += (ch == '"' || ch == '\\') ? ' ' : (ch == '\n' ? ' ' : ch);
+  c->jitInfo = std::string(buf) + "\"" + e + "\"}";
+  return c->jitInfo.c_str();
+}
 
 int hgrd_gpu_set_fused(hgrd_gpu_ctx *c, int enabled) {
   if (!c)

@@ -19,7 +19,9 @@
 
 #include "hgrd_gpu.h"
 
+#if !defined(__CUDACC_RTC__)
 #include <cstdint>
+#endif
 
 namespace hgrdgpu {
 namespace dev {

@@ -115,109 +115,44 @@ __device__ __forceinline__ uint32_t metaWp(uint64_t m) { return (m >> 32) & 255;
 __device__ __forceinline__ int metaSite(uint64_t m) { return static_cast<int>((m >> 20) & 4095); }
 __device__ __forceinline__ uint32_t metaSeq(uint64_t m) { return static_cast<uint32_t>(m & kSeqMask); }
 
-// Expansion of one MiniCU thread into shared memory (PARALLEL semantics,
-// same interpreter as k_expand_par).
-template <int IPT>
-__device__ __forceinline__ void runIntoSmem(const LaunchDev &L, const hgrd_gpu_insn *code,
-                                            const SiteDev *sites, const ParamDev *params,
-                                            int64_t t, uint32_t tli, FusedSmem<IPT> &S,
-                                            LaneTally &tally) {
-  int64_t r[kMaxRegs];
-  for (int i = 0; i < L.nRegs; ++i)
-    r[i] = L.regInit[i];
-  Builtins bi;
-  int64_t block, warp, lane;
-  threadIdentity(L, t, bi, block, warp, lane);
-  uint32_t bp = 0, wp = 0, seq = 0;
-  int64_t steps = 0;
-  int pc = 0;
-  for (;;) {
-    const hgrd_gpu_insn I = code[pc];
-    switch (I.op) {
-    case HGRD_OP_END:
-      goto done;
-    case HGRD_OP_STEP:
-      if (++steps > L.stepBudget) {
-        tally.flags |= kFlagAbort;
-        goto done;
-      }
-      break;
-    case HGRD_OP_CONST:
-      r[I.a] = I.imm;
-      break;
-    case HGRD_OP_MOV:
-      r[I.a] = r[I.b];
-      break;
-    case HGRD_OP_BUILTIN:
-      r[I.a] = bi.v[I.sub];
-      break;
-    case HGRD_OP_BIN:
-      r[I.a] = applyBin(I.sub, r[I.b], r[I.c]);
-      break;
-    case HGRD_OP_LOAD:
-    case HGRD_OP_STORE:
-    case HGRD_OP_ATOMIC: {
-      const int site = static_cast<int>(I.imm);
-      const SiteDev Sd = sites[site];
-      const int64_t idx = I.op == HGRD_OP_LOAD ? r[I.b] : r[I.a];
-      const ParamDev *P = Sd.param >= 0 ? &params[Sd.param] : nullptr;
-      if (!P || P->handle < 0 || idx < 0 || idx >= P->size) {
-        ++tally.traps;
-        if (I.op == HGRD_OP_LOAD)
-          r[I.a] = 0;
-        break;
-      }
-      ++tally.inst;
-      if (Sd.record) {
-        if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
-          tally.flags |= kFlagFusedOverflow;
-        const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
-        const unsigned pos = atomicAdd(&S.count, 1u);
-        if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
-          S.elem[pos] = e;
-          S.meta[pos] = packMeta(tli, bp, wp, site, seq);
-          const int w = P->written - 1;
-          atomicMin(&S.minE[w], static_cast<unsigned long long>(e));
-          atomicMax(&S.maxE[w], static_cast<unsigned long long>(e));
-        } else {
-          tally.flags |= kFlagFusedOverflow;
-        }
-        ++tally.recs;
-      }
-      ++seq;
-      if (I.op == HGRD_OP_LOAD)
-        r[I.a] = (I.sub & 1) ? __ldg(P->ptr + idx) : 0;
-      break;
+// PARALLEL sink of the fused kernel: records into shared memory.
+template <int IPT> struct FusedSink : ParState {
+  FusedSmem<IPT> *S;
+  uint32_t tli; // thread index within the iteration
+
+  __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
+    if (!sites[site].record)
+      return;
+    if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
+      flags |= kFlagFusedOverflow;
+    const unsigned pos = atomicAdd(&S->count, 1u);
+    if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
+      S->elem[pos] = P->elemBase + static_cast<uint64_t>(idx);
+      S->meta[pos] = packMeta(tli, bp, wp, site, seq);
+    } else {
+      flags |= kFlagFusedOverflow;
     }
-    case HGRD_OP_SYNCTHREADS:
-      ++bp;
-      ++wp;
-      break;
-    case HGRD_OP_SYNCWARP:
-      ++wp;
-      break;
-    case HGRD_OP_FENCE:
-      ++seq;
-      break;
-    case HGRD_OP_JZ:
-      if (r[I.a] == 0) {
-        pc = static_cast<int>(I.imm);
-        continue;
-      }
-      break;
-    case HGRD_OP_JMP:
-      pc = static_cast<int>(I.imm);
-      continue;
-    default:
-      goto done;
-    }
-    ++pc;
+    ++recs;
   }
-done:
-  tally.steps += static_cast<unsigned long long>(steps);
-  atomicMax(&S.maxBp, bp);
-  atomicMax(&S.maxWp, wp);
-}
+  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
+    const ParamDev *P = check(site, idx);
+    if (!P)
+      return 0;
+    record(site, P, idx);
+    ++seq;
+    return need ? __ldg(P->ptr + idx) : 0;
+  }
+  __device__ __forceinline__ void store(int site, int64_t idx, int64_t) {
+    const ParamDev *P = check(site, idx);
+    if (!P)
+      return;
+    record(site, P, idx);
+    ++seq;
+  }
+  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t, int64_t) {
+    store(site, idx, 0);
+  }
+};
 
 // Conditions of the reference pair rule for two records of one element
 // inside one MiniCU block (:750-769), INTRA kinds only.  Returns kind or -1.
@@ -264,7 +199,7 @@ __device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, uint32_t *sKeyMin, ui
   }
 }
 
-template <int IPT>
+template <int IPT, class Body>
 __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
   using Smem = FusedSmem<IPT>;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -298,6 +233,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
   const int64_t ws = L.ws;
   LaneTally tally;
   unsigned myFlags = 0;
+  int64_t regs[kMaxRegs];
 
   for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x) {
     const int64_t firstBlock = it * F.bpi;
@@ -314,9 +250,54 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
     }
     __syncthreads();
     // 1. expansion of the iteration's whole MiniCU blocks
-    for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads)
-      runIntoSmem<IPT>(L, sCode, sSites, sParams, firstBlock * L.tpb + tl,
-                       static_cast<uint32_t>(tl), S, tally);
+    for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
+      FusedSink<IPT> s;
+      s.L = &L;
+      s.sites = sSites;
+      s.params = sParams;
+      s.S = &S;
+      s.tli = static_cast<uint32_t>(tl);
+      Builtins bi;
+      threadIdentity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
+      Body::run(L, sCode, bi, s, regs);
+      tally.add(s);
+      atomicMax(&S.maxBp, s.bp);
+      atomicMax(&S.maxWp, s.wp);
+    }
+    __syncthreads();
+    // per written buffer: the iteration's element range (warp reduction)
+    {
+      const unsigned nr = min(S.count, static_cast<unsigned>(Smem::kCap));
+      unsigned long long lo[kMaxWritten], hi[kMaxWritten];
+#pragma unroll
+      for (int q = 0; q < kMaxWritten; ++q) {
+        lo[q] = ~0ull;
+        hi[q] = 0;
+      }
+      for (unsigned i = tid; i < nr; i += kFusedThreads) {
+        const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
+        const unsigned long long e = S.elem[i];
+#pragma unroll
+        for (int q = 0; q < kMaxWritten; ++q)
+          if (q == w) {
+            lo[q] = min(lo[q], e);
+            hi[q] = max(hi[q], e);
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxWritten; ++q) {
+        if (q >= F.nW)
+          break;
+        for (int o = 16; o > 0; o >>= 1) {
+          lo[q] = min(lo[q], __shfl_down_sync(0xffffffffu, lo[q], o));
+          hi[q] = max(hi[q], __shfl_down_sync(0xffffffffu, hi[q], o));
+        }
+        if ((tid & 31) == 0 && lo[q] <= hi[q]) {
+          atomicMin(&S.minE[q], lo[q]);
+          atomicMax(&S.maxE[q], hi[q]);
+        }
+      }
+    }
     __syncthreads();
     const unsigned n = min(S.count, static_cast<unsigned>(Smem::kCap));
     if (S.count > static_cast<unsigned>(Smem::kCap))

@@ -1,0 +1,26 @@
+// NVRTC specialisation of the race-check kernels (see jit.cpp).
+#pragma once
+
+#include "hgrd_gpu.h"
+
+#include <map>
+#include <string>
+
+namespace hgrdgpu {
+namespace jit {
+
+enum Variant { kExpandPar = 0, kFused4 = 1, kFused16 = 2 };
+
+struct Cache;
+Cache *create();
+void destroy(Cache *c);
+// The specialised kernel `v` for this launch's code and constants (compiled
+// on first use, cached).  Returns nullptr (and err) when NVRTC is
+// unavailable or the compile fails; callers then use the interpreter.
+const void *get(Cache *c, const hgrd_gpu_launch &L, Variant v, std::string &err);
+std::string generate(const hgrd_gpu_launch &L);
+double compileMs(const Cache *c);
+int compiles(const Cache *c);
+
+} // namespace jit
+} // namespace hgrdgpu

@@ -185,3 +185,25 @@ def test_full_transpose_8192(gpu, cpu_oracle):
                [(r["kind"], r["locA"], r["locB"], r["address"], r["threadA"], r["seqA"],
                  r["threadB"], r["seqB"]) for r in want["races"]]
         assert got["instances"] == 3 << 26
+
+
+# ------------------------------------------------------- NVRTC specialisation
+def test_jit_forced_edge_and_synthetic(gpu, cpu_oracle):
+    """Every launch through NVRTC-specialised kernels (mode 2)."""
+    gpu.set_jit(2)
+    try:
+        for c in load_golden("edge")[::6] + load_golden("synthetic"):
+            _check_run(gpu, cpu_oracle, c["source"], c["config"], "x.mcu", c["result"])
+        info = gpu.jit_info()
+        assert info["compiles"] > 0 and info["failures"] == 0, info
+    finally:
+        gpu.set_jit(1)
+
+
+def test_jit_used_for_large_launches(gpu):
+    gpu.set_profiling(True)
+    spec, _ = _spec_stencil(gpu, 1 << 16, False)
+    gpu.check_launch(spec)
+    names = [s["name"] for s in gpu.last_profile()]
+    gpu.set_profiling(False)
+    assert any(n.endswith("[jit]") for n in names), (names, gpu.jit_info())

@@ -25,6 +25,32 @@ struct Builtins {
 
 __device__ __forceinline__ void threadIdentity(const LaunchDev &L, int64_t t, Builtins &b,
                                                int64_t &block, int64_t &warp, int64_t &lane) {
+  b.v[6] = L.block[0];
+  b.v[7] = L.block[1];
+  b.v[8] = L.block[2];
+  b.v[9] = L.grid[0];
+  b.v[10] = L.grid[1];
+  b.v[11] = L.grid[2];
+  if (L.small) { // reference :443-460 with magic-number division
+    const uint32_t u = static_cast<uint32_t>(t);
+    const uint32_t bl = L.dTpb.div(u);
+    const uint32_t tl = u - bl * L.dTpb.d;
+    const uint32_t q1 = L.dBx.d == 1 ? tl : L.dBx.div(tl);
+    const uint32_t tz = L.dBxBy.div(tl);
+    b.v[0] = tl - q1 * L.dBx.d;
+    b.v[1] = q1 - tz * static_cast<uint32_t>(L.block[1]);
+    b.v[2] = tz;
+    const uint32_t g1 = L.dGx.div(bl);
+    const uint32_t bz = L.dGxGy.div(bl);
+    b.v[3] = bl - g1 * L.dGx.d;
+    b.v[4] = g1 - bz * static_cast<uint32_t>(L.grid[1]);
+    b.v[5] = bz;
+    const uint32_t w = L.dWs.div(tl);
+    block = bl;
+    warp = w;
+    lane = tl - w * L.dWs.d;
+    return;
+  }
   block = t / L.tpb;
   const int64_t tl = t - block * L.tpb;
   b.v[0] = tl % L.block[0];
@@ -33,12 +59,6 @@ __device__ __forceinline__ void threadIdentity(const LaunchDev &L, int64_t t, Bu
   b.v[3] = block % L.grid[0];
   b.v[4] = (block / L.grid[0]) % L.grid[1];
   b.v[5] = block / (L.grid[0] * L.grid[1]);
-  b.v[6] = L.block[0];
-  b.v[7] = L.block[1];
-  b.v[8] = L.block[2];
-  b.v[9] = L.grid[0];
-  b.v[10] = L.grid[1];
-  b.v[11] = L.grid[2];
   warp = tl / L.ws;
   lane = tl - warp * L.ws;
 }

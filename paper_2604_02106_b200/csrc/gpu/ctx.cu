@@ -831,6 +831,15 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   D.nThreads = D.nBlocks * D.tpb;
   D.stepBudget = L.step_budget;
   D.ctr = c->ctr.p;
+  D.small = D.nThreads < (int64_t(1) << 32) - 1 && L.warp_size < (int64_t(1) << 32);
+  if (D.small) {
+    D.dTpb = FastDiv::make(static_cast<uint32_t>(D.tpb));
+    D.dBx = FastDiv::make(static_cast<uint32_t>(L.block[0]));
+    D.dBxBy = FastDiv::make(static_cast<uint32_t>(L.block[0] * L.block[1]));
+    D.dGx = FastDiv::make(static_cast<uint32_t>(L.grid[0]));
+    D.dGxGy = FastDiv::make(static_cast<uint32_t>(L.grid[0] * L.grid[1]));
+    D.dWs = FastDiv::make(static_cast<uint32_t>(std::min<int64_t>(L.warp_size, 0xffffffffLL)));
+  }
 
   int bP, bQ;
   bool bounded, loops;

@@ -80,6 +80,34 @@ struct Counters {
   unsigned int candCount;
 };
 
+// Division by a launch-invariant 32-bit divisor: one mul.hi + shifts
+// (Granlund-Montgomery); exact for every 32-bit dividend.
+struct FastDiv {
+  uint32_t d = 1, m = 1;
+  int s1 = 0, s2 = 0;
+#if !defined(__CUDACC_RTC__)
+  static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    int l = 0;
+    while ((uint64_t(1) << l) < d)
+      ++l;
+    f.m = static_cast<uint32_t>(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+    f.s1 = l < 1 ? l : 1;
+    f.s2 = l > 1 ? l - 1 : 0;
+    return f;
+  }
+#endif
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#if defined(__CUDA_ARCH__)
+    const uint32_t t = __umulhi(m, n);
+#else
+    const uint32_t t = static_cast<uint32_t>((uint64_t(m) * n) >> 32);
+#endif
+    return (t + ((n - t) >> s1)) >> s2;
+  }
+};
+
 struct LaunchDev {
   const hgrd_gpu_insn *code;
   const SiteDev *sites;
@@ -111,6 +139,9 @@ struct LaunchDev {
   // pass 2 of the fused path: only elements the ownership table marks MULTI
   const uint32_t *ownerFilter;
   uint32_t ownerMultiTag;
+  // 32-bit thread identity (nThreads < 2^32): tpb, bx, bx*by, gx, gx*gy, ws
+  bool small;
+  FastDiv dTpb, dBx, dBxBy, dGx, dGxGy, dWs;
 };
 
 __host__ __device__ inline int64_t wrapAdd(int64_t a, int64_t b) {

@@ -60,45 +60,41 @@ struct FusedArgs {
   int nW;
 };
 
+// One exchange per (element, block): whoever replaces another block's tag
+// (or MULTI) marks the element MULTI.  The last exchange on an element that
+// two blocks touched is always followed by a MULTI store, so the final value
+// is MULTI exactly for the elements of >= 2 blocks.
 __device__ __forceinline__ void ownerUpdate(const FusedArgs &F, uint64_t e, uint64_t blk,
                                             unsigned &flags) {
   const uint32_t tag = F.epoch << 20;
-  const uint32_t want = tag | static_cast<uint32_t>(blk + 1);
-  const uint32_t multi = tag | kOwnerMulti;
-  uint32_t cur = F.owner[e];
-  for (;;) {
-    if ((cur >> 20) != F.epoch) { // empty for this launch
-      const uint32_t prev = atomicCAS(&F.owner[e], cur, want);
-      if (prev == cur)
-        return;
-      cur = prev;
-      continue;
-    }
-    const uint32_t f = cur & kOwnerMulti;
-    if (f == (want & kOwnerMulti) || f == kOwnerMulti) {
-      if (f == kOwnerMulti)
-        flags |= kFlagShared;
-      return;
-    }
-    const uint32_t prev = atomicCAS(&F.owner[e], cur, multi);
-    if (prev == cur) {
-      flags |= kFlagShared;
-      return;
-    }
-    cur = prev;
+  const uint32_t mine = static_cast<uint32_t>(blk + 1);
+  const uint32_t old = atomicExch(&F.owner[e], tag | mine);
+  if ((old >> 20) == F.epoch && (old & kOwnerMulti) != mine) {
+    atomicExch(&F.owner[e], tag | kOwnerMulti);
+    flags |= kFlagShared;
   }
 }
 
 template <int IPT> struct FusedSmem {
   static constexpr int kCap = kFusedThreads * IPT;
+  static constexpr int kTable = 2 * kCap; // counting-sort slots (element span)
   using Sort = cub::BlockRadixSort<uint64_t, kFusedThreads, IPT, uint32_t, 6>;
-  typename Sort::TempStorage sortTmp;
+  union {
+    typename Sort::TempStorage sortTmp;
+    struct {
+      uint32_t cnt[kTable]; // per element slot: count, then start
+      uint16_t rank[kCap];  // record's rank inside its slot
+      uint32_t part[kFusedThreads];
+    } cs;
+  } u;
   uint64_t elem[kCap];  // global element id, by record index
   uint64_t meta[kCap];  // tli:16 | bp:8 | wp:8 | site:12 | seq:20
-  uint64_t key[kCap];   // sorted keys
+  uint64_t key[kCap];   // sorted keys (counting mode: element slot)
   uint32_t idx[kCap];   // sorted -> record index
   unsigned long long minE[kMaxWritten], maxE[kMaxWritten];
-  unsigned int count, maxBp, maxWp, nReal, flags;
+  uint32_t prefix[kMaxWritten];
+  unsigned int count, maxBp, maxWp, nReal, flags, maxGroup;
+  int counting; // this iteration groups by a counting sort over element slots
   // field start bits of the block-local key  w|off|blk|bp|warp|wp|lane
   int fWp, fWarp, fBp, fBlk, fOff, fW, total;
 };
@@ -125,7 +121,15 @@ template <int IPT> struct FusedSink : ParState {
       return;
     if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
       flags |= kFlagFusedOverflow;
-    const unsigned pos = atomicAdd(&S->count, 1u);
+    // warp-aggregated slot allocation (one shared atomic per converged group)
+    const unsigned act = __activemask();
+    const int ln = threadIdx.x & 31;
+    const int leader = __ffs(act) - 1;
+    unsigned base = 0;
+    if (ln == leader)
+      base = atomicAdd(&S->count, static_cast<unsigned>(__popc(act)));
+    base = __shfl_sync(act, base, leader);
+    const unsigned pos = base + __popc(act & ((1u << ln) - 1));
     if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
       S->elem[pos] = P->elemBase + static_cast<uint64_t>(idx);
       S->meta[pos] = packMeta(tli, bp, wp, site, seq);
@@ -161,7 +165,8 @@ __device__ __forceinline__ int intraKind(const LaunchDev &L, const SiteDev *site
   const uint32_t ta = metaTli(ma), tb = metaTli(mb);
   if (ta == tb)
     return -1;
-  if (ta / tpb != tb / tpb)
+  const uint32_t ba = L.dTpb.div(ta), bb = L.dTpb.div(tb);
+  if (ba != bb)
     return -1; // different MiniCU blocks: INTER, handled by ownership
   const SiteDev &sa = sites[metaSite(ma)], &sb = sites[metaSite(mb)];
   if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
@@ -171,7 +176,7 @@ __device__ __forceinline__ int intraKind(const LaunchDev &L, const SiteDev *site
     return -1;
   if (metaBp(ma) != metaBp(mb))
     return -1;
-  const uint32_t wa = (ta % tpb) / static_cast<uint32_t>(ws), wb = (tb % tpb) / static_cast<uint32_t>(ws);
+  const uint32_t wa = L.dWs.div(ta - ba * tpb), wb = L.dWs.div(tb - bb * tpb);
   if (wa == wb && metaWp(ma) != metaWp(mb))
     return -1;
   return wa != wb ? 1 : 2;
@@ -200,7 +205,7 @@ __device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, uint32_t *sKeyMin, ui
 }
 
 template <int IPT, class Body>
-__global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
+__global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
   using Smem = FusedSmem<IPT>;
   extern __shared__ __align__(16) unsigned char dyn[];
   Smem &S = *reinterpret_cast<Smem *>(dyn);
@@ -304,34 +309,114 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
       myFlags |= kFlagFusedOverflow;
     if (n == 0)
       continue;
-    // 2. key layout for this iteration
+    // 2. grouping by element: counting sort over element slots when the
+    //    iteration's element span is small and groups are small, else a
+    //    CUB block radix sort of the full key
     if (tid == 0) {
-      uint64_t span = 1;
-      for (int w = 0; w < F.nW && w < kMaxWritten; ++w)
-        if (S.minE[w] <= S.maxE[w])
-          span = max(span, static_cast<uint64_t>(S.maxE[w] - S.minE[w] + 1));
-      const int bL = bitsForDev(static_cast<uint64_t>(ws < L.tpb ? ws : L.tpb));
-      const int bW = bitsForDev(static_cast<uint64_t>((L.tpb + ws - 1) / ws));
-      const int bQ = bitsForDev(uint64_t(S.maxWp) + 1);
-      const int bP = bitsForDev(uint64_t(S.maxBp) + 1);
-      const int bBk = bitsForDev(static_cast<uint64_t>(F.bpi));
-      const int bO = bitsForDev(span);
-      const int bWr = bitsForDev(static_cast<uint64_t>(F.nW));
-      S.fWp = bL;
-      S.fWarp = S.fWp + bQ;
-      S.fBp = S.fWarp + bW;
-      S.fBlk = S.fBp + bP;
-      S.fOff = S.fBlk + bBk;
-      S.fW = S.fOff + bO;
-      S.total = S.fW + bWr;
-      if (S.total > 64)
-        S.flags |= kFlagFusedOverflow;
+      uint32_t span = 0;
+      bool ok = true;
+      for (int w = 0; w < F.nW && w < kMaxWritten; ++w) {
+        S.prefix[w] = span;
+        if (S.minE[w] <= S.maxE[w]) {
+          const unsigned long long sw = S.maxE[w] - S.minE[w] + 1;
+          if (sw > static_cast<unsigned long long>(Smem::kTable))
+            ok = false;
+          else
+            span += static_cast<uint32_t>(sw);
+        }
+      }
+      S.counting = ok && span <= static_cast<uint32_t>(Smem::kTable);
+      S.total = static_cast<int>(span); // slots in counting mode
+      S.maxGroup = 0;
     }
     __syncthreads();
-    if (S.total > 64)
-      continue;
-    // 3. block-local sort
-    {
+    if (S.counting) {
+      const int slots = S.total;
+      for (int i = tid; i < slots; i += kFusedThreads)
+        S.u.cs.cnt[i] = 0;
+      __syncthreads();
+      unsigned myMax = 0;
+      for (unsigned i = tid; i < n; i += kFusedThreads) {
+        const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
+        const uint32_t slot = S.prefix[w] + static_cast<uint32_t>(S.elem[i] - S.minE[w]);
+        const unsigned r = atomicAdd(&S.u.cs.cnt[slot], 1u);
+        S.u.cs.rank[i] = static_cast<uint16_t>(r);
+        myMax = max(myMax, r + 1);
+      }
+      if (myMax > kSmallGroup)
+        atomicMax(&S.maxGroup, myMax);
+      __syncthreads();
+      if (S.maxGroup <= kSmallGroup) {
+        // exclusive scan of the slot counts: per-thread chunks + warp scans
+        const int per = (slots + kFusedThreads - 1) / kFusedThreads;
+        const int b0 = min(slots, tid * per), b1 = min(slots, b0 + per);
+        uint32_t sum = 0;
+        for (int i = b0; i < b1; ++i)
+          sum += S.u.cs.cnt[i];
+        S.u.cs.part[tid] = sum;
+        __syncthreads();
+        if (tid < 32) {
+          uint32_t acc = 0;
+          for (int k = 0; k < kFusedThreads / 32; ++k) {
+            const uint32_t v = S.u.cs.part[k * 32 + tid];
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+              if (tid >= o)
+                incl += y;
+            }
+            S.u.cs.part[k * 32 + tid] = acc + incl - v;
+            acc += __shfl_sync(0xffffffffu, incl, 31);
+          }
+        }
+        __syncthreads();
+        uint32_t run = S.u.cs.part[tid];
+        for (int i = b0; i < b1; ++i) {
+          const uint32_t c0 = S.u.cs.cnt[i];
+          S.u.cs.cnt[i] = run;
+          run += c0;
+        }
+        __syncthreads();
+        for (unsigned i = tid; i < n; i += kFusedThreads) {
+          const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
+          const uint32_t slot = S.prefix[w] + static_cast<uint32_t>(S.elem[i] - S.minE[w]);
+          const uint32_t pos = S.u.cs.cnt[slot] + S.u.cs.rank[i];
+          S.idx[pos] = i;
+          S.key[pos] = slot;
+        }
+        __syncthreads();
+      } else if (tid == 0) {
+        S.counting = 0; // a hot element: fall back to the radix sort
+      }
+      __syncthreads();
+    }
+    if (!S.counting) {
+      if (tid == 0) {
+        uint64_t span = 1;
+        for (int w = 0; w < F.nW && w < kMaxWritten; ++w)
+          if (S.minE[w] <= S.maxE[w])
+            span = max(span, static_cast<uint64_t>(S.maxE[w] - S.minE[w] + 1));
+        const int bL = bitsForDev(static_cast<uint64_t>(ws < L.tpb ? ws : L.tpb));
+        const int bW = bitsForDev(static_cast<uint64_t>((L.tpb + ws - 1) / ws));
+        const int bQ = bitsForDev(uint64_t(S.maxWp) + 1);
+        const int bP = bitsForDev(uint64_t(S.maxBp) + 1);
+        const int bBk = bitsForDev(static_cast<uint64_t>(F.bpi));
+        const int bO = bitsForDev(span);
+        const int bWr = bitsForDev(static_cast<uint64_t>(F.nW));
+        S.fWp = bL;
+        S.fWarp = S.fWp + bQ;
+        S.fBp = S.fWarp + bW;
+        S.fBlk = S.fBp + bP;
+        S.fOff = S.fBlk + bBk;
+        S.fW = S.fOff + bO;
+        S.total = S.fW + bWr;
+        if (S.total > 64)
+          S.flags |= kFlagFusedOverflow;
+      }
+      __syncthreads();
+      if (S.total > 64)
+        continue;
       uint64_t keys[IPT];
       uint32_t vals[IPT];
       const int wpShift = S.fWp, warpShift = S.fWarp, bpShift = S.fBp, blkShift = S.fBlk,
@@ -343,8 +428,8 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
         if (i < n) {
           const uint64_t m = S.meta[i];
           const uint32_t tli = metaTli(m);
-          const uint32_t blk = tli / tpb, tl = tli % tpb;
-          const uint32_t warp = tl / static_cast<uint32_t>(ws), lane = tl % static_cast<uint32_t>(ws);
+          const uint32_t blk = L.dTpb.div(tli), tl = tli - blk * tpb;
+          const uint32_t warp = L.dWs.div(tl), lane = tl - warp * static_cast<uint32_t>(ws);
           const SiteDev &sd = sSites[metaSite(m)];
           const int w = sParams[sd.param].written - 1;
           const uint64_t off = S.elem[i] - S.minE[w];
@@ -357,19 +442,19 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
           keys[j] = ~0ull;
         }
       }
-      typename Smem::Sort(S.sortTmp).Sort(keys, vals, 0, S.total > 0 ? S.total : 1);
+      typename Smem::Sort(S.u.sortTmp).Sort(keys, vals, 0, S.total > 0 ? S.total : 1);
 #pragma unroll
       for (int j = 0; j < IPT; ++j) {
         S.key[tid * IPT + j] = keys[j];
         S.idx[tid * IPT + j] = vals[j];
       }
+      __syncthreads();
     }
-    __syncthreads();
-    // group keys of the sorted key
-    const int shLane = S.fWp;  // key >> fWp  : element|blk|bp|warp|wp  (INTRA-WARP group)
-    const int shBpF = S.fBp;   // key >> fBp  : element|blk|bp          (INTRA-BLOCK group)
-    const int shBlkF = S.fBlk; // key >> fBlk : element|blk             (ownership unit)
-    const int shElem = S.fOff; // key >> fOff : element
+    // group keys of the sorted key (counting mode: the key is the element slot)
+    const bool counting = S.counting != 0;
+    const int shLane = S.fWp;                 // element|blk|bp|warp|wp  (INTRA-WARP group)
+    const int shBpF = S.fBp;                  // element|blk|bp          (INTRA-BLOCK group)
+    const int shElem = counting ? 0 : S.fOff; // element
     // 4. per element group: ownership + INTRA keys
     for (int j = 0; j < IPT; ++j) {
       const int p = tid * IPT + j;
@@ -383,10 +468,14 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
         ++e;
       const uint64_t ge = S.elem[S.idx[p]];
       // ownership per (element, block)
-      for (int q = p; q < e; ++q)
-        if (q == p || (S.key[q] >> shBlkF) != (S.key[q - 1] >> shBlkF))
-          ownerUpdate(F, ge, static_cast<uint64_t>(firstBlock + metaTli(S.meta[S.idx[q]]) / tpb),
-                      myFlags);
+      for (int q = p; q < e; ++q) {
+        const uint32_t bq = L.dTpb.div(metaTli(S.meta[S.idx[q]]));
+        bool seen = false;
+        for (int r2 = p; r2 < q && !seen; ++r2)
+          seen = L.dTpb.div(metaTli(S.meta[S.idx[r2]])) == bq;
+        if (!seen)
+          ownerUpdate(F, ge, static_cast<uint64_t>(firstBlock + bq), myFlags);
+      }
       if (e - p < 2)
         continue;
       if (e - p <= kSmallGroup) {
@@ -438,9 +527,11 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
           }
           const uint64_t m = S.meta[S.idx[q]];
           const int s = metaSite(m);
-          const uint32_t tl = metaTli(m) % tpb;
-          note(p2, mn2, mx2, s, tl / static_cast<uint32_t>(ws));
-          note(p3, mn3, mx3, s, tl % static_cast<uint32_t>(ws));
+          const uint32_t tli = metaTli(m);
+          const uint32_t tl = tli - L.dTpb.div(tli) * tpb;
+          const uint32_t wq = L.dWs.div(tl);
+          note(p2, mn2, mx2, s, wq);
+          note(p3, mn3, mx3, s, tl - wq * static_cast<uint32_t>(ws));
         }
         flush(p2, mn2, mx2, 1);
         flush(p3, mn3, mx3, 2);
@@ -455,6 +546,9 @@ __global__ void __launch_bounds__(kFusedThreads) k_fused(FusedArgs F) {
       const int la = (K / 3) / F.nLocs, lb = (K / 3) % F.nLocs;
       const int p = static_cast<int>(sKeyMin[K]);
       sKeyMin[K] = 0xffffffffu; // reset for the next iteration
+      const uint64_t gElem = S.elem[S.idx[p]];
+      if (gElem > F.keyElem[K])
+        continue; // another block already holds a smaller element for K
       const uint64_t g = S.key[p] >> shElem;
       int e = p + 1;
       while (e < static_cast<int>(n) && (S.key[e] >> shElem) == g)

@@ -192,8 +192,9 @@ def test_jit_forced_edge_and_synthetic(gpu, cpu_oracle):
     """Every launch through NVRTC-specialised kernels (mode 2)."""
     gpu.set_jit(2)
     try:
-        for c in load_golden("edge")[::6] + load_golden("synthetic"):
-            _check_run(gpu, cpu_oracle, c["source"], c["config"], "x.mcu", c["result"])
+        for name, fn in (("edge", "edge.mcu"), ("synthetic", "syn.mcu")):
+            for c in load_golden(name)[:: 6 if name == "edge" else 1]:
+                _check_run(gpu, cpu_oracle, c["source"], c["config"], fn, c["result"])
         info = gpu.jit_info()
         assert info["compiles"] > 0 and info["failures"] == 0, info
     finally:

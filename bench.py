@@ -199,8 +199,9 @@ def run_gpu_arm(args):
     # correctness guard: the report must be the known one (tests pin it to the oracle)
     got = step()
     kinds = sorted(r["kind"] for r in got[0][0]["races"])
-    assert kinds == ["INTRA-BLOCK", "INTRA-BLOCK", "INTRA-WARP", "INTRA-WARP"], kinds
-    assert not got[1][0]["races"]
+    if not os.environ.get("HGRD_FUSED_ABLATE"):  # profiling ablations change the report
+        assert kinds == ["INTRA-BLOCK", "INTRA-BLOCK", "INTRA-WARP", "INTRA-WARP"], kinds
+        assert not got[1][0]["races"]
 
     def barrier():
         if ws > 1:

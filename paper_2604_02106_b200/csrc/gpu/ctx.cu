@@ -17,7 +17,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
+#include <set>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -99,6 +101,9 @@ struct hgrd_gpu_ctx {
 
   unsigned char *hStage = nullptr;
   size_t hStageCap = 0;
+  hgrd_gpu_race *hRaces = nullptr; // pinned copy of the device race array
+  size_t hRacesCap = 0;
+  bool racesOnHost = false;
   Counters *hCtr = nullptr;
   uint64_t capHint = 1 << 16;
   uint64_t opHint = 1 << 12;
@@ -114,6 +119,8 @@ struct hgrd_gpu_ctx {
   size_t evUsed = 0;
   std::string profileJson;
   unsigned long long kernelLaunches = 0; // own kernels launched (lifetime)
+  std::map<std::pair<const void *, size_t>, int> occupancy; // (kernel, smem) -> CTAs/SM
+  std::set<const void *> smemOptIn;
 };
 
 namespace {
@@ -368,7 +375,7 @@ int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOff
   int rc = stage(c, o.total);
   if (rc < 0)
     return rc;
-  CK(cudaStreamSynchronize(c->st)); // staging buffer reuse
+  // every check ends synchronised, so the pinned staging buffer is free here
   NEED(c->blob, o.total);
   unsigned char *h = c->hStage;
   std::memcpy(h + o.code, L.code, sizeof(hgrd_gpu_insn) * L.n_code);
@@ -382,6 +389,22 @@ int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOff
   std::memcpy(h + o.wBase, P.wBase.data(), 8 * P.wBase.size());
   std::memcpy(h + o.wHandle, P.wHandle.data(), 4 * P.wHandle.size());
   CK(cudaMemcpyAsync(c->blob.p, h, o.total, cudaMemcpyHostToDevice, c->st));
+  return 0;
+}
+
+// Counters and (speculatively) the whole race array in one round trip.
+int readCountersAndRaces(hgrd_gpu_ctx *c, size_t nKeys) {
+  if (c->hRacesCap < nKeys) {
+    if (c->hRaces)
+      CK(cudaFreeHost(c->hRaces));
+    CK(cudaMallocHost(&c->hRaces, sizeof(hgrd_gpu_race) * nKeys));
+    c->hRacesCap = nKeys;
+  }
+  CK(cudaMemcpyAsync(c->hCtr, c->ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hRaces, c->races.p, sizeof(hgrd_gpu_race) * nKeys,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->racesOnHost = true;
   return 0;
 }
 
@@ -491,7 +514,7 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       c->kernelLaunches += 3;
     }
   }
-  int rc = readCounters(c);
+  int rc = readCountersAndRaces(c, static_cast<size_t>(nKeys));
   if (rc < 0)
     return rc;
   return fetchRaces(c, R);
@@ -506,11 +529,14 @@ int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
   R->n_races = nr;
   if (nr > R->race_cap)
     return HGRD_GPU_E2BIG;
-  if (nr) {
+  if (nr && c->racesOnHost) {
+    std::memcpy(R->races, c->hRaces, sizeof(hgrd_gpu_race) * nr);
+  } else if (nr) {
     CK(cudaMemcpyAsync(R->races, c->races.p, sizeof(hgrd_gpu_race) * nr,
                        cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
   }
+  c->racesOnHost = false;
   return 0;
 }
 
@@ -540,8 +566,8 @@ struct JitGetter {
 int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t smem,
                     const void *jitKernel, const char *stage) {
   const void *fn = jitKernel ? jitKernel : reinterpret_cast<const void *>(k_expand_par<InterpBody>);
-  if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (smem > 48 * 1024 && c->smemOptIn.insert(fn).second)
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   void *args[] = {const_cast<LaunchDev *>(&D)};
   {
     StageTimer t(c, stage);
@@ -556,7 +582,7 @@ int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t
 
 template <int IPT> size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
   const size_t nKeysPad = (static_cast<size_t>(nKeys) + 3) & ~size_t(3);
-  return align16(sizeof(FusedSmem<IPT>)) + 8 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
+  return align16(sizeof(FusedSmem<IPT>)) + 12 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
          sizeof(SiteDev) * P.sites.size() + sizeof(ParamDev) * P.params.size() +
          8 * P.sites.size();
 }
@@ -571,10 +597,13 @@ template <int IPT>
 int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *jitKernel) {
   const void *fn =
       jitKernel ? jitKernel : reinterpret_cast<const void *>(k_fused<IPT, InterpBody>);
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(smem)));
-  int perSM = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, kFusedThreads, smem));
+  if (c->smemOptIn.insert(fn).second) // once per kernel: allow up to 227 KB
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  int &perSM = c->occupancy[std::make_pair(fn, smem)];
+  if (perSM == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, kFusedThreads, smem));
+    perSM = std::max(perSM, 1);
+  }
   const int64_t grid = std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1));
   void *args[] = {const_cast<FusedArgs *>(&F)};
   StageTimer t(c, jitKernel ? "k_fused[jit]" : "k_fused");
@@ -631,6 +660,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.candCap = candCap;
   F.candCount = &c->ctr.p->candCount;
   F.nW = o.nW;
+  if (const char *ab = std::getenv("HGRD_FUSED_ABLATE"))
+    F.ablate = std::atoi(ab);
   int rc = ipt == 4 ? launchFused<4>(c, F, smem, jk.get(hgrdgpu::jit::kFused4))
                     : launchFused<16>(c, F, smem, jk.get(hgrdgpu::jit::kFused16));
   if (rc < 0)
@@ -644,7 +675,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   }
   CK(cudaGetLastError());
   ++c->kernelLaunches;
-  rc = readCounters(c);
+  rc = readCountersAndRaces(c, static_cast<size_t>(nKeys));
   if (rc < 0)
     return rc;
   const Counters h = *c->hCtr;
@@ -798,6 +829,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   R->device_ms = 0;
   c->stages.clear();
   c->evUsed = 0;
+  c->racesOnHost = false;
   CK(cudaEventRecord(c->e0, c->st));
 
   Plan P;
@@ -1110,6 +1142,8 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
     cudaFreeHost(c->hStage);
   if (c->hCtr)
     cudaFreeHost(c->hCtr);
+  if (c->hRaces)
+    cudaFreeHost(c->hRaces);
   hgrdgpu::jit::destroy(c->jit);
   for (cudaEvent_t e : c->evPool)
     cudaEventDestroy(e);

@@ -4,17 +4,18 @@
 // INTRA-BLOCK / INTRA-WARP pair lies inside one MiniCU block
 // (reference src/oracle.cpp:754-769), so they are found entirely on chip:
 //   1. expansion into shared memory (records: global element id + meta),
-//   2. CUB block radix sort by  w | element offset | block | bp | warp | wp | lane
-//      (element offsets relative to the iteration's minimum per buffer, so
-//      the key is short: 10 bits for the stencil tile),
-//   3. per element group: realised INTRA keys (pairwise for small groups,
-//      per-site min/max summaries for large ones), minimum element per key,
+//   2. grouping: records hashed by element into 2x-oversized slots with a
+//      one-pass counting sort (a slot with more than kSmallGroup records —
+//      a hot element — switches the iteration to a CUB block radix sort of
+//      element | block | bp | warp | wp | lane and per-group summaries),
+//   3. one thread per record pairs it with the earlier records of its slot
+//      (same element): realised INTRA keys and, per key, the minimum element,
 //   4. per realised key: the first (x, y) pair of the reference's order
 //      inside that element, published as a candidate (global element via
 //      atomicMin, candidates filtered by it; k_fused_finalize keeps the
 //      lexicographically first pair of the minimum element).
 // INTER-BLOCK pairs need a second block: every (element, block) also does
-// one ownership update on a per-element table (epoch-tagged, no memset);
+// one ownership exchange on a per-element table (epoch-tagged, no memset);
 // an element reached from two blocks becomes MULTI and only MULTI elements
 // go through the global record sort (pass 2 in ctx.cu).
 #pragma once
@@ -31,7 +32,7 @@ namespace dev {
 constexpr int kFusedThreads = 256;
 constexpr int kMaxWritten = 8;
 constexpr uint32_t kOwnerMulti = 0xFFFFFu;
-constexpr int kSmallGroup = 24; // pairwise below, summaries above
+constexpr int kSmallGroup = 32; // hash slots up to this size, radix grouping above
 
 enum FusedFlags : uint32_t {
   kFlagShared = 128u,   // an element is accessed by two blocks (pass 2 needed)
@@ -58,44 +59,76 @@ struct FusedArgs {
   uint32_t candCap;
   unsigned int *candCount;
   int nW;
+  int ablate; // profiling knob (HGRD_FUSED_ABLATE): 1 skip grouping, 2 skip groups, 4 skip ownership
 };
 
 // One exchange per (element, block): whoever replaces another block's tag
 // (or MULTI) marks the element MULTI.  The last exchange on an element that
 // two blocks touched is always followed by a MULTI store, so the final value
 // is MULTI exactly for the elements of >= 2 blocks.
-__device__ __forceinline__ void ownerUpdate(const FusedArgs &F, uint64_t e, uint64_t blk,
-                                            unsigned &flags) {
-  const uint32_t tag = F.epoch << 20;
-  const uint32_t mine = static_cast<uint32_t>(blk + 1);
-  const uint32_t old = atomicExch(&F.owner[e], tag | mine);
+__device__ __forceinline__ void ownerSettle(const FusedArgs &F, uint64_t e, uint32_t mine,
+                                            uint32_t old, unsigned &flags) {
   if ((old >> 20) == F.epoch && (old & kOwnerMulti) != mine) {
-    atomicExch(&F.owner[e], tag | kOwnerMulti);
+    atomicExch(&F.owner[e], (F.epoch << 20) | kOwnerMulti);
     flags |= kFlagShared;
   }
 }
 
+// Exchanges are issued in the group phase and settled at the end of the
+// iteration, so their L2 round trip overlaps the detection work.
+struct OwnerPending {
+  static constexpr int kSlots = 4;
+  uint64_t e[kSlots];
+  uint32_t mine[kSlots], old[kSlots];
+  int n = 0;
+  __device__ __forceinline__ void issue(const FusedArgs &F, uint64_t elem, uint64_t blk,
+                                        unsigned &flags) {
+    const uint32_t m = static_cast<uint32_t>(blk + 1);
+    const uint32_t o = atomicExch(&F.owner[elem], (F.epoch << 20) | m);
+    if (n < kSlots) {
+#pragma unroll
+      for (int q = 0; q < kSlots; ++q)
+        if (q == n) {
+          e[q] = elem;
+          mine[q] = m;
+          old[q] = o;
+        }
+      ++n;
+    } else {
+      ownerSettle(F, elem, m, o, flags);
+    }
+  }
+  __device__ __forceinline__ void settle(const FusedArgs &F, unsigned &flags) {
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q)
+      if (q < n)
+        ownerSettle(F, e[q], mine[q], old[q], flags);
+    n = 0;
+  }
+};
+
 template <int IPT> struct FusedSmem {
   static constexpr int kCap = kFusedThreads * IPT;
-  static constexpr int kTable = 2 * kCap; // counting-sort slots (element span)
-  using Sort = cub::BlockRadixSort<uint64_t, kFusedThreads, IPT, uint32_t, 6>;
+  static constexpr int kTable = 2 * kCap; // hash slots (power of two)
+  static constexpr int kLogTable = IPT == 4 ? 11 : 13;
+  using Sort = cub::BlockRadixSort<uint64_t, kFusedThreads, IPT, uint32_t, 5>;
   union {
     typename Sort::TempStorage sortTmp;
     struct {
-      uint32_t cnt[kTable]; // per element slot: count, then start
+      uint32_t cnt[kTable]; // per slot: count, then start offset
       uint16_t rank[kCap];  // record's rank inside its slot
       uint32_t part[kFusedThreads];
     } cs;
+    uint64_t skey[kCap];    // radix mode: sorted keys
   } u;
   uint64_t elem[kCap];  // global element id, by record index
   uint64_t meta[kCap];  // tli:16 | bp:8 | wp:8 | site:12 | seq:20
-  uint64_t key[kCap];   // sorted keys (counting mode: element slot)
-  uint32_t idx[kCap];   // sorted -> record index
+  uint64_t selem[kCap]; // grouped order
+  uint64_t smeta[kCap];
   unsigned long long minE[kMaxWritten], maxE[kMaxWritten];
-  uint32_t prefix[kMaxWritten];
   unsigned int count, maxBp, maxWp, nReal, flags, maxGroup;
-  int counting; // this iteration groups by a counting sort over element slots
-  // field start bits of the block-local key  w|off|blk|bp|warp|wp|lane
+  int hashed; // 1: hash-slot grouping, 0: radix grouping
+  // radix mode: field start bits of the key  w|off|blk|bp|warp|wp|lane
   int fWp, fWarp, fBp, fBlk, fOff, fW, total;
 };
 
@@ -110,6 +143,10 @@ __device__ __forceinline__ uint32_t metaBp(uint64_t m) { return (m >> 40) & 255;
 __device__ __forceinline__ uint32_t metaWp(uint64_t m) { return (m >> 32) & 255; }
 __device__ __forceinline__ int metaSite(uint64_t m) { return static_cast<int>((m >> 20) & 4095); }
 __device__ __forceinline__ uint32_t metaSeq(uint64_t m) { return static_cast<uint32_t>(m & kSeqMask); }
+
+template <int IPT> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
+  return static_cast<uint32_t>((e * 0x9E3779B97F4A7C15ull) >> (64 - FusedSmem<IPT>::kLogTable));
+}
 
 // PARALLEL sink of the fused kernel: records into shared memory.
 template <int IPT> struct FusedSink : ParState {
@@ -161,7 +198,7 @@ template <int IPT> struct FusedSink : ParState {
 // Conditions of the reference pair rule for two records of one element
 // inside one MiniCU block (:750-769), INTRA kinds only.  Returns kind or -1.
 __device__ __forceinline__ int intraKind(const LaunchDev &L, const SiteDev *sites, uint64_t ma,
-                                         uint64_t mb, uint32_t tpb, int64_t ws) {
+                                         uint64_t mb, uint32_t tpb) {
   const uint32_t ta = metaTli(ma), tb = metaTli(mb);
   if (ta == tb)
     return -1;
@@ -192,13 +229,15 @@ __device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa,
   return (la * nLocs + lb) * 3 + kind;
 }
 
+// Keep the minimum `v` (element in hash mode, sorted position in radix
+// mode) per key; the first setter appends the key to the realised list.
 template <int IPT>
-__device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, uint32_t *sKeyMin, uint32_t *sReal,
-                                        int K, uint32_t pos) {
-  if (sKeyMin[K] <= pos)
+__device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, unsigned long long *sKeyMin,
+                                        uint32_t *sReal, int K, unsigned long long v) {
+  if (sKeyMin[K] <= v)
     return;
-  const uint32_t old = atomicMin(&sKeyMin[K], pos);
-  if (old == 0xffffffffu) {
+  const unsigned long long old = atomicMin(&sKeyMin[K], v);
+  if (old == ~0ull) {
     const unsigned slot = atomicAdd(&S.nReal, 1u);
     sReal[slot] = static_cast<uint32_t>(K);
   }
@@ -211,8 +250,8 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
   Smem &S = *reinterpret_cast<Smem *>(dyn);
   unsigned char *after = dyn + ((sizeof(Smem) + 15) & ~size_t(15));
   const int nKeysPad = (F.nKeys + 3) & ~3;
-  uint32_t *sKeyMin = reinterpret_cast<uint32_t *>(after);
-  uint32_t *sReal = sKeyMin + nKeysPad;
+  unsigned long long *sKeyMin = reinterpret_cast<unsigned long long *>(after);
+  uint32_t *sReal = reinterpret_cast<uint32_t *>(sKeyMin + nKeysPad);
   hgrd_gpu_insn *sCode = reinterpret_cast<hgrd_gpu_insn *>(sReal + nKeysPad);
   SiteDev *sSites = reinterpret_cast<SiteDev *>(sCode + F.L.nCode);
   ParamDev *sParams = reinterpret_cast<ParamDev *>(sSites + F.L.nSites);
@@ -229,7 +268,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
   for (int i = tid; i < L.nParams; i += kFusedThreads)
     sParams[i] = L.params[i];
   for (int i = tid; i < F.nKeys; i += kFusedThreads)
-    sKeyMin[i] = 0xffffffffu;
+    sKeyMin[i] = ~0ull;
   if (tid == 0) {
     S.nReal = 0;
     S.flags = 0;
@@ -248,59 +287,36 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       S.count = 0;
       S.maxBp = 0;
       S.maxWp = 0;
+      S.maxGroup = 0;
     }
-    if (tid < kMaxWritten) {
-      S.minE[tid] = ~0ull;
-      S.maxE[tid] = 0;
-    }
+    for (int i = tid; i < Smem::kTable; i += kFusedThreads)
+      S.u.cs.cnt[i] = 0;
     __syncthreads();
     // 1. expansion of the iteration's whole MiniCU blocks
-    for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
-      FusedSink<IPT> s;
-      s.L = &L;
-      s.sites = sSites;
-      s.params = sParams;
-      s.S = &S;
-      s.tli = static_cast<uint32_t>(tl);
-      Builtins bi;
-      threadIdentity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
-      Body::run(L, sCode, bi, s, regs);
-      tally.add(s);
-      atomicMax(&S.maxBp, s.bp);
-      atomicMax(&S.maxWp, s.wp);
-    }
-    __syncthreads();
-    // per written buffer: the iteration's element range (warp reduction)
     {
-      const unsigned nr = min(S.count, static_cast<unsigned>(Smem::kCap));
-      unsigned long long lo[kMaxWritten], hi[kMaxWritten];
-#pragma unroll
-      for (int q = 0; q < kMaxWritten; ++q) {
-        lo[q] = ~0ull;
-        hi[q] = 0;
-      }
-      for (unsigned i = tid; i < nr; i += kFusedThreads) {
-        const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
-        const unsigned long long e = S.elem[i];
-#pragma unroll
-        for (int q = 0; q < kMaxWritten; ++q)
-          if (q == w) {
-            lo[q] = min(lo[q], e);
-            hi[q] = max(hi[q], e);
-          }
+      unsigned myBp = 0, myWp = 0;
+      for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
+        FusedSink<IPT> s;
+        s.L = &L;
+        s.sites = sSites;
+        s.params = sParams;
+        s.S = &S;
+        s.tli = static_cast<uint32_t>(tl);
+        Builtins bi;
+        threadIdentity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
+        Body::run(L, sCode, bi, s, regs);
+        tally.add(s);
+        myBp = max(myBp, s.bp);
+        myWp = max(myWp, s.wp);
       }
 #pragma unroll
-      for (int q = 0; q < kMaxWritten; ++q) {
-        if (q >= F.nW)
-          break;
-        for (int o = 16; o > 0; o >>= 1) {
-          lo[q] = min(lo[q], __shfl_down_sync(0xffffffffu, lo[q], o));
-          hi[q] = max(hi[q], __shfl_down_sync(0xffffffffu, hi[q], o));
-        }
-        if ((tid & 31) == 0 && lo[q] <= hi[q]) {
-          atomicMin(&S.minE[q], lo[q]);
-          atomicMax(&S.maxE[q], hi[q]);
-        }
+      for (int o = 16; o > 0; o >>= 1) {
+        myBp = max(myBp, __shfl_down_sync(0xffffffffu, myBp, o));
+        myWp = max(myWp, __shfl_down_sync(0xffffffffu, myWp, o));
+      }
+      if ((tid & 31) == 0 && (myBp | myWp)) {
+        atomicMax(&S.maxBp, myBp);
+        atomicMax(&S.maxWp, myWp);
       }
     }
     __syncthreads();
@@ -309,89 +325,78 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       myFlags |= kFlagFusedOverflow;
     if (n == 0)
       continue;
-    // 2. grouping by element: counting sort over element slots when the
-    //    iteration's element span is small and groups are small, else a
-    //    CUB block radix sort of the full key
-    if (tid == 0) {
-      uint32_t span = 0;
-      bool ok = true;
-      for (int w = 0; w < F.nW && w < kMaxWritten; ++w) {
-        S.prefix[w] = span;
-        if (S.minE[w] <= S.maxE[w]) {
-          const unsigned long long sw = S.maxE[w] - S.minE[w] + 1;
-          if (sw > static_cast<unsigned long long>(Smem::kTable))
-            ok = false;
-          else
-            span += static_cast<uint32_t>(sw);
-        }
-      }
-      S.counting = ok && span <= static_cast<uint32_t>(Smem::kTable);
-      S.total = static_cast<int>(span); // slots in counting mode
-      S.maxGroup = 0;
-    }
-    __syncthreads();
-    if (S.counting) {
-      const int slots = S.total;
-      for (int i = tid; i < slots; i += kFusedThreads)
-        S.u.cs.cnt[i] = 0;
-      __syncthreads();
+    if (F.ablate & 1)
+      continue;
+    // 2. grouping: records hashed by element into slots (counting sort);
+    //    a slot holding many records (a hot element) falls back to a
+    //    block radix sort of the full key for this iteration
+    {
       unsigned myMax = 0;
       for (unsigned i = tid; i < n; i += kFusedThreads) {
-        const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
-        const uint32_t slot = S.prefix[w] + static_cast<uint32_t>(S.elem[i] - S.minE[w]);
+        const uint32_t slot = hashSlot<IPT>(S.elem[i]);
         const unsigned r = atomicAdd(&S.u.cs.cnt[slot], 1u);
         S.u.cs.rank[i] = static_cast<uint16_t>(r);
         myMax = max(myMax, r + 1);
       }
       if (myMax > kSmallGroup)
         atomicMax(&S.maxGroup, myMax);
-      __syncthreads();
-      if (S.maxGroup <= kSmallGroup) {
-        // exclusive scan of the slot counts: per-thread chunks + warp scans
-        const int per = (slots + kFusedThreads - 1) / kFusedThreads;
-        const int b0 = min(slots, tid * per), b1 = min(slots, b0 + per);
-        uint32_t sum = 0;
-        for (int i = b0; i < b1; ++i)
-          sum += S.u.cs.cnt[i];
-        S.u.cs.part[tid] = sum;
-        __syncthreads();
-        if (tid < 32) {
-          uint32_t acc = 0;
-          for (int k = 0; k < kFusedThreads / 32; ++k) {
-            const uint32_t v = S.u.cs.part[k * 32 + tid];
-            uint32_t incl = v;
+    }
+    __syncthreads();
+    const bool hashed = S.maxGroup <= kSmallGroup;
+    if (hashed) {
+      // exclusive scan of the slot counts: per-thread chunks + one warp
+      constexpr int per = Smem::kTable / kFusedThreads;
+      const int b0 = tid * per;
+      uint32_t sum = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-              if (tid >= o)
-                incl += y;
-            }
-            S.u.cs.part[k * 32 + tid] = acc + incl - v;
-            acc += __shfl_sync(0xffffffffu, incl, 31);
+      for (int i = 0; i < per; ++i)
+        sum += S.u.cs.cnt[b0 + i];
+      S.u.cs.part[tid] = sum;
+      __syncthreads();
+      if (tid < 32) {
+        uint32_t acc = 0;
+        for (int k = 0; k < kFusedThreads / 32; ++k) {
+          const uint32_t v = S.u.cs.part[k * 32 + tid];
+          uint32_t incl = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o)
+              incl += y;
           }
+          S.u.cs.part[k * 32 + tid] = acc + incl - v;
+          acc += __shfl_sync(0xffffffffu, incl, 31);
         }
-        __syncthreads();
-        uint32_t run = S.u.cs.part[tid];
-        for (int i = b0; i < b1; ++i) {
-          const uint32_t c0 = S.u.cs.cnt[i];
-          S.u.cs.cnt[i] = run;
-          run += c0;
-        }
-        __syncthreads();
-        for (unsigned i = tid; i < n; i += kFusedThreads) {
-          const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
-          const uint32_t slot = S.prefix[w] + static_cast<uint32_t>(S.elem[i] - S.minE[w]);
-          const uint32_t pos = S.u.cs.cnt[slot] + S.u.cs.rank[i];
-          S.idx[pos] = i;
-          S.key[pos] = slot;
-        }
-        __syncthreads();
-      } else if (tid == 0) {
-        S.counting = 0; // a hot element: fall back to the radix sort
       }
       __syncthreads();
-    }
-    if (!S.counting) {
+      uint32_t run = S.u.cs.part[tid];
+#pragma unroll
+      for (int i = 0; i < per; ++i) {
+        const uint32_t c0 = S.u.cs.cnt[b0 + i];
+        S.u.cs.cnt[b0 + i] = run;
+        run += c0;
+      }
+      __syncthreads();
+      for (unsigned i = tid; i < n; i += kFusedThreads) {
+        const uint64_t e = S.elem[i];
+        const uint32_t pos = S.u.cs.cnt[hashSlot<IPT>(e)] + S.u.cs.rank[i];
+        S.selem[pos] = e;
+        S.smeta[pos] = S.meta[i];
+      }
+      __syncthreads();
+    } else {
+      // radix mode: key w | off | blk | bp | warp | wp | lane over element offsets
+      if (tid < kMaxWritten) {
+        S.minE[tid] = ~0ull;
+        S.maxE[tid] = 0;
+      }
+      __syncthreads();
+      for (unsigned i = tid; i < n; i += kFusedThreads) {
+        const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
+        atomicMin(&S.minE[w], static_cast<unsigned long long>(S.elem[i]));
+        atomicMax(&S.maxE[w], static_cast<unsigned long long>(S.elem[i]));
+      }
+      __syncthreads();
       if (tid == 0) {
         uint64_t span = 1;
         for (int w = 0; w < F.nW && w < kMaxWritten; ++w)
@@ -419,8 +424,6 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
         continue;
       uint64_t keys[IPT];
       uint32_t vals[IPT];
-      const int wpShift = S.fWp, warpShift = S.fWarp, bpShift = S.fBp, blkShift = S.fBlk,
-                offShift = S.fOff, wShift = S.fW;
 #pragma unroll
       for (int j = 0; j < IPT; ++j) {
         const unsigned i = static_cast<unsigned>(tid * IPT + j);
@@ -430,91 +433,99 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
           const uint32_t tli = metaTli(m);
           const uint32_t blk = L.dTpb.div(tli), tl = tli - blk * tpb;
           const uint32_t warp = L.dWs.div(tl), lane = tl - warp * static_cast<uint32_t>(ws);
-          const SiteDev &sd = sSites[metaSite(m)];
-          const int w = sParams[sd.param].written - 1;
+          const int w = sParams[sSites[metaSite(m)].param].written - 1;
           const uint64_t off = S.elem[i] - S.minE[w];
-          keys[j] = (static_cast<uint64_t>(w) << wShift) | (off << offShift) |
-                    (static_cast<uint64_t>(blk) << blkShift) |
-                    (static_cast<uint64_t>(metaBp(m)) << bpShift) |
-                    (static_cast<uint64_t>(warp) << warpShift) |
-                    (static_cast<uint64_t>(metaWp(m)) << wpShift) | lane;
+          keys[j] = (static_cast<uint64_t>(w) << S.fW) | (off << S.fOff) |
+                    (static_cast<uint64_t>(blk) << S.fBlk) |
+                    (static_cast<uint64_t>(metaBp(m)) << S.fBp) |
+                    (static_cast<uint64_t>(warp) << S.fWarp) |
+                    (static_cast<uint64_t>(metaWp(m)) << S.fWp) | lane;
         } else {
           keys[j] = ~0ull;
         }
       }
       typename Smem::Sort(S.u.sortTmp).Sort(keys, vals, 0, S.total > 0 ? S.total : 1);
+      __syncthreads();
 #pragma unroll
       for (int j = 0; j < IPT; ++j) {
-        S.key[tid * IPT + j] = keys[j];
-        S.idx[tid * IPT + j] = vals[j];
+        const int p = tid * IPT + j;
+        S.u.skey[p] = keys[j];
+        if (p < static_cast<int>(n)) {
+          S.selem[p] = S.elem[vals[j]];
+          S.smeta[p] = S.meta[vals[j]];
+        }
       }
       __syncthreads();
     }
-    // group keys of the sorted key (counting mode: the key is the element slot)
-    const bool counting = S.counting != 0;
-    const int shLane = S.fWp;                 // element|blk|bp|warp|wp  (INTRA-WARP group)
-    const int shBpF = S.fBp;                  // element|blk|bp          (INTRA-BLOCK group)
-    const int shElem = counting ? 0 : S.fOff; // element
-    // 4. per element group: ownership + INTRA keys
-    for (int j = 0; j < IPT; ++j) {
-      const int p = tid * IPT + j;
-      if (p >= static_cast<int>(n))
-        break;
-      const uint64_t g = S.key[p] >> shElem;
-      if (p > 0 && (S.key[p - 1] >> shElem) == g)
-        continue;
-      int e = p + 1;
-      while (e < static_cast<int>(n) && (S.key[e] >> shElem) == g)
-        ++e;
-      const uint64_t ge = S.elem[S.idx[p]];
-      // ownership per (element, block)
-      for (int q = p; q < e; ++q) {
-        const uint32_t bq = L.dTpb.div(metaTli(S.meta[S.idx[q]]));
-        bool seen = false;
-        for (int r2 = p; r2 < q && !seen; ++r2)
-          seen = L.dTpb.div(metaTli(S.meta[S.idx[r2]])) == bq;
-        if (!seen)
-          ownerUpdate(F, ge, static_cast<uint64_t>(firstBlock + bq), myFlags);
-      }
-      if (e - p < 2)
-        continue;
-      if (e - p <= kSmallGroup) {
-        for (int a = p; a < e; ++a) {
-          const uint64_t ma = S.meta[S.idx[a]];
-          for (int b = a + 1; b < e; ++b) {
-            const uint64_t mb = S.meta[S.idx[b]];
-            const int kind = intraKind(L, sSites, ma, mb, tpb, ws);
-            if (kind < 0)
-              continue;
-            const int sa = metaSite(ma), sb = metaSite(mb);
-            if (!((sConf[sa] >> sb) & 1ull))
-              continue;
-            noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, sa, sb, kind),
-                    static_cast<uint32_t>(p));
-          }
+    // 3. detection
+    OwnerPending owners;
+    if (hashed) {
+      // one thread per record: pairs with the earlier records of its slot
+      for (unsigned p = tid; p < n && !(F.ablate & 2); p += kFusedThreads) {
+        const uint64_t e = S.selem[p];
+        const uint64_t m = S.smeta[p];
+        const uint32_t slot = hashSlot<IPT>(e);
+        const uint32_t gs = S.u.cs.cnt[slot];
+        const uint32_t bp_ = L.dTpb.div(metaTli(m));
+        const int sp = metaSite(m);
+        bool first = true;
+        for (uint32_t q = gs; q < p; ++q) {
+          if (S.selem[q] != e)
+            continue;
+          const uint64_t mq = S.smeta[q];
+          if (L.dTpb.div(metaTli(mq)) == bp_)
+            first = false;
+          const int kind = intraKind(L, sSites, mq, m, tpb);
+          if (kind < 0)
+            continue;
+          const int sq = metaSite(mq);
+          if (!((sConf[sq] >> sp) & 1ull))
+            continue;
+          noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, sq, sp, kind), e);
         }
-      } else {
-        // summaries: per site (min,max) warp at (element,blk,bp), lane at (..,warp,wp)
+        if (first && !(F.ablate & 4))
+          owners.issue(F, e, static_cast<uint64_t>(firstBlock + bp_), myFlags);
+      }
+    } else {
+      // radix mode: one thread per element group (hot elements)
+      const int shLane = S.fWp, shBpF = S.fBp, shBlkF = S.fBlk, shElem = S.fOff;
+      for (int j = 0; j < IPT; ++j) {
+        const int p = tid * IPT + j;
+        if (p >= static_cast<int>(n))
+          break;
+        const uint64_t g = S.u.skey[p] >> shElem;
+        if (p > 0 && (S.u.skey[p - 1] >> shElem) == g)
+          continue;
+        int e = p + 1;
+        while (e < static_cast<int>(n) && (S.u.skey[e] >> shElem) == g)
+          ++e;
+        const uint64_t ge = S.selem[p];
+        for (int q = p; q < e; ++q)
+          if (q == p || (S.u.skey[q] >> shBlkF) != (S.u.skey[q - 1] >> shBlkF))
+            owners.issue(F, ge, static_cast<uint64_t>(firstBlock + L.dTpb.div(metaTli(S.smeta[q]))),
+                         myFlags);
+        if (e - p < 2)
+          continue;
         uint32_t mn2[kMaxSites], mx2[kMaxSites], mn3[kMaxSites], mx3[kMaxSites];
         uint64_t p2 = 0, p3 = 0;
-        uint64_t g2 = S.key[p] >> shBpF, g3 = S.key[p] >> shLane;
+        uint64_t g2 = S.u.skey[p] >> shBpF, g3 = S.u.skey[p] >> shLane;
         auto flush = [&](uint64_t pres, const uint32_t *mn, const uint32_t *mx, int kind) {
           uint64_t rem = pres;
           while (rem) {
             const int a = __ffsll(static_cast<long long>(rem)) - 1;
             rem &= rem - 1;
-            uint64_t m = sConf[a] & pres & ~((1ull << a) - 1);
-            while (m) {
-              const int b = __ffsll(static_cast<long long>(m)) - 1;
-              m &= m - 1;
+            uint64_t mm = sConf[a] & pres & ~((1ull << a) - 1);
+            while (mm) {
+              const int b = __ffsll(static_cast<long long>(mm)) - 1;
+              mm &= mm - 1;
               if (min(mn[a], mn[b]) < max(mx[a], mx[b]))
                 noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, a, b, kind),
-                        static_cast<uint32_t>(p));
+                        static_cast<unsigned long long>(p));
             }
           }
         };
         for (int q = p; q < e; ++q) {
-          const uint64_t k = S.key[q];
+          const uint64_t k = S.u.skey[q];
           if ((k >> shBpF) != g2) {
             flush(p2, mn2, mx2, 1);
             p2 = 0;
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
             p3 = 0;
             g3 = k >> shLane;
           }
-          const uint64_t m = S.meta[S.idx[q]];
+          const uint64_t m = S.smeta[q];
           const int s = metaSite(m);
           const uint32_t tli = metaTli(m);
           const uint32_t tl = tli - L.dTpb.div(tli) * tpb;
@@ -538,30 +549,43 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       }
     }
     __syncthreads();
-    // 5. witnesses of the keys realised in this iteration
+    // 4. witnesses of the keys realised in this iteration
     const unsigned nReal = S.nReal;
     for (unsigned r = tid; r < nReal; r += kFusedThreads) {
       const int K = static_cast<int>(sReal[r]);
       const int kind = K % 3;
       const int la = (K / 3) / F.nLocs, lb = (K / 3) % F.nLocs;
-      const int p = static_cast<int>(sKeyMin[K]);
-      sKeyMin[K] = 0xffffffffu; // reset for the next iteration
-      const uint64_t gElem = S.elem[S.idx[p]];
-      if (gElem > F.keyElem[K])
+      const unsigned long long v = sKeyMin[K];
+      sKeyMin[K] = ~0ull; // reset for the next iteration
+      // the key's minimum element in this iteration and its record range
+      uint64_t ge;
+      uint32_t g0, g1;
+      if (hashed) {
+        ge = v;
+        const uint32_t slot = hashSlot<IPT>(ge);
+        g0 = S.u.cs.cnt[slot];
+        g1 = slot + 1 < static_cast<uint32_t>(Smem::kTable) ? S.u.cs.cnt[slot + 1] : n;
+      } else {
+        g0 = static_cast<uint32_t>(v);
+        ge = S.selem[g0];
+        const uint64_t g = S.u.skey[g0] >> S.fOff;
+        g1 = g0 + 1;
+        while (g1 < n && (S.u.skey[g1] >> S.fOff) == g)
+          ++g1;
+      }
+      if (ge > F.keyElem[K])
         continue; // another block already holds a smaller element for K
-      const uint64_t g = S.key[p] >> shElem;
-      int e = p + 1;
-      while (e < static_cast<int>(n) && (S.key[e] >> shElem) == g)
-        ++e;
       uint64_t bestX = ~0ull, bestY = ~0ull;
       int sX = 0, sY = 0;
       auto order = [&](uint64_t m) {
         const uint64_t thread = static_cast<uint64_t>(firstBlock * L.tpb) + metaTli(m);
         return (thread << kSeqBits) | metaSeq(m);
       };
-      // lexicographically first (x, y) over the group's racing pairs of K
-      for (int a = p; a < e; ++a) {
-        const uint64_t ma = S.meta[S.idx[a]];
+      // lexicographically first (x, y) over the element's racing pairs of K
+      for (uint32_t a = g0; a < g1; ++a) {
+        if (S.selem[a] != ge)
+          continue;
+        const uint64_t ma = S.smeta[a];
         const int sa = metaSite(ma);
         const int loa = sSites[sa].loc;
         if (loa != la && loa != lb)
@@ -569,10 +593,10 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
         const uint64_t oa = order(ma);
         if (oa > bestX)
           continue;
-        for (int b = p; b < e; ++b) {
-          if (b == a)
+        for (uint32_t b = g0; b < g1; ++b) {
+          if (b == a || S.selem[b] != ge)
             continue;
-          const uint64_t mb = S.meta[S.idx[b]];
+          const uint64_t mb = S.smeta[b];
           const uint64_t ob = order(mb);
           if (ob <= oa)
             continue; // y must follow x in event order
@@ -582,7 +606,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
             continue;
           if (!((sConf[sa] >> sb) & 1ull))
             continue;
-          if (intraKind(L, sSites, ma, mb, tpb, ws) != kind)
+          if (intraKind(L, sSites, ma, mb, tpb) != kind)
             continue;
           if (oa < bestX || (oa == bestX && ob < bestY)) {
             bestX = oa;
@@ -592,7 +616,6 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
           }
         }
       }
-      const uint64_t ge = S.elem[S.idx[p]];
       const unsigned long long old = atomicMin(&F.keyElem[K], static_cast<unsigned long long>(ge));
       if (ge <= old) {
         const unsigned c = atomicAdd(F.candCount, 1u);
@@ -602,6 +625,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
           myFlags |= kFlagFusedOverflow;
       }
     }
+    owners.settle(F, myFlags);
     if (tid == 0)
       S.nReal = 0;
   }

@@ -101,9 +101,17 @@ struct hgrd_gpu_ctx {
 
   unsigned char *hStage = nullptr;
   size_t hStageCap = 0;
+  // per check: counters / per-key minima / race array live in the blob, so
+  // a check is one H2D (descriptor + zeroed counters), kernels, one D2H
+  Counters *cur = nullptr;
+  hgrd_gpu_race *curRaces = nullptr;
+  unsigned long long *curKeyElem = nullptr;
+  unsigned char *hResult = nullptr; // pinned: counters + races
+  size_t hResultCap = 0;
   hgrd_gpu_race *hRaces = nullptr; // pinned copy of the device race array
   size_t hRacesCap = 0;
   bool racesOnHost = false;
+  hgrd_gpu_race *hRacesView = nullptr;
   Counters *hCtr = nullptr;
   uint64_t capHint = 1 << 16;
   uint64_t opHint = 1 << 12;
@@ -350,8 +358,9 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
 }
 
 struct BlobOffsets {
-  size_t code, sites, params, regs, cInter, cIntra, locMask, wBase, wHandle, total;
-  int nW;
+  size_t code, sites, params, regs, cInter, cIntra, locMask, wBase, wHandle;
+  size_t keyElem, ctr, races, h2d, total;
+  int nW, nKeys;
 };
 
 int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOffsets &o) {
@@ -370,6 +379,12 @@ int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOff
   o.locMask = put(8 * P.locMask.size());
   o.wBase = put(8 * P.wBase.size());
   o.wHandle = put(4 * P.wHandle.size());
+  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+  o.nKeys = 3 * nLocs * nLocs;
+  o.keyElem = put(8 * static_cast<size_t>(o.nKeys));
+  o.ctr = put(sizeof(Counters));
+  o.h2d = off;
+  o.races = put(sizeof(hgrd_gpu_race) * static_cast<size_t>(o.nKeys));
   o.total = off;
   o.nW = static_cast<int>(P.wBase.size());
   int rc = stage(c, o.total);
@@ -388,28 +403,37 @@ int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOff
   std::memcpy(h + o.locMask, P.locMask.data(), 8 * P.locMask.size());
   std::memcpy(h + o.wBase, P.wBase.data(), 8 * P.wBase.size());
   std::memcpy(h + o.wHandle, P.wHandle.data(), 4 * P.wHandle.size());
-  CK(cudaMemcpyAsync(c->blob.p, h, o.total, cudaMemcpyHostToDevice, c->st));
+  std::memset(h + o.keyElem, 0xff, 8 * static_cast<size_t>(o.nKeys));
+  std::memset(h + o.ctr, 0, sizeof(Counters));
+  CK(cudaMemcpyAsync(c->blob.p, h, o.h2d, cudaMemcpyHostToDevice, c->st));
+  c->cur = reinterpret_cast<Counters *>(c->blob.p + o.ctr);
+  c->curRaces = reinterpret_cast<hgrd_gpu_race *>(c->blob.p + o.races);
+  c->curKeyElem = reinterpret_cast<unsigned long long *>(c->blob.p + o.keyElem);
   return 0;
 }
 
-// Counters and (speculatively) the whole race array in one round trip.
+// Counters and (speculatively) the whole race array in one round trip
+// (they are adjacent in the blob).
 int readCountersAndRaces(hgrd_gpu_ctx *c, size_t nKeys) {
-  if (c->hRacesCap < nKeys) {
-    if (c->hRaces)
-      CK(cudaFreeHost(c->hRaces));
-    CK(cudaMallocHost(&c->hRaces, sizeof(hgrd_gpu_race) * nKeys));
-    c->hRacesCap = nKeys;
+  const size_t racesOff = reinterpret_cast<unsigned char *>(c->curRaces) -
+                          reinterpret_cast<unsigned char *>(c->cur);
+  const size_t bytes = racesOff + sizeof(hgrd_gpu_race) * nKeys;
+  if (c->hResultCap < bytes) {
+    if (c->hResult)
+      CK(cudaFreeHost(c->hResult));
+    CK(cudaMallocHost(&c->hResult, std::max<size_t>(bytes, 4096)));
+    c->hResultCap = std::max<size_t>(bytes, 4096);
   }
-  CK(cudaMemcpyAsync(c->hCtr, c->ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(c->hRaces, c->races.p, sizeof(hgrd_gpu_race) * nKeys,
-                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hResult, c->cur, bytes, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  std::memcpy(c->hCtr, c->hResult, sizeof(Counters));
+  c->hRacesView = reinterpret_cast<hgrd_gpu_race *>(c->hResult + racesOff);
   c->racesOnHost = true;
   return 0;
 }
 
 int readCounters(hgrd_gpu_ctx *c) {
-  CK(cudaMemcpyAsync(c->hCtr, c->ctr.p, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hCtr, c->cur, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   return 0;
 }
@@ -442,9 +466,8 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
            bool append = false) {
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
-  NEED(c->races, static_cast<size_t>(nKeys));
   if (!append)
-    CK(cudaMemsetAsync(&c->ctr.p->nRaces, 0, sizeof(unsigned), c->st));
+    CK(cudaMemsetAsync(&c->cur->nRaces, 0, sizeof(unsigned), c->st));
   DetectArgs A = detectArgs(c, L, D, o, n, kindMask);
   (void)A;
   {
@@ -476,8 +499,8 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       CK(cudaGetLastError());
       {
         StageTimer t(c, "k_witness");
-        k_witness<<<(nKeys + 127) / 128, 128, 0, c->st>>>(A, c->keySeg.p, nKeys, c->races.p,
-                                                           c->ctr.p);
+        k_witness<<<(nKeys + 127) / 128, 128, 0, c->st>>>(A, c->keySeg.p, nKeys, c->curRaces,
+                                                           c->cur);
       }
       CK(cudaGetLastError());
       c->kernelLaunches += 2;
@@ -509,7 +532,7 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       }
       CK(cudaGetLastError());
       k_decode_pairwise<<<(nKeys + 127) / 128, 128, 0, c->st>>>(
-          A, dk.Current(), dv.Current(), c->keyPair.p, nKeys, c->races.p, c->ctr.p);
+          A, dk.Current(), dv.Current(), c->keyPair.p, nKeys, c->curRaces, c->cur);
       CK(cudaGetLastError());
       c->kernelLaunches += 3;
     }
@@ -530,9 +553,9 @@ int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
   if (nr > R->race_cap)
     return HGRD_GPU_E2BIG;
   if (nr && c->racesOnHost) {
-    std::memcpy(R->races, c->hRaces, sizeof(hgrd_gpu_race) * nr);
+    std::memcpy(R->races, c->hRacesView, sizeof(hgrd_gpu_race) * nr);
   } else if (nr) {
-    CK(cudaMemcpyAsync(R->races, c->races.p, sizeof(hgrd_gpu_race) * nr,
+    CK(cudaMemcpyAsync(R->races, c->curRaces, sizeof(hgrd_gpu_race) * nr,
                        cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
   }
@@ -566,8 +589,12 @@ struct JitGetter {
 int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t smem,
                     const void *jitKernel, const char *stage) {
   const void *fn = jitKernel ? jitKernel : reinterpret_cast<const void *>(k_expand_par<InterpBody>);
-  if (smem > 48 * 1024 && c->smemOptIn.insert(fn).second)
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  if (smem > 48 * 1024 && c->smemOptIn.insert(fn).second) {
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            227 * 1024 - static_cast<int>(fa.sharedSizeBytes)));
+  }
   void *args[] = {const_cast<LaunchDev *>(&D)};
   {
     StageTimer t(c, stage);
@@ -597,8 +624,12 @@ template <int IPT>
 int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *jitKernel) {
   const void *fn =
       jitKernel ? jitKernel : reinterpret_cast<const void *>(k_fused<IPT, InterpBody>);
-  if (c->smemOptIn.insert(fn).second) // once per kernel: allow up to 227 KB
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  if (c->smemOptIn.insert(fn).second) { // once per kernel: allow up to 227 KB in total
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            227 * 1024 - static_cast<int>(fa.sharedSizeBytes)));
+  }
   int &perSM = c->occupancy[std::make_pair(fn, smem)];
   if (perSM == 0) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, kFusedThreads, smem));
@@ -640,12 +671,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     c->epoch = 0;
   }
   ++c->epoch;
-  NEED(c->keyElem, static_cast<size_t>(nKeys));
-  CK(cudaMemsetAsync(c->keyElem.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
   const uint32_t candCap = 1u << 16;
   NEED(c->cand, candCap);
-  NEED(c->races, static_cast<size_t>(nKeys));
-  CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(Counters), c->st));
 
   FusedArgs F{};
   F.L = D;
@@ -655,24 +682,20 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.nIters = (D.nBlocks + bpi - 1) / bpi;
   F.owner = c->owner.p;
   F.epoch = c->epoch;
-  F.keyElem = c->keyElem.p;
+  F.keyElem = c->curKeyElem;
   F.cand = c->cand.p;
   F.candCap = candCap;
-  F.candCount = &c->ctr.p->candCount;
+  F.candCount = &c->cur->candCount;
   F.nW = o.nW;
+  F.races = c->curRaces;
+  F.wBase = reinterpret_cast<const uint64_t *>(c->blob.p + o.wBase);
+  F.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
   if (const char *ab = std::getenv("HGRD_FUSED_ABLATE"))
     F.ablate = std::atoi(ab);
   int rc = ipt == 4 ? launchFused<4>(c, F, smem, jk.get(hgrdgpu::jit::kFused4))
                     : launchFused<16>(c, F, smem, jk.get(hgrdgpu::jit::kFused16));
   if (rc < 0)
     return rc;
-  CK(cudaGetLastError());
-  ++c->kernelLaunches;
-  DetectArgs A = detectArgs(c, L, D, o, 0, 7);
-  {
-    StageTimer t(c, "k_fused_finalize");
-    k_fused_finalize<<<nKeys, 128, 0, c->st>>>(F, A, c->races.p);
-  }
   CK(cudaGetLastError());
   ++c->kernelLaunches;
   rc = readCountersAndRaces(c, static_cast<size_t>(nKeys));
@@ -838,7 +861,6 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   int rc = uploadBlob(c, L, P, o);
   if (rc < 0)
     return rc;
-  NEED(c->ctr, 1);
 
   LaunchDev D{};
   D.code = reinterpret_cast<const hgrd_gpu_insn *>(c->blob.p + o.code);
@@ -862,7 +884,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   D.nBlocks = L.grid[0] * L.grid[1] * L.grid[2];
   D.nThreads = D.nBlocks * D.tpb;
   D.stepBudget = L.step_budget;
-  D.ctr = c->ctr.p;
+  D.ctr = c->cur;
   D.small = D.nThreads < (int64_t(1) << 32) - 1 && L.warp_size < (int64_t(1) << 32);
   if (D.small) {
     D.dTpb = FastDiv::make(static_cast<uint32_t>(D.tpb));
@@ -918,7 +940,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       c->err = "packed record key wider than 64 bits";
       return HGRD_GPU_ENOTSUP;
     }
-    CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(Counters), c->st));
+    CK(cudaMemsetAsync(c->cur, 0, sizeof(Counters), c->st));
     if (!seq) {
       const uint64_t nBatches = (static_cast<uint64_t>(D.nThreads) + 31) / 32;
       const uint64_t blocks = std::min<uint64_t>((nBatches + 7) / 8, uint64_t(c->nSM) * 8);
@@ -1144,6 +1166,8 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
     cudaFreeHost(c->hCtr);
   if (c->hRaces)
     cudaFreeHost(c->hRaces);
+  if (c->hResult)
+    cudaFreeHost(c->hResult);
   hgrdgpu::jit::destroy(c->jit);
   for (cudaEvent_t e : c->evPool)
     cudaEventDestroy(e);

@@ -78,6 +78,8 @@ struct Counters {
   int abortStmt;
   unsigned int nRaces;
   unsigned int candCount;
+  unsigned int doneCtas; // fused kernel: CTAs finished (last one finalises)
+  unsigned int pad;
 };
 
 // Division by a launch-invariant 32-bit divisor: one mul.hi + shifts

@@ -59,6 +59,9 @@ struct FusedArgs {
   uint32_t candCap;
   unsigned int *candCount;
   int nW;
+  hgrd_gpu_race *races;     // INTRA races are finalised by the last CTA
+  const uint64_t *wBase;    // element -> (handle, index)
+  const int32_t *wHandle;
   int ablate; // profiling knob (HGRD_FUSED_ABLATE): 1 skip grouping, 2 skip groups, 4 skip ownership
 };
 
@@ -655,6 +658,71 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
   }
   if (tid == 0 && S.flags)
     atomicOr(&L.ctr->flags, S.flags);
+
+  // The last CTA to finish turns the candidates into race records: per key,
+  // the lexicographically first pair of the key's minimum element.
+  __shared__ bool amLast;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0)
+    amLast = atomicAdd(&L.ctr->doneCtas, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!amLast)
+    return;
+  __threadfence();
+  const unsigned nc = min(atomicAdd(F.candCount, 0u), F.candCap);
+  const int wid = tid >> 5;
+  for (int K = wid; K < F.nKeys; K += kFusedThreads / 32) {
+    const unsigned long long e = __ldcg(&F.keyElem[K]);
+    if (e == ~0ull)
+      continue;
+    uint64_t x = ~0ull, y = ~0ull;
+    int sx = 0, sy = 0;
+    for (unsigned c = lane; c < nc; c += 32) {
+      const Candidate *cd = &F.cand[c];
+      if (__ldcg(&cd->key) != K || __ldcg(&cd->elem) != e)
+        continue;
+      const uint64_t cx = __ldcg(&cd->xOrd), cy = __ldcg(&cd->yOrd);
+      if (cx < x || (cx == x && cy < y)) {
+        x = cx;
+        y = cy;
+        sx = __ldcg(&cd->siteX);
+        sy = __ldcg(&cd->siteY);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ox = __shfl_down_sync(0xffffffffu, x, o);
+      const uint64_t oy = __shfl_down_sync(0xffffffffu, y, o);
+      const int osx = __shfl_down_sync(0xffffffffu, sx, o);
+      const int osy = __shfl_down_sync(0xffffffffu, sy, o);
+      if (ox < x || (ox == x && oy < y)) {
+        x = ox;
+        y = oy;
+        sx = osx;
+        sy = osy;
+      }
+    }
+    if (lane == 0) {
+      const unsigned pos = atomicAdd(&L.ctr->nRaces, 1u);
+      hgrd_gpu_race &o = F.races[pos];
+      o.kind = K % 3;
+      o.loc_a = (K / 3) / F.nLocs;
+      o.loc_b = (K / 3) % F.nLocs;
+      o.site_x = sx;
+      o.site_y = sy;
+      int w = 0;
+      for (int q = 1; q < F.nW; ++q)
+        if (F.wBase[q] <= e)
+          w = q;
+      o.handle = F.wHandle[w];
+      o.index = static_cast<int64_t>(e - F.wBase[w]);
+      o.thread_x = static_cast<int64_t>(x >> kSeqBits);
+      o.seq_x = static_cast<int32_t>(x & kSeqMask);
+      o.thread_y = static_cast<int64_t>(y >> kSeqBits);
+      o.seq_y = static_cast<int32_t>(y & kSeqMask);
+    }
+  }
 }
 
 // One block per key: the lexicographically first candidate pair of the

@@ -221,6 +221,14 @@ int hgrd_gpu_run_concrete_json(hgrd_gpu_ctx *ctx, const char *source,
 int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
                                     const char *file_name,
                                     const char *caps_json, char **out);
+/* One rank's share of the enumerateVerdict lattice for multi-GPU sweeps:
+ * configs whose canonical index k satisfies k % world == rank, each with its
+ * sorted races: {"total":N,"configs":[{index,warpSize,races:[{kind,locA,locB}]}]}.
+ * Merging all shards in index order with first-wins (locs, kind, warpSize)
+ * dedup reproduces hgrd_gpu_enumerate_verdict_json exactly. */
+int hgrd_gpu_sweep_shard_json(hgrd_gpu_ctx *ctx, const char *source,
+                              const char *file_name, const char *caps_json,
+                              int rank, int world, char **out);
 int hgrd_gpu_count_inputs(const char *source, const char *file_name);
 /* Lowering only: bytecode, sites, locs and per-kernel facts of one kernel as
  * JSON (for callers that fix launch parameters themselves). */

@@ -476,6 +476,15 @@ int hgrd_oracle_enumerate_verdict_json(const char *src, const char *file,
   return rc;
 }
 
+int hgrd_oracle_sweep_shard_json(const char *src, const char *file, const char *caps,
+                                 int rank, int world, char **out) {
+  CpuOracle be;
+  std::string s;
+  int rc = sweepShardJsonRun(be, src, file, caps, rank, world, s);
+  *out = dup(s);
+  return rc;
+}
+
 // Launch-level oracle for descriptors built outside the host interpreter
 // (bench workloads): buffers are given by contents, then one check runs.
 int hgrd_oracle_check_launch(const hgrd_gpu_launch *launch,

@@ -144,6 +144,9 @@ def load_library() -> ctypes.CDLL:
                                      ctypes.POINTER(P)]
     lib.hgrd_gpu_lower_json.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
                                         ctypes.POINTER(P)]
+    lib.hgrd_gpu_sweep_shard_json.argtypes = [P, ctypes.c_char_p, ctypes.c_char_p,
+                                              ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                              ctypes.POINTER(P)]
     lib.hgrd_gpu_count_inputs.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
     lib.hgrd_gpu_free.argtypes = [P]
     lib.hgrd_gpu_set_profiling.argtypes = [P, ctypes.c_int]
@@ -286,6 +289,18 @@ class GpuContext:
         s = _take_string(self._lib, out)
         if rc != 0:
             raise RuntimeError(f"run_concrete failed ({rc}): {s}")
+        return json.loads(s)
+
+    def sweep_shard(self, source: str, caps=None, file_name: str = "prog.mcu",
+                    rank: int = 0, world: int = 1) -> dict:
+        """This rank's share of the enumerateVerdict lattice (see parallel.py)."""
+        out = ctypes.c_void_p()
+        rc = self._lib.hgrd_gpu_sweep_shard_json(self._ctx, source.encode(), file_name.encode(),
+                                                 _cfg_json(caps).encode(), rank, world,
+                                                 ctypes.byref(out))
+        s = _take_string(self._lib, out)
+        if rc != 0:
+            raise RuntimeError(f"sweep_shard failed ({rc}): {s}")
         return json.loads(s)
 
     def enumerate_verdict(self, source: str, caps=None, file_name: str = "prog.mcu") -> dict:

@@ -68,6 +68,17 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
   return rc;
 }
 
+int hgrd_gpu_sweep_shard_json(hgrd_gpu_ctx *ctx, const char *source, const char *file_name,
+                              const char *caps_json, int rank, int world, char **out) {
+  if (!ctx || !out)
+    return HGRD_GPU_EINVAL;
+  GpuBackend be(ctx);
+  std::string s;
+  int rc = sweepShardJsonRun(be, source, file_name, caps_json, rank, world, s);
+  *out = dup(s);
+  return rc;
+}
+
 int hgrd_gpu_count_inputs(const char *source, const char *file_name) {
   ParseOutcome po = parseMiniCU(source ? source : "", file_name ? file_name : "");
   if (!po.program)

@@ -861,6 +861,57 @@ SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
   return out;
 }
 
+SweepShard sweepShard(CompiledProgram &prog, const SweepCaps &caps, int rank, int world,
+                      LaunchBackend &backend) {
+  SweepShard out;
+  const int inputs = prog.inputs;
+  uint64_t configs = 0;
+  std::vector<size_t> cursor(static_cast<size_t>(inputs), 0);
+  for (int64_t ws : caps.warpSizes) {
+    std::fill(cursor.begin(), cursor.end(), 0);
+    for (;;) {
+      if (configs > caps.maxConfigs) { // reference :873 (configs++ > maxConfigs)
+        out.total = configs;
+        return out;
+      }
+      const uint64_t index = configs++;
+      if (static_cast<int>(index % static_cast<uint64_t>(world)) == rank) {
+        ExecConfig c;
+        c.gridCap = caps.gridCap;
+        c.blockCap = caps.blockCap;
+        c.warpSize = ws;
+        c.maxThreads = caps.maxThreads;
+        for (int i = 0; i < inputs; ++i)
+          c.inputs.push_back(caps.inputSet[cursor[static_cast<size_t>(i)]]);
+        RunResult r = runConcrete(prog, c, backend);
+        if (r.error) {
+          out.error = r.error;
+          out.errorMessage = r.errorMessage;
+          return out;
+        }
+        out.stats.instances += r.stats.instances;
+        out.stats.records += r.stats.records;
+        out.stats.deviceMs += r.stats.deviceMs;
+        out.stats.parLaunches += r.stats.parLaunches;
+        out.stats.seqLaunches += r.stats.seqLaunches;
+        out.stats.restarts += r.stats.restarts;
+        out.configs.push_back(ShardConfig{index, ws, std::move(r.races)});
+      }
+      int pos = inputs - 1;
+      while (pos >= 0) {
+        if (++cursor[static_cast<size_t>(pos)] < caps.inputSet.size())
+          break;
+        cursor[static_cast<size_t>(pos)] = 0;
+        --pos;
+      }
+      if (pos < 0)
+        break;
+    }
+  }
+  out.total = configs;
+  return out;
+}
+
 // ---------------------------------------------------------------------------
 // JSON
 
@@ -1188,6 +1239,52 @@ std::string sweepResultJson(const SweepResult &r, const std::string &file) {
   }
   o << "],\"configs\":" << r.configs << ",\"stats\":" << statsJ(r.stats) << "}";
   return o.str();
+}
+
+std::string sweepShardJson(const SweepShard &r, const std::string &file) {
+  std::ostringstream o;
+  o << "{\"total\":" << r.total << ",\"configs\":[";
+  for (size_t i = 0; i < r.configs.size(); ++i) {
+    const ShardConfig &c = r.configs[i];
+    o << (i ? "," : "") << "{\"index\":" << c.index << ",\"warpSize\":" << c.warpSize
+      << ",\"races\":[";
+    for (size_t k = 0; k < c.races.size(); ++k) {
+      const Race &x = c.races[k];
+      o << (k ? "," : "") << "{\"kind\":" << esc(raceKindName(x.kind))
+        << ",\"locA\":" << locJ(x.locA, file) << ",\"locB\":" << locJ(x.locB, file) << "}";
+    }
+    o << "]}";
+  }
+  o << "],\"stats\":" << statsJ(r.stats) << "}";
+  return o.str();
+}
+
+int sweepShardJsonRun(LaunchBackend &be, const char *src, const char *file,
+                      const char *capsJson, int rank, int world, std::string &out) {
+  SweepCaps caps;
+  std::string err;
+  if (world < 1 || rank < 0 || rank >= world) {
+    out = errorJson({"bad rank/world"});
+    return HGRD_GPU_EINVAL;
+  }
+  if (!parseSweepCapsJson(capsJson, caps, err)) {
+    out = errorJson({"caps: " + err});
+    return HGRD_GPU_EINVAL;
+  }
+  ParseOutcome po = parseMiniCU(src ? src : "", file ? file : "");
+  if (!po.program) {
+    out = errorJson(po.diagnostics);
+    return HGRD_GPU_OK;
+  }
+  std::string fileName = po.program->file;
+  auto cp = compileProgram(std::move(po.program));
+  SweepShard r = sweepShard(*cp, caps, rank, world, be);
+  if (r.error) {
+    out = errorJson({"backend: " + r.errorMessage});
+    return r.error;
+  }
+  out = sweepShardJson(r, fileName);
+  return HGRD_GPU_OK;
 }
 
 int runConcreteJson(LaunchBackend &be, const char *src, const char *file,

@@ -129,6 +129,26 @@ RunResult runConcrete(CompiledProgram &prog, const ExecConfig &cfg,
                       LaunchBackend &backend);
 SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
                              LaunchBackend &backend);
+// One rank's share of enumerateVerdict's configuration lattice: the
+// configs with canonical index k (warp-size major, input odometer minor,
+// k <= maxConfigs) and k % world == rank, each with its sorted races.
+struct ShardConfig {
+  uint64_t index = 0;
+  int64_t warpSize = 0;
+  std::vector<Race> races;
+};
+struct SweepShard {
+  uint64_t total = 0; // configs the full sweep runs
+  std::vector<ShardConfig> configs;
+  RunStats stats;
+  int error = 0;
+  std::string errorMessage;
+};
+SweepShard sweepShard(CompiledProgram &prog, const SweepCaps &caps, int rank, int world,
+                      LaunchBackend &backend);
+std::string sweepShardJson(const SweepShard &r, const std::string &file);
+int sweepShardJsonRun(LaunchBackend &be, const char *src, const char *file,
+                      const char *capsJson, int rank, int world, std::string &out);
 int countInputs(const Program &p);                 // oracle.cpp:805-861
 bool hasIndirectIndexing(const Program &p);        // oracle.cpp:86-123
 

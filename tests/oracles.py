@@ -70,6 +70,8 @@ class CpuOracle:
             getattr(self.lib, fn).argtypes = [ctypes.c_char_p] * 3 + [ctypes.POINTER(P)]
         self.lib.hgrd_oracle_free.argtypes = [P]
         self.lib.hgrd_oracle_check_launch.argtypes = [P, P, P, ctypes.c_int32, P]
+        self.lib.hgrd_oracle_sweep_shard_json.argtypes = [ctypes.c_char_p] * 3 + [
+            ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
 
     def _call(self, fn, source, cfg, file_name) -> dict:
         out = ctypes.c_void_p()
@@ -87,6 +89,17 @@ class CpuOracle:
 
     def enumerate_verdict(self, source: str, caps=None, file_name: str = "prog.mcu") -> dict:
         return self._call("hgrd_oracle_enumerate_verdict_json", source, caps, file_name)
+
+    def sweep_shard(self, source: str, caps=None, file_name: str = "prog.mcu",
+                    rank: int = 0, world: int = 1) -> dict:
+        out = ctypes.c_void_p()
+        rc = self.lib.hgrd_oracle_sweep_shard_json(source.encode(), file_name.encode(),
+                                                    _cfg(caps), rank, world, ctypes.byref(out))
+        s = ctypes.string_at(out.value).decode()
+        self.lib.hgrd_oracle_free(out)
+        if rc != 0:
+            raise RuntimeError(f"sweep_shard failed ({rc}): {s}")
+        return json.loads(s)
 
     def check_launch(self, spec, buffers, trap_cap: int = 256) -> dict:
         """Check one LaunchSpec against int64 numpy buffers (handle = list index)."""

@@ -1,0 +1,86 @@
+"""Multi-rank sharding of the sweep (paper_2604_02106_b200/parallel.py).
+
+CPU tests: world_size-2 gloo process groups where each rank runs its shard of
+the configuration lattice through the CPU restatement (the same host code the
+GPU library runs, behind the same shard entry point), gathers, merges, and
+must reproduce the reference's own single-process enumerateVerdict output
+(tests/golden).  The GPU test checks hgrd_gpu_sweep_shard_json on one device
+for every (rank, world) split."""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import load_golden
+from paper_2604_02106_b200.parallel import (enumerate_verdict_distributed, merge_shards,
+                                            shard_jobs)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_merge_shards_any_world(cpu_oracle):
+    corpus = load_golden("corpus")
+    for e in corpus:
+        for world in (1, 2, 3, 8):
+            shards = [cpu_oracle.sweep_shard(e["source"], e["caps"], e["file"], r, world)
+                      for r in range(world)]
+            got = merge_shards(shards)
+            assert got["races"] == e["sweep_manifest"]["races"], (e["name"], world)
+            assert sum(len(s["configs"]) for s in shards) == got["configs"]
+
+
+def _worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracles import CpuOracle
+    ora = CpuOracle()
+    bad = []
+    for e in load_golden("corpus"):
+        got = enumerate_verdict_distributed(ora.sweep_shard, e["source"], e["caps"], e["file"])
+        if got["races"] != e["sweep_manifest"]["races"]:
+            bad.append(e["name"])
+    for f in load_golden("fuzz")[:60]:
+        got = enumerate_verdict_distributed(ora.sweep_shard, f["source"], {}, "fuzz.mcu")
+        if got["races"] != f["sweep"]["races"]:
+            bad.append(f["index"])
+    with open(f"{out_path}.{rank}", "w") as fh:
+        fh.write(repr(bad))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sweep_matches_reference(tmp_path):
+    world = 2
+    out = str(tmp_path / "res")
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        assert open(f"{out}.{r}").read() == "[]"
+
+
+def test_shard_jobs_partition():
+    jobs = [{"id": i, "cost": (i % 7) + 1} for i in range(100)]
+    parts = [shard_jobs(jobs, r, 4) for r in range(4)]
+    ids = sorted(j["id"] for p in parts for j in p)
+    assert ids == list(range(100))
+    loads = [sum(j["cost"] for j in p) for p in parts]
+    assert max(loads) - min(loads) <= 7
+
+
+@pytest.mark.gpu
+def test_gpu_sweep_shards(gpu):
+    for e in load_golden("corpus"):
+        for world in (1, 2, 4):
+            shards = [gpu.sweep_shard(e["source"], e["caps"], e["file"], r, world)
+                      for r in range(world)]
+            assert merge_shards(shards)["races"] == e["sweep_manifest"]["races"], e["name"]

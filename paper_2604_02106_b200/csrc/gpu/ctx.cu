@@ -91,6 +91,9 @@ struct hgrd_gpu_ctx {
   DevVec<unsigned long long> keyElem;  // fused path: per key minimum element
   DevVec<Candidate> cand;
   DevVec<Counters> ctr2;               // fused pass 2 counters
+  DevVec<uint32_t> interTab;           // fused pass 2: (element, site) block sets
+  DevVec<unsigned long long> interKeyElem;
+  DevVec<uint64_t> targets;
   bool fusedEnabled = true;
   // NVRTC specialisation: 0 off, 1 auto (large launches), 2 always
   int jitMode = 1;
@@ -718,6 +721,57 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   D2.ctr = c->ctr2.p;
   D2.ownerFilter = c->owner.p;
   D2.ownerMultiTag = (c->epoch << 20) | kOwnerMulti;
+  const size_t sm2 = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
+                     sizeof(ParamDev) * P.params.size();
+  const unsigned grid2 = static_cast<unsigned>(std::min<uint64_t>(
+      ((static_cast<uint64_t>(D.nThreads) + 31) / 32 + 7) / 8, uint64_t(c->nSM) * 8));
+  {
+    // 2a: record-free INTER summary of the shared elements, then the realised
+    //     INTER keys and their first-found (minimum) elements
+    const size_t nTab = static_cast<size_t>(P.totalW) * L.n_sites;
+    NEED(c->interTab, nTab);
+    CK(cudaMemsetAsync(c->interTab.p, 0xff, nTab * 4, c->st));
+    NEED(c->interKeyElem, static_cast<size_t>(nKeys));
+    CK(cudaMemsetAsync(c->interKeyElem.p, 0xff, 8 * static_cast<size_t>(nKeys), c->st));
+    CK(cudaMemsetAsync(c->ctr2.p, 0, sizeof(Counters), c->st));
+    LaunchDev Ds = D2;
+    Ds.interTab = c->interTab.p;
+    Ds.nSitesTab = static_cast<int>(L.n_sites);
+    Ds.keys = nullptr;
+    Ds.vals = nullptr;
+    Ds.capacity = 0;
+    Ds.chunk = 64;
+    const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
+    rc = launchExpandPar(c, Ds, grid2, sm2, jx,
+                         jx ? "k_expand_par_inter[jit]" : "k_expand_par_inter");
+    if (rc < 0)
+      return rc;
+    {
+      StageTimer t(c, "k_inter_scan");
+      k_inter_scan<<<static_cast<unsigned>((P.totalW + 255) / 256), 256, 0, c->st>>>(
+          c->owner.p, D2.ownerMultiTag, P.totalW, c->interTab.p, static_cast<int>(L.n_sites),
+          D.sites, D.confInter, nLocs, c->interKeyElem.p);
+    }
+    CK(cudaGetLastError());
+    c->kernelLaunches += 1;
+    std::vector<unsigned long long> ke(static_cast<size_t>(nKeys));
+    CK(cudaMemcpyAsync(ke.data(), c->interKeyElem.p, 8 * static_cast<size_t>(nKeys),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<uint64_t> targets;
+    for (int K = 0; K < nKeys; K += 3)
+      if (ke[static_cast<size_t>(K)] != ~0ull)
+        targets.push_back(ke[static_cast<size_t>(K)]);
+    std::sort(targets.begin(), targets.end());
+    targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
+    if (targets.empty())
+      return fetchRaces(c, R) < 0 ? -1 : 1; // no INTER race (pass-1 races stand)
+    NEED(c->targets, targets.size());
+    CK(cudaMemcpy(c->targets.p, targets.data(), 8 * targets.size(), cudaMemcpyHostToDevice));
+    // 2b: records of only those elements -> first pairs (witnesses)
+    D2.targets = c->targets.p;
+    D2.nTargets = static_cast<int>(targets.size());
+  }
   int bP = D.kl.bP, bQ = D.kl.bQ;
   for (int attempt = 0; attempt < 8; ++attempt) {
     if (!makeLayout(D2.kl, D.kl.bE, D.kl.bB, bP, D.kl.bW, bQ, D.kl.bL)) {
@@ -727,8 +781,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     const uint64_t nBatches = (static_cast<uint64_t>(D.nThreads) + 31) / 32;
     const uint64_t blocks = std::min<uint64_t>((nBatches + 7) / 8, uint64_t(c->nSM) * 8);
     const uint64_t warps = blocks * 8;
-    const uint64_t chunk = std::clamp<uint64_t>(h.records / std::max<uint64_t>(warps, 1) / 4, 64, kChunk);
-    uint64_t cap = std::max<uint64_t>(h.records + warps * chunk + 4096, c->capHint);
+    const uint64_t chunk = 64;
+    uint64_t cap = std::max<uint64_t>(warps * chunk * 2 + (uint64_t(1) << 20), c->capHint);
     D2.chunk = static_cast<uint32_t>(chunk);
     NEED(c->keys, cap);
     NEED(c->vals, cap);
@@ -1154,6 +1208,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   f(c->order), f(c->orderAlt), f(c->cubTemp), f(c->blob), f(c->snapshot), f(c->keySeg);
   f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
   f(c->opSeq), f(c->opStart), f(c->traps), f(c->owner), f(c->keyElem), f(c->cand), f(c->ctr2);
+  f(c->interTab), f(c->interKeyElem), f(c->targets);
   for (char *ch : c->chunks)
     cudaFree(ch);
   for (auto &b : c->bigUsed)

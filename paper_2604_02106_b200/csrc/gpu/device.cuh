@@ -141,6 +141,10 @@ struct LaunchDev {
   // pass 2 of the fused path: only elements the ownership table marks MULTI
   const uint32_t *ownerFilter;
   uint32_t ownerMultiTag;
+  uint32_t *interTab;        // INTER summary mode: (element, site) block sets
+  int nSitesTab;
+  const uint64_t *targets;   // witness mode: only these elements
+  int nTargets;
   // 32-bit thread identity (nThreads < 2^32): tpb, bx, bx*by, gx, gx*gy, ws
   bool small;
   FastDiv dTpb, dBx, dBxBy, dGx, dGxGy, dWs;

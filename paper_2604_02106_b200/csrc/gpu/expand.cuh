@@ -41,6 +41,60 @@ struct LaneTally {
   }
 };
 
+// Per (element, site) block set of the INTER summary: EMPTY, a single block,
+// or MULTI.  Atomics only on state changes; repeated blocks are plain reads.
+constexpr uint32_t kInterEmpty = 0xffffffffu, kInterMulti = 0xfffffffeu;
+__device__ __forceinline__ void interUpdate(uint32_t *w, uint32_t block) {
+  uint32_t v = *reinterpret_cast<volatile uint32_t *>(w);
+  if (v == block || v == kInterMulti)
+    return;
+  if (v == kInterEmpty) {
+    v = atomicCAS(w, kInterEmpty, block);
+    if (v == kInterEmpty || v == block || v == kInterMulti)
+      return;
+  }
+  atomicExch(w, kInterMulti);
+}
+
+// Realised INTER keys from the summary table, one thread per element the
+// ownership table marks MULTI: sites s1, s2 (static conflict) race across
+// blocks iff their block sets' union has two members.  Per key the minimum
+// element (the reference's first-found element, :745).
+__global__ void k_inter_scan(const uint32_t *owner, uint32_t multiTag, uint64_t nElems,
+                             const uint32_t *tab, int nSites, const SiteDev *sites,
+                             const uint64_t *confInter, int nLocs,
+                             unsigned long long *keyElem) {
+  const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nElems || owner[e] != multiTag)
+    return;
+  const uint32_t *w = tab + e * static_cast<uint64_t>(nSites);
+  for (int a = 0; a < nSites; ++a) {
+    const uint32_t wa = w[a];
+    if (wa == kInterEmpty)
+      continue;
+    for (int b = a; b < nSites; ++b) {
+      if (!((confInter[a] >> b) & 1ull))
+        continue;
+      const uint32_t wb = w[b];
+      if (wb == kInterEmpty)
+        continue;
+      const bool realised = a == b ? wa == kInterMulti
+                                   : (wa == kInterMulti || wb == kInterMulti || wa != wb);
+      if (!realised)
+        continue;
+      int la = sites[a].loc, lb = sites[b].loc;
+      if (lb < la) {
+        const int t = la;
+        la = lb;
+        lb = t;
+      }
+      const int K = (la * nLocs + lb) * 3; // kind 0: INTER-BLOCK
+      if (keyElem[K] > e)
+        atomicMin(&keyElem[K], static_cast<unsigned long long>(e));
+    }
+  }
+}
+
 // PARALLEL sink of k_expand_par: packed records into the lane buffer.
 struct ParSink : ParState {
   LaneRecords *out;
@@ -51,6 +105,18 @@ struct ParSink : ParState {
     const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
     if (L->ownerFilter && L->ownerFilter[e] != L->ownerMultiTag)
       return; // fused pass 2: only elements shared by blocks
+    if (L->interTab) { // INTER summary: EMPTY -> one block -> MULTI, no record
+      interUpdate(&L->interTab[e * static_cast<uint64_t>(L->nSitesTab) + site],
+                  static_cast<uint32_t>(block));
+      return;
+    }
+    if (L->nTargets) { // witness pass: only the keys' first-found elements
+      bool hit = false;
+      for (int i = 0; i < L->nTargets; ++i)
+        hit |= L->targets[i] == e;
+      if (!hit)
+        return;
+    }
     const KeyLayout &kl = L->kl;
     const uint64_t maskP = fieldMask(kl.bP), maskQ = fieldMask(kl.bQ);
     if (bp > maskP || wp > maskQ)

@@ -208,3 +208,17 @@ def test_jit_used_for_large_launches(gpu):
     names = [s["name"] for s in gpu.last_profile()]
     gpu.set_profiling(False)
     assert any(n.endswith("[jit]") for n in names), (names, gpu.jit_info())
+
+
+@pytest.mark.parametrize("bins", [1 << 16, 65521])
+@pytest.mark.parametrize("update", ["atomic_block", "store", "atomic"])
+def test_full_histogram_2p27(gpu, cpu_oracle, bins, update):
+    """configs[3]: 2^27 threads, 2^28 instances, data-dependent bins.  The
+    first two threads that hit bin 0 are i0 and i0 + bins (< 2^17), so the
+    full-size report (races, addresses, witnesses) equals the 2^17 oracle's."""
+    spec, _ = _spec_hist(gpu, 1 << 27, bins, update)
+    got = gpu.check_launch(spec)
+    small, bufs = _spec_hist(None, 1 << 17, bins, update)
+    want = cpu_oracle.check_launch(small, bufs)
+    assert got["races"] == want["races"]
+    assert got["instances"] == 2 << 27

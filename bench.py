@@ -77,7 +77,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -159,6 +159,7 @@ def run_reference_arm(args):
 
 
 def build_specs(hg, ctx):
+    import torch
     specs = []
     for barrier in (False, True):
         src = programs.stencil(N_THREADS, BLOCK, barrier)
@@ -167,7 +168,9 @@ def build_specs(hg, ctx):
         handles = {k: ctx.alloc(v) for k, v in sizes.items()}
         spec = hg.LaunchSpec(low, (N_THREADS // BLOCK, 1, 1), (BLOCK, 1, 1), WS,
                              handles=handles)
-        host = {k: np.zeros(v, np.int64) for k, v in sizes.items()}  # reference buffers_
+        # the reference's buffers_ (zero-initialised int64), in pinned host memory
+        host = {k: torch.zeros(v, dtype=torch.int64, pin_memory=True).numpy()
+                for k, v in sizes.items()}
         specs.append((spec, handles, host))
     return specs
 
@@ -208,7 +211,12 @@ def run_gpu_arm(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    # clocks: sample across a >= 1 s run of the same steps right before the
+    # timed region and through it (the timed region alone is milliseconds)
     clocks = Clocks(local)
+    t_probe = time.perf_counter()
+    while time.perf_counter() - t_probe < 1.0:
+        step()
     launches0 = ctx.kernel_launches()
     barrier()
     dev_ms = 0.0

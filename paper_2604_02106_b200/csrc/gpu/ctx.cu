@@ -500,13 +500,24 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
         k_detect_summary<<<g, 256, 0, c->st>>>(A, c->keySeg.p);
       }
       CK(cudaGetLastError());
-      {
+      if (kindMask & 6) {
+        DetectArgs Ai = A;
+        Ai.kindMask = kindMask & 6;
         StageTimer t(c, "k_witness");
-        k_witness<<<(nKeys + 127) / 128, 128, 0, c->st>>>(A, c->keySeg.p, nKeys, c->curRaces,
+        k_witness<<<(nKeys + 127) / 128, 128, 0, c->st>>>(Ai, c->keySeg.p, nKeys, c->curRaces,
                                                            c->cur);
+        ++c->kernelLaunches;
       }
       CK(cudaGetLastError());
-      c->kernelLaunches += 2;
+      if (kindMask & 1) { // INTER-BLOCK: warp per key (hot elements)
+        StageTimer t(c, "k_witness_inter");
+        const int warps = (nKeys + 2) / 3;
+        k_witness_inter<<<(warps + 7) / 8, 256, 0, c->st>>>(A, c->keySeg.p, nKeys, c->curRaces,
+                                                             c->cur);
+        ++c->kernelLaunches;
+      }
+      CK(cudaGetLastError());
+      ++c->kernelLaunches;
     } else {
       // canonical-order records, stable sort by element
       A.keys = c->keys.p;

@@ -265,6 +265,122 @@ __global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
   o.seq_y = static_cast<int32_t>(bestY & kSeqMask);
 }
 
+// INTER-BLOCK witness, one warp per key: the whole element segment is one
+// group (level id = block), so the three passes of k_witness become warp
+// reductions — hot elements (histogram bins) have thousands of events.
+__global__ void k_witness_inter(DetectArgs A, const uint32_t *keySeg, int nKeys,
+                                hgrd_gpu_race *races, Counters *ctr) {
+  __shared__ uint32_t smx[8][kMaxSites];
+  __shared__ unsigned long long spres[8];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = (blockIdx.x * (blockDim.x >> 5) + wid) * 3; // kind 0 keys only
+  if (K >= nKeys)
+    return;
+  const uint32_t s = keySeg[K];
+  if (s == 0xffffffffu)
+    return;
+  const KeyLayout kl = A.kl;
+  const int la = (K / 3) / A.nLocs, lb = (K / 3) % A.nLocs;
+  const uint64_t elem = A.keys[s] >> kl.shE;
+  // segment end: lanes probe ahead in strides of 32
+  uint64_t e = s;
+  for (;;) {
+    const uint64_t p = e + lane;
+    const bool in = p < A.n && (A.keys[p] >> kl.shE) == elem;
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if (m != 0xffffffffu) {
+      e += __popc(m);
+      break;
+    }
+    e += 32;
+  }
+  uint32_t *mx = smx[wid];
+  if (lane == 0)
+    spres[wid] = 0;
+  for (int i = lane; i < kMaxSites; i += 32)
+    mx[i] = 0;
+  __syncwarp();
+  for (uint64_t p = s + lane; p < e; p += 32) {
+    const int st = static_cast<int>(A.vals[p] >> kSeqBits);
+    atomicMax(&mx[st], static_cast<uint32_t>((A.keys[p] >> kl.shB) & fieldMask(kl.bB)));
+    atomicOr(&spres[wid], 1ull << st);
+  }
+  __syncwarp();
+  const uint64_t pres = spres[wid];
+  // x: earliest event with a partner in a later block
+  uint64_t bx = ~0ull, bpm = 0, bxi = s;
+  for (uint64_t p = s + lane; p < e; p += 32) {
+    const int st = static_cast<int>(A.vals[p] >> kSeqBits);
+    const int loc = A.sites[st].loc;
+    if (loc != la && loc != lb)
+      continue;
+    const uint64_t pm = A.confInter[st] & A.locMask[loc == la ? lb : la] & pres;
+    const uint32_t id = static_cast<uint32_t>((A.keys[p] >> kl.shB) & fieldMask(kl.bB));
+    bool later = false;
+    for (uint64_t m = pm; m && !later; m &= m - 1)
+      later = mx[__ffsll(static_cast<long long>(m)) - 1] > id;
+    if (!later)
+      continue;
+    const uint64_t ord = eventOrder(A, A.keys[p], A.vals[p]);
+    if (ord < bx) {
+      bx = ord;
+      bpm = pm;
+      bxi = p;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ox = __shfl_down_sync(0xffffffffu, bx, o);
+    const uint64_t om = __shfl_down_sync(0xffffffffu, bpm, o);
+    const uint64_t oi = __shfl_down_sync(0xffffffffu, bxi, o);
+    if (ox < bx) {
+      bx = ox;
+      bpm = om;
+      bxi = oi;
+    }
+  }
+  bx = __shfl_sync(0xffffffffu, bx, 0);
+  bpm = __shfl_sync(0xffffffffu, bpm, 0);
+  bxi = __shfl_sync(0xffffffffu, bxi, 0);
+  if (bx == ~0ull)
+    return;
+  // y: earliest partner event in a later block
+  const uint32_t idx = static_cast<uint32_t>((A.keys[bxi] >> kl.shB) & fieldMask(kl.bB));
+  uint64_t by = ~0ull, byi = bxi;
+  for (uint64_t p = s + lane; p < e; p += 32) {
+    const int st = static_cast<int>(A.vals[p] >> kSeqBits);
+    if (!((bpm >> st) & 1ull) ||
+        static_cast<uint32_t>((A.keys[p] >> kl.shB) & fieldMask(kl.bB)) <= idx)
+      continue;
+    const uint64_t ord = eventOrder(A, A.keys[p], A.vals[p]);
+    if (ord < by) {
+      by = ord;
+      byi = p;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t oy = __shfl_down_sync(0xffffffffu, by, o);
+    const uint64_t oi = __shfl_down_sync(0xffffffffu, byi, o);
+    if (oy < by) {
+      by = oy;
+      byi = oi;
+    }
+  }
+  if (lane != 0)
+    return;
+  const unsigned pos = atomicAdd(&ctr->nRaces, 1u);
+  hgrd_gpu_race &o = races[pos];
+  o.loc_a = la;
+  o.loc_b = lb;
+  o.kind = 0;
+  o.site_x = static_cast<int32_t>(A.vals[bxi] >> kSeqBits);
+  o.site_y = static_cast<int32_t>(A.vals[byi] >> kSeqBits);
+  elementOf(A, elem, o.handle, o.index);
+  o.thread_x = static_cast<int64_t>(bx >> kSeqBits);
+  o.seq_x = static_cast<int32_t>(bx & kSeqMask);
+  o.thread_y = static_cast<int64_t>(by >> kSeqBits);
+  o.seq_y = static_cast<int32_t>(by & kSeqMask);
+}
+
 // ---------------------------------------------------------------------------
 // Pairwise path (lock idioms).  Records are in canonical event order;
 // order[] is the stable sort of record indices by element.

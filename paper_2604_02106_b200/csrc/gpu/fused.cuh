@@ -4,11 +4,12 @@
 // INTRA-BLOCK / INTRA-WARP pair lies inside one MiniCU block
 // (reference src/oracle.cpp:754-769), so they are found entirely on chip:
 //   1. expansion into shared memory (records: global element id + meta),
-//   2. grouping: records hashed by element into 2x-oversized slots with a
-//      one-pass counting sort (a slot with more than kSmallGroup records —
-//      a hot element — switches the iteration to a CUB block radix sort of
-//      element | block | bp | warp | wp | lane and per-group summaries),
-//   3. one thread per record pairs it with the earlier records of its slot
+//   2. grouping: as it is produced, each record is pushed onto the chain of
+//      its element's hash slot (2x-oversized table, one shared atomicExch);
+//      a chain longer than kSmallGroup (a hot element) switches the
+//      iteration to a CUB block radix sort of
+//      element | block | bp | warp | wp | lane and per-group summaries,
+//   3. one thread per record pairs it with the earlier records of its chain
 //      (same element): realised INTRA keys and, per key, the minimum element,
 //   4. per realised key: the first (x, y) pair of the reference's order
 //      inside that element, published as a candidate (global element via
@@ -114,23 +115,23 @@ template <int IPT> struct FusedSmem {
   static constexpr int kCap = kFusedThreads * IPT;
   static constexpr int kTable = 2 * kCap; // hash slots (power of two)
   static constexpr int kLogTable = IPT == 4 ? 11 : 13;
+  static constexpr uint32_t kEnd = 0xffffffffu;
   using Sort = cub::BlockRadixSort<uint64_t, kFusedThreads, IPT, uint32_t, 5>;
   union {
     typename Sort::TempStorage sortTmp;
     struct {
-      uint32_t cnt[kTable]; // per slot: count, then start offset
-      uint16_t rank[kCap];  // record's rank inside its slot
-      uint32_t part[kFusedThreads];
-    } cs;
-    uint64_t skey[kCap];    // radix mode: sorted keys
+      uint32_t head[kTable]; // per hash slot: most recent record (chain head)
+      uint32_t next[kCap];   // per record: previous record of its slot
+    } ch;
+    struct {
+      uint64_t skey[kCap];  // radix mode: sorted keys
+      uint32_t sidx[kCap];  // sorted position -> record index
+    } rx;
   } u;
   uint64_t elem[kCap];  // global element id, by record index
   uint64_t meta[kCap];  // tli:16 | bp:8 | wp:8 | site:12 | seq:20
-  uint64_t selem[kCap]; // grouped order
-  uint64_t smeta[kCap];
   unsigned long long minE[kMaxWritten], maxE[kMaxWritten];
-  unsigned int count, maxBp, maxWp, nReal, flags, maxGroup;
-  int hashed; // 1: hash-slot grouping, 0: radix grouping
+  unsigned int count, maxBp, maxWp, nReal, flags, hot;
   // radix mode: field start bits of the key  w|off|blk|bp|warp|wp|lane
   int fWp, fWarp, fBp, fBlk, fOff, fW, total;
 };
@@ -151,7 +152,8 @@ template <int IPT> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
   return static_cast<uint32_t>((e * 0x9E3779B97F4A7C15ull) >> (64 - FusedSmem<IPT>::kLogTable));
 }
 
-// PARALLEL sink of the fused kernel: records into shared memory.
+// PARALLEL sink of the fused kernel: records into shared memory, each
+// pushed onto the chain of its element's hash slot.
 template <int IPT> struct FusedSink : ParState {
   FusedSmem<IPT> *S;
   uint32_t tli; // thread index within the iteration
@@ -171,8 +173,10 @@ template <int IPT> struct FusedSink : ParState {
     base = __shfl_sync(act, base, leader);
     const unsigned pos = base + __popc(act & ((1u << ln) - 1));
     if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
-      S->elem[pos] = P->elemBase + static_cast<uint64_t>(idx);
+      const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
+      S->elem[pos] = e;
       S->meta[pos] = packMeta(tli, bp, wp, site, seq);
+      S->u.ch.next[pos] = atomicExch(&S->u.ch.head[hashSlot<IPT>(e)], pos);
     } else {
       flags |= kFlagFusedOverflow;
     }
@@ -290,12 +294,13 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       S.count = 0;
       S.maxBp = 0;
       S.maxWp = 0;
-      S.maxGroup = 0;
+      S.hot = 0;
     }
     for (int i = tid; i < Smem::kTable; i += kFusedThreads)
-      S.u.cs.cnt[i] = 0;
+      S.u.ch.head[i] = Smem::kEnd;
     __syncthreads();
-    // 1. expansion of the iteration's whole MiniCU blocks
+    // 1. expansion of the iteration's whole MiniCU blocks (records chained
+    //    per hash slot as they are produced)
     {
       unsigned myBp = 0, myWp = 0;
       for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
@@ -330,70 +335,51 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       continue;
     if (F.ablate & 1)
       continue;
-    // 2. grouping: records hashed by element into slots (counting sort);
-    //    a slot holding many records (a hot element) falls back to a
-    //    block radix sort of the full key for this iteration
-    {
-      unsigned myMax = 0;
-      for (unsigned i = tid; i < n; i += kFusedThreads) {
-        const uint32_t slot = hashSlot<IPT>(S.elem[i]);
-        const unsigned r = atomicAdd(&S.u.cs.cnt[slot], 1u);
-        S.u.cs.rank[i] = static_cast<uint16_t>(r);
-        myMax = max(myMax, r + 1);
+    // 2. detection, hash mode: each record pairs with the earlier records of
+    //    its slot's chain that hold the same element
+    OwnerPending owners;
+    for (unsigned p = tid; p < n && !(F.ablate & 2); p += kFusedThreads) {
+      const uint64_t e = S.elem[p];
+      const uint64_t m = S.meta[p];
+      const uint32_t bp_ = L.dTpb.div(metaTli(m));
+      const int sp = metaSite(m);
+      bool first = true;
+      int len = 0;
+      for (uint32_t q = S.u.ch.next[p]; q != Smem::kEnd; q = S.u.ch.next[q]) {
+        if (++len > kSmallGroup) { // a hot element: radix grouping instead
+          S.hot = 1;
+          break;
+        }
+        if (S.elem[q] != e)
+          continue;
+        const uint64_t mq = S.meta[q];
+        if (L.dTpb.div(metaTli(mq)) == bp_)
+          first = false;
+        const int kind = intraKind(L, sSites, mq, m, tpb);
+        if (kind < 0)
+          continue;
+        const int sq = metaSite(mq);
+        if (!((sConf[sq] >> sp) & 1ull))
+          continue;
+        noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, sq, sp, kind), e);
       }
-      if (myMax > kSmallGroup)
-        atomicMax(&S.maxGroup, myMax);
+      if (first && !(F.ablate & 4))
+        owners.issue(F, e, static_cast<uint64_t>(firstBlock + bp_), myFlags);
     }
     __syncthreads();
-    const bool hashed = S.maxGroup <= kSmallGroup;
-    if (hashed) {
-      // exclusive scan of the slot counts: per-thread chunks + one warp
-      constexpr int per = Smem::kTable / kFusedThreads;
-      const int b0 = tid * per;
-      uint32_t sum = 0;
-#pragma unroll
-      for (int i = 0; i < per; ++i)
-        sum += S.u.cs.cnt[b0 + i];
-      S.u.cs.part[tid] = sum;
-      __syncthreads();
-      if (tid < 32) {
-        uint32_t acc = 0;
-        for (int k = 0; k < kFusedThreads / 32; ++k) {
-          const uint32_t v = S.u.cs.part[k * 32 + tid];
-          uint32_t incl = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (tid >= o)
-              incl += y;
-          }
-          S.u.cs.part[k * 32 + tid] = acc + incl - v;
-          acc += __shfl_sync(0xffffffffu, incl, 31);
-        }
-      }
-      __syncthreads();
-      uint32_t run = S.u.cs.part[tid];
-#pragma unroll
-      for (int i = 0; i < per; ++i) {
-        const uint32_t c0 = S.u.cs.cnt[b0 + i];
-        S.u.cs.cnt[b0 + i] = run;
-        run += c0;
-      }
-      __syncthreads();
-      for (unsigned i = tid; i < n; i += kFusedThreads) {
-        const uint64_t e = S.elem[i];
-        const uint32_t pos = S.u.cs.cnt[hashSlot<IPT>(e)] + S.u.cs.rank[i];
-        S.selem[pos] = e;
-        S.smeta[pos] = S.meta[i];
-      }
-      __syncthreads();
-    } else {
-      // radix mode: key w | off | blk | bp | warp | wp | lane over element offsets
+    const bool hashed = S.hot == 0;
+    if (!hashed) {
+      // radix mode for this iteration: drop the hash-mode keys, sort by
+      // w | off | blk | bp | warp | wp | lane and summarise per group
+      for (unsigned r = tid; r < S.nReal; r += kFusedThreads)
+        sKeyMin[sReal[r]] = ~0ull;
       if (tid < kMaxWritten) {
         S.minE[tid] = ~0ull;
         S.maxE[tid] = 0;
       }
       __syncthreads();
+      if (tid == 0)
+        S.nReal = 0;
       for (unsigned i = tid; i < n; i += kFusedThreads) {
         const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
         atomicMin(&S.minE[w], static_cast<unsigned long long>(S.elem[i]));
@@ -451,67 +437,27 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < IPT; ++j) {
-        const int p = tid * IPT + j;
-        S.u.skey[p] = keys[j];
-        if (p < static_cast<int>(n)) {
-          S.selem[p] = S.elem[vals[j]];
-          S.smeta[p] = S.meta[vals[j]];
-        }
+        S.u.rx.skey[tid * IPT + j] = keys[j];
+        S.u.rx.sidx[tid * IPT + j] = vals[j];
       }
       __syncthreads();
-    }
-    // 3. detection
-    OwnerPending owners;
-    if (hashed) {
-      // one thread per record: pairs with the earlier records of its slot
-      for (unsigned p = tid; p < n && !(F.ablate & 2); p += kFusedThreads) {
-        const uint64_t e = S.selem[p];
-        const uint64_t m = S.smeta[p];
-        const uint32_t slot = hashSlot<IPT>(e);
-        const uint32_t gs = S.u.cs.cnt[slot];
-        const uint32_t bp_ = L.dTpb.div(metaTli(m));
-        const int sp = metaSite(m);
-        bool first = true;
-        for (uint32_t q = gs; q < p; ++q) {
-          if (S.selem[q] != e)
-            continue;
-          const uint64_t mq = S.smeta[q];
-          if (L.dTpb.div(metaTli(mq)) == bp_)
-            first = false;
-          const int kind = intraKind(L, sSites, mq, m, tpb);
-          if (kind < 0)
-            continue;
-          const int sq = metaSite(mq);
-          if (!((sConf[sq] >> sp) & 1ull))
-            continue;
-          noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, sq, sp, kind), e);
-        }
-        if (first && !(F.ablate & 4))
-          owners.issue(F, e, static_cast<uint64_t>(firstBlock + bp_), myFlags);
-      }
-    } else {
-      // radix mode: one thread per element group (hot elements)
-      const int shLane = S.fWp, shBpF = S.fBp, shBlkF = S.fBlk, shElem = S.fOff;
+      // one thread per element group
+      const int shLane = S.fWp, shBpF = S.fBp, shElem = S.fOff;
       for (int j = 0; j < IPT; ++j) {
         const int p = tid * IPT + j;
         if (p >= static_cast<int>(n))
           break;
-        const uint64_t g = S.u.skey[p] >> shElem;
-        if (p > 0 && (S.u.skey[p - 1] >> shElem) == g)
+        const uint64_t g = S.u.rx.skey[p] >> shElem;
+        if (p > 0 && (S.u.rx.skey[p - 1] >> shElem) == g)
           continue;
         int e = p + 1;
-        while (e < static_cast<int>(n) && (S.u.skey[e] >> shElem) == g)
+        while (e < static_cast<int>(n) && (S.u.rx.skey[e] >> shElem) == g)
           ++e;
-        const uint64_t ge = S.selem[p];
-        for (int q = p; q < e; ++q)
-          if (q == p || (S.u.skey[q] >> shBlkF) != (S.u.skey[q - 1] >> shBlkF))
-            owners.issue(F, ge, static_cast<uint64_t>(firstBlock + L.dTpb.div(metaTli(S.smeta[q]))),
-                         myFlags);
         if (e - p < 2)
           continue;
         uint32_t mn2[kMaxSites], mx2[kMaxSites], mn3[kMaxSites], mx3[kMaxSites];
         uint64_t p2 = 0, p3 = 0;
-        uint64_t g2 = S.u.skey[p] >> shBpF, g3 = S.u.skey[p] >> shLane;
+        uint64_t g2 = S.u.rx.skey[p] >> shBpF, g3 = S.u.rx.skey[p] >> shLane;
         auto flush = [&](uint64_t pres, const uint32_t *mn, const uint32_t *mx, int kind) {
           uint64_t rem = pres;
           while (rem) {
@@ -528,7 +474,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
           }
         };
         for (int q = p; q < e; ++q) {
-          const uint64_t k = S.u.skey[q];
+          const uint64_t k = S.u.rx.skey[q];
           if ((k >> shBpF) != g2) {
             flush(p2, mn2, mx2, 1);
             p2 = 0;
@@ -539,7 +485,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
             p3 = 0;
             g3 = k >> shLane;
           }
-          const uint64_t m = S.smeta[q];
+          const uint64_t m = S.meta[S.u.rx.sidx[q]];
           const int s = metaSite(m);
           const uint32_t tli = metaTli(m);
           const uint32_t tl = tli - L.dTpb.div(tli) * tpb;
@@ -550,9 +496,9 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
         flush(p2, mn2, mx2, 1);
         flush(p3, mn3, mx3, 2);
       }
+      __syncthreads();
     }
-    __syncthreads();
-    // 4. witnesses of the keys realised in this iteration
+    // 3. witnesses of the keys realised in this iteration
     const unsigned nReal = S.nReal;
     for (unsigned r = tid; r < nReal; r += kFusedThreads) {
       const int K = static_cast<int>(sReal[r]);
@@ -560,24 +506,32 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       const int la = (K / 3) / F.nLocs, lb = (K / 3) % F.nLocs;
       const unsigned long long v = sKeyMin[K];
       sKeyMin[K] = ~0ull; // reset for the next iteration
-      // the key's minimum element in this iteration and its record range
+      // the key's minimum element in this iteration: its records are the
+      // slot chain (hash mode) or a sorted range (radix mode)
       uint64_t ge;
-      uint32_t g0, g1;
+      uint32_t g0 = 0, g1 = 0;
       if (hashed) {
         ge = v;
-        const uint32_t slot = hashSlot<IPT>(ge);
-        g0 = S.u.cs.cnt[slot];
-        g1 = slot + 1 < static_cast<uint32_t>(Smem::kTable) ? S.u.cs.cnt[slot + 1] : n;
       } else {
         g0 = static_cast<uint32_t>(v);
-        ge = S.selem[g0];
-        const uint64_t g = S.u.skey[g0] >> S.fOff;
+        ge = S.elem[S.u.rx.sidx[g0]];
+        const uint64_t g = S.u.rx.skey[g0] >> S.fOff;
         g1 = g0 + 1;
-        while (g1 < n && (S.u.skey[g1] >> S.fOff) == g)
+        while (g1 < n && (S.u.rx.skey[g1] >> S.fOff) == g)
           ++g1;
       }
       if (ge > F.keyElem[K])
         continue; // another block already holds a smaller element for K
+      uint32_t mem[kSmallGroup + 1];
+      int nm = 0;
+      if (hashed) {
+        for (uint32_t q = S.u.ch.head[hashSlot<IPT>(ge)]; q != Smem::kEnd && nm <= kSmallGroup;
+             q = S.u.ch.next[q])
+          if (S.elem[q] == ge)
+            mem[nm++] = q;
+      }
+      const int cnt = hashed ? nm : static_cast<int>(g1 - g0);
+      auto rec = [&](int i) -> uint32_t { return hashed ? mem[i] : S.u.rx.sidx[g0 + i]; };
       uint64_t bestX = ~0ull, bestY = ~0ull;
       int sX = 0, sY = 0;
       auto order = [&](uint64_t m) {
@@ -585,10 +539,8 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
         return (thread << kSeqBits) | metaSeq(m);
       };
       // lexicographically first (x, y) over the element's racing pairs of K
-      for (uint32_t a = g0; a < g1; ++a) {
-        if (S.selem[a] != ge)
-          continue;
-        const uint64_t ma = S.smeta[a];
+      for (int a = 0; a < cnt; ++a) {
+        const uint64_t ma = S.meta[rec(a)];
         const int sa = metaSite(ma);
         const int loa = sSites[sa].loc;
         if (loa != la && loa != lb)
@@ -596,10 +548,10 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
         const uint64_t oa = order(ma);
         if (oa > bestX)
           continue;
-        for (uint32_t b = g0; b < g1; ++b) {
-          if (b == a || S.selem[b] != ge)
+        for (int b = 0; b < cnt; ++b) {
+          if (b == a)
             continue;
-          const uint64_t mb = S.smeta[b];
+          const uint64_t mb = S.meta[rec(b)];
           const uint64_t ob = order(mb);
           if (ob <= oa)
             continue; // y must follow x in event order

@@ -64,6 +64,10 @@ __device__ __forceinline__ void threadIdentity(const LaunchDev &L, int64_t t, Bu
 }
 
 struct InterpBody {
+  __device__ static __forceinline__ void identity(const LaunchDev &L, int64_t t, Builtins &b,
+                                                  int64_t &block, int64_t &warp, int64_t &lane) {
+    threadIdentity(L, t, b, block, warp, lane);
+  }
   // `r` holds nRegs registers (local array or global scratch).
   template <class Sink>
   __device__ static void run(const LaunchDev &L, const hgrd_gpu_insn *__restrict__ code,
@@ -148,8 +152,11 @@ struct ParState {
   }
   // Returns the parameter when the access is in bounds (an instance).
   __device__ __forceinline__ const ParamDev *check(int site, int64_t idx) {
-    const SiteDev &S = sites[site];
-    const ParamDev *P = S.param >= 0 ? &params[S.param] : nullptr;
+    return checkK(sites[site].param, idx);
+  }
+  // Same with the site's parameter known (JIT bodies pass it as a constant).
+  __device__ __forceinline__ const ParamDev *checkK(int param, int64_t idx) {
+    const ParamDev *P = param >= 0 ? &params[param] : nullptr;
     if (!P || P->handle < 0 || idx < 0 || idx >= P->size) {
       ++traps; // any trap sends the launch to the ordered path
       return nullptr;

@@ -585,13 +585,14 @@ struct JitGetter {
   hgrd_gpu_ctx *c;
   const hgrd_gpu_launch *L;
   bool enabled;
+  std::vector<uint8_t> rec; // per site: produces race-check records
   const void *get(hgrdgpu::jit::Variant v) {
     if (!enabled)
       return nullptr;
     if (!c->jit)
       c->jit = hgrdgpu::jit::create();
     std::string err;
-    const void *k = hgrdgpu::jit::get(c->jit, *L, v, err);
+    const void *k = hgrdgpu::jit::get(c->jit, *L, rec, v, err);
     if (!k && !err.empty()) {
       c->jitErr = err;
       ++c->jitFailures;
@@ -693,6 +694,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.nLocs = nLocs;
   F.nKeys = nKeys;
   F.bpi = static_cast<int>(bpi);
+  F.R = (loops || recInsns == 0) ? 0u : recInsns; // straight-line code: static record slots
   F.nIters = (D.nBlocks + bpi - 1) / bpi;
   F.owner = c->owner.p;
   F.epoch = c->epoch;
@@ -991,7 +993,9 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
                        !(L.flags & HGRD_LAUNCH_GENERAL);
   // NVRTC specialisation for large PARALLEL launches (compiled on first use)
   const bool useJit = !seq && (c->jitMode == 2 || (c->jitMode == 1 && D.nThreads >= (int64_t(1) << 14)));
-  JitGetter jk{c, &L, useJit};
+  JitGetter jk{c, &L, useJit, {}};
+  for (const auto &s : P.sites)
+    jk.rec.push_back(s.record ? 1 : 0);
   if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
     rc = runFused(c, L, D, o, P, R, recInsns, loops, jk);
     if (rc < 0)

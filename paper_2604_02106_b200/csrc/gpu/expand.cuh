@@ -100,8 +100,6 @@ struct ParSink : ParState {
   LaneRecords *out;
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
-    if (!sites[site].record)
-      return;
     const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
     if (L->ownerFilter && L->ownerFilter[e] != L->ownerMultiTag)
       return; // fused pass 2: only elements shared by blocks
@@ -142,23 +140,37 @@ struct ParSink : ParState {
     }
     ++recs;
   }
-  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
-    const ParamDev *P = check(site, idx);
+  // K variants: the site's parameter and record flag as (JIT) constants
+  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, int64_t idx,
+                                           bool need) {
+    const ParamDev *P = checkK(param, idx);
     if (!P)
       return 0;
-    record(site, P, idx);
+    if (rec)
+      record(site, P, idx);
     ++seq;
     return need ? __ldg(P->ptr + idx) : 0;
   }
-  __device__ __forceinline__ void store(int site, int64_t idx, int64_t) {
-    const ParamDev *P = check(site, idx);
+  __device__ __forceinline__ void storeK(int site, int param, bool rec, int64_t idx, int64_t) {
+    const ParamDev *P = checkK(param, idx);
     if (!P)
       return;
-    record(site, P, idx);
+    if (rec)
+      record(site, P, idx);
     ++seq;
   }
-  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t, int64_t) {
-    store(site, idx, 0);
+  __device__ __forceinline__ void atomicK(int site, int param, bool rec, int64_t idx, int64_t,
+                                          int64_t) {
+    storeK(site, param, rec, idx, 0);
+  }
+  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
+    return loadK(site, sites[site].param, sites[site].record, idx, need);
+  }
+  __device__ __forceinline__ void store(int site, int64_t idx, int64_t v) {
+    storeK(site, sites[site].param, sites[site].record, idx, v);
+  }
+  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t v, int64_t c) {
+    atomicK(site, sites[site].param, sites[site].record, idx, v, c);
   }
 };
 
@@ -192,7 +204,7 @@ template <class Body> __global__ void __launch_bounds__(256) k_expand_par(Launch
       s.params = sParams;
       s.out = &out;
       Builtins bi;
-      threadIdentity(L, t, bi, s.block, s.warp, s.lane);
+      Body::identity(L, t, bi, s.block, s.warp, s.lane);
       Body::run(L, sCode, bi, s, regs);
       tally.add(s);
     }
@@ -371,7 +383,7 @@ template <class Body> __global__ void k_expand_seq(LaunchDev L) {
   s.L = &L;
   for (int64_t t = 0; t < L.nThreads && !s.aborted; ++t) {
     Builtins bi;
-    threadIdentity(L, t, bi, s.block, s.warp, s.lane);
+    Body::identity(L, t, bi, s.block, s.warp, s.lane);
     s.t = t;
     s.bp = s.wp = s.seq = 0;
     if (L.opStart)

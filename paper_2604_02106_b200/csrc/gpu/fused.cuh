@@ -52,6 +52,7 @@ struct FusedArgs {
   LaunchDev L;
   int nLocs, nKeys;
   int bpi;              // whole MiniCU blocks per iteration
+  uint32_t R;           // records per MiniCU thread when static (0: allocate)
   int64_t nIters;
   uint32_t *owner;
   uint32_t epoch;
@@ -156,22 +157,29 @@ template <int IPT> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
 // pushed onto the chain of its element's hash slot.
 template <int IPT> struct FusedSink : ParState {
   FusedSmem<IPT> *S;
-  uint32_t tli; // thread index within the iteration
+  uint32_t tli;      // thread index within the iteration
+  uint32_t stride;   // fixed-slot mode: threads in the iteration
+  uint32_t nrec = 0; // records produced by this thread
+  uint32_t R;        // fixed-slot mode: slots per thread (0: allocate)
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
-    if (!sites[site].record)
-      return;
     if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
       flags |= kFlagFusedOverflow;
-    // warp-aggregated slot allocation (one shared atomic per converged group)
-    const unsigned act = __activemask();
-    const int ln = threadIdx.x & 31;
-    const int leader = __ffs(act) - 1;
-    unsigned base = 0;
-    if (ln == leader)
-      base = atomicAdd(&S->count, static_cast<unsigned>(__popc(act)));
-    base = __shfl_sync(act, base, leader);
-    const unsigned pos = base + __popc(act & ((1u << ln) - 1));
+    unsigned pos;
+    if (R) { // static record count per thread: slot k of thread t at k * stride + t
+      // (column-major, so a warp's k-th records are adjacent), no atomics
+      pos = nrec < R ? nrec * stride + tli : 0xffffffffu;
+    } else { // warp-aggregated allocation (one shared atomic per converged group)
+      const unsigned act = __activemask();
+      const int ln = threadIdx.x & 31;
+      const int leader = __ffs(act) - 1;
+      unsigned base = 0;
+      if (ln == leader)
+        base = atomicAdd(&S->count, static_cast<unsigned>(__popc(act)));
+      base = __shfl_sync(act, base, leader);
+      pos = base + __popc(act & ((1u << ln) - 1));
+    }
+    ++nrec;
     if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
       const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
       S->elem[pos] = e;
@@ -182,25 +190,41 @@ template <int IPT> struct FusedSink : ParState {
     }
     ++recs;
   }
-  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
-    const ParamDev *P = check(site, idx);
+  // K variants: the site's parameter and record flag as (JIT) constants
+  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, int64_t idx,
+                                           bool need) {
+    const ParamDev *P = checkK(param, idx);
     if (!P)
       return 0;
-    record(site, P, idx);
+    if (rec)
+      record(site, P, idx);
     ++seq;
     return need ? __ldg(P->ptr + idx) : 0;
   }
-  __device__ __forceinline__ void store(int site, int64_t idx, int64_t) {
-    const ParamDev *P = check(site, idx);
+  __device__ __forceinline__ void storeK(int site, int param, bool rec, int64_t idx, int64_t) {
+    const ParamDev *P = checkK(param, idx);
     if (!P)
       return;
-    record(site, P, idx);
+    if (rec)
+      record(site, P, idx);
     ++seq;
   }
-  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t, int64_t) {
-    store(site, idx, 0);
+  __device__ __forceinline__ void atomicK(int site, int param, bool rec, int64_t idx, int64_t,
+                                          int64_t) {
+    storeK(site, param, rec, idx, 0);
+  }
+  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
+    return loadK(site, sites[site].param, sites[site].record, idx, need);
+  }
+  __device__ __forceinline__ void store(int site, int64_t idx, int64_t v) {
+    storeK(site, sites[site].param, sites[site].record, idx, v);
+  }
+  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t v, int64_t c) {
+    atomicK(site, sites[site].param, sites[site].record, idx, v, c);
   }
 };
+
+constexpr uint64_t kNoElem = ~0ull; // fixed-slot mode: a slot its thread did not fill
 
 // Conditions of the reference pair rule for two records of one element
 // inside one MiniCU block (:750-769), INTRA kinds only.  Returns kind or -1.
@@ -291,7 +315,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
     const int64_t nb = min(static_cast<int64_t>(F.bpi), L.nBlocks - firstBlock);
     __syncthreads();
     if (tid == 0) {
-      S.count = 0;
+      S.count = F.R ? static_cast<unsigned>(nb * L.tpb) * F.R : 0;
       S.maxBp = 0;
       S.maxWp = 0;
       S.hot = 0;
@@ -310,9 +334,14 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
         s.params = sParams;
         s.S = &S;
         s.tli = static_cast<uint32_t>(tl);
+        s.R = F.R;
+        s.stride = static_cast<uint32_t>(nb * L.tpb);
         Builtins bi;
-        threadIdentity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
+        Body::identity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
         Body::run(L, sCode, bi, s, regs);
+        for (uint32_t j = s.nrec; j < F.R; ++j)
+          if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))
+            S.elem[j * s.stride + s.tli] = kNoElem;
         tally.add(s);
         myBp = max(myBp, s.bp);
         myWp = max(myWp, s.wp);
@@ -340,6 +369,8 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
     OwnerPending owners;
     for (unsigned p = tid; p < n && !(F.ablate & 2); p += kFusedThreads) {
       const uint64_t e = S.elem[p];
+      if (e == kNoElem)
+        continue;
       const uint64_t m = S.meta[p];
       const uint32_t bp_ = L.dTpb.div(metaTli(m));
       const int sp = metaSite(m);
@@ -381,6 +412,8 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       if (tid == 0)
         S.nReal = 0;
       for (unsigned i = tid; i < n; i += kFusedThreads) {
+        if (S.elem[i] == kNoElem)
+          continue;
         const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
         atomicMin(&S.minE[w], static_cast<unsigned long long>(S.elem[i]));
         atomicMax(&S.maxE[w], static_cast<unsigned long long>(S.elem[i]));
@@ -417,7 +450,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       for (int j = 0; j < IPT; ++j) {
         const unsigned i = static_cast<unsigned>(tid * IPT + j);
         vals[j] = i;
-        if (i < n) {
+        if (i < n && S.elem[i] != kNoElem) {
           const uint64_t m = S.meta[i];
           const uint32_t tli = metaTli(m);
           const uint32_t blk = L.dTpb.div(tli), tl = tli - blk * tpb;
@@ -445,8 +478,8 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       const int shLane = S.fWp, shBpF = S.fBp, shElem = S.fOff;
       for (int j = 0; j < IPT; ++j) {
         const int p = tid * IPT + j;
-        if (p >= static_cast<int>(n))
-          break;
+        if (p >= static_cast<int>(n) || S.u.rx.skey[p] == ~0ull)
+          break; // unfilled slots sort last
         const uint64_t g = S.u.rx.skey[p] >> shElem;
         if (p > 0 && (S.u.rx.skey[p - 1] >> shElem) == g)
           continue;

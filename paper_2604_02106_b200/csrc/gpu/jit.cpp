@@ -36,20 +36,68 @@ const char *kNames[3] = {"hgrdgpu::dev::k_expand_par<hgrdgpu::dev::JitBody>",
                          "hgrdgpu::dev::k_fused<4, hgrdgpu::dev::JitBody>",
                          "hgrdgpu::dev::k_fused<16, hgrdgpu::dev::JitBody>"};
 
+// Thread identity (reference src/oracle.cpp:443-460) with the launch
+// geometry as literals, so every division is by a constant.
+void emitIdentity(std::ostringstream &o, const hgrd_gpu_launch &L) {
+  const int64_t tpb = L.block[0] * L.block[1] * L.block[2];
+  const int64_t nThreads = tpb * L.grid[0] * L.grid[1] * L.grid[2];
+  const bool small = nThreads < (int64_t(1) << 32) - 1 && L.warp_size < (int64_t(1) << 32);
+  o << "  __device__ static __forceinline__ void identity(const LaunchDev &, int64_t t, Builtins &b,\n"
+       "      int64_t &block, int64_t &warp, int64_t &lane) {\n";
+  for (int i = 0; i < 3; ++i) {
+    o << "    b.v[" << 6 + i << "] = " << lit(L.block[i]) << ";\n";
+    o << "    b.v[" << 9 + i << "] = " << lit(L.grid[i]) << ";\n";
+  }
+  if (small) {
+    auto u = [](int64_t v) { return std::to_string(static_cast<unsigned long long>(v)) + "u"; };
+    o << "    const uint32_t x = static_cast<uint32_t>(t);\n"
+         "    const uint32_t bl = x / " << u(tpb) << ", tl = x - bl * " << u(tpb) << ";\n"
+         "    b.v[0] = tl % " << u(L.block[0]) << ";\n"
+         "    b.v[1] = (tl / " << u(L.block[0]) << ") % " << u(L.block[1]) << ";\n"
+         "    b.v[2] = tl / " << u(L.block[0] * L.block[1]) << ";\n"
+         "    b.v[3] = bl % " << u(L.grid[0]) << ";\n"
+         "    b.v[4] = (bl / " << u(L.grid[0]) << ") % " << u(L.grid[1]) << ";\n"
+         "    b.v[5] = bl / " << u(L.grid[0] * L.grid[1]) << ";\n"
+         "    block = bl;\n"
+         "    warp = tl / " << u(L.warp_size) << ";\n"
+         "    lane = tl % " << u(L.warp_size) << ";\n";
+  } else {
+    o << "    block = t / " << lit(tpb) << ";\n"
+         "    const int64_t tl = t - block * " << lit(tpb) << ";\n"
+         "    b.v[0] = tl % " << lit(L.block[0]) << ";\n"
+         "    b.v[1] = (tl / " << lit(L.block[0]) << ") % " << lit(L.block[1]) << ";\n"
+         "    b.v[2] = tl / " << lit(L.block[0] * L.block[1]) << ";\n"
+         "    b.v[3] = block % " << lit(L.grid[0]) << ";\n"
+         "    b.v[4] = (block / " << lit(L.grid[0]) << ") % " << lit(L.grid[1]) << ";\n"
+         "    b.v[5] = block / " << lit(L.grid[0] * L.grid[1]) << ";\n"
+         "    warp = tl / " << lit(L.warp_size) << ";\n"
+         "    lane = tl - warp * " << lit(L.warp_size) << ";\n";
+  }
+  o << "  }\n";
+}
+
 } // namespace
 
-std::string generate(const hgrd_gpu_launch &L) {
+std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec) {
   std::vector<char> target(L.n_code, 0);
   for (uint32_t pc = 0; pc < L.n_code; ++pc) {
     const auto &I = L.code[pc];
     if (I.op == HGRD_OP_JZ || I.op == HGRD_OP_JMP)
       target[static_cast<size_t>(I.imm)] = 1;
   }
+  // site -> "site, param, record" literal arguments of the sink's K accessors
+  auto site = [&](int64_t s) {
+    const size_t i = static_cast<size_t>(s);
+    const bool r = i < rec.size() ? rec[i] != 0 : true;
+    return std::to_string(s) + ", " + std::to_string(i < L.n_sites ? L.sites[i].param : 0) +
+           ", " + (r ? "true" : "false");
+  };
   std::ostringstream o;
   o << "#include \"jit_kernels.cuh\"\n"
        "namespace hgrdgpu {\nnamespace dev {\n"
-       "struct JitBody {\n"
-       "  template <class Sink>\n"
+       "struct JitBody {\n";
+  emitIdentity(o, L);
+  o << "  template <class Sink>\n"
        "  __device__ static __forceinline__ void run(const LaunchDev &, const hgrd_gpu_insn *,\n"
        "                                             const Builtins &bi, Sink &s, int64_t *) {\n";
   for (uint32_t i = 0; i < L.n_regs; ++i)
@@ -79,14 +127,14 @@ std::string generate(const hgrd_gpu_launch &L) {
       o << "r" << I.a << " = applyBin(" << int(I.sub) << ", r" << I.b << ", r" << I.c << ");";
       break;
     case HGRD_OP_LOAD:
-      o << "r" << I.a << " = s.load(" << I.imm << ", r" << I.b << ", "
+      o << "r" << I.a << " = s.loadK(" << site(I.imm) << ", r" << I.b << ", "
         << ((I.sub & 1) ? "true" : "false") << ");";
       break;
     case HGRD_OP_STORE:
-      o << "s.store(" << I.imm << ", r" << I.a << ", r" << I.b << ");";
+      o << "s.storeK(" << site(I.imm) << ", r" << I.a << ", r" << I.b << ");";
       break;
     case HGRD_OP_ATOMIC:
-      o << "s.atomic(" << I.imm << ", r" << I.a << ", r" << I.b << ", r" << I.c << ");";
+      o << "s.atomicK(" << site(I.imm) << ", r" << I.a << ", r" << I.b << ", r" << I.c << ");";
       break;
     case HGRD_OP_SYNCTHREADS:
       o << "s.syncthreads();";
@@ -144,8 +192,9 @@ void destroy(Cache *c) {
 double compileMs(const Cache *c) { return c ? c->compileMs : 0; }
 int compiles(const Cache *c) { return c ? c->compiles : 0; }
 
-const void *get(Cache *c, const hgrd_gpu_launch &L, Variant v, std::string &err) {
-  const std::string src = generate(L);
+const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
+                std::string &err) {
+  const std::string src = generate(L, rec);
   const std::string key = std::to_string(static_cast<int>(v)) + "\n" + src;
   auto it = c->mods.find(key);
   if (it != c->mods.end())

@@ -5,6 +5,7 @@
 
 #include <map>
 #include <string>
+#include <vector>
 
 namespace hgrdgpu {
 namespace jit {
@@ -17,8 +18,10 @@ void destroy(Cache *c);
 // The specialised kernel `v` for this launch's code and constants (compiled
 // on first use, cached).  Returns nullptr (and err) when NVRTC is
 // unavailable or the compile fails; callers then use the interpreter.
-const void *get(Cache *c, const hgrd_gpu_launch &L, Variant v, std::string &err);
-std::string generate(const hgrd_gpu_launch &L);
+// `rec[s]`: whether site s produces race-check records (host value analysis).
+const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
+                std::string &err);
+std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec);
 double compileMs(const Cache *c);
 int compiles(const Cache *c);
 

@@ -232,6 +232,14 @@ int hgrd_gpu_sweep_shard_json(hgrd_gpu_ctx *ctx, const char *source,
 int hgrd_gpu_count_inputs(const char *source, const char *file_name);
 /* Lowering only: bytecode, sites, locs and per-kernel facts of one kernel as
  * JSON (for callers that fix launch parameters themselves). */
+/* Development check (no GPU needed): lower `kernel`, generate its NVRTC
+ * thread body for the given geometry (scalar parameters 0, every site
+ * recording) and compile all three specialised kernels for sm_100a without
+ * loading them.  *out = {"variants":[{"cubin_bytes":N,"error":"..."}x3]}.
+ * Returns HGRD_GPU_ENOTSUP when a variant does not compile. */
+int hgrd_gpu_jit_check(const char *source, const char *file_name, const char *kernel,
+                       const int64_t grid[3], const int64_t block[3], int64_t warp_size,
+                       char **out);
 int hgrd_gpu_lower_json(const char *source, const char *file_name,
                         const char *kernel, char **out);
 void hgrd_gpu_free(char *p);

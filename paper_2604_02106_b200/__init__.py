@@ -148,6 +148,9 @@ def load_library() -> ctypes.CDLL:
                                               ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
                                               ctypes.POINTER(P)]
     lib.hgrd_gpu_count_inputs.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+    I3 = ctypes.c_int64 * 3
+    lib.hgrd_gpu_jit_check.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, I3, I3,
+                                       ctypes.c_int64, ctypes.POINTER(P)]
     lib.hgrd_gpu_free.argtypes = [P]
     lib.hgrd_gpu_set_profiling.argtypes = [P, ctypes.c_int]
     lib.hgrd_gpu_last_profile.argtypes = [P]
@@ -182,6 +185,21 @@ def lower(source: str, kernel: str, file_name: str = "prog.mcu") -> dict:
     d = json.loads(_take_string(lib, out))
     if rc != 0:
         raise ValueError(f"lowering failed: {d}")
+    return d
+
+
+def jit_check(source: str, kernel: str, grid=(1, 1, 1), block=(256, 1, 1),
+              warp_size: int = 32, file_name: str = "prog.mcu") -> dict:
+    """Compile the NVRTC-specialised kernels of one kernel for sm_100a
+    without loading them (no GPU needed); raises on a compile error."""
+    lib = load_library()
+    I3 = ctypes.c_int64 * 3
+    out = ctypes.c_void_p()
+    rc = lib.hgrd_gpu_jit_check(source.encode(), file_name.encode(), kernel.encode(),
+                                I3(*grid), I3(*block), warp_size, ctypes.byref(out))
+    d = json.loads(_take_string(lib, out))
+    if rc != 0:
+        raise RuntimeError(f"jit_check failed ({rc}): {d}")
     return d
 
 

@@ -3,6 +3,7 @@
 // device-buffer / check-launch ABI of include/hgrd_gpu.h.
 #include "hgrd_gpu.h"
 #include "host.hpp"
+#include "gpu/jit.hpp"
 
 #include <cstdlib>
 #include <cstring>
@@ -93,6 +94,69 @@ void hgrd_gpu_free(char *p) { std::free(p); }
 // Lowering only (no host interpretation): the bytecode, site table and
 // per-kernel facts of one kernel, as JSON.  Used by callers that fix the
 // launch parameters themselves (bench workloads, reference-side adapters).
+namespace {
+std::string escapeJson(const std::string &in) {
+  std::string o;
+  for (char ch : in) {
+    if (ch == '"' || ch == '\\')
+      o += '\\';
+    if (ch == '\n') {
+      o += "\\n";
+      continue;
+    }
+    if (static_cast<unsigned char>(ch) < 0x20)
+      continue;
+    o += ch;
+  }
+  return o;
+}
+} // namespace
+
+extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, const char *kernel,
+                                  const int64_t grid[3], const int64_t block[3],
+                                  int64_t warp_size, char **out) {
+  if (!out || !grid || !block)
+    return HGRD_GPU_EINVAL;
+  ParseOutcome po = parseMiniCU(source ? source : "", file_name ? file_name : "");
+  const Function *k = po.program ? po.program->findKernel(kernel ? kernel : "") : nullptr;
+  if (!k) {
+    *out = dup(errorJson(po.program ? std::vector<std::string>{"unknown kernel"}
+                                    : po.diagnostics));
+    return HGRD_GPU_EINVAL;
+  }
+  LoweredKernel lk = lowerKernel(*k);
+  std::vector<int64_t> regInit(lk.nRegs, 0);
+  std::vector<int32_t> handles(k->params.size(), 0);
+  hgrd_gpu_launch L{};
+  L.code = lk.code.data();
+  L.n_code = static_cast<uint32_t>(lk.code.size());
+  L.n_regs = lk.nRegs;
+  L.reg_init = regInit.data();
+  L.sites = lk.sites.data();
+  L.n_sites = static_cast<uint32_t>(lk.sites.size());
+  L.n_locs = static_cast<uint32_t>(lk.locs.size());
+  L.param_handle = handles.data();
+  L.n_params = static_cast<uint32_t>(handles.size());
+  for (int i = 0; i < 3; ++i) {
+    L.grid[i] = grid[i];
+    L.block[i] = block[i];
+  }
+  L.warp_size = warp_size;
+  const std::vector<uint8_t> rec(lk.sites.size(), 1);
+  std::string s = "{\"variants\":[";
+  bool ok = true;
+  for (int v = 0; v < 3; ++v) {
+    std::string err;
+    const size_t bytes = hgrdgpu::jit::compileOnly(L, rec, static_cast<hgrdgpu::jit::Variant>(v), err);
+    ok = ok && bytes > 0;
+    s += (v ? "," : "") + std::string("{\"cubin_bytes\":") + std::to_string(bytes) +
+         ",\"error\":\"" + escapeJson(err) + "\"}";
+  }
+  s += "]}";
+  *out = dup(s);
+  return ok ? HGRD_GPU_OK : HGRD_GPU_ENOTSUP;
+}
+
 extern "C" int hgrd_gpu_lower_json(const char *source, const char *file_name,
                                    const char *kernel, char **out) {
   if (!out)

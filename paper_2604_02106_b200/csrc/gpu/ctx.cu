@@ -622,9 +622,10 @@ int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t
 // ---------------------------------------------------------------------------
 // Fused block-local path (fused.cuh) + pass 2 for elements shared by blocks.
 
-template <int IPT> size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
+template <int NT, int IPT>
+size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
   const size_t nKeysPad = (static_cast<size_t>(nKeys) + 3) & ~size_t(3);
-  return align16(sizeof(FusedSmem<IPT>)) + 12 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
+  return align16(sizeof(FusedSmem<NT, IPT>)) + 12 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
          sizeof(SiteDev) * P.sites.size() + sizeof(ParamDev) * P.params.size() +
          8 * P.sites.size();
 }
@@ -635,10 +636,10 @@ int readCountersFrom(hgrd_gpu_ctx *c, Counters *dev) {
   return 0;
 }
 
-template <int IPT>
+template <int NT, int IPT>
 int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *jitKernel) {
   const void *fn =
-      jitKernel ? jitKernel : reinterpret_cast<const void *>(k_fused<IPT, InterpBody>);
+      jitKernel ? jitKernel : reinterpret_cast<const void *>(k_fused<NT, IPT, InterpBody>);
   if (c->smemOptIn.insert(fn).second) { // once per kernel: allow up to 227 KB in total
     cudaFuncAttributes fa{};
     CK(cudaFuncGetAttributes(&fa, fn));
@@ -647,13 +648,13 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *ji
   }
   int &perSM = c->occupancy[std::make_pair(fn, smem)];
   if (perSM == 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, kFusedThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, NT, smem));
     perSM = std::max(perSM, 1);
   }
   const int64_t grid = std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1));
   void *args[] = {const_cast<FusedArgs *>(&F)};
   StageTimer t(c, jitKernel ? "k_fused[jit]" : "k_fused");
-  CK(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kFusedThreads), args, smem,
+  CK(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(NT), args, smem,
                       c->st));
   return 0;
 }
@@ -666,15 +667,17 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
              JitGetter &jk) {
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
-  int64_t bpi = std::max<int64_t>(1, kFusedThreads / D.tpb);
+  int64_t bpi = std::max<int64_t>(1, 256 / D.tpb); // ~256 MiniCU threads per iteration
   const uint64_t per = std::max<uint32_t>(recInsns, 1);
   while (bpi > 1 && static_cast<uint64_t>(bpi * D.tpb) * per > 4096)
     bpi /= 2;
   const uint64_t perIter = static_cast<uint64_t>(bpi * D.tpb) * per;
   if (bpi * D.tpb > 65536 || (!loops && perIter > 4096))
     return 0;
-  const int ipt = (!loops && perIter <= 1024) ? 4 : 16;
-  const size_t smem = ipt == 4 ? fusedSmemBytes<4>(L, P, nKeys) : fusedSmemBytes<16>(L, P, nKeys);
+  // up to 1024 records: 256 threads x 4; else 256 x 16
+  const bool narrow = !loops && perIter <= 1024;
+  const size_t smem =
+      narrow ? fusedSmemBytes<256, 4>(L, P, nKeys) : fusedSmemBytes<256, 16>(L, P, nKeys);
   if (smem > 227 * 1024)
     return 0;
 
@@ -708,8 +711,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
   if (const char *ab = std::getenv("HGRD_FUSED_ABLATE"))
     F.ablate = std::atoi(ab);
-  int rc = ipt == 4 ? launchFused<4>(c, F, smem, jk.get(hgrdgpu::jit::kFused4))
-                    : launchFused<16>(c, F, smem, jk.get(hgrdgpu::jit::kFused16));
+  int rc = narrow ? launchFused<256, 4>(c, F, smem, jk.get(hgrdgpu::jit::kFusedNarrow))
+                  : launchFused<256, 16>(c, F, smem, jk.get(hgrdgpu::jit::kFusedWide));
   if (rc < 0)
     return rc;
   CK(cudaGetLastError());

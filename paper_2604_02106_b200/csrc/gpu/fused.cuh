@@ -13,7 +13,7 @@
 //      (same element): realised INTRA keys and, per key, the minimum element,
 //   4. per realised key: the first (x, y) pair of the reference's order
 //      inside that element, published as a candidate (global element via
-//      atomicMin, candidates filtered by it; k_fused_finalize keeps the
+//      atomicMin, candidates filtered by it; the last CTA keeps the
 //      lexicographically first pair of the minimum element).
 // INTER-BLOCK pairs need a second block: every (element, block) also does
 // one ownership exchange on a per-element table (epoch-tagged, no memset);
@@ -30,7 +30,6 @@
 namespace hgrdgpu {
 namespace dev {
 
-constexpr int kFusedThreads = 256;
 constexpr int kMaxWritten = 8;
 constexpr uint32_t kOwnerMulti = 0xFFFFFu;
 constexpr int kSmallGroup = 32; // hash slots up to this size, radix grouping above
@@ -112,12 +111,16 @@ struct OwnerPending {
   }
 };
 
-template <int IPT> struct FusedSmem {
-  static constexpr int kCap = kFusedThreads * IPT;
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
+// NT threads x IPT records per thread of shared-memory record capacity.
+template <int NT, int IPT> struct FusedSmem {
+  static constexpr int kThreads = NT;
+  static constexpr int kCap = NT * IPT;
   static constexpr int kTable = 2 * kCap; // hash slots (power of two)
-  static constexpr int kLogTable = IPT == 4 ? 11 : 13;
+  static constexpr int kLogTable = ilog2(kTable);
   static constexpr uint32_t kEnd = 0xffffffffu;
-  using Sort = cub::BlockRadixSort<uint64_t, kFusedThreads, IPT, uint32_t, 5>;
+  using Sort = cub::BlockRadixSort<uint64_t, NT, IPT, uint32_t, 5>;
   union {
     typename Sort::TempStorage sortTmp;
     struct {
@@ -149,14 +152,14 @@ __device__ __forceinline__ uint32_t metaWp(uint64_t m) { return (m >> 32) & 255;
 __device__ __forceinline__ int metaSite(uint64_t m) { return static_cast<int>((m >> 20) & 4095); }
 __device__ __forceinline__ uint32_t metaSeq(uint64_t m) { return static_cast<uint32_t>(m & kSeqMask); }
 
-template <int IPT> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
-  return static_cast<uint32_t>((e * 0x9E3779B97F4A7C15ull) >> (64 - FusedSmem<IPT>::kLogTable));
+template <class Smem> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
+  return static_cast<uint32_t>((e * 0x9E3779B97F4A7C15ull) >> (64 - Smem::kLogTable));
 }
 
 // PARALLEL sink of the fused kernel: records into shared memory, each
 // pushed onto the chain of its element's hash slot.
-template <int IPT> struct FusedSink : ParState {
-  FusedSmem<IPT> *S;
+template <class Smem> struct FusedSink : ParState {
+  Smem *S;
   uint32_t tli;      // thread index within the iteration
   uint32_t stride;   // fixed-slot mode: threads in the iteration
   uint32_t nrec = 0; // records produced by this thread
@@ -180,11 +183,11 @@ template <int IPT> struct FusedSink : ParState {
       pos = base + __popc(act & ((1u << ln) - 1));
     }
     ++nrec;
-    if (pos < static_cast<unsigned>(FusedSmem<IPT>::kCap)) {
+    if (pos < static_cast<unsigned>(Smem::kCap)) {
       const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
       S->elem[pos] = e;
       S->meta[pos] = packMeta(tli, bp, wp, site, seq);
-      S->u.ch.next[pos] = atomicExch(&S->u.ch.head[hashSlot<IPT>(e)], pos);
+      S->u.ch.next[pos] = atomicExch(&S->u.ch.head[hashSlot<Smem>(e)], pos);
     } else {
       flags |= kFlagFusedOverflow;
     }
@@ -262,8 +265,8 @@ __device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa,
 
 // Keep the minimum `v` (element in hash mode, sorted position in radix
 // mode) per key; the first setter appends the key to the realised list.
-template <int IPT>
-__device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, unsigned long long *sKeyMin,
+template <class Smem>
+__device__ __forceinline__ void noteKey(Smem &S, unsigned long long *sKeyMin,
                                         uint32_t *sReal, int K, unsigned long long v) {
   if (sKeyMin[K] <= v)
     return;
@@ -274,9 +277,11 @@ __device__ __forceinline__ void noteKey(FusedSmem<IPT> &S, unsigned long long *s
   }
 }
 
-template <int IPT, class Body>
-__global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
-  using Smem = FusedSmem<IPT>;
+// NT = 128 (6 CTAs per SM: short barrier groups) or 256 threads per CTA.
+template <int NT, int IPT, class Body>
+__global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
+  using Smem = FusedSmem<NT, IPT>;
+  constexpr int kFusedThreads = NT;
   extern __shared__ __align__(16) unsigned char dyn[];
   Smem &S = *reinterpret_cast<Smem *>(dyn);
   unsigned char *after = dyn + ((sizeof(Smem) + 15) & ~size_t(15));
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
     {
       unsigned myBp = 0, myWp = 0;
       for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
-        FusedSink<IPT> s;
+        FusedSink<Smem> s;
         s.L = &L;
         s.sites = sSites;
         s.params = sParams;
@@ -558,7 +563,7 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       uint32_t mem[kSmallGroup + 1];
       int nm = 0;
       if (hashed) {
-        for (uint32_t q = S.u.ch.head[hashSlot<IPT>(ge)]; q != Smem::kEnd && nm <= kSmallGroup;
+        for (uint32_t q = S.u.ch.head[hashSlot<Smem>(ge)]; q != Smem::kEnd && nm <= kSmallGroup;
              q = S.u.ch.next[q])
           if (S.elem[q] == ge)
             mem[nm++] = q;
@@ -708,72 +713,6 @@ __global__ void __launch_bounds__(kFusedThreads, 3) k_fused(FusedArgs F) {
       o.seq_y = static_cast<int32_t>(y & kSeqMask);
     }
   }
-}
-
-// One block per key: the lexicographically first candidate pair of the
-// key's minimum element becomes the race record.
-__global__ void k_fused_finalize(FusedArgs F, DetectArgs A, hgrd_gpu_race *races) {
-  const int K = blockIdx.x;
-  const unsigned long long e = F.keyElem[K];
-  if (e == ~0ull)
-    return;
-  const unsigned nc = min(*F.candCount, F.candCap);
-  __shared__ uint64_t bx[32], by[32];
-  __shared__ int bs[32], bt[32];
-  uint64_t x = ~0ull, y = ~0ull;
-  int sx = 0, sy = 0;
-  for (unsigned c = threadIdx.x; c < nc; c += blockDim.x) {
-    const Candidate &cd = F.cand[c];
-    if (cd.key != K || cd.elem != e)
-      continue;
-    if (cd.xOrd < x || (cd.xOrd == x && cd.yOrd < y)) {
-      x = cd.xOrd;
-      y = cd.yOrd;
-      sx = cd.siteX;
-      sy = cd.siteY;
-    }
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t ox = __shfl_down_sync(0xffffffffu, x, o);
-    const uint64_t oy = __shfl_down_sync(0xffffffffu, y, o);
-    const int osx = __shfl_down_sync(0xffffffffu, sx, o);
-    const int osy = __shfl_down_sync(0xffffffffu, sy, o);
-    if (ox < x || (ox == x && oy < y)) {
-      x = ox;
-      y = oy;
-      sx = osx;
-      sy = osy;
-    }
-  }
-  if (lane == 0) {
-    bx[wid] = x;
-    by[wid] = y;
-    bs[wid] = sx;
-    bt[wid] = sy;
-  }
-  __syncthreads();
-  if (threadIdx.x != 0)
-    return;
-  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
-    if (bx[w] < x || (bx[w] == x && by[w] < y)) {
-      x = bx[w];
-      y = by[w];
-      sx = bs[w];
-      sy = bt[w];
-    }
-  const unsigned pos = atomicAdd(&F.L.ctr->nRaces, 1u);
-  hgrd_gpu_race &o = races[pos];
-  o.kind = K % 3;
-  o.loc_a = (K / 3) / F.nLocs;
-  o.loc_b = (K / 3) % F.nLocs;
-  o.site_x = sx;
-  o.site_y = sy;
-  elementOf(A, e, o.handle, o.index);
-  o.thread_x = static_cast<int64_t>(x >> kSeqBits);
-  o.seq_x = static_cast<int32_t>(x & kSeqMask);
-  o.thread_y = static_cast<int64_t>(y >> kSeqBits);
-  o.seq_y = static_cast<int32_t>(y & kSeqMask);
 }
 
 } // namespace dev

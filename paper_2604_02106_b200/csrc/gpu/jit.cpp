@@ -14,6 +14,7 @@
 #include <nvrtc.h>
 
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <sstream>
 #include <vector>
@@ -33,8 +34,8 @@ std::string dirOf(const std::string &p) {
 }
 
 const char *kNames[3] = {"hgrdgpu::dev::k_expand_par<hgrdgpu::dev::JitBody>",
-                         "hgrdgpu::dev::k_fused<4, hgrdgpu::dev::JitBody>",
-                         "hgrdgpu::dev::k_fused<16, hgrdgpu::dev::JitBody>"};
+                         "hgrdgpu::dev::k_fused<256, 4, hgrdgpu::dev::JitBody>",
+                         "hgrdgpu::dev::k_fused<256, 16, hgrdgpu::dev::JitBody>"};
 
 // Thread identity (reference src/oracle.cpp:443-460) with the launch
 // geometry as literals, so every division is by a constant.
@@ -192,23 +193,17 @@ void destroy(Cache *c) {
 double compileMs(const Cache *c) { return c ? c->compileMs : 0; }
 int compiles(const Cache *c) { return c ? c->compiles : 0; }
 
-const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
-                std::string &err) {
-  const std::string src = generate(L, rec);
-  const std::string key = std::to_string(static_cast<int>(v)) + "\n" + src;
-  auto it = c->mods.find(key);
-  if (it != c->mods.end())
-    return it->second;
-  const auto t0 = std::chrono::steady_clock::now();
+namespace {
+
+// NVRTC: generated source -> sm_100a cubin and the lowered kernel name.
+bool compile(const Cache *c, const std::string &src, Variant v, std::vector<char> &cubin,
+             std::string &lowered, std::string &err) {
   const std::string name = std::string("&") + kNames[v];
-  auto fail = [&](const std::string &why) -> const void * {
-    err = why;
-    c->mods.emplace(key, nullptr);
-    return nullptr;
-  };
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "hgrd_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
-    return fail("nvrtcCreateProgram failed");
+  if (nvrtcCreateProgram(&prog, src.c_str(), "hgrd_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    err = "nvrtcCreateProgram failed";
+    return false;
+  }
   nvrtcAddNameExpression(prog, name.c_str());
   const std::string i1 = "-I" + c->incGpu, i2 = "-I" + c->incRoot, i3 = "-I" + c->incCuda;
   const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-w",
@@ -220,16 +215,39 @@ const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &
     std::string log(n, '\0');
     nvrtcGetProgramLog(prog, log.data());
     nvrtcDestroyProgram(&prog);
-    return fail(std::string("NVRTC: ") + nvrtcGetErrorString(rc) + "\n" + log.substr(0, 4000));
+    err = std::string("NVRTC: ") + nvrtcGetErrorString(rc) + "\n" + log.substr(0, 4000);
+    return false;
   }
   size_t cubinSize = 0;
   nvrtcGetCUBINSize(prog, &cubinSize);
-  std::vector<char> cubin(cubinSize);
+  cubin.resize(cubinSize);
   nvrtcGetCUBIN(prog, cubin.data());
   const char *ln = nullptr;
   nvrtcGetLoweredName(prog, name.c_str(), &ln);
-  const std::string lowered = ln ? ln : "";
+  lowered = ln ? ln : "";
   nvrtcDestroyProgram(&prog);
+  return true;
+}
+
+} // namespace
+
+const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
+                std::string &err) {
+  const std::string src = generate(L, rec);
+  const std::string key = std::to_string(static_cast<int>(v)) + "\n" + src;
+  auto it = c->mods.find(key);
+  if (it != c->mods.end())
+    return it->second;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto fail = [&](const std::string &why) -> const void * {
+    err = why;
+    c->mods.emplace(key, nullptr);
+    return nullptr;
+  };
+  std::vector<char> cubin;
+  std::string lowered, cerr;
+  if (!compile(c, src, v, cubin, lowered, cerr))
+    return fail(cerr);
   cudaLibrary_t lib;
   if (cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
       cudaSuccess)
@@ -246,6 +264,23 @@ const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &
   const void *fn = reinterpret_cast<const void *>(k);
   c->mods.emplace(key, fn);
   return fn;
+}
+
+size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
+                   std::string &err) {
+  Cache *c = create();
+  std::vector<char> cubin;
+  std::string lowered;
+  const std::string src = generate(L, rec);
+  if (const char *dump = std::getenv("HGRD_JIT_DUMP")) { // development: keep the source
+    if (FILE *f = std::fopen(dump, "w")) {
+      std::fputs(src.c_str(), f);
+      std::fclose(f);
+    }
+  }
+  const bool ok = compile(c, src, v, cubin, lowered, err);
+  destroy(c);
+  return ok ? cubin.size() : 0;
 }
 
 } // namespace jit

@@ -10,7 +10,7 @@
 namespace hgrdgpu {
 namespace jit {
 
-enum Variant { kExpandPar = 0, kFused4 = 1, kFused16 = 2 };
+enum Variant { kExpandPar = 0, kFusedNarrow = 1, kFusedWide = 2 }; // k_fused<256,4> / <256,16>
 
 struct Cache;
 Cache *create();
@@ -22,6 +22,9 @@ void destroy(Cache *c);
 const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
                 std::string &err);
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec);
+// Compile without loading (no GPU needed): cubin size, 0 and err on failure.
+size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
+                   std::string &err);
 double compileMs(const Cache *c);
 int compiles(const Cache *c);
 

@@ -61,3 +61,16 @@ def test_count_inputs_matches_goldens():
     for e in load_golden("corpus"):
         n = hg.count_inputs(e["source"], e["file"])
         assert n == e["source"].count("__input()")
+
+
+@pytest.mark.parametrize("name", ["stencil", "transpose", "histogram"])
+def test_jit_bodies_compile_for_sm100a(name):
+    """The NVRTC thread bodies (jit.cpp) and all three kernels they are
+    specialised into compile for sm_100a (NVRTC needs no device)."""
+    src, kernel, grid, block = {
+        "stencil": (programs.stencil(1 << 12), "st", (16, 1, 1), (256, 1, 1)),
+        "transpose": (programs.transpose(256), "tr", (8, 8, 1), (32, 32, 1)),
+        "histogram": (programs.histogram(1 << 12, 64, "store"), "h", (16, 1, 1), (256, 1, 1)),
+    }[name]
+    d = hg.jit_check(src, kernel, grid, block)
+    assert all(v["cubin_bytes"] > 0 for v in d["variants"]), d

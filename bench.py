@@ -9,9 +9,10 @@ and the fixed one (clean) — i.e. 2 x 5 x 2^20 = 10,485,760 instances/step.
 * ``value``: instances / device time of hgrd_gpu_check_launch with the launch
   buffers already resident in HBM (CUDA events on the context's stream),
   L2 flushed (256 MiB write) between steps.
-* ``e2e``: the same checks through the C ABI from HOST buffers: every step
-  writes the launch's int64 buffers host->device and reads the race report
-  back; wall clock with the copies inside.
+* ``e2e``: the same checks through the reference-facing entry point
+  (hgrd_gpu_run_concrete_json = hgrd::runConcrete): MiniCU source text in,
+  JSON race report out, wall clock; h2d/d2h bytes are the context's counted
+  host<->device copies per step (launch descriptors, counters, race records).
 * ``roofline``: dominant pipeline stage vs the measured HBM copy bandwidth,
   algorithmic bytes = 32 B per instance.
 * ``cpu_baseline``: the unmodified reference (oracle/_ref/libhgrd_ref.so,
@@ -238,20 +239,27 @@ def run_gpu_arm(args):
     launches = ctx.kernel_launches() - launches0
     clk = clocks.stop()
 
-    # e2e: host buffers -> device, check, report back (wall clock)
-    h2d = sum(sum(a.nbytes for a in host.values()) for _, _, host in specs)
+    # e2e: the reference-facing call (hgrd::runConcrete, src/oracle.cpp:378):
+    # MiniCU source text in, JSON race report out — front end, host
+    # interpretation of main(), zero-initialised cudaMalloc buffers, the
+    # launch descriptor upload, the check and the report read-back, wall clock.
+    sources = [programs.stencil(N_THREADS, BLOCK, b) for b in (False, True)]
+    cfg = programs.synthetic_config()  # same ExecConfig as the reference arm
+    for src in sources:  # warm (allocation arena, NVRTC cache)
+        ctx.run_concrete(src, cfg, "syn.mcu")
     barrier()
+    xfer0 = ctx.transfer_bytes()
     t0 = time.perf_counter()
-    d2h = 0
+    e2e_races = []
     for _ in range(args.steps):
-        for spec, handles, host in specs:
-            for name, arr in host.items():
-                ctx.write(handles[name], arr)
-            raw = ctx.check_launch(spec, raw=True)
-            d2h += raw.n_races * 56 + 88
+        e2e_races = [ctx.run_concrete(src, cfg, "syn.mcu")["races"] for src in sources]
     barrier()
     e2e_s = time.perf_counter() - t0
-    d2h //= max(args.steps, 1)
+    xfer1 = ctx.transfer_bytes()
+    h2d = (xfer1[0] - xfer0[0]) // max(args.steps, 1)
+    d2h = (xfer1[1] - xfer0[1]) // max(args.steps, 1)
+    if not os.environ.get("HGRD_FUSED_ABLATE"):
+        assert sorted(r["kind"] for r in e2e_races[0]) == kinds and not e2e_races[1]
 
     if ws > 1:
         t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=dev)
@@ -280,7 +288,7 @@ def run_gpu_arm(args):
                    "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"replicas{ws}"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "api": "hgrd_gpu_run_concrete_json"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": dom,

@@ -205,6 +205,9 @@ int hgrd_gpu_set_jit(hgrd_gpu_ctx *ctx, int mode);
 const char *hgrd_gpu_jit_info(hgrd_gpu_ctx *ctx);
 /* Number of this library's own kernels launched by the context so far. */
 unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *ctx);
+/* Bytes copied host->device and device->host by this context (lifetime):
+ * buffer writes/reads, launch descriptors, counters, race/trap records. */
+int hgrd_gpu_transfer_bytes(hgrd_gpu_ctx *ctx, unsigned long long *h2d, unsigned long long *d2h);
 
 /* ---- reference-shaped entry points (JSON in / JSON out) ---------------- */
 /* cfg: {"gridCap":[3],"blockCap":[3],"warpSize":n,"inputs":[..],

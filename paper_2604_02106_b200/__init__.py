@@ -161,6 +161,8 @@ def load_library() -> ctypes.CDLL:
     lib.hgrd_gpu_jit_info.restype = ctypes.c_char_p
     lib.hgrd_gpu_kernel_launches.argtypes = [P]
     lib.hgrd_gpu_kernel_launches.restype = ctypes.c_ulonglong
+    lib.hgrd_gpu_transfer_bytes.argtypes = [P, ctypes.POINTER(ctypes.c_ulonglong),
+                                            ctypes.POINTER(ctypes.c_ulonglong)]
     _lib = lib
     return lib
 
@@ -353,6 +355,14 @@ class GpuContext:
 
     def kernel_launches(self) -> int:
         return int(self._lib.hgrd_gpu_kernel_launches(self._ctx))
+
+    def transfer_bytes(self):
+        """(host->device, device->host) bytes copied by this context so far."""
+        h, d = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        rc = self._lib.hgrd_gpu_transfer_bytes(self._ctx, ctypes.byref(h), ctypes.byref(d))
+        if rc:
+            self._err("transfer_bytes", rc)
+        return int(h.value), int(d.value)
 
     # -- device buffers --
     def reset(self):

@@ -130,6 +130,7 @@ struct hgrd_gpu_ctx {
   size_t evUsed = 0;
   std::string profileJson;
   unsigned long long kernelLaunches = 0; // own kernels launched (lifetime)
+  unsigned long long h2dBytes = 0, d2hBytes = 0; // host<->device copies (lifetime)
   std::map<std::pair<const void *, size_t>, int> occupancy; // (kernel, smem) -> CTAs/SM
   std::set<const void *> smemOptIn;
 };
@@ -409,6 +410,7 @@ int uploadBlob(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const Plan &P, BlobOff
   std::memset(h + o.keyElem, 0xff, 8 * static_cast<size_t>(o.nKeys));
   std::memset(h + o.ctr, 0, sizeof(Counters));
   CK(cudaMemcpyAsync(c->blob.p, h, o.h2d, cudaMemcpyHostToDevice, c->st));
+  c->h2dBytes += o.h2d;
   c->cur = reinterpret_cast<Counters *>(c->blob.p + o.ctr);
   c->curRaces = reinterpret_cast<hgrd_gpu_race *>(c->blob.p + o.races);
   c->curKeyElem = reinterpret_cast<unsigned long long *>(c->blob.p + o.keyElem);
@@ -428,6 +430,7 @@ int readCountersAndRaces(hgrd_gpu_ctx *c, size_t nKeys) {
     c->hResultCap = std::max<size_t>(bytes, 4096);
   }
   CK(cudaMemcpyAsync(c->hResult, c->cur, bytes, cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += bytes;
   CK(cudaStreamSynchronize(c->st));
   std::memcpy(c->hCtr, c->hResult, sizeof(Counters));
   c->hRacesView = reinterpret_cast<hgrd_gpu_race *>(c->hResult + racesOff);
@@ -437,6 +440,7 @@ int readCountersAndRaces(hgrd_gpu_ctx *c, size_t nKeys) {
 
 int readCounters(hgrd_gpu_ctx *c) {
   CK(cudaMemcpyAsync(c->hCtr, c->cur, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += sizeof(Counters);
   CK(cudaStreamSynchronize(c->st));
   return 0;
 }
@@ -571,6 +575,7 @@ int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
   } else if (nr) {
     CK(cudaMemcpyAsync(R->races, c->curRaces, sizeof(hgrd_gpu_race) * nr,
                        cudaMemcpyDeviceToHost, c->st));
+    c->d2hBytes += sizeof(hgrd_gpu_race) * nr;
     CK(cudaStreamSynchronize(c->st));
   }
   c->racesOnHost = false;
@@ -632,6 +637,7 @@ size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
 
 int readCountersFrom(hgrd_gpu_ctx *c, Counters *dev) {
   CK(cudaMemcpyAsync(c->hCtr, dev, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += sizeof(Counters);
   CK(cudaStreamSynchronize(c->st));
   return 0;
 }
@@ -773,6 +779,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     std::vector<unsigned long long> ke(static_cast<size_t>(nKeys));
     CK(cudaMemcpyAsync(ke.data(), c->interKeyElem.p, 8 * static_cast<size_t>(nKeys),
                        cudaMemcpyDeviceToHost, c->st));
+    c->d2hBytes += 8 * static_cast<size_t>(nKeys);
     CK(cudaStreamSynchronize(c->st));
     std::vector<uint64_t> targets;
     for (int K = 0; K < nKeys; K += 3)
@@ -784,6 +791,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
       return fetchRaces(c, R) < 0 ? -1 : 1; // no INTER race (pass-1 races stand)
     NEED(c->targets, targets.size());
     CK(cudaMemcpy(c->targets.p, targets.data(), 8 * targets.size(), cudaMemcpyHostToDevice));
+    c->h2dBytes += 8 * targets.size();
     // 2b: records of only those elements -> first pairs (witnesses)
     D2.targets = c->targets.p;
     D2.nTargets = static_cast<int>(targets.size());
@@ -1144,6 +1152,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     if (nt) {
       CK(cudaMemcpyAsync(R->traps, c->traps.p, sizeof(hgrd_gpu_trap) * nt,
                          cudaMemcpyDeviceToHost, c->st));
+      c->d2hBytes += sizeof(hgrd_gpu_trap) * nt;
       CK(cudaStreamSynchronize(c->st));
     }
     R->n_traps = nt;
@@ -1292,6 +1301,14 @@ int hgrd_gpu_set_fused(hgrd_gpu_ctx *c, int enabled) {
 
 unsigned long long hgrd_gpu_kernel_launches(hgrd_gpu_ctx *c) { return c ? c->kernelLaunches : 0; }
 
+int hgrd_gpu_transfer_bytes(hgrd_gpu_ctx *c, unsigned long long *h2d, unsigned long long *d2h) {
+  if (!c || !h2d || !d2h)
+    return HGRD_GPU_EINVAL;
+  *h2d = c->h2dBytes;
+  *d2h = c->d2hBytes;
+  return 0;
+}
+
 int hgrd_gpu_buffers_reset(hgrd_gpu_ctx *c) {
   if (!c)
     return HGRD_GPU_EINVAL;
@@ -1356,6 +1373,7 @@ int hgrd_gpu_buffer_write(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n,
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->bufs[static_cast<size_t>(h)].p + off, src, static_cast<size_t>(n) * 8,
                      cudaMemcpyHostToDevice, c->st));
+  c->h2dBytes += static_cast<size_t>(n) * 8;
   return 0;
 }
 
@@ -1368,6 +1386,7 @@ int hgrd_gpu_buffer_read(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n, int
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(dst, c->bufs[static_cast<size_t>(h)].p + off, static_cast<size_t>(n) * 8,
                      cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += static_cast<size_t>(n) * 8;
   CK(cudaStreamSynchronize(c->st));
   return 0;
 }

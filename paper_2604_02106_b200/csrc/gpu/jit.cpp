@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <sstream>
+#include <unordered_map>
 #include <vector>
 
 namespace hgrdgpu {
@@ -162,7 +163,7 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec) 
 }
 
 struct Cache {
-  std::map<std::string, const void *> mods; // generated source + variant -> kernel
+  std::unordered_map<std::string, const void *> mods; // launch inputs + variant -> kernel
   std::vector<cudaLibrary_t> libs;
   std::string incGpu, incRoot, incCuda;
   double compileMs = 0;
@@ -233,11 +234,24 @@ bool compile(const Cache *c, const std::string &src, Variant v, std::vector<char
 
 const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
                 std::string &err) {
-  const std::string src = generate(L, rec);
-  const std::string key = std::to_string(static_cast<int>(v)) + "\n" + src;
+  // cache key: the raw launch inputs of generate() (cheaper than the source)
+  std::string key;
+  auto put = [&key](const void *p, size_t n) { key.append(static_cast<const char *>(p), n); };
+  const int vi = static_cast<int>(v);
+  put(&vi, sizeof vi);
+  put(L.grid, sizeof L.grid);
+  put(L.block, sizeof L.block);
+  put(&L.warp_size, sizeof L.warp_size);
+  put(&L.n_regs, sizeof L.n_regs);
+  put(L.code, sizeof(hgrd_gpu_insn) * L.n_code);
+  if (L.reg_init)
+    put(L.reg_init, 8 * L.n_regs);
+  put(L.sites, sizeof(hgrd_gpu_site) * L.n_sites);
+  put(rec.data(), rec.size());
   auto it = c->mods.find(key);
   if (it != c->mods.end())
     return it->second;
+  const std::string src = generate(L, rec);
   const auto t0 = std::chrono::steady_clock::now();
   auto fail = [&](const std::string &why) -> const void * {
     err = why;

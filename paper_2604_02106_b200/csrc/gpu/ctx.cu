@@ -630,7 +630,7 @@ int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t
 template <int NT, int IPT>
 size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
   const size_t nKeysPad = (static_cast<size_t>(nKeys) + 3) & ~size_t(3);
-  return align16(sizeof(FusedSmem<NT, IPT>)) + 12 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
+  return align16(sizeof(FusedSmem<NT, IPT>)) + 8 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
          sizeof(SiteDev) * P.sites.size() + sizeof(ParamDev) * P.params.size() +
          8 * P.sites.size();
 }
@@ -999,7 +999,9 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     seq = true;
   bool snapped = false;
 
+  // (the fused kernel keeps per-key minimum elements as 32-bit values)
   const bool fusedOk = c->fusedEnabled && !seq && !locks && P.summaryOk && L.n_locs <= 32 &&
+                       P.totalW < 0xFFFFFFFFull &&
                        o.nW <= kMaxWritten && D.nBlocks < (1 << 20) - 2 &&
                        !(L.flags & HGRD_LAUNCH_GENERAL);
   // NVRTC specialisation for large PARALLEL launches (compiled on first use)

@@ -78,39 +78,6 @@ __device__ __forceinline__ void ownerSettle(const FusedArgs &F, uint64_t e, uint
   }
 }
 
-// Exchanges are issued in the group phase and settled at the end of the
-// iteration, so their L2 round trip overlaps the detection work.
-struct OwnerPending {
-  static constexpr int kSlots = 4;
-  uint64_t e[kSlots];
-  uint32_t mine[kSlots], old[kSlots];
-  int n = 0;
-  __device__ __forceinline__ void issue(const FusedArgs &F, uint64_t elem, uint64_t blk,
-                                        unsigned &flags) {
-    const uint32_t m = static_cast<uint32_t>(blk + 1);
-    const uint32_t o = atomicExch(&F.owner[elem], (F.epoch << 20) | m);
-    if (n < kSlots) {
-#pragma unroll
-      for (int q = 0; q < kSlots; ++q)
-        if (q == n) {
-          e[q] = elem;
-          mine[q] = m;
-          old[q] = o;
-        }
-      ++n;
-    } else {
-      ownerSettle(F, elem, m, o, flags);
-    }
-  }
-  __device__ __forceinline__ void settle(const FusedArgs &F, unsigned &flags) {
-#pragma unroll
-    for (int q = 0; q < kSlots; ++q)
-      if (q < n)
-        ownerSettle(F, e[q], mine[q], old[q], flags);
-    n = 0;
-  }
-};
-
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
 // NT threads x IPT records per thread of shared-memory record capacity.
@@ -134,6 +101,7 @@ template <int NT, int IPT> struct FusedSmem {
   } u;
   uint64_t elem[kCap];  // global element id, by record index
   uint64_t meta[kCap];  // tli:16 | bp:8 | wp:8 | site:12 | seq:20
+  uint8_t first[kCap];  // record is its (element, MiniCU block)'s first: owns the exchange
   unsigned long long minE[kMaxWritten], maxE[kMaxWritten];
   unsigned int count, maxBp, maxWp, nReal, flags, hot;
   // radix mode: field start bits of the key  w|off|blk|bp|warp|wp|lane
@@ -155,77 +123,6 @@ __device__ __forceinline__ uint32_t metaSeq(uint64_t m) { return static_cast<uin
 template <class Smem> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
   return static_cast<uint32_t>((e * 0x9E3779B97F4A7C15ull) >> (64 - Smem::kLogTable));
 }
-
-// PARALLEL sink of the fused kernel: records into shared memory, each
-// pushed onto the chain of its element's hash slot.
-template <class Smem> struct FusedSink : ParState {
-  Smem *S;
-  uint32_t tli;      // thread index within the iteration
-  uint32_t stride;   // fixed-slot mode: threads in the iteration
-  uint32_t nrec = 0; // records produced by this thread
-  uint32_t R;        // fixed-slot mode: slots per thread (0: allocate)
-
-  __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
-    if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
-      flags |= kFlagFusedOverflow;
-    unsigned pos;
-    if (R) { // static record count per thread: slot k of thread t at k * stride + t
-      // (column-major, so a warp's k-th records are adjacent), no atomics
-      pos = nrec < R ? nrec * stride + tli : 0xffffffffu;
-    } else { // warp-aggregated allocation (one shared atomic per converged group)
-      const unsigned act = __activemask();
-      const int ln = threadIdx.x & 31;
-      const int leader = __ffs(act) - 1;
-      unsigned base = 0;
-      if (ln == leader)
-        base = atomicAdd(&S->count, static_cast<unsigned>(__popc(act)));
-      base = __shfl_sync(act, base, leader);
-      pos = base + __popc(act & ((1u << ln) - 1));
-    }
-    ++nrec;
-    if (pos < static_cast<unsigned>(Smem::kCap)) {
-      const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
-      S->elem[pos] = e;
-      S->meta[pos] = packMeta(tli, bp, wp, site, seq);
-      S->u.ch.next[pos] = atomicExch(&S->u.ch.head[hashSlot<Smem>(e)], pos);
-    } else {
-      flags |= kFlagFusedOverflow;
-    }
-    ++recs;
-  }
-  // K variants: the site's parameter and record flag as (JIT) constants
-  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, int64_t idx,
-                                           bool need) {
-    const ParamDev *P = checkK(param, idx);
-    if (!P)
-      return 0;
-    if (rec)
-      record(site, P, idx);
-    ++seq;
-    return need ? __ldg(P->ptr + idx) : 0;
-  }
-  __device__ __forceinline__ void storeK(int site, int param, bool rec, int64_t idx, int64_t) {
-    const ParamDev *P = checkK(param, idx);
-    if (!P)
-      return;
-    if (rec)
-      record(site, P, idx);
-    ++seq;
-  }
-  __device__ __forceinline__ void atomicK(int site, int param, bool rec, int64_t idx, int64_t,
-                                          int64_t) {
-    storeK(site, param, rec, idx, 0);
-  }
-  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
-    return loadK(site, sites[site].param, sites[site].record, idx, need);
-  }
-  __device__ __forceinline__ void store(int site, int64_t idx, int64_t v) {
-    storeK(site, sites[site].param, sites[site].record, idx, v);
-  }
-  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t v, int64_t c) {
-    atomicK(site, sites[site].param, sites[site].record, idx, v, c);
-  }
-};
 
 constexpr uint64_t kNoElem = ~0ull; // fixed-slot mode: a slot its thread did not fill
 
@@ -266,27 +163,171 @@ __device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa,
 // Keep the minimum `v` (element in hash mode, sorted position in radix
 // mode) per key; the first setter appends the key to the realised list.
 template <class Smem>
-__device__ __forceinline__ void noteKey(Smem &S, unsigned long long *sKeyMin,
-                                        uint32_t *sReal, int K, unsigned long long v) {
+__device__ __forceinline__ void noteKey(Smem &S, uint32_t *sKeyMin, uint32_t *sReal, int K,
+                                        uint32_t v) {
   if (sKeyMin[K] <= v)
     return;
-  const unsigned long long old = atomicMin(&sKeyMin[K], v);
-  if (old == ~0ull) {
+  const uint32_t old = atomicMin(&sKeyMin[K], v);
+  if (old == ~0u) {
     const unsigned slot = atomicAdd(&S.nReal, 1u);
     sReal[slot] = static_cast<uint32_t>(K);
   }
 }
 
 // NT = 128 (6 CTAs per SM: short barrier groups) or 256 threads per CTA.
+// Lock-free push of record `pos` onto a hash slot's chain.  acq_rel: the
+// record's fields (written before) are visible to whoever later reads the
+// chain through the slot, and this thread sees the fields of every record
+// pushed before it.
+__device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_t val) {
+  uint32_t old;
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("atom.acq_rel.cta.shared::cta.cas.b32 %0, [%1], %2, %3;"
+               : "=r"(old)
+               : "r"(a), "r"(cmp), "r"(val)
+               : "memory");
+  return old;
+}
+
+// PARALLEL sink of the fused kernel: records into shared memory, each
+// pushed onto the chain of its element's hash slot and, at that moment,
+// paired with the records of its element pushed before it (every pair is
+// seen exactly once: by whichever of the two was pushed second).
+template <class Smem> struct FusedSink : ParState {
+  Smem *S;
+  uint32_t tli;      // thread index within the iteration
+  uint32_t stride;   // fixed-slot mode: threads in the iteration
+  uint32_t nrec = 0; // records produced by this thread
+  uint32_t R;        // fixed-slot mode: slots per thread (0: allocate)
+  uint32_t myBlk;    // MiniCU block within the iteration
+  uint32_t tpb;
+  int nLocs;
+  uint32_t *keyMin;  // per key: minimum element (32-bit) realised in the iteration
+  uint32_t *real;    // realised keys
+  const uint64_t *conf; // per site: conflicting sites (bit mask)
+  uint32_t *owner;      // per element ownership table (see ownerSettle)
+  uint32_t epochTag;    // epoch << 20
+  uint32_t mine;        // this thread's block + 1
+
+  __device__ __forceinline__ void pairWithEarlier(uint64_t e, uint64_t m, int site, uint32_t q,
+                                                  uint32_t pos) {
+    bool first = true;
+    int len = 0;
+    for (; q != Smem::kEnd; q = S->u.ch.next[q]) {
+      if (++len > kSmallGroup) { // a hot element: radix grouping instead
+        S->hot = 1;
+        break;
+      }
+      if (S->elem[q] != e)
+        continue;
+      const uint64_t mq = S->meta[q];
+      if (L->dTpb.div(metaTli(mq)) == myBlk)
+        first = false;
+      const int kind = intraKind(*L, sites, mq, m, tpb);
+      if (kind < 0)
+        continue;
+      const int sq = metaSite(mq);
+      if (!((conf[sq] >> site) & 1ull))
+        continue;
+      noteKey(*S, keyMin, real, keyIndex(sites, nLocs, sq, site, kind), static_cast<uint32_t>(e));
+    }
+#ifdef HGRD_OWN_POSTPASS
+    S->first[pos] = first;
+#else
+    if (first && owner) { // the block's first record of e: one ownership exchange
+      const uint32_t old = atomicExch(&owner[e], epochTag | mine);
+      if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
+        atomicExch(&owner[e], epochTag | kOwnerMulti);
+        flags |= kFlagShared;
+      }
+    }
+#endif
+  }
+
+  __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
+    if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
+      flags |= kFlagFusedOverflow;
+    unsigned pos;
+    if (R) { // static record count per thread: slot k of thread t at k * stride + t
+      // (column-major, so a warp's k-th records are adjacent), no atomics
+      pos = nrec < R ? nrec * stride + tli : 0xffffffffu;
+    } else { // warp-aggregated allocation (one shared atomic per converged group)
+      const unsigned act = __activemask();
+      const int ln = threadIdx.x & 31;
+      const int leader = __ffs(act) - 1;
+      unsigned base = 0;
+      if (ln == leader)
+        base = atomicAdd(&S->count, static_cast<unsigned>(__popc(act)));
+      base = __shfl_sync(act, base, leader);
+      pos = base + __popc(act & ((1u << ln) - 1));
+    }
+    ++nrec;
+    if (pos < static_cast<unsigned>(Smem::kCap)) {
+      const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
+      const uint64_t m = packMeta(tli, bp, wp, site, seq);
+      S->elem[pos] = e;
+      S->meta[pos] = m;
+      uint32_t *head = &S->u.ch.head[hashSlot<Smem>(e)];
+      uint32_t h = *reinterpret_cast<volatile uint32_t *>(head);
+      for (;;) {
+        S->u.ch.next[pos] = h;
+        const uint32_t o = casAcqRel(head, h, pos);
+        if (o == h)
+          break;
+        h = o;
+      }
+      pairWithEarlier(e, m, site, h, pos);
+    } else {
+      flags |= kFlagFusedOverflow;
+    }
+    ++recs;
+  }
+  // K variants: the site's parameter and record flag as (JIT) constants
+  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, int64_t idx,
+                                           bool need) {
+    const ParamDev *P = checkK(param, idx);
+    if (!P)
+      return 0;
+    if (rec)
+      record(site, P, idx);
+    ++seq;
+    return need ? __ldg(P->ptr + idx) : 0;
+  }
+  __device__ __forceinline__ void storeK(int site, int param, bool rec, int64_t idx, int64_t) {
+    const ParamDev *P = checkK(param, idx);
+    if (!P)
+      return;
+    if (rec)
+      record(site, P, idx);
+    ++seq;
+  }
+  __device__ __forceinline__ void atomicK(int site, int param, bool rec, int64_t idx, int64_t,
+                                          int64_t) {
+    storeK(site, param, rec, idx, 0);
+  }
+  __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
+    return loadK(site, sites[site].param, sites[site].record, idx, need);
+  }
+  __device__ __forceinline__ void store(int site, int64_t idx, int64_t v) {
+    storeK(site, sites[site].param, sites[site].record, idx, v);
+  }
+  __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t v, int64_t c) {
+    atomicK(site, sites[site].param, sites[site].record, idx, v, c);
+  }
+};
+
 template <int NT, int IPT, class Body>
-__global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
+#ifndef HGRD_FUSED_MINB
+#define HGRD_FUSED_MINB 3
+#endif
+__global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(FusedArgs F) {
   using Smem = FusedSmem<NT, IPT>;
   constexpr int kFusedThreads = NT;
   extern __shared__ __align__(16) unsigned char dyn[];
   Smem &S = *reinterpret_cast<Smem *>(dyn);
   unsigned char *after = dyn + ((sizeof(Smem) + 15) & ~size_t(15));
   const int nKeysPad = (F.nKeys + 3) & ~3;
-  unsigned long long *sKeyMin = reinterpret_cast<unsigned long long *>(after);
+  uint32_t *sKeyMin = reinterpret_cast<uint32_t *>(after);
   uint32_t *sReal = reinterpret_cast<uint32_t *>(sKeyMin + nKeysPad);
   hgrd_gpu_insn *sCode = reinterpret_cast<hgrd_gpu_insn *>(sReal + nKeysPad);
   SiteDev *sSites = reinterpret_cast<SiteDev *>(sCode + F.L.nCode);
@@ -304,7 +345,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
   for (int i = tid; i < L.nParams; i += kFusedThreads)
     sParams[i] = L.params[i];
   for (int i = tid; i < F.nKeys; i += kFusedThreads)
-    sKeyMin[i] = ~0ull;
+    sKeyMin[i] = ~0u;
   if (tid == 0) {
     S.nReal = 0;
     S.flags = 0;
@@ -341,12 +382,23 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
         s.tli = static_cast<uint32_t>(tl);
         s.R = F.R;
         s.stride = static_cast<uint32_t>(nb * L.tpb);
+        s.myBlk = L.dTpb.div(static_cast<uint32_t>(tl));
+        s.tpb = tpb;
+        s.nLocs = F.nLocs;
+        s.keyMin = sKeyMin;
+        s.real = sReal;
+        s.conf = sConf;
+        s.owner = (F.ablate & 4) ? nullptr : F.owner;
+        s.epochTag = F.epoch << 20;
+        s.mine = static_cast<uint32_t>(firstBlock + s.myBlk + 1);
         Builtins bi;
         Body::identity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
         Body::run(L, sCode, bi, s, regs);
         for (uint32_t j = s.nrec; j < F.R; ++j)
-          if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))
+          if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap)) {
             S.elem[j * s.stride + s.tli] = kNoElem;
+            S.first[j * s.stride + s.tli] = 0;
+          }
         tally.add(s);
         myBp = max(myBp, s.bp);
         myWp = max(myWp, s.wp);
@@ -369,46 +421,46 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
       continue;
     if (F.ablate & 1)
       continue;
-    // 2. detection, hash mode: each record pairs with the earlier records of
-    //    its slot's chain that hold the same element
-    OwnerPending owners;
-    for (unsigned p = tid; p < n && !(F.ablate & 2); p += kFusedThreads) {
-      const uint64_t e = S.elem[p];
-      if (e == kNoElem)
-        continue;
-      const uint64_t m = S.meta[p];
-      const uint32_t bp_ = L.dTpb.div(metaTli(m));
-      const int sp = metaSite(m);
-      bool first = true;
-      int len = 0;
-      for (uint32_t q = S.u.ch.next[p]; q != Smem::kEnd; q = S.u.ch.next[q]) {
-        if (++len > kSmallGroup) { // a hot element: radix grouping instead
-          S.hot = 1;
-          break;
+    // 2. ownership: one exchange per (element, MiniCU block) — by the
+    //    block's first record of the element (INTRA pairs were found as the
+    //    records were pushed); issued in batches of kOwnBatch, the last batch
+    //    settled at the end of the iteration
+    constexpr int kOwnBatch = 4;
+    static_assert(IPT % kOwnBatch == 0, "IPT must be a multiple of the owner batch");
+    uint64_t oE[kOwnBatch];
+    uint32_t oMine[kOwnBatch], oOld[kOwnBatch];
+    bool oHas[kOwnBatch];
+    auto settleOwners = [&]() {
+#pragma unroll
+      for (int j = 0; j < kOwnBatch; ++j)
+        if (oHas[j])
+          ownerSettle(F, oE[j], oMine[j], oOld[j], myFlags);
+    };
+#pragma unroll
+    for (int k0 = 0; k0 < IPT; k0 += kOwnBatch) {
+      if (k0)
+        settleOwners();
+#pragma unroll
+      for (int j = 0; j < kOwnBatch; ++j) {
+        const unsigned p = tid + static_cast<unsigned>((k0 + j) * NT);
+#ifdef HGRD_OWN_POSTPASS
+        oHas[j] = p < n && S.first[p] && !(F.ablate & 4);
+#else
+        oHas[j] = false;
+#endif
+        if (oHas[j]) {
+          oE[j] = S.elem[p];
+          oMine[j] = static_cast<uint32_t>(firstBlock + L.dTpb.div(metaTli(S.meta[p])) + 1);
+          oOld[j] = atomicExch(&F.owner[oE[j]], (F.epoch << 20) | oMine[j]);
         }
-        if (S.elem[q] != e)
-          continue;
-        const uint64_t mq = S.meta[q];
-        if (L.dTpb.div(metaTli(mq)) == bp_)
-          first = false;
-        const int kind = intraKind(L, sSites, mq, m, tpb);
-        if (kind < 0)
-          continue;
-        const int sq = metaSite(mq);
-        if (!((sConf[sq] >> sp) & 1ull))
-          continue;
-        noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, sq, sp, kind), e);
       }
-      if (first && !(F.ablate & 4))
-        owners.issue(F, e, static_cast<uint64_t>(firstBlock + bp_), myFlags);
     }
-    __syncthreads();
     const bool hashed = S.hot == 0;
     if (!hashed) {
       // radix mode for this iteration: drop the hash-mode keys, sort by
       // w | off | blk | bp | warp | wp | lane and summarise per group
       for (unsigned r = tid; r < S.nReal; r += kFusedThreads)
-        sKeyMin[sReal[r]] = ~0ull;
+        sKeyMin[sReal[r]] = ~0u;
       if (tid < kMaxWritten) {
         S.minE[tid] = ~0ull;
         S.maxE[tid] = 0;
@@ -507,7 +559,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
               mm &= mm - 1;
               if (min(mn[a], mn[b]) < max(mx[a], mx[b]))
                 noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, a, b, kind),
-                        static_cast<unsigned long long>(p));
+                        static_cast<uint32_t>(p));
             }
           }
         };
@@ -542,8 +594,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
       const int K = static_cast<int>(sReal[r]);
       const int kind = K % 3;
       const int la = (K / 3) / F.nLocs, lb = (K / 3) % F.nLocs;
-      const unsigned long long v = sKeyMin[K];
-      sKeyMin[K] = ~0ull; // reset for the next iteration
+      const uint32_t v = sKeyMin[K];
+      sKeyMin[K] = ~0u; // reset for the next iteration
       // the key's minimum element in this iteration: its records are the
       // slot chain (hash mode) or a sorted range (radix mode)
       uint64_t ge;
@@ -618,7 +670,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) k_fused(FusedArgs F) {
           myFlags |= kFlagFusedOverflow;
       }
     }
-    owners.settle(F, myFlags);
+    settleOwners();
     if (tid == 0)
       S.nReal = 0;
   }

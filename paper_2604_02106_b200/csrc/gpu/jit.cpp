@@ -207,9 +207,18 @@ bool compile(const Cache *c, const std::string &src, Variant v, std::vector<char
   }
   nvrtcAddNameExpression(prog, name.c_str());
   const std::string i1 = "-I" + c->incGpu, i2 = "-I" + c->incRoot, i3 = "-I" + c->incCuda;
-  const char *opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "-w",
-                        "-DHGRD_JIT=1", i1.c_str(), i2.c_str(), i3.c_str()};
-  const nvrtcResult rc = nvrtcCompileProgram(prog, sizeof(opts) / sizeof(opts[0]), opts);
+  std::vector<const char *> opts = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo",
+                                    "-w", "-DHGRD_JIT=1", i1.c_str(), i2.c_str(), i3.c_str()};
+  // development: extra NVRTC options (e.g. -DHGRD_FUSED_MINB=4), space separated
+  std::vector<std::string> extra;
+  if (const char *x = std::getenv("HGRD_JIT_OPTS")) {
+    std::istringstream is(x);
+    for (std::string w; is >> w;)
+      extra.push_back(w);
+  }
+  for (const auto &w : extra)
+    opts.push_back(w.c_str());
+  const nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(opts.size()), opts.data());
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);

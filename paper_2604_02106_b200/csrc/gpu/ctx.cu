@@ -687,6 +687,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   if (smem > 227 * 1024)
     return 0;
 
+  // ownership table (epoch-tagged, no memset between launches)
   const size_t ownerN = std::max<uint64_t>(P.totalW, 1);
   const bool fresh = c->owner.cap < ownerN;
   NEED(c->owner, ownerN);

@@ -3,22 +3,22 @@
 // One CTA iteration takes one or more whole MiniCU blocks.  Every
 // INTRA-BLOCK / INTRA-WARP pair lies inside one MiniCU block
 // (reference src/oracle.cpp:754-769), so they are found entirely on chip:
-//   1. expansion into shared memory (records: global element id + meta),
-//   2. grouping: as it is produced, each record is pushed onto the chain of
-//      its element's hash slot (2x-oversized table, one shared atomicExch);
-//      a chain longer than kSmallGroup (a hot element) switches the
-//      iteration to a CUB block radix sort of
-//      element | block | bp | warp | wp | lane and per-group summaries,
-//   3. one thread per record pairs it with the earlier records of its chain
-//      (same element): realised INTRA keys and, per key, the minimum element,
-//   4. per realised key: the first (x, y) pair of the reference's order
+//   1. expansion into shared memory (two-word records, see packR0/packR1);
+//      each record is pushed onto the chain of its element's hash slot
+//      (2x-oversized table, lock-free acq_rel CAS) and at that moment paired
+//      with the earlier records of its element on the chain: realised INTRA
+//      keys and, per key, the minimum element.  A chain longer than
+//      kSmallGroup (a hot element) switches the iteration to a CUB block
+//      radix sort of element | block | bp | warp | wp | lane with per-group
+//      summaries instead,
+//   2. per realised key: the first (x, y) pair of the reference's order
 //      inside that element, published as a candidate (global element via
 //      atomicMin, candidates filtered by it; the last CTA keeps the
 //      lexicographically first pair of the minimum element).
 // INTER-BLOCK pairs need a second block: every (element, block) also does
-// one ownership exchange on a per-element table (epoch-tagged, no memset);
-// an element reached from two blocks becomes MULTI and only MULTI elements
-// go through the global record sort (pass 2 in ctx.cu).
+// one ownership exchange on a per-element table; an element reached from
+// two blocks becomes MULTI and only MULTI elements go through pass 2
+// (ctx.cu).
 #pragma once
 
 #include "detect.cuh"
@@ -53,7 +53,7 @@ struct FusedArgs {
   int bpi;              // whole MiniCU blocks per iteration
   uint32_t R;           // records per MiniCU thread when static (0: allocate)
   int64_t nIters;
-  uint32_t *owner;
+  uint32_t *owner; // per element ownership word (see FusedSink)
   uint32_t epoch;
   unsigned long long *keyElem;
   Candidate *cand;
@@ -63,22 +63,55 @@ struct FusedArgs {
   hgrd_gpu_race *races;     // INTRA races are finalised by the last CTA
   const uint64_t *wBase;    // element -> (handle, index)
   const int32_t *wHandle;
-  int ablate; // profiling knob (HGRD_FUSED_ABLATE): 1 skip grouping, 2 skip groups, 4 skip ownership
+  int ablate; // profiling knob (HGRD_FUSED_ABLATE): 1 skip the post-expansion phases,
+              // 4 skip ownership exchanges, 8 skip expansion
 };
 
-// One exchange per (element, block): whoever replaces another block's tag
-// (or MULTI) marks the element MULTI.  The last exchange on an element that
-// two blocks touched is always followed by a MULTI store, so the final value
-// is MULTI exactly for the elements of >= 2 blocks.
-__device__ __forceinline__ void ownerSettle(const FusedArgs &F, uint64_t e, uint32_t mine,
-                                            uint32_t old, unsigned &flags) {
-  if ((old >> 20) == F.epoch && (old & kOwnerMulti) != mine) {
-    atomicExch(&F.owner[e], (F.epoch << 20) | kOwnerMulti);
-    flags |= kFlagShared;
-  }
-}
-
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
+
+// Records are two words (elements < 2^32 - 1 on this path):
+//   r0 = site:12 | seq:20 | elem:32
+//   r1 = tli:16 | blk:8 | bp:8 | wp:8 | warp:16 | 0:8
+// tli = thread within the iteration, blk = MiniCU block within the
+// iteration, warp = warp within the MiniCU block; the pair rule reads
+// XORs of r1 words (no divisions).
+constexpr uint64_t kNoRec = ~0ull; // fixed-slot mode: a slot its thread did not fill
+
+__device__ __forceinline__ uint64_t packR0(int site, uint32_t seq, uint32_t e) {
+  return (static_cast<uint64_t>(site & 4095) << 52) |
+         (static_cast<uint64_t>(seq & kSeqMask) << 32) | e;
+}
+__device__ __forceinline__ uint64_t packR1(uint32_t tli, uint32_t blk, uint32_t bp, uint32_t wp,
+                                           uint32_t warp) {
+  return (static_cast<uint64_t>(tli) << 48) | (static_cast<uint64_t>(blk & 255) << 40) |
+         (static_cast<uint64_t>(bp & 255) << 32) | (static_cast<uint64_t>(wp & 255) << 24) |
+         (static_cast<uint64_t>(warp & 0xFFFF) << 8);
+}
+__device__ __forceinline__ uint32_t rElem(uint64_t r0) { return static_cast<uint32_t>(r0); }
+__device__ __forceinline__ int rSite(uint64_t r0) { return static_cast<int>(r0 >> 52); }
+__device__ __forceinline__ uint32_t rSeq(uint64_t r0) {
+  return static_cast<uint32_t>(r0 >> 32) & kSeqMask;
+}
+__device__ __forceinline__ uint32_t rTli(uint64_t r1) { return static_cast<uint32_t>(r1 >> 48); }
+__device__ __forceinline__ uint32_t rBlk(uint64_t r1) { return (r1 >> 40) & 255; }
+__device__ __forceinline__ uint32_t rBp(uint64_t r1) { return (r1 >> 32) & 255; }
+__device__ __forceinline__ uint32_t rWp(uint64_t r1) { return (r1 >> 24) & 255; }
+__device__ __forceinline__ uint32_t rWarp(uint64_t r1) { return (r1 >> 8) & 0xFFFF; }
+
+// The reference pair rule (:750-769) for two records of one element, given
+// that their sites conflict statically (confIntra covers "a write" and "not
+// two covering atomics"): -1 when the pair is excluded or INTER-BLOCK, else
+// 1 (INTRA-BLOCK) or 2 (INTRA-WARP).
+__device__ __forceinline__ int intraRule(uint64_t a1, uint64_t b1) {
+  const uint64_t x = a1 ^ b1;
+  if ((x >> 48) == 0)
+    return -1; // same thread
+  if ((x >> 32) & 0xFFFF)
+    return -1; // other MiniCU block (INTER) or other barrier phase
+  if ((x >> 8) & 0xFFFF)
+    return 1; // other warp
+  return ((x >> 24) & 255) ? -1 : 2; // same warp: same warp phase only
+}
 
 // NT threads x IPT records per thread of shared-memory record capacity.
 template <int NT, int IPT> struct FusedSmem {
@@ -99,55 +132,16 @@ template <int NT, int IPT> struct FusedSmem {
       uint32_t sidx[kCap];  // sorted position -> record index
     } rx;
   } u;
-  uint64_t elem[kCap];  // global element id, by record index
-  uint64_t meta[kCap];  // tli:16 | bp:8 | wp:8 | site:12 | seq:20
-  uint8_t first[kCap];  // record is its (element, MiniCU block)'s first: owns the exchange
-  unsigned long long minE[kMaxWritten], maxE[kMaxWritten];
+  uint64_t r0[kCap]; // site | seq | elem, by record index
+  uint64_t r1[kCap]; // tli | blk | bp | wp | warp
+  uint32_t minE[kMaxWritten], maxE[kMaxWritten];
   unsigned int count, maxBp, maxWp, nReal, flags, hot;
   // radix mode: field start bits of the key  w|off|blk|bp|warp|wp|lane
   int fWp, fWarp, fBp, fBlk, fOff, fW, total;
 };
 
-__device__ __forceinline__ uint64_t packMeta(uint32_t tli, uint32_t bp, uint32_t wp, int site,
-                                             uint32_t seq) {
-  return (static_cast<uint64_t>(tli) << 48) | (static_cast<uint64_t>(bp & 255) << 40) |
-         (static_cast<uint64_t>(wp & 255) << 32) | (static_cast<uint64_t>(site & 4095) << 20) |
-         (seq & kSeqMask);
-}
-__device__ __forceinline__ uint32_t metaTli(uint64_t m) { return static_cast<uint32_t>(m >> 48); }
-__device__ __forceinline__ uint32_t metaBp(uint64_t m) { return (m >> 40) & 255; }
-__device__ __forceinline__ uint32_t metaWp(uint64_t m) { return (m >> 32) & 255; }
-__device__ __forceinline__ int metaSite(uint64_t m) { return static_cast<int>((m >> 20) & 4095); }
-__device__ __forceinline__ uint32_t metaSeq(uint64_t m) { return static_cast<uint32_t>(m & kSeqMask); }
-
-template <class Smem> __device__ __forceinline__ uint32_t hashSlot(uint64_t e) {
-  return static_cast<uint32_t>((e * 0x9E3779B97F4A7C15ull) >> (64 - Smem::kLogTable));
-}
-
-constexpr uint64_t kNoElem = ~0ull; // fixed-slot mode: a slot its thread did not fill
-
-// Conditions of the reference pair rule for two records of one element
-// inside one MiniCU block (:750-769), INTRA kinds only.  Returns kind or -1.
-__device__ __forceinline__ int intraKind(const LaunchDev &L, const SiteDev *sites, uint64_t ma,
-                                         uint64_t mb, uint32_t tpb) {
-  const uint32_t ta = metaTli(ma), tb = metaTli(mb);
-  if (ta == tb)
-    return -1;
-  const uint32_t ba = L.dTpb.div(ta), bb = L.dTpb.div(tb);
-  if (ba != bb)
-    return -1; // different MiniCU blocks: INTER, handled by ownership
-  const SiteDev &sa = sites[metaSite(ma)], &sb = sites[metaSite(mb)];
-  if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
-    return -1;
-  if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC && sa.scope != HGRD_SCOPE_NONE &&
-      sb.scope != HGRD_SCOPE_NONE)
-    return -1;
-  if (metaBp(ma) != metaBp(mb))
-    return -1;
-  const uint32_t wa = L.dWs.div(ta - ba * tpb), wb = L.dWs.div(tb - bb * tpb);
-  if (wa == wb && metaWp(ma) != metaWp(mb))
-    return -1;
-  return wa != wb ? 1 : 2;
+template <class Smem> __device__ __forceinline__ uint32_t hashSlot(uint32_t e) {
+  return (e * 0x9E3779B1u) >> (32 - Smem::kLogTable);
 }
 
 __device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa, int sb, int kind) {
@@ -174,10 +168,9 @@ __device__ __forceinline__ void noteKey(Smem &S, uint32_t *sKeyMin, uint32_t *sR
   }
 }
 
-// NT = 128 (6 CTAs per SM: short barrier groups) or 256 threads per CTA.
 // Lock-free push of record `pos` onto a hash slot's chain.  acq_rel: the
-// record's fields (written before) are visible to whoever later reads the
-// chain through the slot, and this thread sees the fields of every record
+// record's words (written before) are visible to whoever later reads the
+// chain through the slot, and this thread sees the words of every record
 // pushed before it.
 __device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_t val) {
   uint32_t old;
@@ -192,7 +185,15 @@ __device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_
 // PARALLEL sink of the fused kernel: records into shared memory, each
 // pushed onto the chain of its element's hash slot and, at that moment,
 // paired with the records of its element pushed before it (every pair is
-// seen exactly once: by whichever of the two was pushed second).
+// seen exactly once: by whichever of the two was pushed second).  The
+// block's first record of an element also does the element's ownership
+// exchange (the INTER-BLOCK filter): one exchange of epoch:12 | block+1:20
+// per (element, block); whoever replaces another block's tag (or MULTI)
+// marks the element MULTI.  The last exchange on an element that two blocks
+// touched is always followed by a MULTI store, so the final value is MULTI
+// exactly for the elements of >= 2 blocks (epochs: no memset between
+// launches).  Sites whose parameter is provably block-private (host affine
+// analysis, `own` = false) skip it: no other block can reach their elements.
 template <class Smem> struct FusedSink : ParState {
   Smem *S;
   uint32_t tli;      // thread index within the iteration
@@ -200,40 +201,43 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t nrec = 0; // records produced by this thread
   uint32_t R;        // fixed-slot mode: slots per thread (0: allocate)
   uint32_t myBlk;    // MiniCU block within the iteration
-  uint32_t tpb;
   int nLocs;
-  uint32_t *keyMin;  // per key: minimum element (32-bit) realised in the iteration
+  uint32_t *keyMin;  // per key: minimum element realised in the iteration
   uint32_t *real;    // realised keys
-  const uint64_t *conf; // per site: conflicting sites (bit mask)
-  uint32_t *owner;      // per element ownership table (see ownerSettle)
+  const uint64_t *conf; // per site: statically conflicting sites (bit mask)
+  uint32_t *owner;      // per element ownership words (nullptr: ablated)
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
 
-  __device__ __forceinline__ void pairWithEarlier(uint64_t e, uint64_t m, int site, uint32_t q,
-                                                  uint32_t pos) {
+  __device__ __forceinline__ void pairWithEarlier(uint32_t e, uint64_t r1, int site, uint32_t q) {
     bool first = true;
     int len = 0;
+    const int myLoc = sites[site].loc;
     for (; q != Smem::kEnd; q = S->u.ch.next[q]) {
       if (++len > kSmallGroup) { // a hot element: radix grouping instead
         S->hot = 1;
         break;
       }
-      if (S->elem[q] != e)
+      const uint64_t q0 = S->r0[q];
+      if (rElem(q0) != e)
         continue;
-      const uint64_t mq = S->meta[q];
-      if (L->dTpb.div(metaTli(mq)) == myBlk)
+      const uint64_t q1 = S->r1[q];
+      if (rBlk(q1) == myBlk)
         first = false;
-      const int kind = intraKind(*L, sites, mq, m, tpb);
+      const int kind = intraRule(q1, r1);
       if (kind < 0)
         continue;
-      const int sq = metaSite(mq);
+      const int sq = rSite(q0);
       if (!((conf[sq] >> site) & 1ull))
         continue;
-      noteKey(*S, keyMin, real, keyIndex(sites, nLocs, sq, site, kind), static_cast<uint32_t>(e));
+      int la = sites[sq].loc, lb = myLoc;
+      if (lb < la) {
+        const int t = la;
+        la = lb;
+        lb = t;
+      }
+      noteKey(*S, keyMin, real, (la * nLocs + lb) * 3 + kind, e);
     }
-#ifdef HGRD_OWN_POSTPASS
-    S->first[pos] = first;
-#else
     if (first && owner) { // the block's first record of e: one ownership exchange
       const uint32_t old = atomicExch(&owner[e], epochTag | mine);
       if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
@@ -241,7 +245,6 @@ template <class Smem> struct FusedSink : ParState {
         flags |= kFlagShared;
       }
     }
-#endif
   }
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
@@ -263,10 +266,10 @@ template <class Smem> struct FusedSink : ParState {
     }
     ++nrec;
     if (pos < static_cast<unsigned>(Smem::kCap)) {
-      const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
-      const uint64_t m = packMeta(tli, bp, wp, site, seq);
-      S->elem[pos] = e;
-      S->meta[pos] = m;
+      const uint32_t e = static_cast<uint32_t>(P->elemBase + static_cast<uint64_t>(idx));
+      const uint64_t r1 = packR1(tli, myBlk, bp, wp, static_cast<uint32_t>(warp));
+      S->r0[pos] = packR0(site, seq, e);
+      S->r1[pos] = r1;
       uint32_t *head = &S->u.ch.head[hashSlot<Smem>(e)];
       uint32_t h = *reinterpret_cast<volatile uint32_t *>(head);
       for (;;) {
@@ -276,7 +279,7 @@ template <class Smem> struct FusedSink : ParState {
           break;
         h = o;
       }
-      pairWithEarlier(e, m, site, h, pos);
+      pairWithEarlier(e, r1, site, h);
     } else {
       flags |= kFlagFusedOverflow;
     }
@@ -316,10 +319,11 @@ template <class Smem> struct FusedSink : ParState {
   }
 };
 
-template <int NT, int IPT, class Body>
 #ifndef HGRD_FUSED_MINB
 #define HGRD_FUSED_MINB 3
 #endif
+// NT = 128 or 256 threads per CTA; IPT records per thread of capacity.
+template <int NT, int IPT, class Body>
 __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(FusedArgs F) {
   using Smem = FusedSmem<NT, IPT>;
   constexpr int kFusedThreads = NT;
@@ -369,9 +373,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
     for (int i = tid; i < Smem::kTable; i += kFusedThreads)
       S.u.ch.head[i] = Smem::kEnd;
     __syncthreads();
-    // 1. expansion of the iteration's whole MiniCU blocks (records chained
-    //    per hash slot as they are produced)
-    {
+    // 1. expansion of the iteration's whole MiniCU blocks: records pushed
+    //    per hash slot and paired as they are produced (FusedSink)
+    if (!(F.ablate & 8)) {
       unsigned myBp = 0, myWp = 0;
       for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
         FusedSink<Smem> s;
@@ -383,7 +387,6 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.R = F.R;
         s.stride = static_cast<uint32_t>(nb * L.tpb);
         s.myBlk = L.dTpb.div(static_cast<uint32_t>(tl));
-        s.tpb = tpb;
         s.nLocs = F.nLocs;
         s.keyMin = sKeyMin;
         s.real = sReal;
@@ -395,10 +398,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         Body::identity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
         Body::run(L, sCode, bi, s, regs);
         for (uint32_t j = s.nrec; j < F.R; ++j)
-          if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap)) {
-            S.elem[j * s.stride + s.tli] = kNoElem;
-            S.first[j * s.stride + s.tli] = 0;
-          }
+          if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))
+            S.r0[j * s.stride + s.tli] = kNoRec;
         tally.add(s);
         myBp = max(myBp, s.bp);
         myWp = max(myWp, s.wp);
@@ -421,40 +422,6 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       continue;
     if (F.ablate & 1)
       continue;
-    // 2. ownership: one exchange per (element, MiniCU block) — by the
-    //    block's first record of the element (INTRA pairs were found as the
-    //    records were pushed); issued in batches of kOwnBatch, the last batch
-    //    settled at the end of the iteration
-    constexpr int kOwnBatch = 4;
-    static_assert(IPT % kOwnBatch == 0, "IPT must be a multiple of the owner batch");
-    uint64_t oE[kOwnBatch];
-    uint32_t oMine[kOwnBatch], oOld[kOwnBatch];
-    bool oHas[kOwnBatch];
-    auto settleOwners = [&]() {
-#pragma unroll
-      for (int j = 0; j < kOwnBatch; ++j)
-        if (oHas[j])
-          ownerSettle(F, oE[j], oMine[j], oOld[j], myFlags);
-    };
-#pragma unroll
-    for (int k0 = 0; k0 < IPT; k0 += kOwnBatch) {
-      if (k0)
-        settleOwners();
-#pragma unroll
-      for (int j = 0; j < kOwnBatch; ++j) {
-        const unsigned p = tid + static_cast<unsigned>((k0 + j) * NT);
-#ifdef HGRD_OWN_POSTPASS
-        oHas[j] = p < n && S.first[p] && !(F.ablate & 4);
-#else
-        oHas[j] = false;
-#endif
-        if (oHas[j]) {
-          oE[j] = S.elem[p];
-          oMine[j] = static_cast<uint32_t>(firstBlock + L.dTpb.div(metaTli(S.meta[p])) + 1);
-          oOld[j] = atomicExch(&F.owner[oE[j]], (F.epoch << 20) | oMine[j]);
-        }
-      }
-    }
     const bool hashed = S.hot == 0;
     if (!hashed) {
       // radix mode for this iteration: drop the hash-mode keys, sort by
@@ -462,25 +429,26 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       for (unsigned r = tid; r < S.nReal; r += kFusedThreads)
         sKeyMin[sReal[r]] = ~0u;
       if (tid < kMaxWritten) {
-        S.minE[tid] = ~0ull;
+        S.minE[tid] = ~0u;
         S.maxE[tid] = 0;
       }
       __syncthreads();
       if (tid == 0)
         S.nReal = 0;
       for (unsigned i = tid; i < n; i += kFusedThreads) {
-        if (S.elem[i] == kNoElem)
+        const uint64_t r0 = S.r0[i];
+        if (r0 == kNoRec)
           continue;
-        const int w = sParams[sSites[metaSite(S.meta[i])].param].written - 1;
-        atomicMin(&S.minE[w], static_cast<unsigned long long>(S.elem[i]));
-        atomicMax(&S.maxE[w], static_cast<unsigned long long>(S.elem[i]));
+        const int w = sParams[sSites[rSite(r0)].param].written - 1;
+        atomicMin(&S.minE[w], rElem(r0));
+        atomicMax(&S.maxE[w], rElem(r0));
       }
       __syncthreads();
       if (tid == 0) {
         uint64_t span = 1;
         for (int w = 0; w < F.nW && w < kMaxWritten; ++w)
           if (S.minE[w] <= S.maxE[w])
-            span = max(span, static_cast<uint64_t>(S.maxE[w] - S.minE[w] + 1));
+            span = max(span, static_cast<uint64_t>(S.maxE[w] - S.minE[w]) + 1);
         const int bL = bitsForDev(static_cast<uint64_t>(ws < L.tpb ? ws : L.tpb));
         const int bW = bitsForDev(static_cast<uint64_t>((L.tpb + ws - 1) / ws));
         const int bQ = bitsForDev(uint64_t(S.maxWp) + 1);
@@ -507,18 +475,19 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       for (int j = 0; j < IPT; ++j) {
         const unsigned i = static_cast<unsigned>(tid * IPT + j);
         vals[j] = i;
-        if (i < n && S.elem[i] != kNoElem) {
-          const uint64_t m = S.meta[i];
-          const uint32_t tli = metaTli(m);
-          const uint32_t blk = L.dTpb.div(tli), tl = tli - blk * tpb;
-          const uint32_t warp = L.dWs.div(tl), lane = tl - warp * static_cast<uint32_t>(ws);
-          const int w = sParams[sSites[metaSite(m)].param].written - 1;
-          const uint64_t off = S.elem[i] - S.minE[w];
+        const uint64_t r0 = i < n ? S.r0[i] : kNoRec;
+        if (r0 != kNoRec) {
+          const uint64_t r1 = S.r1[i];
+          const uint32_t blk = rBlk(r1), warp = rWarp(r1);
+          const uint32_t tl = rTli(r1) - blk * tpb;
+          const uint32_t lane = tl - warp * static_cast<uint32_t>(ws);
+          const int w = sParams[sSites[rSite(r0)].param].written - 1;
+          const uint64_t off = rElem(r0) - S.minE[w];
           keys[j] = (static_cast<uint64_t>(w) << S.fW) | (off << S.fOff) |
                     (static_cast<uint64_t>(blk) << S.fBlk) |
-                    (static_cast<uint64_t>(metaBp(m)) << S.fBp) |
+                    (static_cast<uint64_t>(rBp(r1)) << S.fBp) |
                     (static_cast<uint64_t>(warp) << S.fWarp) |
-                    (static_cast<uint64_t>(metaWp(m)) << S.fWp) | lane;
+                    (static_cast<uint64_t>(rWp(r1)) << S.fWp) | lane;
         } else {
           keys[j] = ~0ull;
         }
@@ -575,11 +544,11 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
             p3 = 0;
             g3 = k >> shLane;
           }
-          const uint64_t m = S.meta[S.u.rx.sidx[q]];
-          const int s = metaSite(m);
-          const uint32_t tli = metaTli(m);
-          const uint32_t tl = tli - L.dTpb.div(tli) * tpb;
-          const uint32_t wq = L.dWs.div(tl);
+          const uint32_t ri = S.u.rx.sidx[q];
+          const int s = rSite(S.r0[ri]);
+          const uint64_t r1 = S.r1[ri];
+          const uint32_t wq = rWarp(r1);
+          const uint32_t tl = rTli(r1) - rBlk(r1) * tpb;
           note(p2, mn2, mx2, s, wq);
           note(p3, mn3, mx3, s, tl - wq * static_cast<uint32_t>(ws));
         }
@@ -588,7 +557,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       }
       __syncthreads();
     }
-    // 3. witnesses of the keys realised in this iteration
+    // 2. witnesses of the keys realised in this iteration
     const unsigned nReal = S.nReal;
     for (unsigned r = tid; r < nReal; r += kFusedThreads) {
       const int K = static_cast<int>(sReal[r]);
@@ -598,13 +567,13 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       sKeyMin[K] = ~0u; // reset for the next iteration
       // the key's minimum element in this iteration: its records are the
       // slot chain (hash mode) or a sorted range (radix mode)
-      uint64_t ge;
+      uint32_t ge;
       uint32_t g0 = 0, g1 = 0;
       if (hashed) {
         ge = v;
       } else {
-        g0 = static_cast<uint32_t>(v);
-        ge = S.elem[S.u.rx.sidx[g0]];
+        g0 = v;
+        ge = rElem(S.r0[S.u.rx.sidx[g0]]);
         const uint64_t g = S.u.rx.skey[g0] >> S.fOff;
         g1 = g0 + 1;
         while (g1 < n && (S.u.rx.skey[g1] >> S.fOff) == g)
@@ -617,41 +586,41 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       if (hashed) {
         for (uint32_t q = S.u.ch.head[hashSlot<Smem>(ge)]; q != Smem::kEnd && nm <= kSmallGroup;
              q = S.u.ch.next[q])
-          if (S.elem[q] == ge)
+          if (rElem(S.r0[q]) == ge)
             mem[nm++] = q;
       }
       const int cnt = hashed ? nm : static_cast<int>(g1 - g0);
       auto rec = [&](int i) -> uint32_t { return hashed ? mem[i] : S.u.rx.sidx[g0 + i]; };
       uint64_t bestX = ~0ull, bestY = ~0ull;
       int sX = 0, sY = 0;
-      auto order = [&](uint64_t m) {
-        const uint64_t thread = static_cast<uint64_t>(firstBlock * L.tpb) + metaTli(m);
-        return (thread << kSeqBits) | metaSeq(m);
+      auto order = [&](uint64_t r0, uint64_t r1) {
+        const uint64_t thread = static_cast<uint64_t>(firstBlock * L.tpb) + rTli(r1);
+        return (thread << kSeqBits) | rSeq(r0);
       };
       // lexicographically first (x, y) over the element's racing pairs of K
       for (int a = 0; a < cnt; ++a) {
-        const uint64_t ma = S.meta[rec(a)];
-        const int sa = metaSite(ma);
+        const uint64_t a0 = S.r0[rec(a)], a1 = S.r1[rec(a)];
+        const int sa = rSite(a0);
         const int loa = sSites[sa].loc;
         if (loa != la && loa != lb)
           continue;
-        const uint64_t oa = order(ma);
+        const uint64_t oa = order(a0, a1);
         if (oa > bestX)
           continue;
         for (int b = 0; b < cnt; ++b) {
           if (b == a)
             continue;
-          const uint64_t mb = S.meta[rec(b)];
-          const uint64_t ob = order(mb);
+          const uint64_t b0 = S.r0[rec(b)], b1 = S.r1[rec(b)];
+          const uint64_t ob = order(b0, b1);
           if (ob <= oa)
             continue; // y must follow x in event order
-          const int sb = metaSite(mb);
+          const int sb = rSite(b0);
           const int lob = sSites[sb].loc;
           if (!((loa == la && lob == lb) || (loa == lb && lob == la)))
             continue;
           if (!((sConf[sa] >> sb) & 1ull))
             continue;
-          if (intraKind(L, sSites, ma, mb, tpb) != kind)
+          if (intraRule(a1, b1) != kind)
             continue;
           if (oa < bestX || (oa == bestX && ob < bestY)) {
             bestX = oa;
@@ -670,7 +639,6 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
           myFlags |= kFlagFusedOverflow;
       }
     }
-    settleOwners();
     if (tid == 0)
       S.nReal = 0;
   }

@@ -235,6 +235,12 @@ int hgrd_gpu_sweep_shard_json(hgrd_gpu_ctx *ctx, const char *source,
 int hgrd_gpu_count_inputs(const char *source, const char *file_name);
 /* Lowering only: bytecode, sites, locs and per-kernel facts of one kernel as
  * JSON (for callers that fix launch parameters themselves). */
+/* Host analysis (no GPU needed): out[s] = 1 when site s's buffer is proven
+ * block-private for this launch (affine indices whose per-block element
+ * ranges are disjoint), so the fused path skips its ownership exchange.
+ * out has launch->n_sites entries. */
+int hgrd_gpu_block_private(const hgrd_gpu_launch *launch, uint8_t *out);
+
 /* Development check (no GPU needed): lower `kernel`, generate its NVRTC
  * thread body for the given geometry (scalar parameters 0, every site
  * recording) and compile all three specialised kernels for sm_100a without

@@ -148,6 +148,7 @@ def load_library() -> ctypes.CDLL:
                                               ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
                                               ctypes.POINTER(P)]
     lib.hgrd_gpu_count_inputs.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+    lib.hgrd_gpu_block_private.argtypes = [P, ctypes.POINTER(ctypes.c_uint8)]
     I3 = ctypes.c_int64 * 3
     lib.hgrd_gpu_jit_check.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, I3, I3,
                                        ctypes.c_int64, ctypes.POINTER(P)]
@@ -239,6 +240,17 @@ class LaunchSpec:
                              self._sites, len(sites), len(lowered["locs"]), self._ph, len(ph),
                              flags, (c_int64 * 3)(*grid), (c_int64 * 3)(*block), warp_size,
                              step_budget)
+
+    def block_private(self):
+        """Per site: True when its buffer is proven block-private (host
+        affine analysis, affine.cpp); no GPU needed."""
+        lib = load_library()
+        n = self.launch.n_sites
+        out = (ctypes.c_uint8 * max(n, 1))()
+        rc = lib.hgrd_gpu_block_private(ctypes.byref(self.launch), out)
+        if rc:
+            raise RuntimeError(f"block_private failed ({rc})")
+        return [bool(out[i]) for i in range(n)]
 
     @property
     def n_threads(self) -> int:

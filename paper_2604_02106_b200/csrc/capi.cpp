@@ -3,6 +3,7 @@
 // device-buffer / check-launch ABI of include/hgrd_gpu.h.
 #include "hgrd_gpu.h"
 #include "host.hpp"
+#include "gpu/affine.hpp"
 #include "gpu/jit.hpp"
 
 #include <cstdlib>
@@ -112,6 +113,15 @@ std::string escapeJson(const std::string &in) {
 }
 } // namespace
 
+extern "C" int hgrd_gpu_block_private(const hgrd_gpu_launch *launch, uint8_t *out) {
+  if (!launch || (!out && launch->n_sites))
+    return HGRD_GPU_EINVAL;
+  const std::vector<uint8_t> p = blockPrivateSites(*launch);
+  for (size_t s = 0; s < p.size(); ++s)
+    out[s] = p[s];
+  return HGRD_GPU_OK;
+}
+
 extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, const char *kernel,
                                   const int64_t grid[3], const int64_t block[3],
                                   int64_t warp_size, char **out) {
@@ -142,7 +152,7 @@ extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, con
     L.block[i] = block[i];
   }
   L.warp_size = warp_size;
-  const std::vector<uint8_t> rec(lk.sites.size(), 1);
+  const std::vector<uint8_t> rec(lk.sites.size(), 3);
   std::string s = "{\"variants\":[";
   bool ok = true;
   for (int v = 0; v < 3; ++v) {

@@ -9,6 +9,7 @@
 #include "device.cuh"
 #include "expand.cuh"
 #include "fused.cuh"
+#include "affine.hpp"
 #include "jit.hpp"
 
 #include <cub/cub.cuh>
@@ -326,6 +327,7 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
     P.params[p] = d;
   }
   P.sites.resize(std::max<uint32_t>(L.n_sites, 1));
+  const std::vector<uint8_t> priv = hgrdgpu::blockPrivateSites(L);
   for (uint32_t s = 0; s < L.n_sites; ++s) {
     SiteDev d{};
     d.param = L.sites[s].param;
@@ -335,6 +337,7 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
     d.scope = L.sites[s].scope;
     int32_t h = handleOfParam(d.param);
     d.record = (h >= 0 && written[static_cast<size_t>(h)]) ? 1 : 0;
+    d.own = d.record && !priv[s];
     P.sites[s] = d;
   }
   P.summaryOk = L.n_sites <= static_cast<uint32_t>(kMaxSites);
@@ -630,7 +633,7 @@ int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t
 template <int NT, int IPT>
 size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
   const size_t nKeysPad = (static_cast<size_t>(nKeys) + 3) & ~size_t(3);
-  return align16(sizeof(FusedSmem<NT, IPT>)) + 8 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
+  return align16(sizeof(FusedSmem<NT, IPT>)) + 12 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
          sizeof(SiteDev) * P.sites.size() + sizeof(ParamDev) * P.params.size() +
          8 * P.sites.size();
 }
@@ -1008,8 +1011,8 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   // NVRTC specialisation for large PARALLEL launches (compiled on first use)
   const bool useJit = !seq && (c->jitMode == 2 || (c->jitMode == 1 && D.nThreads >= (int64_t(1) << 14)));
   JitGetter jk{c, &L, useJit, {}};
-  for (const auto &s : P.sites)
-    jk.rec.push_back(s.record ? 1 : 0);
+  for (const auto &s : P.sites) // bit 0: record, bit 1: ownership exchange
+    jk.rec.push_back(static_cast<uint8_t>((s.record ? 1 : 0) | (s.own ? 2 : 0)));
   if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
     rc = runFused(c, L, D, o, P, R, recInsns, loops, jk);
     if (rc < 0)

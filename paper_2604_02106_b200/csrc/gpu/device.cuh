@@ -56,7 +56,8 @@ struct SiteDev {
   int32_t param;
   int32_t loc;
   uint8_t kind, aop, scope, record; // record: access lands in a written buffer
-  int32_t valueNeeded;
+  uint8_t own;  // fused path: the buffer may be reached from two blocks (ownership exchange)
+  uint8_t pad0, pad1, pad2;
 };
 
 struct KeyLayout {

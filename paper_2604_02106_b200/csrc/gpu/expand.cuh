@@ -141,7 +141,7 @@ struct ParSink : ParState {
     ++recs;
   }
   // K variants: the site's parameter and record flag as (JIT) constants
-  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, int64_t idx,
+  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, bool, int64_t idx,
                                            bool need) {
     const ParamDev *P = checkK(param, idx);
     if (!P)
@@ -151,7 +151,8 @@ struct ParSink : ParState {
     ++seq;
     return need ? __ldg(P->ptr + idx) : 0;
   }
-  __device__ __forceinline__ void storeK(int site, int param, bool rec, int64_t idx, int64_t) {
+  __device__ __forceinline__ void storeK(int site, int param, bool rec, bool, int64_t idx,
+                                         int64_t) {
     const ParamDev *P = checkK(param, idx);
     if (!P)
       return;
@@ -159,18 +160,18 @@ struct ParSink : ParState {
       record(site, P, idx);
     ++seq;
   }
-  __device__ __forceinline__ void atomicK(int site, int param, bool rec, int64_t idx, int64_t,
-                                          int64_t) {
-    storeK(site, param, rec, idx, 0);
+  __device__ __forceinline__ void atomicK(int site, int param, bool rec, bool own, int64_t idx,
+                                          int64_t, int64_t) {
+    storeK(site, param, rec, own, idx, 0);
   }
   __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
-    return loadK(site, sites[site].param, sites[site].record, idx, need);
+    return loadK(site, sites[site].param, sites[site].record, false, idx, need);
   }
   __device__ __forceinline__ void store(int site, int64_t idx, int64_t v) {
-    storeK(site, sites[site].param, sites[site].record, idx, v);
+    storeK(site, sites[site].param, sites[site].record, false, idx, v);
   }
   __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t v, int64_t c) {
-    atomicK(site, sites[site].param, sites[site].record, idx, v, c);
+    atomicK(site, sites[site].param, sites[site].record, false, idx, v, c);
   }
 };
 

@@ -209,7 +209,8 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
 
-  __device__ __forceinline__ void pairWithEarlier(uint32_t e, uint64_t r1, int site, uint32_t q) {
+  __device__ __forceinline__ void pairWithEarlier(uint32_t e, uint64_t r1, int site, uint32_t q,
+                                                  bool own) {
     bool first = true;
     int len = 0;
     const int myLoc = sites[site].loc;
@@ -238,7 +239,7 @@ template <class Smem> struct FusedSink : ParState {
       }
       noteKey(*S, keyMin, real, (la * nLocs + lb) * 3 + kind, e);
     }
-    if (first && owner) { // the block's first record of e: one ownership exchange
+    if (own && first && owner) { // the block's first record of e: one ownership exchange
       const uint32_t old = atomicExch(&owner[e], epochTag | mine);
       if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
         atomicExch(&owner[e], epochTag | kOwnerMulti);
@@ -247,7 +248,7 @@ template <class Smem> struct FusedSink : ParState {
     }
   }
 
-  __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
+  __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx, bool own) {
     if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
       flags |= kFlagFusedOverflow;
     unsigned pos;
@@ -279,43 +280,48 @@ template <class Smem> struct FusedSink : ParState {
           break;
         h = o;
       }
-      pairWithEarlier(e, r1, site, h);
+      pairWithEarlier(e, r1, site, h, own);
     } else {
       flags |= kFlagFusedOverflow;
     }
     ++recs;
   }
-  // K variants: the site's parameter and record flag as (JIT) constants
-  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, int64_t idx,
+  // K variants: the site's parameter, record and ownership flags as (JIT)
+  // constants
+  __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, bool own, int64_t idx,
                                            bool need) {
     const ParamDev *P = checkK(param, idx);
     if (!P)
       return 0;
     if (rec)
-      record(site, P, idx);
+      record(site, P, idx, own);
     ++seq;
     return need ? __ldg(P->ptr + idx) : 0;
   }
-  __device__ __forceinline__ void storeK(int site, int param, bool rec, int64_t idx, int64_t) {
+  __device__ __forceinline__ void storeK(int site, int param, bool rec, bool own, int64_t idx,
+                                         int64_t) {
     const ParamDev *P = checkK(param, idx);
     if (!P)
       return;
     if (rec)
-      record(site, P, idx);
+      record(site, P, idx, own);
     ++seq;
   }
-  __device__ __forceinline__ void atomicK(int site, int param, bool rec, int64_t idx, int64_t,
-                                          int64_t) {
-    storeK(site, param, rec, idx, 0);
+  __device__ __forceinline__ void atomicK(int site, int param, bool rec, bool own, int64_t idx,
+                                          int64_t, int64_t) {
+    storeK(site, param, rec, own, idx, 0);
   }
   __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
-    return loadK(site, sites[site].param, sites[site].record, idx, need);
+    const SiteDev &S_ = sites[site];
+    return loadK(site, S_.param, S_.record, S_.own, idx, need);
   }
   __device__ __forceinline__ void store(int site, int64_t idx, int64_t v) {
-    storeK(site, sites[site].param, sites[site].record, idx, v);
+    const SiteDev &S_ = sites[site];
+    storeK(site, S_.param, S_.record, S_.own, idx, v);
   }
   __device__ __forceinline__ void atomic(int site, int64_t idx, int64_t v, int64_t c) {
-    atomicK(site, sites[site].param, sites[site].record, idx, v, c);
+    const SiteDev &S_ = sites[site];
+    atomicK(site, S_.param, S_.record, S_.own, idx, v, c);
   }
 };
 
@@ -333,7 +339,10 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   const int nKeysPad = (F.nKeys + 3) & ~3;
   uint32_t *sKeyMin = reinterpret_cast<uint32_t *>(after);
   uint32_t *sReal = reinterpret_cast<uint32_t *>(sKeyMin + nKeysPad);
-  hgrd_gpu_insn *sCode = reinterpret_cast<hgrd_gpu_insn *>(sReal + nKeysPad);
+  // per key: an upper bound of the global minimum element F.keyElem[K]
+  // (it only decreases), so later iterations skip most global reads
+  uint32_t *sKeyBound = sReal + nKeysPad;
+  hgrd_gpu_insn *sCode = reinterpret_cast<hgrd_gpu_insn *>(sKeyBound + nKeysPad);
   SiteDev *sSites = reinterpret_cast<SiteDev *>(sCode + F.L.nCode);
   ParamDev *sParams = reinterpret_cast<ParamDev *>(sSites + F.L.nSites);
   uint64_t *sConf = reinterpret_cast<uint64_t *>(sParams + F.L.nParams);
@@ -348,8 +357,10 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   }
   for (int i = tid; i < L.nParams; i += kFusedThreads)
     sParams[i] = L.params[i];
-  for (int i = tid; i < F.nKeys; i += kFusedThreads)
+  for (int i = tid; i < F.nKeys; i += kFusedThreads) {
     sKeyMin[i] = ~0u;
+    sKeyBound[i] = ~0u;
+  }
   if (tid == 0) {
     S.nReal = 0;
     S.flags = 0;
@@ -579,8 +590,15 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         while (g1 < n && (S.u.rx.skey[g1] >> S.fOff) == g)
           ++g1;
       }
-      if (ge > F.keyElem[K])
-        continue; // another block already holds a smaller element for K
+      if (ge > sKeyBound[K])
+        continue; // a smaller element for K is known
+      {
+        const unsigned long long g = __ldcg(&F.keyElem[K]);
+        if (ge > g) { // another block already holds a smaller element for K
+          sKeyBound[K] = static_cast<uint32_t>(g);
+          continue;
+        }
+      }
       uint32_t mem[kSmallGroup + 1];
       int nm = 0;
       if (hashed) {
@@ -631,6 +649,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         }
       }
       const unsigned long long old = atomicMin(&F.keyElem[K], static_cast<unsigned long long>(ge));
+      sKeyBound[K] = old < ge ? static_cast<uint32_t>(old) : ge;
       if (ge <= old) {
         const unsigned c = atomicAdd(F.candCount, 1u);
         if (c < F.candCap)

@@ -87,12 +87,13 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec) 
     if (I.op == HGRD_OP_JZ || I.op == HGRD_OP_JMP)
       target[static_cast<size_t>(I.imm)] = 1;
   }
-  // site -> "site, param, record" literal arguments of the sink's K accessors
+  // site -> "site, param, record, own" literal arguments of the sink's K
+  // accessors (rec[s]: bit 0 record, bit 1 ownership exchange)
   auto site = [&](int64_t s) {
     const size_t i = static_cast<size_t>(s);
-    const bool r = i < rec.size() ? rec[i] != 0 : true;
+    const uint8_t f = i < rec.size() ? rec[i] : 3;
     return std::to_string(s) + ", " + std::to_string(i < L.n_sites ? L.sites[i].param : 0) +
-           ", " + (r ? "true" : "false");
+           ", " + ((f & 1) ? "true" : "false") + ", " + ((f & 2) ? "true" : "false");
   };
   std::ostringstream o;
   o << "#include \"jit_kernels.cuh\"\n"

@@ -18,7 +18,8 @@ void destroy(Cache *c);
 // The specialised kernel `v` for this launch's code and constants (compiled
 // on first use, cached).  Returns nullptr (and err) when NVRTC is
 // unavailable or the compile fails; callers then use the interpreter.
-// `rec[s]`: whether site s produces race-check records (host value analysis).
+// `rec[s]`: bit 0: site s produces race-check records (written buffer);
+// bit 1: its buffer may be reached from two blocks (ownership exchange).
 const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
                 std::string &err);
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec);

@@ -74,3 +74,39 @@ def test_jit_bodies_compile_for_sm100a(name):
     }[name]
     d = hg.jit_check(src, kernel, grid, block)
     assert all(v["cubin_bytes"] > 0 for v in d["variants"]), d
+
+
+def _block_private(src, kernel, grid, block, handles, scalars=None):
+    low = hg.lower(src, kernel)
+    spec = hg.LaunchSpec(low, grid, block, 32, handles=handles, scalars=scalars)
+    return {(s["array"], s["kind"]): p for s, p in zip(low["sites"], spec.block_private())}
+
+
+def test_block_private_analysis():
+    """Affine partition proof (csrc/gpu/affine.cpp) that lets the fused path
+    skip ownership exchanges: per-block tiles are private, a transposed
+    store and data-dependent bins are not, aliasing defeats the proof."""
+    st = programs.stencil(1 << 12)
+    got = _block_private(st, "st", (16, 1, 1), (256, 1, 1), {"in_": 0, "tile": 1, "out_": 2})
+    assert all(got.values())
+    # tile and out_ aliased: strides 258 vs 256 per block -> no proof
+    got = _block_private(st, "st", (16, 1, 1), (256, 1, 1), {"in_": 0, "tile": 1, "out_": 1})
+    assert not got[("tile", 1)] and not got[("out_", 1)] and got[("in_", 0)]
+    tr = programs.transpose(256)
+    got = _block_private(tr, "tr", (8, 8, 1), (32, 32, 1), {"tile": 0, "out_": 1}, {"n": 256})
+    assert got[("tile", 1)] and not got[("out_", 1)]
+    hist = programs.histogram(1 << 12, 64)
+    got = _block_private(hist, "h", (16, 1, 1), (256, 1, 1), {"data": 0, "hist": 1})
+    assert got[("data", 0)] and not got[("hist", 1)]
+    # a block stride equal to the tile width still separates; one less does not
+    for stride, ok in ((256, True), (255, False)):
+        src = ("__global__ void k(int *A) {\n"
+               f"  A[blockIdx.x * {stride} + threadIdx.x] = 1;\n}}\n"
+               "void main() { int *A; cudaMalloc(&A, 8192);\n"
+               "  k<<<16,256>>>(A); }\n")
+        assert _block_private(src, "k", (16, 1, 1), (256, 1, 1), {"A": 0})[("A", 1)] is ok
+    # loops: no proof
+    src = ("__global__ void k(int *A) {\n  for (int i = 0; i < 2; i++) {\n"
+           "    A[blockIdx.x * 512 + threadIdx.x + i] = 1;\n  }\n}\n"
+           "void main() { int *A; cudaMalloc(&A, 8192);\n  k<<<4,256>>>(A); }\n")
+    assert not _block_private(src, "k", (4, 1, 1), (256, 1, 1), {"A": 0})[("A", 1)]

@@ -155,7 +155,7 @@ extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, con
   const std::vector<uint8_t> rec(lk.sites.size(), 3);
   std::string s = "{\"variants\":[";
   bool ok = true;
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < 4; ++v) {
     std::string err;
     const size_t bytes = hgrdgpu::jit::compileOnly(L, rec, static_cast<hgrdgpu::jit::Variant>(v), err);
     ok = ok && bytes > 0;

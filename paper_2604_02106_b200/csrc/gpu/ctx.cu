@@ -676,17 +676,22 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
              JitGetter &jk) {
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
-  int64_t bpi = std::max<int64_t>(1, 256 / D.tpb); // ~256 MiniCU threads per iteration
+  static const int64_t kIterThreads = [] { // development knob: MiniCU threads per iteration
+    const char *e = std::getenv("HGRD_FUSED_ITER");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(512);
+  }();
+  int64_t bpi = std::max<int64_t>(1, kIterThreads / D.tpb);
   const uint64_t per = std::max<uint32_t>(recInsns, 1);
   while (bpi > 1 && static_cast<uint64_t>(bpi * D.tpb) * per > 4096)
     bpi /= 2;
   const uint64_t perIter = static_cast<uint64_t>(bpi * D.tpb) * per;
   if (bpi * D.tpb > 65536 || (!loops && perIter > 4096))
     return 0;
-  // up to 1024 records: 256 threads x 4; else 256 x 16
-  const bool narrow = !loops && perIter <= 1024;
-  const size_t smem =
-      narrow ? fusedSmemBytes<256, 4>(L, P, nKeys) : fusedSmemBytes<256, 16>(L, P, nKeys);
+  // record capacity per iteration: 256 threads x 4, x 8 or x 16
+  const int ipt = (!loops && perIter <= 1024) ? 4 : (!loops && perIter <= 2048) ? 8 : 16;
+  const size_t smem = ipt == 4   ? fusedSmemBytes<256, 4>(L, P, nKeys)
+                      : ipt == 8 ? fusedSmemBytes<256, 8>(L, P, nKeys)
+                                 : fusedSmemBytes<256, 16>(L, P, nKeys);
   if (smem > 227 * 1024)
     return 0;
 
@@ -721,8 +726,9 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
   if (const char *ab = std::getenv("HGRD_FUSED_ABLATE"))
     F.ablate = std::atoi(ab);
-  int rc = narrow ? launchFused<256, 4>(c, F, smem, jk.get(hgrdgpu::jit::kFusedNarrow))
-                  : launchFused<256, 16>(c, F, smem, jk.get(hgrdgpu::jit::kFusedWide));
+  int rc = ipt == 4   ? launchFused<256, 4>(c, F, smem, jk.get(hgrdgpu::jit::kFusedNarrow))
+           : ipt == 8 ? launchFused<256, 8>(c, F, smem, jk.get(hgrdgpu::jit::kFusedMid))
+                      : launchFused<256, 16>(c, F, smem, jk.get(hgrdgpu::jit::kFusedWide));
   if (rc < 0)
     return rc;
   CK(cudaGetLastError());

@@ -10,7 +10,8 @@
 namespace hgrdgpu {
 namespace jit {
 
-enum Variant { kExpandPar = 0, kFusedNarrow = 1, kFusedWide = 2 }; // k_fused<256,4> / <256,16>
+// k_expand_par, k_fused<256,4> / <256,8> / <256,16>
+enum Variant { kExpandPar = 0, kFusedNarrow = 1, kFusedWide = 2, kFusedMid = 3 };
 
 struct Cache;
 Cache *create();

@@ -153,11 +153,14 @@ extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, con
   }
   L.warp_size = warp_size;
   const std::vector<uint8_t> rec(lk.sites.size(), 3);
+  std::vector<hgrdgpu::jit::JitParam> params(handles.size(),
+                                             hgrdgpu::jit::JitParam{int64_t(1) << 20, 0});
+  L.step_budget = int64_t(1) << 40;
   std::string s = "{\"variants\":[";
   bool ok = true;
   for (int v = 0; v < 4; ++v) {
     std::string err;
-    const size_t bytes = hgrdgpu::jit::compileOnly(L, rec, static_cast<hgrdgpu::jit::Variant>(v), err);
+    const size_t bytes = hgrdgpu::jit::compileOnly(L, rec, params, static_cast<hgrdgpu::jit::Variant>(v), err);
     ok = ok && bytes > 0;
     s += (v ? "," : "") + std::string("{\"cubin_bytes\":") + std::to_string(bytes) +
          ",\"error\":\"" + escapeJson(err) + "\"}";

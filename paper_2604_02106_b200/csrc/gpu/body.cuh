@@ -64,6 +64,7 @@ __device__ __forceinline__ void threadIdentity(const LaunchDev &L, int64_t t, Bu
 }
 
 struct InterpBody {
+  static constexpr int kFixedR = -1; // records per thread not known at compile time
   __device__ static __forceinline__ void identity(const LaunchDev &L, int64_t t, Builtins &b,
                                                   int64_t &block, int64_t &warp, int64_t &lane) {
     threadIdentity(L, t, b, block, warp, lane);
@@ -150,6 +151,8 @@ struct ParState {
     }
     return true;
   }
+  // JIT bodies of loop-free kernels whose statement count fits the budget
+  __device__ __forceinline__ void stepNC() { ++steps; }
   // Returns the parameter when the access is in bounds (an instance).
   __device__ __forceinline__ const ParamDev *check(int site, int64_t idx) {
     return checkK(sites[site].param, idx);

@@ -594,13 +594,14 @@ struct JitGetter {
   const hgrd_gpu_launch *L;
   bool enabled;
   std::vector<uint8_t> rec; // per site: produces race-check records
+  std::vector<hgrdgpu::jit::JitParam> params; // per kernel parameter: size, element base
   const void *get(hgrdgpu::jit::Variant v) {
     if (!enabled)
       return nullptr;
     if (!c->jit)
       c->jit = hgrdgpu::jit::create();
     std::string err;
-    const void *k = hgrdgpu::jit::get(c->jit, *L, rec, v, err);
+    const void *k = hgrdgpu::jit::get(c->jit, *L, rec, params, v, err);
     if (!k && !err.empty()) {
       c->jitErr = err;
       ++c->jitFailures;
@@ -1016,7 +1017,11 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
                        !(L.flags & HGRD_LAUNCH_GENERAL);
   // NVRTC specialisation for large PARALLEL launches (compiled on first use)
   const bool useJit = !seq && (c->jitMode == 2 || (c->jitMode == 1 && D.nThreads >= (int64_t(1) << 14)));
-  JitGetter jk{c, &L, useJit, {}};
+  JitGetter jk{c, &L, useJit, {}, {}};
+  for (uint32_t p = 0; p < L.n_params; ++p) {
+    const ParamDev &d = P.params[p];
+    jk.params.push_back(hgrdgpu::jit::JitParam{d.handle >= 0 ? d.size : 0, d.elemBase});
+  }
   for (const auto &s : P.sites) // bit 0: record, bit 1: ownership exchange
     jk.rec.push_back(static_cast<uint8_t>((s.record ? 1 : 0) | (s.own ? 2 : 0)));
   if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {

@@ -100,7 +100,9 @@ struct ParSink : ParState {
   LaneRecords *out;
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
-    const uint64_t e = P->elemBase + static_cast<uint64_t>(idx);
+    recordE(site, P->elemBase + static_cast<uint64_t>(idx));
+  }
+  __device__ __forceinline__ void recordE(int site, uint64_t e) {
     if (L->ownerFilter && L->ownerFilter[e] != L->ownerMultiTag)
       return; // fused pass 2: only elements shared by blocks
     if (L->interTab) { // INTER summary: EMPTY -> one block -> MULTI, no record
@@ -139,6 +141,28 @@ struct ParSink : ParState {
       }
     }
     ++recs;
+  }
+  // C variants (JIT bodies): the site's parameter, flags, buffer size and
+  // element base as constants (size 0: unallocated parameter, always traps)
+  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool, int64_t idx,
+                                           bool need, int64_t size, uint64_t base) {
+    if (static_cast<uint64_t>(idx) >= static_cast<uint64_t>(size)) {
+      ++traps;
+      return 0;
+    }
+    ++inst;
+    if (rec)
+      recordE(site, base + static_cast<uint64_t>(idx));
+    ++seq;
+    return need ? __ldg(params[param].ptr + idx) : 0;
+  }
+  __device__ __forceinline__ void storeC(int site, int param, bool rec, bool own, int64_t idx,
+                                         int64_t, int64_t size, uint64_t base) {
+    loadC(site, param, rec, own, idx, false, size, base);
+  }
+  __device__ __forceinline__ void atomicC(int site, int param, bool rec, bool own, int64_t idx,
+                                          int64_t, int64_t, int64_t size, uint64_t base) {
+    loadC(site, param, rec, own, idx, false, size, base);
   }
   // K variants: the site's parameter and record flag as (JIT) constants
   __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, bool, int64_t idx,

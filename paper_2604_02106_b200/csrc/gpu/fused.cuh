@@ -249,6 +249,9 @@ template <class Smem> struct FusedSink : ParState {
   }
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx, bool own) {
+    recordE(site, P->elemBase + static_cast<uint64_t>(idx), own);
+  }
+  __device__ __forceinline__ void recordE(int site, uint64_t elem, bool own) {
     if (bp > 255 || wp > 255 || seq > kSeqMask || site > kMaxSiteId)
       flags |= kFlagFusedOverflow;
     unsigned pos;
@@ -267,7 +270,7 @@ template <class Smem> struct FusedSink : ParState {
     }
     ++nrec;
     if (pos < static_cast<unsigned>(Smem::kCap)) {
-      const uint32_t e = static_cast<uint32_t>(P->elemBase + static_cast<uint64_t>(idx));
+      const uint32_t e = static_cast<uint32_t>(elem);
       const uint64_t r1 = packR1(tli, myBlk, bp, wp, static_cast<uint32_t>(warp));
       S->r0[pos] = packR0(site, seq, e);
       S->r1[pos] = r1;
@@ -285,6 +288,28 @@ template <class Smem> struct FusedSink : ParState {
       flags |= kFlagFusedOverflow;
     }
     ++recs;
+  }
+  // C variants (JIT bodies): the site's parameter, flags, buffer size and
+  // element base as constants (size 0: unallocated parameter, always traps)
+  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool own, int64_t idx,
+                                           bool need, int64_t size, uint64_t base) {
+    if (static_cast<uint64_t>(idx) >= static_cast<uint64_t>(size)) {
+      ++traps;
+      return 0;
+    }
+    ++inst;
+    if (rec)
+      recordE(site, base + static_cast<uint64_t>(idx), own);
+    ++seq;
+    return need ? __ldg(params[param].ptr + idx) : 0;
+  }
+  __device__ __forceinline__ void storeC(int site, int param, bool rec, bool own, int64_t idx,
+                                         int64_t, int64_t size, uint64_t base) {
+    loadC(site, param, rec, own, idx, false, size, base);
+  }
+  __device__ __forceinline__ void atomicC(int site, int param, bool rec, bool own, int64_t idx,
+                                          int64_t, int64_t, int64_t size, uint64_t base) {
+    loadC(site, param, rec, own, idx, false, size, base);
   }
   // K variants: the site's parameter, record and ownership flags as (JIT)
   // constants
@@ -367,6 +392,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   }
   const uint32_t tpb = static_cast<uint32_t>(L.tpb);
   const int64_t ws = L.ws;
+  // records per thread (fixed slots) — a compile-time constant in JIT bodies
+  const uint32_t fixedR = Body::kFixedR >= 0 ? static_cast<uint32_t>(Body::kFixedR) : F.R;
   LaneTally tally;
   unsigned myFlags = 0;
   int64_t regs[kMaxRegs];
@@ -376,7 +403,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
     const int64_t nb = min(static_cast<int64_t>(F.bpi), L.nBlocks - firstBlock);
     __syncthreads();
     if (tid == 0) {
-      S.count = F.R ? static_cast<unsigned>(nb * L.tpb) * F.R : 0;
+      S.count = fixedR ? static_cast<unsigned>(nb * L.tpb) * fixedR : 0;
       S.maxBp = 0;
       S.maxWp = 0;
       S.hot = 0;
@@ -395,7 +422,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.params = sParams;
         s.S = &S;
         s.tli = static_cast<uint32_t>(tl);
-        s.R = F.R;
+        s.R = fixedR;
         s.stride = static_cast<uint32_t>(nb * L.tpb);
         s.myBlk = L.dTpb.div(static_cast<uint32_t>(tl));
         s.nLocs = F.nLocs;
@@ -408,7 +435,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         Builtins bi;
         Body::identity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
         Body::run(L, sCode, bi, s, regs);
-        for (uint32_t j = s.nrec; j < F.R; ++j)
+        for (uint32_t j = s.nrec; j < s.R; ++j)
           if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))
             S.r0[j * s.stride + s.tli] = kNoRec;
         tally.add(s);

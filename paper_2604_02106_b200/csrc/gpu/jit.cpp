@@ -81,25 +81,64 @@ void emitIdentity(std::ostringstream &o, const hgrd_gpu_launch &L) {
 
 } // namespace
 
-std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec) {
-  std::vector<char> target(L.n_code, 0);
+// Loop-free code (no backward jump; ctx.cu phaseBounds uses the same rule)
+// executes every access and statement at most once per thread.
+bool hasLoops(const hgrd_gpu_launch &L) {
+  for (uint32_t pc = 0; pc < L.n_code; ++pc)
+    if (L.code[pc].op == HGRD_OP_JMP && L.code[pc].imm <= static_cast<int64_t>(pc))
+      return true;
+  return false;
+}
+
+// A loop-free thread executes each STEP at most once: no per-statement
+// budget checks when the launch's budget covers them all (the host still
+// compares the launch's total steps with the budget).
+bool stepFree(const hgrd_gpu_launch &L) {
+  if (hasLoops(L))
+    return false;
+  int64_t n = 0;
+  for (uint32_t pc = 0; pc < L.n_code; ++pc)
+    n += L.code[pc].op == HGRD_OP_STEP;
+  return n <= L.step_budget;
+}
+
+std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
+                     const std::vector<JitParam> &params) {
+  std::vector<char> target(L.n_code + 1, 0);
+  uint32_t nRec = 0;
   for (uint32_t pc = 0; pc < L.n_code; ++pc) {
     const auto &I = L.code[pc];
-    if (I.op == HGRD_OP_JZ || I.op == HGRD_OP_JMP)
+    if ((I.op == HGRD_OP_JZ || I.op == HGRD_OP_JMP) && I.imm >= 0 &&
+        I.imm <= static_cast<int64_t>(L.n_code))
       target[static_cast<size_t>(I.imm)] = 1;
+    if ((I.op == HGRD_OP_LOAD || I.op == HGRD_OP_STORE || I.op == HGRD_OP_ATOMIC) &&
+        static_cast<size_t>(I.imm) < rec.size() && (rec[static_cast<size_t>(I.imm)] & 1))
+      ++nRec;
   }
-  // site -> "site, param, record, own" literal arguments of the sink's K
-  // accessors (rec[s]: bit 0 record, bit 1 ownership exchange)
+  const bool loops = hasLoops(L);
+  const bool noStepChecks = stepFree(L);
+  // access -> literal arguments of the sink's C accessors: site, param,
+  // record, own (rec[s]: bit 0 record, bit 1 ownership exchange), ... , size,
+  // element base
   auto site = [&](int64_t s) {
     const size_t i = static_cast<size_t>(s);
     const uint8_t f = i < rec.size() ? rec[i] : 3;
     return std::to_string(s) + ", " + std::to_string(i < L.n_sites ? L.sites[i].param : 0) +
            ", " + ((f & 1) ? "true" : "false") + ", " + ((f & 2) ? "true" : "false");
   };
+  auto buf = [&](int64_t s) {
+    const size_t i = static_cast<size_t>(s);
+    const int32_t p = i < L.n_sites ? L.sites[i].param : -1;
+    const JitParam jp = (p >= 0 && static_cast<size_t>(p) < params.size())
+                            ? params[static_cast<size_t>(p)]
+                            : JitParam{0, 0};
+    return ", " + lit(jp.size) + ", " + std::to_string(jp.base) + "ULL";
+  };
   std::ostringstream o;
   o << "#include \"jit_kernels.cuh\"\n"
        "namespace hgrdgpu {\nnamespace dev {\n"
        "struct JitBody {\n";
+  o << "  static constexpr int kFixedR = " << (loops ? 0 : nRec) << ";\n";
   emitIdentity(o, L);
   o << "  template <class Sink>\n"
        "  __device__ static __forceinline__ void run(const LaunchDev &, const hgrd_gpu_insn *,\n"
@@ -116,7 +155,10 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec) 
       o << "return;";
       break;
     case HGRD_OP_STEP:
-      o << "if (!s.step(" << I.imm << ")) return;";
+      if (noStepChecks)
+        o << "s.stepNC();";
+      else
+        o << "if (!s.step(" << I.imm << ")) return;";
       break;
     case HGRD_OP_CONST:
       o << "r" << I.a << " = " << lit(I.imm) << ";";
@@ -131,14 +173,15 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec) 
       o << "r" << I.a << " = applyBin(" << int(I.sub) << ", r" << I.b << ", r" << I.c << ");";
       break;
     case HGRD_OP_LOAD:
-      o << "r" << I.a << " = s.loadK(" << site(I.imm) << ", r" << I.b << ", "
-        << ((I.sub & 1) ? "true" : "false") << ");";
+      o << "r" << I.a << " = s.loadC(" << site(I.imm) << ", r" << I.b << ", "
+        << ((I.sub & 1) ? "true" : "false") << buf(I.imm) << ");";
       break;
     case HGRD_OP_STORE:
-      o << "s.storeK(" << site(I.imm) << ", r" << I.a << ", r" << I.b << ");";
+      o << "s.storeC(" << site(I.imm) << ", r" << I.a << ", r" << I.b << buf(I.imm) << ");";
       break;
     case HGRD_OP_ATOMIC:
-      o << "s.atomicK(" << site(I.imm) << ", r" << I.a << ", r" << I.b << ", r" << I.c << ");";
+      o << "s.atomicC(" << site(I.imm) << ", r" << I.a << ", r" << I.b << ", r" << I.c
+        << buf(I.imm) << ");";
       break;
     case HGRD_OP_SYNCTHREADS:
       o << "s.syncthreads();";
@@ -243,8 +286,8 @@ bool compile(const Cache *c, const std::string &src, Variant v, std::vector<char
 
 } // namespace
 
-const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
-                std::string &err) {
+const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
+                const std::vector<JitParam> &params, Variant v, std::string &err) {
   // cache key: the raw launch inputs of generate() (cheaper than the source)
   std::string key;
   auto put = [&key](const void *p, size_t n) { key.append(static_cast<const char *>(p), n); };
@@ -259,10 +302,13 @@ const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &
     put(L.reg_init, 8 * L.n_regs);
   put(L.sites, sizeof(hgrd_gpu_site) * L.n_sites);
   put(rec.data(), rec.size());
+  put(params.data(), sizeof(JitParam) * params.size());
+  const bool noStepChecks = stepFree(L);
+  put(&noStepChecks, sizeof noStepChecks);
   auto it = c->mods.find(key);
   if (it != c->mods.end())
     return it->second;
-  const std::string src = generate(L, rec);
+  const std::string src = generate(L, rec, params);
   const auto t0 = std::chrono::steady_clock::now();
   auto fail = [&](const std::string &why) -> const void * {
     err = why;
@@ -291,12 +337,12 @@ const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &
   return fn;
 }
 
-size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
-                   std::string &err) {
+size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
+                   const std::vector<JitParam> &params, Variant v, std::string &err) {
   Cache *c = create();
   std::vector<char> cubin;
   std::string lowered;
-  const std::string src = generate(L, rec);
+  const std::string src = generate(L, rec, params);
   if (const char *dump = std::getenv("HGRD_JIT_DUMP")) { // development: keep the source
     if (FILE *f = std::fopen(dump, "w")) {
       std::fputs(src.c_str(), f);

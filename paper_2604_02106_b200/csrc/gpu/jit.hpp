@@ -13,6 +13,13 @@ namespace jit {
 // k_expand_par, k_fused<256,4> / <256,8> / <256,16>
 enum Variant { kExpandPar = 0, kFusedNarrow = 1, kFusedWide = 2, kFusedMid = 3 };
 
+// Per kernel parameter: its buffer's element count (0: none, every access
+// traps) and global element base, folded into the generated accesses.
+struct JitParam {
+  int64_t size;
+  uint64_t base;
+};
+
 struct Cache;
 Cache *create();
 void destroy(Cache *c);
@@ -21,12 +28,13 @@ void destroy(Cache *c);
 // unavailable or the compile fails; callers then use the interpreter.
 // `rec[s]`: bit 0: site s produces race-check records (written buffer);
 // bit 1: its buffer may be reached from two blocks (ownership exchange).
-const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
-                std::string &err);
-std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec);
+const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
+                const std::vector<JitParam> &params, Variant v, std::string &err);
+std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
+                     const std::vector<JitParam> &params);
 // Compile without loading (no GPU needed): cubin size, 0 and err on failure.
-size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec, Variant v,
-                   std::string &err);
+size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
+                   const std::vector<JitParam> &params, Variant v, std::string &err);
 double compileMs(const Cache *c);
 int compiles(const Cache *c);
 

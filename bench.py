@@ -47,6 +47,7 @@ WS = 32
 INST_PER_THREAD = 5
 B_ALG = 32  # algorithmic bytes per instance
 SAMPLE_THREADS = 1 << 16  # CPU reference sample (per host thread, per step)
+CPU_BASELINE_REPS = 24    # cpu_baseline leg of the GPU arm: ~10 s of reference work
 METRIC = "access instances race-checked/sec"
 UNIT = "instances/s"
 WORKLOAD = "stencil1d_2^20threads_block256_ws32_missing+fixed"
@@ -299,10 +300,11 @@ def run_gpu_arm(args):
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, kind, threads, secs, n = reference_rate(threads, 2, SAMPLE_THREADS)
+        reps = CPU_BASELINE_REPS  # ~10 s of host work on the GPU box
+        v, kind, threads, secs, n = reference_rate(threads, reps, SAMPLE_THREADS)
         line["cpu_baseline"] = {
             "value": v, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{threads} host threads x 2 reps x both variants at {SAMPLE_THREADS} "
+            "sample": f"{threads} host threads x {reps} reps x both variants at {SAMPLE_THREADS} "
                       f"threads ({n} instances, {secs:.1f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -235,6 +235,39 @@ int hgrd_gpu_sweep_shard_json(hgrd_gpu_ctx *ctx, const char *source,
 int hgrd_gpu_count_inputs(const char *source, const char *file_name);
 /* Lowering only: bytecode, sites, locs and per-kernel facts of one kernel as
  * JSON (for callers that fix launch parameters themselves). */
+/* ---- sharded single-launch check (one launch over several GPUs) -------
+ * Each rank checks the whole-block range [block_begin, block_end) of the
+ * launch's dense block index:
+ *  1. hgrd_gpu_shard_check: INTRA-BLOCK / INTRA-WARP races of these blocks
+ *     (complete: same-block pairs never leave a shard; per key the minimum
+ *     element and its first pair, merged across ranks by the caller as the
+ *     lexicographic minimum of (handle, index, x, y)), the shard's counters
+ *     and, when a written buffer may be reached from two blocks, the
+ *     shard's INTER summary: two device tables of inter_n u32 entries per
+ *     (element, site) — min and max (block + 1), empty = 0x7F7F7F7F / 0 —
+ *     which the caller MIN / MAX all-reduces across ranks in place;
+ *  2. hgrd_gpu_shard_inter (after the all-reduce): the realised INTER keys'
+ *     first-found elements, and this shard's packed records of them (key
+ *     layout identical on every rank), copied to host;
+ *  3. hgrd_gpu_shard_detect: the INTER-BLOCK races (with witnesses) of the
+ *     records gathered from all ranks.
+ * HGRD_GPU_ENOTSUP means the launch (or a shard: traps, step budget) needs
+ * the ordered path: run hgrd_gpu_check_launch on every rank instead. */
+typedef struct hgrd_gpu_shard {
+  int64_t block_begin, block_end; /* in: dense block range of this rank   */
+  uint32_t *inter_lo, *inter_hi;  /* out: device tables (or NULL)         */
+  uint64_t inter_n;               /* out: entries per table (0: no INTER)  */
+} hgrd_gpu_shard;
+
+int hgrd_gpu_shard_check(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
+                         hgrd_gpu_shard *shard, hgrd_gpu_result *result);
+int hgrd_gpu_shard_inter(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
+                         const hgrd_gpu_shard *shard, uint64_t *keys, uint32_t *vals,
+                         uint64_t cap, uint64_t *n);
+int hgrd_gpu_shard_detect(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
+                          const uint64_t *keys, const uint32_t *vals, uint64_t n,
+                          hgrd_gpu_result *result);
+
 /* Host analysis (no GPU needed): out[s] = 1 when site s's buffer is proven
  * block-private for this launch (affine indices whose per-block element
  * ranges are disjoint), so the fused path skips its ownership exchange.

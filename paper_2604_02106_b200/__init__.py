@@ -74,6 +74,28 @@ class Result(ctypes.Structure):
                 ("mode", c_uint32), ("device_ms", ctypes.c_float)]
 
 
+class Shard(ctypes.Structure):
+    """hgrd_gpu_shard: a whole-block range of one launch (sharded check)."""
+    _fields_ = [("block_begin", c_int64), ("block_end", c_int64),
+                ("inter_lo", ctypes.c_void_p), ("inter_hi", ctypes.c_void_p),
+                ("inter_n", ctypes.c_uint64)]
+
+
+HGRD_GPU_ENOTSUP = -95
+
+
+class NotShardable(RuntimeError):
+    """The launch (or this shard) needs the ordered path: run it unsharded."""
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a context-owned device table."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
 # ----------------------------------------------------------- configuration
 @dataclass
 class ExecConfig:
@@ -149,6 +171,12 @@ def load_library() -> ctypes.CDLL:
                                               ctypes.POINTER(P)]
     lib.hgrd_gpu_count_inputs.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
     lib.hgrd_gpu_block_private.argtypes = [P, ctypes.POINTER(ctypes.c_uint8)]
+    lib.hgrd_gpu_shard_check.argtypes = [P, P, P, P]
+    lib.hgrd_gpu_shard_inter.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(c_uint32), ctypes.c_uint64,
+                                         ctypes.POINTER(ctypes.c_uint64)]
+    lib.hgrd_gpu_shard_detect.argtypes = [P, P, ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.POINTER(c_uint32), ctypes.c_uint64, P]
     I3 = ctypes.c_int64 * 3
     lib.hgrd_gpu_jit_check.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, I3, I3,
                                        ctypes.c_int64, ctypes.POINTER(P)]
@@ -403,6 +431,65 @@ class GpuContext:
             self._err("buffer_read", rc)
         return out
 
+    # -- sharded single-launch check (parallel.check_launch_sharded) --
+    def shard_check(self, spec: LaunchSpec, block_begin: int, block_end: int):
+        """INTRA races + counters of blocks [block_begin, block_end) and the
+        shard's INTER summary tables (device).  Raises NotShardable."""
+        res, races, traps = spec.new_result(0)
+        sh = Shard(block_begin, block_end, None, None, 0)
+        rc = self._lib.hgrd_gpu_shard_check(self._ctx, ctypes.byref(spec.launch),
+                                            ctypes.byref(sh), ctypes.byref(res))
+        if rc == HGRD_GPU_ENOTSUP:
+            raise NotShardable(self._lib.hgrd_gpu_last_error(self._ctx).decode())
+        if rc:
+            self._err("shard_check", rc)
+        return spec.decode(res), sh
+
+    def shard_tables(self, sh: Shard, device: int = 0):
+        """The shard's (lo, hi) INTER tables as int32 torch tensors sharing
+        the context's device memory (for an in-place MIN / MAX all-reduce)."""
+        import torch
+        dev = torch.device("cuda", device)
+        lo = torch.as_tensor(_CudaArray(sh.inter_lo, sh.inter_n), device=dev)
+        hi = torch.as_tensor(_CudaArray(sh.inter_hi, sh.inter_n), device=dev)
+        return lo, hi
+
+    def shard_inter(self, spec: LaunchSpec, sh: Shard):
+        """After the all-reduce: this shard's packed records of the realised
+        INTER keys' first-found elements (numpy uint64 keys, uint32 vals)."""
+        import numpy as np
+        cap = 1 << 16
+        while True:
+            keys = np.zeros(cap, dtype=np.uint64)
+            vals = np.zeros(cap, dtype=np.uint32)
+            n = ctypes.c_uint64()
+            rc = self._lib.hgrd_gpu_shard_inter(
+                self._ctx, ctypes.byref(spec.launch), ctypes.byref(sh),
+                keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                vals.ctypes.data_as(ctypes.POINTER(c_uint32)), cap, ctypes.byref(n))
+            if rc == -7:  # E2BIG
+                cap = max(cap * 2, int(n.value))
+                continue
+            if rc == HGRD_GPU_ENOTSUP:
+                raise NotShardable(self._lib.hgrd_gpu_last_error(self._ctx).decode())
+            if rc:
+                self._err("shard_inter", rc)
+            return keys[: n.value].copy(), vals[: n.value].copy()
+
+    def shard_detect(self, spec: LaunchSpec, keys, vals) -> dict:
+        """INTER-BLOCK races (with witnesses) of records gathered from all shards."""
+        import numpy as np
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        vals = np.ascontiguousarray(vals, dtype=np.uint32)
+        res, races, traps = spec.new_result(0)
+        rc = self._lib.hgrd_gpu_shard_detect(
+            self._ctx, ctypes.byref(spec.launch),
+            keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+            vals.ctypes.data_as(ctypes.POINTER(c_uint32)), len(keys), ctypes.byref(res))
+        if rc:
+            self._err("shard_detect", rc)
+        return spec.decode(res)
+
     def check_launch(self, spec: LaunchSpec, trap_cap: int = 256, raw: bool = False):
         res, races, traps = spec.new_result(trap_cap)
         rc = self._lib.hgrd_gpu_check_launch(self._ctx, ctypes.byref(spec.launch),
@@ -412,6 +499,7 @@ class GpuContext:
         return res if raw else spec.decode(res)
 
 
-__all__ = ["ExecConfig", "SweepCaps", "GpuContext", "LaunchSpec", "count_inputs", "lower",
+__all__ = ["ExecConfig", "SweepCaps", "GpuContext", "LaunchSpec", "Shard", "NotShardable",
+           "count_inputs", "lower",
            "load_library", "LIBRARY_PATH", "RACE_KINDS", "LAUNCH_SEQUENTIAL",
            "LAUNCH_PAIRWISE", "LAUNCH_NO_WITNESS", "LAUNCH_GENERAL"]

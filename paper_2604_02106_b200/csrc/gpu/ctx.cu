@@ -88,6 +88,7 @@ struct hgrd_gpu_ctx {
   DevVec<uint64_t> opStart;
   DevVec<hgrd_gpu_trap> traps;
   DevVec<uint32_t> owner;              // fused path: per-element ownership
+  DevVec<uint32_t> shardLo, shardHi;   // sharded launches: INTER summary (min / max block)
   uint32_t epoch = 0;
   DevVec<unsigned long long> keyElem;  // fused path: per key minimum element
   DevVec<Candidate> cand;
@@ -661,7 +662,8 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *ji
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, NT, smem));
     perSM = std::max(perSM, 1);
   }
-  const int64_t grid = std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1));
+  const int64_t grid = std::max<int64_t>(
+      1, std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1)));
   void *args[] = {const_cast<FusedArgs *>(&F)};
   StageTimer t(c, jitKernel ? "k_fused[jit]" : "k_fused");
   CK(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(NT), args, smem,
@@ -672,9 +674,14 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *ji
 // Returns 1 when the launch was fully checked, 0 to fall back to the
 // general pipeline, < 0 on error.  D.kl must hold the general key layout
 // (used by pass 2).
+// Shard mode (shard = true): only blocks [b0, b1), no ownership exchanges
+// and no pass 2 — the caller combines the shards' INTER summaries
+// (hgrd_gpu_shard_*).
 int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobOffsets &o,
              const Plan &P, hgrd_gpu_result *R, uint32_t recInsns, bool loops,
-             JitGetter &jk) {
+             JitGetter &jk, int64_t b0 = 0, int64_t b1 = -1, bool shard = false) {
+  if (b1 < 0)
+    b1 = D.nBlocks;
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
   static const int64_t kIterThreads = [] { // development knob: MiniCU threads per iteration
@@ -714,8 +721,10 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.nKeys = nKeys;
   F.bpi = static_cast<int>(bpi);
   F.R = (loops || recInsns == 0) ? 0u : recInsns; // straight-line code: static record slots
-  F.nIters = (D.nBlocks + bpi - 1) / bpi;
-  F.owner = c->owner.p;
+  F.blockBase = b0;
+  F.blockEnd = b1;
+  F.nIters = (b1 - b0 + bpi - 1) / bpi;
+  F.owner = shard ? nullptr : c->owner.p;
   F.epoch = c->epoch;
   F.keyElem = c->curKeyElem;
   F.cand = c->cand.p;
@@ -745,7 +754,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   R->instances = h.instances;
   R->records = h.records;
   R->mode = L.flags & ~HGRD_LAUNCH_SEQUENTIAL;
-  if (!(h.flags & kFlagShared))
+  if (shard || !(h.flags & kFlagShared))
     return fetchRaces(c, R) < 0 ? -1 : 1;
 
   // pass 2: INTER-BLOCK over the elements two or more blocks touched
@@ -928,30 +937,15 @@ int snapshot(hgrd_gpu_ctx *c, const Plan &P, bool restore) {
   return 0;
 }
 
-int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
-  R->n_races = 0;
-  R->n_traps = 0;
-  R->n_traps_total = 0;
-  R->steps = 0;
-  R->instances = 0;
-  R->records = 0;
-  R->aborted = 0;
-  R->abort_stmt = -1;
-  R->mode = 0;
-  R->device_ms = 0;
-  c->stages.clear();
-  c->evUsed = 0;
-  c->racesOnHost = false;
-  CK(cudaEventRecord(c->e0, c->st));
-
-  Plan P;
+// Per-launch setup shared by the full and the sharded checks: plan (buffer
+// bases, site flags, conflict masks), one blob upload, device descriptor.
+int prepareLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P, BlobOffsets &o,
+                  LaunchDev &D) {
   planLaunch(c, L, P);
-  BlobOffsets o{};
   int rc = uploadBlob(c, L, P, o);
   if (rc < 0)
     return rc;
-
-  LaunchDev D{};
+  D = LaunchDev{};
   D.code = reinterpret_cast<const hgrd_gpu_insn *>(c->blob.p + o.code);
   D.sites = reinterpret_cast<const SiteDev *>(c->blob.p + o.sites);
   D.params = reinterpret_cast<const ParamDev *>(c->blob.p + o.params);
@@ -983,6 +977,34 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     D.dGxGy = FastDiv::make(static_cast<uint32_t>(L.grid[0] * L.grid[1]));
     D.dWs = FastDiv::make(static_cast<uint32_t>(std::min<int64_t>(L.warp_size, 0xffffffffLL)));
   }
+
+  D.threadBase = 0;
+  D.threadEnd = D.nThreads;
+  return 0;
+}
+
+int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
+  R->n_races = 0;
+  R->n_traps = 0;
+  R->n_traps_total = 0;
+  R->steps = 0;
+  R->instances = 0;
+  R->records = 0;
+  R->aborted = 0;
+  R->abort_stmt = -1;
+  R->mode = 0;
+  R->device_ms = 0;
+  c->stages.clear();
+  c->evUsed = 0;
+  c->racesOnHost = false;
+  CK(cudaEventRecord(c->e0, c->st));
+
+  Plan P;
+  BlobOffsets o{};
+  LaunchDev D{};
+  int rc = prepareLaunch(c, L, P, o, D);
+  if (rc < 0)
+    return rc;
 
   int bP, bQ;
   bool bounded, loops;
@@ -1209,6 +1231,283 @@ finish:
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Sharded single-launch check: each rank checks a whole-
+// block range; INTRA kinds are rank-local, INTER-BLOCK needs the ranks'
+// per-(element, site) block summaries combined (MIN/MAX all-reduce by the
+// caller), then the witness records of the realised INTER keys' elements.
+
+struct ShardSetup {
+  Plan P;
+  BlobOffsets o{};
+  LaunchDev D{};
+  uint32_t recInsns = 0;
+  bool loops = false;
+};
+
+// Plan + key layout; HGRD_GPU_ENOTSUP (c->err says why) when the launch
+// needs a path that does not shard (replicas then).
+int shardPrepare(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, int64_t b0, int64_t b1,
+                 ShardSetup &S) {
+  int rc = prepareLaunch(c, L, S.P, S.o, S.D);
+  if (rc < 0)
+    return rc;
+  LaunchDev &D = S.D;
+  if (b0 < 0 || b1 < b0 || b1 > D.nBlocks) {
+    c->err = "bad shard block range";
+    return HGRD_GPU_EINVAL;
+  }
+  int bP, bQ;
+  bool bounded;
+  uint32_t accessInsns;
+  phaseBounds(L, bP, bQ, bounded, accessInsns, S.loops);
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    const auto &I = L.code[pc];
+    if ((I.op == HGRD_OP_LOAD || I.op == HGRD_OP_STORE || I.op == HGRD_OP_ATOMIC) &&
+        S.P.sites[static_cast<size_t>(I.imm)].record)
+      ++S.recInsns;
+  }
+  const size_t smem = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * S.P.sites.size() +
+                      sizeof(ParamDev) * S.P.params.size();
+  const char *why = nullptr;
+  if (L.flags & (HGRD_LAUNCH_SEQUENTIAL | HGRD_LAUNCH_PAIRWISE | HGRD_LAUNCH_GENERAL))
+    why = "sequential / lock-idiom launches are replicas only";
+  else if (!S.P.summaryOk || L.n_locs > 32 || L.n_regs > kMaxRegs || smem > 200 * 1024)
+    why = "launch outside the fused envelope";
+  else if (S.P.totalW >= 0xFFFFFFFFull || S.o.nW > kMaxWritten || D.nBlocks >= (1 << 20) - 2)
+    why = "written buffers / blocks outside the fused envelope";
+  else if (!bounded)
+    why = "barriers inside loops (phase bits not static)";
+  const int bE = bitsFor(S.P.totalW + 1);
+  const int bB = bitsFor(static_cast<uint64_t>(D.nBlocks));
+  const int bW = bitsFor(static_cast<uint64_t>((D.tpb + D.ws - 1) / D.ws));
+  const int bL = bitsFor(static_cast<uint64_t>(std::min<int64_t>(D.ws, D.tpb)));
+  if (!why && !makeLayout(D.kl, bE, bB, bP, bW, bQ, bL))
+    why = "packed record key wider than 64 bits";
+  if (why) {
+    c->err = std::string("not shardable: ") + why;
+    return HGRD_GPU_ENOTSUP;
+  }
+  return 0;
+}
+
+JitGetter shardJit(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const ShardSetup &S) {
+  const bool useJit =
+      c->jitMode == 2 || (c->jitMode == 1 && S.D.nThreads >= (int64_t(1) << 14));
+  JitGetter jk{c, &L, useJit, {}, {}};
+  for (uint32_t p = 0; p < L.n_params; ++p) {
+    const ParamDev &d = S.P.params[p];
+    jk.params.push_back(hgrdgpu::jit::JitParam{d.handle >= 0 ? d.size : 0, d.elemBase});
+  }
+  for (const auto &s : S.P.sites)
+    jk.rec.push_back(static_cast<uint8_t>((s.record ? 1 : 0) | (s.own ? 2 : 0)));
+  return jk;
+}
+
+void resetResult(hgrd_gpu_result *R) {
+  R->n_races = 0;
+  R->n_traps = 0;
+  R->n_traps_total = 0;
+  R->steps = 0;
+  R->instances = 0;
+  R->records = 0;
+  R->aborted = 0;
+  R->abort_stmt = -1;
+  R->mode = 0;
+  R->device_ms = 0;
+}
+
+int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
+               hgrd_gpu_result *R) {
+  resetResult(R);
+  Sh->inter_lo = Sh->inter_hi = nullptr;
+  Sh->inter_n = 0;
+  c->stages.clear();
+  c->evUsed = 0;
+  c->racesOnHost = false;
+  CK(cudaEventRecord(c->e0, c->st));
+  ShardSetup S;
+  int rc = shardPrepare(c, L, Sh->block_begin, Sh->block_end, S);
+  if (rc < 0)
+    return rc;
+  JitGetter jk = shardJit(c, L, S);
+  rc = runFused(c, L, S.D, S.o, S.P, R, S.recInsns, S.loops, jk, Sh->block_begin,
+                Sh->block_end, true);
+  if (rc < 0)
+    return rc;
+  if (rc == 0) { // traps, step budget, overflow: the canonical order is needed
+    c->err = "shard needs the ordered path (traps / step budget / capacity)";
+    return HGRD_GPU_ENOTSUP;
+  }
+  bool anyOwn = false;
+  for (const auto &s : S.P.sites)
+    anyOwn |= s.record && s.own;
+  if (anyOwn) { // INTER summary of this shard's blocks
+    const uint64_t n = S.P.totalW * static_cast<uint64_t>(L.n_sites);
+    NEED(c->shardLo, n);
+    NEED(c->shardHi, n);
+    CK(cudaMemsetAsync(c->shardLo.p, 0x7f, n * sizeof(uint32_t), c->st)); // kShardEmpty
+    CK(cudaMemsetAsync(c->shardHi.p, 0, n * sizeof(uint32_t), c->st));
+    NEED(c->ctr2, 1);
+    CK(cudaMemsetAsync(c->ctr2.p, 0, sizeof(Counters), c->st));
+    LaunchDev Ds = S.D;
+    Ds.ctr = c->ctr2.p;
+    Ds.interLo = c->shardLo.p;
+    Ds.interHi = c->shardHi.p;
+    Ds.nSitesTab = static_cast<int>(L.n_sites);
+    Ds.keys = nullptr;
+    Ds.vals = nullptr;
+    Ds.capacity = 0;
+    Ds.chunk = 64;
+    Ds.threadBase = Sh->block_begin * S.D.tpb;
+    Ds.threadEnd = Sh->block_end * S.D.tpb;
+    const size_t sm = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * S.P.sites.size() +
+                      sizeof(ParamDev) * S.P.params.size();
+    const uint64_t nt = static_cast<uint64_t>(std::max<int64_t>(Ds.threadEnd - Ds.threadBase, 1));
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>(((nt + 31) / 32 + 7) / 8, uint64_t(c->nSM) * 8));
+    const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
+    rc = launchExpandPar(c, Ds, grid, sm, jx, jx ? "k_expand_par_shard[jit]" : "k_expand_par_shard");
+    if (rc < 0)
+      return rc;
+    CK(cudaStreamSynchronize(c->st));
+    Sh->inter_lo = c->shardLo.p;
+    Sh->inter_hi = c->shardHi.p;
+    Sh->inter_n = n;
+  }
+  CK(cudaEventRecord(c->e1, c->st));
+  CK(cudaEventSynchronize(c->e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  R->device_ms = ms;
+  return 0;
+}
+
+int shardInter(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const hgrd_gpu_shard *Sh,
+               uint64_t *keys, uint32_t *vals, uint64_t cap, uint64_t *nOut) {
+  *nOut = 0;
+  ShardSetup S;
+  int rc = shardPrepare(c, L, Sh->block_begin, Sh->block_end, S);
+  if (rc < 0)
+    return rc;
+  const uint64_t nTab = S.P.totalW * static_cast<uint64_t>(L.n_sites);
+  if (Sh->inter_n == 0)
+    return 0; // no buffer reachable from two blocks
+  if (Sh->inter_n != nTab || c->shardLo.cap < nTab) {
+    c->err = "shard INTER tables do not match the launch";
+    return HGRD_GPU_EINVAL;
+  }
+  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+  const int nKeys = 3 * nLocs * nLocs;
+  NEED(c->interKeyElem, static_cast<size_t>(nKeys));
+  CK(cudaMemsetAsync(c->interKeyElem.p, 0xff, 8 * static_cast<size_t>(nKeys), c->st));
+  k_inter_scan_minmax<<<static_cast<unsigned>((S.P.totalW + 255) / 256), 256, 0, c->st>>>(
+      c->shardLo.p, c->shardHi.p, S.P.totalW, static_cast<int>(L.n_sites), S.D.sites,
+      S.D.confInter, nLocs, c->interKeyElem.p);
+  CK(cudaGetLastError());
+  ++c->kernelLaunches;
+  std::vector<unsigned long long> ke(static_cast<size_t>(nKeys));
+  CK(cudaMemcpyAsync(ke.data(), c->interKeyElem.p, 8 * static_cast<size_t>(nKeys),
+                     cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += 8 * static_cast<size_t>(nKeys);
+  CK(cudaStreamSynchronize(c->st));
+  std::vector<uint64_t> targets;
+  for (int K = 0; K < nKeys; K += 3)
+    if (ke[static_cast<size_t>(K)] != ~0ull)
+      targets.push_back(ke[static_cast<size_t>(K)]);
+  std::sort(targets.begin(), targets.end());
+  targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
+  if (targets.empty())
+    return 0;
+  NEED(c->targets, targets.size());
+  CK(cudaMemcpy(c->targets.p, targets.data(), 8 * targets.size(), cudaMemcpyHostToDevice));
+  c->h2dBytes += 8 * targets.size();
+  JitGetter jk = shardJit(c, L, S);
+  LaunchDev D2 = S.D;
+  NEED(c->ctr2, 1);
+  D2.ctr = c->ctr2.p;
+  D2.targets = c->targets.p;
+  D2.nTargets = static_cast<int>(targets.size());
+  D2.threadBase = Sh->block_begin * S.D.tpb;
+  D2.threadEnd = Sh->block_end * S.D.tpb;
+  const uint64_t nt = static_cast<uint64_t>(std::max<int64_t>(D2.threadEnd - D2.threadBase, 1));
+  const uint64_t blocks = std::min<uint64_t>(((nt + 31) / 32 + 7) / 8, uint64_t(c->nSM) * 8);
+  const uint64_t warps = blocks * 8, chunk = 64;
+  const size_t sm = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * S.P.sites.size() +
+                    sizeof(ParamDev) * S.P.params.size();
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    const uint64_t dcap = std::max<uint64_t>(warps * chunk * 2 + (uint64_t(1) << 16), c->capHint);
+    NEED(c->keys, dcap);
+    NEED(c->vals, dcap);
+    D2.keys = c->keys.p;
+    D2.vals = c->vals.p;
+    D2.capacity = dcap;
+    D2.chunk = static_cast<uint32_t>(chunk);
+    CK(cudaMemsetAsync(c->ctr2.p, 0, sizeof(Counters), c->st));
+    const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
+    rc = launchExpandPar(c, D2, static_cast<unsigned>(blocks), sm, jx,
+                         jx ? "k_expand_par_shard_targets[jit]" : "k_expand_par_shard_targets");
+    if (rc < 0)
+      return rc;
+    rc = readCountersFrom(c, c->ctr2.p);
+    if (rc < 0)
+      return rc;
+    const Counters h = *c->hCtr;
+    if (h.flags & kFlagCapacity) {
+      c->capHint = std::max<uint64_t>(c->capHint, h.cursor + warps * chunk + 4096) * 2;
+      continue;
+    }
+    if (h.flags & (kFlagPhase | kFlagSeqSite)) {
+      c->err = "shard records outside the static key layout";
+      return HGRD_GPU_ENOTSUP;
+    }
+    const uint64_t n = std::min<uint64_t>(h.cursor, dcap);
+    std::vector<uint64_t> hk(n);
+    std::vector<uint32_t> hv(n);
+    if (n) {
+      CK(cudaMemcpyAsync(hk.data(), c->keys.p, 8 * n, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(hv.data(), c->vals.p, 4 * n, cudaMemcpyDeviceToHost, c->st));
+      c->d2hBytes += 12 * n;
+      CK(cudaStreamSynchronize(c->st));
+    }
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      if (hk[i] == S.D.kl.sentinel)
+        continue; // chunk padding
+      if (m >= cap) {
+        *nOut = m + 1;
+        return HGRD_GPU_E2BIG;
+      }
+      keys[m] = hk[i];
+      vals[m] = hv[i];
+      ++m;
+    }
+    *nOut = m;
+    return 0;
+  }
+  c->err = "shard target records exceed capacity";
+  return HGRD_GPU_ENOTSUP;
+}
+
+int shardDetect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const uint64_t *keys,
+                const uint32_t *vals, uint64_t n, hgrd_gpu_result *R) {
+  resetResult(R);
+  c->racesOnHost = false;
+  ShardSetup S;
+  int rc = shardPrepare(c, L, 0, 0, S);
+  if (rc < 0)
+    return rc;
+  const uint64_t cap = std::max<uint64_t>(n, 1);
+  NEED(c->keys, cap);
+  NEED(c->vals, cap);
+  if (n) {
+    CK(cudaMemcpyAsync(c->keys.p, keys, 8 * n, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->vals.p, vals, 4 * n, cudaMemcpyHostToDevice, c->st));
+    c->h2dBytes += 12 * n;
+  }
+  return detect(c, L, S.D, S.o, n, false, false, R, /*kindMask=*/1);
+}
 } // namespace
 
 extern "C" {
@@ -1252,7 +1551,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   f(c->order), f(c->orderAlt), f(c->cubTemp), f(c->blob), f(c->snapshot), f(c->keySeg);
   f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
   f(c->opSeq), f(c->opStart), f(c->traps), f(c->owner), f(c->keyElem), f(c->cand), f(c->ctr2);
-  f(c->interTab), f(c->interKeyElem), f(c->targets);
+  f(c->interTab), f(c->interKeyElem), f(c->targets), f(c->shardLo), f(c->shardHi);
   for (char *ch : c->chunks)
     cudaFree(ch);
   for (auto &b : c->bigUsed)
@@ -1420,6 +1719,47 @@ int hgrd_gpu_check_launch(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
   }
   CK(cudaSetDevice(c->device));
   return checkLaunch(c, *launch, result);
+}
+
+int hgrd_gpu_shard_check(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, hgrd_gpu_shard *shard,
+                         hgrd_gpu_result *result) {
+  if (!c || !launch || !shard || !result || (!result->races && result->race_cap))
+    return HGRD_GPU_EINVAL;
+  std::string why;
+  if (!validLaunch(*launch, why)) {
+    c->err = why;
+    return HGRD_GPU_EINVAL;
+  }
+  CK(cudaSetDevice(c->device));
+  return shardCheck(c, *launch, shard, result);
+}
+
+int hgrd_gpu_shard_inter(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
+                         const hgrd_gpu_shard *shard, uint64_t *keys, uint32_t *vals,
+                         uint64_t cap, uint64_t *n) {
+  if (!c || !launch || !shard || !n || (cap && (!keys || !vals)))
+    return HGRD_GPU_EINVAL;
+  std::string why;
+  if (!validLaunch(*launch, why)) {
+    c->err = why;
+    return HGRD_GPU_EINVAL;
+  }
+  CK(cudaSetDevice(c->device));
+  return shardInter(c, *launch, shard, keys, vals, cap, n);
+}
+
+int hgrd_gpu_shard_detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, const uint64_t *keys,
+                          const uint32_t *vals, uint64_t n, hgrd_gpu_result *result) {
+  if (!c || !launch || !result || (n && (!keys || !vals)) ||
+      (!result->races && result->race_cap))
+    return HGRD_GPU_EINVAL;
+  std::string why;
+  if (!validLaunch(*launch, why)) {
+    c->err = why;
+    return HGRD_GPU_EINVAL;
+  }
+  CK(cudaSetDevice(c->device));
+  return shardDetect(c, *launch, keys, vals, n, result);
 }
 
 } // extern "C"

@@ -144,6 +144,8 @@ struct LaunchDev {
   uint32_t ownerMultiTag;
   uint32_t *interTab;        // INTER summary mode: (element, site) block sets
   int nSitesTab;
+  uint32_t *interLo, *interHi; // sharded INTER summary: (element, site) min / max block + 1
+  int64_t threadBase, threadEnd; // k_expand_par: dense thread range (a shard of the launch)
   const uint64_t *targets;   // witness mode: only these elements
   int nTargets;
   // 32-bit thread identity (nThreads < 2^32): tpb, bx, bx*by, gx, gx*gy, ws

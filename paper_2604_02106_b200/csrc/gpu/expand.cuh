@@ -95,14 +95,70 @@ __global__ void k_inter_scan(const uint32_t *owner, uint32_t multiTag, uint64_t 
   }
 }
 
+// Empty lo entry of the sharded INTER summary: positive as int32 too, so a
+// signed or unsigned MIN all-reduce treats it alike (byte pattern 0x7F).
+constexpr uint32_t kShardEmpty = 0x7F7F7F7Fu;
+
+// Sharded INTER summary after the cross-shard MIN/MAX reduction: per
+// element, site pairs (a, b) with a static INTER conflict race across
+// blocks iff some block of a's set differs from some block of b's set
+// (a == b: two distinct blocks).  lo = kShardEmpty marks an empty set.  Per
+// key the minimum element (the reference's first-found element, :745).
+__global__ void k_inter_scan_minmax(const uint32_t *lo, const uint32_t *hi, uint64_t nElems,
+                                    int nSites, const SiteDev *sites, const uint64_t *confInter,
+                                    int nLocs, unsigned long long *keyElem) {
+  const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nElems)
+    return;
+  const uint32_t *l = lo + e * static_cast<uint64_t>(nSites);
+  const uint32_t *h = hi + e * static_cast<uint64_t>(nSites);
+  for (int a = 0; a < nSites; ++a) {
+    const uint32_t la = l[a];
+    if (la == kShardEmpty)
+      continue;
+    const uint32_t ha = h[a];
+    for (int b = a; b < nSites; ++b) {
+      if (!((confInter[a] >> b) & 1ull))
+        continue;
+      const uint32_t lb = l[b];
+      if (lb == kShardEmpty)
+        continue;
+      const uint32_t hb = h[b];
+      const bool realised = a == b ? la != ha : !(la == ha && lb == hb && la == lb);
+      if (!realised)
+        continue;
+      int ka = sites[a].loc, kb = sites[b].loc;
+      if (kb < ka) {
+        const int t = ka;
+        ka = kb;
+        kb = t;
+      }
+      const int K = (ka * nLocs + kb) * 3; // kind 0: INTER-BLOCK
+      if (keyElem[K] > e)
+        atomicMin(&keyElem[K], static_cast<unsigned long long>(e));
+    }
+  }
+}
+
 // PARALLEL sink of k_expand_par: packed records into the lane buffer.
 struct ParSink : ParState {
   LaneRecords *out;
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
-    recordE(site, P->elemBase + static_cast<uint64_t>(idx));
+    recordE(site, P->elemBase + static_cast<uint64_t>(idx), sites[site].own != 0);
   }
-  __device__ __forceinline__ void recordE(int site, uint64_t e) {
+  __device__ __forceinline__ void recordE(int site, uint64_t e, bool own) {
+    if (L->interLo) { // sharded INTER summary: min / max block per (element, site)
+      if (!own)
+        return; // block-private buffer: no INTER pair possible
+      const uint64_t i = e * static_cast<uint64_t>(L->nSitesTab) + site;
+      const uint32_t b = static_cast<uint32_t>(block) + 1;
+      if (L->interLo[i] > b)
+        atomicMin(&L->interLo[i], b);
+      if (L->interHi[i] < b)
+        atomicMax(&L->interHi[i], b);
+      return;
+    }
     if (L->ownerFilter && L->ownerFilter[e] != L->ownerMultiTag)
       return; // fused pass 2: only elements shared by blocks
     if (L->interTab) { // INTER summary: EMPTY -> one block -> MULTI, no record
@@ -144,7 +200,7 @@ struct ParSink : ParState {
   }
   // C variants (JIT bodies): the site's parameter, flags, buffer size and
   // element base as constants (size 0: unallocated parameter, always traps)
-  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool, int64_t idx,
+  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool own, int64_t idx,
                                            bool need, int64_t size, uint64_t base) {
     if (static_cast<uint64_t>(idx) >= static_cast<uint64_t>(size)) {
       ++traps;
@@ -152,7 +208,7 @@ struct ParSink : ParState {
     }
     ++inst;
     if (rec)
-      recordE(site, base + static_cast<uint64_t>(idx));
+      recordE(site, base + static_cast<uint64_t>(idx), own);
     ++seq;
     return need ? __ldg(params[param].ptr + idx) : 0;
   }
@@ -219,10 +275,10 @@ template <class Body> __global__ void __launch_bounds__(256) k_expand_par(Launch
   LaneTally tally;
   LaneRecords out;
   int64_t regs[kMaxRegs];
-  for (int64_t batch = warpId; batch * 32 < L.nThreads; batch += nWarps) {
-    const int64_t t = batch * 32 + lane;
+  for (int64_t batch = warpId; L.threadBase + batch * 32 < L.threadEnd; batch += nWarps) {
+    const int64_t t = L.threadBase + batch * 32 + lane;
     out.n = 0;
-    if (t < L.nThreads) {
+    if (t < L.threadEnd) {
       ParSink s;
       s.L = &L;
       s.sites = sSites;

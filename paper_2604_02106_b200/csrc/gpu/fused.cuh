@@ -51,6 +51,7 @@ struct FusedArgs {
   LaunchDev L;
   int nLocs, nKeys;
   int bpi;              // whole MiniCU blocks per iteration
+  int64_t blockBase, blockEnd; // dense MiniCU block range of this launch (or shard)
   uint32_t R;           // records per MiniCU thread when static (0: allocate)
   int64_t nIters;
   uint32_t *owner; // per element ownership word (see FusedSink)
@@ -399,8 +400,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   int64_t regs[kMaxRegs];
 
   for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x) {
-    const int64_t firstBlock = it * F.bpi;
-    const int64_t nb = min(static_cast<int64_t>(F.bpi), L.nBlocks - firstBlock);
+    const int64_t firstBlock = F.blockBase + it * F.bpi;
+    const int64_t nb = min(static_cast<int64_t>(F.bpi), F.blockEnd - firstBlock);
     __syncthreads();
     if (tid == 0) {
       S.count = fixedR ? static_cast<unsigned>(nb * L.tpb) * fixedR : 0;

@@ -84,3 +84,45 @@ def test_gpu_sweep_shards(gpu):
             shards = [gpu.sweep_shard(e["source"], e["caps"], e["file"], r, world)
                       for r in range(world)]
             assert merge_shards(shards)["races"] == e["sweep_manifest"]["races"], e["name"]
+
+
+def _comm_worker(rank, world, port, out):
+    """TorchComm over gloo: the sharded launch's collectives (MIN / MAX of the
+    INTER summary tables, gather of the per-rank INTRA races and records)."""
+    import numpy as np
+    import torch
+    from paper_2604_02106_b200.parallel import TorchComm, block_ranges
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        assert (comm.rank, comm.world, comm.nccl) == (rank, world, False)
+        empty = 0x7F7F7F7F  # kShardEmpty: positive as int32
+        # element e touched by block 2e+rank on rank `rank` when e % world == rank,
+        # element 0 by every rank (-> MULTI after the reduction)
+        lo = torch.full((8,), empty, dtype=torch.int32)
+        hi = torch.zeros(8, dtype=torch.int32)
+        for e in range(8):
+            if e % world == rank or e == 0:
+                lo[e] = hi[e] = 2 * e + rank + 1
+        comm.allreduce_minmax(lo, hi)
+        got = comm.allgather({"rank": rank, "keys": np.arange(rank + 1, dtype=np.uint64)})
+        res = {"lo": lo.tolist(), "hi": hi.tolist(), "ranks": [g["rank"] for g in got],
+               "nkeys": [len(g["keys"]) for g in got], "ranges": block_ranges(9, world)}
+        open(f"{out}.{rank}", "w").write(repr(res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_shard_collectives(tmp_path):
+    world = 2
+    out = str(tmp_path / "comm")
+    mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    res = [eval(open(f"{out}.{r}").read()) for r in range(world)]
+    assert res[0] == res[1]
+    lo, hi = res[0]["lo"], res[0]["hi"]
+    assert (lo[0], hi[0]) == (1, 2)  # element 0: blocks of both ranks -> lo != hi (MULTI)
+    for e in range(1, 8):
+        assert lo[e] == hi[e] == 2 * e + (e % world) + 1  # one block: not MULTI
+    assert res[0]["ranks"] == [0, 1] and res[0]["nkeys"] == [1, 2]
+    assert res[0]["ranges"] == [(0, 5), (5, 9)]

@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       S.maxBp = 0;
       S.maxWp = 0;
       S.hot = 0;
+      S.nReal = 0; // (every thread read it after the previous iteration's barrier)
     }
     for (int i = tid; i < Smem::kTable; i += kFusedThreads)
       S.u.ch.head[i] = Smem::kEnd;
@@ -686,8 +687,6 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
           myFlags |= kFlagFusedOverflow;
       }
     }
-    if (tid == 0)
-      S.nReal = 0;
   }
   // counters
   __syncthreads();

@@ -41,8 +41,14 @@ struct Tok {
 // Whole-input tokenization.  A character outside the alphabet ends the
 // token stream exactly like end of input (the reference lexer returns its
 // End token for it, parser.cpp:225-228).
+// ASCII classes (the "C" locale's, without the libc calls)
+inline bool isSpace(char c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
+inline bool isAlpha(char c) { return (c >= 'a' && c <= 'z') || (c >= 'A' && c <= 'Z'); }
+inline bool isDigit(char c) { return c >= '0' && c <= '9'; }
+
 std::vector<Tok> tokenize(const std::string &src) {
   std::vector<Tok> out;
+  out.reserve(src.size() / 3 + 8);
   size_t i = 0;
   int line = 1, col = 1;
   auto bump = [&] {
@@ -63,7 +69,7 @@ std::vector<Tok> tokenize(const std::string &src) {
       if (i >= src.size())
         break;
       char c = src[i];
-      if (std::isspace(static_cast<unsigned char>(c))) {
+      if (isSpace(c)) {
         bump();
       } else if (c == '/' && at(i + 1) == '/') {
         while (i < src.size() && src[i] != '\n')
@@ -82,28 +88,28 @@ std::vector<Tok> tokenize(const std::string &src) {
     Tok tk;
     tk.loc = Loc{line, col};
     if (i >= src.size()) {
-      out.push_back(tk);
+      out.push_back(std::move(tk));
       return out;
     }
     char c = src[i];
-    if (std::isalpha(static_cast<unsigned char>(c)) || c == '_') {
+    if (isAlpha(c) || c == '_') {
       size_t b = i;
       while (i < src.size() &&
-             (std::isalnum(static_cast<unsigned char>(src[i])) || src[i] == '_'))
+             (isAlpha(src[i]) || isDigit(src[i]) || src[i] == '_'))
         bump();
       tk.t = T::Ident;
       tk.s = src.substr(b, i - b);
-      out.push_back(tk);
+      out.push_back(std::move(tk));
       continue;
     }
-    if (std::isdigit(static_cast<unsigned char>(c))) {
+    if (isDigit(c)) {
       size_t b = i;
-      while (i < src.size() && std::isdigit(static_cast<unsigned char>(src[i])))
+      while (i < src.size() && isDigit(src[i]))
         bump();
       tk.t = T::Num;
       tk.s = src.substr(b, i - b);
       tk.n = std::stoll(tk.s);
-      out.push_back(tk);
+      out.push_back(std::move(tk));
       continue;
     }
     struct Multi {
@@ -117,6 +123,8 @@ std::vector<Tok> tokenize(const std::string &src) {
                                    {"++", T::Inc}};
     bool matched = false;
     for (const auto &m : multis) {
+      if (m.text[0] != c)
+        continue; // cheap first-character filter
       size_t len = std::char_traits<char>::length(m.text);
       if (src.compare(i, len, m.text) == 0) {
         for (size_t k = 0; k < len; ++k)
@@ -127,7 +135,7 @@ std::vector<Tok> tokenize(const std::string &src) {
       }
     }
     if (matched) {
-      out.push_back(tk);
+      out.push_back(std::move(tk));
       continue;
     }
     static const std::string singles = "(){}[],;&=+-*/%<>.";
@@ -138,12 +146,12 @@ std::vector<Tok> tokenize(const std::string &src) {
                                 T::Gt,    T::Dot};
     size_t p = singles.find(c);
     if (p == std::string::npos) {
-      out.push_back(tk); // End
+      out.push_back(std::move(tk)); // End
       return out;
     }
     bump();
     tk.t = singleT[p];
-    out.push_back(tk);
+    out.push_back(std::move(tk));
   }
 }
 
@@ -185,8 +193,8 @@ private:
   const Tok &cur() const { return toks_[pos_]; }
   bool is(T t) const { return cur().t == t; }
   bool isWord(const char *w) const { return cur().t == T::Ident && cur().s == w; }
-  Tok take() {
-    Tok t = toks_[pos_];
+  const Tok &take() {
+    const Tok &t = toks_[pos_];
     if (pos_ + 1 < toks_.size())
       ++pos_;
     return t;
@@ -195,7 +203,7 @@ private:
     throw SyntaxFail{l, m};
   }
   [[noreturn]] void fail(const std::string &m) { failAt(cur().loc, m); }
-  Tok need(T t, const char *what) {
+  const Tok &need(T t, const char *what) {
     if (!is(t))
       fail(std::string("expected ") + what);
     return take();

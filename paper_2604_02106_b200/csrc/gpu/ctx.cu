@@ -89,6 +89,7 @@ struct hgrd_gpu_ctx {
   DevVec<hgrd_gpu_trap> traps;
   DevVec<uint32_t> owner;              // fused path: per-element ownership
   DevVec<uint32_t> shardLo, shardHi;   // sharded launches: INTER summary (min / max block)
+  DevVec<uint32_t> hot;                // INTER detection: [0] count, then hot element starts
   uint32_t epoch = 0;
   DevVec<unsigned long long> keyElem;  // fused path: per key minimum element
   DevVec<Candidate> cand;
@@ -503,11 +504,25 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       NEED(c->keySeg, static_cast<size_t>(nKeys));
       CK(cudaMemsetAsync(c->keySeg.p, 0xff, sizeof(uint32_t) * nKeys, c->st));
       const unsigned g = static_cast<unsigned>((n + 255) / 256);
+      if (kindMask == 1) { // INTER only: hot elements go to a warp each
+        const uint32_t hotCap = 1u << 16;
+        NEED(c->hot, hotCap + 1);
+        CK(cudaMemsetAsync(c->hot.p, 0, sizeof(uint32_t), c->st));
+        A.hotCount = c->hot.p;
+        A.hotList = c->hot.p + 1;
+        A.hotCap = hotCap;
+      }
       {
         StageTimer t(c, "k_detect_summary");
         k_detect_summary<<<g, 256, 0, c->st>>>(A, c->keySeg.p);
       }
       CK(cudaGetLastError());
+      if (A.hotList) {
+        StageTimer t(c, "k_detect_hot");
+        k_detect_hot<<<c->nSM * 2, 256, 0, c->st>>>(A, c->keySeg.p);
+        CK(cudaGetLastError());
+        ++c->kernelLaunches;
+      }
       if (kindMask & 6) {
         DetectArgs Ai = A;
         Ai.kindMask = kindMask & 6;
@@ -1551,7 +1566,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   f(c->order), f(c->orderAlt), f(c->cubTemp), f(c->blob), f(c->snapshot), f(c->keySeg);
   f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
   f(c->opSeq), f(c->opStart), f(c->traps), f(c->owner), f(c->keyElem), f(c->cand), f(c->ctr2);
-  f(c->interTab), f(c->interKeyElem), f(c->targets), f(c->shardLo), f(c->shardHi);
+  f(c->interTab), f(c->interKeyElem), f(c->targets), f(c->shardLo), f(c->shardHi), f(c->hot);
   for (char *ch : c->chunks)
     cudaFree(ch);
   for (auto &b : c->bigUsed)

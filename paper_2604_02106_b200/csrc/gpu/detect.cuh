@@ -51,7 +51,14 @@ struct DetectArgs {
   const int32_t *wHandle;
   int nW;
   int kindMask; // kinds to report: bit 0 INTER-BLOCK, 1 INTRA-BLOCK, 2 INTRA-WARP
+  // INTER-only detection: elements with more than kHotGroup records are
+  // listed here and summarised by a warp each (k_detect_hot)
+  uint32_t *hotList;
+  unsigned *hotCount;
+  uint32_t hotCap;
 };
+
+constexpr int kHotGroup = 64;
 
 __device__ __forceinline__ void siteKey(const DetectArgs &A, int a, int b, int kind,
                                         uint32_t segStart, uint32_t *keySeg) {
@@ -112,16 +119,30 @@ __global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
     return; // not the first record of its element
   if (i + 1 >= A.n || (A.keys[i + 1] >> kl.shE) != elem)
     return; // a lone access cannot race
+  if (A.hotList && A.kindMask == 1 && i + kHotGroup < A.n &&
+      (A.keys[i + kHotGroup] >> kl.shE) == elem) { // a hot element: one warp (k_detect_hot)
+    const unsigned slot = atomicAdd(A.hotCount, 1u);
+    if (slot < A.hotCap) {
+      A.hotList[slot] = static_cast<uint32_t>(i);
+      return;
+    }
+  }
   const uint64_t mB = fieldMask(kl.bB), mW = fieldMask(kl.bW), mL = fieldMask(kl.bL);
   uint32_t mn1[kMaxSites], mx1[kMaxSites], mn2[kMaxSites], mx2[kMaxSites],
       mn3[kMaxSites], mx3[kMaxSites];
   uint64_t p1 = 0, p2 = 0, p3 = 0;
   uint64_t g2 = k0 >> kl.shP, g3 = k0 >> kl.shQ;
   const uint32_t seg = static_cast<uint32_t>(i);
+  const bool lv1 = A.kindMask & 1, lv2 = A.kindMask & 2, lv3 = A.kindMask & 4;
   for (uint64_t j = i; j < A.n; ++j) {
     const uint64_t k = A.keys[j];
     if ((k >> kl.shE) != elem)
       break;
+    const int s = static_cast<int>(A.vals[j] >> kSeqBits);
+    if (!(lv2 | lv3)) { // INTER only (fused pass 2): the block level alone
+      note(p1, mn1, mx1, s, static_cast<uint32_t>((k >> kl.shB) & mB));
+      continue;
+    }
     if ((k >> kl.shP) != g2) {
       if (A.kindMask & 2)
         flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
@@ -134,10 +155,12 @@ __global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
       p3 = 0;
       g3 = k >> kl.shQ;
     }
-    const int s = static_cast<int>(A.vals[j] >> kSeqBits);
-    note(p1, mn1, mx1, s, static_cast<uint32_t>((k >> kl.shB) & mB));
-    note(p2, mn2, mx2, s, static_cast<uint32_t>((k >> kl.shW) & mW));
-    note(p3, mn3, mx3, s, static_cast<uint32_t>(k & mL));
+    if (lv1)
+      note(p1, mn1, mx1, s, static_cast<uint32_t>((k >> kl.shB) & mB));
+    if (lv2)
+      note(p2, mn2, mx2, s, static_cast<uint32_t>((k >> kl.shW) & mW));
+    if (lv3)
+      note(p3, mn3, mx3, s, static_cast<uint32_t>(k & mL));
   }
   if (A.kindMask & 1)
     flushLevel(A, p1, mn1, mx1, A.confInter, 0, seg, keySeg);
@@ -145,6 +168,53 @@ __global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
     flushLevel(A, p2, mn2, mx2, A.confIntra, 1, seg, keySeg);
   if (A.kindMask & 4)
     flushLevel(A, p3, mn3, mx3, A.confIntra, 2, seg, keySeg);
+}
+
+// INTER level of the hot elements listed by k_detect_summary: the lanes of
+// a warp stride over the element's records keeping per-site (min, max)
+// block, the warp reduces them per present site and lane 0 flushes.
+__global__ void k_detect_hot(DetectArgs A, uint32_t *keySeg) {
+  const int lane = threadIdx.x & 31;
+  const unsigned nHot = min(*A.hotCount, A.hotCap);
+  const unsigned warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned nWarps = (gridDim.x * blockDim.x) >> 5;
+  const KeyLayout kl = A.kl;
+  const uint64_t mB = fieldMask(kl.bB);
+  for (unsigned h = warp; h < nHot; h += nWarps) {
+    const uint64_t i = A.hotList[h];
+    const uint64_t elem = A.keys[i] >> kl.shE;
+    uint32_t mn[kMaxSites], mx[kMaxSites];
+    uint64_t p = 0;
+    for (uint64_t j = i + lane; j < A.n; j += 32) {
+      const uint64_t k = A.keys[j];
+      if ((k >> kl.shE) != elem)
+        break;
+      note(p, mn, mx, static_cast<int>(A.vals[j] >> kSeqBits),
+           static_cast<uint32_t>((k >> kl.shB) & mB));
+    }
+    uint64_t all = p;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      all |= __shfl_xor_sync(0xffffffffu, all, o);
+    uint64_t rem = all;
+    while (rem) { // warp-uniform
+      const int s = __ffsll(static_cast<long long>(rem)) - 1;
+      rem &= rem - 1;
+      const bool has = (p >> s) & 1ull;
+      uint32_t a = has ? mn[s] : 0xffffffffu, b = has ? mx[s] : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+      }
+      if (lane == 0) {
+        mn[s] = a;
+        mx[s] = b;
+      }
+    }
+    if (lane == 0)
+      flushLevel(A, all, mn, mx, A.confInter, 0, static_cast<uint32_t>(i), keySeg);
+  }
 }
 
 __device__ __forceinline__ void elementOf(const DetectArgs &A, uint64_t elem,

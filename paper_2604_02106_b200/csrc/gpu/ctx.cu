@@ -782,7 +782,36 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
                      sizeof(ParamDev) * P.params.size();
   const unsigned grid2 = static_cast<unsigned>(std::min<uint64_t>(
       ((static_cast<uint64_t>(D.nThreads) + 31) / 32 + 7) / 8, uint64_t(c->nSM) * 8));
-  {
+  // buffers two blocks can reach with exactly one recording site each: the
+  // ownership table alone gives the INTER keys (no summary pass)
+  SingleSites ss{};
+  bool single = o.nW <= 8;
+  if (single) {
+    ss.nW = o.nW;
+    for (int w = 0; w < o.nW; ++w) {
+      ss.wBase[w] = P.wBase[static_cast<size_t>(w)];
+      ss.site[w] = -1;
+    }
+    for (uint32_t s = 0; s < L.n_sites && single; ++s) {
+      const SiteDev &sd = P.sites[s];
+      if (!sd.record || !sd.own || sd.param < 0)
+        continue;
+      const int w = P.params[static_cast<size_t>(sd.param)].written - 1;
+      if (w < 0 || w >= o.nW)
+        continue;
+      if (ss.site[w] >= 0 && ss.site[w] != static_cast<int32_t>(s))
+        single = false;
+      ss.site[w] = static_cast<int32_t>(s);
+    }
+  }
+  if (single) {
+    NEED(c->interKeyElem, static_cast<size_t>(nKeys));
+    CK(cudaMemsetAsync(c->interKeyElem.p, 0xff, 8 * static_cast<size_t>(nKeys), c->st));
+    StageTimer t(c, "k_inter_scan_single");
+    k_inter_scan_single<<<static_cast<unsigned>((P.totalW + 255) / 256), 256, 0, c->st>>>(
+        c->owner.p, D2.ownerMultiTag, P.totalW, ss, D.sites, D.confInter, nLocs,
+        c->interKeyElem.p);
+  } else {
     // 2a: record-free INTER summary of the shared elements, then the realised
     //     INTER keys and their first-found (minimum) elements
     const size_t nTab = static_cast<size_t>(P.totalW) * L.n_sites;
@@ -809,6 +838,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
           c->owner.p, D2.ownerMultiTag, P.totalW, c->interTab.p, static_cast<int>(L.n_sites),
           D.sites, D.confInter, nLocs, c->interKeyElem.p);
     }
+  }
+  {
     CK(cudaGetLastError());
     c->kernelLaunches += 1;
     std::vector<unsigned long long> ke(static_cast<size_t>(nKeys));

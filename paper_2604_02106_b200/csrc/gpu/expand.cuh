@@ -89,10 +89,45 @@ __global__ void k_inter_scan(const uint32_t *owner, uint32_t multiTag, uint64_t 
         lb = t;
       }
       const int K = (la * nLocs + lb) * 3; // kind 0: INTER-BLOCK
-      if (keyElem[K] > e)
+      if (__ldcg(&keyElem[K]) > e)
         atomicMin(&keyElem[K], static_cast<unsigned long long>(e));
     }
   }
+}
+
+// Written buffers (<= 8) with their single recording site, by value.
+struct SingleSites {
+  uint64_t wBase[8];
+  int32_t site[8]; // -1: no recording site on the buffer
+  int nW;
+};
+
+// INTER keys without a summary pass, for launches where every buffer two
+// blocks can reach has exactly one recording site s: an element is then
+// realised for (s, s) iff the ownership table marks it MULTI (two blocks
+// reached it, both through s) and s conflicts with itself across blocks.
+__global__ void k_inter_scan_single(const uint32_t *owner, uint32_t multiTag, uint64_t nElems,
+                                    SingleSites ss, const SiteDev *sites,
+                                    const uint64_t *confInter, int nLocs,
+                                    unsigned long long *keyElem) {
+  const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int K = -1;
+  if (e < nElems && owner[e] == multiTag) {
+    int s = ss.site[0]; // static indices only: the by-value table stays in the parameter bank
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < ss.nW && ss.wBase[q] <= e)
+        s = ss.site[q];
+    if (s >= 0 && ((confInter[s] >> s) & 1ull))
+      K = (sites[s].loc * nLocs + sites[s].loc) * 3; // kind 0: INTER-BLOCK
+  }
+  // one atomic per key and warp: the lowest lane holds the warp's minimum
+  const unsigned act = __ballot_sync(0xffffffffu, K >= 0);
+  if (K < 0)
+    return;
+  const unsigned peers = __match_any_sync(act, K);
+  if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1) && __ldcg(&keyElem[K]) > e)
+    atomicMin(&keyElem[K], static_cast<unsigned long long>(e));
 }
 
 // Empty lo entry of the sharded INTER summary: positive as int32 too, so a
@@ -134,7 +169,7 @@ __global__ void k_inter_scan_minmax(const uint32_t *lo, const uint32_t *hi, uint
         kb = t;
       }
       const int K = (ka * nLocs + kb) * 3; // kind 0: INTER-BLOCK
-      if (keyElem[K] > e)
+      if (__ldcg(&keyElem[K]) > e)
         atomicMin(&keyElem[K], static_cast<unsigned long long>(e));
     }
   }

@@ -220,9 +220,24 @@ std::vector<uint8_t> blockPrivateSites(const hgrd_gpu_launch &L) {
   std::sort(handles.begin(), handles.end());
   handles.erase(std::unique(handles.begin(), handles.end()), handles.end());
   for (int32_t h : handles) {
-    bool ok = true, any = false;
+    bool ok = true, any = false, same = true, known = true;
+    std::optional<Form> first;
     std::array<i128, 3> a{};
     i128 lo = 0, hi = 0;
+    for (uint32_t s = 0; s < L.n_sites; ++s) { // test B input: one shared form?
+      const int32_t p = L.sites[s].param;
+      if (p < 0 || static_cast<uint32_t>(p) >= L.n_params || L.param_handle[p] != h ||
+          !siteSeen[s])
+        continue;
+      if (siteUnknown[s] || !siteIdx[s]) {
+        known = false;
+        break;
+      }
+      if (!first)
+        first = *siteIdx[s];
+      else if (!(*first == *siteIdx[s]))
+        same = false;
+    }
     for (uint32_t s = 0; s < L.n_sites && ok; ++s) {
       const int32_t p = L.sites[s].param;
       if (p < 0 || static_cast<uint32_t>(p) >= L.n_params || L.param_handle[p] != h)
@@ -254,8 +269,9 @@ std::vector<uint8_t> blockPrivateSites(const hgrd_gpu_launch &L) {
         hi = std::max(hi, thi);
       }
     }
-    if (!ok || !any)
+    if (!any)
       continue;
+    const bool formsOk = ok; // test A needs known forms sharing block coefficients
     const i128 W = hi - lo;
     std::array<std::pair<i128, i128>, 3> dims{}; // (|a_d|, grid extent)
     int nd = 0;
@@ -264,10 +280,45 @@ std::vector<uint8_t> blockPrivateSites(const hgrd_gpu_launch &L) {
         dims[nd++] = {a[d] < 0 ? -a[d] : a[d], D.extent[3 + d]};
     std::sort(dims.begin(), dims.begin() + nd);
     i128 reach = W; // largest in-block distance so far
-    for (int i = 0; i < nd && ok; ++i) {
+    for (int i = 0; i < nd && formsOk && ok; ++i) {
       if (dims[i].first <= reach)
         ok = false;
       reach += dims[i].first * (dims[i].second - 1);
+    }
+    // test B: every access of the buffer uses one form whose map from
+    // (threadIdx dims it depends on, blockIdx dims) to the index is
+    // injective (mixed radix: each coefficient exceeds the reach of the
+    // smaller ones), so equal indices imply equal blocks
+    if (!ok && known && same && first) {
+      std::array<std::pair<i128, i128>, 6> v{};
+      int nv = 0;
+      bool inj = true;
+      for (int d = 0; d < 6; ++d) {
+        if (D.extent[d] <= 1)
+          continue;
+        const i128 c = first->c[d] < 0 ? -first->c[d] : first->c[d];
+        if (c == 0) {
+          if (d >= 3)
+            inj = false; // two blocks on one range
+          continue;      // threads of one block may share elements
+        }
+        v[nv++] = {c, D.extent[d]};
+      }
+      std::sort(v.begin(), v.begin() + nv);
+      i128 reach = 0;
+      for (int i = 0; i < nv && inj; ++i) {
+        if (v[i].first <= reach)
+          inj = false;
+        reach += v[i].first * (v[i].second - 1);
+      }
+      if (inj) {
+        for (uint32_t s = 0; s < L.n_sites; ++s) {
+          const int32_t p = L.sites[s].param;
+          if (p >= 0 && static_cast<uint32_t>(p) < L.n_params && L.param_handle[p] == h)
+            priv[s] = 1;
+        }
+        continue;
+      }
     }
     if (!ok)
       continue;

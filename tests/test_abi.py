@@ -94,7 +94,17 @@ def test_block_private_analysis():
     assert not got[("tile", 1)] and not got[("out_", 1)] and got[("in_", 0)]
     tr = programs.transpose(256)
     got = _block_private(tr, "tr", (8, 8, 1), (32, 32, 1), {"tile": 0, "out_": 1}, {"n": 256})
-    assert got[("tile", 1)] and not got[("out_", 1)]
+    # out_'s per-block ranges interleave, but its single index form is
+    # injective over (threadIdx, blockIdx) in mixed radix (test B)
+    assert got[("tile", 1)] and got[("out_", 1)]
+    for n, ok in ((64, True), (4, True), (3, False)):  # A[tx * n + bx], 4 blocks
+        src = ("__global__ void k(int *A, int n) {\n  A[threadIdx.x * n + blockIdx.x] = 1;\n}\n"
+               "void main() { int *A; cudaMalloc(&A, 8192); k<<<4,32>>>(A, 64); }\n")
+        assert _block_private(src, "k", (4, 1, 1), (32, 1, 1), {"A": 0}, {"n": n})[("A", 1)] is ok
+    src = ("__global__ void k(int *A, int n) {\n  A[threadIdx.x * n + blockIdx.y] = 1;\n}\n"
+           "void main() { int *A; cudaMalloc(&A, 8192); k<<<(2,4,1),(32,1,1)>>>(A, 64); }\n")
+    # blockIdx.x does not move the index: blocks (0, y) and (1, y) share elements
+    assert not _block_private(src, "k", (2, 4, 1), (32, 1, 1), {"A": 0}, {"n": 64})[("A", 1)]
     hist = programs.histogram(1 << 12, 64)
     got = _block_private(hist, "h", (16, 1, 1), (256, 1, 1), {"data": 0, "hist": 1})
     assert got[("data", 0)] and not got[("hist", 1)]

@@ -21,7 +21,8 @@ from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIBRARY_PATH = os.path.join(_HERE, "libhgrd_gpu.so")
+# (HGRD_GPU_LIBRARY: development A/B runs against another build of the same tree)
+LIBRARY_PATH = os.environ.get("HGRD_GPU_LIBRARY") or os.path.join(_HERE, "libhgrd_gpu.so")
 
 # ---------------------------------------------------------------- ABI types
 c_int32, c_int64, c_uint8, c_uint16, c_uint32, c_uint64 = (

@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   const uint32_t fixedR = Body::kFixedR >= 0 ? static_cast<uint32_t>(Body::kFixedR) : F.R;
   LaneTally tally;
   unsigned myFlags = 0;
+  bool wroteCand = false; // this thread stored a candidate (released before the done count)
   int64_t regs[kMaxRegs];
 
   for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x) {
@@ -681,10 +682,12 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       sKeyBound[K] = old < ge ? static_cast<uint32_t>(old) : ge;
       if (ge <= old) {
         const unsigned c = atomicAdd(F.candCount, 1u);
-        if (c < F.candCap)
+        if (c < F.candCap) {
           F.cand[c] = Candidate{K, sX, sY, 0, ge, bestX, bestY};
-        else
+          wroteCand = true;
+        } else {
           myFlags |= kFlagFusedOverflow;
+        }
       }
     }
   }
@@ -718,7 +721,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   // The last CTA to finish turns the candidates into race records: per key,
   // the lexicographically first pair of the key's minimum element.
   __shared__ bool amLast;
-  __threadfence();
+  if (wroteCand) // candidate stores visible device-wide before this CTA counts as done
+    __threadfence();
   __syncthreads();
   if (tid == 0)
     amLast = atomicAdd(&L.ctr->doneCtas, 1u) == gridDim.x - 1;

@@ -63,6 +63,21 @@ __device__ __forceinline__ void threadIdentity(const LaunchDev &L, int64_t t, Bu
   lane = tl - warp * L.ws;
 }
 
+// Bounds check and element of a JIT access (C variants of the sinks); the
+// 32-bit forms are emitted only when the buffer size is below 2^31.
+__device__ __forceinline__ bool outOfRange(int64_t idx, int64_t size) {
+  return static_cast<uint64_t>(idx) >= static_cast<uint64_t>(size);
+}
+__device__ __forceinline__ bool outOfRange(int32_t idx, int64_t size) {
+  return static_cast<uint32_t>(idx) >= static_cast<uint32_t>(size);
+}
+__device__ __forceinline__ uint64_t elementAt(uint64_t base, int64_t idx) {
+  return base + static_cast<uint64_t>(idx);
+}
+__device__ __forceinline__ uint64_t elementAt(uint64_t base, int32_t idx) {
+  return base + static_cast<uint32_t>(idx);
+}
+
 struct InterpBody {
   static constexpr int kFixedR = -1; // records per thread not known at compile time
   __device__ static __forceinline__ void identity(const LaunchDev &L, int64_t t, Builtins &b,

@@ -235,23 +235,27 @@ struct ParSink : ParState {
   }
   // C variants (JIT bodies): the site's parameter, flags, buffer size and
   // element base as constants (size 0: unallocated parameter, always traps)
-  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool own, int64_t idx,
+  // (I: int64_t, or int32_t when the index and the buffer size fit 32 bits)
+  template <class I>
+  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool own, I idx,
                                            bool need, int64_t size, uint64_t base) {
-    if (static_cast<uint64_t>(idx) >= static_cast<uint64_t>(size)) {
+    if (outOfRange(idx, size)) {
       ++traps;
       return 0;
     }
     ++inst;
     if (rec)
-      recordE(site, base + static_cast<uint64_t>(idx), own);
+      recordE(site, elementAt(base, idx), own);
     ++seq;
     return need ? __ldg(params[param].ptr + idx) : 0;
   }
-  __device__ __forceinline__ void storeC(int site, int param, bool rec, bool own, int64_t idx,
-                                         int64_t, int64_t size, uint64_t base) {
+  template <class I>
+  __device__ __forceinline__ void storeC(int site, int param, bool rec, bool own, I idx, int64_t,
+                                         int64_t size, uint64_t base) {
     loadC(site, param, rec, own, idx, false, size, base);
   }
-  __device__ __forceinline__ void atomicC(int site, int param, bool rec, bool own, int64_t idx,
+  template <class I>
+  __device__ __forceinline__ void atomicC(int site, int param, bool rec, bool own, I idx,
                                           int64_t, int64_t, int64_t size, uint64_t base) {
     loadC(site, param, rec, own, idx, false, size, base);
   }

@@ -17,6 +17,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <sstream>
+#include <algorithm>
+#include <climits>
+#include <optional>
 #include <unordered_map>
 #include <vector>
 
@@ -90,6 +93,132 @@ bool hasLoops(const hgrd_gpu_launch &L) {
   return false;
 }
 
+// Value ranges of the registers before every instruction of loop-free code
+// (interval arithmetic in 128 bits over the launch's builtin ranges; loaded
+// values are unknown unless the PARALLEL sink returns 0 for them).  An
+// operation whose operands and result all fit in int32 computes the same
+// value in 32-bit arithmetic, which the generated body then uses.
+struct Range {
+  bool known = false;
+  __int128 lo = 0, hi = 0;
+  bool fits32() const { return known && lo >= INT32_MIN && hi <= INT32_MAX; }
+  bool operator==(const Range &o) const {
+    return known == o.known && (!known || (lo == o.lo && hi == o.hi));
+  }
+};
+
+std::vector<std::vector<Range>> valueRanges(const hgrd_gpu_launch &L) {
+  using R = std::vector<Range>;
+  const size_t nr = L.n_regs;
+  std::vector<R> before(L.n_code); // empty: unreachable
+  std::vector<std::optional<R>> pending(L.n_code + 1);
+  auto k = [](__int128 v) { return Range{true, v, v}; };
+  auto join = [](std::optional<R> &into, const R &s) {
+    if (!into) {
+      into = s;
+      return;
+    }
+    for (size_t r = 0; r < s.size(); ++r) {
+      Range &a = (*into)[r];
+      const Range &b = s[r];
+      if (!a.known || !b.known)
+        a = Range{};
+      else
+        a = Range{true, std::min(a.lo, b.lo), std::max(a.hi, b.hi)};
+    }
+  };
+  std::optional<R> cur = R(nr);
+  for (size_t r = 0; r < nr; ++r)
+    (*cur)[r] = k(L.reg_init ? L.reg_init[r] : 0);
+  const __int128 lim = static_cast<__int128>(INT64_MAX);
+  auto clip = [&](Range v) { // wrapping int64: only exact ranges are kept
+    if (!v.known || v.lo < -lim - 1 || v.hi > lim)
+      return Range{};
+    return v;
+  };
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    if (pending[pc]) {
+      if (cur)
+        join(pending[pc], *cur);
+      cur = pending[pc];
+      pending[pc].reset();
+    }
+    if (!cur)
+      continue;
+    before[pc] = *cur;
+    const auto &I = L.code[pc];
+    R &S = *cur;
+    auto get = [&](uint16_t r) { return r < nr ? S[r] : Range{}; };
+    auto put = [&](uint16_t r, Range v) {
+      if (r < nr)
+        S[r] = clip(v);
+    };
+    switch (I.op) {
+    case HGRD_OP_CONST:
+      put(I.a, k(I.imm));
+      break;
+    case HGRD_OP_MOV:
+      put(I.a, get(I.b));
+      break;
+    case HGRD_OP_BUILTIN:
+      if (I.sub < 3)
+        put(I.a, Range{true, 0, L.block[I.sub] - 1});
+      else if (I.sub < 6)
+        put(I.a, Range{true, 0, L.grid[I.sub - 3] - 1});
+      else if (I.sub < 9)
+        put(I.a, k(L.block[I.sub - 6]));
+      else if (I.sub < 12)
+        put(I.a, k(L.grid[I.sub - 9]));
+      else
+        put(I.a, Range{});
+      break;
+    case HGRD_OP_BIN: {
+      const Range l = get(I.b), r = get(I.c);
+      Range v;
+      if (I.sub >= HGRD_LT) {
+        v = Range{true, 0, 1}; // comparisons and logic yield 0 / 1
+      } else if (l.known && r.known) {
+        if (I.sub == HGRD_ADD) {
+          v = Range{true, l.lo + r.lo, l.hi + r.hi};
+        } else if (I.sub == HGRD_SUB) {
+          v = Range{true, l.lo - r.hi, l.hi - r.lo};
+        } else if (I.sub == HGRD_MUL) {
+          const __int128 c[4] = {l.lo * r.lo, l.lo * r.hi, l.hi * r.lo, l.hi * r.hi};
+          v = Range{true, *std::min_element(c, c + 4), *std::max_element(c, c + 4)};
+        } else if (r.lo == r.hi && r.lo != 0 && r.lo != -1) { // constant divisor
+          const __int128 d = r.lo;
+          if (I.sub == HGRD_DIV) {
+            const __int128 a = l.lo / d, b = l.hi / d;
+            v = Range{true, std::min(a, b), std::max(a, b)};
+          } else { // MOD: |result| < |d|, sign of the dividend
+            const __int128 m = (d < 0 ? -d : d) - 1;
+            v = Range{true, l.lo >= 0 ? 0 : -m, l.hi <= 0 ? 0 : m};
+          }
+        }
+      }
+      put(I.a, v);
+      break;
+    }
+    case HGRD_OP_LOAD:
+      put(I.a, (I.sub & 1) ? Range{} : k(0)); // PARALLEL: unneeded values read as 0
+      break;
+    case HGRD_OP_JZ:
+      join(pending[static_cast<size_t>(I.imm)], S);
+      break;
+    case HGRD_OP_JMP:
+      join(pending[static_cast<size_t>(I.imm)], S);
+      cur.reset();
+      break;
+    case HGRD_OP_END:
+      cur.reset();
+      break;
+    default:
+      break;
+    }
+  }
+  return before;
+}
+
 // A loop-free thread executes each STEP at most once: no per-statement
 // budget checks when the launch's budget covers them all (the host still
 // compares the launch's total steps with the budget).
@@ -117,6 +246,25 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
   }
   const bool loops = hasLoops(L);
   const bool noStepChecks = stepFree(L);
+  // 32-bit arithmetic where value ranges allow (loop-free kernels)
+  std::vector<std::vector<Range>> ranges;
+  if (!loops)
+    ranges = valueRanges(L);
+  auto rangeAt = [&](uint32_t pc, uint16_t r) -> Range {
+    return pc < ranges.size() && r < ranges[pc].size() ? ranges[pc][r] : Range{};
+  };
+  // the access's index register as a 32-bit value when it and the buffer
+  // size fit (one unsigned compare bounds-checks it)
+  auto idxArg = [&](uint32_t pc, uint16_t r, int64_t site) -> std::string {
+    const size_t i = static_cast<size_t>(site);
+    const int32_t p = i < L.n_sites ? L.sites[i].param : -1;
+    const int64_t size = (p >= 0 && static_cast<size_t>(p) < params.size())
+                             ? params[static_cast<size_t>(p)].size
+                             : 0;
+    if (rangeAt(pc, r).fits32() && size <= INT32_MAX)
+      return "static_cast<int32_t>(r" + std::to_string(r) + ")";
+    return "r" + std::to_string(r);
+  };
   // access -> literal arguments of the sink's C accessors: site, param,
   // record, own (rec[s]: bit 0 record, bit 1 ownership exchange), ... , size,
   // element base
@@ -169,19 +317,32 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
     case HGRD_OP_BUILTIN:
       o << "r" << I.a << " = bi.v[" << int(I.sub) << "];";
       break;
-    case HGRD_OP_BIN:
-      o << "r" << I.a << " = applyBin(" << int(I.sub) << ", r" << I.b << ", r" << I.c << ");";
+    case HGRD_OP_BIN: {
+      const Range rl = rangeAt(pc, I.b), rr = rangeAt(pc, I.c);
+      const Range res = pc + 1 < ranges.size() ? rangeAt(pc + 1, I.a) : Range{};
+      static const char *ops[] = {"+", "-", "*", "/", "%", "<", "<=", ">", ">=", "==", "!="};
+      const bool narrow = rl.fits32() && rr.fits32() && I.sub <= HGRD_NE &&
+                          (I.sub >= HGRD_LT || res.fits32()) &&
+                          ((I.sub != HGRD_DIV && I.sub != HGRD_MOD) ||
+                           (rr.lo == rr.hi && rr.lo != 0 && rr.lo != -1));
+      if (narrow)
+        o << "r" << I.a << " = static_cast<int64_t>(static_cast<int32_t>(r" << I.b << ") "
+          << ops[I.sub] << " static_cast<int32_t>(r" << I.c << "));";
+      else
+        o << "r" << I.a << " = applyBin(" << int(I.sub) << ", r" << I.b << ", r" << I.c << ");";
       break;
+    }
     case HGRD_OP_LOAD:
-      o << "r" << I.a << " = s.loadC(" << site(I.imm) << ", r" << I.b << ", "
+      o << "r" << I.a << " = s.loadC(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm) << ", "
         << ((I.sub & 1) ? "true" : "false") << buf(I.imm) << ");";
       break;
     case HGRD_OP_STORE:
-      o << "s.storeC(" << site(I.imm) << ", r" << I.a << ", r" << I.b << buf(I.imm) << ");";
+      o << "s.storeC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm) << ", r" << I.b
+        << buf(I.imm) << ");";
       break;
     case HGRD_OP_ATOMIC:
-      o << "s.atomicC(" << site(I.imm) << ", r" << I.a << ", r" << I.b << ", r" << I.c
-        << buf(I.imm) << ");";
+      o << "s.atomicC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm) << ", r" << I.b
+        << ", r" << I.c << buf(I.imm) << ");";
       break;
     case HGRD_OP_SYNCTHREADS:
       o << "s.syncthreads();";

@@ -90,6 +90,8 @@ struct hgrd_gpu_ctx {
   DevVec<uint32_t> owner;              // fused path: per-element ownership
   DevVec<uint32_t> shardLo, shardHi;   // sharded launches: INTER summary (min / max block)
   DevVec<uint32_t> hot;                // INTER detection: [0] count, then hot element starts
+  DevVec<int> doneKeys;                // pass 2b early stop: per INTER key done flag, key id
+  DevVec<uint64_t> doneTargets;        // ... and its first-found element
   uint32_t epoch = 0;
   DevVec<unsigned long long> keyElem;  // fused path: per key minimum element
   DevVec<Candidate> cand;
@@ -782,6 +784,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
                      sizeof(ParamDev) * P.params.size();
   const unsigned grid2 = static_cast<unsigned>(std::min<uint64_t>(
       ((static_cast<uint64_t>(D.nThreads) + 31) / 32 + 7) / 8, uint64_t(c->nSM) * 8));
+  std::vector<int> interKeys;        // realised INTER keys ...
+  std::vector<uint64_t> interTarget; // ... and their first-found elements
   // buffers two blocks can reach with exactly one recording site each: the
   // ownership table alone gives the INTER keys (no summary pass)
   SingleSites ss{};
@@ -849,8 +853,11 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     CK(cudaStreamSynchronize(c->st));
     std::vector<uint64_t> targets;
     for (int K = 0; K < nKeys; K += 3)
-      if (ke[static_cast<size_t>(K)] != ~0ull)
+      if (ke[static_cast<size_t>(K)] != ~0ull) {
         targets.push_back(ke[static_cast<size_t>(K)]);
+        interKeys.push_back(K);
+        interTarget.push_back(ke[static_cast<size_t>(K)]);
+      }
     std::sort(targets.begin(), targets.end());
     targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
     if (targets.empty())
@@ -883,23 +890,65 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     const size_t sm = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
                       sizeof(ParamDev) * P.params.size();
     const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
-    rc = launchExpandPar(c, D2, static_cast<unsigned>(blocks), sm, jx,
-                         jx ? "k_expand_par_shared[jit]" : "k_expand_par_shared");
-    if (rc < 0)
-      return rc;
-    rc = readCountersFrom(c, c->ctr2.p);
-    if (rc < 0)
-      return rc;
-    const Counters h2 = *c->hCtr;
-    if (h2.flags & kFlagCapacity) {
-      c->capHint = std::max<uint64_t>(c->capHint, h2.cursor + warps * chunk + 4096) * 2;
-      continue;
+    // block prefixes of doubling length: every key's witness lies in the
+    // earliest blocks reaching its element (later blocks' events come later
+    // in the reference order), so k_inter_done usually stops this pass after
+    // the first 1/64 of the launch
+    const int nK = static_cast<int>(interKeys.size());
+    NEED(c->doneKeys, 2 * static_cast<size_t>(std::max(nK, 1)));
+    int *dDone = c->doneKeys.p;
+    int *dKeys = dDone + std::max(nK, 1);
+    NEED(c->doneTargets, static_cast<size_t>(std::max(nK, 1)));
+    CK(cudaMemcpyAsync(dKeys, interKeys.data(), 4 * static_cast<size_t>(nK),
+                       cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->doneTargets.p, interTarget.data(), 8 * static_cast<size_t>(nK),
+                       cudaMemcpyHostToDevice, c->st));
+    c->h2dBytes += 12 * static_cast<size_t>(nK);
+    bool retry = false;
+    Counters h2{};
+    for (int64_t b0 = 0, b1 = std::max<int64_t>(1, D.nBlocks / 64); b0 < D.nBlocks;
+         b0 = b1, b1 = std::min<int64_t>(D.nBlocks, 2 * b1)) {
+      D2.threadBase = b0 * D.tpb;
+      D2.threadEnd = b1 * D.tpb;
+      rc = launchExpandPar(c, D2, static_cast<unsigned>(blocks), sm, jx,
+                           jx ? "k_expand_par_shared[jit]" : "k_expand_par_shared");
+      if (rc < 0)
+        return rc;
+      rc = readCountersFrom(c, c->ctr2.p);
+      if (rc < 0)
+        return rc;
+      h2 = *c->hCtr;
+      if (h2.flags & kFlagCapacity) {
+        c->capHint = std::max<uint64_t>(c->capHint, h2.cursor + warps * chunk + 4096) * 2;
+        retry = true;
+        break;
+      }
+      if (h2.flags & kFlagPhase) {
+        bP = std::max(bP, bitsFor(uint64_t(h2.maxBp) + 1));
+        bQ = std::max(bQ, bitsFor(uint64_t(h2.maxWp) + 1));
+        retry = true;
+        break;
+      }
+      if (b1 < D.nBlocks && nK > 0) {
+        {
+          StageTimer t(c, "k_inter_done");
+          k_inter_done<<<(nK + 7) / 8, 256, 0, c->st>>>(
+              c->keys.p, c->vals.p, std::min<uint64_t>(h2.cursor, cap), D2.kl, D.tpb, D.ws,
+              D.sites, D.confInter, nLocs, dKeys, c->doneTargets.p, nK, dDone);
+        }
+        CK(cudaGetLastError());
+        ++c->kernelLaunches;
+        std::vector<int> dn(static_cast<size_t>(nK));
+        CK(cudaMemcpyAsync(dn.data(), dDone, 4 * static_cast<size_t>(nK), cudaMemcpyDeviceToHost,
+                           c->st));
+        c->d2hBytes += 4 * static_cast<size_t>(nK);
+        CK(cudaStreamSynchronize(c->st));
+        if (std::all_of(dn.begin(), dn.end(), [](int v) { return v != 0; }))
+          break; // every INTER key's witness is in the records so far
+      }
     }
-    if (h2.flags & kFlagPhase) {
-      bP = std::max(bP, bitsFor(uint64_t(h2.maxBp) + 1));
-      bQ = std::max(bQ, bitsFor(uint64_t(h2.maxWp) + 1));
+    if (retry)
       continue;
-    }
     rc = detect(c, L, D2, o, std::min<uint64_t>(h2.cursor, cap), false, false, R, 1, true);
     return rc < 0 ? rc : 1;
   }
@@ -1598,6 +1647,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
   f(c->opSeq), f(c->opStart), f(c->traps), f(c->owner), f(c->keyElem), f(c->cand), f(c->ctr2);
   f(c->interTab), f(c->interKeyElem), f(c->targets), f(c->shardLo), f(c->shardHi), f(c->hot);
+  f(c->doneKeys), f(c->doneTargets);
   for (char *ch : c->chunks)
     cudaFree(ch);
   for (auto &b : c->bigUsed)

@@ -237,6 +237,78 @@ __device__ __forceinline__ uint64_t eventOrder(const DetectArgs &A, uint64_t k, 
   return (thread << kSeqBits) | (v & kSeqMask);
 }
 
+// Early stop of the prefix-wise INTER witness pass (fused pass 2b): for
+// INTER key keyList[w] with first-found element target[w], done[w] = 1 once
+// the earliest recorded event of that element at one of the key's locs, x,
+// has a partner among the records so far — a later event of another block
+// at the other loc whose site conflicts across blocks.  Records of later
+// blocks come later in the reference order, so x and its first partner are
+// then final.
+__global__ void k_inter_done(const uint64_t *keys, const uint32_t *vals, uint64_t n,
+                             KeyLayout kl, int64_t tpb, int64_t ws, const SiteDev *sites,
+                             const uint64_t *confInter, int nLocs, const int *keyList,
+                             const uint64_t *target, int nK, int *done) {
+  const int w = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= nK)
+    return;
+  const int K = keyList[w];
+  const int la = (K / 3) / nLocs, lb = (K / 3) % nLocs;
+  const uint64_t e = target[w];
+  const uint64_t mB = fieldMask(kl.bB), mW = fieldMask(kl.bW), mL = fieldMask(kl.bL);
+  auto order = [&](uint64_t k, uint32_t v) {
+    const uint64_t thread = ((k >> kl.shB) & mB) * static_cast<uint64_t>(tpb) +
+                            ((k >> kl.shW) & mW) * static_cast<uint64_t>(ws) + (k & mL);
+    return (thread << kSeqBits) | (v & kSeqMask);
+  };
+  uint64_t best = ~0ull; // earliest eligible event (order), its site and block
+  int bs = -1;
+  uint64_t bb = 0;
+  for (uint64_t i = lane; i < n; i += 32) {
+    const uint64_t k = keys[i];
+    if (k == kl.sentinel || (k >> kl.shE) != e)
+      continue;
+    const int s = static_cast<int>(vals[i] >> kSeqBits);
+    const int loc = sites[s].loc;
+    if (loc != la && loc != lb)
+      continue;
+    const uint64_t o = order(k, vals[i]);
+    if (o < best) {
+      best = o;
+      bs = s;
+      bb = (k >> kl.shB) & mB;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int os = __shfl_xor_sync(0xffffffffu, bs, off);
+    const uint64_t obb = __shfl_xor_sync(0xffffffffu, bb, off);
+    if (ob < best) {
+      best = ob;
+      bs = os;
+      bb = obb;
+    }
+  }
+  bool found = false;
+  if (bs >= 0) {
+    const int lx = sites[bs].loc;
+    const int want = lx == la ? lb : la; // the partner's loc
+    for (uint64_t i = lane; i < n && !found; i += 32) {
+      const uint64_t k = keys[i];
+      if (k == kl.sentinel || (k >> kl.shE) != e || ((k >> kl.shB) & mB) == bb)
+        continue;
+      const int s = static_cast<int>(vals[i] >> kSeqBits);
+      if (sites[s].loc != want || !((confInter[bs] >> s) & 1ull))
+        continue;
+      found = order(k, vals[i]) > best;
+    }
+  }
+  found = __any_sync(0xffffffffu, found);
+  if (lane == 0)
+    done[w] = found ? 1 : 0;
+}
+
 __device__ __forceinline__ uint32_t levelId(const KeyLayout &kl, int kind, uint64_t k) {
   if (kind == 0)
     return static_cast<uint32_t>((k >> kl.shB) & fieldMask(kl.bB));

@@ -6,10 +6,17 @@
 #include "gpu/affine.hpp"
 #include "gpu/jit.hpp"
 
+#include <algorithm>
 #include <cstdlib>
+#include <memory>
+#include <vector>
 #include <cstring>
 
 using namespace hgrdgpu;
+
+namespace hgrdgpu {
+hgrd_gpu_ctx *sweepWorker(hgrd_gpu_ctx *c, int i); // ctx.cu
+}
 
 namespace {
 
@@ -63,9 +70,25 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
                                     char **out) {
   if (!ctx || !out)
     return HGRD_GPU_EINVAL;
-  GpuBackend be(ctx);
+  // configurations are independent runs: spread them over worker contexts
+  // (own streams and buffers on the same GPU, one host thread each) so the
+  // small launches of a sweep overlap instead of queueing behind each
+  // other's host round trips (HGRD_SWEEP_WORKERS, default 8)
+  const char *env = std::getenv("HGRD_SWEEP_WORKERS");
+  const int n = std::max(1, env ? std::atoi(env) : 8);
+  std::vector<std::unique_ptr<GpuBackend>> bes(static_cast<size_t>(n));
+  auto worker = [&](int i) -> LaunchBackend * {
+    if (i >= n)
+      return nullptr;
+    hgrd_gpu_ctx *w = sweepWorker(ctx, i);
+    if (!w)
+      return nullptr;
+    if (!bes[static_cast<size_t>(i)])
+      bes[static_cast<size_t>(i)] = std::make_unique<GpuBackend>(w);
+    return bes[static_cast<size_t>(i)].get();
+  };
   std::string s;
-  int rc = enumerateVerdictJson(be, source, file_name, caps_json, s);
+  int rc = enumerateVerdictJsonParallel(worker, n, source, file_name, caps_json, s);
   *out = dup(s);
   return rc;
 }

@@ -58,6 +58,7 @@ int bitsFor(uint64_t n) { // bits to hold values 0 .. n-1
 } // namespace
 
 struct hgrd_gpu_ctx {
+  std::vector<hgrd_gpu_ctx *> workers; // sweep workers: own streams and buffers (same device)
   int device = 0;
   int nSM = 148;
   cudaStream_t st = nullptr;
@@ -1636,6 +1637,8 @@ int hgrd_gpu_create(int device, hgrd_gpu_ctx **out) {
 void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   if (!c)
     return;
+  for (hgrd_gpu_ctx *w : c->workers)
+    hgrd_gpu_destroy(w);
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
   auto f = [](auto &v) {
@@ -1859,3 +1862,22 @@ int hgrd_gpu_shard_detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, const 
 }
 
 } // extern "C"
+
+namespace hgrdgpu {
+// Worker i (>= 1) of a context for parallel sweeps: a further context on
+// the same device, created on first use and destroyed with its parent;
+// worker 0 is the context itself.  nullptr when it cannot be created.
+hgrd_gpu_ctx *sweepWorker(hgrd_gpu_ctx *c, int i) {
+  if (i == 0)
+    return c;
+  while (static_cast<int>(c->workers.size()) < i) {
+    hgrd_gpu_ctx *w = nullptr;
+    if (hgrd_gpu_create(c->device, &w) != HGRD_GPU_OK)
+      return nullptr;
+    w->fusedEnabled = c->fusedEnabled;
+    w->jitMode = c->jitMode;
+    c->workers.push_back(w);
+  }
+  return c->workers[static_cast<size_t>(i - 1)];
+}
+} // namespace hgrdgpu

@@ -20,6 +20,8 @@
 // that writes memory runs SEQUENTIAL, so buffers are always exact.
 #include "host.hpp"
 
+#include <thread>
+
 #include <algorithm>
 #include <cinttypes>
 #include <cstdio>
@@ -1308,6 +1310,95 @@ int runConcreteJson(LaunchBackend &be, const char *src, const char *file,
     return r.error;
   }
   out = runResultJson(r, fileName);
+  return HGRD_GPU_OK;
+}
+
+uint64_t sweepSize(const CompiledProgram &prog, const SweepCaps &caps) {
+  long double per = 1;
+  for (int i = 0; i < prog.inputs; ++i)
+    per *= static_cast<long double>(caps.inputSet.size());
+  const long double all = per * static_cast<long double>(caps.warpSizes.size());
+  const long double cap = static_cast<long double>(caps.maxConfigs) + 1;
+  return static_cast<uint64_t>(all < cap ? all : cap);
+}
+
+SweepResult enumerateVerdictParallel(CompiledProgram &prog, const SweepCaps &caps,
+                                     const std::vector<LaunchBackend *> &backends) {
+  // lower every kernel first: the shards then only read the program
+  for (const auto &k : prog.program->kernels)
+    prog.kernel(&k);
+  const int world = static_cast<int>(backends.size());
+  std::vector<SweepShard> shards(static_cast<size_t>(world));
+  std::vector<std::thread> threads;
+  for (int r = 0; r < world; ++r)
+    threads.emplace_back([&, r] {
+      shards[static_cast<size_t>(r)] = sweepShard(prog, caps, r, world, *backends[static_cast<size_t>(r)]);
+    });
+  for (auto &t : threads)
+    t.join();
+  SweepResult out;
+  std::vector<const ShardConfig *> all;
+  for (const auto &sh : shards) {
+    if (sh.error) {
+      out.error = sh.error;
+      out.errorMessage = sh.errorMessage;
+      return out;
+    }
+    out.configs = std::max<uint64_t>(out.configs, sh.total);
+    out.stats.instances += sh.stats.instances;
+    out.stats.records += sh.stats.records;
+    out.stats.deviceMs += sh.stats.deviceMs;
+    out.stats.parLaunches += sh.stats.parLaunches;
+    out.stats.seqLaunches += sh.stats.seqLaunches;
+    out.stats.restarts += sh.stats.restarts;
+    for (const auto &c : sh.configs)
+      all.push_back(&c);
+  }
+  std::sort(all.begin(), all.end(),
+            [](const ShardConfig *a, const ShardConfig *b) { return a->index < b->index; });
+  std::set<std::tuple<int, int, int, int, int, int64_t>> seen; // reference :883-889
+  for (const ShardConfig *c : all)
+    for (const auto &race : c->races) {
+      auto key = std::make_tuple(race.locA.line, race.locA.col, race.locB.line, race.locB.col,
+                                 race.kind, c->warpSize);
+      if (seen.insert(key).second)
+        out.races.push_back(SweepRace{race.locA, race.locB, race.kind, c->warpSize});
+    }
+  return out;
+}
+
+int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &workers, int n,
+                                 const char *src, const char *file, const char *capsJson,
+                                 std::string &out) {
+  SweepCaps caps;
+  std::string err;
+  if (!parseSweepCapsJson(capsJson, caps, err)) {
+    out = errorJson({"caps: " + err});
+    return HGRD_GPU_EINVAL;
+  }
+  ParseOutcome po = parseMiniCU(src ? src : "", file ? file : "");
+  if (!po.program) {
+    out = errorJson(po.diagnostics);
+    return HGRD_GPU_OK;
+  }
+  std::string fileName = po.program->file;
+  auto cp = compileProgram(std::move(po.program));
+  const uint64_t size = sweepSize(*cp, caps);
+  int use = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(std::max(n, 1)), size / 4));
+  std::vector<LaunchBackend *> bes;
+  for (int i = 0; i < std::max(use, 1); ++i) {
+    LaunchBackend *b = workers(i);
+    if (!b)
+      break;
+    bes.push_back(b);
+  }
+  SweepResult r = bes.size() > 1 ? enumerateVerdictParallel(*cp, caps, bes)
+                                 : enumerateVerdict(*cp, caps, *bes[0]);
+  if (r.error) {
+    out = errorJson({"backend: " + r.errorMessage});
+    return r.error;
+  }
+  out = sweepResultJson(r, fileName);
   return HGRD_GPU_OK;
 }
 

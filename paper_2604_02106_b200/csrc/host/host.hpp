@@ -10,6 +10,7 @@
 
 #include <array>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -147,6 +148,13 @@ struct SweepShard {
 SweepShard sweepShard(CompiledProgram &prog, const SweepCaps &caps, int rank, int world,
                       LaunchBackend &backend);
 std::string sweepShardJson(const SweepShard &r, const std::string &file);
+// enumerateVerdict over several backends at once (one host thread each, a
+// strided share of the lattice per backend), merged in canonical order with
+// the reference's first-wins dedup: the result equals enumerateVerdict's.
+SweepResult enumerateVerdictParallel(CompiledProgram &prog, const SweepCaps &caps,
+                                     const std::vector<LaunchBackend *> &backends);
+// Configurations enumerateVerdict runs (warp sizes x input odometer, capped).
+uint64_t sweepSize(const CompiledProgram &prog, const SweepCaps &caps);
 int sweepShardJsonRun(LaunchBackend &be, const char *src, const char *file,
                       const char *capsJson, int rank, int world, std::string &out);
 int countInputs(const Program &p);                 // oracle.cpp:805-861
@@ -165,5 +173,11 @@ int runConcreteJson(LaunchBackend &be, const char *src, const char *file,
                     const char *cfgJson, std::string &out);
 int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
                          const char *capsJson, std::string &out);
+// Same with the configurations spread over `workers` backends.  `workers`
+// returns backend i (0 = the caller's) or nullptr; used when the lattice has
+// at least 4 configurations per worker.
+int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &workers, int n,
+                                 const char *src, const char *file, const char *capsJson,
+                                 std::string &out);
 
 } // namespace hgrdgpu

@@ -16,6 +16,7 @@ using namespace hgrdgpu;
 
 namespace hgrdgpu {
 hgrd_gpu_ctx *sweepWorker(hgrd_gpu_ctx *c, int i); // ctx.cu
+bool setTiming(hgrd_gpu_ctx *c, bool on);            // ctx.cu
 }
 
 namespace {
@@ -83,12 +84,16 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
     hgrd_gpu_ctx *w = sweepWorker(ctx, i);
     if (!w)
       return nullptr;
+    if (i > 0)
+      setTiming(w, false); // worker contexts only run sweeps
     if (!bes[static_cast<size_t>(i)])
       bes[static_cast<size_t>(i)] = std::make_unique<GpuBackend>(w);
     return bes[static_cast<size_t>(i)].get();
   };
   std::string s;
+  const bool timing = setTiming(ctx, false);
   int rc = enumerateVerdictJsonParallel(worker, n, source, file_name, caps_json, s);
+  setTiming(ctx, timing);
   *out = dup(s);
   return rc;
 }

@@ -103,6 +103,7 @@ struct hgrd_gpu_ctx {
   bool fusedEnabled = true;
   // NVRTC specialisation: 0 off, 1 auto (large launches), 2 always
   int jitMode = 1;
+  bool timing = std::getenv("HGRD_NO_DEVICE_TIMING") == nullptr; // device_ms via events
   hgrdgpu::jit::Cache *jit = nullptr;
   std::string jitErr;
   int jitFailures = 0;
@@ -1093,7 +1094,8 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   c->stages.clear();
   c->evUsed = 0;
   c->racesOnHost = false;
-  CK(cudaEventRecord(c->e0, c->st));
+  if (c->timing)
+    CK(cudaEventRecord(c->e0, c->st));
 
   Plan P;
   BlobOffsets o{};
@@ -1307,10 +1309,14 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     break;
   }
 finish:
-  CK(cudaEventRecord(c->e1, c->st));
-  CK(cudaEventSynchronize(c->e1));
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  if (c->timing) {
+    CK(cudaEventRecord(c->e1, c->st));
+    CK(cudaEventSynchronize(c->e1));
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  } else {
+    CK(cudaStreamSynchronize(c->st));
+  }
   R->device_ms = ms;
   if (c->profiling) {
     std::string j = "[";
@@ -1422,7 +1428,8 @@ int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
   c->stages.clear();
   c->evUsed = 0;
   c->racesOnHost = false;
-  CK(cudaEventRecord(c->e0, c->st));
+  if (c->timing)
+    CK(cudaEventRecord(c->e0, c->st));
   ShardSetup S;
   int rc = shardPrepare(c, L, Sh->block_begin, Sh->block_end, S);
   if (rc < 0)
@@ -1472,10 +1479,14 @@ int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
     Sh->inter_hi = c->shardHi.p;
     Sh->inter_n = n;
   }
-  CK(cudaEventRecord(c->e1, c->st));
-  CK(cudaEventSynchronize(c->e1));
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  if (c->timing) {
+    CK(cudaEventRecord(c->e1, c->st));
+    CK(cudaEventSynchronize(c->e1));
+    CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
+  } else {
+    CK(cudaStreamSynchronize(c->st));
+  }
   R->device_ms = ms;
   return 0;
 }
@@ -1879,5 +1890,12 @@ hgrd_gpu_ctx *sweepWorker(hgrd_gpu_ctx *c, int i) {
     c->workers.push_back(w);
   }
   return c->workers[static_cast<size_t>(i - 1)];
+}
+// Per-check device timing (events around the check; device_ms).  Sweeps of
+// tiny launches turn it off: the extra event round trip is ~12% of a check.
+bool setTiming(hgrd_gpu_ctx *c, bool on) {
+  const bool was = c->timing;
+  c->timing = on && std::getenv("HGRD_NO_DEVICE_TIMING") == nullptr;
+  return was;
 }
 } // namespace hgrdgpu

@@ -656,7 +656,7 @@ size_t fusedSmemBytes(const hgrd_gpu_launch &L, const Plan &P, int nKeys) {
   const size_t nKeysPad = (static_cast<size_t>(nKeys) + 3) & ~size_t(3);
   return align16(sizeof(FusedSmem<NT, IPT>)) + 12 * nKeysPad + sizeof(hgrd_gpu_insn) * L.n_code +
          sizeof(SiteDev) * P.sites.size() + sizeof(ParamDev) * P.params.size() +
-         8 * P.sites.size();
+         16 * P.sites.size();
 }
 
 int readCountersFrom(hgrd_gpu_ctx *c, Counters *dev) {
@@ -743,7 +743,10 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.blockBase = b0;
   F.blockEnd = b1;
   F.nIters = (b1 - b0 + bpi - 1) / bpi;
-  F.owner = shard ? nullptr : c->owner.p;
+  // a launch that fits one iteration finds its INTER pairs on chip as well
+  // (no ownership exchanges, no pass 2); shards leave INTER to their tables
+  F.interOnChip = !shard && F.nIters == 1;
+  F.owner = (shard || F.interOnChip) ? nullptr : c->owner.p;
   F.epoch = c->epoch;
   F.keyElem = c->curKeyElem;
   F.cand = c->cand.p;

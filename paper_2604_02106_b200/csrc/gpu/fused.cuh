@@ -52,6 +52,7 @@ struct FusedArgs {
   int nLocs, nKeys;
   int bpi;              // whole MiniCU blocks per iteration
   int64_t blockBase, blockEnd; // dense MiniCU block range of this launch (or shard)
+  int interOnChip; // the whole launch is one iteration: INTER-BLOCK pairs found on chip too
   uint32_t R;           // records per MiniCU thread when static (0: allocate)
   int64_t nIters;
   uint32_t *owner; // per element ownership word (see FusedSink)
@@ -205,7 +206,9 @@ template <class Smem> struct FusedSink : ParState {
   int nLocs;
   uint32_t *keyMin;  // per key: minimum element realised in the iteration
   uint32_t *real;    // realised keys
-  const uint64_t *conf; // per site: statically conflicting sites (bit mask)
+  const uint64_t *conf;  // per site: statically conflicting sites within a block (bit mask)
+  const uint64_t *confX; // ... across blocks (interOnChip)
+  bool interOnChip;
   uint32_t *owner;      // per element ownership words (nullptr: ablated)
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
@@ -224,13 +227,21 @@ template <class Smem> struct FusedSink : ParState {
       if (rElem(q0) != e)
         continue;
       const uint64_t q1 = S->r1[q];
-      if (rBlk(q1) == myBlk)
+      const uint64_t *cf = conf;
+      int kind;
+      if (rBlk(q1) == myBlk) {
         first = false;
-      const int kind = intraRule(q1, r1);
+        kind = intraRule(q1, r1);
+      } else if (interOnChip) { // another block of this one-iteration launch
+        kind = 0;
+        cf = confX;
+      } else {
+        continue; // INTER: the ownership exchange and pass 2
+      }
       if (kind < 0)
         continue;
       const int sq = rSite(q0);
-      if (!((conf[sq] >> site) & 1ull))
+      if (!((cf[sq] >> site) & 1ull))
         continue;
       int la = sites[sq].loc, lb = myLoc;
       if (lb < la) {
@@ -376,6 +387,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   SiteDev *sSites = reinterpret_cast<SiteDev *>(sCode + F.L.nCode);
   ParamDev *sParams = reinterpret_cast<ParamDev *>(sSites + F.L.nSites);
   uint64_t *sConf = reinterpret_cast<uint64_t *>(sParams + F.L.nParams);
+  uint64_t *sConfX = sConf + F.L.nSites;
   // dynamic shared memory layout mirrored by fusedSmemBytes() in ctx.cu
   const LaunchDev &L = F.L;
   const int tid = threadIdx.x;
@@ -384,6 +396,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   for (int i = tid; i < L.nSites; i += kFusedThreads) {
     sSites[i] = L.sites[i];
     sConf[i] = L.confIntra[i];
+    sConfX[i] = L.confInter[i];
   }
   for (int i = tid; i < L.nParams; i += kFusedThreads)
     sParams[i] = L.params[i];
@@ -436,6 +449,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.keyMin = sKeyMin;
         s.real = sReal;
         s.conf = sConf;
+        s.confX = sConfX;
+        s.interOnChip = F.interOnChip != 0;
         s.owner = (F.ablate & 4) ? nullptr : F.owner;
         s.epochTag = F.epoch << 20;
         s.mine = static_cast<uint32_t>(firstBlock + s.myBlk + 1);
@@ -468,6 +483,10 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
     if (F.ablate & 1)
       continue;
     const bool hashed = S.hot == 0;
+    if (!hashed && F.interOnChip) { // radix grouping has no INTER level: general path
+      myFlags |= kFlagFusedOverflow;
+      continue;
+    }
     if (!hashed) {
       // radix mode for this iteration: drop the hash-mode keys, sort by
       // w | off | blk | bp | warp | wp | lane and summarise per group
@@ -670,10 +689,12 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
           const int lob = sSites[sb].loc;
           if (!((loa == la && lob == lb) || (loa == lb && lob == la)))
             continue;
-          if (!((sConf[sa] >> sb) & 1ull))
+          if (kind == 0) { // interOnChip: other block, conflicting across blocks
+            if (rBlk(a1) == rBlk(b1) || !((sConfX[sa] >> sb) & 1ull))
+              continue;
+          } else if (!((sConf[sa] >> sb) & 1ull) || intraRule(a1, b1) != kind) {
             continue;
-          if (intraRule(a1, b1) != kind)
-            continue;
+          }
           if (oa < bestX || (oa == bestX && ob < bestY)) {
             bestX = oa;
             bestY = ob;

@@ -68,6 +68,7 @@ struct hgrd_gpu_ctx {
   struct Buf {
     int64_t *p;
     int64_t elems;
+    bool zeroPending; // allocated, zero-initialisation not yet materialised
   };
   std::vector<Buf> bufs;
   // small allocations: bump arena over 256 MiB chunks; large: size-keyed cache
@@ -294,6 +295,17 @@ struct Plan {
   bool summaryOk = true;
 };
 
+// A buffer's pending zero-initialisation, done before anything reads its
+// values (host reads and writes, value-needed loads, sequential launches).
+int materialize(hgrd_gpu_ctx *c, int32_t h) {
+  auto &b = c->bufs[static_cast<size_t>(h)];
+  if (b.zeroPending) {
+    CK(cudaMemsetAsync(b.p, 0, static_cast<size_t>(b.elems) * 8, c->st));
+    b.zeroPending = false;
+  }
+  return 0;
+}
+
 void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
   std::vector<char> written(c->bufs.size(), 0);
   auto handleOfParam = [&](int p) -> int32_t {
@@ -332,8 +344,23 @@ void planLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P) {
     }
     P.params[p] = d;
   }
+  // value-needed loads read buffer contents even in PARALLEL mode
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    const auto &I = L.code[pc];
+    if (I.op == HGRD_OP_LOAD && (I.sub & 1) && static_cast<uint64_t>(I.imm) < L.n_sites) {
+      const int32_t h = handleOfParam(L.sites[static_cast<size_t>(I.imm)].param);
+      if (h >= 0)
+        materialize(c, h);
+    }
+  }
   P.sites.resize(std::max<uint32_t>(L.n_sites, 1));
-  const std::vector<uint8_t> priv = hgrdgpu::blockPrivateSites(L);
+  // block privacy only matters for launches spread over several k_fused
+  // iterations (one-iteration launches pair INTER on chip): tiny launches
+  // skip the analysis and keep every exchange (always correct)
+  const int64_t nThreads = L.grid[0] * L.grid[1] * L.grid[2] * L.block[0] * L.block[1] *
+                           L.block[2];
+  const std::vector<uint8_t> priv = nThreads <= 512 ? std::vector<uint8_t>(L.n_sites, 0)
+                                                    : hgrdgpu::blockPrivateSites(L);
   for (uint32_t s = 0; s < L.n_sites; ++s) {
     SiteDev d{};
     d.param = L.sites[s].param;
@@ -1212,7 +1239,11 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
         return rc;
       break;
     }
-    // SEQUENTIAL
+    // SEQUENTIAL: kernel loads and stores read and write every parameter buffer
+    for (uint32_t p = 0; p < L.n_params; ++p)
+      if (L.param_handle[p] >= 0 && static_cast<size_t>(L.param_handle[p]) < c->bufs.size() &&
+          materialize(c, L.param_handle[p]) < 0)
+        return HGRD_GPU_ECUDA;
     if (!snapped) {
       size_t bytes = 0;
       for (int32_t hnd : P.wHandle)
@@ -1786,8 +1817,8 @@ int hgrd_gpu_buffer_alloc(hgrd_gpu_ctx *c, int64_t elems, int32_t *handle) {
     }
     c->bigUsed.push_back(BigBlock{p, bytes});
   }
-  CK(cudaMemsetAsync(p, 0, static_cast<size_t>(elems) * 8, c->st));
-  c->bufs.push_back(hgrd_gpu_ctx::Buf{reinterpret_cast<int64_t *>(p), elems});
+  // zero-initialised lazily: only values a check or the host reads need it
+  c->bufs.push_back(hgrd_gpu_ctx::Buf{reinterpret_cast<int64_t *>(p), elems, true});
   *handle = static_cast<int32_t>(c->bufs.size() - 1);
   return 0;
 }
@@ -1800,6 +1831,10 @@ int hgrd_gpu_buffer_write(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n,
   if (n == 0)
     return 0;
   CK(cudaSetDevice(c->device));
+  if (off == 0 && n == c->bufs[static_cast<size_t>(h)].elems)
+    c->bufs[static_cast<size_t>(h)].zeroPending = false; // fully overwritten
+  if (materialize(c, h) < 0)
+    return HGRD_GPU_ECUDA;
   CK(cudaMemcpyAsync(c->bufs[static_cast<size_t>(h)].p + off, src, static_cast<size_t>(n) * 8,
                      cudaMemcpyHostToDevice, c->st));
   c->h2dBytes += static_cast<size_t>(n) * 8;
@@ -1813,6 +1848,8 @@ int hgrd_gpu_buffer_read(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n, int
   if (n == 0)
     return 0;
   CK(cudaSetDevice(c->device));
+  if (materialize(c, h) < 0)
+    return HGRD_GPU_ECUDA;
   CK(cudaMemcpyAsync(dst, c->bufs[static_cast<size_t>(h)].p + off, static_cast<size_t>(n) * 8,
                      cudaMemcpyDeviceToHost, c->st));
   c->d2hBytes += static_cast<size_t>(n) * 8;

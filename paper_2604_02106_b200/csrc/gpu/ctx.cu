@@ -594,9 +594,18 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       NEED(c->keyPair, static_cast<size_t>(nKeys));
       CK(cudaMemsetAsync(c->keyPair.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
       {
+        const uint32_t bigCap = 1u << 16;
+        NEED(c->hot, bigCap + 1);
+        CK(cudaMemsetAsync(c->hot.p, 0, sizeof(uint32_t), c->st));
+        A.hotCount = c->hot.p;
+        A.hotList = c->hot.p + 1;
+        A.hotCap = bigCap;
         StageTimer t(c, "k_detect_pairwise");
         k_detect_pairwise<<<g, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(), locks,
                                                  c->keyPair.p);
+        k_detect_pairwise_big<<<c->nSM * 4, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(),
+                                                             locks, c->keyPair.p);
+        ++c->kernelLaunches;
       }
       CK(cudaGetLastError());
       k_decode_pairwise<<<(nKeys + 127) / 128, 128, 0, c->st>>>(

@@ -618,6 +618,59 @@ __device__ __forceinline__ Ev decodeEv(const DetectArgs &A, uint64_t k, uint32_t
   return e;
 }
 
+// Pairs of one element group (sorted by element, canonical order within),
+// the reference's detectRaces rule (:730-784) including lockOrdered.  The
+// first-found pair per key is the minimum of element | x | y, packed as
+// group start (24 bits) | x offset (20) | y offset (20).
+constexpr uint64_t kPairGroupMax = 1u << 20, kPairEventsMax = 1u << 24;
+constexpr uint64_t kPairBig = 64; // larger groups: k_detect_pairwise_big
+
+__device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
+                                        const uint32_t *order, bool locks, uint64_t i,
+                                        uint64_t e, uint64_t x, unsigned long long *keyPair,
+                                        unsigned &flags) {
+  LockInfo la, lb;
+  const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
+  const SiteDev sa = A.sites[a.site];
+  if (locks)
+    lockInfoOf(L, a.thread, a.seq, la, flags);
+  for (uint64_t y = x + 1; y < e; ++y) {
+    const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
+    if (a.thread == b.thread)
+      continue;
+    const SiteDev sb = A.sites[b.site];
+    if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
+      continue;
+    const bool sameBlock = a.block == b.block;
+    if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC &&
+        covers(sa.scope, sameBlock) && covers(sb.scope, sameBlock))
+      continue;
+    if (sameBlock && a.bp != b.bp)
+      continue;
+    const bool sameWarp = sameBlock && a.warp == b.warp;
+    if (sameWarp && a.wp != b.wp)
+      continue;
+    if (locks) {
+      lockInfoOf(L, b.thread, b.seq, lb, flags);
+      if (crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
+          crossed(lb.rel, la.acq, sameBlock))
+        continue;
+    }
+    const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
+    int l0 = sa.loc, l1 = sb.loc;
+    if (l1 < l0) {
+      int t = l0;
+      l0 = l1;
+      l1 = t;
+    }
+    const int K = (l0 * A.nLocs + l1) * 3 + kind;
+    const unsigned long long packed =
+        (static_cast<unsigned long long>(i) << 40) | ((x - i) << 20) | (y - i);
+    if (keyPair[K] > packed)
+      atomicMin(&keyPair[K], packed);
+  }
+}
+
 __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
                                   const uint32_t *order, bool locks,
                                   unsigned long long *keyPair) {
@@ -630,52 +683,55 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
   uint64_t e = i + 1;
   while (e < A.n && elemSorted[e] == elem)
     ++e;
-  unsigned flags = 0;
-  if (e - i > 65535) {
+  if (e - i < 2)
+    return;
+  if (e - i >= kPairGroupMax || A.n >= kPairEventsMax) {
     atomicOr(&L.ctr->flags, static_cast<unsigned>(kFlagSegment));
     return;
   }
-  LockInfo la, lb;
-  for (uint64_t x = i; x < e; ++x) {
-    const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
-    const SiteDev sa = A.sites[a.site];
-    if (locks)
-      lockInfoOf(L, a.thread, a.seq, la, flags);
-    for (uint64_t y = x + 1; y < e; ++y) {
-      const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
-      if (a.thread == b.thread)
-        continue;
-      const SiteDev sb = A.sites[b.site];
-      if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
-        continue;
-      const bool sameBlock = a.block == b.block;
-      if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC &&
-          covers(sa.scope, sameBlock) && covers(sb.scope, sameBlock))
-        continue;
-      if (sameBlock && a.bp != b.bp)
-        continue;
-      const bool sameWarp = sameBlock && a.warp == b.warp;
-      if (sameWarp && a.wp != b.wp)
-        continue;
-      if (locks) {
-        lockInfoOf(L, b.thread, b.seq, lb, flags);
-        if (crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
-            crossed(lb.rel, la.acq, sameBlock))
-          continue;
-      }
-      const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
-      int l0 = sa.loc, l1 = sb.loc;
-      if (l1 < l0) {
-        int t = l0;
-        l0 = l1;
-        l1 = t;
-      }
-      const int K = (l0 * A.nLocs + l1) * 3 + kind;
-      const unsigned long long packed =
-          (static_cast<unsigned long long>(i) << 32) | ((x - i) << 16) | (y - i);
-      if (keyPair[K] > packed)
-        atomicMin(&keyPair[K], packed);
+  if (A.nSites <= 64) { // no statically conflicting pair of the group's sites: skip
+    uint64_t pres = 0;
+    for (uint64_t x = i; x < e; ++x)
+      pres |= 1ull << (A.vals[order[x]] >> kSeqBits);
+    bool any = false;
+    for (uint64_t rem = pres; rem && !any; rem &= rem - 1) {
+      const int s = __ffsll(static_cast<long long>(rem)) - 1;
+      any = ((A.confInter[s] | A.confIntra[s]) & pres) != 0;
     }
+    if (!any)
+      return;
+  }
+  if (e - i > kPairBig && A.hotList) { // a large group: all CTAs of k_detect_pairwise_big
+    const unsigned slot = atomicAdd(A.hotCount, 1u);
+    if (slot < A.hotCap) {
+      A.hotList[slot] = static_cast<uint32_t>(i);
+      return;
+    }
+  }
+  unsigned flags = 0;
+  for (uint64_t x = i; x < e; ++x)
+    pairRow(A, L, order, locks, i, e, x, keyPair, flags);
+  if (flags)
+    atomicOr(&L.ctr->flags, flags);
+}
+
+// The large groups listed by k_detect_pairwise: every CTA takes a share of
+// each group's rows, so a hot element (a lock word, a histogram bin) is
+// spread over the whole GPU.
+__global__ void k_detect_pairwise_big(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
+                                      const uint32_t *order, bool locks,
+                                      unsigned long long *keyPair) {
+  const unsigned nBig = min(*A.hotCount, A.hotCap);
+  unsigned flags = 0;
+  for (unsigned h = 0; h < nBig; ++h) {
+    const uint64_t i = A.hotList[h];
+    const uint64_t elem = elemSorted[i];
+    uint64_t e = i + 1;
+    while (e < A.n && elemSorted[e] == elem)
+      ++e;
+    for (uint64_t x = i + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < e;
+         x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+      pairRow(A, L, order, locks, i, e, x, keyPair, flags);
   }
   if (flags)
     atomicOr(&L.ctr->flags, flags);
@@ -691,8 +747,8 @@ __global__ void k_decode_pairwise(DetectArgs A, const uint64_t *elemSorted,
   const unsigned long long p = keyPair[K];
   if (p == ~0ull)
     return;
-  const uint64_t s = p >> 32;
-  const uint64_t x = s + ((p >> 16) & 0xffff), y = s + (p & 0xffff);
+  const uint64_t s = p >> 40;
+  const uint64_t x = s + ((p >> 20) & 0xfffff), y = s + (p & 0xfffff);
   const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
   const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
   const unsigned pos = atomicAdd(&ctr->nRaces, 1u);

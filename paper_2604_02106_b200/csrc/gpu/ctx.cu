@@ -1284,6 +1284,12 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     if (locks) {
       NEED(c->opStart, static_cast<size_t>(D.nThreads) + 1);
       uint64_t ocap = std::max<uint64_t>(c->opHint, 16);
+      if (!loops) { // loop-free: each sync-op instruction runs at most once per thread
+        uint64_t perThread = 0;
+        for (uint32_t pc = 0; pc < L.n_code; ++pc)
+          perThread += L.code[pc].op == HGRD_OP_ATOMIC || L.code[pc].op == HGRD_OP_FENCE;
+        ocap = std::max<uint64_t>(ocap, static_cast<uint64_t>(D.nThreads) * perThread + 16);
+      }
       NEED(c->opIndex, ocap);
       NEED(c->opMeta, ocap);
       NEED(c->opSeq, ocap);

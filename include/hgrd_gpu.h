@@ -276,8 +276,9 @@ int hgrd_gpu_block_private(const hgrd_gpu_launch *launch, uint8_t *out);
 
 /* Development check (no GPU needed): lower `kernel`, generate its NVRTC
  * thread body for the given geometry (scalar parameters 0, every site
- * recording) and compile all three specialised kernels for sm_100a without
- * loading them.  *out = {"variants":[{"cubin_bytes":N,"error":"..."}x3]}.
+ * recording) and compile every specialised kernel for sm_100a without
+ * loading them (k_expand_par, k_fused<256,4>, <256,16>, <256,8>,
+ * k_expand_seq).  *out = {"variants":[{"cubin_bytes":N,"error":"..."}x5]}.
  * Returns HGRD_GPU_ENOTSUP when a variant does not compile. */
 int hgrd_gpu_jit_check(const char *source, const char *file_name, const char *kernel,
                        const int64_t grid[3], const int64_t block[3], int64_t warp_size,

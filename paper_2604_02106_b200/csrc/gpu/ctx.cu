@@ -57,7 +57,12 @@ int bitsFor(uint64_t n) { // bits to hold values 0 .. n-1
 
 } // namespace
 
+// k_expand_seq's shared-memory register file limit (larger register files
+// stay in global scratch)
+constexpr size_t kSeqSharedMax = 200 * 1024;
+
 struct hgrd_gpu_ctx {
+  bool seqSharedSet = false;           // k_expand_seq opted into > 48 KB
   std::vector<hgrd_gpu_ctx *> workers; // sweep workers: own streams and buffers (same device)
   int device = 0;
   int nSM = 148;
@@ -1175,7 +1180,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
                        o.nW <= kMaxWritten && D.nBlocks < (1 << 20) - 2 &&
                        !(L.flags & HGRD_LAUNCH_GENERAL);
   // NVRTC specialisation for large PARALLEL launches (compiled on first use)
-  const bool useJit = !seq && (c->jitMode == 2 || (c->jitMode == 1 && D.nThreads >= (int64_t(1) << 14)));
+  const bool useJit = c->jitMode == 2 || (c->jitMode == 1 && D.nThreads >= (int64_t(1) << 14));
   JitGetter jk{c, &L, useJit, {}, {}};
   for (uint32_t p = 0; p < L.n_params; ++p) {
     const ParamDev &d = P.params[p];
@@ -1304,7 +1309,22 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     }
     {
       StageTimer t(c, "k_expand_seq");
-      k_expand_seq<InterpBody><<<1, 32, 0, c->st>>>(D);
+      const size_t sh = static_cast<size_t>(D.nRegs) * sizeof(int64_t);
+      const bool staged = sh <= kSeqSharedMax;
+      if (staged && sh > 48 * 1024 && !c->seqSharedSet) {
+        CK(cudaFuncSetAttribute(k_expand_seq<InterpBody>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSeqSharedMax)));
+        c->seqSharedSet = true;
+      }
+      // an NVRTC body removes the interpreter's dispatch from the chain
+      if (const void *jf = jk.get(hgrdgpu::jit::kExpandSeq)) {
+        int noStage = 0;
+        void *args[] = {&D, &noStage};
+        CK(cudaLaunchKernel(jf, dim3(1), dim3(32), args, 0, c->st));
+      } else {
+        k_expand_seq<InterpBody><<<1, 32, staged ? sh : 0, c->st>>>(D, staged ? 1 : 0);
+      }
     }
     CK(cudaGetLastError());
     ++c->kernelLaunches;

@@ -494,9 +494,66 @@ struct SeqSink {
     op(2, scope, -1, 0, seq);
     ++seq;
   }
+  // NVRTC bodies (jit.cpp): the site's parameter, record flag, buffer size
+  // and element base are constants, so in-range accesses skip the site and
+  // parameter lookups; out-of-range ones take the generic path, which
+  // classifies and orders the trap (a folded size of 0 covers unallocated)
+  __device__ __forceinline__ void stepNC() { ++steps; }
+  __device__ __forceinline__ int64_t *fastAccess(int site, int param, bool rec, int64_t idx,
+                                                 uint64_t base) {
+    ++inst;
+    if (rec) {
+      const KeyLayout &kl = L->kl;
+      const uint64_t maskP = fieldMask(kl.bP), maskQ = fieldMask(kl.bQ);
+      if (bp > maskP || wp > maskQ)
+        flags |= kFlagPhase;
+      if (seq > kSeqMask)
+        flags |= kFlagSeqSite;
+      if (cursor < L->capacity) {
+        L->keys[cursor] = packKey(kl, base + static_cast<uint64_t>(idx),
+                                  static_cast<uint64_t>(block), bp & maskP,
+                                  static_cast<uint64_t>(warp), wp & maskQ,
+                                  static_cast<uint64_t>(lane));
+        L->vals[cursor] = (static_cast<uint32_t>(site) << kSeqBits) | (seq & kSeqMask);
+      } else {
+        flags |= kFlagCapacity;
+      }
+      ++cursor;
+    }
+    ++seq;
+    return L->params[param].ptr + idx;
+  }
+  template <class I>
+  __device__ __forceinline__ int64_t loadC(int site, int param, bool rec, bool, I idx, bool need,
+                                           int64_t size, uint64_t base) {
+    if (outOfRange(idx, size))
+      return load(site, static_cast<int64_t>(idx), need);
+    return *fastAccess(site, param, rec, static_cast<int64_t>(idx), base);
+  }
+  template <class I>
+  __device__ __forceinline__ void storeC(int site, int param, bool rec, bool, I idx, int64_t v,
+                                         int64_t size, uint64_t base) {
+    if (outOfRange(idx, size))
+      store(site, static_cast<int64_t>(idx), v);
+    else
+      *fastAccess(site, param, rec, static_cast<int64_t>(idx), base) = v;
+  }
+  template <class I>
+  __device__ __forceinline__ void atomicC(int site, int, bool, bool, I idx, int64_t v,
+                                          int64_t cmp, int64_t, uint64_t) {
+    atomic(site, static_cast<int64_t>(idx), v, cmp);
+  }
 };
 
-template <class Body> __global__ void k_expand_seq(LaunchDev L) {
+// The canonical order is one serial chain, so its cost is latency: with
+// `staged` the register file lives in shared memory (nRegs * 8 bytes of
+// dynamic smem) instead of global scratch, where every register
+// read-after-write was an L2 round trip.  (The bytecode and initial values
+// stay global: the compiler addresses pointers reached from the launch
+// parameters as global, and they are read-only L1 hits anyway.)
+template <class Body> __global__ void k_expand_seq(LaunchDev L, int staged) {
+  extern __shared__ int64_t seqSh[];
+  int64_t *regs = staged ? seqSh : L.seqRegs;
   if (blockIdx.x != 0 || threadIdx.x != 0)
     return;
   SeqSink s;
@@ -508,7 +565,7 @@ template <class Body> __global__ void k_expand_seq(LaunchDev L) {
     s.bp = s.wp = s.seq = 0;
     if (L.opStart)
       L.opStart[t] = s.nOps;
-    Body::run(L, L.code, bi, s, L.seqRegs);
+    Body::run(L, L.code, bi, s, regs);
     s.maxBp = max(s.maxBp, s.bp);
     s.maxWp = max(s.maxWp, s.wp);
   }

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -110,6 +111,11 @@ struct hgrd_gpu_ctx {
   // NVRTC specialisation: 0 off, 1 auto (large launches), 2 always
   int jitMode = 1;
   bool timing = std::getenv("HGRD_NO_DEVICE_TIMING") == nullptr; // device_ms via events
+  // development: HGRD_HOST_TRACE=1 prints host-side phase times per check
+  bool hostTrace = std::getenv("HGRD_HOST_TRACE") != nullptr;
+  bool e1AtSync = false; // e1 recorded at readCountersAndRaces' synchronisation
+  bool e1Done = false;   // ... and no GPU work since: the check's end
+  std::vector<std::pair<const char *, std::chrono::steady_clock::time_point>> trace;
   hgrdgpu::jit::Cache *jit = nullptr;
   std::string jitErr;
   int jitFailures = 0;
@@ -206,6 +212,11 @@ cudaEvent_t poolEvent(hgrd_gpu_ctx *c) {
 }
 
 // RAII marker around one pipeline stage when profiling is on.
+inline void htrace(hgrd_gpu_ctx *c, const char *what) {
+  if (c->hostTrace)
+    c->trace.emplace_back(what, std::chrono::steady_clock::now());
+}
+
 struct StageTimer {
   hgrd_gpu_ctx *c;
   size_t idx = SIZE_MAX;
@@ -472,7 +483,12 @@ int readCountersAndRaces(hgrd_gpu_ctx *c, size_t nKeys) {
   }
   CK(cudaMemcpyAsync(c->hResult, c->cur, bytes, cudaMemcpyDeviceToHost, c->st));
   c->d2hBytes += bytes;
+  // the check's end event rides on this synchronisation: when the check
+  // finishes here (no INTER pass), no second round trip is needed
+  if (c->timing)
+    CK(cudaEventRecord(c->e1, c->st));
   CK(cudaStreamSynchronize(c->st));
+  c->e1AtSync = c->timing;
   std::memcpy(c->hCtr, c->hResult, sizeof(Counters));
   c->hRacesView = reinterpret_cast<hgrd_gpu_race *>(c->hResult + racesOff);
   c->racesOnHost = true;
@@ -725,9 +741,11 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *ji
   const int64_t grid = std::max<int64_t>(
       1, std::min<int64_t>(F.nIters, static_cast<int64_t>(c->nSM) * std::max(perSM, 1)));
   void *args[] = {const_cast<FusedArgs *>(&F)};
+  htrace(c, "pre-launch");
   StageTimer t(c, jitKernel ? "k_fused[jit]" : "k_fused");
   CK(cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(NT), args, smem,
                       c->st));
+  htrace(c, "launched");
   return 0;
 }
 
@@ -809,6 +827,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   rc = readCountersAndRaces(c, static_cast<size_t>(nKeys));
   if (rc < 0)
     return rc;
+  htrace(c, "counters");
   const Counters h = *c->hCtr;
   if ((h.flags & (kFlagAbort | kFlagFusedOverflow)) || h.traps > 0 ||
       static_cast<int64_t>(h.steps) > L.step_budget)
@@ -817,8 +836,12 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   R->instances = h.instances;
   R->records = h.records;
   R->mode = L.flags & ~HGRD_LAUNCH_SEQUENTIAL;
-  if (shard || !(h.flags & kFlagShared))
-    return fetchRaces(c, R) < 0 ? -1 : 1;
+  if (shard || !(h.flags & kFlagShared)) {
+    if (fetchRaces(c, R) < 0) // (races read from the same synchronisation)
+      return -1;
+    c->e1Done = c->e1AtSync;
+    return 1;
+  }
 
   // pass 2: INTER-BLOCK over the elements two or more blocks touched
   NEED(c->ctr2, 1);
@@ -1083,9 +1106,11 @@ int snapshot(hgrd_gpu_ctx *c, const Plan &P, bool restore) {
 int prepareLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P, BlobOffsets &o,
                   LaunchDev &D) {
   planLaunch(c, L, P);
+  htrace(c, "plan");
   int rc = uploadBlob(c, L, P, o);
   if (rc < 0)
     return rc;
+  htrace(c, "upload");
   D = LaunchDev{};
   D.code = reinterpret_cast<const hgrd_gpu_insn *>(c->blob.p + o.code);
   D.sites = reinterpret_cast<const SiteDev *>(c->blob.p + o.sites);
@@ -1125,6 +1150,10 @@ int prepareLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P, BlobOffset
 }
 
 int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
+  if (c->hostTrace) {
+    c->trace.clear();
+    c->trace.emplace_back("start", std::chrono::steady_clock::now());
+  }
   R->n_races = 0;
   R->n_traps = 0;
   R->n_traps_total = 0;
@@ -1138,6 +1167,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   c->stages.clear();
   c->evUsed = 0;
   c->racesOnHost = false;
+  c->e1Done = false;
   if (c->timing)
     CK(cudaEventRecord(c->e0, c->st));
 
@@ -1380,13 +1410,25 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
 finish:
   float ms = 0;
   if (c->timing) {
-    CK(cudaEventRecord(c->e1, c->st));
-    CK(cudaEventSynchronize(c->e1));
+    if (!c->e1Done) {
+      CK(cudaEventRecord(c->e1, c->st));
+      CK(cudaEventSynchronize(c->e1));
+    }
     CK(cudaEventElapsedTime(&ms, c->e0, c->e1));
   } else {
     CK(cudaStreamSynchronize(c->st));
   }
   R->device_ms = ms;
+  if (c->hostTrace) {
+    htrace(c, "end");
+    std::fprintf(stderr, "[hgrd host]");
+    for (size_t i = 1; i < c->trace.size(); ++i)
+      std::fprintf(stderr, " %s %.1f", c->trace[i].first,
+                   std::chrono::duration<double, std::micro>(c->trace[i].second -
+                                                             c->trace[i - 1].second)
+                       .count());
+    std::fprintf(stderr, " (us)\n");
+  }
   if (c->profiling) {
     std::string j = "[";
     for (size_t i = 0; i < c->stages.size(); ++i) {

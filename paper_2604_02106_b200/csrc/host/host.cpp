@@ -23,8 +23,10 @@
 #include <thread>
 
 #include <algorithm>
+#include <chrono>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <set>
@@ -1297,6 +1299,9 @@ int runConcreteJson(LaunchBackend &be, const char *src, const char *file,
     out = errorJson({"config: " + err});
     return HGRD_GPU_EINVAL;
   }
+  // development: HGRD_HOST_TRACE=1 prints the host phases of the call
+  static const bool trace = std::getenv("HGRD_HOST_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   ParseOutcome po = parseMiniCU(src ? src : "", file ? file : "");
   if (!po.program) {
     out = errorJson(po.diagnostics);
@@ -1304,12 +1309,20 @@ int runConcreteJson(LaunchBackend &be, const char *src, const char *file,
   }
   std::string fileName = po.program->file;
   auto cp = compileProgram(std::move(po.program));
+  const auto t1 = std::chrono::steady_clock::now();
   RunResult r = runConcrete(*cp, cfg, be);
+  const auto t2 = std::chrono::steady_clock::now();
   if (r.error) {
     out = errorJson({"backend: " + r.errorMessage});
     return r.error;
   }
   out = runResultJson(r, fileName);
+  if (trace) {
+    const auto t3 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "[hgrd run_concrete] parse+compile %.1f run %.1f json %.1f (us)\n",
+                 us(t0, t1), us(t1, t2), us(t2, t3));
+  }
   return HGRD_GPU_OK;
 }
 

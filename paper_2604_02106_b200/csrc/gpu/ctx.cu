@@ -1338,7 +1338,6 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       D.opCap = 0;
     }
     {
-      StageTimer t(c, "k_expand_seq");
       const size_t sh = static_cast<size_t>(D.nRegs) * sizeof(int64_t);
       const bool staged = sh <= kSeqSharedMax;
       if (staged && sh > 48 * 1024 && !c->seqSharedSet) {
@@ -1351,8 +1350,10 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       if (const void *jf = jk.get(hgrdgpu::jit::kExpandSeq)) {
         int noStage = 0;
         void *args[] = {&D, &noStage};
+        StageTimer t(c, "k_expand_seq[jit]");
         CK(cudaLaunchKernel(jf, dim3(1), dim3(32), args, 0, c->st));
       } else {
+        StageTimer t(c, "k_expand_seq");
         k_expand_seq<InterpBody><<<1, 32, staged ? sh : 0, c->st>>>(D, staged ? 1 : 0);
       }
     }

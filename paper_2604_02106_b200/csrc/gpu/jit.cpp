@@ -223,17 +223,23 @@ std::vector<std::vector<Range>> valueRanges(const hgrd_gpu_launch &L) {
 // A loop-free thread executes each STEP at most once: no per-statement
 // budget checks when the launch's budget covers them all (the host still
 // compares the launch's total steps with the budget).
-bool stepFree(const hgrd_gpu_launch &L) {
+// The canonical-order kernel is itself the exact (aborting) path, so there
+// the whole launch's steps must fit the budget.
+bool stepFree(const hgrd_gpu_launch &L, bool seq) {
   if (hasLoops(L))
     return false;
   int64_t n = 0;
   for (uint32_t pc = 0; pc < L.n_code; ++pc)
     n += L.code[pc].op == HGRD_OP_STEP;
-  return n <= L.step_budget;
+  if (!seq)
+    return n <= L.step_budget;
+  const __int128 threads = static_cast<__int128>(L.grid[0]) * L.grid[1] * L.grid[2] *
+                           L.block[0] * L.block[1] * L.block[2];
+  return threads * n <= L.step_budget;
 }
 
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
-                     const std::vector<JitParam> &params) {
+                     const std::vector<JitParam> &params, bool seq) {
   std::vector<char> target(L.n_code + 1, 0);
   uint32_t nRec = 0;
   for (uint32_t pc = 0; pc < L.n_code; ++pc) {
@@ -246,7 +252,7 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
       ++nRec;
   }
   const bool loops = hasLoops(L);
-  const bool noStepChecks = stepFree(L);
+  const bool noStepChecks = stepFree(L, seq);
   // 32-bit arithmetic where value ranges allow (loop-free kernels)
   std::vector<std::vector<Range>> ranges;
   if (!loops)
@@ -465,12 +471,12 @@ const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &
   put(L.sites, sizeof(hgrd_gpu_site) * L.n_sites);
   put(rec.data(), rec.size());
   put(params.data(), sizeof(JitParam) * params.size());
-  const bool noStepChecks = stepFree(L);
+  const bool noStepChecks = stepFree(L, v == kExpandSeq);
   put(&noStepChecks, sizeof noStepChecks);
   auto it = c->mods.find(key);
   if (it != c->mods.end())
     return it->second;
-  const std::string src = generate(L, rec, params);
+  const std::string src = generate(L, rec, params, v == kExpandSeq);
   const auto t0 = std::chrono::steady_clock::now();
   auto fail = [&](const std::string &why) -> const void * {
     err = why;
@@ -504,7 +510,7 @@ size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
   Cache *c = create();
   std::vector<char> cubin;
   std::string lowered;
-  const std::string src = generate(L, rec, params);
+  const std::string src = generate(L, rec, params, v == kExpandSeq);
   if (const char *dump = std::getenv("HGRD_JIT_DUMP")) { // development: keep the source
     if (FILE *f = std::fopen(dump, "w")) {
       std::fputs(src.c_str(), f);

@@ -31,7 +31,7 @@ void destroy(Cache *c);
 const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                 const std::vector<JitParam> &params, Variant v, std::string &err);
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
-                     const std::vector<JitParam> &params);
+                     const std::vector<JitParam> &params, bool seq = false);
 // Compile without loading (no GPU needed): cubin size, 0 and err on failure.
 size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                    const std::vector<JitParam> &params, Variant v, std::string &err);

@@ -222,3 +222,41 @@ def test_full_histogram_2p27(gpu, cpu_oracle, bins, update):
     want = cpu_oracle.check_launch(small, bufs)
     assert got["races"] == want["races"]
     assert got["instances"] == 2 << 27
+
+
+# ------------------------------------------------- SEQUENTIAL at launch scale
+def _chain(n, a_elems):
+    """Each thread reads what the previous one stored (value-relevant loads:
+    canonical order, k_expand_seq); with a_elems == n the last thread's
+    store is out of bounds (a trap in canonical order)."""
+    return ("__global__ void k(int *A, int *B) {\n"
+            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+            "  int v = A[t];\n"
+            f"  B[(v + t) % {n}] = t;\n"
+            "  A[t + 1] = v + 1;\n"
+            "}\n"
+            f"void main() {{ int *A; int *B; cudaMalloc(&A, {a_elems}); cudaMalloc(&B, {n});\n"
+            f"  k<<<({n // 256},1,1),(256,1,1)>>>(A, B); }}\n")
+
+
+@pytest.mark.parametrize("case", ["clean_bounds", "trap_last", "budget"])
+def test_sequential_large(gpu, cpu_oracle, case):
+    """A 2^16-thread SEQUENTIAL launch through the NVRTC canonical-order body
+    (k_expand_seq[jit]): races, traps and the step-budget abort equal the
+    CPU restatement's."""
+    n = 1 << 16
+    src = _chain(n, n if case == "trap_last" else n + 1)
+    cfg = programs.synthetic_config(**({"maxSteps": 200000} if case == "budget" else {}))
+    gpu.set_profiling(True)
+    try:
+        got = gpu.run_concrete(src, cfg, "seq.mcu")
+        names = [s["name"] for s in gpu.last_profile()]
+    finally:
+        gpu.set_profiling(False)
+    want = cpu_oracle.run_concrete(src, cfg, "seq.mcu")
+    assert strip_extras(got) == strip_extras(want), (got, want)
+    assert got["witnesses"] == want["witnesses"]
+    assert got["stats"]["instances"] == want["stats"]["instances"]
+    assert "k_expand_seq[jit]" in names, names
+    if case == "trap_last":
+        assert got["traps"]

@@ -92,6 +92,7 @@ struct hgrd_gpu_ctx {
   DevVec<hgrd_gpu_race> races;
   DevVec<Counters> ctr;
   DevVec<int64_t> seqRegs, opIndex;
+  DevVec<uint64_t> lockC;              // pairwise path: per-event compact lock facts
   DevVec<int32_t> opMeta, opSeq;
   DevVec<uint64_t> opStart;
   DevVec<hgrd_gpu_trap> traps;
@@ -621,11 +622,19 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
         A.hotCount = c->hot.p;
         A.hotList = c->hot.p + 1;
         A.hotCap = bigCap;
+        LockC *lc = nullptr;
+        if (locks) {
+          NEED(c->lockC, n * (sizeof(LockC) / 8));
+          lc = reinterpret_cast<LockC *>(c->lockC.p);
+          StageTimer t(c, "k_lock_info");
+          k_lock_info<<<g, 256, 0, c->st>>>(A, D, dv.Current(), lc);
+          ++c->kernelLaunches;
+        }
         StageTimer t(c, "k_detect_pairwise");
-        k_detect_pairwise<<<g, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(), locks,
+        k_detect_pairwise<<<g, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(), locks, lc,
                                                  c->keyPair.p);
         k_detect_pairwise_big<<<c->nSM * 4, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(),
-                                                             locks, c->keyPair.p);
+                                                             locks, lc, c->keyPair.p);
         ++c->kernelLaunches;
       }
       CK(cudaGetLastError());
@@ -1773,7 +1782,7 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   f(c->keyPair), f(c->races), f(c->ctr), f(c->seqRegs), f(c->opIndex), f(c->opMeta);
   f(c->opSeq), f(c->opStart), f(c->traps), f(c->owner), f(c->keyElem), f(c->cand), f(c->ctr2);
   f(c->interTab), f(c->interKeyElem), f(c->targets), f(c->shardLo), f(c->shardHi), f(c->hot);
-  f(c->doneKeys), f(c->doneTargets);
+  f(c->doneKeys), f(c->doneTargets), f(c->lockC);
   for (char *ch : c->chunks)
     cudaFree(ch);
   for (auto &b : c->bigUsed)

@@ -599,6 +599,43 @@ __device__ __forceinline__ bool crossed(const LockSet &x, const LockSet &y, bool
   return false;
 }
 
+// Per-event lock facts precomputed once (k_lock_info) instead of per pair:
+// up to two entries per set, entry = (handle + 1) << 48 | scope << 46 |
+// index, 0 = empty.  Wider sets, handles or indices mark the event
+// kLockWide and pairRow recomputes its LockInfo.
+struct LockC {
+  uint64_t cs[2], acq[2], rel[2];
+};
+constexpr uint64_t kLockWide = ~0ull;
+constexpr uint64_t kLockScopeBits = 3ull << 46;
+
+__device__ __forceinline__ bool packSet(const LockSet &s, uint64_t *out) {
+  if (s.n > 2)
+    return false;
+  for (int i = 0; i < 2; ++i) {
+    out[i] = 0;
+    if (i < s.n) {
+      if (s.h[i] < 0 || s.h[i] >= 0xffff || s.idx[i] < 0 || s.idx[i] >= (int64_t(1) << 46) ||
+          s.scope[i] < 0 || s.scope[i] > 3)
+        return false;
+      out[i] = (static_cast<uint64_t>(s.h[i] + 1) << 48) |
+               (static_cast<uint64_t>(s.scope[i]) << 46) | static_cast<uint64_t>(s.idx[i]);
+    }
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool crossedC(const uint64_t *x, const uint64_t *y, bool sameBlock) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (x[i] && y[j] && ((x[i] ^ y[j]) & ~kLockScopeBits) == 0 &&
+          covers(static_cast<int32_t>(min(x[i], y[j]) >> 46) & 3, sameBlock))
+        return true;
+  return false;
+}
+
 struct Ev {
   uint64_t block, warp, lane, bp, wp, thread;
   int site, seq;
@@ -626,14 +663,20 @@ constexpr uint64_t kPairGroupMax = 1u << 20, kPairEventsMax = 1u << 24;
 constexpr uint64_t kPairBig = 64; // larger groups: k_detect_pairwise_big
 
 __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
-                                        const uint32_t *order, bool locks, uint64_t i,
-                                        uint64_t e, uint64_t x, unsigned long long *keyPair,
-                                        unsigned &flags) {
+                                        const uint32_t *order, bool locks, const LockC *lc,
+                                        uint64_t i, uint64_t e, uint64_t x,
+                                        unsigned long long *keyPair, unsigned &flags) {
   LockInfo la, lb;
   const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
   const SiteDev sa = A.sites[a.site];
-  if (locks)
+  LockC ca{};
+  bool laFull = false;
+  if (locks && lc) {
+    ca = lc[x];
+  } else if (locks) {
     lockInfoOf(L, a.thread, a.seq, la, flags);
+    laFull = true;
+  }
   for (uint64_t y = x + 1; y < e; ++y) {
     const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
     if (a.thread == b.thread)
@@ -651,9 +694,21 @@ __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
     if (sameWarp && a.wp != b.wp)
       continue;
     if (locks) {
-      lockInfoOf(L, b.thread, b.seq, lb, flags);
-      if (crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
-          crossed(lb.rel, la.acq, sameBlock))
+      bool ordered;
+      const LockC cb = lc ? lc[y] : LockC{};
+      if (lc && ca.cs[0] != kLockWide && cb.cs[0] != kLockWide) {
+        ordered = crossedC(ca.cs, cb.cs, sameBlock) || crossedC(ca.rel, cb.acq, sameBlock) ||
+                  crossedC(cb.rel, ca.acq, sameBlock);
+      } else {
+        if (!laFull) {
+          lockInfoOf(L, a.thread, a.seq, la, flags);
+          laFull = true;
+        }
+        lockInfoOf(L, b.thread, b.seq, lb, flags);
+        ordered = crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
+                  crossed(lb.rel, la.acq, sameBlock);
+      }
+      if (ordered)
         continue;
     }
     const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
@@ -671,8 +726,26 @@ __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
   }
 }
 
+// Lock facts of every event (sorted position x), once: lockInfoOf per pair
+// was the pairwise pass's dominant cost on lock kernels.
+__global__ void k_lock_info(DetectArgs A, LaunchDev L, const uint32_t *order, LockC *out) {
+  const uint64_t x = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= A.n)
+    return;
+  const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
+  LockInfo li;
+  unsigned flags = 0;
+  lockInfoOf(L, a.thread, a.seq, li, flags);
+  LockC c;
+  if (!packSet(li.cs, c.cs) || !packSet(li.acq, c.acq) || !packSet(li.rel, c.rel))
+    c.cs[0] = kLockWide;
+  out[x] = c;
+  if (flags)
+    atomicOr(&L.ctr->flags, flags);
+}
+
 __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
-                                  const uint32_t *order, bool locks,
+                                  const uint32_t *order, bool locks, const LockC *lc,
                                   unsigned long long *keyPair) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= A.n)
@@ -710,7 +783,7 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
   }
   unsigned flags = 0;
   for (uint64_t x = i; x < e; ++x)
-    pairRow(A, L, order, locks, i, e, x, keyPair, flags);
+    pairRow(A, L, order, locks, lc, i, e, x, keyPair, flags);
   if (flags)
     atomicOr(&L.ctr->flags, flags);
 }
@@ -719,7 +792,7 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
 // each group's rows, so a hot element (a lock word, a histogram bin) is
 // spread over the whole GPU.
 __global__ void k_detect_pairwise_big(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
-                                      const uint32_t *order, bool locks,
+                                      const uint32_t *order, bool locks, const LockC *lc,
                                       unsigned long long *keyPair) {
   const unsigned nBig = min(*A.hotCount, A.hotCap);
   unsigned flags = 0;
@@ -731,7 +804,7 @@ __global__ void k_detect_pairwise_big(DetectArgs A, LaunchDev L, const uint64_t 
       ++e;
     for (uint64_t x = i + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < e;
          x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-      pairRow(A, L, order, locks, i, e, x, keyPair, flags);
+      pairRow(A, L, order, locks, lc, i, e, x, keyPair, flags);
   }
   if (flags)
     atomicOr(&L.ctr->flags, flags);

@@ -616,8 +616,8 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       NEED(c->keyPair, static_cast<size_t>(nKeys));
       CK(cudaMemsetAsync(c->keyPair.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
       {
-        const uint32_t bigCap = 1u << 16;
-        NEED(c->hot, bigCap + 1);
+        const uint32_t bigCap = 1u << 16; // (group start, end) pairs
+        NEED(c->hot, 2 * bigCap + 1);
         CK(cudaMemsetAsync(c->hot.p, 0, sizeof(uint32_t), c->st));
         A.hotCount = c->hot.p;
         A.hotList = c->hot.p + 1;

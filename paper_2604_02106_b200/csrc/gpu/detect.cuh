@@ -777,7 +777,8 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
   if (e - i > kPairBig && A.hotList) { // a large group: all CTAs of k_detect_pairwise_big
     const unsigned slot = atomicAdd(A.hotCount, 1u);
     if (slot < A.hotCap) {
-      A.hotList[slot] = static_cast<uint32_t>(i);
+      A.hotList[2 * slot] = static_cast<uint32_t>(i);
+      A.hotList[2 * slot + 1] = static_cast<uint32_t>(e);
       return;
     }
   }
@@ -788,23 +789,131 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
     atomicOr(&L.ctr->flags, flags);
 }
 
-// The large groups listed by k_detect_pairwise: every CTA takes a share of
-// each group's rows, so a hot element (a lock word, a histogram bin) is
-// spread over the whole GPU.
-__global__ void k_detect_pairwise_big(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
-                                      const uint32_t *order, bool locks, const LockC *lc,
-                                      unsigned long long *keyPair) {
+// The large groups listed by k_detect_pairwise, tiled like an n-body pass:
+// a work item is (row chunk, column tile) of one group, 256 events each;
+// the tile is decoded once into shared memory and every thread tests its
+// row event against it, so a hot element (a lock word, a histogram bin, a
+// shared counter) is spread over the whole GPU and each pair costs shared
+// memory reads only.  Work items of a group are numbered column-tile major
+// (tile t holds t + 1 row chunks).
+struct EvT {
+  unsigned long long thread;
+  uint32_t block, warp, bp, wp;
+  int32_t seq, loc;
+  uint16_t site;
+  uint8_t kind, scope;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ EvT loadEvT(const DetectArgs &A, const uint32_t *order, uint64_t x) {
+  const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
+  const SiteDev sd = A.sites[a.site];
+  EvT t;
+  t.thread = a.thread;
+  t.block = static_cast<uint32_t>(a.block);
+  t.warp = static_cast<uint32_t>(a.warp);
+  t.bp = static_cast<uint32_t>(a.bp);
+  t.wp = static_cast<uint32_t>(a.wp);
+  t.seq = a.seq;
+  t.loc = sd.loc;
+  t.site = static_cast<uint16_t>(a.site);
+  t.kind = sd.kind;
+  t.scope = sd.scope;
+  return t;
+}
+
+__global__ void __launch_bounds__(256) k_detect_pairwise_big(DetectArgs A, LaunchDev L,
+                                                             const uint64_t *elemSorted,
+                                                             const uint32_t *order, bool locks,
+                                                             const LockC *lc,
+                                                             unsigned long long *keyPair) {
+  constexpr int kT = 256;
+  __shared__ EvT tEv[kT];
+  __shared__ LockC tLc[kT];
   const unsigned nBig = min(*A.hotCount, A.hotCap);
+  const int tid = threadIdx.x;
   unsigned flags = 0;
+  uint64_t base = 0; // work items of the groups before this one
   for (unsigned h = 0; h < nBig; ++h) {
-    const uint64_t i = A.hotList[h];
-    const uint64_t elem = elemSorted[i];
-    uint64_t e = i + 1;
-    while (e < A.n && elemSorted[e] == elem)
-      ++e;
-    for (uint64_t x = i + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < e;
-         x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-      pairRow(A, L, order, locks, lc, i, e, x, keyPair, flags);
+    const uint64_t i = A.hotList[2 * h], e = A.hotList[2 * h + 1];
+    const uint64_t g = e - i;
+    const uint64_t nC = (g + kT - 1) / kT;
+    const uint64_t items = nC * (nC + 1) / 2;
+    uint64_t w = base + ((blockIdx.x + gridDim.x - base % gridDim.x) % gridDim.x);
+    for (; w < base + items; w += gridDim.x) {
+      const uint64_t local = w - base;
+      uint64_t tb = static_cast<uint64_t>((sqrt(8.0 * static_cast<double>(local) + 1.0) - 1.0) / 2.0);
+      while (tb * (tb + 1) / 2 > local)
+        --tb;
+      while ((tb + 1) * (tb + 2) / 2 <= local)
+        ++tb;
+      const uint64_t rb = local - tb * (tb + 1) / 2;
+      const uint64_t y0 = i + tb * kT, x = i + rb * kT + tid;
+      const int nTile = e - y0 < static_cast<uint64_t>(kT) ? static_cast<int>(e - y0) : kT;
+      __syncthreads(); // previous item's tile fully read
+      if (tid < nTile) {
+        tEv[tid] = loadEvT(A, order, y0 + tid);
+        if (locks)
+          tLc[tid] = lc[y0 + tid];
+      }
+      __syncthreads();
+      if (x >= e)
+        continue;
+      const EvT a = loadEvT(A, order, x);
+      LockC ca{};
+      if (locks)
+        ca = lc[x];
+      LockInfo la, lb;
+      bool laFull = false;
+      const int jStart = rb == tb ? tid + 1 : 0;
+      for (int j = jStart; j < nTile; ++j) {
+        const EvT &b = tEv[j];
+        if (a.thread == b.thread)
+          continue;
+        if (a.kind == HGRD_SITE_LOAD && b.kind == HGRD_SITE_LOAD)
+          continue;
+        const bool sameBlock = a.block == b.block;
+        if (a.kind == HGRD_SITE_ATOMIC && b.kind == HGRD_SITE_ATOMIC &&
+            covers(a.scope, sameBlock) && covers(b.scope, sameBlock))
+          continue;
+        if (sameBlock && a.bp != b.bp)
+          continue;
+        const bool sameWarp = sameBlock && a.warp == b.warp;
+        if (sameWarp && a.wp != b.wp)
+          continue;
+        if (locks) {
+          bool ordered;
+          const LockC &cb = tLc[j];
+          if (ca.cs[0] != kLockWide && cb.cs[0] != kLockWide) {
+            ordered = crossedC(ca.cs, cb.cs, sameBlock) || crossedC(ca.rel, cb.acq, sameBlock) ||
+                      crossedC(cb.rel, ca.acq, sameBlock);
+          } else {
+            if (!laFull) {
+              lockInfoOf(L, a.thread, a.seq, la, flags);
+              laFull = true;
+            }
+            lockInfoOf(L, b.thread, b.seq, lb, flags);
+            ordered = crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
+                      crossed(lb.rel, la.acq, sameBlock);
+          }
+          if (ordered)
+            continue;
+        }
+        const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
+        int l0 = a.loc, l1 = b.loc;
+        if (l1 < l0) {
+          const int t = l0;
+          l0 = l1;
+          l1 = t;
+        }
+        const int K = (l0 * A.nLocs + l1) * 3 + kind;
+        const unsigned long long packed = (static_cast<unsigned long long>(i) << 40) |
+                                          ((x - i) << 20) | (y0 + j - i);
+        if (keyPair[K] > packed)
+          atomicMin(&keyPair[K], packed);
+      }
+    }
+    base += items;
   }
   if (flags)
     atomicOr(&L.ctr->flags, flags);

@@ -260,3 +260,38 @@ def test_sequential_large(gpu, cpu_oracle, case):
     assert "k_expand_seq[jit]" in names, names
     if case == "trap_last":
         assert got["traps"]
+
+
+# ------------------------------------------------ lock idioms at launch scale
+def _lock_kernel(n, variant):
+    """CAS / fence / critical section / fence / Exch on two lock words with
+    64 shared cells (groups of hundreds of events: the tiled pairwise pass);
+    `block` uses block-scope fences (ordering only within a block), `leak`
+    adds an unprotected write after the release."""
+    fence = "__threadfence_block();" if variant == "block" else "__threadfence();"
+    leak = "  acc[64 + t % 7] = t;\n" if variant == "leak" else ""
+    return ("__global__ void k(int *acc, lock *L) {\n"
+            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+            "  atomicCAS(L[t % 2], 0, 1);\n"
+            f"  {fence}\n"
+            "  acc[t % 64] = acc[t % 64] + t;\n"
+            f"  {fence}\n"
+            "  atomicExch(L[t % 2], 0);\n"
+            f"{leak}"
+            "}\n"
+            f"void main() {{ int *acc; lock *L; cudaMalloc(&acc, 128); cudaMalloc(&L, 2);\n"
+            f"  k<<<({n // 256},1,1),(256,1,1)>>>(acc, L); }}\n")
+
+
+@pytest.mark.parametrize("variant", ["device", "block", "leak"])
+@pytest.mark.parametrize("n", [4096, 16384])
+def test_lock_kernels_large(gpu, cpu_oracle, n, variant):
+    """Lock-idiom launches with element groups far above the per-thread
+    pairwise limit: k_lock_info + the tiled k_detect_pairwise_big against
+    the CPU restatement of lockInfo / lockOrdered / detectRaces."""
+    src = _lock_kernel(n, variant)
+    cfg = programs.synthetic_config()
+    got = gpu.run_concrete(src, cfg, "lk.mcu")
+    want = cpu_oracle.run_concrete(src, cfg, "lk.mcu")
+    assert strip_extras(got) == strip_extras(want), (got, want)
+    assert got["witnesses"] == want["witnesses"]

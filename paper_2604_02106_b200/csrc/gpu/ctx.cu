@@ -38,6 +38,35 @@ __global__ void k_elem_keys(const uint64_t *keys, uint64_t n, int shE, uint64_t 
   }
 }
 
+// the same with the canonical event order below the element: element |
+// thread | seq (sentinel padding records keep an all-ones element)
+__global__ void k_elem_keys_canon(const uint64_t *keys, const uint32_t *vals, uint64_t n,
+                                  KeyLayout kl, int64_t tpb, int64_t ws, int bT, int bS,
+                                  uint64_t *elem, uint32_t *order) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n)
+    return;
+  order[i] = static_cast<uint32_t>(i);
+  const uint64_t k = keys[i];
+  if (k == kl.sentinel) { // chunk padding: the all-ones element, sorts last
+    elem[i] = (fieldMask(kl.bE) << (bT + bS)) | fieldMask(bT + bS);
+    return;
+  }
+  const uint64_t e = kl.shE >= 64 ? 0 : k >> kl.shE;
+  const uint64_t block = (k >> kl.shB) & fieldMask(kl.bB);
+  const uint64_t warp = (k >> kl.shW) & fieldMask(kl.bW);
+  const uint64_t lane = k & fieldMask(kl.bL);
+  const uint64_t thread =
+      block * static_cast<uint64_t>(tpb) + warp * static_cast<uint64_t>(ws) + lane;
+  elem[i] = (e << (bT + bS)) | (thread << bS) | (vals[i] & kSeqMask);
+}
+
+__global__ void k_shift_keys(uint64_t *x, uint64_t n, int sh) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n)
+    x[i] >>= sh;
+}
+
 namespace {
 
 template <class T> struct DevVec {
@@ -603,16 +632,33 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
       NEED(c->order, n);
       NEED(c->orderAlt, n);
       const unsigned g = static_cast<unsigned>((n + 255) / 256);
-      k_elem_keys<<<g, 256, 0, c->st>>>(c->keys.p, n, D.kl.shE, c->elemK.p, c->order.p);
+      // PARALLEL lock launches (D.opStride): records arrive in chunk order,
+      // so the sort key carries the canonical order too (element | thread |
+      // seq), shifted back to the element afterwards
+      const int canonBits = D.opStride ? bitsFor(static_cast<uint64_t>(D.nThreads)) +
+                                             bitsFor(L.n_code + 1)
+                                       : 0;
+      if (canonBits)
+        k_elem_keys_canon<<<g, 256, 0, c->st>>>(
+            c->keys.p, c->vals.p, n, D.kl, D.tpb, D.ws,
+            bitsFor(static_cast<uint64_t>(D.nThreads)), bitsFor(L.n_code + 1), c->elemK.p,
+            c->order.p);
+      else
+        k_elem_keys<<<g, 256, 0, c->st>>>(c->keys.p, n, D.kl.shE, c->elemK.p, c->order.p);
       CK(cudaGetLastError());
       cub::DoubleBuffer<uint64_t> dk(c->elemK.p, c->elemKAlt.p);
       cub::DoubleBuffer<uint32_t> dv(c->order.p, c->orderAlt.p);
       size_t tb = 0;
+      const int sortBits = std::max(D.kl.bE, 1) + canonBits;
       CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, static_cast<int64_t>(n), 0,
-                                         std::max(D.kl.bE, 1), c->st));
+                                         sortBits, c->st));
       NEED(c->cubTemp, tb);
       CK(cub::DeviceRadixSort::SortPairs(c->cubTemp.p, tb, dk, dv, static_cast<int64_t>(n), 0,
-                                         std::max(D.kl.bE, 1), c->st));
+                                         sortBits, c->st));
+      if (canonBits) {
+        k_shift_keys<<<g, 256, 0, c->st>>>(dk.Current(), n, canonBits);
+        CK(cudaGetLastError());
+      }
       NEED(c->keyPair, static_cast<size_t>(nKeys));
       CK(cudaMemsetAsync(c->keyPair.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
       {
@@ -1205,7 +1251,19 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
 
   const bool locks = (L.flags & HGRD_LAUNCH_PAIRWISE) != 0;
   const bool pairwise = locks || !P.summaryOk;
-  bool seq = (L.flags & HGRD_LAUNCH_SEQUENTIAL) || pairwise || L.n_regs > kMaxRegs;
+  // Lock idioms in a PARALLEL launch: loop-free threads have a static op
+  // count (fixed op slots per thread) and at most kLaneBuf records (kept in
+  // program order), and the canonical sort key (element | thread | seq)
+  // must fit 64 bits
+  uint32_t opsPerThread = 0;
+  for (uint32_t pc = 0; pc < L.n_code; ++pc)
+    opsPerThread += L.code[pc].op == HGRD_OP_ATOMIC || L.code[pc].op == HGRD_OP_FENCE;
+  const int canonBits = bitsFor(static_cast<uint64_t>(D.nThreads)) + bitsFor(L.n_code + 1);
+  const bool parLocks = locks && !loops && recInsns <= static_cast<uint32_t>(kLaneBuf) &&
+                        opsPerThread > 0 && bE + canonBits <= 64 &&
+                        static_cast<uint64_t>(D.nThreads) * opsPerThread < (uint64_t(1) << 32);
+  bool seq = (L.flags & HGRD_LAUNCH_SEQUENTIAL) || (pairwise && !parLocks) ||
+             L.n_regs > kMaxRegs;
   // (the interpreter keeps at most kMaxRegs registers per lane)
   const size_t smem = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
                       sizeof(ParamDev) * P.params.size();
@@ -1256,6 +1314,19 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       D.keys = c->keys.p;
       D.vals = c->vals.p;
       D.capacity = cap;
+      D.opStart = nullptr;
+      D.opStride = 0;
+      if (parLocks) {
+        const size_t nOps = static_cast<size_t>(D.nThreads) * opsPerThread;
+        NEED(c->opIndex, nOps);
+        NEED(c->opMeta, nOps);
+        NEED(c->opSeq, nOps);
+        D.opIndex = c->opIndex.p;
+        D.opMeta = c->opMeta.p;
+        D.opSeq = c->opSeq.p;
+        D.opCap = nOps;
+        D.opStride = opsPerThread;
+      }
       const void *jx = jk.get(hgrdgpu::jit::kExpandPar);
       rc = launchExpandPar(c, D, static_cast<unsigned>(blocks), smem, jx,
                            jx ? "k_expand_par[jit]" : "k_expand_par");
@@ -1283,15 +1354,20 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
         c->err = "more than 2^20 accesses in one thread";
         return HGRD_GPU_ENOTSUP;
       }
+      if (h.flags & kFlagOps) { // (cannot happen: static op count)
+        seq = true;
+        continue;
+      }
       R->steps = static_cast<int64_t>(h.steps);
       R->instances = h.instances;
       R->records = h.records;
       R->mode = L.flags & ~HGRD_LAUNCH_SEQUENTIAL;
-      rc = detect(c, L, D, o, std::min<uint64_t>(h.cursor, cap), false, false, R);
+      rc = detect(c, L, D, o, std::min<uint64_t>(h.cursor, cap), parLocks, parLocks, R);
       if (rc < 0)
         return rc;
       break;
     }
+    D.opStride = 0;
     // SEQUENTIAL: kernel loads and stores read and write every parameter buffer
     for (uint32_t p = 0; p < L.n_params; ++p)
       if (L.param_handle[p] >= 0 && static_cast<size_t>(L.param_handle[p]) < c->bufs.size() &&

@@ -560,7 +560,9 @@ struct LockInfo {
 __device__ void lockInfoOf(const LaunchDev &L, uint64_t thread, int32_t seq,
                            LockInfo &li, unsigned &flags) {
   li.acq.n = li.rel.n = li.cs.n = 0;
-  const uint64_t b = L.opStart[thread], e = L.opStart[thread + 1];
+  // (PARALLEL launches: fixed slots per thread, unused ones kind 15)
+  const uint64_t b = L.opStride ? thread * L.opStride : L.opStart[thread];
+  const uint64_t e = L.opStride ? b + L.opStride : L.opStart[thread + 1];
   for (uint64_t f = b; f < e; ++f) {
     const int32_t mf = L.opMeta[f];
     if ((mf & 15) != 2)
@@ -730,7 +732,7 @@ __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
 // was the pairwise pass's dominant cost on lock kernels.
 __global__ void k_lock_info(DetectArgs A, LaunchDev L, const uint32_t *order, LockC *out) {
   const uint64_t x = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= A.n)
+  if (x >= A.n || A.keys[order[x]] == A.kl.sentinel)
     return;
   const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
   LockInfo li;
@@ -753,6 +755,8 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
   const uint64_t elem = elemSorted[i];
   if (i > 0 && elemSorted[i - 1] == elem)
     return;
+  if (elem == fieldMask(A.kl.bE))
+    return; // chunk padding of PARALLEL records (never a valid element)
   uint64_t e = i + 1;
   while (e < A.n && elemSorted[e] == elem)
     ++e;

@@ -139,6 +139,7 @@ struct LaunchDev {
   int32_t *opSeq;
   uint64_t opCap;
   uint64_t *opStart;         // nThreads + 1
+  uint32_t opStride;         // PARALLEL lock launches: ops at thread * opStride (no opStart)
   // pass 2 of the fused path: only elements the ownership table marks MULTI
   const uint32_t *ownerFilter;
   uint32_t ownerMultiTag;

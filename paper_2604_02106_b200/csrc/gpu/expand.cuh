@@ -178,6 +178,33 @@ __global__ void k_inter_scan_minmax(const uint32_t *lo, const uint32_t *hi, uint
 // PARALLEL sink of k_expand_par: packed records into the lane buffer.
 struct ParSink : ParState {
   LaneRecords *out;
+  int64_t t = 0;     // global thread (lock launches: op slots)
+  uint32_t nOps = 0; // sync ops pushed by this thread
+
+  // PARALLEL lock launches (L->opStride > 0): CAS / Exch / fence ops in the
+  // thread's fixed slots, as SeqSink::op does in canonical order (:601-618)
+  __device__ __forceinline__ void opPush(int kind, int scope, int handle, int64_t idx,
+                                         uint32_t s) {
+    if (nOps < L->opStride) {
+      const uint64_t slot = static_cast<uint64_t>(t) * L->opStride + nOps;
+      L->opMeta[slot] = kind | (scope << 4) | ((handle + 1) << 8);
+      L->opIndex[slot] = idx;
+      L->opSeq[slot] = static_cast<int32_t>(s);
+    } else {
+      flags |= kFlagOps;
+    }
+    ++nOps;
+  }
+  __device__ __forceinline__ void atomicOp(int site, int param, int64_t idx) {
+    const SiteDev &S = sites[site];
+    if (S.aop != HGRD_ATOMIC_ADD)
+      opPush(S.aop == HGRD_ATOMIC_CAS ? 0 : 1, S.scope, params[param].handle, idx, seq - 1);
+  }
+  __device__ __forceinline__ void fence(int scope) {
+    if (L->opStride)
+      opPush(2, scope, -1, 0, seq);
+    ++seq;
+  }
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx) {
     recordE(site, P->elemBase + static_cast<uint64_t>(idx), sites[site].own != 0);
@@ -258,6 +285,8 @@ struct ParSink : ParState {
   __device__ __forceinline__ void atomicC(int site, int param, bool rec, bool own, I idx,
                                           int64_t, int64_t, int64_t size, uint64_t base) {
     loadC(site, param, rec, own, idx, false, size, base);
+    if (L->opStride && !outOfRange(idx, size))
+      atomicOp(site, param, static_cast<int64_t>(idx));
   }
   // K variants: the site's parameter and record flag as (JIT) constants
   __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, bool, int64_t idx,
@@ -281,7 +310,10 @@ struct ParSink : ParState {
   }
   __device__ __forceinline__ void atomicK(int site, int param, bool rec, bool own, int64_t idx,
                                           int64_t, int64_t) {
+    const unsigned long long before = inst;
     storeK(site, param, rec, own, idx, 0);
+    if (L->opStride && inst != before) // in bounds
+      atomicOp(site, param, idx);
   }
   __device__ __forceinline__ int64_t load(int site, int64_t idx, bool need) {
     return loadK(site, sites[site].param, sites[site].record, false, idx, need);
@@ -323,9 +355,12 @@ template <class Body> __global__ void __launch_bounds__(256) k_expand_par(Launch
       s.sites = sSites;
       s.params = sParams;
       s.out = &out;
+      s.t = t;
       Builtins bi;
       Body::identity(L, t, bi, s.block, s.warp, s.lane);
       Body::run(L, sCode, bi, s, regs);
+      for (uint32_t j = s.nOps; j < L.opStride; ++j) // unused op slots
+        L.opMeta[static_cast<uint64_t>(t) * L.opStride + j] = 15;
       tally.add(s);
     }
     __syncwarp();

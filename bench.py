@@ -315,6 +315,59 @@ def run_gpu_arm(args):
         torch.distributed.destroy_process_group()
 
 
+def run_paths(args):
+    """--paths: the other GPU paths against the unmodified reference
+    (hgrd::runConcrete / enumerateVerdict from oracle/_ref) on side
+    workloads, one JSON line each (device wall clock through the public
+    API; reports compared field by field).  Opt-in: the reference needs
+    ~40 s of host time here."""
+    import paper_2604_02106_b200 as hg
+    from conftest import load_golden
+    from oracles import RefOracle, REF_LIB, strip_extras
+    if not os.path.exists(REF_LIB):
+        print(json.dumps({"paths": "unavailable", "why": f"{REF_LIB} not built"}))
+        return
+    ctx, ref = hg.GpuContext(0), RefOracle()
+    cfg = programs.synthetic_config()
+
+    def timed(fn, reps):
+        fn()  # warm (NVRTC cache, arena)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts) * 1e3, out
+
+    n = 1 << 16
+    for name, src, mode in (
+            (f"locks_{n}threads", programs.lock_kernel(n, "leak"), "PARALLEL + pairwise lockInfo"),
+            (f"sequential_chain_{n}threads", programs.chain_kernel(n, n + 1),
+             "SEQUENTIAL (canonical order, NVRTC body)")):
+        g_ms, g = timed(lambda: ctx.run_concrete(src, cfg, "paths.mcu"), 3)
+        t0 = time.perf_counter()
+        r = ref.run_concrete(src, cfg, "paths.mcu")
+        r_ms = (time.perf_counter() - t0) * 1e3
+        print(json.dumps({"workload": name, "mode": mode, "gpu_ms": g_ms, "reference_ms": r_ms,
+                          "reference_threads": 1,
+                          "same_report": strip_extras(g) == strip_extras(r),
+                          "instances": g["stats"]["instances"], "races": len(g["races"])}),
+              flush=True)
+    corpus = load_golden("corpus")
+    sweep = lambda: [ctx.enumerate_verdict(e["source"], e["caps"], e["file"])  # noqa: E731
+                     for e in corpus]
+    g_ms, g = timed(sweep, 3)
+    t0 = time.perf_counter()
+    r = [ref.enumerate_verdict(e["source"], e["caps"], e["file"]) for e in corpus]
+    r_ms = (time.perf_counter() - t0) * 1e3
+    print(json.dumps({"workload": "corpus_sweep_29_entries_manifest_caps",
+                      "mode": "enumerateVerdict, 8 worker contexts", "gpu_ms": g_ms,
+                      "reference_ms": r_ms, "reference_threads": 1,
+                      "same_report": [strip_extras(x) for x in g] == [strip_extras(x) for x in r]}),
+          flush=True)
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -322,8 +375,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--paths", action="store_true",
+                    help="time the lock-idiom, SEQUENTIAL and sweep paths against the reference")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.paths:
+        run_paths(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_gpu_arm(args)

@@ -252,3 +252,37 @@ EDGE_CONFIGS = [
     {"warpSize": 1, "inputs": [0], "gridCap": [2, 4, 2], "blockCap": [4, 2, 2]},
     {"warpSize": 3, "inputs": [2, 2], "gridCap": [2, 4, 2], "blockCap": [4, 2, 2]},
 ]
+
+
+def chain_kernel(n, a_elems):
+    """Each thread reads what the previous one stored (value-relevant loads:
+    canonical order, k_expand_seq); with a_elems == n the last thread's
+    store is out of bounds (a trap in canonical order)."""
+    return ("__global__ void k(int *A, int *B) {\n"
+            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+            "  int v = A[t];\n"
+            f"  B[(v + t) % {n}] = t;\n"
+            "  A[t + 1] = v + 1;\n"
+            "}\n"
+            f"void main() {{ int *A; int *B; cudaMalloc(&A, {a_elems}); cudaMalloc(&B, {n});\n"
+            f"  k<<<({n // 256},1,1),(256,1,1)>>>(A, B); }}\n")
+
+
+def lock_kernel(n, variant):
+    """CAS / fence / critical section / fence / Exch on two lock words with
+    64 shared cells (groups of hundreds of events: the tiled pairwise pass);
+    `block` uses block-scope fences (ordering only within a block), `leak`
+    adds an unprotected write after the release."""
+    fence = "__threadfence_block();" if variant == "block" else "__threadfence();"
+    leak = "  acc[64 + t % 7] = t;\n" if variant == "leak" else ""
+    return ("__global__ void k(int *acc, lock *L) {\n"
+            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+            "  atomicCAS(L[t % 2], 0, 1);\n"
+            f"  {fence}\n"
+            "  acc[t % 64] = acc[t % 64] + t;\n"
+            f"  {fence}\n"
+            "  atomicExch(L[t % 2], 0);\n"
+            f"{leak}"
+            "}\n"
+            f"void main() {{ int *acc; lock *L; cudaMalloc(&acc, 128); cudaMalloc(&L, 2);\n"
+            f"  k<<<({n // 256},1,1),(256,1,1)>>>(acc, L); }}\n")

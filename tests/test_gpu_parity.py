@@ -225,27 +225,13 @@ def test_full_histogram_2p27(gpu, cpu_oracle, bins, update):
 
 
 # ------------------------------------------------- SEQUENTIAL at launch scale
-def _chain(n, a_elems):
-    """Each thread reads what the previous one stored (value-relevant loads:
-    canonical order, k_expand_seq); with a_elems == n the last thread's
-    store is out of bounds (a trap in canonical order)."""
-    return ("__global__ void k(int *A, int *B) {\n"
-            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
-            "  int v = A[t];\n"
-            f"  B[(v + t) % {n}] = t;\n"
-            "  A[t + 1] = v + 1;\n"
-            "}\n"
-            f"void main() {{ int *A; int *B; cudaMalloc(&A, {a_elems}); cudaMalloc(&B, {n});\n"
-            f"  k<<<({n // 256},1,1),(256,1,1)>>>(A, B); }}\n")
-
-
 @pytest.mark.parametrize("case", ["clean_bounds", "trap_last", "budget"])
 def test_sequential_large(gpu, cpu_oracle, case):
     """A 2^16-thread SEQUENTIAL launch through the NVRTC canonical-order body
     (k_expand_seq[jit]): races, traps and the step-budget abort equal the
     CPU restatement's."""
     n = 1 << 16
-    src = _chain(n, n if case == "trap_last" else n + 1)
+    src = programs.chain_kernel(n, n if case == "trap_last" else n + 1)
     cfg = programs.synthetic_config(**({"maxSteps": 200000} if case == "budget" else {}))
     gpu.set_profiling(True)
     try:
@@ -263,33 +249,13 @@ def test_sequential_large(gpu, cpu_oracle, case):
 
 
 # ------------------------------------------------ lock idioms at launch scale
-def _lock_kernel(n, variant):
-    """CAS / fence / critical section / fence / Exch on two lock words with
-    64 shared cells (groups of hundreds of events: the tiled pairwise pass);
-    `block` uses block-scope fences (ordering only within a block), `leak`
-    adds an unprotected write after the release."""
-    fence = "__threadfence_block();" if variant == "block" else "__threadfence();"
-    leak = "  acc[64 + t % 7] = t;\n" if variant == "leak" else ""
-    return ("__global__ void k(int *acc, lock *L) {\n"
-            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
-            "  atomicCAS(L[t % 2], 0, 1);\n"
-            f"  {fence}\n"
-            "  acc[t % 64] = acc[t % 64] + t;\n"
-            f"  {fence}\n"
-            "  atomicExch(L[t % 2], 0);\n"
-            f"{leak}"
-            "}\n"
-            f"void main() {{ int *acc; lock *L; cudaMalloc(&acc, 128); cudaMalloc(&L, 2);\n"
-            f"  k<<<({n // 256},1,1),(256,1,1)>>>(acc, L); }}\n")
-
-
 @pytest.mark.parametrize("variant", ["device", "block", "leak"])
 @pytest.mark.parametrize("n", [4096, 16384])
 def test_lock_kernels_large(gpu, cpu_oracle, n, variant):
     """Lock-idiom launches with element groups far above the per-thread
     pairwise limit: k_lock_info + the tiled k_detect_pairwise_big against
     the CPU restatement of lockInfo / lockOrdered / detectRaces."""
-    src = _lock_kernel(n, variant)
+    src = programs.lock_kernel(n, variant)
     cfg = programs.synthetic_config()
     got = gpu.run_concrete(src, cfg, "lk.mcu")
     want = cpu_oracle.run_concrete(src, cfg, "lk.mcu")

@@ -757,10 +757,19 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   __threadfence();
   const unsigned nc = min(atomicAdd(F.candCount, 0u), F.candCap);
   const int wid = tid >> 5;
-  for (int K = wid; K < F.nKeys; K += kFusedThreads / 32) {
+  // realised keys first, all threads at once (one load latency instead of
+  // one per key and warp: this is the kernel's serial tail), listed in sReal
+  __shared__ unsigned sFinN;
+  if (tid == 0)
+    sFinN = 0;
+  __syncthreads();
+  for (int K = tid; K < F.nKeys; K += kFusedThreads)
+    if (__ldcg(&F.keyElem[K]) != ~0ull)
+      sReal[atomicAdd(&sFinN, 1u)] = static_cast<uint32_t>(K);
+  __syncthreads();
+  for (unsigned r = wid; r < sFinN; r += kFusedThreads / 32) {
+    const int K = static_cast<int>(sReal[r]);
     const unsigned long long e = __ldcg(&F.keyElem[K]);
-    if (e == ~0ull)
-      continue;
     uint64_t x = ~0ull, y = ~0ull;
     int sx = 0, sy = 0;
     for (unsigned c = lane; c < nc; c += 32) {

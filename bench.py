@@ -365,7 +365,47 @@ def run_paths(args):
                       "reference_ms": r_ms, "reference_threads": 1,
                       "same_report": [strip_extras(x) for x in g] == [strip_extras(x) for x in r]}),
           flush=True)
+    # config 5: the launch-config sweep -- every corpus program over a
+    # 10-value input set plus the reference's 200 soundness-fuzz programs
+    # (tests/test_soundness.cpp:80-84), warp sizes {2,4,8,16,32}
+    jobs = sweep_jobs(corpus, load_golden("fuzz"))
+    n_cfg = sum(j["configs"] for j in jobs)
+    sweep = lambda: [ctx.enumerate_verdict(j["source"], j["caps"], j["file"])  # noqa: E731
+                     for j in jobs]
+    g_ms, g = timed(sweep, 3)
+    t0 = time.perf_counter()
+    r = [ref.enumerate_verdict(j["source"], j["caps"], j["file"]) for j in jobs]
+    r_ms = (time.perf_counter() - t0) * 1e3
+    print(json.dumps({"workload": f"config5_sweep_{len(jobs)}programs_{n_cfg}configs",
+                      "mode": "enumerateVerdict, 8 worker contexts", "gpu_ms": g_ms,
+                      "reference_ms": r_ms, "reference_threads": 1,
+                      "gpu_configs_per_s": n_cfg / g_ms * 1e3,
+                      "reference_configs_per_s": n_cfg / r_ms * 1e3,
+                      "same_report": [strip_extras(x) for x in g] == [strip_extras(x) for x in r]}),
+          flush=True)
     ctx.close()
+
+
+SWEEP_INPUTS = [-1, 0, 1, 2, 3, 4, 7, 16, 127, 255]
+SWEEP_WARPS = [2, 4, 8, 16, 32]
+
+
+def sweep_jobs(corpus, fuzz):
+    """BASELINE config 5's job list: (program, SweepCaps) with the number
+    of configurations each enumerates (|inputSet|^inputs x |warpSizes|)."""
+    import paper_2604_02106_b200 as hg
+    jobs = []
+    for e in corpus:
+        caps = dict(e["caps"], inputSet=SWEEP_INPUTS, warpSizes=SWEEP_WARPS)
+        k = hg.count_inputs(e["source"], e["file"])
+        jobs.append({"source": e["source"], "file": e["file"], "caps": caps,
+                     "configs": len(SWEEP_INPUTS) ** k * len(SWEEP_WARPS)})
+    for f in fuzz:
+        k = hg.count_inputs(f["source"], "fuzz.mcu")
+        jobs.append({"source": f["source"], "file": "fuzz.mcu",
+                     "caps": {"warpSizes": SWEEP_WARPS},
+                     "configs": 5 ** k * len(SWEEP_WARPS)})
+    return jobs
 
 
 def main():

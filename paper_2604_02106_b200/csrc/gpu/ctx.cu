@@ -161,6 +161,8 @@ struct hgrd_gpu_ctx {
   unsigned char *hResult = nullptr; // pinned: counters + races
   size_t hResultCap = 0;
   hgrd_gpu_race *hRaces = nullptr; // pinned copy of the device race array
+  hgrd_gpu_trap *hTraps = nullptr; // pinned: traps read with the counters
+  size_t hTrapsCap = 0;
   size_t hRacesCap = 0;
   bool racesOnHost = false;
   hgrd_gpu_race *hRacesView = nullptr;
@@ -525,6 +527,28 @@ int readCountersAndRaces(hgrd_gpu_ctx *c, size_t nKeys) {
   return 0;
 }
 
+// Counters and (speculatively) the first `trapCap` trap slots in one round
+// trip: a SEQUENTIAL launch needs both, and tiny sweep launches are bound by
+// round trips.
+int readCountersAndTraps(hgrd_gpu_ctx *c, size_t trapCap) {
+  if (c->hTrapsCap < trapCap) {
+    if (c->hTraps)
+      CK(cudaFreeHost(c->hTraps));
+    c->hTraps = nullptr;
+    CK(cudaMallocHost(&c->hTraps, sizeof(hgrd_gpu_trap) * trapCap));
+    c->hTrapsCap = trapCap;
+  }
+  CK(cudaMemcpyAsync(c->hCtr, c->cur, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hTraps, c->traps.p, sizeof(hgrd_gpu_trap) * trapCap,
+                     cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += sizeof(Counters) + sizeof(hgrd_gpu_trap) * trapCap;
+  if (c->timing) // the check's end event, when nothing follows (see e1AtSync)
+    CK(cudaEventRecord(c->e1, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->e1AtSync = c->timing;
+  return 0;
+}
+
 int readCounters(hgrd_gpu_ctx *c) {
   CK(cudaMemcpyAsync(c->hCtr, c->cur, sizeof(Counters), cudaMemcpyDeviceToHost, c->st));
   c->d2hBytes += sizeof(Counters);
@@ -560,6 +584,14 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
            bool append = false) {
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
+  if (n <= 1 && !append) {
+    // fewer than two records hold no pair (detectRaces needs x < y in one
+    // element group): no detect kernels, no read-back round trip -- tiny
+    // sweep launches are bound by these round trips
+    c->racesOnHost = false;
+    R->n_races = 0;
+    return 0;
+  }
   if (!append)
     CK(cudaMemsetAsync(&c->cur->nRaces, 0, sizeof(unsigned), c->st));
   DetectArgs A = detectArgs(c, L, D, o, n, kindMask);
@@ -1444,7 +1476,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     }
     CK(cudaGetLastError());
     ++c->kernelLaunches;
-    rc = readCounters(c);
+    rc = readCountersAndTraps(c, std::max<uint32_t>(R->trap_cap, 1));
     if (rc < 0)
       return rc;
     const Counters h = *c->hCtr;
@@ -1471,12 +1503,8 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
         return HGRD_GPU_ENOTSUP;
       }
     }
-    if (nt) {
-      CK(cudaMemcpyAsync(R->traps, c->traps.p, sizeof(hgrd_gpu_trap) * nt,
-                         cudaMemcpyDeviceToHost, c->st));
-      c->d2hBytes += sizeof(hgrd_gpu_trap) * nt;
-      CK(cudaStreamSynchronize(c->st));
-    }
+    if (nt) // (read with the counters)
+      std::memcpy(R->traps, c->hTraps, sizeof(hgrd_gpu_trap) * nt);
     R->n_traps = nt;
     R->n_traps_total = h.traps;
     R->steps = static_cast<int64_t>(h.steps);
@@ -1491,6 +1519,8 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
     rc = detect(c, L, D, o, h.cursor, pairwise, locks, R);
     if (rc < 0)
       return rc;
+    if (h.cursor <= 1) // no GPU work since the counters' synchronisation
+      c->e1Done = c->e1AtSync;
     break;
   }
 finish:
@@ -1871,6 +1901,8 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
     cudaFreeHost(c->hCtr);
   if (c->hRaces)
     cudaFreeHost(c->hRaces);
+  if (c->hTraps)
+    cudaFreeHost(c->hTraps);
   if (c->hResult)
     cudaFreeHost(c->hResult);
   hgrdgpu::jit::destroy(c->jit);

@@ -145,6 +145,7 @@ struct hgrd_gpu_ctx {
   bool hostTrace = std::getenv("HGRD_HOST_TRACE") != nullptr;
   bool e1AtSync = false; // e1 recorded at readCountersAndRaces' synchronisation
   bool e1Done = false;   // ... and no GPU work since: the check's end
+  bool fusedOrdered = false; // the fused attempt saw traps / the step budget
   std::vector<std::pair<const char *, std::chrono::steady_clock::time_point>> trace;
   hgrdgpu::jit::Cache *jit = nullptr;
   std::string jitErr;
@@ -845,6 +846,7 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *ji
 int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobOffsets &o,
              const Plan &P, hgrd_gpu_result *R, uint32_t recInsns, bool loops,
              JitGetter &jk, int64_t b0 = 0, int64_t b1 = -1, bool shard = false) {
+  c->fusedOrdered = false;
   if (b1 < 0)
     b1 = D.nBlocks;
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
@@ -916,8 +918,11 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     return rc;
   htrace(c, "counters");
   const Counters h = *c->hCtr;
-  if ((h.flags & (kFlagAbort | kFlagFusedOverflow)) || h.traps > 0 ||
-      static_cast<int64_t>(h.steps) > L.step_budget)
+  // traps and the step budget need the canonical order: the PARALLEL
+  // expansion would see the same counts, so the caller goes SEQUENTIAL
+  c->fusedOrdered = (h.flags & kFlagAbort) || h.traps > 0 ||
+                    static_cast<int64_t>(h.steps) > L.step_budget;
+  if (c->fusedOrdered || (h.flags & kFlagFusedOverflow))
     return 0;
   R->steps = static_cast<int64_t>(h.steps);
   R->instances = h.instances;
@@ -1323,6 +1328,8 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       return rc;
     if (rc == 1)
       goto finish;
+    if (c->fusedOrdered)
+      seq = true; // (one round trip less than finding it again in k_expand_par)
   }
 
   for (int attempt = 0; attempt < 16; ++attempt) {

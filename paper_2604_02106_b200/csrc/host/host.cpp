@@ -1397,7 +1397,9 @@ int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &work
   std::string fileName = po.program->file;
   auto cp = compileProgram(std::move(po.program));
   const uint64_t size = sweepSize(*cp, caps);
-  int use = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(std::max(n, 1)), size / 4));
+  // one configuration per worker at least: a configuration costs a few
+  // GPU round trips (~30 us each), more than spawning its worker thread
+  int use = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(std::max(n, 1)), size));
   std::vector<LaunchBackend *> bes;
   for (int i = 0; i < std::max(use, 1); ++i) {
     LaunchBackend *b = workers(i);

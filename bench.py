@@ -41,16 +41,207 @@ import numpy as np  # noqa: E402
 
 import programs  # noqa: E402
 
-N_THREADS = 1 << 20
-BLOCK = 256
-WS = 32
-INST_PER_THREAD = 5
-B_ALG = 32  # algorithmic bytes per instance
-SAMPLE_THREADS = 1 << 16  # CPU reference sample (per host thread, per step)
-CPU_BASELINE_REPS = 24    # cpu_baseline leg of the GPU arm: ~10 s of reference work
 METRIC = "access instances race-checked/sec"
 UNIT = "instances/s"
-WORKLOAD = "stencil1d_2^20threads_block256_ws32_missing+fixed"
+
+
+# ----------------------------------------------------------------- workloads
+class Workload:
+    """One BASELINE.json config as bench steps: `launches` are checked once
+    per step (every variant of the config); `b_alg` is SURVEY.md §8(d)'s
+    algorithmic bytes per instance; `cpu_sample` gives the reference CPU
+    sample (sources with the launch, and the same host code without it so the
+    host-side init loop can be subtracted)."""
+
+    name = ""
+    config_index = 0
+    b_alg = 32
+    e2e_api = "hgrd_gpu_buffer_write + hgrd_gpu_check_launch"
+
+    def variants(self):
+        raise NotImplementedError
+
+
+def _no_launch(src: str) -> str:
+    """The same program without its kernel launch (host work only)."""
+    lines = src.splitlines(keepends=True)
+    out = []
+    for ln in lines:
+        if "<<<" in ln:
+            head, tail = ln.split("<<<", 1)
+            name = head.split()[-1]
+            head = head[: len(head) - len(name)]
+            ln = head + tail.split(";", 1)[1]
+        out.append(ln)
+    return "".join(out)
+
+
+class Histogram(Workload):
+    """configs[3]: global-memory histogram with data-dependent bins, 2^27
+    MiniCU threads (2^28 instances per launch: the indexed load of data[t]
+    and one update), bins 2^16 (hot, 2048 threads per bin) or 2^24; one
+    step checks the three update variants of SURVEY §8(d) row 4 — (i)
+    atomicAdd (clean), (ii) atomicAdd_block (INTER-BLOCK), (iii) store
+    (every kind the collisions allow) — over the same 1 GiB data array."""
+
+    config_index = 3
+    b_alg = 36  # 32 B per instance + 8 B per value-consumed load (1 per 2 instances)
+    updates = ("atomic", "atomic_block", "store")
+
+    def __init__(self, n=1 << 27, bins=1 << 16):
+        self.n, self.bins = n, bins
+        self.name = (f"histogram_2^{n.bit_length() - 1}threads_2^{bins.bit_length() - 1}bins_"
+                     f"block256_ws32_atomic+atomic_block+store")
+        self.inst_per_launch = 2 * n
+
+    def program(self, n, upd, host_init):
+        return programs.histogram(n, self.bins, upd, host_init=host_init)
+
+    def data(self, n):
+        return programs.histogram_data(n, self.bins)
+
+    def expected(self, upd):
+        if self.bins & (self.bins - 1) == 0 and self.bins >= 256:
+            return programs.histogram_pow2_expected(self.n, self.bins, upd)
+        return None
+
+    def table(self):
+        return self.bins
+
+    def build(self, hg, ctx, pinned):
+        n = self.n
+        data_h = ctx.alloc(n)
+        table_h = ctx.alloc(self.table())
+        host = pinned(self.data(n))
+        ctx.write(data_h, host)
+        out = []
+        for upd in self.updates:
+            low = hg.lower(self.program(n, upd, False), "h")
+            spec = hg.LaunchSpec(low, (n // 256, 1, 1), (256, 1, 1), 32,
+                                 handles={"data": data_h, "hist": table_h})
+            out.append((upd, spec))
+        self.inputs = [(data_h, host)]
+        return out
+
+    def check(self, upd, res):
+        want = self.expected(upd)
+        if want is not None:
+            got = [(r["kind"], r["address"], r["threadA"], r["threadB"]) for r in res["races"]]
+            assert got == want, (upd, got, want)
+        assert res["instances"] == self.inst_per_launch, res["instances"]
+
+    def cpu_sample(self, sample_n):
+        return [(self.program(sample_n, u, True), _no_launch(self.program(sample_n, u, True)),
+                 2 * sample_n) for u in self.updates]
+
+
+class Permutation(Histogram):
+    """configs[3] permutation-scatter variant: B = n = 2^27 bins, every bin
+    hit once except the injected duplicates (programs.PERM_DUPS)."""
+
+    updates = ("store", "atomic_block")
+
+    def __init__(self, n=1 << 27):
+        self.n = n
+        self.name = f"permutation_scatter_2^{n.bit_length() - 1}threads_block256_ws32_store+atomic_block"
+        self.inst_per_launch = 2 * n
+
+    def program(self, n, upd, host_init):
+        return programs.permutation_scatter(n, upd, host_init=host_init)
+
+    def data(self, n):
+        return programs.permutation_data(n)
+
+    def expected(self, upd):
+        return programs.permutation_expected(self.n, upd)
+
+    def table(self):
+        return self.n
+
+
+class ZeroInit(Workload):
+    """Workloads whose buffers are all zero-initialised by cudaMalloc (the
+    host supplies no data): e2e goes through hgrd_gpu_run_concrete_json,
+    MiniCU source in, JSON report out."""
+
+    e2e_api = "hgrd_gpu_run_concrete_json"
+    inputs = []
+
+    def check(self, var, res):
+        want = self.expect[var]
+        got = sorted(r["kind"] for r in res["races"])
+        assert got == want, (var, got, want)
+        assert res["instances"] == self.inst_per_launch, res["instances"]
+
+
+class Stencil(ZeroInit):
+    """configs[1]: 1D stencil with a per-block tile, 2^20 threads, block 256,
+    warp 32; missing-barrier and fixed variants."""
+
+    config_index = 1
+    expect = {"missing": ["INTRA-BLOCK", "INTRA-BLOCK", "INTRA-WARP", "INTRA-WARP"], "fixed": []}
+
+    def __init__(self, n=1 << 20):
+        self.n = n
+        self.name = f"stencil1d_2^{n.bit_length() - 1}threads_block256_ws32_missing+fixed"
+        self.inst_per_launch = 5 * n
+
+    def source(self, n, var):
+        return programs.stencil(n, 256, var == "fixed")
+
+    def build(self, hg, ctx, pinned):
+        n, out = self.n, []
+        for var in ("missing", "fixed"):
+            low = hg.lower(self.source(n, var), "st")
+            h = {"in_": ctx.alloc(n), "tile": ctx.alloc(n // 256 * 258), "out_": ctx.alloc(n)}
+            out.append((var, hg.LaunchSpec(low, (n // 256, 1, 1), (256, 1, 1), 32, handles=h)))
+        return out
+
+    def cpu_sample(self, sample_n):
+        return [(self.source(sample_n, v), None, 5 * sample_n) for v in ("missing", "fixed")]
+
+
+class Transpose(ZeroInit):
+    """configs[2]: tiled n x n transpose through a padded 32x33 tile per
+    block, n = 8192: 2^26 instances per barrier interval, 3 * 2^26 per
+    launch; missing-barrier and fixed variants."""
+
+    config_index = 2
+    expect = {"missing": ["INTRA-BLOCK"], "fixed": []}
+
+    def __init__(self, n=8192):
+        self.n = n
+        self.name = f"transpose_{n}x{n}_block32x32_ws32_missing+fixed"
+        self.inst_per_launch = 3 * n * n
+
+    def source(self, n, var):
+        return programs.transpose(n, var == "fixed")
+
+    def build(self, hg, ctx, pinned):
+        n, out = self.n, []
+        for var in ("missing", "fixed"):
+            low = hg.lower(self.source(n, var), "tr")
+            ntile = (n // 32) * (n // 32) * 1056
+            h = {"tile": ctx.alloc(ntile), "out_": ctx.alloc(n * n)}
+            out.append((var, hg.LaunchSpec(low, (n // 32, n // 32, 1), (32, 32, 1), 32,
+                                           scalars={"n": n}, handles=h)))
+        return out
+
+    def cpu_sample(self, sample_n):
+        side = int(round(sample_n ** 0.5))
+        return [(self.source(side, v), None, 3 * side * side) for v in ("missing", "fixed")]
+
+
+WORKLOADS = {
+    "histogram": lambda: Histogram(),
+    "histogram_2p24": lambda: Histogram(bins=1 << 24),
+    "permutation": lambda: Permutation(),
+    "transpose": lambda: Transpose(),
+    "stencil": lambda: Stencil(),
+}
+# reference CPU sample per host thread (MiniCU threads per launch)
+CPU_SAMPLE = {"histogram": 1 << 18, "histogram_2p24": 1 << 18, "permutation": 1 << 18,
+              "transpose": 1 << 18, "stencil": 1 << 16}
 
 
 def peaks():
@@ -108,73 +299,76 @@ class Clocks:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def reference_rate(threads: int, reps: int, sample: int):
+def reference_rate(wl, threads: int, reps: int, sample: int):
     """The unmodified reference runConcrete, `threads` host threads at once,
-    each running both variants of the stencil on a `sample`-thread launch."""
+    each running every variant of the workload at `sample` MiniCU threads;
+    the host-only run of the same program (init loop, no launch) is timed
+    the same way and subtracted, so the rate is the race-check stage's."""
     from oracles import RefOracle, REF_LIB, CpuOracle, ORACLE_LIB
     cfg = programs.synthetic_config()
-    srcs = [programs.stencil(sample, barrier=b) for b in (False, True)]
     if os.path.exists(REF_LIB):
         ref, kind = RefOracle(), "reference"
-        secs = 0.0
-        for s in srcs:
-            t, _ = ref.time_parallel(s, cfg, threads, reps, "syn.mcu")
-            secs += t
+
+        def run(src):
+            return ref.time_parallel(src, cfg, threads, reps, "syn.mcu")[0]
     else:
         ora, kind = CpuOracle(ORACLE_LIB), "port"
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            for s in srcs:
-                ora.run_concrete(s, cfg, "syn.mcu")
-        secs = time.perf_counter() - t0
         threads = 1
-    inst = threads * reps * len(srcs) * INST_PER_THREAD * sample
-    return inst / secs, kind, threads, secs, inst
+
+        def run(src):
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                ora.run_concrete(src, cfg, "syn.mcu")
+            return time.perf_counter() - t0
+    secs = host_secs = 0.0
+    inst = 0
+    for src, host_only, n_inst in wl.cpu_sample(sample):
+        secs += run(src)
+        if host_only is not None:
+            host_secs += run(host_only)
+        inst += threads * reps * n_inst
+    return inst / max(secs - host_secs, 1e-9), kind, threads, secs, host_secs, inst
+
+
+def _sample_text(wl, threads, reps, sample, inst, secs, host_secs):
+    t = (f"{threads} host threads x {reps} reps x {len(wl.cpu_sample(sample))} variants of "
+         f"{wl.name.split('_')[0]} at {sample} MiniCU threads per launch "
+         f"({inst} instances, {secs:.1f} s")
+    if host_secs:
+        t += f", minus {host_secs:.1f} s of the same host init without the launch"
+    return t + "; hgrd::runConcrete, caps raised)"
 
 
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    wl = WORKLOADS[args.workload]()
+    sample = CPU_SAMPLE[args.workload]
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        reference_rate(threads, 1, SAMPLE_THREADS)
-    tot_inst, tot_secs = 0, 0.0
+        reference_rate(wl, threads, 1, sample // 4)
+    tot_inst, tot_secs, tot_host = 0, 0.0, 0.0
     kind = "reference"
     for _ in range(args.steps):
-        _, kind, threads, secs, inst = reference_rate(threads, 1, SAMPLE_THREADS)
+        _, kind, threads, secs, host_secs, inst = reference_rate(wl, threads, 1, sample)
         tot_inst += inst
         tot_secs += secs
-    v = tot_inst / tot_secs
-    sample = (f"{threads} host threads x both stencil variants at {SAMPLE_THREADS} MiniCU "
-              f"threads each per step (hgrd::runConcrete, caps raised)")
+        tot_host += host_secs
+    v = tot_inst / (tot_secs - tot_host)
+    sample_txt = _sample_text(wl, threads, 1, sample, tot_inst // args.steps,
+                              tot_secs / args.steps, tot_host / args.steps) + " per step"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_secs / args.steps, "higher_is_better": True,
+        "ms_per_step": 1e3 * (tot_secs - tot_host) / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample_threads": SAMPLE_THREADS},
+        "config": {"workload": wl.name, "baseline_config": wl.config_index,
+                   "sample_threads_per_launch": sample},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": sample_txt},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
-
-
-def build_specs(hg, ctx):
-    import torch
-    specs = []
-    for barrier in (False, True):
-        src = programs.stencil(N_THREADS, BLOCK, barrier)
-        low = hg.lower(src, "st")
-        sizes = {"in_": N_THREADS, "tile": N_THREADS // BLOCK * (BLOCK + 2), "out_": N_THREADS}
-        handles = {k: ctx.alloc(v) for k, v in sizes.items()}
-        spec = hg.LaunchSpec(low, (N_THREADS // BLOCK, 1, 1), (BLOCK, 1, 1), WS,
-                             handles=handles)
-        # the reference's buffers_ (zero-initialised int64), in pinned host memory
-        host = {k: torch.zeros(v, dtype=torch.int64, pin_memory=True).numpy()
-                for k, v in sizes.items()}
-        specs.append((spec, handles, host))
-    return specs
 
 
 def run_gpu_arm(args):
@@ -191,24 +385,30 @@ def run_gpu_arm(args):
     dev = torch.device("cuda", local)
     ctx = hg.GpuContext(local)
     ctx.set_profiling(True)
-    specs = build_specs(hg, ctx)
+    wl = WORKLOADS[args.workload]()
+
+    def pinned(a):
+        t = torch.empty(a.size, dtype=torch.int64, pin_memory=True).numpy()
+        t[:] = a
+        return t
+
+    launches = wl.build(hg, ctx, pinned)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step():
         out = []
-        for spec, _, _ in specs:
+        for var, spec in launches:
             res = ctx.check_launch(spec)
-            out.append((res, ctx.last_profile()))
+            out.append((var, res, ctx.last_profile()))
         return out
 
     for _ in range(max(args.warmup, 3)):
         step()
-    # correctness guard: the report must be the known one (tests pin it to the oracle)
-    got = step()
-    kinds = sorted(r["kind"] for r in got[0][0]["races"])
-    if not os.environ.get("HGRD_FUSED_ABLATE"):  # profiling ablations change the report
-        assert kinds == ["INTRA-BLOCK", "INTRA-BLOCK", "INTRA-WARP", "INTRA-WARP"], kinds
-        assert not got[1][0]["races"]
+    # correctness guard: the report must be the known one (tests pin it to the reference)
+    ablate = bool(os.environ.get("HGRD_FUSED_ABLATE"))  # profiling ablations change reports
+    if not ablate:
+        for var, res, _ in step():
+            wl.check(var, res)
 
     def barrier():
         if use_dist:
@@ -216,7 +416,7 @@ def run_gpu_arm(args):
         torch.cuda.synchronize()
 
     # clocks: sample across a >= 1 s run of the same steps right before the
-    # timed region and through it (the timed region alone is milliseconds)
+    # timed region and through it
     clocks = Clocks(local)
     t_probe = time.perf_counter()
     while time.perf_counter() - t_probe < 1.0:
@@ -224,14 +424,13 @@ def run_gpu_arm(args):
     launches0 = ctx.kernel_launches()
     barrier()
     dev_ms = 0.0
-    stage_ms = {}
-    stage_n = {}
+    stage_ms, stage_n = {}, {}
     inst = 0
     wall0 = time.perf_counter()
     for _ in range(args.steps):
-        flush.zero_()
+        flush.zero_()  # L2 flush between steps (the data arrays exceed L2 as well)
         torch.cuda.synchronize()
-        for res, prof in step():
+        for var, res, prof in step():
             dev_ms += res["deviceMs"]
             inst += res["instances"]
             for s in prof:
@@ -239,30 +438,40 @@ def run_gpu_arm(args):
                 stage_n[s["name"]] = stage_n.get(s["name"], 0) + 1
     barrier()
     wall = time.perf_counter() - wall0
-    launches = ctx.kernel_launches() - launches0
+    n_launch = ctx.kernel_launches() - launches0
     clk = clocks.stop()
 
-    # e2e: the reference-facing call (hgrd::runConcrete, src/oracle.cpp:378):
-    # MiniCU source text in, JSON race report out — front end, host
-    # interpretation of main(), zero-initialised cudaMalloc buffers, the
-    # launch descriptor upload, the check and the report read-back, wall clock.
-    sources = [programs.stencil(N_THREADS, BLOCK, b) for b in (False, True)]
-    cfg = programs.synthetic_config()  # same ExecConfig as the reference arm
-    for src in sources:  # warm (allocation arena, NVRTC cache)
-        ctx.run_concrete(src, cfg, "syn.mcu")
+    # e2e through the C ABI with HOST buffers: every step copies the host's
+    # input arrays (pinned) into the context's buffers (hgrd_gpu_buffer_write),
+    # checks every variant and reads the reports back; workloads without
+    # host data go through hgrd_gpu_run_concrete_json (source in, JSON out).
+    cfg = programs.synthetic_config()
+
+    def e2e_step():
+        if wl.e2e_api.startswith("hgrd_gpu_run_concrete"):
+            return [(var, ctx.run_concrete(wl.source(wl.n, var), cfg, "syn.mcu"))
+                    for var, _ in launches]
+        for h, host in wl.inputs:
+            ctx.write(h, host)
+        return [(var, ctx.check_launch(spec)) for var, spec in launches]
+
+    e2e_step()  # warm (allocation arena, NVRTC cache)
     barrier()
     xfer0 = ctx.transfer_bytes()
     t0 = time.perf_counter()
-    e2e_races = []
     for _ in range(args.steps):
-        e2e_races = [ctx.run_concrete(src, cfg, "syn.mcu")["races"] for src in sources]
+        got = e2e_step()
     barrier()
     e2e_s = time.perf_counter() - t0
     xfer1 = ctx.transfer_bytes()
     h2d = (xfer1[0] - xfer0[0]) // max(args.steps, 1)
     d2h = (xfer1[1] - xfer0[1]) // max(args.steps, 1)
-    if not os.environ.get("HGRD_FUSED_ABLATE"):
-        assert sorted(r["kind"] for r in e2e_races[0]) == kinds and not e2e_races[1]
+    if not ablate:
+        for var, res in got:
+            if "stats" in res:
+                assert sorted(r["kind"] for r in res["races"]) == wl.expect[var]
+            else:
+                wl.check(var, res)
 
     if use_dist:
         t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=dev)
@@ -274,40 +483,45 @@ def run_gpu_arm(args):
 
     peak, peak_kind = peaks()
     dom = max(stage_ms, key=stage_ms.get)
-    per_launch_inst = INST_PER_THREAD * N_THREADS
     dom_avg_ms = stage_ms[dom] / stage_n[dom]
-    achieved = B_ALG * per_launch_inst / (dom_avg_ms / 1e3) / 1e9
+    # algorithmic bytes per launch of the dominant kernel: B_alg x instances
+    # of one launch (it runs once per check)
+    achieved = wl.b_alg * wl.inst_per_launch / (dom_avg_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
+        tr = json.load(open(tpath))
+        traffic = tr.get(args.workload, {}).get(dom) if isinstance(tr.get(args.workload),
+                                                                   dict) else None
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "threads_per_launch": N_THREADS,
-                   "instances_per_step": 2 * per_launch_inst,
+        "config": {"workload": wl.name, "baseline_config": wl.config_index,
+                   "instances_per_launch": wl.inst_per_launch,
+                   "launches_per_step": len(launches),
+                   "instances_per_step": wl.inst_per_launch * len(launches),
                    "l2": "flushed between steps (256 MiB write)",
                    "parallelism": f"replicas{ws}"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "hgrd_gpu_run_concrete_json"},
-        "gpu_launches": launches,
+                "d2h_bytes_per_step": d2h, "api": wl.e2e_api},
+        "gpu_launches": n_launch,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": dom,
-                     "kernel_avg_ms": dom_avg_ms, "peak_source": peak_kind,
+                     "kernel_avg_ms": dom_avg_ms, "b_alg_per_instance": wl.b_alg,
+                     "peak_source": peak_kind,
                      "stage_share": {k: v / sum(stage_ms.values()) for k, v in stage_ms.items()}},
         "clocks": clk,
         "wall_s": wall,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        reps = CPU_BASELINE_REPS  # ~10 s of host work on the GPU box
-        v, kind, threads, secs, n = reference_rate(threads, reps, SAMPLE_THREADS)
-        line["cpu_baseline"] = {
-            "value": v, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{threads} host threads x {reps} reps x both variants at {SAMPLE_THREADS} "
-                      f"threads ({n} instances, {secs:.1f} s)"}
+        sample = CPU_SAMPLE[args.workload]
+        v, kind, threads, secs, host_secs, n = reference_rate(wl, threads, 1, sample)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                                "sample": _sample_text(wl, threads, 1, sample, n, secs,
+                                                       host_secs)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -415,6 +629,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="histogram", choices=sorted(WORKLOADS),
+                    help="BASELINE config to time (default: configs[3], the largest)")
     ap.add_argument("--paths", action="store_true",
                     help="time the lock-idiom, SEQUENTIAL and sweep paths against the reference")
     args = ap.parse_args()

@@ -855,7 +855,9 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     const char *e = std::getenv("HGRD_FUSED_ITER");
     return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(512);
   }();
-  int64_t bpi = std::max<int64_t>(1, kIterThreads / D.tpb);
+  // (at most 256: a record keeps its MiniCU block within the iteration in
+  // 8 bits, packR1 / rBlk in fused.cuh)
+  int64_t bpi = std::min<int64_t>(kMaxIterBlocks, std::max<int64_t>(1, kIterThreads / D.tpb));
   const uint64_t per = std::max<uint32_t>(recInsns, 1);
   while (bpi > 1 && static_cast<uint64_t>(bpi * D.tpb) * per > 4096)
     bpi /= 2;

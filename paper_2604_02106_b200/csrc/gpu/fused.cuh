@@ -33,6 +33,7 @@ namespace dev {
 constexpr int kMaxWritten = 8;
 constexpr uint32_t kOwnerMulti = 0xFFFFFu;
 constexpr int kSmallGroup = 32; // hash slots up to this size, radix grouping above
+constexpr int kMaxIterBlocks = 256; // MiniCU blocks per iteration: the 8-bit blk field of r1
 
 enum FusedFlags : uint32_t {
   kFlagShared = 128u,   // an element is accessed by two blocks (pass 2 needed)

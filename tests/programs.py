@@ -286,3 +286,145 @@ def lock_kernel(n, variant):
             "}\n"
             f"void main() {{ int *acc; lock *L; cudaMalloc(&acc, 128); cudaMalloc(&L, 2);\n"
             f"  k<<<({n // 256},1,1),(256,1,1)>>>(acc, L); }}\n")
+
+
+# Permutation scatter ("B = n, conflict-free, with k
+# injected duplicates"): data[i] = (i*M + S) mod n is a bijection for
+# power-of-two n and odd M, so every bin has exactly one thread except the
+# duplicated ones.  PERM_DUPS: (j, j2) host assignments data[j] = data[j2],
+# chosen so the duplicate pairs realise each kind at block 256 / warp 32:
+#   (9, 5)        same warp                 -> INTRA-WARP
+#   (100, 37)     block 0, warps 3 and 1    -> INTRA-BLOCK
+#   (1000, 70000) blocks 3 and 273          -> INTER-BLOCK
+#   (600, 601)    block 2, same warp        -> INTRA-WARP (a later element)
+#   (n-1, 3)      last block and block 0    -> INTER-BLOCK
+PERM_DUPS = ((9, 5), (100, 37), (1000, 70000), (600, 601), (-1, 3))
+
+
+def perm_dups(n_threads: int):
+    return [((j if j >= 0 else n_threads + j), j2) for j, j2 in PERM_DUPS]
+
+
+def permutation_scatter(n_threads: int, update: str = "store", block: int = 256,
+                        host_init: bool = True) -> str:
+    """Scatter through a permutation with injected duplicate targets; with
+    host_init=False the host loop and duplicate assignments are omitted and
+    the caller writes `data` (permutation_data)."""
+    init = ""
+    if host_init:
+        init = (f"  for (int i = 0; i < {n_threads}; i++) {{ data[i] = (i * {HIST_MULT} + "
+                f"{HIST_SEED}) % {n_threads}; }}\n")
+        for j, j2 in perm_dups(n_threads):
+            init += f"  data[{j}] = data[{j2}];\n"
+    return (
+        "__global__ void h(int *data, int *hist) {\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  int b = data[t];\n"
+        f"{HIST_UPDATES[update]}"
+        "}\n"
+        f"void main() {{ int *data; int *hist; cudaMalloc(&data, {n_threads});"
+        f" cudaMalloc(&hist, {n_threads});\n"
+        f"{init}"
+        f"  h<<<({n_threads // block},1,1),({block},1,1)>>>(data, hist); }}\n")
+
+
+def permutation_data(n_threads: int):
+    import numpy as np
+    i = np.arange(n_threads, dtype=np.int64)
+    d = (i * HIST_MULT + HIST_SEED) % n_threads
+    for j, j2 in perm_dups(n_threads):
+        d[j] = d[j2]
+    return d
+
+
+# Launches of many tiny MiniCU blocks: more blocks than one fused iteration
+# holds (the per-iteration block field of k_fused's records is 8 bits).
+TINY_BLOCK_PROGRAMS: Dict[str, str] = {
+    # clean: each single-thread block reads and writes its own element
+    "own_rw_300": (
+        "__global__ void k(int *A) {\n"
+        "  int t = blockIdx.x;\n"
+        "  A[t] = A[t] + 1;\n"
+        "}\n"
+        "void main() { int *A; cudaMalloc(&A, 300);\n"
+        "  k<<<(300,1,1),(1,1,1)>>>(A); }\n"),
+    # INTER-BLOCK only: every block stores element 0
+    "hot_store_300": (
+        "__global__ void k(int *A) {\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  A[0] = t;\n"
+        "}\n"
+        "void main() { int *A; cudaMalloc(&A, 4);\n"
+        "  k<<<(300,1,1),(1,1,1)>>>(A); }\n"),
+    "hot_store_1024": (
+        "__global__ void k(int *A) {\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  A[0] = t;\n"
+        "}\n"
+        "void main() { int *A; cudaMalloc(&A, 4);\n"
+        "  k<<<(1024,1,1),(1,1,1)>>>(A); }\n"),
+    # hot element over > 512 two-thread blocks (radix grouping in k_fused):
+    # INTRA kinds inside each block plus INTER, and block-private pairs
+    "hot_pairs_600": (
+        "__global__ void k(int *A, int *B) {\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  A[0] = t;\n"
+        "  B[blockIdx.x] = B[blockIdx.x] + threadIdx.x;\n"
+        "  A[1 + t % 3] = A[1 + blockIdx.x % 2];\n"
+        "}\n"
+        "void main() { int *A; int *B; cudaMalloc(&A, 8); cudaMalloc(&B, 600);\n"
+        "  k<<<(600,1,1),(2,1,1)>>>(A, B); }\n"),
+    # 3-D grid of single-thread blocks, private and shared elements
+    "grid3_800": (
+        "__global__ void k(int *A) {\n"
+        "  int b = blockIdx.x + blockIdx.y * gridDim.x + blockIdx.z * gridDim.x * gridDim.y;\n"
+        "  A[b] = A[b] + 1;\n"
+        "  A[800 + b % 5] = A[800 + (b + 1) % 7];\n"
+        "}\n"
+        "void main() { int *A; cudaMalloc(&A, 816);\n"
+        "  k<<<(20,20,2),(1,1,1)>>>(A); }\n"),
+}
+
+
+def permutation_expected(n_threads: int, update: str = "store", block: int = 256,
+                         ws: int = 32):
+    """The report of permutation_scatter(n_threads, update) derived from its
+    structure, for sizes no CPU run reaches (2^27): only the duplicated bins
+    hold two events (threads j < j2, store seq 1 each).  Reference rules
+    (src/oracle.cpp:745-784): kind by block / warp, block-scope atomics cover
+    pairs inside one block, and each key keeps its first-found element =
+    the minimum element (ordered map by (handle, index)), witness = its pair.
+    Pinned against the reference at 2^20 (tests/test_golden_extra.py).
+    Returns [(kind, address, threadA, threadB)] in report order."""
+    d = permutation_data(n_threads)
+    best = {}
+    for j, j2 in perm_dups(n_threads):
+        a, b = sorted((j, j2))
+        if a // block != b // block:
+            kind = "INTER-BLOCK"
+        elif (a % block) // ws != (b % block) // ws:
+            kind = "INTRA-BLOCK"
+        else:
+            kind = "INTRA-WARP"
+        if update == "atomic" or (update == "atomic_block" and kind != "INTER-BLOCK"):
+            continue
+        e = int(d[j2])
+        if kind not in best or e < best[kind][0]:
+            best[kind] = (e, a, b)
+    order = ("INTER-BLOCK", "INTRA-BLOCK", "INTRA-WARP")
+    return [(k, *best[k]) for k in order if k in best]
+
+
+def histogram_pow2_expected(n_threads: int, bins: int, update: str = "store"):
+    """The report of histogram(n_threads, bins, update) for power-of-two
+    bins >= 256 (one block of 256 never repeats a bin: the multiplier is
+    odd) and n_threads >= 2 * bins: only INTER-BLOCK pairs exist, the
+    first-found element is bin 0 (the minimum element, src/oracle.cpp:745),
+    and its first pair is (i0, i0 + bins), i0 = the first thread mapped to
+    bin 0.  [(kind, address, threadA, threadB)]; pinned against the reference
+    at 2^20 / 2^22 threads x 2^16 bins (test_golden_extra.py)."""
+    assert bins >= 256 and bins & (bins - 1) == 0 and n_threads >= 2 * bins
+    if update == "atomic":
+        return []
+    i0 = (-HIST_SEED * pow(HIST_MULT, -1, bins)) % bins
+    return [("INTER-BLOCK", 0, i0, i0 + bins)]

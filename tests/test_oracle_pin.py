@@ -121,3 +121,35 @@ def test_live_reference_crosscheck(ref_oracle, cpu_oracle):
                    "maxThreads": 200}
             assert strip_extras(cpu_oracle.run_concrete(src, cfg)) == \
                 ref_oracle.run_concrete(src, cfg), (name, ws)
+
+
+def test_regress_tiny_blocks(cpu_oracle):
+    """Launches of more MiniCU blocks than one k_fused iteration holds."""
+    for c in load_golden("regress"):
+        got = cpu_oracle.run_concrete(c["source"], c["config"], "tiny.mcu")
+        assert strip_extras(got) == c["result"], (c["name"], c["config"])
+        assert got["witnesses"] == c["witnesses_restatement"]
+
+
+def test_structural_predictors_pinned():
+    """programs.permutation_expected / histogram_pow2_expected (used by the
+    2^27 GPU tests) reproduce the reference's reports at 2^20 / 2^22."""
+    import programs
+    n_checked = 0
+    for g in ("large", "xlarge"):
+        for c in load_golden(g):
+            name, res = c["name"], c["result"]
+            got = [(r["kind"], r["address"]) for r in res["races"]]
+            wit = [(w["threadA"], w["threadB"]) for w in c["witnesses_restatement"]]
+            if name.startswith("permutation_"):
+                n, upd = int(name.split("_")[1]), name.split("_", 2)[2]
+                want = programs.permutation_expected(n, upd)
+            elif name.startswith("histogram_") and name.split("_")[2] == "65536":
+                n, upd = int(name.split("_")[1]), name.split("_", 3)[3]
+                want = programs.histogram_pow2_expected(n, 65536, upd)
+            else:
+                continue
+            assert got == [(k, a) for k, a, _, _ in want], name
+            assert wit == [(x, y) for _, _, x, y in want], name
+            n_checked += 1
+    assert n_checked >= 5

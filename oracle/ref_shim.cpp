@@ -15,6 +15,8 @@
 
 #include <nlohmann/json.hpp>
 
+#include "ref_config.hpp"
+
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
@@ -35,48 +37,6 @@ char *dupString(const std::string &s) {
 
 ordered_json locJson(const hgrd::SourceLoc &l) {
   return ordered_json{{"file", l.file}, {"line", l.line}, {"column", l.column}};
-}
-
-template <class A> void readArr3(const ordered_json &j, const char *k, A &dst) {
-  if (!j.contains(k))
-    return;
-  const auto &v = j.at(k);
-  for (size_t i = 0; i < 3 && i < v.size(); ++i)
-    dst[i] = v[i].get<long long>();
-}
-
-hgrd::ExecConfig parseExec(const char *cfgJson) {
-  hgrd::ExecConfig c;
-  ordered_json j = ordered_json::parse(cfgJson ? cfgJson : "{}");
-  readArr3(j, "gridCap", c.gridCap);
-  readArr3(j, "blockCap", c.blockCap);
-  if (j.contains("warpSize"))
-    c.warpSize = j["warpSize"].get<long long>();
-  if (j.contains("inputs"))
-    c.inputs = j["inputs"].get<std::vector<long long>>();
-  if (j.contains("maxThreads"))
-    c.maxThreads = j["maxThreads"].get<long long>();
-  if (j.contains("maxArrayElems"))
-    c.maxArrayElems = j["maxArrayElems"].get<long long>();
-  if (j.contains("maxSteps"))
-    c.maxSteps = j["maxSteps"].get<long long>();
-  return c;
-}
-
-hgrd::SweepCaps parseCaps(const char *capsJson) {
-  hgrd::SweepCaps c;
-  ordered_json j = ordered_json::parse(capsJson ? capsJson : "{}");
-  readArr3(j, "gridCap", c.gridCap);
-  readArr3(j, "blockCap", c.blockCap);
-  if (j.contains("inputSet"))
-    c.inputSet = j["inputSet"].get<std::vector<long long>>();
-  if (j.contains("warpSizes"))
-    c.warpSizes = j["warpSizes"].get<std::vector<long long>>();
-  if (j.contains("maxThreads"))
-    c.maxThreads = j["maxThreads"].get<long long>();
-  if (j.contains("maxConfigs"))
-    c.maxConfigs = j["maxConfigs"].get<size_t>();
-  return c;
 }
 
 ordered_json parseErrorJson(const hgrd::ParseResult &r) {

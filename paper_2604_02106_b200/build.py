@@ -34,8 +34,9 @@ def _sources():
 
 
 def _headers():
-    hs = [os.path.join(ROOT, "include", "hgrd_gpu.h")]
-    for sub in ("host", "gpu"):
+    inc = os.path.join(ROOT, "include")
+    hs = [os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h")]
+    for sub in ("host", "gpu", ""):
         d = os.path.join(CSRC, sub)
         hs += [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".hpp", ".cuh"))]
     return hs

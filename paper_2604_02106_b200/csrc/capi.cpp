@@ -5,6 +5,7 @@
 #include "host.hpp"
 #include "gpu/affine.hpp"
 #include "gpu/jit.hpp"
+#include "gpu_backend.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -14,34 +15,8 @@
 
 using namespace hgrdgpu;
 
-namespace hgrdgpu {
-hgrd_gpu_ctx *sweepWorker(hgrd_gpu_ctx *c, int i); // ctx.cu
-bool setTiming(hgrd_gpu_ctx *c, bool on);            // ctx.cu
-}
 
 namespace {
-
-class GpuBackend final : public LaunchBackend {
-public:
-  explicit GpuBackend(hgrd_gpu_ctx *c) : c_(c) {}
-  int reset() override { return hgrd_gpu_buffers_reset(c_); }
-  int alloc(int64_t elems, int32_t *handle) override {
-    return hgrd_gpu_buffer_alloc(c_, elems, handle);
-  }
-  int write(int32_t h, int64_t off, int64_t n, const int64_t *src) override {
-    return hgrd_gpu_buffer_write(c_, h, off, n, src);
-  }
-  int read(int32_t h, int64_t off, int64_t n, int64_t *dst) override {
-    return hgrd_gpu_buffer_read(c_, h, off, n, dst);
-  }
-  int checkLaunch(const hgrd_gpu_launch &l, hgrd_gpu_result &r) override {
-    return hgrd_gpu_check_launch(c_, &l, &r);
-  }
-  std::string lastError() override { return hgrd_gpu_last_error(c_); }
-
-private:
-  hgrd_gpu_ctx *c_;
-};
 
 char *dup(const std::string &s) {
   char *p = static_cast<char *>(std::malloc(s.size() + 1));
@@ -75,25 +50,9 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
   // (own streams and buffers on the same GPU, one host thread each) so the
   // small launches of a sweep overlap instead of queueing behind each
   // other's host round trips (HGRD_SWEEP_WORKERS, default 8)
-  const char *env = std::getenv("HGRD_SWEEP_WORKERS");
-  const int n = std::max(1, env ? std::atoi(env) : 8);
-  std::vector<std::unique_ptr<GpuBackend>> bes(static_cast<size_t>(n));
-  auto worker = [&](int i) -> LaunchBackend * {
-    if (i >= n)
-      return nullptr;
-    hgrd_gpu_ctx *w = sweepWorker(ctx, i);
-    if (!w)
-      return nullptr;
-    if (i > 0)
-      setTiming(w, false); // worker contexts only run sweeps
-    if (!bes[static_cast<size_t>(i)])
-      bes[static_cast<size_t>(i)] = std::make_unique<GpuBackend>(w);
-    return bes[static_cast<size_t>(i)].get();
-  };
+  SweepWorkers pool(ctx);
   std::string s;
-  const bool timing = setTiming(ctx, false);
-  int rc = enumerateVerdictJsonParallel(worker, n, source, file_name, caps_json, s);
-  setTiming(ctx, timing);
+  int rc = enumerateVerdictJsonParallel(pool.getter(), pool.n, source, file_name, caps_json, s);
   *out = dup(s);
   return rc;
 }

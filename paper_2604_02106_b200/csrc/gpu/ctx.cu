@@ -2119,6 +2119,11 @@ int hgrd_gpu_shard_detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, const 
 } // extern "C"
 
 namespace hgrdgpu {
+void setError(hgrd_gpu_ctx *c, const std::string &m) {
+  if (c)
+    c->err = m;
+}
+
 // Worker i (>= 1) of a context for parallel sweeps: a further context on
 // the same device, created on first use and destroyed with its parent;
 // worker 0 is the context itself.  nullptr when it cannot be created.

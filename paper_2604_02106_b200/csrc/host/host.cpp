@@ -1380,6 +1380,29 @@ SweepResult enumerateVerdictParallel(CompiledProgram &prog, const SweepCaps &cap
   return out;
 }
 
+SweepResult enumerateVerdictOnWorkers(const std::function<LaunchBackend *(int)> &workers, int n,
+                                      CompiledProgram &cp, const SweepCaps &caps) {
+  const uint64_t size = sweepSize(cp, caps);
+  // one configuration per worker at least: a configuration costs a few
+  // GPU round trips (~30 us each), more than spawning its worker thread
+  int use = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(std::max(n, 1)), size));
+  std::vector<LaunchBackend *> bes;
+  for (int i = 0; i < std::max(use, 1); ++i) {
+    LaunchBackend *b = workers(i);
+    if (!b)
+      break;
+    bes.push_back(b);
+  }
+  if (bes.empty()) {
+    SweepResult r;
+    r.error = HGRD_GPU_ENODEV;
+    r.errorMessage = "no sweep worker";
+    return r;
+  }
+  return bes.size() > 1 ? enumerateVerdictParallel(cp, caps, bes)
+                        : enumerateVerdict(cp, caps, *bes[0]);
+}
+
 int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &workers, int n,
                                  const char *src, const char *file, const char *capsJson,
                                  std::string &out) {
@@ -1396,19 +1419,7 @@ int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &work
   }
   std::string fileName = po.program->file;
   auto cp = compileProgram(std::move(po.program));
-  const uint64_t size = sweepSize(*cp, caps);
-  // one configuration per worker at least: a configuration costs a few
-  // GPU round trips (~30 us each), more than spawning its worker thread
-  int use = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(std::max(n, 1)), size));
-  std::vector<LaunchBackend *> bes;
-  for (int i = 0; i < std::max(use, 1); ++i) {
-    LaunchBackend *b = workers(i);
-    if (!b)
-      break;
-    bes.push_back(b);
-  }
-  SweepResult r = bes.size() > 1 ? enumerateVerdictParallel(*cp, caps, bes)
-                                 : enumerateVerdict(*cp, caps, *bes[0]);
+  SweepResult r = enumerateVerdictOnWorkers(workers, n, *cp, caps);
   if (r.error) {
     out = errorJson({"backend: " + r.errorMessage});
     return r.error;

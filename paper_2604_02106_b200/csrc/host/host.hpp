@@ -176,6 +176,8 @@ int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
 // Same with the configurations spread over `workers` backends.  `workers`
 // returns backend i (0 = the caller's) or nullptr; used when the lattice has
 // at least 4 configurations per worker.
+SweepResult enumerateVerdictOnWorkers(const std::function<LaunchBackend *(int)> &workers, int n,
+                                      CompiledProgram &cp, const SweepCaps &caps);
 int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &workers, int n,
                                  const char *src, const char *file, const char *capsJson,
                                  std::string &out);

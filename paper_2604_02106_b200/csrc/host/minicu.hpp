@@ -120,5 +120,8 @@ struct ParseOutcome {
 };
 
 ParseOutcome parseMiniCU(const std::string &source, const std::string &file);
+// The resolver's diagnostics for a program built without the parser (empty:
+// accepted), reference parser.cpp:1017-1180.
+std::vector<std::string> resolveMiniCU(Program &p);
 
 } // namespace hgrdgpu

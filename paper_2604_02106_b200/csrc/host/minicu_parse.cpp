@@ -185,6 +185,13 @@ public:
     return out;
   }
 
+  // The resolver alone, over a program built elsewhere (the flat-program
+  // ABI, include/hgrd_gpu_program.h).
+  std::vector<std::string> resolveOnly(Program &p) {
+    resolveProgram(p);
+    return diags_;
+  }
+
 private:
   std::string diag(const Loc &l, const char *kind, const std::string &m) {
     return file_ + ":" + std::to_string(l.line) + ":" + std::to_string(l.col) +
@@ -935,6 +942,8 @@ private:
 };
 
 } // namespace
+
+std::vector<std::string> resolveMiniCU(Program &p) { return Parser("", p.file).resolveOnly(p); }
 
 ParseOutcome parseMiniCU(const std::string &source, const std::string &file) {
   try {

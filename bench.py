@@ -56,6 +56,7 @@ class Workload:
     name = ""
     config_index = 0
     b_alg = 32
+    shardable = False
     e2e_api = "hgrd_gpu_buffer_write + hgrd_gpu_check_launch"
 
     def variants(self):
@@ -88,39 +89,54 @@ class Histogram(Workload):
     b_alg = 36  # 32 B per instance + 8 B per value-consumed load (1 per 2 instances)
     updates = ("atomic", "atomic_block", "store")
 
+    shardable = True  # --gpus N: one launch of N x n threads, whole-block ranges per rank
+
     def __init__(self, n=1 << 27, bins=1 << 16):
         self.n, self.bins = n, bins
         self.name = (f"histogram_2^{n.bit_length() - 1}threads_2^{bins.bit_length() - 1}bins_"
                      f"block256_ws32_atomic+atomic_block+store")
         self.inst_per_launch = 2 * n
+        self.world, self.rank = 1, 0
+
+    def shard(self, world, rank):
+        """Weak scaling: the launch grows to world x n threads; this rank
+        checks (and supplies the data of) its n threads' whole blocks."""
+        self.world, self.rank = world, rank
+        self.name = self.name.replace(f"2^{self.n.bit_length() - 1}threads",
+                                      f"{world}x2^{self.n.bit_length() - 1}threads")
+        self.inst_per_launch = 2 * self.n * world
 
     def program(self, n, upd, host_init):
         return programs.histogram(n, self.bins, upd, host_init=host_init)
 
-    def data(self, n):
-        return programs.histogram_data(n, self.bins)
+    def data(self, n, lo=0, hi=None):
+        """data[lo:hi] of an n-thread launch."""
+        import numpy as np
+        i = np.arange(lo, n if hi is None else hi, dtype=np.int64)
+        return (i * programs.HIST_MULT + programs.HIST_SEED) % self.bins
 
     def expected(self, upd):
         if self.bins & (self.bins - 1) == 0 and self.bins >= 256:
-            return programs.histogram_pow2_expected(self.n, self.bins, upd)
+            return programs.histogram_pow2_expected(self.n * self.world, self.bins, upd)
         return None
 
     def table(self):
         return self.bins
 
     def build(self, hg, ctx, pinned):
-        n = self.n
+        n = self.n * self.world
+        lo = self.rank * self.n
         data_h = ctx.alloc(n)
         table_h = ctx.alloc(self.table())
-        host = pinned(self.data(n))
-        ctx.write(data_h, host)
+        host = pinned(self.data(n, lo, lo + self.n))
+        ctx.write(data_h, host, lo)  # (the other ranks' blocks never read this rank's range)
         out = []
         for upd in self.updates:
             low = hg.lower(self.program(n, upd, False), "h")
             spec = hg.LaunchSpec(low, (n // 256, 1, 1), (256, 1, 1), 32,
                                  handles={"data": data_h, "hist": table_h})
             out.append((upd, spec))
-        self.inputs = [(data_h, host)]
+        self.inputs = [(data_h, host, lo)]
         return out
 
     def check(self, upd, res):
@@ -140,17 +156,19 @@ class Permutation(Histogram):
     hit once except the injected duplicates (programs.PERM_DUPS)."""
 
     updates = ("store", "atomic_block")
+    shardable = False  # (the permutation spans the whole launch: replicas)
 
     def __init__(self, n=1 << 27):
         self.n = n
         self.name = f"permutation_scatter_2^{n.bit_length() - 1}threads_block256_ws32_store+atomic_block"
         self.inst_per_launch = 2 * n
+        self.world, self.rank = 1, 0
 
     def program(self, n, upd, host_init):
         return programs.permutation_scatter(n, upd, host_init=host_init)
 
-    def data(self, n):
-        return programs.permutation_data(n)
+    def data(self, n, lo=0, hi=None):
+        return programs.permutation_data(n)[lo:hi]
 
     def expected(self, upd):
         return programs.permutation_expected(self.n, upd)
@@ -166,6 +184,7 @@ class ZeroInit(Workload):
 
     e2e_api = "hgrd_gpu_run_concrete_json"
     inputs = []
+    shardable = False
 
     def check(self, var, res):
         want = self.expect[var]
@@ -386,6 +405,15 @@ def run_gpu_arm(args):
     ctx = hg.GpuContext(local)
     ctx.set_profiling(True)
     wl = WORKLOADS[args.workload]()
+    # --gpus N on a shardable workload: ONE launch of N x the per-GPU threads,
+    # whole-block ranges per rank (INTRA kinds rank-local; INTER-BLOCK through
+    # an NCCL reduce-scatter of the block summaries, parallel.py); otherwise
+    # every rank checks its own replica of the workload
+    sharded = use_dist and wl.shardable
+    if sharded:
+        from paper_2604_02106_b200.parallel import TorchComm, check_launch_sharded
+        wl.shard(ws, rank)
+        comm = TorchComm()
 
     def pinned(a):
         t = torch.empty(a.size, dtype=torch.int64, pin_memory=True).numpy()
@@ -395,11 +423,20 @@ def run_gpu_arm(args):
     launches = wl.build(hg, ctx, pinned)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    ext = torch.cuda.ExternalStream(ctx.stream(), device=dev)  # the context's stream
+
+    def check(spec):
+        if sharded:
+            res = check_launch_sharded(ctx, spec, comm, device=local)
+            return res, res["stages"]
+        res = ctx.check_launch(spec)
+        return res, ctx.last_profile()
+
     def step():
         out = []
         for var, spec in launches:
-            res = ctx.check_launch(spec)
-            out.append((var, res, ctx.last_profile()))
+            res, prof = check(spec)
+            out.append((var, res, prof))
         return out
 
     for _ in range(max(args.warmup, 3)):
@@ -430,8 +467,17 @@ def run_gpu_arm(args):
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between steps (the data arrays exceed L2 as well)
         torch.cuda.synchronize()
-        for var, res, prof in step():
-            dev_ms += res["deviceMs"]
+        if sharded:  # the step spans collectives: events on the context's stream around it
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(ext)
+        results = step()
+        if sharded:
+            ev1.record(ext)
+            ev1.synchronize()
+            dev_ms += ev0.elapsed_time(ev1)
+        for var, res, prof in results:
+            if not sharded:
+                dev_ms += res["deviceMs"]
             inst += res["instances"]
             for s in prof:
                 stage_ms[s["name"]] = stage_ms.get(s["name"], 0.0) + s["ms"]
@@ -451,9 +497,9 @@ def run_gpu_arm(args):
         if wl.e2e_api.startswith("hgrd_gpu_run_concrete"):
             return [(var, ctx.run_concrete(wl.source(wl.n, var), cfg, "syn.mcu"))
                     for var, _ in launches]
-        for h, host in wl.inputs:
-            ctx.write(h, host)
-        return [(var, ctx.check_launch(spec)) for var, spec in launches]
+        for h, host, off in wl.inputs:
+            ctx.write(h, host, off)
+        return [(var, check(spec)[0]) for var, spec in launches]
 
     e2e_step()  # warm (allocation arena, NVRTC cache)
     barrier()
@@ -477,7 +523,7 @@ def run_gpu_arm(args):
         t = torch.tensor([dev_ms, e2e_s], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dev_ms, e2e_s = float(t[0]), float(t[1])
-    total_inst = inst * ws
+    total_inst = inst if sharded else inst * ws  # (a sharded report counts every rank's)
     value = total_inst / (dev_ms / 1e3)
     e2e_value = total_inst / e2e_s
 
@@ -486,7 +532,9 @@ def run_gpu_arm(args):
     dom_avg_ms = stage_ms[dom] / stage_n[dom]
     # algorithmic bytes per launch of the dominant kernel: B_alg x instances
     # of one launch (it runs once per check)
-    achieved = wl.b_alg * wl.inst_per_launch / (dom_avg_ms / 1e3) / 1e9
+    # (sharded: one rank's kernel processes its share of the launch)
+    kernel_inst = wl.inst_per_launch // (ws if sharded else 1)
+    achieved = wl.b_alg * kernel_inst / (dom_avg_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -503,7 +551,7 @@ def run_gpu_arm(args):
                    "launches_per_step": len(launches),
                    "instances_per_step": wl.inst_per_launch * len(launches),
                    "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"replicas{ws}"},
+                   "parallelism": f"blockshard{ws}" if sharded else f"replicas{ws}"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": wl.e2e_api},
         "gpu_launches": n_launch,

@@ -245,10 +245,17 @@ int hgrd_gpu_count_inputs(const char *source, const char *file_name);
  *     and, when a written buffer may be reached from two blocks, the
  *     shard's INTER summary: two device tables of inter_n u32 entries per
  *     (element, site) — min and max (block + 1), empty = 0x7F7F7F7F / 0 —
- *     which the caller MIN / MAX all-reduces across ranks in place;
- *  2. hgrd_gpu_shard_inter (after the all-reduce): the realised INTER keys'
- *     first-found elements, and this shard's packed records of them (key
- *     layout identical on every rank), copied to host;
+ *     which the caller combines across ranks (MIN on lo, MAX on hi);
+ *  2. either (a) reduce-scatter: each rank reduces one element range of the
+ *     tables (e.g. ncclReduceScatter, MIN / MAX, after padding the tables to
+ *     world x ranks' elements x n_sites entries) and scans it with
+ *     hgrd_gpu_shard_inter_scan -> per INTER key its minimum element in the
+ *     range; the ranks MIN all-reduce that n_keys table; then
+ *     hgrd_gpu_shard_inter_records gives this shard's packed records of the
+ *     realised keys' first-found elements (key layout identical on every
+ *     rank), copied to host;
+ *     or (b) all-reduce: the tables reduced in place, then
+ *     hgrd_gpu_shard_inter (scan of the whole tables + the records);
  *  3. hgrd_gpu_shard_detect: the INTER-BLOCK races (with witnesses) of the
  *     records gathered from all ranks.
  * HGRD_GPU_ENOTSUP means the launch (or a shard: traps, step budget) needs
@@ -264,9 +271,50 @@ int hgrd_gpu_shard_check(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
 int hgrd_gpu_shard_inter(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
                          const hgrd_gpu_shard *shard, uint64_t *keys, uint32_t *vals,
                          uint64_t cap, uint64_t *n);
+/* lo / hi: device tables of elements [elem_begin, elem_begin + n_elems)
+ * (n_sites entries per element), already reduced across ranks; key_elem:
+ * host, n_keys >= 3 * n_locs^2 entries, UINT64_MAX where a key has no
+ * element in the range.  Runs on the context's stream (hgrd_gpu_stream):
+ * the caller orders it after the collective that produced lo / hi
+ * (cudaStreamWaitEvent). */
+int hgrd_gpu_shard_inter_scan(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
+                              const void *lo, const void *hi, uint64_t elem_begin,
+                              uint64_t n_elems, uint64_t *key_elem, uint32_t n_keys);
+int hgrd_gpu_shard_inter_records(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
+                                 const hgrd_gpu_shard *shard, const uint64_t *key_elem,
+                                 uint32_t n_keys, uint64_t *keys, uint32_t *vals, uint64_t cap,
+                                 uint64_t *n);
+/* The context's CUDA stream (cudaStream_t): every kernel of the context
+ * runs on it, so a caller orders its own work (a collective on another
+ * stream) before or after the context's with events. */
+void *hgrd_gpu_stream(hgrd_gpu_ctx *ctx);
 int hgrd_gpu_shard_detect(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
                           const uint64_t *keys, const uint32_t *vals, uint64_t n,
                           hgrd_gpu_result *result);
+
+/* ---- batched check of many small launches (sweeps) --------------------
+ * Reference enumerateVerdict (src/oracle.cpp:863-903) runs thousands of
+ * configurations whose launches have a few dozen MiniCU threads; one
+ * hgrd_gpu_check_launch per launch is one GPU round trip each.
+ * hgrd_gpu_check_batch checks n such launches with one H2D, one kernel and
+ * one D2H.  Each launch brings its own buffers (the launch's param_handle
+ * indexes buffer_elems / buffer_data, which hold every buffer's size and,
+ * for buffers read by value-needed loads, the launch-entry contents; NULL
+ * data means zeros).  results[i] is what hgrd_gpu_check_launch would report
+ * (race handles index the launch's buffers), or carries
+ * HGRD_RESULT_UNCHECKED in `mode` when the launch is outside the batch
+ * envelope (sequential / lock-idiom launches, more than 512 threads or 256
+ * blocks, record capacity) or needs the ordered path (traps, the step
+ * budget, a hot element): check those with hgrd_gpu_check_launch. */
+typedef struct hgrd_gpu_batch_launch {
+  hgrd_gpu_launch launch;
+  const int64_t *buffer_elems;       /* n_buffers sizes */
+  const int64_t *const *buffer_data; /* per buffer: contents or NULL (zeros); may be NULL */
+  uint32_t n_buffers;
+} hgrd_gpu_batch_launch;
+#define HGRD_RESULT_UNCHECKED 0x80000000u
+int hgrd_gpu_check_batch(hgrd_gpu_ctx *ctx, const hgrd_gpu_batch_launch *launches, uint32_t n,
+                         hgrd_gpu_result *results);
 
 /* Host analysis (no GPU needed): out[s] = 1 when site s's buffer is proven
  * block-private for this launch (affine indices whose per-block element

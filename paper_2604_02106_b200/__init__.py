@@ -176,6 +176,14 @@ def load_library() -> ctypes.CDLL:
     lib.hgrd_gpu_shard_inter.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(c_uint32), ctypes.c_uint64,
                                          ctypes.POINTER(ctypes.c_uint64)]
+    lib.hgrd_gpu_shard_inter_scan.argtypes = [P, P, P, P, ctypes.c_uint64, ctypes.c_uint64,
+                                              ctypes.POINTER(ctypes.c_uint64), c_uint32]
+    lib.hgrd_gpu_shard_inter_records.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_uint64),
+                                                 c_uint32, ctypes.POINTER(ctypes.c_uint64),
+                                                 ctypes.POINTER(c_uint32), ctypes.c_uint64,
+                                                 ctypes.POINTER(ctypes.c_uint64)]
+    lib.hgrd_gpu_stream.argtypes = [P]
+    lib.hgrd_gpu_stream.restype = ctypes.c_void_p
     lib.hgrd_gpu_shard_detect.argtypes = [P, P, ctypes.POINTER(ctypes.c_uint64),
                                           ctypes.POINTER(c_uint32), ctypes.c_uint64, P]
     I3 = ctypes.c_int64 * 3
@@ -454,6 +462,64 @@ class GpuContext:
         lo = torch.as_tensor(_CudaArray(sh.inter_lo, sh.inter_n), device=dev)
         hi = torch.as_tensor(_CudaArray(sh.inter_hi, sh.inter_n), device=dev)
         return lo, hi
+
+    def stream(self) -> int:
+        """The context's cudaStream_t (every kernel of the context runs on it)."""
+        return int(self._lib.hgrd_gpu_stream(self._ctx) or 0)
+
+    def wait_torch_stream(self, device: int = 0):
+        """Order the context's stream after the work already queued on
+        torch's current stream (a collective that produced its inputs)."""
+        import torch
+        cur = torch.cuda.current_stream(device)
+        ext = torch.cuda.ExternalStream(self.stream(), device=torch.device("cuda", device))
+        ext.wait_stream(cur)
+
+    def shard_inter_scan(self, spec: LaunchSpec, lo, hi, elem_begin: int, n_elems: int,
+                         device: int = 0):
+        """Reduce-scatter variant, step 2a: per INTER key the minimum element
+        of [elem_begin, elem_begin + n_elems) from the reduced tables `lo` /
+        `hi` (int32 CUDA tensors of n_elems * n_sites entries, produced on
+        torch's current stream — the context's stream waits for it).
+        Returns uint64 numpy [3 * n_locs^2], 2^64 - 1 where none."""
+        import numpy as np
+        n_locs = max(len(spec.lowered["locs"]), 1)
+        ke = np.zeros(3 * n_locs * n_locs, dtype=np.uint64)
+        if n_elems:
+            self.wait_torch_stream(device)
+        rc = self._lib.hgrd_gpu_shard_inter_scan(
+            self._ctx, ctypes.byref(spec.launch), lo.data_ptr() if n_elems else None,
+            hi.data_ptr() if n_elems else None, elem_begin, n_elems,
+            ke.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(ke))
+        if rc == HGRD_GPU_ENOTSUP:
+            raise NotShardable(self._lib.hgrd_gpu_last_error(self._ctx).decode())
+        if rc:
+            self._err("shard_inter_scan", rc)
+        return ke
+
+    def shard_inter_records(self, spec: LaunchSpec, sh: Shard, key_elem):
+        """Step 2b: this shard's packed records of the realised INTER keys'
+        first-found elements (`key_elem`: the MIN-reduced scan tables)."""
+        import numpy as np
+        key_elem = np.ascontiguousarray(key_elem, dtype=np.uint64)
+        cap = 1 << 16
+        while True:
+            keys = np.zeros(cap, dtype=np.uint64)
+            vals = np.zeros(cap, dtype=np.uint32)
+            n = ctypes.c_uint64()
+            rc = self._lib.hgrd_gpu_shard_inter_records(
+                self._ctx, ctypes.byref(spec.launch), ctypes.byref(sh),
+                key_elem.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(key_elem),
+                keys.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                vals.ctypes.data_as(ctypes.POINTER(c_uint32)), cap, ctypes.byref(n))
+            if rc == -7:  # E2BIG
+                cap = max(cap * 2, int(n.value))
+                continue
+            if rc == HGRD_GPU_ENOTSUP:
+                raise NotShardable(self._lib.hgrd_gpu_last_error(self._ctx).decode())
+            if rc:
+                self._err("shard_inter_records", rc)
+            return keys[: n.value].copy(), vals[: n.value].copy()
 
     def shard_inter(self, spec: LaunchSpec, sh: Shard):
         """After the all-reduce: this shard's packed records of the realised

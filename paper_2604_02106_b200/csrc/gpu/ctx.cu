@@ -9,6 +9,7 @@
 #include "device.cuh"
 #include "expand.cuh"
 #include "fused.cuh"
+#include "batch.cuh"
 #include "affine.hpp"
 #include "jit.hpp"
 
@@ -137,6 +138,9 @@ struct hgrd_gpu_ctx {
   DevVec<uint32_t> interTab;           // fused pass 2: (element, site) block sets
   DevVec<unsigned long long> interKeyElem;
   DevVec<uint64_t> targets;
+  DevVec<unsigned char> batchBlob;     // hgrd_gpu_check_batch: descriptors | outputs
+  unsigned char *hBatch = nullptr;     // pinned staging of the batch blob / outputs
+  size_t hBatchCap = 0;
   bool fusedEnabled = true;
   // NVRTC specialisation: 0 off, 1 auto (large launches), 2 always
   int jitMode = 1;
@@ -1727,38 +1731,62 @@ int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
   return 0;
 }
 
-int shardInter(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const hgrd_gpu_shard *Sh,
-               uint64_t *keys, uint32_t *vals, uint64_t cap, uint64_t *nOut) {
+// INTER keys of one element range of the (reduced) summary tables: per key
+// its minimum element in [e0, e0 + nE) into keyElem (host, ~0: none).
+int shardInterScan(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const uint32_t *lo,
+                   const uint32_t *hi, uint64_t e0, uint64_t nE, uint64_t *keyElem,
+                   uint32_t nKeysCap) {
+  ShardSetup S;
+  int rc = shardPrepare(c, L, 0, 0, S);
+  if (rc < 0)
+    return rc;
+  const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+  const int nKeys = 3 * nLocs * nLocs;
+  if (nKeysCap < static_cast<uint32_t>(nKeys)) {
+    c->err = "key table too small";
+    return HGRD_GPU_E2BIG;
+  }
+  if (e0 + nE > S.P.totalW) {
+    c->err = "element range outside the launch's written buffers";
+    return HGRD_GPU_EINVAL;
+  }
+  NEED(c->interKeyElem, static_cast<size_t>(nKeys));
+  CK(cudaMemsetAsync(c->interKeyElem.p, 0xff, 8 * static_cast<size_t>(nKeys), c->st));
+  if (nE) {
+    StageTimer t(c, "k_inter_scan_minmax");
+    k_inter_scan_minmax<<<static_cast<unsigned>((nE + 255) / 256), 256, 0, c->st>>>(
+        lo, hi, nE, e0, static_cast<int>(L.n_sites), S.D.sites, S.D.confInter, nLocs,
+        c->interKeyElem.p);
+    CK(cudaGetLastError());
+    ++c->kernelLaunches;
+  }
+  CK(cudaMemcpyAsync(keyElem, c->interKeyElem.p, 8 * static_cast<size_t>(nKeys),
+                     cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += 8 * static_cast<size_t>(nKeys);
+  CK(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+// This shard's packed records of the realised INTER keys' first-found
+// elements (keyElem: the ranks' per-key minima, MIN-reduced).
+int shardInterRecords(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const hgrd_gpu_shard *Sh,
+                      const uint64_t *keyElem, uint32_t nKeysIn, uint64_t *keys, uint32_t *vals,
+                      uint64_t cap, uint64_t *nOut) {
   *nOut = 0;
   ShardSetup S;
   int rc = shardPrepare(c, L, Sh->block_begin, Sh->block_end, S);
   if (rc < 0)
     return rc;
-  const uint64_t nTab = S.P.totalW * static_cast<uint64_t>(L.n_sites);
-  if (Sh->inter_n == 0)
-    return 0; // no buffer reachable from two blocks
-  if (Sh->inter_n != nTab || c->shardLo.cap < nTab) {
-    c->err = "shard INTER tables do not match the launch";
-    return HGRD_GPU_EINVAL;
-  }
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
   const int nKeys = 3 * nLocs * nLocs;
-  NEED(c->interKeyElem, static_cast<size_t>(nKeys));
-  CK(cudaMemsetAsync(c->interKeyElem.p, 0xff, 8 * static_cast<size_t>(nKeys), c->st));
-  k_inter_scan_minmax<<<static_cast<unsigned>((S.P.totalW + 255) / 256), 256, 0, c->st>>>(
-      c->shardLo.p, c->shardHi.p, S.P.totalW, static_cast<int>(L.n_sites), S.D.sites,
-      S.D.confInter, nLocs, c->interKeyElem.p);
-  CK(cudaGetLastError());
-  ++c->kernelLaunches;
-  std::vector<unsigned long long> ke(static_cast<size_t>(nKeys));
-  CK(cudaMemcpyAsync(ke.data(), c->interKeyElem.p, 8 * static_cast<size_t>(nKeys),
-                     cudaMemcpyDeviceToHost, c->st));
-  c->d2hBytes += 8 * static_cast<size_t>(nKeys);
-  CK(cudaStreamSynchronize(c->st));
+  if (nKeysIn < static_cast<uint32_t>(nKeys)) {
+    c->err = "key table too small";
+    return HGRD_GPU_EINVAL;
+  }
   std::vector<uint64_t> targets;
   for (int K = 0; K < nKeys; K += 3)
-    if (ke[static_cast<size_t>(K)] != ~0ull)
-      targets.push_back(ke[static_cast<size_t>(K)]);
+    if (keyElem[K] != ~0ull)
+      targets.push_back(keyElem[K]);
   std::sort(targets.begin(), targets.end());
   targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
   if (targets.empty())
@@ -1833,6 +1861,30 @@ int shardInter(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const hgrd_gpu_shard *
   return HGRD_GPU_ENOTSUP;
 }
 
+
+// All-reduce variant: the caller reduced the whole tables in place.
+int shardInter(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const hgrd_gpu_shard *Sh,
+               uint64_t *keys, uint32_t *vals, uint64_t cap, uint64_t *nOut) {
+  *nOut = 0;
+  ShardSetup S;
+  int rc = shardPrepare(c, L, Sh->block_begin, Sh->block_end, S);
+  if (rc < 0)
+    return rc;
+  const uint64_t nTab = S.P.totalW * static_cast<uint64_t>(L.n_sites);
+  if (Sh->inter_n == 0)
+    return 0; // no buffer reachable from two blocks
+  if (Sh->inter_n != nTab || c->shardLo.cap < nTab) {
+    c->err = "shard INTER tables do not match the launch";
+    return HGRD_GPU_EINVAL;
+  }
+  const uint32_t nKeys = 3 * std::max<uint32_t>(L.n_locs, 1) * std::max<uint32_t>(L.n_locs, 1);
+  std::vector<uint64_t> ke(nKeys);
+  rc = shardInterScan(c, L, c->shardLo.p, c->shardHi.p, 0, S.P.totalW, ke.data(), nKeys);
+  if (rc < 0)
+    return rc;
+  return shardInterRecords(c, L, Sh, ke.data(), nKeys, keys, vals, cap, nOut);
+}
+
 int shardDetect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const uint64_t *keys,
                 const uint32_t *vals, uint64_t n, hgrd_gpu_result *R) {
   resetResult(R);
@@ -1850,6 +1902,339 @@ int shardDetect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const uint64_t *keys,
     c->h2dBytes += 12 * n;
   }
   return detect(c, L, S.D, S.o, n, false, false, R, /*kindMask=*/1);
+}
+
+// ---------------------------------------------------------------------------
+// Batched check of many small launches (batch.cuh): one H2D of every
+// descriptor, one k_batch launch, one D2H of every launch's counters and
+// races.
+
+struct BatchPlan {
+  bool ok = false;
+  uint32_t R = 0;
+  std::vector<ParamDev> params;
+  std::vector<SiteDev> sites;
+  std::vector<uint64_t> confInter, confIntra, wBase;
+  std::vector<int32_t> wHandle;
+  std::vector<char> needData; // per buffer: a value-needed load reads it
+  uint64_t totalW = 0;
+};
+
+void planBatchLaunch(const hgrd_gpu_batch_launch &B, BatchPlan &P) {
+  const hgrd_gpu_launch &L = B.launch;
+  std::string why;
+  if (!validLaunch(L, why))
+    return;
+  if (L.flags & (HGRD_LAUNCH_SEQUENTIAL | HGRD_LAUNCH_PAIRWISE | HGRD_LAUNCH_GENERAL))
+    return;
+  const int64_t tpb = L.block[0] * L.block[1] * L.block[2];
+  const int64_t nBlocks = L.grid[0] * L.grid[1] * L.grid[2];
+  if (L.n_regs > static_cast<uint32_t>(kMaxRegs) || L.n_sites > static_cast<uint32_t>(kMaxSites) ||
+      L.n_locs > 32 || nBlocks > kBatchMaxBlocks || tpb > kBatchMaxThreads ||
+      nBlocks * tpb > kBatchMaxThreads || L.warp_size >= (int64_t(1) << 31))
+    return;
+  const uint32_t nb = B.n_buffers;
+  auto bufOf = [&](int32_t param) -> int32_t {
+    if (param < 0 || static_cast<uint32_t>(param) >= L.n_params)
+      return -1;
+    const int32_t h = L.param_handle[param];
+    return (h >= 0 && static_cast<uint32_t>(h) < nb) ? h : -1;
+  };
+  std::vector<char> written(nb, 0);
+  for (uint32_t s = 0; s < L.n_sites; ++s)
+    if (L.sites[s].kind != HGRD_SITE_LOAD && bufOf(L.sites[s].param) >= 0)
+      written[static_cast<size_t>(bufOf(L.sites[s].param))] = 1;
+  std::vector<uint64_t> base(nb, 0);
+  std::vector<int> windex(nb, 0);
+  for (uint32_t h = 0; h < nb; ++h)
+    if (written[h]) {
+      windex[h] = static_cast<int>(P.wBase.size()) + 1;
+      base[h] = P.totalW;
+      P.wBase.push_back(P.totalW);
+      P.wHandle.push_back(static_cast<int32_t>(h));
+      P.totalW += static_cast<uint64_t>(std::max<int64_t>(B.buffer_elems[h], 0));
+    }
+  if (P.wBase.empty()) {
+    P.wBase.push_back(0);
+    P.wHandle.push_back(-1);
+  }
+  if (P.totalW >= 0xFFFFFFFFull || P.wBase.size() > static_cast<size_t>(kMaxWritten))
+    return;
+  P.needData.assign(nb, 0);
+  uint32_t recInsns = 0;
+  bool loops = false;
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    const auto &I = L.code[pc];
+    if (I.op == HGRD_OP_LOAD && (I.sub & 1)) {
+      const int32_t h = bufOf(L.sites[static_cast<size_t>(I.imm)].param);
+      if (h >= 0)
+        P.needData[static_cast<size_t>(h)] = 1;
+    }
+    if ((I.op == HGRD_OP_LOAD || I.op == HGRD_OP_STORE || I.op == HGRD_OP_ATOMIC) &&
+        bufOf(L.sites[static_cast<size_t>(I.imm)].param) >= 0 &&
+        written[static_cast<size_t>(bufOf(L.sites[static_cast<size_t>(I.imm)].param))])
+      ++recInsns;
+    if (I.op == HGRD_OP_JMP && I.imm <= static_cast<int64_t>(pc))
+      loops = true;
+  }
+  P.R = loops ? 0 : recInsns;
+  if (!loops && static_cast<uint64_t>(nBlocks * tpb) * recInsns > BatchSmem::kCap)
+    return;
+  P.params.resize(std::max<uint32_t>(L.n_params, 1));
+  for (uint32_t p = 0; p < L.n_params; ++p) {
+    ParamDev d{};
+    const int32_t h = bufOf(static_cast<int32_t>(p));
+    d.handle = h;
+    if (h >= 0) {
+      d.size = B.buffer_elems[h];
+      d.written = windex[static_cast<size_t>(h)];
+      d.elemBase = base[static_cast<size_t>(h)];
+    }
+    P.params[p] = d;
+  }
+  P.sites.resize(std::max<uint32_t>(L.n_sites, 1));
+  for (uint32_t s = 0; s < L.n_sites; ++s) {
+    SiteDev d{};
+    d.param = L.sites[s].param;
+    d.loc = L.sites[s].loc;
+    d.kind = L.sites[s].kind;
+    d.aop = L.sites[s].atomic_op;
+    d.scope = L.sites[s].scope;
+    const int32_t h = bufOf(d.param);
+    d.record = (h >= 0 && written[static_cast<size_t>(h)]) ? 1 : 0;
+    P.sites[s] = d;
+  }
+  P.confInter.assign(P.sites.size(), 0);
+  P.confIntra.assign(P.sites.size(), 0);
+  for (uint32_t a = 0; a < L.n_sites; ++a) // reference :752-758, as planLaunch
+    for (uint32_t b = 0; b < L.n_sites; ++b) {
+      const auto &X = L.sites[a];
+      const auto &Y = L.sites[b];
+      const bool write = X.kind != HGRD_SITE_LOAD || Y.kind != HGRD_SITE_LOAD;
+      const bool bothAtomic = X.kind == HGRD_SITE_ATOMIC && Y.kind == HGRD_SITE_ATOMIC;
+      const bool devBoth = X.scope == HGRD_SCOPE_DEVICE && Y.scope == HGRD_SCOPE_DEVICE;
+      const bool blkBoth = X.scope != HGRD_SCOPE_NONE && Y.scope != HGRD_SCOPE_NONE;
+      if (write && !(bothAtomic && devBoth))
+        P.confInter[a] |= 1ull << b;
+      if (write && !(bothAtomic && blkBoth))
+        P.confIntra[a] |= 1ull << b;
+    }
+  P.ok = true;
+}
+
+template <class T> size_t batchPut(std::vector<unsigned char> &blob, const T *src, size_t n) {
+  const size_t at = align16(blob.size());
+  blob.resize(at + sizeof(T) * n);
+  if (n)
+    std::memcpy(blob.data() + at, src, sizeof(T) * n);
+  return at;
+}
+
+int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
+               hgrd_gpu_result *R) {
+  for (uint32_t i = 0; i < n; ++i) {
+    resetResult(&R[i]);
+    R[i].mode = HGRD_RESULT_UNCHECKED;
+  }
+  // host blob: [BatchLaunch x m] | per launch: code (shared), sites, params,
+  // regs, masks, wBase | buffer contents | next counter; device pointers
+  // are fixed up once the blob's device address is known
+  std::vector<unsigned char> blob;
+  std::vector<uint32_t> idx; // batch entry -> launch
+  std::vector<BatchPlan> plans(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    planBatchLaunch(BL[i], plans[i]);
+    if (plans[i].ok)
+      idx.push_back(i);
+  }
+  const uint32_t m = static_cast<uint32_t>(idx.size());
+  if (m == 0)
+    return 0;
+  blob.resize(align16(sizeof(BatchLaunch) * m));
+  std::vector<BatchLaunch> bl(m);
+  struct Fix {
+    size_t code, sites, params, regs, cInter, cIntra, wBase;
+  };
+  std::vector<Fix> fix(m);
+  std::map<const hgrd_gpu_insn *, size_t> codeAt;
+  std::vector<std::vector<size_t>> dataAt(m); // per launch, per param: blob offset of contents
+  int maxKeys = 3, maxCode = 1, maxSites = 1, maxParams = 1, maxW = 1;
+  uint32_t raceOff = 0;
+  for (uint32_t k = 0; k < m; ++k) {
+    const hgrd_gpu_batch_launch &B = BL[idx[k]];
+    const hgrd_gpu_launch &L = B.launch;
+    BatchPlan &P = plans[idx[k]];
+    auto ci = codeAt.find(L.code);
+    if (ci == codeAt.end())
+      ci = codeAt.emplace(L.code, batchPut(blob, L.code, L.n_code)).first;
+    fix[k].code = ci->second;
+    fix[k].sites = batchPut(blob, P.sites.data(), P.sites.size());
+    std::vector<int64_t> regs(std::max<uint32_t>(L.n_regs, 1), 0);
+    if (L.n_regs)
+      std::memcpy(regs.data(), L.reg_init, 8 * L.n_regs);
+    fix[k].regs = batchPut(blob, regs.data(), regs.size());
+    fix[k].cInter = batchPut(blob, P.confInter.data(), P.confInter.size());
+    fix[k].cIntra = batchPut(blob, P.confIntra.data(), P.confIntra.size());
+    fix[k].wBase = batchPut(blob, P.wBase.data(), P.wBase.size());
+    // value-needed buffers: their launch-entry contents (zeros when absent)
+    std::vector<size_t> bufAt(B.n_buffers, SIZE_MAX);
+    for (uint32_t h = 0; h < B.n_buffers; ++h) {
+      if (!P.needData[h] || B.buffer_elems[h] <= 0)
+        continue;
+      const size_t at = align16(blob.size());
+      const size_t bytes = 8 * static_cast<size_t>(B.buffer_elems[h]);
+      blob.resize(at + bytes);
+      if (B.buffer_data && B.buffer_data[h])
+        std::memcpy(blob.data() + at, B.buffer_data[h], bytes);
+      else
+        std::memset(blob.data() + at, 0, bytes);
+      bufAt[h] = at;
+    }
+    dataAt[k].assign(P.params.size(), SIZE_MAX);
+    for (uint32_t p = 0; p < L.n_params; ++p)
+      if (P.params[p].handle >= 0)
+        dataAt[k][p] = bufAt[static_cast<size_t>(P.params[p].handle)];
+    fix[k].params = batchPut(blob, P.params.data(), P.params.size());
+    LaunchDev &D = bl[k].L;
+    D = LaunchDev{};
+    D.nCode = static_cast<int>(L.n_code);
+    D.nRegs = static_cast<int>(L.n_regs);
+    D.nSites = static_cast<int>(L.n_sites);
+    D.nParams = static_cast<int>(L.n_params);
+    D.nLocs = static_cast<int>(L.n_locs);
+    for (int d = 0; d < 3; ++d) {
+      D.grid[d] = L.grid[d];
+      D.block[d] = L.block[d];
+    }
+    D.ws = L.warp_size;
+    D.tpb = L.block[0] * L.block[1] * L.block[2];
+    D.nBlocks = L.grid[0] * L.grid[1] * L.grid[2];
+    D.nThreads = D.nBlocks * D.tpb;
+    D.stepBudget = L.step_budget;
+    D.small = true;
+    D.dTpb = FastDiv::make(static_cast<uint32_t>(D.tpb));
+    D.dBx = FastDiv::make(static_cast<uint32_t>(L.block[0]));
+    D.dBxBy = FastDiv::make(static_cast<uint32_t>(L.block[0] * L.block[1]));
+    D.dGx = FastDiv::make(static_cast<uint32_t>(L.grid[0]));
+    D.dGxGy = FastDiv::make(static_cast<uint32_t>(L.grid[0] * L.grid[1]));
+    D.dWs = FastDiv::make(static_cast<uint32_t>(L.warp_size));
+    D.threadEnd = D.nThreads;
+    const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+    bl[k].nW = static_cast<int32_t>(P.wBase.size());
+    bl[k].nLocs = nLocs;
+    bl[k].R = P.R;
+    bl[k].raceOff = raceOff;
+    raceOff += static_cast<uint32_t>(3 * nLocs * nLocs);
+    maxKeys = std::max(maxKeys, 3 * nLocs * nLocs);
+    maxCode = std::max(maxCode, D.nCode);
+    maxSites = std::max(maxSites, std::max(D.nSites, 1));
+    maxParams = std::max(maxParams, std::max(D.nParams, 1));
+    maxW = std::max(maxW, bl[k].nW);
+  }
+  const size_t nextAt = batchPut(blob, &raceOff, 0);
+  blob.resize(nextAt + 16);
+  std::memset(blob.data() + nextAt, 0, 16);
+  const size_t h2d = blob.size();
+  const size_t outAt = align16(h2d);
+  const size_t racesAt = align16(outAt + sizeof(BatchOut) * m);
+  const size_t total = racesAt + sizeof(hgrd_gpu_race) * std::max<uint32_t>(raceOff, 1);
+  NEED(c->batchBlob, total);
+  unsigned char *dev = c->batchBlob.p;
+  for (uint32_t k = 0; k < m; ++k) {
+    LaunchDev &D = bl[k].L;
+    D.code = reinterpret_cast<const hgrd_gpu_insn *>(dev + fix[k].code);
+    D.sites = reinterpret_cast<const SiteDev *>(dev + fix[k].sites);
+    D.params = reinterpret_cast<const ParamDev *>(dev + fix[k].params);
+    D.regInit = reinterpret_cast<const int64_t *>(dev + fix[k].regs);
+    D.confInter = reinterpret_cast<const uint64_t *>(dev + fix[k].cInter);
+    D.confIntra = reinterpret_cast<const uint64_t *>(dev + fix[k].cIntra);
+    bl[k].wBase = reinterpret_cast<const uint64_t *>(dev + fix[k].wBase);
+    auto *pd = reinterpret_cast<ParamDev *>(blob.data() + fix[k].params);
+    for (size_t p = 0; p < dataAt[k].size(); ++p)
+      pd[p].ptr = dataAt[k][p] == SIZE_MAX ? nullptr
+                                           : reinterpret_cast<int64_t *>(dev + dataAt[k][p]);
+  }
+  std::memcpy(blob.data(), bl.data(), sizeof(BatchLaunch) * m);
+  if (c->hBatchCap < std::max(h2d, total - outAt)) {
+    if (c->hBatch)
+      CK(cudaFreeHost(c->hBatch));
+    c->hBatch = nullptr;
+    c->hBatchCap = std::max(std::max(h2d, total - outAt), size_t(1) << 20);
+    CK(cudaMallocHost(&c->hBatch, c->hBatchCap));
+  }
+  std::memcpy(c->hBatch, blob.data(), h2d);
+  CK(cudaMemcpyAsync(dev, c->hBatch, h2d, cudaMemcpyHostToDevice, c->st));
+  c->h2dBytes += h2d;
+
+  const int keysPad = (maxKeys + 3) & ~3;
+  const size_t smem = align16(sizeof(BatchSmem)) + 8 * static_cast<size_t>(keysPad) +
+                      sizeof(hgrd_gpu_insn) * maxCode + sizeof(SiteDev) * maxSites +
+                      sizeof(ParamDev) * maxParams + 16 * static_cast<size_t>(maxSites) +
+                      8 * static_cast<size_t>(maxW) + 64;
+  if (smem > 200 * 1024) {
+    c->err = "batch launches too large for shared memory";
+    return HGRD_GPU_ENOTSUP;
+  }
+  const void *fn = reinterpret_cast<const void *>(k_batch);
+  if (c->smemOptIn.insert(fn).second) {
+    cudaFuncAttributes fa{};
+    CK(cudaFuncGetAttributes(&fa, fn));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            227 * 1024 - static_cast<int>(fa.sharedSizeBytes)));
+  }
+  int &perSM = c->occupancy[std::make_pair(fn, smem)];
+  if (perSM == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSM, fn, kBatchThreads, smem));
+    perSM = std::max(perSM, 1);
+  }
+  BatchArgs A{};
+  A.launches = reinterpret_cast<const BatchLaunch *>(dev);
+  A.n = m;
+  A.out = reinterpret_cast<BatchOut *>(dev + outAt);
+  A.races = reinterpret_cast<hgrd_gpu_race *>(dev + racesAt);
+  A.next = reinterpret_cast<unsigned *>(dev + nextAt);
+  A.maxKeys = maxKeys;
+  A.maxCode = maxCode;
+  A.maxSites = maxSites;
+  A.maxParams = maxParams;
+  A.maxW = maxW;
+  const unsigned grid =
+      static_cast<unsigned>(std::min<int64_t>(m, static_cast<int64_t>(c->nSM) * perSM));
+  {
+    StageTimer t(c, "k_batch");
+    void *args[] = {&A};
+    CK(cudaLaunchKernel(fn, dim3(grid), dim3(kBatchThreads), args, smem, c->st));
+  }
+  CK(cudaGetLastError());
+  ++c->kernelLaunches;
+  const size_t d2h = total - outAt;
+  CK(cudaMemcpyAsync(c->hBatch, dev + outAt, d2h, cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += d2h;
+  CK(cudaStreamSynchronize(c->st));
+  const BatchOut *out = reinterpret_cast<const BatchOut *>(c->hBatch);
+  const hgrd_gpu_race *races = reinterpret_cast<const hgrd_gpu_race *>(c->hBatch + (racesAt - outAt));
+  for (uint32_t k = 0; k < m; ++k) {
+    const BatchOut &o = out[k];
+    hgrd_gpu_result &r = R[idx[k]];
+    if (o.traps || (o.flags & (kFlagFusedOverflow | kFlagAbort)))
+      continue; // the ordered path decides (traps in canonical order, the abort statement)
+    if (o.nRaces > r.race_cap) {
+      r.n_races = o.nRaces;
+      continue;
+    }
+    const BatchPlan &P = plans[idx[k]];
+    for (uint32_t q = 0; q < o.nRaces; ++q) {
+      hgrd_gpu_race x = races[bl[k].raceOff + q];
+      x.handle = P.wHandle[static_cast<size_t>(x.handle)];
+      r.races[q] = x;
+    }
+    r.n_races = o.nRaces;
+    r.steps = static_cast<int64_t>(o.steps);
+    r.instances = o.instances;
+    r.records = o.records;
+    r.mode = 0;
+  }
+  return 0;
 }
 } // namespace
 
@@ -1914,6 +2299,10 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
     cudaFreeHost(c->hTraps);
   if (c->hResult)
     cudaFreeHost(c->hResult);
+  if (c->hBatch)
+    cudaFreeHost(c->hBatch);
+  if (c->batchBlob.p)
+    cudaFree(c->batchBlob.p);
   hgrdgpu::jit::destroy(c->jit);
   for (cudaEvent_t e : c->evPool)
     cudaEventDestroy(e);
@@ -2086,6 +2475,54 @@ int hgrd_gpu_shard_check(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, hgrd_gp
   }
   CK(cudaSetDevice(c->device));
   return shardCheck(c, *launch, shard, result);
+}
+
+int hgrd_gpu_check_batch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *launches, uint32_t n,
+                         hgrd_gpu_result *results) {
+  if (!c || (n && (!launches || !results)))
+    return HGRD_GPU_EINVAL;
+  for (uint32_t i = 0; i < n; ++i)
+    if (!launches[i].buffer_elems && launches[i].n_buffers)
+      return HGRD_GPU_EINVAL;
+  CK(cudaSetDevice(c->device));
+  try {
+    return checkBatch(c, launches, n, results);
+  } catch (const std::exception &e) {
+    c->err = e.what();
+    return HGRD_GPU_ENOMEM;
+  }
+}
+
+void *hgrd_gpu_stream(hgrd_gpu_ctx *c) { return c ? static_cast<void *>(c->st) : nullptr; }
+
+int hgrd_gpu_shard_inter_scan(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, const void *lo,
+                              const void *hi, uint64_t elem_begin, uint64_t n_elems,
+                              uint64_t *key_elem, uint32_t n_keys) {
+  if (!c || !launch || !key_elem || (n_elems && (!lo || !hi)))
+    return HGRD_GPU_EINVAL;
+  std::string why;
+  if (!validLaunch(*launch, why)) {
+    c->err = why;
+    return HGRD_GPU_EINVAL;
+  }
+  CK(cudaSetDevice(c->device));
+  return shardInterScan(c, *launch, static_cast<const uint32_t *>(lo),
+                        static_cast<const uint32_t *>(hi), elem_begin, n_elems, key_elem, n_keys);
+}
+
+int hgrd_gpu_shard_inter_records(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
+                                 const hgrd_gpu_shard *shard, const uint64_t *key_elem,
+                                 uint32_t n_keys, uint64_t *keys, uint32_t *vals, uint64_t cap,
+                                 uint64_t *n) {
+  if (!c || !launch || !shard || !key_elem || !n || (cap && (!keys || !vals)))
+    return HGRD_GPU_EINVAL;
+  std::string why;
+  if (!validLaunch(*launch, why)) {
+    c->err = why;
+    return HGRD_GPU_EINVAL;
+  }
+  CK(cudaSetDevice(c->device));
+  return shardInterRecords(c, *launch, shard, key_elem, n_keys, keys, vals, cap, n);
 }
 
 int hgrd_gpu_shard_inter(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,

@@ -139,8 +139,9 @@ constexpr uint32_t kShardEmpty = 0x7F7F7F7Fu;
 // blocks iff some block of a's set differs from some block of b's set
 // (a == b: two distinct blocks).  lo = kShardEmpty marks an empty set.  Per
 // key the minimum element (the reference's first-found element, :745).
+// (lo / hi: the tables of elements [e0, e0 + nElems))
 __global__ void k_inter_scan_minmax(const uint32_t *lo, const uint32_t *hi, uint64_t nElems,
-                                    int nSites, const SiteDev *sites, const uint64_t *confInter,
+                                    uint64_t e0, int nSites, const SiteDev *sites, const uint64_t *confInter,
                                     int nLocs, unsigned long long *keyElem) {
   const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= nElems)
@@ -169,8 +170,8 @@ __global__ void k_inter_scan_minmax(const uint32_t *lo, const uint32_t *hi, uint
         kb = t;
       }
       const int K = (ka * nLocs + kb) * 3; // kind 0: INTER-BLOCK
-      if (__ldcg(&keyElem[K]) > e)
-        atomicMin(&keyElem[K], static_cast<unsigned long long>(e));
+      if (__ldcg(&keyElem[K]) > e0 + e)
+        atomicMin(&keyElem[K], static_cast<unsigned long long>(e0 + e));
     }
   }
 }

@@ -20,6 +20,7 @@
 // that writes memory runs SEQUENTIAL, so buffers are always exact.
 #include "host.hpp"
 
+#include <atomic>
 #include <thread>
 
 #include <algorithm>
@@ -255,12 +256,86 @@ struct BackendFail {
   std::string msg;
 };
 
+struct SpecFail {}; // a speculative host run needs what only a real check gives
+
+// A launch of a speculative host run (enumerateVerdictBatched): everything
+// hgrd_gpu_check_batch needs, kept until the batch is checked.
+struct PendingLaunch {
+  const LoweredKernel *lk = nullptr;
+  int launchIndex = 0;
+  std::array<int64_t, 3> grid{}, block{};
+  int64_t warpSize = 32, budget = 0;
+  std::vector<int64_t> regInit;
+  std::vector<int32_t> paramHandle;
+  std::vector<int64_t> bufElems;             // every buffer of the run
+  std::vector<std::vector<int64_t>> bufData; // value-needed buffers' contents (empty: zeros)
+};
+
+using SeenKeys = std::set<std::tuple<int, int, int, int, int>>;
+
+void decomposeThread(int64_t thread, const std::array<int64_t, 3> &grid,
+                     const std::array<int64_t, 3> &block, int64_t tpb, int64_t (&b)[3],
+                     int64_t (&t)[3]) {
+  int64_t bl = thread / tpb, tl = thread % tpb;
+  b[0] = bl % grid[0];
+  b[1] = (bl / grid[0]) % grid[1];
+  b[2] = bl / (grid[0] * grid[1]);
+  t[0] = tl % block[0];
+  t[1] = (tl / block[0]) % block[1];
+  t[2] = tl / (block[0] * block[1]);
+}
+
+// detectRaces' tail (reference :766-780): a launch's races in the run's
+// report, first insert of (locA, locB, kind) across the run's launches.
+void mergeLaunchRaces(RunResult &res, SeenKeys &seen, const LoweredKernel &lk,
+                      const std::array<int64_t, 3> &grid, const std::array<int64_t, 3> &block,
+                      const hgrd_gpu_race *races, uint32_t n, int launchIndex) {
+  const int64_t tpb = block[0] * block[1] * block[2];
+  for (uint32_t i = 0; i < n; ++i) {
+    const hgrd_gpu_race &g = races[i];
+    Race r;
+    r.locA = lk.locs[static_cast<size_t>(g.loc_a)];
+    r.locB = lk.locs[static_cast<size_t>(g.loc_b)];
+    r.kind = g.kind;
+    r.array = lk.siteArray[static_cast<size_t>(g.site_x)];
+    r.address = g.index;
+    r.launch = launchIndex;
+    r.threadX = g.thread_x;
+    r.threadY = g.thread_y;
+    r.seqX = g.seq_x;
+    r.seqY = g.seq_y;
+    decomposeThread(g.thread_x, grid, block, tpb, r.blockX, r.tidX);
+    decomposeThread(g.thread_y, grid, block, tpb, r.blockY, r.tidY);
+    auto key = std::make_tuple(r.locA.line, r.locA.col, r.locB.line, r.locB.col, r.kind);
+    if (seen.insert(key).second)
+      res.races.push_back(std::move(r));
+  }
+}
+
+// reference operator< (src/oracle.cpp:9-19): the run's final order (:76)
+void sortRaces(std::vector<Race> &races) {
+  std::sort(races.begin(), races.end(), [](const Race &a, const Race &b) {
+    if (!(a.locA == b.locA))
+      return a.locA < b.locA;
+    if (!(a.locB == b.locB))
+      return a.locB < b.locB;
+    if (a.kind != b.kind)
+      return a.kind < b.kind;
+    if (a.array != b.array)
+      return a.array < b.array;
+    return a.address < b.address;
+  });
+}
+
 class HostRun {
 public:
   HostRun(CompiledProgram &cp, const ExecConfig &cfg, LaunchBackend &be,
-          bool conservative)
+          bool conservative, std::vector<PendingLaunch> *spec = nullptr)
       : cp_(cp), prog_(*cp.program), cfg_(cfg), be_(be),
-        conservative_(conservative) {}
+        conservative_(conservative), spec_(spec) {}
+
+  bool budgetAborted() const { return budgetAbort_; }
+  int64_t steps() const { return steps_; }
 
   RunResult run() {
     res_.indirectIndexing = cp_.indirectIndexing;
@@ -287,17 +362,7 @@ public:
     } catch (const BackendFail &bf) {
       return fail(bf.code, bf.msg);
     }
-    std::sort(res_.races.begin(), res_.races.end(), [](const Race &a, const Race &b) {
-      if (!(a.locA == b.locA))
-        return a.locA < b.locA;
-      if (!(a.locB == b.locB))
-        return a.locB < b.locB;
-      if (a.kind != b.kind)
-        return a.kind < b.kind;
-      if (a.array != b.array)
-        return a.array < b.array;
-      return a.address < b.address;
-    });
+    sortRaces(res_.races);
     return std::move(res_);
   }
 
@@ -337,6 +402,7 @@ private:
   void step(const Loc &loc) {
     if (++steps_ > cfg_.maxSteps) {
       trap(loc, "step budget exhausted");
+      budgetAbort_ = true;
       throw Abort{};
     }
   }
@@ -664,6 +730,36 @@ private:
           throw NeedConservative{};
       }
     }
+    if (spec_) { // speculative run: keep the launch for the batch, assume no traps
+      if (sequential || lk.hasLocks)
+        throw SpecFail{};
+      PendingLaunch p;
+      p.lk = &lk;
+      p.launchIndex = launchIndex;
+      p.grid = grid;
+      p.block = block;
+      p.warpSize = cfg_.warpSize;
+      p.budget = cfg_.maxSteps;
+      p.regInit.assign(lk.nRegs, 0);
+      for (size_t i = 0; i < lk.paramReg.size(); ++i)
+        if (lk.paramReg[i] >= 0)
+          p.regInit[static_cast<size_t>(lk.paramReg[i])] = scalarVal[i];
+      p.paramHandle = paramHandle;
+      p.bufElems.resize(bufs_.size());
+      p.bufData.resize(bufs_.size());
+      for (size_t h = 0; h < bufs_.size(); ++h)
+        p.bufElems[h] = bufs_[h].elems;
+      for (size_t i = 0; i < lk.sites.size(); ++i) { // launch-entry contents of value-needed loads
+        const int32_t h = handleOf(lk.sites[i]);
+        if (lk.sites[i].kind == HGRD_SITE_LOAD && h >= 0 && lk.siteValueNeeded[i])
+          p.bufData[static_cast<size_t>(h)] = bufs_[static_cast<size_t>(h)].host;
+      }
+      spec_->push_back(std::move(p));
+      ++res_.stats.parLaunches;
+      for (int32_t h : written)
+        bufs_[static_cast<size_t>(h)].stale = true;
+      return;
+    }
     // Bring host-side writes to the device.
     for (size_t h = 0; h < bufs_.size(); ++h) {
       Buf &b = bufs_[h];
@@ -743,38 +839,7 @@ private:
       else
         b.stale = true;
     }
-    const int64_t tpb = block[0] * block[1] * block[2];
-    for (uint32_t i = 0; i < R.n_races; ++i) {
-      const hgrd_gpu_race &g = races[i];
-      Race r;
-      r.locA = lk.locs[static_cast<size_t>(g.loc_a)];
-      r.locB = lk.locs[static_cast<size_t>(g.loc_b)];
-      r.kind = g.kind;
-      r.array = lk.siteArray[static_cast<size_t>(g.site_x)];
-      r.address = g.index;
-      r.launch = launchIndex;
-      r.threadX = g.thread_x;
-      r.threadY = g.thread_y;
-      r.seqX = g.seq_x;
-      r.seqY = g.seq_y;
-      decompose(g.thread_x, grid, block, tpb, r.blockX, r.tidX);
-      decompose(g.thread_y, grid, block, tpb, r.blockY, r.tidY);
-      auto key = std::make_tuple(r.locA.line, r.locA.col, r.locB.line, r.locB.col, r.kind);
-      if (seen_.insert(key).second)
-        res_.races.push_back(std::move(r));
-    }
-  }
-
-  static void decompose(int64_t thread, const std::array<int64_t, 3> &grid,
-                        const std::array<int64_t, 3> &block, int64_t tpb,
-                        int64_t (&b)[3], int64_t (&t)[3]) {
-    int64_t bl = thread / tpb, tl = thread % tpb;
-    b[0] = bl % grid[0];
-    b[1] = (bl / grid[0]) % grid[1];
-    b[2] = bl / (grid[0] * grid[1]);
-    t[0] = tl % block[0];
-    t[1] = (tl / block[0]) % block[1];
-    t[2] = tl / (block[0] * block[1]);
+    mergeLaunchRaces(res_, seen_, lk, grid, block, races.data(), R.n_races, launchIndex);
   }
 
   CompiledProgram &cp_;
@@ -782,10 +847,12 @@ private:
   const ExecConfig &cfg_;
   LaunchBackend &be_;
   const bool conservative_;
+  std::vector<PendingLaunch> *spec_;
+  bool budgetAbort_ = false;
   RunResult res_;
   std::vector<Buf> bufs_;
   std::map<std::pair<int, int>, DefVal> defs_;
-  std::set<std::tuple<int, int, int, int, int>> seen_;
+  SeenKeys seen_;
   size_t inputCursor_ = 0;
   int64_t steps_ = 0;
   int callDepth_ = 0;
@@ -862,6 +929,234 @@ SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
     }
   }
   out.configs = configs;
+  return out;
+}
+
+namespace {
+
+// enumerateVerdict's configurations in canonical order (warp sizes outer,
+// input odometer inner, last input fastest; at most maxConfigs + 1),
+// reference src/oracle.cpp:863-903.
+std::vector<ExecConfig> sweepConfigs(const CompiledProgram &prog, const SweepCaps &caps) {
+  std::vector<ExecConfig> out;
+  const int inputs = prog.inputs;
+  uint64_t configs = 0;
+  std::vector<size_t> cursor(static_cast<size_t>(inputs), 0);
+  for (int64_t ws : caps.warpSizes) {
+    std::fill(cursor.begin(), cursor.end(), 0);
+    for (;;) {
+      if (configs++ > caps.maxConfigs)
+        return out;
+      ExecConfig c;
+      c.gridCap = caps.gridCap;
+      c.blockCap = caps.blockCap;
+      c.warpSize = ws;
+      c.maxThreads = caps.maxThreads;
+      for (int i = 0; i < inputs; ++i)
+        c.inputs.push_back(caps.inputSet[cursor[static_cast<size_t>(i)]]);
+      out.push_back(std::move(c));
+      int pos = inputs - 1;
+      while (pos >= 0) {
+        if (++cursor[static_cast<size_t>(pos)] < caps.inputSet.size())
+          break;
+        cursor[static_cast<size_t>(pos)] = 0;
+        --pos;
+      }
+      if (pos < 0)
+        break;
+    }
+  }
+  return out;
+}
+
+// Host-only backend of a speculative run: handles and sizes, no device.
+class SpecBackend final : public LaunchBackend {
+public:
+  int reset() override {
+    n_ = 0;
+    return 0;
+  }
+  int alloc(int64_t, int32_t *handle) override {
+    *handle = n_++;
+    return 0;
+  }
+  int write(int32_t, int64_t, int64_t, const int64_t *) override { return 0; }
+  int read(int32_t, int64_t, int64_t, int64_t *) override { return HGRD_GPU_EINVAL; }
+  int checkLaunch(const hgrd_gpu_launch &, hgrd_gpu_result &) override { return HGRD_GPU_EINVAL; }
+  std::string lastError() override { return "speculative run"; }
+
+private:
+  int32_t n_ = 0;
+};
+
+struct SpecRun {
+  bool ok = false;
+  RunResult res;
+  std::vector<PendingLaunch> launches;
+  int64_t hostSteps = 0;
+};
+
+SpecRun speculate(CompiledProgram &prog, const ExecConfig &cfg) {
+  SpecRun out;
+  SpecBackend be;
+  try {
+    HostRun run(prog, cfg, be, false, &out.launches);
+    out.res = run.run();
+    out.ok = !run.budgetAborted() && out.res.error == 0;
+    out.hostSteps = run.steps();
+  } catch (const SpecFail &) {
+  } catch (const NeedConservative &) {
+  }
+  return out;
+}
+
+} // namespace
+
+SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps,
+                                    LaunchBackend &backend, int hostThreads) {
+  const std::vector<ExecConfig> cfgs = sweepConfigs(prog, caps);
+  const size_t nc = cfgs.size();
+  // lower every kernel up front (the cache is not thread-safe)
+  for (const Function &k : prog.program->kernels)
+    prog.kernel(&k);
+  // 1. speculative host runs, spread over host threads
+  std::vector<SpecRun> spec(nc);
+  {
+    const int nt = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(static_cast<size_t>(std::max(hostThreads, 1)), (nc + 31) / 32)));
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+      for (size_t i; (i = next.fetch_add(1)) < nc;)
+        spec[i] = speculate(prog, cfgs[i]);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t)
+      pool.emplace_back(work);
+    work();
+    for (auto &th : pool)
+      th.join();
+  }
+  // 2. every pending launch of every configuration in one batched check
+  std::vector<hgrd_gpu_batch_launch> bl;
+  std::vector<std::vector<const int64_t *>> dataPtrs;
+  std::vector<std::pair<size_t, size_t>> owner; // batch entry -> (config, launch)
+  size_t nRaceSlots = 0;
+  for (size_t i = 0; i < nc; ++i)
+    if (spec[i].ok)
+      for (size_t k = 0; k < spec[i].launches.size(); ++k) {
+        owner.emplace_back(i, k);
+        const size_t nl = std::max<size_t>(spec[i].launches[k].lk->locs.size(), 1);
+        nRaceSlots += 3 * nl * nl;
+      }
+  bl.resize(owner.size());
+  dataPtrs.resize(owner.size());
+  std::vector<hgrd_gpu_race> raceStore(std::max<size_t>(nRaceSlots, 1));
+  std::vector<hgrd_gpu_result> results(owner.size());
+  size_t raceAt = 0;
+  for (size_t e = 0; e < owner.size(); ++e) {
+    const PendingLaunch &p = spec[owner[e].first].launches[owner[e].second];
+    const LoweredKernel &lk = *p.lk;
+    hgrd_gpu_launch &L = bl[e].launch;
+    L = hgrd_gpu_launch{};
+    L.code = lk.code.data();
+    L.n_code = static_cast<uint32_t>(lk.code.size());
+    L.n_regs = lk.nRegs;
+    L.reg_init = p.regInit.data();
+    L.sites = lk.sites.data();
+    L.n_sites = static_cast<uint32_t>(lk.sites.size());
+    L.n_locs = static_cast<uint32_t>(lk.locs.size());
+    L.param_handle = p.paramHandle.data();
+    L.n_params = static_cast<uint32_t>(p.paramHandle.size());
+    L.flags = 0;
+    for (int d = 0; d < 3; ++d) {
+      L.grid[d] = p.grid[d];
+      L.block[d] = p.block[d];
+    }
+    L.warp_size = p.warpSize;
+    L.step_budget = p.budget;
+    dataPtrs[e].resize(p.bufData.size());
+    for (size_t h = 0; h < p.bufData.size(); ++h)
+      dataPtrs[e][h] = p.bufData[h].empty() ? nullptr : p.bufData[h].data();
+    bl[e].buffer_elems = p.bufElems.data();
+    bl[e].buffer_data = dataPtrs[e].data();
+    bl[e].n_buffers = static_cast<uint32_t>(p.bufElems.size());
+    const size_t nl = std::max<size_t>(lk.locs.size(), 1);
+    results[e] = hgrd_gpu_result{};
+    results[e].races = raceStore.data() + raceAt;
+    results[e].race_cap = static_cast<uint32_t>(3 * nl * nl);
+    raceAt += 3 * nl * nl;
+  }
+  if (!bl.empty()) {
+    constexpr size_t kChunk = 1 << 16; // launches per batched check
+    for (size_t b = 0; b < bl.size(); b += kChunk) {
+      const uint32_t m = static_cast<uint32_t>(std::min(kChunk, bl.size() - b));
+      const int rc = backend.checkBatch(bl.data() + b, m, results.data() + b);
+      if (rc == HGRD_GPU_ENOTSUP)
+        return enumerateVerdict(prog, caps, backend);
+      if (rc < 0) {
+        SweepResult r;
+        r.error = rc;
+        r.errorMessage = backend.lastError();
+        return r;
+      }
+    }
+  }
+  // 3. per configuration in canonical order: the speculation's report, or an
+  //    exact re-run; then the sweep's first-wins dedup (:883-889)
+  std::vector<char> exact(nc, 0);
+  for (size_t i = 0; i < nc; ++i)
+    exact[i] = !spec[i].ok;
+  std::vector<int64_t> kernelSteps(nc, 0);
+  for (size_t e = 0; e < owner.size(); ++e) {
+    const size_t i = owner[e].first;
+    if (results[e].mode & HGRD_RESULT_UNCHECKED)
+      exact[i] = 1;
+    kernelSteps[i] += results[e].steps;
+  }
+  SweepResult out;
+  out.configs = nc;
+  std::set<std::tuple<int, int, int, int, int, int64_t>> seen;
+  size_t e = 0;
+  for (size_t i = 0; i < nc; ++i) {
+    RunResult r;
+    const size_t e0 = e;
+    while (e < owner.size() && owner[e].first == i)
+      ++e;
+    if (!exact[i] && spec[i].hostSteps + kernelSteps[i] > cfgs[i].maxSteps)
+      exact[i] = 1; // the budget runs out somewhere: the exact run finds where
+    if (exact[i]) {
+      r = runConcrete(prog, cfgs[i], backend);
+      if (r.error) {
+        out.error = r.error;
+        out.errorMessage = r.errorMessage;
+        return out;
+      }
+      ++out.stats.restarts;
+    } else {
+      r = std::move(spec[i].res);
+      SeenKeys keys;
+      for (size_t q = e0; q < e; ++q) {
+        const PendingLaunch &p = spec[i].launches[q - e0];
+        mergeLaunchRaces(r, keys, *p.lk, p.grid, p.block, results[q].races, results[q].n_races,
+                         p.launchIndex);
+        r.stats.instances += results[q].instances;
+        r.stats.records += results[q].records;
+        r.stats.kernelSteps += results[q].steps;
+      }
+      sortRaces(r.races);
+    }
+    out.stats.instances += r.stats.instances;
+    out.stats.records += r.stats.records;
+    out.stats.parLaunches += r.stats.parLaunches;
+    out.stats.seqLaunches += r.stats.seqLaunches;
+    out.stats.restarts += r.stats.restarts;
+    for (const auto &race : r.races) {
+      auto key = std::make_tuple(race.locA.line, race.locA.col, race.locB.line, race.locB.col,
+                                 race.kind, cfgs[i].warpSize);
+      if (seen.insert(key).second)
+        out.races.push_back(SweepRace{race.locA, race.locB, race.kind, cfgs[i].warpSize});
+    }
+  }
   return out;
 }
 

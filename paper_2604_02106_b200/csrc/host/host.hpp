@@ -112,6 +112,11 @@ public:
   virtual int write(int32_t h, int64_t off, int64_t n, const int64_t *src) = 0;
   virtual int read(int32_t h, int64_t off, int64_t n, int64_t *dst) = 0;
   virtual int checkLaunch(const hgrd_gpu_launch &launch, hgrd_gpu_result &res) = 0;
+  // Many small launches at once (hgrd_gpu_check_batch); HGRD_GPU_ENOTSUP
+  // when the backend has no batched path.
+  virtual int checkBatch(const hgrd_gpu_batch_launch *, uint32_t, hgrd_gpu_result *) {
+    return HGRD_GPU_ENOTSUP;
+  }
   virtual std::string lastError() = 0;
 };
 
@@ -153,6 +158,14 @@ std::string sweepShardJson(const SweepShard &r, const std::string &file);
 // the reference's first-wins dedup: the result equals enumerateVerdict's.
 SweepResult enumerateVerdictParallel(CompiledProgram &prog, const SweepCaps &caps,
                                      const std::vector<LaunchBackend *> &backends);
+// enumerateVerdict with the configurations' host runs done speculatively on
+// `hostThreads` threads (assuming no kernel traps, no step-budget abort and
+// no device values read back) and all their launches checked by one batched
+// backend call; a configuration whose speculation fails is re-run exactly
+// through runConcrete.  Same result as enumerateVerdict.  Falls back to it
+// when the backend has no batched path.
+SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps,
+                                    LaunchBackend &backend, int hostThreads);
 // Configurations enumerateVerdict runs (warp sizes x input odometer, capped).
 uint64_t sweepSize(const CompiledProgram &prog, const SweepCaps &caps);
 int sweepShardJsonRun(LaunchBackend &be, const char *src, const char *file,

@@ -5,9 +5,11 @@ Two shardings:
 * independent jobs — sweep configs / programs — with no data-path
   collective (below), and
 * one huge launch by whole-block ranges (``check_launch_sharded``): INTRA
-  kinds stay rank-local; INTER-BLOCK takes one MIN / MAX all-reduce of the
-  per-(element, site) block summaries (NCCL over NVLink on GPUs), then the
-  few witness records of the realised keys' elements are gathered.
+  kinds stay rank-local; INTER-BLOCK takes one MIN / MAX reduce-scatter of
+  the per-(element, site) block summaries over element ranges (NCCL over
+  NVLink on GPUs), a scan of each rank's range, a MIN all-reduce of the
+  per-key first-found elements (3 * locs^2 words), then the few witness
+  records of the realised keys' elements are gathered.
 
 The configuration lattice of ``enumerateVerdict`` (reference
 src/oracle.cpp:863-903: warp sizes outer, input odometer inner, at most
@@ -93,10 +95,23 @@ def block_ranges(n_blocks: int, world: int) -> List[tuple]:
     return out
 
 
+EMPTY_LO = 0x7F7F7F7F  # kShardEmpty: an element / site no block of the shard reached
+NO_ELEM = (1 << 64) - 1  # key without an element
+
+
+def element_slices(n_elems: int, world: int) -> List[tuple]:
+    """Equal element ranges of the reduce-scatter (the last ones may be
+    short or empty): rank r reduces and scans elements [b, e)."""
+    per = (n_elems + world - 1) // world if n_elems else 0
+    return [(min(r * per, n_elems), min((r + 1) * per, n_elems)) for r in range(world)]
+
+
 class TorchComm:
-    """Collectives of ``check_launch_sharded`` over ``torch.distributed``:
-    NCCL all-reduces the device tables in place; gloo (CPU tests) reduces
-    host copies."""
+    """Collectives of ``check_launch_sharded`` over ``torch.distributed``.
+    NCCL: the device tables are reduce-scattered (MIN / MAX) into equal
+    element ranges, the per-key minima are MIN all-reduced on the device.
+    gloo (CPU tests): the same results through host copies (all-reduce, then
+    each rank keeps its range)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -107,6 +122,8 @@ class TorchComm:
         self.nccl = dist.get_backend(group) == "nccl"
 
     def allreduce_minmax(self, lo, hi):
+        """In-place MIN / MAX all-reduce of whole tables (the all-reduce
+        variant of the protocol, hgrd_gpu_shard_inter)."""
         d = self.dist
         if self.nccl:
             d.all_reduce(lo, op=d.ReduceOp.MIN, group=self.group)
@@ -117,6 +134,48 @@ class TorchComm:
         d.all_reduce(hhi, op=d.ReduceOp.MAX, group=self.group)
         lo.copy_(hlo)
         hi.copy_(hhi)
+
+    def reduce_scatter_minmax(self, lo, hi, unit: int):
+        """lo / hi: int32 tables of n_elems * unit entries (unit = sites per
+        element).  Returns this rank's reduced range (lo_r, hi_r, elem_begin,
+        n_elems_r); lo_r / hi_r live on lo's device."""
+        import torch
+        d = self.dist
+        n_elems = lo.numel() // unit
+        b, e = element_slices(n_elems, self.world)[self.rank]
+        per = (n_elems + self.world - 1) // self.world
+        if self.nccl:
+            pad = per * self.world * unit
+            plo = torch.full((pad,), EMPTY_LO, dtype=torch.int32, device=lo.device)
+            phi = torch.zeros(pad, dtype=torch.int32, device=lo.device)
+            plo[: lo.numel()].copy_(lo)
+            phi[: hi.numel()].copy_(hi)
+            olo = torch.empty(per * unit, dtype=torch.int32, device=lo.device)
+            ohi = torch.empty(per * unit, dtype=torch.int32, device=lo.device)
+            d.reduce_scatter_tensor(olo, plo, op=d.ReduceOp.MIN, group=self.group)
+            d.reduce_scatter_tensor(ohi, phi, op=d.ReduceOp.MAX, group=self.group)
+            return olo[: (e - b) * unit], ohi[: (e - b) * unit], b, e - b
+        hlo, hhi = lo.cpu(), hi.cpu()
+        d.all_reduce(hlo, op=d.ReduceOp.MIN, group=self.group)
+        d.all_reduce(hhi, op=d.ReduceOp.MAX, group=self.group)
+        return (hlo[b * unit: e * unit].to(lo.device), hhi[b * unit: e * unit].to(lo.device),
+                b, e - b)
+
+    def allreduce_min_u64(self, values, device=None):
+        """MIN all-reduce of a uint64 numpy vector (NO_ELEM = none)."""
+        import numpy as np
+        import torch
+        d = self.dist
+        v = values.astype(np.uint64)
+        signed = np.where(v == np.uint64(NO_ELEM), np.int64(2 ** 63 - 1),
+                          v.astype(np.int64))
+        t = torch.from_numpy(signed)
+        if self.nccl:
+            t = t.to(device if device is not None else torch.cuda.current_device())
+        d.all_reduce(t, op=d.ReduceOp.MIN, group=self.group)
+        out = t.cpu().numpy()
+        return np.where(out == np.int64(2 ** 63 - 1), np.uint64(NO_ELEM),
+                        out.astype(np.uint64))
 
     def allgather(self, obj) -> list:
         out: List[Optional[object]] = [None] * self.world
@@ -142,10 +201,11 @@ def check_launch_sharded(ctx, spec, comm, device: int = 0) -> dict:
     b0, b1 = block_ranges(n_blocks, comm.world)[comm.rank]
     try:
         res, sh = ctx.shard_check(spec, b0, b1)
+        stages = ctx.last_profile()  # (empty unless profiling is on)
         mine = {"ok": True, "steps": res["steps"], "instances": res["instances"],
                 "records": res["records"], "mode": res["mode"], "ms": res["deviceMs"]}
     except NotShardable:
-        res, sh, mine = None, None, {"ok": False}
+        res, sh, mine, stages = None, None, {"ok": False}, []
     stats = comm.allgather(mine)
     steps = sum(s.get("steps", 0) for s in stats)
     if not all(s["ok"] for s in stats) or steps > spec.launch.step_budget:
@@ -154,8 +214,17 @@ def check_launch_sharded(ctx, spec, comm, device: int = 0) -> dict:
         return out
     if sh.inter_n:
         lo, hi = ctx.shard_tables(sh, device)
-        comm.allreduce_minmax(lo, hi)
-        keys, vals = ctx.shard_inter(spec, sh)
+        if hasattr(comm, "reduce_scatter_minmax"):
+            # reduce-scatter over element ranges, scan of this rank's range,
+            # MIN all-reduce of the per-key first-found elements
+            rlo, rhi, e0, ne = comm.reduce_scatter_minmax(lo, hi, spec.launch.n_sites)
+            ke = ctx.shard_inter_scan(spec, rlo, rhi, e0, ne, device)
+            ke = comm.allreduce_min_u64(ke, device)
+            keys, vals = ctx.shard_inter_records(spec, sh, ke)
+        else:
+            comm.allreduce_minmax(lo, hi)
+            ctx.wait_torch_stream(device)
+            keys, vals = ctx.shard_inter(spec, sh)
     else:
         import numpy as np
         keys, vals = np.zeros(0, np.uint64), np.zeros(0, np.uint32)
@@ -179,8 +248,8 @@ def check_launch_sharded(ctx, spec, comm, device: int = 0) -> dict:
             "instances": sum(s["instances"] for s in stats),
             "records": sum(s["records"] for s in stats), "aborted": False, "abortStmt": -1,
             "mode": stats[0]["mode"], "deviceMs": max(s["ms"] for s in stats),
-            "path": "sharded", "interRecords": int(len(all_keys))}
+            "path": "sharded", "interRecords": int(len(all_keys)), "stages": stages}
 
 
 __all__ = ["merge_shards", "enumerate_verdict_distributed", "shard_jobs", "block_ranges",
-           "TorchComm", "check_launch_sharded"]
+           "element_slices", "TorchComm", "check_launch_sharded"]

@@ -105,13 +105,62 @@ def _comm_worker(rank, world, port, out):
         for e in range(8):
             if e % world == rank or e == 0:
                 lo[e] = hi[e] = 2 * e + rank + 1
+        rlo, rhi, e0, ne = comm.reduce_scatter_minmax(lo.clone(), hi.clone(), 2)
+        ke = np.full(6, (1 << 64) - 1, dtype=np.uint64)
+        ke[rank] = 10 + rank
+        ke[3] = 7 - rank
+        ke_red = comm.allreduce_min_u64(ke)
         comm.allreduce_minmax(lo, hi)
         got = comm.allgather({"rank": rank, "keys": np.arange(rank + 1, dtype=np.uint64)})
         res = {"lo": lo.tolist(), "hi": hi.tolist(), "ranks": [g["rank"] for g in got],
+               "rs": [rank, rlo.tolist(), rhi.tolist(), e0, ne], "ke": ke_red.tolist(),
                "nkeys": [len(g["keys"]) for g in got], "ranges": block_ranges(9, world)}
         open(f"{out}.{rank}", "w").write(repr(res))
     finally:
         dist.destroy_process_group()
+
+
+def _sharded_worker(rank, world, port, out):
+    """check_launch_sharded end to end: one process per rank, each with its
+    own context on cuda:0, collectives over gloo (host-side rendezvous between
+    kernels: no kernel waits on another rank's)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import paper_2604_02106_b200 as hg
+    from paper_2604_02106_b200.parallel import TorchComm, check_launch_sharded
+    from test_gpu_parity import _spec_hist, _spec_stencil, _spec_transpose
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    keys = ("races", "steps", "instances", "records")
+    try:
+        ctx = hg.GpuContext(0)
+        comm = TorchComm()
+        bad = []
+        cases = [("stencil", lambda c: _spec_stencil(c, 1 << 14, False)),
+                 ("transpose", lambda c: _spec_transpose(c, 128, False)),
+                 ("hist64_store", lambda c: _spec_hist(c, 1 << 13, 64, "store")),
+                 ("hist61_block", lambda c: _spec_hist(c, 1 << 13, 61, "atomic_block")),
+                 ("hist1024_atomic", lambda c: _spec_hist(c, 1 << 13, 1024, "atomic"))]
+        for name, mk in cases:
+            spec = mk(ctx)[0]
+            got = check_launch_sharded(ctx, spec, comm, device=0)
+            full = ctx.check_launch(mk(ctx)[0])
+            if got.get("path") != "sharded" or {k: got[k] for k in keys} != \
+                    {k: full[k] for k in keys}:
+                bad.append(name)
+        open(f"{out}.{rank}", "w").write(repr(bad))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_check_launch_sharded_gpu(tmp_path):
+    world = 2
+    out = str(tmp_path / "sharded")
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        assert open(f"{out}.{r}").read() == "[]"
 
 
 def test_gloo_world2_shard_collectives(tmp_path):
@@ -119,6 +168,14 @@ def test_gloo_world2_shard_collectives(tmp_path):
     out = str(tmp_path / "comm")
     mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     res = [eval(open(f"{out}.{r}").read()) for r in range(world)]
+    # reduce-scatter: rank r holds elements [2r, 2r + 2) of the 4 two-site elements
+    for r in range(world):
+        rank, rlo, rhi, e0, ne = res[r].pop("rs")
+        assert (e0, ne) == (2 * rank, 2)
+        assert rlo == res[r]["lo"][4 * rank: 4 * rank + 4]
+        assert rhi == res[r]["hi"][4 * rank: 4 * rank + 4]
+    big = (1 << 64) - 1
+    assert res[0]["ke"] == [10, 11, big, 6, big, big]
     assert res[0] == res[1]
     lo, hi = res[0]["lo"], res[0]["hi"]
     assert (lo[0], hi[0]) == (1, 2)  # element 0: blocks of both ranks -> lo != hi (MULTI)

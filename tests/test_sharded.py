@@ -39,11 +39,18 @@ class ThreadComm:
                 outer.barrier.wait()
                 return out
 
-            def allreduce_minmax(self, lo, hi):
-                parts = self.allgather((lo.cpu(), hi.cpu()))
+            def reduce_scatter_minmax(self, lo, hi, unit):
                 import torch
-                lo.copy_(torch.stack([p[0] for p in parts]).min(0).values)
-                hi.copy_(torch.stack([p[1] for p in parts]).max(0).values)
+                from paper_2604_02106_b200.parallel import element_slices
+                parts = self.allgather((lo.cpu(), hi.cpu()))
+                rlo = torch.stack([p[0] for p in parts]).min(0).values
+                rhi = torch.stack([p[1] for p in parts]).max(0).values
+                b, e = element_slices(lo.numel() // unit, self.world)[r]
+                return (rlo[b * unit: e * unit].to(lo.device),
+                        rhi[b * unit: e * unit].to(lo.device), b, e - b)
+
+            def allreduce_min_u64(self, v, device=None):
+                return np.minimum.reduce(self.allgather(v.copy()))
 
         return Rank()
 

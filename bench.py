@@ -670,6 +670,150 @@ def sweep_jobs(corpus, fuzz):
     return jobs
 
 
+# ------------------------------------------------------- sweep workloads
+SWEEP_WORKLOADS = ("lattice", "corpus")
+
+
+def sweep_job_list(name):
+    """configs[4] ("lattice"): the 229-program x 10-input x 5-warp-size
+    lattice (9695 configurations); configs[0] ("corpus"): the 29 corpus
+    entries at their manifest SweepCaps (acceptance criterion 4).  Jobs are
+    [{"source", "file", "caps"}]; the expected reports are the reference's
+    (tests/golden)."""
+    from conftest import load_golden
+    if name == "lattice":
+        gold = load_golden("lattice")
+        return ([{"source": j["source"], "file": j["file"], "caps": j["caps"]} for j in gold],
+                [j["sweep"] for j in gold], 4)
+    gold = load_golden("corpus")
+    return ([{"source": e["source"], "file": e["file"], "caps": e["caps"]} for e in gold],
+            [e["sweep_manifest"] for e in gold], 0)
+
+
+def sweep_instances(jobs):
+    """Access instances the sweep checks (identical on every path by
+    construction; counted by the CPU restatement, test infrastructure)."""
+    from oracles import CpuOracle
+    return sum(r["stats"]["instances"] for r in CpuOracle().enumerate_verdict_many(jobs))
+
+
+def run_sweep_arm(args):
+    """configs[0] / configs[4]: every job's enumerateVerdict per step through
+    hgrd_gpu_enumerate_verdict_many_json (host runs speculated on host
+    threads, the launches of all jobs in one batched kernel; configurations
+    that cannot be speculated run exactly on worker contexts meanwhile).
+    A sweep is a host-driven pipeline, so a step is timed end to end (wall
+    clock around the synchronous call, max over ranks); `value` and `e2e`
+    are the same measurement.  --gpus N: rank r runs the configurations with
+    canonical index % N == r of every job (no data-path collective), the
+    shards are gathered and merged (parallel.merge_shards)."""
+    import torch
+    import paper_2604_02106_b200 as hg
+    from oracles import strip_extras
+    from paper_2604_02106_b200.parallel import merge_shards
+    ws, rank, local = dist_env()
+    use_dist = ws > 1 or os.environ.get("HGRD_BENCH_DIST") == "1"
+    if use_dist:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    jobs, want, cfg_index = sweep_job_list(args.workload)
+    ctx = hg.GpuContext(local)
+
+    def step():
+        if not use_dist:
+            return ctx.enumerate_verdict_many(jobs)
+        mine = ctx.enumerate_verdict_many(jobs, rank, ws)
+        parts = [None] * ws
+        torch.distributed.all_gather_object(parts, mine)
+        return [merge_shards([p[q] for p in parts]) | {"stats": {}} for q in range(len(jobs))]
+
+    for _ in range(max(args.warmup, 3)):
+        got = step()
+    assert [strip_extras(g)["races"] for g in got] == [w["races"] for w in want]
+    n_configs = sum(g.get("configs", 0) for g in got)
+    inst = sweep_instances(jobs)
+    clocks = Clocks(local)
+    launches0 = ctx.kernel_launches()
+    xfer0 = ctx.transfer_bytes()
+    times = []
+    for _ in range(args.steps):
+        if use_dist:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        got = step()
+        times.append(time.perf_counter() - t0)
+    clk = clocks.stop()
+    n_launch = ctx.kernel_launches() - launches0
+    xfer1 = ctx.transfer_bytes()
+    secs = sum(times)
+    if use_dist:
+        t = torch.tensor([secs], dtype=torch.float64, device=torch.device("cuda", local))
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        secs = float(t[0])
+    value = inst * args.steps / secs
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}_sweep_{len(jobs)}programs_{n_configs}configs",
+                   "baseline_config": cfg_index, "instances_per_step": inst,
+                   "configs_per_s": n_configs * args.steps / secs,
+                   "timing": "wall clock around the synchronous sweep call, max over ranks",
+                   "parallelism": f"configshard{ws}" if use_dist else "1 GPU + host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": (xfer1[0] - xfer0[0]) // args.steps,
+                "d2h_bytes_per_step": (xfer1[1] - xfer0[1]) // args.steps,
+                "api": "hgrd_gpu_enumerate_verdict_many_json (MiniCU source in, reports out)"},
+        "gpu_launches": n_launch, "clocks": clk,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        from oracles import RefOracle
+        threads = os.cpu_count() or 1
+        tj = [(j["source"], j["file"], j["caps"]) for j in jobs]
+        reps = 5
+        t = sum(RefOracle().time_sweeps(tj, threads)[0] for _ in range(reps))
+        line["cpu_baseline"] = {"value": inst * reps / t, "unit": UNIT, "cores": threads,
+                                "kind": "reference",
+                                "sample": f"the whole workload x {reps}: enumerateVerdict of "
+                                          f"every job (parse included), jobs over {threads} "
+                                          f"host threads ({t:.2f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if use_dist:
+        torch.distributed.destroy_process_group()
+
+
+def run_sweep_reference_arm(args):
+    """The unmodified reference's enumerateVerdict over the same jobs, the
+    jobs spread over every host thread (re-entrant), whole workload per step."""
+    from oracles import RefOracle
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    jobs, _, cfg_index = sweep_job_list(args.workload)
+    tj = [(j["source"], j["file"], j["caps"]) for j in jobs]
+    inst = sweep_instances(jobs)
+    ref = RefOracle()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        ref.time_sweeps(tj, threads)
+    secs = sum(ref.time_sweeps(tj, threads)[0] for _ in range(args.steps))
+    v = inst * args.steps / secs
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}_sweep_{len(jobs)}programs",
+                   "baseline_config": cfg_index},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"the whole workload per step: enumerateVerdict of every "
+                                   f"job, jobs over {threads} host threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -677,13 +821,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="histogram", choices=sorted(WORKLOADS),
+    ap.add_argument("--workload", default="histogram",
+                    choices=sorted(WORKLOADS) + list(SWEEP_WORKLOADS),
                     help="BASELINE config to time (default: configs[3], the largest)")
     ap.add_argument("--paths", action="store_true",
                     help="time the lock-idiom, SEQUENTIAL and sweep paths against the reference")
     args = ap.parse_args()
     if args.paths:
         run_paths(args)
+    elif args.workload in SWEEP_WORKLOADS:
+        (run_sweep_reference_arm if args.impl == "reference" else run_sweep_arm)(args)
     elif args.impl == "reference":
         run_reference_arm(args)
     else:

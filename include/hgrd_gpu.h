@@ -229,6 +229,16 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
  * sorted races: {"total":N,"configs":[{index,warpSize,races:[{kind,locA,locB}]}]}.
  * Merging all shards in index order with first-wins (locs, kind, warpSize)
  * dedup reproduces hgrd_gpu_enumerate_verdict_json exactly. */
+/* Many programs' sweeps at once (BASELINE config 5, the launch-config sweep
+ * of thousands of program x configuration jobs).  jobs_json:
+ * [{"source": MiniCU text, "file": name, "caps": SweepCaps}, ...].  All the
+ * jobs' configurations (with world > 1 only this rank's: canonical index
+ * % world == rank) are speculated on host threads and their launches
+ * checked by one batched kernel.  out: a JSON array with, per job, its
+ * enumerateVerdict result (world == 1), its sweep shard as
+ * hgrd_gpu_sweep_shard_json returns it (world > 1), or {"error": [...]}. */
+int hgrd_gpu_enumerate_verdict_many_json(hgrd_gpu_ctx *ctx, const char *jobs_json, int rank,
+                                         int world, char **out);
 int hgrd_gpu_sweep_shard_json(hgrd_gpu_ctx *ctx, const char *source,
                               const char *file_name, const char *caps_json,
                               int rank, int world, char **out);
@@ -301,11 +311,13 @@ int hgrd_gpu_shard_detect(hgrd_gpu_ctx *ctx, const hgrd_gpu_launch *launch,
  * indexes buffer_elems / buffer_data, which hold every buffer's size and,
  * for buffers read by value-needed loads, the launch-entry contents; NULL
  * data means zeros).  results[i] is what hgrd_gpu_check_launch would report
- * (race handles index the launch's buffers), or carries
+ * (race handles index the launch's buffers; the first trap_cap traps in
+ * canonical order, n_traps_total all of them), or carries
  * HGRD_RESULT_UNCHECKED in `mode` when the launch is outside the batch
  * envelope (sequential / lock-idiom launches, more than 512 threads or 256
- * blocks, record capacity) or needs the ordered path (traps, the step
- * budget, a hot element): check those with hgrd_gpu_check_launch. */
+ * blocks, record capacity, more than 1024 traps) or needs the ordered path
+ * (the step budget runs out, a hot element): check those with
+ * hgrd_gpu_check_launch. */
 typedef struct hgrd_gpu_batch_launch {
   hgrd_gpu_launch launch;
   const int64_t *buffer_elems;       /* n_buffers sizes */

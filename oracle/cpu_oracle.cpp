@@ -179,6 +179,33 @@ public:
   std::string lastError() override { return err_; }
   std::vector<std::vector<int64_t>> &buffers() { return bufs_; }
 
+  // The batched check restated launch by launch (each with its own
+  // buffers), with the batch's contract: launches that run out of budget
+  // come back HGRD_RESULT_UNCHECKED (the caller re-checks them in order), so
+  // the speculative sweep logic runs on CPU exactly as on GPU.
+  int checkBatch(const hgrd_gpu_batch_launch *B, uint32_t n, hgrd_gpu_result *R) override {
+    std::vector<std::vector<int64_t>> saved = std::move(bufs_);
+    for (uint32_t i = 0; i < n; ++i) {
+      bufs_.clear();
+      for (uint32_t h = 0; h < B[i].n_buffers; ++h) {
+        bufs_.emplace_back(static_cast<size_t>(std::max<int64_t>(B[i].buffer_elems[h], 0)), 0);
+        if (B[i].buffer_data && B[i].buffer_data[h])
+          std::memcpy(bufs_.back().data(), B[i].buffer_data[h],
+                      8 * static_cast<size_t>(B[i].buffer_elems[h]));
+      }
+      hgrd_gpu_result &r = R[i];
+      int rc = checkLaunch(B[i].launch, r);
+      if (rc < 0)
+        return rc;
+      if (r.aborted || (B[i].launch.flags & (HGRD_LAUNCH_SEQUENTIAL | HGRD_LAUNCH_PAIRWISE)))
+        r.mode = HGRD_RESULT_UNCHECKED;
+    }
+    bufs_ = std::move(saved);
+    return 0;
+  }
+  bool hasBatch() const override { return batch_; }
+  bool batch_ = false;
+
   int checkLaunch(const hgrd_gpu_launch &L, hgrd_gpu_result &R) override {
     L_ = &L;
     R.n_races = 0;
@@ -472,6 +499,31 @@ int hgrd_oracle_enumerate_verdict_json(const char *src, const char *file,
   CpuOracle be;
   std::string s;
   int rc = enumerateVerdictJson(be, src, file, caps, s);
+  *out = dup(s);
+  return rc;
+}
+
+// enumerateVerdict through the speculative batched sweep (the product's
+// sweep path) with the restatement as its batch backend.
+int hgrd_oracle_enumerate_verdict_batched_json(const char *src, const char *file,
+                                               const char *caps, char **out) {
+  CpuOracle be;
+  be.batch_ = true;
+  std::string s;
+  int rc = enumerateVerdictJson(be, src, file, caps, s);
+  *out = dup(s);
+  return rc;
+}
+
+// Many sweeps at once through the product's sweepManyJson (batched when
+// `batched` is set) with the restatement as backend.
+int hgrd_oracle_enumerate_verdict_many_json(const char *jobs, int rank, int world, int batched,
+                                            char **out) {
+  CpuOracle be;
+  be.batch_ = batched != 0;
+  std::string s;
+  int rc = sweepManyJson([&](int i) -> LaunchBackend * { return i == 0 ? &be : nullptr; }, 1,
+                         jobs, rank, world, s);
   *out = dup(s);
   return rc;
 }

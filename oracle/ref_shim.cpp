@@ -152,4 +152,33 @@ double hgrd_ref_time_parallel(const char *src, const char *file,
   return std::chrono::duration<double>(t1 - t0).count();
 }
 
+// Bench reference arm of the sweep workloads (BASELINE config 5): every
+// job's enumerateVerdict (parse included), the jobs spread over `nThreads`
+// host threads (enumerateVerdict is re-entrant). Returns wall seconds; the
+// total number of sweep races found goes to *nRaces.
+double hgrd_ref_time_sweeps(const char *const *srcs, const char *const *files,
+                            const char *const *capsJson, int n, int nThreads, int *nRaces) {
+  std::vector<hgrd::SweepCaps> caps;
+  for (int i = 0; i < n; ++i)
+    caps.push_back(parseCaps(capsJson[i]));
+  std::atomic<int> next{0}, races{0};
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::max(nThreads, 1); ++t)
+    pool.emplace_back([&] {
+      for (int i; (i = next.fetch_add(1)) < n;) {
+        hgrd::ParseResult parsed = hgrd::parseTranslationUnit(srcs[i], files[i]);
+        if (!parsed.ok())
+          continue;
+        races += static_cast<int>(hgrd::enumerateVerdict(*parsed.program, caps[i]).size());
+      }
+    });
+  for (auto &th : pool)
+    th.join();
+  auto t1 = std::chrono::steady_clock::now();
+  if (nRaces)
+    *nRaces = races;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
 } // extern "C"

@@ -165,6 +165,8 @@ def load_library() -> ctypes.CDLL:
     for fn in ("hgrd_gpu_run_concrete_json", "hgrd_gpu_enumerate_verdict_json"):
         getattr(lib, fn).argtypes = [P, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
                                      ctypes.POINTER(P)]
+    lib.hgrd_gpu_enumerate_verdict_many_json.argtypes = [P, ctypes.c_char_p, ctypes.c_int,
+                                                         ctypes.c_int, ctypes.POINTER(P)]
     lib.hgrd_gpu_lower_json.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
                                         ctypes.POINTER(P)]
     lib.hgrd_gpu_sweep_shard_json.argtypes = [P, ctypes.c_char_p, ctypes.c_char_p,
@@ -370,6 +372,20 @@ class GpuContext:
         s = _take_string(self._lib, out)
         if rc != 0:
             raise RuntimeError(f"sweep_shard failed ({rc}): {s}")
+        return json.loads(s)
+
+    def enumerate_verdict_many(self, jobs, rank: int = 0, world: int = 1) -> List[dict]:
+        """Many programs' sweeps at once (BASELINE config 5): jobs is a list
+        of {"source", "file", "caps"}; returns per job its enumerateVerdict
+        result (world 1) or this rank's sweep shard (parallel.merge_shards)."""
+        out = ctypes.c_void_p()
+        payload = json.dumps([{"source": j["source"], "file": j.get("file", "prog.mcu"),
+                               "caps": j.get("caps") or {}} for j in jobs])
+        rc = self._lib.hgrd_gpu_enumerate_verdict_many_json(self._ctx, payload.encode(), rank,
+                                                            world, ctypes.byref(out))
+        s = _take_string(self._lib, out)
+        if rc != 0:
+            raise RuntimeError(f"enumerate_verdict_many failed ({rc}): {s}")
         return json.loads(s)
 
     def enumerate_verdict(self, source: str, caps=None, file_name: str = "prog.mcu") -> dict:

@@ -46,13 +46,26 @@ int hgrd_gpu_enumerate_verdict_json(hgrd_gpu_ctx *ctx, const char *source,
                                     char **out) {
   if (!ctx || !out)
     return HGRD_GPU_EINVAL;
-  // configurations are independent runs: spread them over worker contexts
-  // (own streams and buffers on the same GPU, one host thread each) so the
-  // small launches of a sweep overlap instead of queueing behind each
-  // other's host round trips (HGRD_SWEEP_WORKERS, default 8)
+  // Batched (default): the configurations' host runs speculated on host
+  // threads and all their launches checked by one k_batch launch on this
+  // context; configurations that cannot be speculated run exactly on the
+  // worker contexts meanwhile (enumerateVerdictBatched).  HGRD_SWEEP_BATCH=0:
+  // per-launch checks spread over the worker contexts (own streams and
+  // buffers on the same GPU, one host thread each).
   SweepWorkers pool(ctx);
   std::string s;
   int rc = enumerateVerdictJsonParallel(pool.getter(), pool.n, source, file_name, caps_json, s);
+  *out = dup(s);
+  return rc;
+}
+
+int hgrd_gpu_enumerate_verdict_many_json(hgrd_gpu_ctx *ctx, const char *jobs_json, int rank,
+                                         int world, char **out) {
+  if (!ctx || !out)
+    return HGRD_GPU_EINVAL;
+  SweepWorkers pool(ctx);
+  std::string s;
+  int rc = sweepManyJson(pool.getter(), pool.n, jobs_json, rank, world, s);
   *out = dup(s);
   return rc;
 }

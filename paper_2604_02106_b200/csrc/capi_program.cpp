@@ -521,7 +521,7 @@ int hgrd_gpu_enumerate_verdict_program(hgrd_gpu_ctx *ctx, const hgrd_gpu_program
                       caps->warp_sizes + (caps->warp_sizes ? caps->n_warp_sizes : 0));
   sc.maxThreads = caps->max_threads;
   sc.maxConfigs = caps->max_configs;
-  SweepWorkers pool(ctx);
+  SweepWorkers pool(ctx); // (batched unless HGRD_SWEEP_BATCH=0, as the JSON entry point)
   SweepResult r = enumerateVerdictOnWorkers(pool.getter(), pool.n, *cp, sc);
   if (r.error) {
     setError(ctx, "backend: " + r.errorMessage);

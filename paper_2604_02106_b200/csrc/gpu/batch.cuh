@@ -26,6 +26,7 @@ constexpr int kBatchIPT = 8; // 2048 records per launch
 using BatchSmem = FusedSmem<kBatchThreads, kBatchIPT>;
 constexpr int kBatchMaxThreads = 2 * kBatchThreads; // MiniCU threads per launch
 constexpr int kBatchMaxBlocks = kMaxIterBlocks;     // the records' 8-bit block field
+constexpr int kBatchTraps = 1024;                   // traps per launch kept on chip
 
 struct BatchLaunch {
   LaunchDev L;           // code / sites / params / regInit / conflict masks in the batch blob
@@ -39,6 +40,7 @@ struct BatchLaunch {
 struct BatchOut {
   unsigned long long steps, instances, records, traps;
   unsigned int flags, nRaces;
+  unsigned int trapOff, nTraps; // this launch's trap entries in the trap area
 };
 
 struct BatchArgs {
@@ -47,6 +49,10 @@ struct BatchArgs {
   BatchOut *out;
   hgrd_gpu_race *races;
   unsigned *next; // work counter
+  uint64_t *trapKey; // trap area (all launches): key, site << 1 | unallocated
+  uint32_t *trapSite;
+  unsigned *trapCursor;
+  unsigned trapCap;
   int maxKeys, maxCode, maxSites, maxParams, maxW;
 };
 
@@ -68,6 +74,9 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
   __shared__ LaunchDev sL;
   __shared__ unsigned sLaunch, sFlags, sNRaces;
   __shared__ unsigned long long sSteps, sInst, sTraps, sRecs;
+  __shared__ uint64_t sTrapKey[kBatchTraps];
+  __shared__ uint32_t sTrapSite[kBatchTraps];
+  __shared__ unsigned sTrapN, sTrapOff;
   const int tid = threadIdx.x;
   int64_t regs[kMaxRegs];
 
@@ -114,6 +123,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
       S.flags = 0;
       sFlags = 0;
       sNRaces = 0;
+      sTrapN = 0;
       sSteps = sInst = sTraps = sRecs = 0;
     }
     __syncthreads();
@@ -140,6 +150,10 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
       s.owner = nullptr;
       s.epochTag = 0;
       s.mine = 0;
+      s.trapKey = sTrapKey;
+      s.trapSite = sTrapSite;
+      s.trapCount = &sTrapN;
+      s.trapCap = kBatchTraps;
       Builtins bi;
       InterpBody::identity(sL, tl, bi, s.block, s.warp, s.lane);
       InterpBody::run(sL, sCode, bi, s, regs);
@@ -177,9 +191,22 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
       if (S.count > static_cast<unsigned>(BatchSmem::kCap) || S.hot)
         sFlags |= kFlagFusedOverflow; // (a hot element needs radix grouping: the host re-checks)
       sFlags |= S.flags;
+      sTrapOff = 0;
+      if (sTrapN > static_cast<unsigned>(kBatchTraps)) {
+        sFlags |= kFlagFusedOverflow;
+      } else if (sTrapN) {
+        sTrapOff = atomicAdd(A.trapCursor, sTrapN);
+        if (sTrapOff + sTrapN > A.trapCap)
+          sFlags |= kFlagFusedOverflow;
+      }
     }
     __syncthreads();
-    const bool ok = (sFlags & (kFlagFusedOverflow | kFlagAbort)) == 0 && sTraps == 0;
+    const bool ok = (sFlags & (kFlagFusedOverflow | kFlagAbort)) == 0;
+    if (ok) // the launch's traps, unordered (the host sorts them by key)
+      for (unsigned i = tid; i < sTrapN; i += NT) {
+        A.trapKey[sTrapOff + i] = sTrapKey[i];
+        A.trapSite[sTrapOff + i] = sTrapSite[i];
+      }
 
     // 2. per realised key: the first (x, y) pair of its minimum element
     if (ok) {
@@ -262,6 +289,8 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
       o.traps = sTraps;
       o.flags = sFlags;
       o.nRaces = ok ? sNRaces : 0;
+      o.trapOff = sTrapOff;
+      o.nTraps = ok ? sTrapN : 0;
     }
     __syncthreads(); // the next launch reuses the shared state
   }

@@ -2132,13 +2132,19 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     maxW = std::max(maxW, bl[k].nW);
   }
   const size_t nextAt = batchPut(blob, &raceOff, 0);
-  blob.resize(nextAt + 16);
+  blob.resize(nextAt + 16); // work counter, trap cursor
   std::memset(blob.data() + nextAt, 0, 16);
   const size_t h2d = blob.size();
   const size_t outAt = align16(h2d);
   const size_t racesAt = align16(outAt + sizeof(BatchOut) * m);
   const size_t total = racesAt + sizeof(hgrd_gpu_race) * std::max<uint32_t>(raceOff, 1);
-  NEED(c->batchBlob, total);
+  // trap area: every trap of the batch's launches (12 B each), read back only
+  // when the trap cursor is non-zero
+  const unsigned trapCap = static_cast<unsigned>(std::min<uint64_t>(uint64_t(m) * 256, 1u << 22));
+  const size_t trapKeyAt = align16(total);
+  const size_t trapSiteAt = align16(trapKeyAt + 8 * static_cast<size_t>(trapCap));
+  const size_t devTotal = trapSiteAt + 4 * static_cast<size_t>(trapCap);
+  NEED(c->batchBlob, devTotal);
   unsigned char *dev = c->batchBlob.p;
   for (uint32_t k = 0; k < m; ++k) {
     LaunchDev &D = bl[k].L;
@@ -2193,6 +2199,10 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
   A.out = reinterpret_cast<BatchOut *>(dev + outAt);
   A.races = reinterpret_cast<hgrd_gpu_race *>(dev + racesAt);
   A.next = reinterpret_cast<unsigned *>(dev + nextAt);
+  A.trapCursor = reinterpret_cast<unsigned *>(dev + nextAt + 4);
+  A.trapKey = reinterpret_cast<uint64_t *>(dev + trapKeyAt);
+  A.trapSite = reinterpret_cast<uint32_t *>(dev + trapSiteAt);
+  A.trapCap = trapCap;
   A.maxKeys = maxKeys;
   A.maxCode = maxCode;
   A.maxSites = maxSites;
@@ -2209,18 +2219,47 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
   ++c->kernelLaunches;
   const size_t d2h = total - outAt;
   CK(cudaMemcpyAsync(c->hBatch, dev + outAt, d2h, cudaMemcpyDeviceToHost, c->st));
-  c->d2hBytes += d2h;
+  unsigned nTrapsAll = 0;
+  CK(cudaMemcpyAsync(&nTrapsAll, dev + nextAt + 4, 4, cudaMemcpyDeviceToHost, c->st));
+  c->d2hBytes += d2h + 4;
   CK(cudaStreamSynchronize(c->st));
+  std::vector<uint64_t> trapKey;
+  std::vector<uint32_t> trapSite;
+  nTrapsAll = std::min(nTrapsAll, trapCap);
+  if (nTrapsAll) { // second round trip only when some launch trapped
+    trapKey.resize(nTrapsAll);
+    trapSite.resize(nTrapsAll);
+    CK(cudaMemcpyAsync(trapKey.data(), dev + trapKeyAt, 8 * static_cast<size_t>(nTrapsAll),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(trapSite.data(), dev + trapSiteAt, 4 * static_cast<size_t>(nTrapsAll),
+                       cudaMemcpyDeviceToHost, c->st));
+    c->d2hBytes += 12 * static_cast<size_t>(nTrapsAll);
+    CK(cudaStreamSynchronize(c->st));
+  }
   const BatchOut *out = reinterpret_cast<const BatchOut *>(c->hBatch);
   const hgrd_gpu_race *races = reinterpret_cast<const hgrd_gpu_race *>(c->hBatch + (racesAt - outAt));
   for (uint32_t k = 0; k < m; ++k) {
     const BatchOut &o = out[k];
     hgrd_gpu_result &r = R[idx[k]];
-    if (o.traps || (o.flags & (kFlagFusedOverflow | kFlagAbort)))
-      continue; // the ordered path decides (traps in canonical order, the abort statement)
+    if (o.flags & (kFlagFusedOverflow | kFlagAbort))
+      continue; // capacity, a hot element or the step budget: the ordered path decides
     if (o.nRaces > r.race_cap) {
       r.n_races = o.nRaces;
       continue;
+    }
+    if (o.nTraps) { // canonical order: thread, then the thread's program order
+      std::vector<uint32_t> ord(o.nTraps);
+      std::iota(ord.begin(), ord.end(), o.trapOff);
+      std::sort(ord.begin(), ord.end(),
+                [&](uint32_t a, uint32_t b) { return trapKey[a] < trapKey[b]; });
+      for (uint32_t q = 0; q < o.nTraps && q < r.trap_cap; ++q) {
+        const uint32_t t = ord[q];
+        r.traps[q] = hgrd_gpu_trap{static_cast<int32_t>(trapSite[t] >> 1),
+                                   (trapSite[t] & 1) ? HGRD_TRAP_UNALLOCATED : HGRD_TRAP_OOB,
+                                   static_cast<int64_t>(trapKey[t] >> 20)};
+        r.n_traps = q + 1;
+      }
+      r.n_traps_total = o.nTraps;
     }
     const BatchPlan &P = plans[idx[k]];
     for (uint32_t q = 0; q < o.nRaces; ++q) {

@@ -213,6 +213,27 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t *owner;      // per element ownership words (nullptr: ablated)
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
+  // k_batch: every trap of the launch, keyed thread << 20 | n-th trap of the
+  // thread (canonical order once sorted); nullptr in k_fused (any trap sends
+  // the launch to the ordered path there)
+  uint64_t *trapKey = nullptr;
+  uint32_t *trapSite = nullptr; // site << 1 | unallocated
+  unsigned *trapCount = nullptr;
+  unsigned trapCap = 0;
+  uint32_t myTraps = 0;
+
+  __device__ __forceinline__ void noteTrap(int site, int param) {
+    if (!trapKey)
+      return;
+    const ParamDev *P = param >= 0 ? &params[param] : nullptr;
+    const bool unalloc = !P || P->handle < 0;
+    const unsigned i = atomicAdd(trapCount, 1u);
+    if (i < trapCap) {
+      trapKey[i] = (static_cast<uint64_t>(tli) << 20) | myTraps;
+      trapSite[i] = (static_cast<uint32_t>(site) << 1) | (unalloc ? 1u : 0u);
+    }
+    ++myTraps;
+  }
 
   __device__ __forceinline__ void pairWithEarlier(uint32_t e, uint64_t r1, int site, uint32_t q,
                                                   bool own) {
@@ -333,8 +354,10 @@ template <class Smem> struct FusedSink : ParState {
   __device__ __forceinline__ int64_t loadK(int site, int param, bool rec, bool own, int64_t idx,
                                            bool need) {
     const ParamDev *P = checkK(param, idx);
-    if (!P)
+    if (!P) {
+      noteTrap(site, param);
       return 0;
+    }
     if (rec)
       record(site, P, idx, own);
     ++seq;
@@ -343,8 +366,10 @@ template <class Smem> struct FusedSink : ParState {
   __device__ __forceinline__ void storeK(int site, int param, bool rec, bool own, int64_t idx,
                                          int64_t) {
     const ParamDev *P = checkK(param, idx);
-    if (!P)
+    if (!P) {
+      noteTrap(site, param);
       return;
+    }
     if (rec)
       record(site, P, idx, own);
     ++seq;

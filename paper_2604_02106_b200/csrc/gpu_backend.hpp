@@ -35,11 +35,25 @@ public:
   int checkLaunch(const hgrd_gpu_launch &l, hgrd_gpu_result &r) override {
     return hgrd_gpu_check_launch(c_, &l, &r);
   }
+  int checkBatch(const hgrd_gpu_batch_launch *b, uint32_t n, hgrd_gpu_result *r) override {
+    return hgrd_gpu_check_batch(c_, b, n, r);
+  }
+  bool hasBatch() const override { return batch_; }
+  void setBatch(bool on) { batch_ = on; }
   std::string lastError() override { return hgrd_gpu_last_error(c_); }
 
 private:
   hgrd_gpu_ctx *c_;
+  bool batch_ = true;
 };
+
+// Sweeps check their configurations' launches in batches (one GPU round
+// trip per batch) unless HGRD_SWEEP_BATCH=0 selects the per-launch path
+// spread over worker contexts.
+inline bool sweepBatched() {
+  const char *e = std::getenv("HGRD_SWEEP_BATCH");
+  return !e || std::atoi(e) != 0;
+}
 
 // Configurations of a sweep are independent runs: they are spread over
 // worker contexts (own streams and buffers on the same GPU, one host thread
@@ -70,8 +84,10 @@ struct SweepWorkers {
       return nullptr;
     if (i > 0)
       setTiming(w, false); // worker contexts only run sweeps
-    if (!bes[static_cast<size_t>(i)])
+    if (!bes[static_cast<size_t>(i)]) {
       bes[static_cast<size_t>(i)] = std::make_unique<GpuBackend>(w);
+      bes[static_cast<size_t>(i)]->setBatch(sweepBatched());
+    }
     return bes[static_cast<size_t>(i)].get();
   }
   std::function<LaunchBackend *(int)> getter() {

@@ -30,6 +30,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <set>
 #include <sstream>
 #include <stdexcept>
@@ -265,6 +266,7 @@ struct PendingLaunch {
   int launchIndex = 0;
   std::array<int64_t, 3> grid{}, block{};
   int64_t warpSize = 32, budget = 0;
+  size_t trapPos = 0; // host traps recorded before the launch
   std::vector<int64_t> regInit;
   std::vector<int32_t> paramHandle;
   std::vector<int64_t> bufElems;             // every buffer of the run
@@ -740,6 +742,7 @@ private:
       p.block = block;
       p.warpSize = cfg_.warpSize;
       p.budget = cfg_.maxSteps;
+      p.trapPos = res_.traps.size();
       p.regInit.assign(lk.nRegs, 0);
       for (size_t i = 0; i < lk.paramReg.size(); ++i)
         if (lk.paramReg[i] >= 0)
@@ -1012,13 +1015,84 @@ SpecRun speculate(CompiledProgram &prog, const ExecConfig &cfg) {
 
 } // namespace
 
-SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps,
-                                    LaunchBackend &backend, int hostThreads) {
-  const std::vector<ExecConfig> cfgs = sweepConfigs(prog, caps);
-  const size_t nc = cfgs.size();
+namespace {
+
+// A configuration of one program's sweep (several programs' sweeps can be
+// batched together).
+struct ConfigJob {
+  CompiledProgram *prog;
+  ExecConfig cfg;
+};
+
+// runConcrete of every configuration in `jobs` (results in order): host
+// runs speculated on host threads, their launches checked in batches, the
+// configurations whose speculation fails re-run exactly.  ENOTSUP when the
+// backend has no batched path.
+// Exact runs of configurations `which` (runConcrete), spread over worker
+// backends 1..n-1 (backend 0 is the batch's), one host thread each.
+struct ExactPool {
+  const std::function<LaunchBackend *(int)> *workers;
+  int n;
+  std::vector<std::thread> threads;
+  std::atomic<size_t> next{0};
+  std::atomic<int> error{0};
+  std::string err;
+
+  void start(const std::vector<ConfigJob> &jobs, const std::vector<size_t> &which,
+             std::vector<RunResult> &out) {
+    const int nt = static_cast<int>(std::min<size_t>(static_cast<size_t>(std::max(n - 1, 0)),
+                                                     which.size()));
+    for (int t = 1; t <= nt; ++t) {
+      LaunchBackend *be = (*workers)(t);
+      if (!be)
+        break;
+      threads.emplace_back([&, be] {
+        for (size_t k; (k = next.fetch_add(1)) < which.size();) {
+          const ConfigJob &j = jobs[which[k]];
+          RunResult r = runConcrete(*j.prog, j.cfg, *be);
+          if (r.error) {
+            error = r.error;
+            err = r.errorMessage;
+          }
+          ++r.stats.restarts;
+          out[which[k]] = std::move(r);
+        }
+      });
+    }
+  }
+  // remaining configurations on the caller's backend, then wait
+  int finish(const std::vector<ConfigJob> &jobs, const std::vector<size_t> &which,
+             std::vector<RunResult> &out, LaunchBackend &be) {
+    for (size_t k; (k = next.fetch_add(1)) < which.size();) {
+      const ConfigJob &j = jobs[which[k]];
+      RunResult r = runConcrete(*j.prog, j.cfg, be);
+      if (r.error) {
+        error = r.error;
+        err = r.errorMessage;
+      }
+      ++r.stats.restarts;
+      out[which[k]] = std::move(r);
+    }
+    for (auto &t : threads)
+      t.join();
+    threads.clear();
+    return error;
+  }
+};
+
+int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend,
+                      int hostThreads, std::vector<RunResult> &outRuns, std::string &err,
+                      const std::function<LaunchBackend *(int)> *workers, int nWorkers) {
+  const size_t nc = jobs.size();
+  const auto tA = std::chrono::steady_clock::now();
   // lower every kernel up front (the cache is not thread-safe)
-  for (const Function &k : prog.program->kernels)
-    prog.kernel(&k);
+  {
+    std::set<CompiledProgram *> progs;
+    for (const ConfigJob &j : jobs)
+      if (progs.insert(j.prog).second)
+        for (const Function &k : j.prog->program->kernels)
+          j.prog->kernel(&k);
+  }
   // 1. speculative host runs, spread over host threads
   std::vector<SpecRun> spec(nc);
   {
@@ -1027,7 +1101,7 @@ SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps
     std::atomic<size_t> next{0};
     auto work = [&] {
       for (size_t i; (i = next.fetch_add(1)) < nc;)
-        spec[i] = speculate(prog, cfgs[i]);
+        spec[i] = speculate(*jobs[i].prog, jobs[i].cfg);
     };
     std::vector<std::thread> pool;
     for (int t = 1; t < nt; ++t)
@@ -1036,6 +1110,18 @@ SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps
     for (auto &th : pool)
       th.join();
   }
+  // configurations whose speculation failed (sequential or lock-idiom
+  // launches, host reads of device results, the host's step budget) run
+  // exactly on the worker backends while the batch is checked
+  outRuns.assign(nc, RunResult{});
+  std::vector<size_t> failed;
+  for (size_t i = 0; i < nc; ++i)
+    if (!spec[i].ok)
+      failed.push_back(i);
+  ExactPool pool{workers, workers ? nWorkers : 0};
+  if (workers && !failed.empty())
+    pool.start(jobs, failed, outRuns);
+  const auto tB = std::chrono::steady_clock::now();
   // 2. every pending launch of every configuration in one batched check
   std::vector<hgrd_gpu_batch_launch> bl;
   std::vector<std::vector<const int64_t *>> dataPtrs;
@@ -1052,6 +1138,9 @@ SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps
   dataPtrs.resize(owner.size());
   std::vector<hgrd_gpu_race> raceStore(std::max<size_t>(nRaceSlots, 1));
   std::vector<hgrd_gpu_result> results(owner.size());
+  constexpr uint32_t kTrapsPerLaunch = 64; // more: the configuration is re-run exactly
+  std::unique_ptr<hgrd_gpu_trap[]> trapStore(
+      new hgrd_gpu_trap[std::max<size_t>(owner.size(), 1) * kTrapsPerLaunch]);
   size_t raceAt = 0;
   for (size_t e = 0; e < owner.size(); ++e) {
     const PendingLaunch &p = spec[owner[e].first].launches[owner[e].second];
@@ -1084,56 +1173,115 @@ SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps
     results[e] = hgrd_gpu_result{};
     results[e].races = raceStore.data() + raceAt;
     results[e].race_cap = static_cast<uint32_t>(3 * nl * nl);
+    results[e].traps = trapStore.get() + e * kTrapsPerLaunch;
+    results[e].trap_cap = kTrapsPerLaunch;
     raceAt += 3 * nl * nl;
   }
+  const auto tC = std::chrono::steady_clock::now();
   if (!bl.empty()) {
     constexpr size_t kChunk = 1 << 16; // launches per batched check
     for (size_t b = 0; b < bl.size(); b += kChunk) {
       const uint32_t m = static_cast<uint32_t>(std::min(kChunk, bl.size() - b));
       const int rc = backend.checkBatch(bl.data() + b, m, results.data() + b);
-      if (rc == HGRD_GPU_ENOTSUP)
-        return enumerateVerdict(prog, caps, backend);
       if (rc < 0) {
-        SweepResult r;
-        r.error = rc;
-        r.errorMessage = backend.lastError();
-        return r;
+        pool.finish(jobs, failed, outRuns, backend);
+        err = backend.lastError();
+        return rc;
       }
     }
   }
+  const auto tD = std::chrono::steady_clock::now();
   // 3. per configuration in canonical order: the speculation's report, or an
-  //    exact re-run; then the sweep's first-wins dedup (:883-889)
+  //    exact re-run
   std::vector<char> exact(nc, 0);
   for (size_t i = 0; i < nc; ++i)
     exact[i] = !spec[i].ok;
   std::vector<int64_t> kernelSteps(nc, 0);
+  size_t nSpecFail = 0, nUnchecked = 0;
+  for (size_t i = 0; i < nc; ++i)
+    nSpecFail += !spec[i].ok;
   for (size_t e = 0; e < owner.size(); ++e) {
     const size_t i = owner[e].first;
-    if (results[e].mode & HGRD_RESULT_UNCHECKED)
+    if (results[e].mode & HGRD_RESULT_UNCHECKED) {
+      nUnchecked += !exact[i];
       exact[i] = 1;
+    }
     kernelSteps[i] += results[e].steps;
   }
-  SweepResult out;
-  out.configs = nc;
-  std::set<std::tuple<int, int, int, int, int, int64_t>> seen;
+  // development: HGRD_SWEEP_TRACE=1 prints why configurations were re-run
+  static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
+  if (trace) {
+    auto us = [](auto a, auto b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    std::fprintf(stderr, "[hgrd sweep] %zu configs, %zu launches batched, %zu speculation "
+                 "failures, %zu with unchecked launches; speculate %.0f prepare %.0f batch %.0f "
+                 "(us)\n", nc, owner.size(), nSpecFail, nUnchecked, us(tA, tB), us(tB, tC),
+                 us(tC, tD));
+  }
+  if (pool.finish(jobs, failed, outRuns, backend) < 0) {
+    err = pool.err;
+    return pool.error;
+  }
   size_t e = 0;
   for (size_t i = 0; i < nc; ++i) {
-    RunResult r;
+    RunResult &r = outRuns[i];
     const size_t e0 = e;
     while (e < owner.size() && owner[e].first == i)
       ++e;
-    if (!exact[i] && spec[i].hostSteps + kernelSteps[i] > cfgs[i].maxSteps)
+    if (!spec[i].ok)
+      continue; // (run exactly by the pool)
+    if (!exact[i] && spec[i].hostSteps + kernelSteps[i] > jobs[i].cfg.maxSteps)
       exact[i] = 1; // the budget runs out somewhere: the exact run finds where
     if (exact[i]) {
-      r = runConcrete(prog, cfgs[i], backend);
+      r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend);
       if (r.error) {
-        out.error = r.error;
-        out.errorMessage = r.errorMessage;
-        return out;
+        err = r.errorMessage;
+        return r.error;
       }
-      ++out.stats.restarts;
+      ++r.stats.restarts;
     } else {
+      // kernel traps go between the host traps recorded before and after
+      // their launch; the run keeps the first 256 (reference :125-130)
+      std::vector<std::string> traps;
+      const std::vector<std::string> &hostTraps = spec[i].res.traps;
+      size_t hostAt = 0;
+      bool truncated = false;
+      for (size_t q = e0; q < e && !truncated; ++q) {
+        const PendingLaunch &p = spec[i].launches[q - e0];
+        while (hostAt < p.trapPos && hostAt < hostTraps.size())
+          traps.push_back(hostTraps[hostAt++]);
+        const hgrd_gpu_result &kr = results[q];
+        const uint64_t want = std::min<uint64_t>(kr.n_traps_total,
+                                                 traps.size() < 256 ? 256 - traps.size() : 0);
+        if (want > kr.n_traps) {
+          truncated = true; // more traps than the batch handed back
+          break;
+        }
+        for (uint64_t t = 0; t < want; ++t) {
+          const auto si = static_cast<size_t>(kr.traps[t].site);
+          traps.push_back(jobs[i].prog->program->file + ":" + std::to_string(p.lk->siteLoc[si].line) +
+                          ": " +
+                          (kr.traps[t].kind == HGRD_TRAP_OOB ? "kernel access out of bounds on "
+                                                             : "kernel access to unallocated array ") +
+                          p.lk->siteArray[si]);
+        }
+      }
+      if (truncated) {
+        r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend);
+        if (r.error) {
+          err = r.errorMessage;
+          return r.error;
+        }
+        ++r.stats.restarts;
+        continue;
+      }
+      while (hostAt < hostTraps.size())
+        traps.push_back(hostTraps[hostAt++]);
+      if (traps.size() > 256)
+        traps.resize(256);
       r = std::move(spec[i].res);
+      r.traps = std::move(traps);
       SeenKeys keys;
       for (size_t q = e0; q < e; ++q) {
         const PendingLaunch &p = spec[i].launches[q - e0];
@@ -1142,14 +1290,51 @@ SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps
         r.stats.instances += results[q].instances;
         r.stats.records += results[q].records;
         r.stats.kernelSteps += results[q].steps;
+        ++r.stats.batchedLaunches;
       }
       sortRaces(r.races);
     }
+  }
+  return 0;
+}
+
+} // namespace
+
+int sweepHostThreads() {
+  if (const char *e = std::getenv("HGRD_SWEEP_THREADS"))
+    return std::max(1, std::atoi(e));
+  return static_cast<int>(std::min(32u, std::max(1u, std::thread::hardware_concurrency())));
+}
+
+SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps,
+                                    LaunchBackend &backend, int hostThreads,
+                                    const std::function<LaunchBackend *(int)> *workers,
+                                    int nWorkers) {
+  const std::vector<ExecConfig> cfgs = sweepConfigs(prog, caps);
+  std::vector<ConfigJob> jobs;
+  for (const ExecConfig &c : cfgs)
+    jobs.push_back(ConfigJob{&prog, c});
+  std::vector<RunResult> runs;
+  std::string err;
+  const int rc = runConfigsBatched(jobs, backend, hostThreads, runs, err, workers, nWorkers);
+  if (rc == HGRD_GPU_ENOTSUP)
+    return enumerateVerdict(prog, caps, backend);
+  SweepResult out;
+  if (rc < 0) {
+    out.error = rc;
+    out.errorMessage = err;
+    return out;
+  }
+  out.configs = cfgs.size();
+  std::set<std::tuple<int, int, int, int, int, int64_t>> seen; // first wins, :883-889
+  for (size_t i = 0; i < cfgs.size(); ++i) {
+    const RunResult &r = runs[i];
     out.stats.instances += r.stats.instances;
     out.stats.records += r.stats.records;
     out.stats.parLaunches += r.stats.parLaunches;
     out.stats.seqLaunches += r.stats.seqLaunches;
     out.stats.restarts += r.stats.restarts;
+    out.stats.batchedLaunches += r.stats.batchedLaunches;
     for (const auto &race : r.races) {
       auto key = std::make_tuple(race.locA.line, race.locA.col, race.locB.line, race.locB.col,
                                  race.kind, cfgs[i].warpSize);
@@ -1159,6 +1344,45 @@ SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps
   }
   return out;
 }
+
+SweepShard sweepShardBatched(CompiledProgram &prog, const SweepCaps &caps, int rank, int world,
+                             LaunchBackend &backend, int hostThreads) {
+  const std::vector<ExecConfig> all = sweepConfigs(prog, caps);
+  std::vector<ExecConfig> mine;
+  std::vector<uint64_t> index;
+  for (size_t k = 0; k < all.size(); ++k)
+    if (static_cast<int>(k % static_cast<size_t>(world)) == rank) {
+      mine.push_back(all[k]);
+      index.push_back(k);
+    }
+  std::vector<ConfigJob> jobs;
+  for (const ExecConfig &c : mine)
+    jobs.push_back(ConfigJob{&prog, c});
+  std::vector<RunResult> runs;
+  std::string err;
+  const int rc = runConfigsBatched(jobs, backend, hostThreads, runs, err, nullptr, 0);
+  if (rc == HGRD_GPU_ENOTSUP)
+    return sweepShard(prog, caps, rank, world, backend);
+  SweepShard out;
+  out.total = all.size();
+  if (rc < 0) {
+    out.error = rc;
+    out.errorMessage = err;
+    return out;
+  }
+  for (size_t i = 0; i < mine.size(); ++i) {
+    RunResult &r = runs[i];
+    out.stats.instances += r.stats.instances;
+    out.stats.records += r.stats.records;
+    out.stats.parLaunches += r.stats.parLaunches;
+    out.stats.seqLaunches += r.stats.seqLaunches;
+    out.stats.restarts += r.stats.restarts;
+    out.stats.batchedLaunches += r.stats.batchedLaunches;
+    out.configs.push_back(ShardConfig{index[i], mine[i].warpSize, std::move(r.races)});
+  }
+  return out;
+}
+
 
 SweepShard sweepShard(CompiledProgram &prog, const SweepCaps &caps, int rank, int world,
                       LaunchBackend &backend) {
@@ -1430,9 +1654,9 @@ std::string statsJ(const RunStats &s) {
   std::snprintf(buf, sizeof buf,
                 "{\"instances\":%" PRIu64 ",\"records\":%" PRIu64
                 ",\"kernelSteps\":%" PRId64 ",\"deviceMs\":%.6f,\"parallelLaunches\":%d,"
-                "\"sequentialLaunches\":%d,\"restarts\":%d}",
+                "\"sequentialLaunches\":%d,\"restarts\":%d,\"batchedLaunches\":%d}",
                 s.instances, s.records, s.kernelSteps, s.deviceMs, s.parLaunches,
-                s.seqLaunches, s.restarts);
+                s.seqLaunches, s.restarts, s.batchedLaunches);
   return buf;
 }
 
@@ -1455,17 +1679,20 @@ bool parseExecConfigJson(const char *json, ExecConfig &c, std::string &err) {
   return true;
 }
 
+void capsFromJson(const JVal &o, SweepCaps &c) {
+  readArr3(o, "gridCap", c.gridCap);
+  readArr3(o, "blockCap", c.blockCap);
+  readVec(o, "inputSet", c.inputSet);
+  readVec(o, "warpSizes", c.warpSizes);
+  readI64(o, "maxThreads", c.maxThreads);
+  int64_t mc;
+  if (readI64(o, "maxConfigs", mc))
+    c.maxConfigs = static_cast<uint64_t>(mc);
+}
+
 bool parseSweepCapsJson(const char *json, SweepCaps &c, std::string &err) {
   try {
-    JVal o = JParse(json && *json ? json : "{}").value();
-    readArr3(o, "gridCap", c.gridCap);
-    readArr3(o, "blockCap", c.blockCap);
-    readVec(o, "inputSet", c.inputSet);
-    readVec(o, "warpSizes", c.warpSizes);
-    readI64(o, "maxThreads", c.maxThreads);
-    int64_t mc;
-    if (readI64(o, "maxConfigs", mc))
-      c.maxConfigs = static_cast<uint64_t>(mc);
+    capsFromJson(JParse(json && *json ? json : "{}").value(), c);
   } catch (const std::exception &e) {
     err = e.what();
     return false;
@@ -1577,7 +1804,8 @@ int sweepShardJsonRun(LaunchBackend &be, const char *src, const char *file,
   }
   std::string fileName = po.program->file;
   auto cp = compileProgram(std::move(po.program));
-  SweepShard r = sweepShard(*cp, caps, rank, world, be);
+  SweepShard r = be.hasBatch() ? sweepShardBatched(*cp, caps, rank, world, be, sweepHostThreads())
+                               : sweepShard(*cp, caps, rank, world, be);
   if (r.error) {
     out = errorJson({"backend: " + r.errorMessage});
     return r.error;
@@ -1677,6 +1905,8 @@ SweepResult enumerateVerdictParallel(CompiledProgram &prog, const SweepCaps &cap
 
 SweepResult enumerateVerdictOnWorkers(const std::function<LaunchBackend *(int)> &workers, int n,
                                       CompiledProgram &cp, const SweepCaps &caps) {
+  if (LaunchBackend *b0 = workers(0); b0 && b0->hasBatch())
+    return enumerateVerdictBatched(cp, caps, *b0, sweepHostThreads(), &workers, n);
   const uint64_t size = sweepSize(cp, caps);
   // one configuration per worker at least: a configuration costs a few
   // GPU round trips (~30 us each), more than spawning its worker thread
@@ -1723,6 +1953,134 @@ int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &work
   return HGRD_GPU_OK;
 }
 
+int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
+                  const char *jobsJson, int rank, int world, std::string &out) {
+  if (world < 1 || rank < 0 || rank >= world) {
+    out = errorJson({"bad rank / world"});
+    return HGRD_GPU_EINVAL;
+  }
+  struct Job {
+    std::string file, error;
+    std::unique_ptr<CompiledProgram> cp;
+    SweepCaps caps;
+    std::vector<ExecConfig> cfgs; // this rank's configurations
+    std::vector<uint64_t> index;  // their canonical indices
+    uint64_t total = 0;
+    size_t first = 0;             // first entry in the combined list
+  };
+  std::vector<Job> jobs;
+  try {
+    JVal arr = JParse(jobsJson ? jobsJson : "[]").value();
+    if (arr.kind != JVal::Arr)
+      throw std::runtime_error("jobs: expected an array");
+    for (const JVal &j : arr.arr) {
+      Job job;
+      const JVal *src = j.get("source");
+      const JVal *file = j.get("file");
+      job.file = file && file->kind == JVal::Str ? file->s : "prog.mcu";
+      if (const JVal *c = j.get("caps"))
+        capsFromJson(*c, job.caps);
+      ParseOutcome po = parseMiniCU(src && src->kind == JVal::Str ? src->s : "", job.file);
+      if (!po.program) {
+        job.error = errorJson(po.diagnostics);
+      } else {
+        job.cp = compileProgram(std::move(po.program));
+        const std::vector<ExecConfig> all = sweepConfigs(*job.cp, job.caps);
+        job.total = all.size();
+        for (size_t k = 0; k < all.size(); ++k)
+          if (static_cast<int>(k % static_cast<size_t>(world)) == rank) {
+            job.cfgs.push_back(all[k]);
+            job.index.push_back(k);
+          }
+      }
+      jobs.push_back(std::move(job));
+    }
+  } catch (const std::exception &e) {
+    out = errorJson({std::string("jobs: ") + e.what()});
+    return HGRD_GPU_EINVAL;
+  }
+  // every job's configurations in one batched run
+  std::vector<ConfigJob> all;
+  for (Job &j : jobs) {
+    j.first = all.size();
+    for (const ExecConfig &c : j.cfgs)
+      all.push_back(ConfigJob{j.cp.get(), c});
+  }
+  LaunchBackend *b0 = workers(0);
+  if (!b0) {
+    out = errorJson({"no backend"});
+    return HGRD_GPU_ENODEV;
+  }
+  std::vector<RunResult> runs;
+  std::string err;
+  int rc = b0->hasBatch() ? runConfigsBatched(all, *b0, sweepHostThreads(), runs, err, &workers, n)
+                          : HGRD_GPU_ENOTSUP;
+  if (rc == HGRD_GPU_ENOTSUP) {
+    runs.clear();
+    for (const ConfigJob &c : all) {
+      runs.push_back(runConcrete(*c.prog, c.cfg, *b0));
+      if (runs.back().error) {
+        rc = runs.back().error;
+        err = runs.back().errorMessage;
+        break;
+      }
+    }
+    if (rc == HGRD_GPU_ENOTSUP)
+      rc = 0;
+  }
+  if (rc < 0) {
+    out = errorJson({"backend: " + err});
+    return rc;
+  }
+  out = "[";
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    Job &j = jobs[q];
+    if (q)
+      out += ",";
+    if (!j.error.empty()) {
+      out += j.error;
+      continue;
+    }
+    if (world == 1) { // the job's enumerateVerdict result
+      SweepResult sr;
+      sr.configs = j.total;
+      std::set<std::tuple<int, int, int, int, int, int64_t>> seen; // first wins, :883-889
+      for (size_t k = 0; k < j.cfgs.size(); ++k) {
+        const RunResult &r = runs[j.first + k];
+        sr.stats.instances += r.stats.instances;
+        sr.stats.records += r.stats.records;
+        sr.stats.parLaunches += r.stats.parLaunches;
+        sr.stats.seqLaunches += r.stats.seqLaunches;
+        sr.stats.restarts += r.stats.restarts;
+        sr.stats.batchedLaunches += r.stats.batchedLaunches;
+        for (const auto &race : r.races) {
+          auto key = std::make_tuple(race.locA.line, race.locA.col, race.locB.line,
+                                     race.locB.col, race.kind, j.cfgs[k].warpSize);
+          if (seen.insert(key).second)
+            sr.races.push_back(SweepRace{race.locA, race.locB, race.kind, j.cfgs[k].warpSize});
+        }
+      }
+      out += sweepResultJson(sr, j.file);
+    } else { // this rank's share (parallel.merge_shards combines them)
+      SweepShard sh;
+      sh.total = j.total;
+      for (size_t k = 0; k < j.cfgs.size(); ++k) {
+        RunResult &r = runs[j.first + k];
+        sh.stats.instances += r.stats.instances;
+        sh.stats.records += r.stats.records;
+        sh.stats.parLaunches += r.stats.parLaunches;
+        sh.stats.seqLaunches += r.stats.seqLaunches;
+        sh.stats.restarts += r.stats.restarts;
+        sh.stats.batchedLaunches += r.stats.batchedLaunches;
+        sh.configs.push_back(ShardConfig{j.index[k], j.cfgs[k].warpSize, std::move(r.races)});
+      }
+      out += sweepShardJson(sh, j.file);
+    }
+  }
+  out += "]";
+  return HGRD_GPU_OK;
+}
+
 int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
                          const char *capsJson, std::string &out) {
   SweepCaps caps;
@@ -1738,7 +2096,8 @@ int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
   }
   std::string fileName = po.program->file;
   auto cp = compileProgram(std::move(po.program));
-  SweepResult r = enumerateVerdict(*cp, caps, be);
+  SweepResult r = be.hasBatch() ? enumerateVerdictBatched(*cp, caps, be, sweepHostThreads())
+                                : enumerateVerdict(*cp, caps, be);
   if (r.error) {
     out = errorJson({"backend: " + r.errorMessage});
     return r.error;

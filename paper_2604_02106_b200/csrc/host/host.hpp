@@ -72,6 +72,7 @@ struct RunStats {
   int64_t kernelSteps = 0;
   double deviceMs = 0;
   int parLaunches = 0, seqLaunches = 0, restarts = 0;
+  int batchedLaunches = 0; // checked by a batched backend call (sweeps)
 };
 
 // reference OracleResult (oracle.hpp:47-55)
@@ -117,6 +118,7 @@ public:
   virtual int checkBatch(const hgrd_gpu_batch_launch *, uint32_t, hgrd_gpu_result *) {
     return HGRD_GPU_ENOTSUP;
   }
+  virtual bool hasBatch() const { return false; }
   virtual std::string lastError() = 0;
 };
 
@@ -164,8 +166,18 @@ SweepResult enumerateVerdictParallel(CompiledProgram &prog, const SweepCaps &cap
 // backend call; a configuration whose speculation fails is re-run exactly
 // through runConcrete.  Same result as enumerateVerdict.  Falls back to it
 // when the backend has no batched path.
+// `workers` (optional): backends 1..nWorkers-1 run the configurations that
+// cannot be speculated (sequential / lock-idiom launches, host reads of
+// device results) while the batch is checked on `backend`.
 SweepResult enumerateVerdictBatched(CompiledProgram &prog, const SweepCaps &caps,
-                                    LaunchBackend &backend, int hostThreads);
+                                    LaunchBackend &backend, int hostThreads,
+                                    const std::function<LaunchBackend *(int)> *workers = nullptr,
+                                    int nWorkers = 0);
+SweepShard sweepShardBatched(CompiledProgram &prog, const SweepCaps &caps, int rank, int world,
+                             LaunchBackend &backend, int hostThreads);
+// Host threads for the speculative runs of a batched sweep
+// (HGRD_SWEEP_THREADS, default: the hardware threads, at most 32).
+int sweepHostThreads();
 // Configurations enumerateVerdict runs (warp sizes x input odometer, capped).
 uint64_t sweepSize(const CompiledProgram &prog, const SweepCaps &caps);
 int sweepShardJsonRun(LaunchBackend &be, const char *src, const char *file,
@@ -191,6 +203,14 @@ int enumerateVerdictJson(LaunchBackend &be, const char *src, const char *file,
 // at least 4 configurations per worker.
 SweepResult enumerateVerdictOnWorkers(const std::function<LaunchBackend *(int)> &workers, int n,
                                       CompiledProgram &cp, const SweepCaps &caps);
+// Many programs' sweeps at once (BASELINE config 5: thousands of program x
+// configuration jobs).  jobsJson: [{"source", "file", "caps"}, ...].  Every
+// job's configurations (this rank's share: canonical index % world == rank)
+// are run together, batched when workers(0) has a batched path.  out: one
+// entry per job — its enumerateVerdict result (world 1) or its sweep shard
+// (world > 1, merged by parallel.merge_shards) or its parse error.
+int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
+                  const char *jobsJson, int rank, int world, std::string &out);
 int enumerateVerdictJsonParallel(const std::function<LaunchBackend *(int)> &workers, int n,
                                  const char *src, const char *file, const char *capsJson,
                                  std::string &out);

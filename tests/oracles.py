@@ -37,9 +37,24 @@ class RefOracle:
         self.lib.hgrd_ref_enumerate_verdict.restype = ctypes.c_void_p
         self.lib.hgrd_ref_enumerate_verdict.argtypes = [ctypes.c_char_p] * 3
         self.lib.hgrd_ref_free.argtypes = [ctypes.c_void_p]
+        self.lib.hgrd_ref_time_sweeps.restype = ctypes.c_double
+        self.lib.hgrd_ref_time_sweeps.argtypes = [ctypes.c_void_p] * 3 + [
+            ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         self.lib.hgrd_ref_time_parallel.restype = ctypes.c_double
         self.lib.hgrd_ref_time_parallel.argtypes = [ctypes.c_char_p] * 3 + [
             ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+
+    def time_sweeps(self, jobs, threads: int):
+        """Wall seconds of enumerateVerdict over `jobs` [(source, file, caps)]
+        on `threads` host threads; returns (seconds, total sweep races)."""
+        n = len(jobs)
+        arr = ctypes.c_char_p * max(n, 1)
+        srcs = arr(*[j[0].encode() for j in jobs])
+        files = arr(*[j[1].encode() for j in jobs])
+        caps = arr(*[_cfg(j[2]) for j in jobs])
+        races = ctypes.c_int(0)
+        secs = self.lib.hgrd_ref_time_sweeps(srcs, files, caps, n, threads, ctypes.byref(races))
+        return secs, races.value
 
     def _take(self, p) -> dict:
         s = ctypes.string_at(p).decode()
@@ -66,9 +81,12 @@ class CpuOracle:
     def __init__(self, path: str = ORACLE_LIB):
         self.lib = ctypes.CDLL(path)
         P = ctypes.c_void_p
-        for fn in ("hgrd_oracle_run_concrete_json", "hgrd_oracle_enumerate_verdict_json"):
+        for fn in ("hgrd_oracle_run_concrete_json", "hgrd_oracle_enumerate_verdict_json",
+                   "hgrd_oracle_enumerate_verdict_batched_json"):
             getattr(self.lib, fn).argtypes = [ctypes.c_char_p] * 3 + [ctypes.POINTER(P)]
         self.lib.hgrd_oracle_free.argtypes = [P]
+        self.lib.hgrd_oracle_enumerate_verdict_many_json.argtypes = [
+            ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
         self.lib.hgrd_oracle_check_launch.argtypes = [P, P, P, ctypes.c_int32, P]
         self.lib.hgrd_oracle_sweep_shard_json.argtypes = [ctypes.c_char_p] * 3 + [
             ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
@@ -89,6 +107,25 @@ class CpuOracle:
 
     def enumerate_verdict(self, source: str, caps=None, file_name: str = "prog.mcu") -> dict:
         return self._call("hgrd_oracle_enumerate_verdict_json", source, caps, file_name)
+
+    def enumerate_verdict_batched(self, source: str, caps=None,
+                                  file_name: str = "prog.mcu") -> dict:
+        """The product's speculative batched sweep (host.cpp
+        enumerateVerdictBatched) with the restatement as its batch backend."""
+        return self._call("hgrd_oracle_enumerate_verdict_batched_json", source, caps, file_name)
+
+    def enumerate_verdict_many(self, jobs, rank: int = 0, world: int = 1,
+                               batched: bool = True) -> list:
+        """sweepManyJson over [{"source", "file", "caps"}] (the product's
+        many-sweeps path) with the restatement as backend."""
+        out = ctypes.c_void_p()
+        rc = self.lib.hgrd_oracle_enumerate_verdict_many_json(
+            json.dumps(jobs).encode(), rank, world, 1 if batched else 0, ctypes.byref(out))
+        s = ctypes.string_at(out.value).decode()
+        self.lib.hgrd_oracle_free(out)
+        if rc != 0:
+            raise RuntimeError(f"enumerate_verdict_many failed ({rc}): {s}")
+        return json.loads(s)
 
     def sweep_shard(self, source: str, caps=None, file_name: str = "prog.mcu",
                     rank: int = 0, world: int = 1) -> dict:

@@ -70,12 +70,31 @@ def test_xlarge(gpu):
 
 def test_lattice_config5(gpu):
     """BASELINE config 5: the reference's enumerateVerdict output for every
-    program of the 10k-configuration lattice."""
+    program of the 10k-configuration lattice, through the batched sweep
+    (k_batch: nearly every launch of the lattice in one batched check per
+    program)."""
     jobs = load_golden("lattice")
     assert len(jobs) == 229
+    batched = 0
     for j in jobs:
-        got = strip_extras(gpu.enumerate_verdict(j["source"], j["caps"], j["file"]))
-        assert got == j["sweep"], j["name"]
+        got = gpu.enumerate_verdict(j["source"], j["caps"], j["file"])
+        assert strip_extras(got) == j["sweep"], j["name"]
+        batched += got["stats"]["batchedLaunches"]
+    assert batched > 8000, batched
+
+
+def test_sweeps_per_launch_path(gpu):
+    """HGRD_SWEEP_BATCH=0: the per-launch sweep path over worker contexts
+    gives the same reports (and batches nothing)."""
+    import os
+    os.environ["HGRD_SWEEP_BATCH"] = "0"
+    try:
+        for e in load_golden("corpus"):
+            got = gpu.enumerate_verdict(e["source"], e["caps"], e["file"])
+            assert strip_extras(got) == e["sweep_manifest"], e["name"]
+            assert got["stats"]["batchedLaunches"] == 0
+    finally:
+        del os.environ["HGRD_SWEEP_BATCH"]
 
 
 # ------------------------------------------- permutation scatter, full size

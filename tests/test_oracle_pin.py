@@ -153,3 +153,25 @@ def test_structural_predictors_pinned():
             assert wit == [(x, y) for _, _, x, y in want], name
             n_checked += 1
     assert n_checked >= 5
+
+
+def test_batched_sweeps(cpu_oracle):
+    """The speculative batched sweep (configurations' host runs speculated,
+    launches checked as one batch with traps merged in canonical order,
+    failed speculations re-run exactly) reproduces the reference's
+    enumerateVerdict on the corpus (manifest and default caps), the fuzz
+    programs and the config-5 lattice."""
+    restarts = configs = 0
+    for e in load_golden("corpus"):
+        for caps, want in ((e["caps"], e["sweep_manifest"]), ({}, e["sweep_default"])):
+            got = cpu_oracle.enumerate_verdict_batched(e["source"], caps, e["file"])
+            assert strip_extras(got) == want, e["name"]
+    for f in load_golden("fuzz"):
+        got = cpu_oracle.enumerate_verdict_batched(f["source"], {}, "fuzz.mcu")
+        assert strip_extras(got) == f["sweep"], f["index"]
+    for j in load_golden("lattice"):
+        got = cpu_oracle.enumerate_verdict_batched(j["source"], j["caps"], j["file"])
+        assert strip_extras(got) == j["sweep"], j["name"]
+        restarts += got["stats"]["restarts"]
+        configs += got["configs"]
+    assert configs == 9695 and restarts < configs // 50  # most configurations batched

@@ -272,6 +272,23 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def init_dist(local):
+    """NCCL process group (torchrun's env://; HGRD_BENCH_DIST=1 alone: a
+    single-rank group on this GPU, to exercise the multi-rank code path)."""
+    import torch
+    import torch.distributed as dist
+    if "RANK" not in os.environ:
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(port))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -398,9 +415,7 @@ def run_gpu_arm(args):
     # (HGRD_BENCH_DIST=1: the multi-rank code path at world size 1, for testing)
     use_dist = ws > 1 or os.environ.get("HGRD_BENCH_DIST") == "1"
     if use_dist:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     dev = torch.device("cuda", local)
     ctx = hg.GpuContext(local)
     ctx.set_profiling(True)
@@ -714,9 +729,7 @@ def run_sweep_arm(args):
     ws, rank, local = dist_env()
     use_dist = ws > 1 or os.environ.get("HGRD_BENCH_DIST") == "1"
     if use_dist:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     jobs, want, cfg_index = sweep_job_list(args.workload)
     ctx = hg.GpuContext(local)
 

@@ -158,7 +158,7 @@ extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, con
   L.step_budget = int64_t(1) << 40;
   std::string s = "{\"variants\":[";
   bool ok = true;
-  for (int v = 0; v <= hgrdgpu::jit::kExpandSeq; ++v) {
+  for (int v = 0; v < hgrdgpu::jit::kVariants; ++v) {
     std::string err;
     const size_t bytes = hgrdgpu::jit::compileOnly(L, rec, params, static_cast<hgrdgpu::jit::Variant>(v), err);
     ok = ok && bytes > 0;

@@ -735,7 +735,11 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
 
 int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
   if (c->hCtr->flags & (kFlagLockSet | kFlagSegment)) {
-    c->err = "pairwise detector limits exceeded (lock sets > 8 or element > 65535 events)";
+    c->err = (c->hCtr->flags & kFlagLockSet)
+                 ? std::string("pairwise detector limit exceeded: a lock set of more than 8 locks")
+                 : "pairwise detector limit exceeded: an element of more than " +
+                       std::to_string(kPairGroupMax - 1) + " events or more than " +
+                       std::to_string(kPairEventsMax - 1) + " events in total";
     return HGRD_GPU_ENOTSUP;
   }
   const unsigned nr = c->hCtr->nRaces;
@@ -868,16 +872,23 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   const uint64_t perIter = static_cast<uint64_t>(bpi * D.tpb) * per;
   if (bpi * D.tpb > 65536 || (!loops && perIter > 4096))
     return 0;
-  // record capacity per iteration: 256 threads x 4, x 8 or x 16
-  const int ipt = (!loops && perIter <= 1024) ? 4 : (!loops && perIter <= 2048) ? 8 : 16;
-  const size_t smem = ipt == 4   ? fusedSmemBytes<256, 4>(L, P, nKeys)
-                      : ipt == 8 ? fusedSmemBytes<256, 8>(L, P, nKeys)
-                                 : fusedSmemBytes<256, 16>(L, P, nKeys);
+  // record capacity per iteration: 256 threads x 4, x 8, x 12 or x 16 (the
+  // smallest that holds a straight-line iteration: shared memory decides how
+  // many CTAs share an SM — x 12 keeps two, x 16 one)
+  const int ipt = (!loops && perIter <= 1024)   ? 4
+                  : (!loops && perIter <= 2048) ? 8
+                  : (!loops && perIter <= 3072) ? 12
+                                                : 16;
+  const size_t smem = ipt == 4    ? fusedSmemBytes<256, 4>(L, P, nKeys)
+                      : ipt == 8  ? fusedSmemBytes<256, 8>(L, P, nKeys)
+                      : ipt == 12 ? fusedSmemBytes<256, 12>(L, P, nKeys)
+                                  : fusedSmemBytes<256, 16>(L, P, nKeys);
   if (smem > 227 * 1024)
     return 0;
 
-  // ownership table (epoch-tagged, no memset between launches)
-  const size_t ownerN = std::max<uint64_t>(P.totalW, 1);
+  // ownership table (two epoch-tagged words per element, no memset between
+  // launches; device.cuh ownerJoin)
+  const size_t ownerN = 2 * std::max<uint64_t>(P.totalW, 1);
   const bool fresh = c->owner.cap < ownerN;
   NEED(c->owner, ownerN);
   if (fresh || c->epoch >= 4094) {
@@ -900,7 +911,10 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   // a launch that fits one iteration finds its INTER pairs on chip as well
   // (no ownership exchanges, no pass 2); shards leave INTER to their tables
   F.interOnChip = !shard && F.nIters == 1;
-  F.owner = (shard || F.interOnChip) ? nullptr : c->owner.p;
+  bool anyOwn = false; // a buffer two blocks may reach (affine.cpp could not prove privacy)
+  for (const SiteDev &sd : P.sites)
+    anyOwn |= sd.record && sd.own;
+  F.owner = (shard || F.interOnChip || !anyOwn) ? nullptr : c->owner.p;
   F.epoch = c->epoch;
   F.keyElem = c->curKeyElem;
   F.cand = c->cand.p;
@@ -912,13 +926,22 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
   if (const char *ab = std::getenv("HGRD_FUSED_ABLATE"))
     F.ablate = std::atoi(ab);
-  int rc = ipt == 4   ? launchFused<256, 4>(c, F, smem, jk.get(hgrdgpu::jit::kFusedNarrow))
-           : ipt == 8 ? launchFused<256, 8>(c, F, smem, jk.get(hgrdgpu::jit::kFusedMid))
-                      : launchFused<256, 16>(c, F, smem, jk.get(hgrdgpu::jit::kFusedWide));
+  int rc = ipt == 4    ? launchFused<256, 4>(c, F, smem, jk.get(hgrdgpu::jit::kFusedNarrow))
+           : ipt == 8  ? launchFused<256, 8>(c, F, smem, jk.get(hgrdgpu::jit::kFusedMid))
+           : ipt == 12 ? launchFused<256, 12>(c, F, smem, jk.get(hgrdgpu::jit::kFused12))
+                       : launchFused<256, 16>(c, F, smem, jk.get(hgrdgpu::jit::kFusedWide));
   if (rc < 0)
     return rc;
   CK(cudaGetLastError());
   ++c->kernelLaunches;
+  if (F.owner) { // any element reached from two blocks? (read with the counters)
+    StageTimer t(c, "k_owner_any");
+    k_owner_any<<<static_cast<unsigned>(std::min<uint64_t>((P.totalW + 255) / 256,
+                                                           uint64_t(c->nSM) * 8)),
+                  256, 0, c->st>>>(c->owner.p, P.totalW, c->epoch << 20, D.ctr);
+    CK(cudaGetLastError());
+    ++c->kernelLaunches;
+  }
   rc = readCountersAndRaces(c, static_cast<size_t>(nKeys));
   if (rc < 0)
     return rc;
@@ -946,7 +969,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   LaunchDev D2 = D;
   D2.ctr = c->ctr2.p;
   D2.ownerFilter = c->owner.p;
-  D2.ownerMultiTag = (c->epoch << 20) | kOwnerMulti;
+  D2.ownerMultiTag = c->epoch << 20; // (the launch's epoch tag: ownerIsMulti)
   const size_t sm2 = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
                      sizeof(ParamDev) * P.params.size();
   const unsigned grid2 = static_cast<unsigned>(std::min<uint64_t>(
@@ -2032,6 +2055,9 @@ template <class T> size_t batchPut(std::vector<unsigned char> &blob, const T *sr
 
 int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
                hgrd_gpu_result *R) {
+  // development: HGRD_SWEEP_TRACE=1 prints the batch's size and phase times
+  static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   for (uint32_t i = 0; i < n; ++i) {
     resetResult(&R[i]);
     R[i].mode = HGRD_RESULT_UNCHECKED;
@@ -2169,6 +2195,7 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     CK(cudaMallocHost(&c->hBatch, c->hBatchCap));
   }
   std::memcpy(c->hBatch, blob.data(), h2d);
+  const auto t1 = std::chrono::steady_clock::now();
   CK(cudaMemcpyAsync(dev, c->hBatch, h2d, cudaMemcpyHostToDevice, c->st));
   c->h2dBytes += h2d;
 
@@ -2223,6 +2250,7 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
   CK(cudaMemcpyAsync(&nTrapsAll, dev + nextAt + 4, 4, cudaMemcpyDeviceToHost, c->st));
   c->d2hBytes += d2h + 4;
   CK(cudaStreamSynchronize(c->st));
+  const auto t2 = std::chrono::steady_clock::now();
   std::vector<uint64_t> trapKey;
   std::vector<uint32_t> trapSite;
   nTrapsAll = std::min(nTrapsAll, trapCap);
@@ -2272,6 +2300,15 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     r.instances = o.instances;
     r.records = o.records;
     r.mode = 0;
+  }
+  if (trace) {
+    const auto t3 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    std::fprintf(stderr, "[hgrd batch] %u launches (%u in the envelope), blob %zu B, smem %zu B, "
+                 "grid %u, traps %u; plan+stage %.0f, h2d+kernel+d2h %.0f, results %.0f (us)\n",
+                 n, m, h2d, smem, grid, nTrapsAll, us(t0, t1), us(t1, t2), us(t2, t3));
   }
   return 0;
 }

@@ -207,5 +207,26 @@ __device__ __forceinline__ uint64_t fieldMask(int bits) {
   return bits >= 64 ? ~0ull : ((1ull << bits) - 1);
 }
 
+constexpr uint32_t kOwnerMulti = 0xFFFFFu; // block+1 field of an ownership word
+
+// Ownership table: per element two words, hi = max(epoch:12 | block+1:20)
+// and lo = max(epoch:12 | (0xFFFFF - (block+1))) over the blocks whose
+// records reached it in this launch — the maximum and (complemented) the
+// minimum block with the launch's epoch on top, so words of earlier launches
+// lose every max (no memset between launches).  An element is MULTI (two
+// blocks reached it: INTER-BLOCK candidates, pass 2) iff both words carry
+// the epoch and min != max.  The joins are RED.MAX (no value returned).
+__device__ __forceinline__ void ownerJoin(uint32_t *owner, uint64_t e, uint32_t epochTag,
+                                          uint32_t blockPlus1) {
+  atomicMax(&owner[2 * e], epochTag | blockPlus1);
+  atomicMax(&owner[2 * e + 1], epochTag | (kOwnerMulti - blockPlus1));
+}
+__device__ __forceinline__ bool ownerIsMulti(const uint32_t *owner, uint64_t e,
+                                             uint32_t epochTag) {
+  const uint2 w = *reinterpret_cast<const uint2 *>(owner + 2 * e);
+  return (w.x >> 20) == (epochTag >> 20) && (w.y >> 20) == (epochTag >> 20) &&
+         (w.x & kOwnerMulti) != kOwnerMulti - (w.y & kOwnerMulti);
+}
+
 } // namespace dev
 } // namespace hgrdgpu

@@ -65,7 +65,7 @@ __global__ void k_inter_scan(const uint32_t *owner, uint32_t multiTag, uint64_t 
                              const uint64_t *confInter, int nLocs,
                              unsigned long long *keyElem) {
   const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= nElems || owner[e] != multiTag)
+  if (e >= nElems || !ownerIsMulti(owner, e, multiTag))
     return;
   const uint32_t *w = tab + e * static_cast<uint64_t>(nSites);
   for (int a = 0; a < nSites; ++a) {
@@ -112,7 +112,7 @@ __global__ void k_inter_scan_single(const uint32_t *owner, uint32_t multiTag, ui
                                     unsigned long long *keyElem) {
   const uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int K = -1;
-  if (e < nElems && owner[e] == multiTag) {
+  if (e < nElems && ownerIsMulti(owner, e, multiTag)) {
     int s = ss.site[0]; // static indices only: the by-value table stays in the parameter bank
 #pragma unroll
     for (int q = 1; q < 8; ++q)
@@ -222,7 +222,7 @@ struct ParSink : ParState {
         atomicMax(&L->interHi[i], b);
       return;
     }
-    if (L->ownerFilter && L->ownerFilter[e] != L->ownerMultiTag)
+    if (L->ownerFilter && !ownerIsMulti(L->ownerFilter, e, L->ownerMultiTag))
       return; // fused pass 2: only elements shared by blocks
     if (L->interTab) { // INTER summary: EMPTY -> one block -> MULTI, no record
       interUpdate(&L->interTab[e * static_cast<uint64_t>(L->nSitesTab) + site],

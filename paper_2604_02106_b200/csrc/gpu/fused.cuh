@@ -31,7 +31,6 @@ namespace hgrdgpu {
 namespace dev {
 
 constexpr int kMaxWritten = 8;
-constexpr uint32_t kOwnerMulti = 0xFFFFFu;
 constexpr int kSmallGroup = 32; // hash slots up to this size, radix grouping above
 constexpr int kMaxIterBlocks = 256; // MiniCU blocks per iteration: the 8-bit blk field of r1
 
@@ -116,6 +115,18 @@ __device__ __forceinline__ int intraRule(uint64_t a1, uint64_t b1) {
   return ((x >> 24) & 255) ? -1 : 2; // same warp: same warp phase only
 }
 
+// After k_fused: whether any element is MULTI (then pass 2 runs); read with
+// the counters, so no extra round trip.
+__global__ void k_owner_any(const uint32_t *owner, uint64_t nElems, uint32_t epochTag,
+                            Counters *ctr) {
+  bool any = false;
+  for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < nElems;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    any |= ownerIsMulti(owner, e, epochTag);
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0)
+    atomicOr(&ctr->flags, static_cast<unsigned>(kFlagShared));
+}
+
 // NT threads x IPT records per thread of shared-memory record capacity.
 template <int NT, int IPT> struct FusedSmem {
   static constexpr int kThreads = NT;
@@ -189,14 +200,12 @@ __device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_
 // pushed onto the chain of its element's hash slot and, at that moment,
 // paired with the records of its element pushed before it (every pair is
 // seen exactly once: by whichever of the two was pushed second).  The
-// block's first record of an element also does the element's ownership
-// exchange (the INTER-BLOCK filter): one exchange of epoch:12 | block+1:20
-// per (element, block); whoever replaces another block's tag (or MULTI)
-// marks the element MULTI.  The last exchange on an element that two blocks
-// touched is always followed by a MULTI store, so the final value is MULTI
-// exactly for the elements of >= 2 blocks (epochs: no memset between
-// launches).  Sites whose parameter is provably block-private (host affine
-// analysis, `own` = false) skip it: no other block can reach their elements.
+// block's first record of an element also joins the element's block range
+// in the ownership table (the INTER-BLOCK filter, ownerJoin): two
+// fire-and-forget max reductions, no round trip to L2 on the thread's
+// critical path.  Sites whose parameter is provably block-private (host
+// affine analysis, `own` = false) skip it: no other block can reach their
+// elements.
 template <class Smem> struct FusedSink : ParState {
   Smem *S;
   uint32_t tli;      // thread index within the iteration
@@ -273,13 +282,8 @@ template <class Smem> struct FusedSink : ParState {
       }
       noteKey(*S, keyMin, real, (la * nLocs + lb) * 3 + kind, e);
     }
-    if (own && first && owner) { // the block's first record of e: one ownership exchange
-      const uint32_t old = atomicExch(&owner[e], epochTag | mine);
-      if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
-        atomicExch(&owner[e], epochTag | kOwnerMulti);
-        flags |= kFlagShared;
-      }
-    }
+    if (own && first && owner) // the block's first record of e: the block joins e's block range
+      ownerJoin(owner, e, epochTag, mine);
   }
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx, bool own) {

@@ -37,11 +37,12 @@ std::string dirOf(const std::string &p) {
   return s == std::string::npos ? "." : p.substr(0, s);
 }
 
-const char *kNames[5] = {"hgrdgpu::dev::k_expand_par<hgrdgpu::dev::JitBody>",
-                         "hgrdgpu::dev::k_fused<256, 4, hgrdgpu::dev::JitBody>",
-                         "hgrdgpu::dev::k_fused<256, 16, hgrdgpu::dev::JitBody>",
-                         "hgrdgpu::dev::k_fused<256, 8, hgrdgpu::dev::JitBody>",
-                         "hgrdgpu::dev::k_expand_seq<hgrdgpu::dev::JitBody>"};
+const char *kNames[kVariants] = {"hgrdgpu::dev::k_expand_par<hgrdgpu::dev::JitBody>",
+                                 "hgrdgpu::dev::k_fused<256, 4, hgrdgpu::dev::JitBody>",
+                                 "hgrdgpu::dev::k_fused<256, 16, hgrdgpu::dev::JitBody>",
+                                 "hgrdgpu::dev::k_fused<256, 8, hgrdgpu::dev::JitBody>",
+                                 "hgrdgpu::dev::k_expand_seq<hgrdgpu::dev::JitBody>",
+                                 "hgrdgpu::dev::k_fused<256, 12, hgrdgpu::dev::JitBody>"};
 
 // Thread identity (reference src/oracle.cpp:443-460) with the launch
 // geometry as literals, so every division is by a constant.

@@ -10,8 +10,16 @@
 namespace hgrdgpu {
 namespace jit {
 
-// k_expand_par, k_fused<256,4> / <256,16> / <256,8>, k_expand_seq
-enum Variant { kExpandPar = 0, kFusedNarrow = 1, kFusedWide = 2, kFusedMid = 3, kExpandSeq = 4 };
+// k_expand_par, k_fused<256,4> / <256,16> / <256,8>, k_expand_seq, k_fused<256,12>
+enum Variant {
+  kExpandPar = 0,
+  kFusedNarrow = 1,
+  kFusedWide = 2,
+  kFusedMid = 3,
+  kExpandSeq = 4,
+  kFused12 = 5,
+  kVariants = 6
+};
 
 // Per kernel parameter: its buffer's element count (0: none, every access
 // traps) and global element base, folded into the generated accesses.

@@ -334,6 +334,13 @@ int hgrd_gpu_check_batch(hgrd_gpu_ctx *ctx, const hgrd_gpu_batch_launch *launche
  * out has launch->n_sites entries. */
 int hgrd_gpu_block_private(const hgrd_gpu_launch *launch, uint8_t *out);
 
+/* Host analysis (no GPU needed): out[s] = c when site s is a load whose
+ * index is always the MiniCU thread's dense id plus the constant c (one
+ * contiguous stream per fused iteration: its values are staged in shared
+ * memory by TMA bulk copies), else INT64_MIN.  out has launch->n_sites
+ * entries. */
+int hgrd_gpu_stream_sites(const hgrd_gpu_launch *launch, int64_t *out);
+
 /* Development check (no GPU needed): lower `kernel`, generate its NVRTC
  * thread body for the given geometry (scalar parameters 0, every site
  * recording) and compile every specialised kernel for sm_100a without

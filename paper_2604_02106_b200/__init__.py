@@ -174,6 +174,7 @@ def load_library() -> ctypes.CDLL:
                                               ctypes.POINTER(P)]
     lib.hgrd_gpu_count_inputs.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
     lib.hgrd_gpu_block_private.argtypes = [P, ctypes.POINTER(ctypes.c_uint8)]
+    lib.hgrd_gpu_stream_sites.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
     lib.hgrd_gpu_shard_check.argtypes = [P, P, P, P]
     lib.hgrd_gpu_shard_inter.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(c_uint32), ctypes.c_uint64,
@@ -290,6 +291,17 @@ class LaunchSpec:
         if rc:
             raise RuntimeError(f"block_private failed ({rc})")
         return [bool(out[i]) for i in range(n)]
+
+    def stream_sites(self):
+        """Per site: c when its index is always the dense thread id + c
+        (a streamed load, affine.cpp streamSites), else None; no GPU needed."""
+        lib = load_library()
+        n = self.launch.n_sites
+        out = (ctypes.c_int64 * max(n, 1))()
+        rc = lib.hgrd_gpu_stream_sites(ctypes.byref(self.launch), out)
+        if rc:
+            raise RuntimeError(f"stream_sites failed ({rc})")
+        return [None if out[i] == -(1 << 63) else int(out[i]) for i in range(n)]
 
     @property
     def n_threads(self) -> int:

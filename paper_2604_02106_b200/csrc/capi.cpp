@@ -113,6 +113,15 @@ std::string escapeJson(const std::string &in) {
 }
 } // namespace
 
+extern "C" int hgrd_gpu_stream_sites(const hgrd_gpu_launch *launch, int64_t *out) {
+  if (!launch || (!out && launch->n_sites))
+    return HGRD_GPU_EINVAL;
+  const std::vector<int64_t> p = hgrdgpu::streamSites(*launch);
+  for (size_t s = 0; s < p.size(); ++s)
+    out[s] = p[s];
+  return HGRD_GPU_OK;
+}
+
 extern "C" int hgrd_gpu_block_private(const hgrd_gpu_launch *launch, uint8_t *out) {
   if (!launch || (!out && launch->n_sites))
     return HGRD_GPU_EINVAL;
@@ -152,7 +161,14 @@ extern "C" int hgrd_gpu_jit_check(const char *source, const char *file_name, con
     L.block[i] = block[i];
   }
   L.warp_size = warp_size;
-  const std::vector<uint8_t> rec(lk.sites.size(), 3);
+  std::vector<uint8_t> rec(lk.sites.size(), 3);
+  { // streamed value-needed loads compile to the staged accessor (loadS)
+    const std::vector<int64_t> off = hgrdgpu::streamSites(L);
+    for (uint32_t pc = 0; pc < L.n_code; ++pc)
+      if (L.code[pc].op == HGRD_OP_LOAD && (L.code[pc].sub & 1) &&
+          off[static_cast<size_t>(L.code[pc].imm)] != hgrdgpu::kNoStream)
+        rec[static_cast<size_t>(L.code[pc].imm)] |= 4;
+  }
   std::vector<hgrdgpu::jit::JitParam> params(handles.size(),
                                              hgrdgpu::jit::JitParam{int64_t(1) << 20, 0});
   L.step_budget = int64_t(1) << 40;

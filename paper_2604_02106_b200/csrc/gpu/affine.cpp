@@ -88,17 +88,22 @@ void merge(std::optional<State> &into, const State &s) {
       (*into)[r] = Form{};
 }
 
-} // namespace
+// Per-site index forms of a loop-free launch (abstract interpretation of the
+// bytecode): false when the code has loops.
+struct SiteForms {
+  Domain D;
+  std::vector<std::optional<Form>> idx;
+  std::vector<uint8_t> seen, unknown;
+};
 
-std::vector<uint8_t> blockPrivateSites(const hgrd_gpu_launch &L) {
-  std::vector<uint8_t> priv(L.n_sites, 0);
+bool siteForms(const hgrd_gpu_launch &L, SiteForms &out) {
   if (!L.code || L.n_code == 0)
-    return priv;
+    return false;
   for (uint32_t pc = 0; pc < L.n_code; ++pc) {
     const auto &I = L.code[pc];
     if ((I.op == HGRD_OP_JMP || I.op == HGRD_OP_JZ) &&
         (I.imm <= static_cast<int64_t>(pc) || I.imm > static_cast<int64_t>(L.n_code)))
-      return priv; // loops (or malformed jumps): no proof
+      return false; // loops (or malformed jumps): no forms
   }
   Domain D;
   for (int d = 0; d < 3; ++d) {
@@ -208,6 +213,46 @@ std::vector<uint8_t> blockPrivateSites(const hgrd_gpu_launch &L) {
       break;
     }
   }
+  out.D = D;
+  out.idx = std::move(siteIdx);
+  out.seen = std::move(siteSeen);
+  out.unknown = std::move(siteUnknown);
+  return true;
+}
+
+} // namespace
+
+std::vector<int64_t> streamSites(const hgrd_gpu_launch &L) {
+  std::vector<int64_t> off(L.n_sites, kNoStream);
+  SiteForms F;
+  if (!siteForms(L, F))
+    return off;
+  // coefficients of the dense thread id (reference :443-460): tid x, y, z,
+  // then bid x, y, z; a builtin with extent 1 is always 0 (any coefficient)
+  const i128 bx = L.block[0], by = L.block[1], tpb = bx * by * L.block[2];
+  const i128 gx = L.grid[0], gy = L.grid[1];
+  const std::array<i128, 6> dense{1, bx, bx * by, tpb, gx * tpb, gx * gy * tpb};
+  for (uint32_t s = 0; s < L.n_sites; ++s) {
+    if (L.sites[s].kind != HGRD_SITE_LOAD || !F.seen[s] || F.unknown[s] || !F.idx[s])
+      continue;
+    const Form &f = *F.idx[s];
+    bool ok = f.k >= kI64Min && f.k <= kI64Max;
+    for (int d = 0; d < 6 && ok; ++d)
+      ok = F.D.extent[d] <= 1 || f.c[d] == dense[d];
+    if (ok)
+      off[s] = static_cast<int64_t>(f.k);
+  }
+  return off;
+}
+
+std::vector<uint8_t> blockPrivateSites(const hgrd_gpu_launch &L) {
+  std::vector<uint8_t> priv(L.n_sites, 0);
+  SiteForms F;
+  if (!siteForms(L, F))
+    return priv;
+  const Domain &D = F.D;
+  const std::vector<std::optional<Form>> &siteIdx = F.idx;
+  const std::vector<uint8_t> &siteSeen = F.seen, &siteUnknown = F.unknown;
 
   // per buffer handle: the reached sites' forms must share the block
   // coefficients, and blocks' element ranges must be separated (mixed radix)

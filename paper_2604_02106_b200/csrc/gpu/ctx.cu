@@ -768,6 +768,8 @@ struct JitGetter {
   bool enabled;
   std::vector<uint8_t> rec; // per site: produces race-check records
   std::vector<hgrdgpu::jit::JitParam> params; // per kernel parameter: size, element base
+  int streamSite = -1;      // a streamed load (staged by k_fused), or -1
+  int64_t streamOff = 0;
   const void *get(hgrdgpu::jit::Variant v) {
     if (!enabled)
       return nullptr;
@@ -782,6 +784,36 @@ struct JitGetter {
     return k;
   }
 };
+
+// The launch's streamed load, if any (JIT bodies only): a value-needed load
+// of a buffer the launch does not write whose index is the dense thread id
+// plus a constant (affine.hpp streamSites) — k_fused stages its values.
+void markStream(const hgrd_gpu_launch &L, const std::vector<ParamDev> &params,
+                JitGetter &jk) {
+  if (!jk.enabled || std::getenv("HGRD_NO_STREAM"))
+    return;
+  std::vector<char> needed(L.n_sites, 0);
+  for (uint32_t pc = 0; pc < L.n_code; ++pc)
+    if (L.code[pc].op == HGRD_OP_LOAD && (L.code[pc].sub & 1))
+      needed[static_cast<size_t>(L.code[pc].imm)] = 1;
+  bool any = false;
+  for (char n : needed)
+    any |= n != 0;
+  if (!any)
+    return;
+  const std::vector<int64_t> off = hgrdgpu::streamSites(L);
+  for (uint32_t s = 0; s < L.n_sites; ++s) {
+    const int32_t p = L.sites[s].param;
+    if (!needed[s] || off[s] == hgrdgpu::kNoStream || p < 0 ||
+        static_cast<size_t>(p) >= params.size() || params[static_cast<size_t>(p)].handle < 0 ||
+        params[static_cast<size_t>(p)].written)
+      continue;
+    jk.streamSite = static_cast<int>(s);
+    jk.streamOff = off[s];
+    jk.rec[s] |= 4;
+    return;
+  }
+}
 
 int launchExpandPar(hgrd_gpu_ctx *c, const LaunchDev &D, unsigned blocks, size_t smem,
                     const void *jitKernel, const char *stage) {
@@ -879,10 +911,20 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
                   : (!loops && perIter <= 2048) ? 8
                   : (!loops && perIter <= 3072) ? 12
                                                 : 16;
-  const size_t smem = ipt == 4    ? fusedSmemBytes<256, 4>(L, P, nKeys)
-                      : ipt == 8  ? fusedSmemBytes<256, 8>(L, P, nKeys)
-                      : ipt == 12 ? fusedSmemBytes<256, 12>(L, P, nKeys)
-                                  : fusedSmemBytes<256, 16>(L, P, nKeys);
+  const hgrdgpu::jit::Variant variant = ipt == 4    ? hgrdgpu::jit::kFusedNarrow
+                                        : ipt == 8  ? hgrdgpu::jit::kFusedMid
+                                        : ipt == 12 ? hgrdgpu::jit::kFused12
+                                                    : hgrdgpu::jit::kFusedWide;
+  const void *jitKernel = jk.get(variant);
+  // the streamed load's staging: two buffers of one iteration's values (+
+  // 16-byte alignment slack), only with the JIT body that reads them
+  const bool streamed = jitKernel && jk.streamSite >= 0;
+  const int stageCap = streamed ? static_cast<int>(bpi * D.tpb) + 4 : 0;
+  const size_t smem = (ipt == 4    ? fusedSmemBytes<256, 4>(L, P, nKeys)
+                       : ipt == 8  ? fusedSmemBytes<256, 8>(L, P, nKeys)
+                       : ipt == 12 ? fusedSmemBytes<256, 12>(L, P, nKeys)
+                                   : fusedSmemBytes<256, 16>(L, P, nKeys)) +
+                      (streamed ? 16 + 16 * static_cast<size_t>(stageCap) : 0);
   if (smem > 227 * 1024)
     return 0;
 
@@ -926,10 +968,17 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   F.wHandle = reinterpret_cast<const int32_t *>(c->blob.p + o.wHandle);
   if (const char *ab = std::getenv("HGRD_FUSED_ABLATE"))
     F.ablate = std::atoi(ab);
-  int rc = ipt == 4    ? launchFused<256, 4>(c, F, smem, jk.get(hgrdgpu::jit::kFusedNarrow))
-           : ipt == 8  ? launchFused<256, 8>(c, F, smem, jk.get(hgrdgpu::jit::kFusedMid))
-           : ipt == 12 ? launchFused<256, 12>(c, F, smem, jk.get(hgrdgpu::jit::kFused12))
-                       : launchFused<256, 16>(c, F, smem, jk.get(hgrdgpu::jit::kFusedWide));
+  if (streamed) {
+    const ParamDev &sp = P.params[static_cast<size_t>(P.sites[jk.streamSite].param)];
+    F.stream = sp.ptr;
+    F.streamOff = jk.streamOff;
+    F.streamSize = sp.size;
+    F.stageCap = stageCap;
+  }
+  int rc = ipt == 4    ? launchFused<256, 4>(c, F, smem, jitKernel)
+           : ipt == 8  ? launchFused<256, 8>(c, F, smem, jitKernel)
+           : ipt == 12 ? launchFused<256, 12>(c, F, smem, jitKernel)
+                       : launchFused<256, 16>(c, F, smem, jitKernel);
   if (rc < 0)
     return rc;
   CK(cudaGetLastError());
@@ -1351,6 +1400,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   }
   for (const auto &s : P.sites) // bit 0: record, bit 1: ownership exchange
     jk.rec.push_back(static_cast<uint8_t>((s.record ? 1 : 0) | (s.own ? 2 : 0)));
+  markStream(L, P.params, jk); // bit 2: streamed load
   if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
     rc = runFused(c, L, D, o, P, R, recInsns, loops, jk);
     if (rc < 0)
@@ -1667,6 +1717,7 @@ JitGetter shardJit(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const ShardSetup &
   }
   for (const auto &s : S.P.sites)
     jk.rec.push_back(static_cast<uint8_t>((s.record ? 1 : 0) | (s.own ? 2 : 0)));
+  markStream(L, S.P.params, jk);
   return jk;
 }
 

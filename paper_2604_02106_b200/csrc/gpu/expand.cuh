@@ -277,6 +277,13 @@ struct ParSink : ParState {
     ++seq;
     return need ? __ldg(params[param].ptr + idx) : 0;
   }
+  // S variant: a streamed load (affine.hpp streamSites; staged in shared
+  // memory by k_fused only — here a plain value-needed load)
+  template <class I>
+  __device__ __forceinline__ int64_t loadS(int site, int param, bool rec, bool own, I idx,
+                                           int64_t size, uint64_t base) {
+    return loadC(site, param, rec, own, idx, true, size, base);
+  }
   template <class I>
   __device__ __forceinline__ void storeC(int site, int param, bool rec, bool own, I idx, int64_t,
                                          int64_t size, uint64_t base) {
@@ -565,6 +572,11 @@ struct SeqSink {
     if (outOfRange(idx, size))
       return load(site, static_cast<int64_t>(idx), need);
     return *fastAccess(site, param, rec, static_cast<int64_t>(idx), base);
+  }
+  template <class I>
+  __device__ __forceinline__ int64_t loadS(int site, int param, bool rec, bool own, I idx,
+                                           int64_t size, uint64_t base) {
+    return loadC(site, param, rec, own, idx, true, size, base);
   }
   template <class I>
   __device__ __forceinline__ void storeC(int site, int param, bool rec, bool, I idx, int64_t v,

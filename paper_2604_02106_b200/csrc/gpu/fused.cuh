@@ -67,7 +67,67 @@ struct FusedArgs {
   const int32_t *wHandle;
   int ablate; // profiling knob (HGRD_FUSED_ABLATE): 1 skip the post-expansion phases,
               // 4 skip ownership exchanges, 8 skip expansion
+  // streamed load (affine.hpp streamSites; JIT bodies' loadS): index = dense
+  // thread + streamOff into `stream` (streamSize elements); each iteration's
+  // values arrive in shared memory by a TMA bulk copy issued one iteration
+  // ahead (double-buffered, mbarrier-completed); nullptr: no stream
+  const int64_t *stream;
+  int64_t streamOff, streamSize;
+  int stageCap; // elements per staging buffer
 };
+
+// TMA bulk copies (cp.async.bulk -> UBLKCP) completing on an mbarrier
+__device__ __forceinline__ uint32_t smemAddr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbarInit(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smemAddr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbarArriveTx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemAddr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbarArrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smemAddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbarWait(uint64_t *bar, unsigned parity) {
+  asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+               "@!P1 bra WAIT_%=;\n\t}" ::"r"(smemAddr(bar)),
+               "r"(parity)
+               : "memory");
+}
+__device__ __forceinline__ void bulkToShared(void *dst, const void *src, unsigned bytes,
+                                             uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+               "%2, [%3];" ::"r"(smemAddr(dst)),
+               "l"(src), "r"(bytes), "r"(smemAddr(bar))
+               : "memory");
+}
+
+// Stage iteration `it`'s streamed values: elements [first + off, first +
+// off + n) clamped to the buffer, widened to 16-byte alignment (buffers are
+// 256-byte aligned and padded); one elected thread.  Returns the first
+// staged element index.
+__device__ __forceinline__ int64_t stageIssue(const FusedArgs &F, int64_t it, int64_t *buf,
+                                              uint64_t *bar) {
+  const int64_t first = (F.blockBase + it * F.bpi) * F.L.tpb;
+  const int64_t n = (min(static_cast<int64_t>(F.bpi), F.blockEnd - (F.blockBase + it * F.bpi))) *
+                    F.L.tpb;
+  const int64_t lo = max(first + F.streamOff, static_cast<int64_t>(0));
+  const int64_t hi = min(first + F.streamOff + n, F.streamSize);
+  if (hi <= lo) {
+    mbarArrive(bar); // nothing in bounds: complete the phase without data
+    return 0;
+  }
+  const int64_t a = (lo * 8) & ~int64_t(15), b = (hi * 8 + 15) & ~int64_t(15);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); // generic reads before TMA writes
+  mbarArriveTx(bar, static_cast<unsigned>(b - a));
+  bulkToShared(buf, reinterpret_cast<const char *>(F.stream) + a, static_cast<unsigned>(b - a), bar);
+  return a / 8;
+}
 
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
@@ -343,6 +403,27 @@ template <class Smem> struct FusedSink : ParState {
     ++seq;
     return need ? __ldg(params[param].ptr + idx) : 0;
   }
+  // S variant: a streamed load (affine.hpp streamSites): idx is the MiniCU
+  // thread's dense id plus a constant, so the iteration's values were staged
+  // in shared memory by a bulk copy (k_fused) — no global load latency on the
+  // thread's critical path
+  const int64_t *stage = nullptr; // staged values, element stageBase first
+  int64_t stageBase = 0;
+  template <class I>
+  __device__ __forceinline__ int64_t loadS(int site, int param, bool rec, bool own, I idx,
+                                           int64_t size, uint64_t base) {
+    if (!stage)
+      return loadC(site, param, rec, own, idx, true, size, base);
+    if (outOfRange(idx, size)) {
+      ++traps;
+      return 0;
+    }
+    ++inst;
+    if (rec)
+      recordE(site, elementAt(base, idx), own);
+    ++seq;
+    return stage[static_cast<int64_t>(idx) - stageBase];
+  }
   template <class I>
   __device__ __forceinline__ void storeC(int site, int param, bool rec, bool own, I idx, int64_t,
                                          int64_t size, uint64_t base) {
@@ -418,7 +499,12 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   ParamDev *sParams = reinterpret_cast<ParamDev *>(sSites + F.L.nSites);
   uint64_t *sConf = reinterpret_cast<uint64_t *>(sParams + F.L.nParams);
   uint64_t *sConfX = sConf + F.L.nSites;
+  int64_t *sStage = reinterpret_cast<int64_t *>(
+      (reinterpret_cast<uintptr_t>(sConfX + F.L.nSites) + 15) & ~uintptr_t(15));
   // dynamic shared memory layout mirrored by fusedSmemBytes() in ctx.cu
+  __shared__ __align__(8) uint64_t sBar[2];
+  __shared__ int64_t sStageBase[2];
+  const bool streamed = F.stream != nullptr;
   const LaunchDev &L = F.L;
   const int tid = threadIdx.x;
   for (int i = tid; i < L.nCode; i += kFusedThreads)
@@ -446,11 +532,26 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   unsigned myFlags = 0;
   bool wroteCand = false; // this thread stored a candidate (released before the done count)
   int64_t regs[kMaxRegs];
+  if (streamed && tid == 0) {
+    mbarInit(&sBar[0], 1);
+    mbarInit(&sBar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (static_cast<int64_t>(blockIdx.x) < F.nIters)
+      sStageBase[0] = stageIssue(F, blockIdx.x, sStage, &sBar[0]);
+  }
 
-  for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x) {
+  int64_t k = 0; // this CTA's iteration count (staging buffer k & 1)
+  for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x, ++k) {
     const int64_t firstBlock = F.blockBase + it * F.bpi;
     const int64_t nb = min(static_cast<int64_t>(F.bpi), F.blockEnd - firstBlock);
     __syncthreads();
+    const int sb = static_cast<int>(k & 1);
+    if (streamed) { // prefetch the next iteration's values, then wait for this one's
+      if (tid == 0 && it + gridDim.x < F.nIters)
+        sStageBase[sb ^ 1] =
+            stageIssue(F, it + gridDim.x, sStage + (sb ^ 1) * F.stageCap, &sBar[sb ^ 1]);
+      mbarWait(&sBar[sb], static_cast<unsigned>((k >> 1) & 1));
+    }
     if (tid == 0) {
       S.count = fixedR ? static_cast<unsigned>(nb * L.tpb) * fixedR : 0;
       S.maxBp = 0;
@@ -484,6 +585,10 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.owner = (F.ablate & 4) ? nullptr : F.owner;
         s.epochTag = F.epoch << 20;
         s.mine = static_cast<uint32_t>(firstBlock + s.myBlk + 1);
+        if (streamed) {
+          s.stage = sStage + sb * F.stageCap;
+          s.stageBase = sStageBase[sb];
+        }
         Builtins bi;
         Body::identity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
         Body::run(L, sCode, bi, s, regs);

@@ -341,8 +341,13 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
       break;
     }
     case HGRD_OP_LOAD:
-      o << "r" << I.a << " = s.loadC(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm) << ", "
-        << ((I.sub & 1) ? "true" : "false") << buf(I.imm) << ");";
+      if ((I.sub & 1) && static_cast<size_t>(I.imm) < rec.size() &&
+          (rec[static_cast<size_t>(I.imm)] & 4)) // streamed (staged) value-needed load
+        o << "r" << I.a << " = s.loadS(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm)
+          << buf(I.imm) << ");";
+      else
+        o << "r" << I.a << " = s.loadC(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm) << ", "
+          << ((I.sub & 1) ? "true" : "false") << buf(I.imm) << ");";
       break;
     case HGRD_OP_STORE:
       o << "s.storeC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm) << ", r" << I.b

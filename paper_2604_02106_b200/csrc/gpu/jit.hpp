@@ -35,7 +35,8 @@ void destroy(Cache *c);
 // on first use, cached).  Returns nullptr (and err) when NVRTC is
 // unavailable or the compile fails; callers then use the interpreter.
 // `rec[s]`: bit 0: site s produces race-check records (written buffer);
-// bit 1: its buffer may be reached from two blocks (ownership exchange).
+// bit 1: its buffer may be reached from two blocks (ownership exchange);
+// bit 2: a streamed load (affine.hpp streamSites; k_fused stages its values).
 const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                 const std::vector<JitParam> &params, Variant v, std::string &err);
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,

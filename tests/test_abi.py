@@ -1,5 +1,5 @@
 """CPU-side checks of the product library: it loads, exports every function
-include/hgrd_gpu.h declares, fails loudly without a device (no CPU
+include/*.h declares, fails loudly without a device (no CPU
 fallback), and its lowering honours the reference's evaluation order."""
 import ctypes
 import os
@@ -14,15 +14,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_functions():
-    text = open(os.path.join(ROOT, "include", "hgrd_gpu.h")).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(hgrd_gpu_[a-z_]+)\s*\(", text)))
+    names = set()
+    inc = os.path.join(ROOT, "include")
+    for h in sorted(os.listdir(inc)):
+        if h.endswith(".h"):
+            text = re.sub(r"/\*.*?\*/", "", open(os.path.join(inc, h)).read(), flags=re.S)
+            names |= set(re.findall(r"\b(hgrd_gpu_[a-z_]+)\s*\(", text))
+    return sorted(names)
 
 
 def test_library_exports_every_declared_symbol():
     lib = hg.load_library()
     names = declared_functions()
-    assert len(names) >= 16
+    assert len(names) >= 30
     for n in names:
         assert hasattr(lib, n), n
 
@@ -120,3 +124,34 @@ def test_block_private_analysis():
            "    A[blockIdx.x * 512 + threadIdx.x + i] = 1;\n  }\n}\n"
            "void main() { int *A; cudaMalloc(&A, 8192);\n  k<<<4,256>>>(A); }\n")
     assert not _block_private(src, "k", (4, 1, 1), (256, 1, 1), {"A": 0})[("A", 1)]
+
+
+def _stream(src, kernel, grid, block, handles, scalars=None):
+    low = hg.lower(src, kernel)
+    spec = hg.LaunchSpec(low, grid, block, 32, handles=handles, scalars=scalars)
+    return {(s["array"], s["kind"]): p for s, p in zip(low["sites"], spec.stream_sites())}
+
+
+def test_stream_sites_analysis():
+    """Streamed loads (affine.cpp streamSites): an index that is always the
+    dense thread id (blockLin * tpb + threadLin, reference oracle.cpp:443-460)
+    plus a constant, whose values k_fused stages by TMA bulk copies."""
+    hist = programs.histogram(1 << 12, 64)
+    got = _stream(hist, "h", (16, 1, 1), (256, 1, 1), {"data": 0, "hist": 1})
+    assert got[("data", 0)] == 0 and got[("hist", 1)] is None
+    perm = programs.permutation_scatter(1 << 17, host_init=False)
+    assert _stream(perm, "h", (512, 1, 1), (256, 1, 1), {"data": 0, "hist": 1})[("data", 0)] == 0
+    st = programs.stencil(1 << 12)  # in_[t]: the stream; tile loads are not
+    got = _stream(st, "st", (16, 1, 1), (256, 1, 1), {"in_": 0, "tile": 1, "out_": 2})
+    assert got[("in_", 0)] == 0 and got[("tile", 0)] is None
+    # 2-D: t = (by * gx + bx) * tpb + ty * bdx + tx, offset 5
+    src = ("__global__ void k(int *A, int *B) {\n"
+           "  int t = (blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x * blockDim.y)"
+           " + threadIdx.y * blockDim.x + threadIdx.x;\n"
+           "  B[A[t + 5]] = 1;\n}\n"
+           "void main() { int *A; int *B; cudaMalloc(&A, 8192); cudaMalloc(&B, 64);\n"
+           "  k<<<(4,2,1),(8,4,1)>>>(A, B); }\n")
+    assert _stream(src, "k", (4, 2, 1), (8, 4, 1), {"A": 0, "B": 1})[("A", 0)] == 5
+    # transposed thread order: not the dense id
+    src2 = src.replace("threadIdx.y * blockDim.x + threadIdx.x", "threadIdx.x * blockDim.y + threadIdx.y")
+    assert _stream(src2, "k", (4, 2, 1), (8, 4, 1), {"A": 0, "B": 1})[("A", 0)] is None

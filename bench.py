@@ -543,6 +543,8 @@ def run_gpu_arm(args):
     e2e_value = total_inst / e2e_s
 
     peak, peak_kind = peaks()
+    if not stage_ms:  # (no per-stage profile: the whole check as one stage)
+        stage_ms, stage_n = {"check": dev_ms}, {"check": args.steps * len(launches)}
     dom = max(stage_ms, key=stage_ms.get)
     dom_avg_ms = stage_ms[dom] / stage_n[dom]
     # algorithmic bytes per launch of the dominant kernel: B_alg x instances
@@ -734,7 +736,7 @@ def run_sweep_arm(args):
     ctx = hg.GpuContext(local)
 
     def step():
-        if not use_dist:
+        if ws == 1:  # (world 1: the merged sweep results directly)
             return ctx.enumerate_verdict_many(jobs)
         mine = ctx.enumerate_verdict_many(jobs, rank, ws)
         parts = [None] * ws

@@ -26,6 +26,9 @@
 #include <numeric>
 #include <string>
 #include <vector>
+#include <thread>
+#include <atomic>
+#include <unordered_map>
 
 using namespace hgrdgpu::dev;
 
@@ -928,9 +931,11 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   if (smem > 227 * 1024)
     return 0;
 
-  // ownership table (two epoch-tagged words per element, no memset between
-  // launches; device.cuh ownerJoin)
-  const size_t ownerN = 2 * std::max<uint64_t>(P.totalW, 1);
+  // ownership table (epoch-tagged, no memset between launches, device.cuh):
+  // reduction layout (two words per element) when it fits L2 comfortably,
+  // else the exchange layout (one word)
+  const bool ownerRed = 8 * P.totalW <= (uint64_t(32) << 20);
+  const size_t ownerN = (ownerRed ? 2 : 1) * std::max<uint64_t>(P.totalW, 1);
   const bool fresh = c->owner.cap < ownerN;
   NEED(c->owner, ownerN);
   if (fresh || c->epoch >= 4094) {
@@ -957,6 +962,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   for (const SiteDev &sd : P.sites)
     anyOwn |= sd.record && sd.own;
   F.owner = (shard || F.interOnChip || !anyOwn) ? nullptr : c->owner.p;
+  F.ownerRed = ownerRed;
   F.epoch = c->epoch;
   F.keyElem = c->curKeyElem;
   F.cand = c->cand.p;
@@ -983,7 +989,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     return rc;
   CK(cudaGetLastError());
   ++c->kernelLaunches;
-  if (F.owner) { // any element reached from two blocks? (read with the counters)
+  if (F.owner && ownerRed) { // any element reached from two blocks? (read with the counters)
     StageTimer t(c, "k_owner_any");
     k_owner_any<<<static_cast<unsigned>(std::min<uint64_t>((P.totalW + 255) / 256,
                                                            uint64_t(c->nSM) * 8)),
@@ -1018,7 +1024,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   LaunchDev D2 = D;
   D2.ctr = c->ctr2.p;
   D2.ownerFilter = c->owner.p;
-  D2.ownerMultiTag = c->epoch << 20; // (the launch's epoch tag: ownerIsMulti)
+  D2.ownerMultiTag = (c->epoch << 20) | (ownerRed ? 0u : kOwnerMulti); // (ownerIsMulti)
   const size_t sm2 = sizeof(hgrd_gpu_insn) * L.n_code + sizeof(SiteDev) * P.sites.size() +
                      sizeof(ParamDev) * P.params.size();
   const unsigned grid2 = static_cast<unsigned>(std::min<uint64_t>(
@@ -1317,6 +1323,23 @@ int prepareLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, Plan &P, BlobOffset
   D.threadBase = 0;
   D.threadEnd = D.nThreads;
   return 0;
+}
+
+// Per-stage device times of the check just finished (profiling on; the
+// stream is synchronised), as the JSON hgrd_gpu_last_profile returns.
+void finishProfile(hgrd_gpu_ctx *c) {
+  if (!c->profiling)
+    return;
+  std::string j = "[";
+  for (size_t i = 0; i < c->stages.size(); ++i) {
+    float sm = 0;
+    cudaEventElapsedTime(&sm, c->stages[i].a, c->stages[i].b);
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "%s{\"name\":\"%s\",\"ms\":%.6f}", i ? "," : "",
+                  c->stages[i].name, sm);
+    j += buf;
+  }
+  c->profileJson = j + "]";
 }
 
 int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
@@ -1631,18 +1654,7 @@ finish:
                        .count());
     std::fprintf(stderr, " (us)\n");
   }
-  if (c->profiling) {
-    std::string j = "[";
-    for (size_t i = 0; i < c->stages.size(); ++i) {
-      float sm = 0;
-      cudaEventElapsedTime(&sm, c->stages[i].a, c->stages[i].b);
-      char buf[128];
-      std::snprintf(buf, sizeof buf, "%s{\"name\":\"%s\",\"ms\":%.6f}", i ? "," : "",
-                    c->stages[i].name, sm);
-      j += buf;
-    }
-    c->profileJson = j + "]";
-  }
+  finishProfile(c);
   return 0;
 }
 
@@ -1802,6 +1814,7 @@ int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
     CK(cudaStreamSynchronize(c->st));
   }
   R->device_ms = ms;
+  finishProfile(c);
   return 0;
 }
 
@@ -1983,6 +1996,29 @@ int shardDetect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const uint64_t *keys,
 // descriptor, one k_batch launch, one D2H of every launch's counters and
 // races.
 
+// fn(i) for i < n on up to the hardware's threads (chunks of 64).
+template <class F> void parallelFor(size_t n, F &&fn) {
+  const size_t hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const size_t nt = std::min(hw, (n + 255) / 256);
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; ++i)
+      fn(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t b; (b = next.fetch_add(64)) < n;)
+      for (size_t i = b; i < std::min(n, b + 64); ++i)
+        fn(i);
+  };
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < nt; ++t)
+    pool.emplace_back(work);
+  work();
+  for (auto &t : pool)
+    t.join();
+}
+
 struct BatchPlan {
   bool ok = false;
   uint32_t R = 0;
@@ -2113,67 +2149,125 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     resetResult(&R[i]);
     R[i].mode = HGRD_RESULT_UNCHECKED;
   }
-  // host blob: [BatchLaunch x m] | per launch: code (shared), sites, params,
-  // regs, masks, wBase | buffer contents | next counter; device pointers
-  // are fixed up once the blob's device address is known
-  std::vector<unsigned char> blob;
-  std::vector<uint32_t> idx; // batch entry -> launch
+  // 1. per-launch plans, on host threads
   std::vector<BatchPlan> plans(n);
-  for (uint32_t i = 0; i < n; ++i) {
-    planBatchLaunch(BL[i], plans[i]);
+  parallelFor(n, [&](size_t i) { planBatchLaunch(BL[i], plans[i]); });
+  std::vector<uint32_t> idx; // batch entry -> launch
+  for (uint32_t i = 0; i < n; ++i)
     if (plans[i].ok)
       idx.push_back(i);
-  }
   const uint32_t m = static_cast<uint32_t>(idx.size());
   if (m == 0)
     return 0;
-  blob.resize(align16(sizeof(BatchLaunch) * m));
-  std::vector<BatchLaunch> bl(m);
+  // 2. layout of the blob: [BatchLaunch x m] | per launch: code (shared by
+  //    launches of one kernel), sites, params, regs, masks, wBase, the
+  //    contents of value-needed buffers | work counter, trap cursor
   struct Fix {
-    size_t code, sites, params, regs, cInter, cIntra, wBase;
+    size_t code, sites, params, regs, cInter, cIntra, wBase, data;
+    bool codeOwner;
   };
   std::vector<Fix> fix(m);
-  std::map<const hgrd_gpu_insn *, size_t> codeAt;
-  std::vector<std::vector<size_t>> dataAt(m); // per launch, per param: blob offset of contents
+  std::unordered_map<const hgrd_gpu_insn *, size_t> codeAt;
+  size_t off = align16(sizeof(BatchLaunch) * m);
+  auto put = [&](size_t bytes) {
+    const size_t at = off;
+    off = align16(off + bytes);
+    return at;
+  };
   int maxKeys = 3, maxCode = 1, maxSites = 1, maxParams = 1, maxW = 1;
+  std::vector<uint32_t> raceOffs(m);
   uint32_t raceOff = 0;
   for (uint32_t k = 0; k < m; ++k) {
     const hgrd_gpu_batch_launch &B = BL[idx[k]];
     const hgrd_gpu_launch &L = B.launch;
-    BatchPlan &P = plans[idx[k]];
+    const BatchPlan &P = plans[idx[k]];
+    Fix &f = fix[k];
     auto ci = codeAt.find(L.code);
-    if (ci == codeAt.end())
-      ci = codeAt.emplace(L.code, batchPut(blob, L.code, L.n_code)).first;
-    fix[k].code = ci->second;
-    fix[k].sites = batchPut(blob, P.sites.data(), P.sites.size());
-    std::vector<int64_t> regs(std::max<uint32_t>(L.n_regs, 1), 0);
+    f.codeOwner = ci == codeAt.end();
+    if (f.codeOwner)
+      ci = codeAt.emplace(L.code, put(sizeof(hgrd_gpu_insn) * L.n_code)).first;
+    f.code = ci->second;
+    f.sites = put(sizeof(SiteDev) * P.sites.size());
+    f.params = put(sizeof(ParamDev) * P.params.size());
+    f.regs = put(8 * std::max<size_t>(L.n_regs, 1));
+    f.cInter = put(8 * P.confInter.size());
+    f.cIntra = put(8 * P.confIntra.size());
+    f.wBase = put(8 * P.wBase.size());
+    f.data = off;
+    for (uint32_t h = 0; h < B.n_buffers; ++h)
+      if (P.needData[h] && B.buffer_elems[h] > 0)
+        put(8 * static_cast<size_t>(B.buffer_elems[h]));
+    const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
+    raceOffs[k] = raceOff;
+    raceOff += static_cast<uint32_t>(3 * nLocs * nLocs);
+    maxKeys = std::max(maxKeys, 3 * nLocs * nLocs);
+    maxCode = std::max(maxCode, static_cast<int>(L.n_code));
+    maxSites = std::max(maxSites, std::max(static_cast<int>(L.n_sites), 1));
+    maxParams = std::max(maxParams, std::max(static_cast<int>(L.n_params), 1));
+    maxW = std::max(maxW, static_cast<int>(P.wBase.size()));
+  }
+  const size_t nextAt = put(16); // work counter, trap cursor
+  const size_t h2d = off;
+  const size_t outAt = align16(h2d);
+  const size_t racesAt = align16(outAt + sizeof(BatchOut) * m);
+  const size_t total = racesAt + sizeof(hgrd_gpu_race) * std::max<uint32_t>(raceOff, 1);
+  // trap area: every trap of the batch's launches (12 B each), read back only
+  // when the trap cursor is non-zero
+  const unsigned trapCap = static_cast<unsigned>(std::min<uint64_t>(uint64_t(m) * 256, 1u << 22));
+  const size_t trapKeyAt = align16(total);
+  const size_t trapSiteAt = align16(trapKeyAt + 8 * static_cast<size_t>(trapCap));
+  const size_t devTotal = trapSiteAt + 4 * static_cast<size_t>(trapCap);
+  NEED(c->batchBlob, devTotal);
+  unsigned char *dev = c->batchBlob.p;
+  if (c->hBatchCap < std::max(h2d, total - outAt)) {
+    if (c->hBatch)
+      CK(cudaFreeHost(c->hBatch));
+    c->hBatch = nullptr;
+    c->hBatchCap = std::max(std::max(h2d, total - outAt), size_t(1) << 20);
+    CK(cudaMallocHost(&c->hBatch, c->hBatchCap));
+  }
+  // 3. fill the pinned staging buffer (device addresses fixed up), on host threads
+  unsigned char *h = c->hBatch;
+  std::memset(h + nextAt, 0, 16);
+  parallelFor(m, [&](size_t k) {
+    const hgrd_gpu_batch_launch &B = BL[idx[k]];
+    const hgrd_gpu_launch &L = B.launch;
+    BatchPlan &P = plans[idx[k]];
+    const Fix &f = fix[k];
+    if (f.codeOwner)
+      std::memcpy(h + f.code, L.code, sizeof(hgrd_gpu_insn) * L.n_code);
+    std::memcpy(h + f.sites, P.sites.data(), sizeof(SiteDev) * P.sites.size());
+    int64_t *regs = reinterpret_cast<int64_t *>(h + f.regs);
+    regs[0] = 0;
     if (L.n_regs)
-      std::memcpy(regs.data(), L.reg_init, 8 * L.n_regs);
-    fix[k].regs = batchPut(blob, regs.data(), regs.size());
-    fix[k].cInter = batchPut(blob, P.confInter.data(), P.confInter.size());
-    fix[k].cIntra = batchPut(blob, P.confIntra.data(), P.confIntra.size());
-    fix[k].wBase = batchPut(blob, P.wBase.data(), P.wBase.size());
+      std::memcpy(regs, L.reg_init, 8 * L.n_regs);
+    std::memcpy(h + f.cInter, P.confInter.data(), 8 * P.confInter.size());
+    std::memcpy(h + f.cIntra, P.confIntra.data(), 8 * P.confIntra.size());
+    std::memcpy(h + f.wBase, P.wBase.data(), 8 * P.wBase.size());
     // value-needed buffers: their launch-entry contents (zeros when absent)
-    std::vector<size_t> bufAt(B.n_buffers, SIZE_MAX);
-    for (uint32_t h = 0; h < B.n_buffers; ++h) {
-      if (!P.needData[h] || B.buffer_elems[h] <= 0)
+    size_t at = f.data;
+    for (uint32_t b = 0; b < B.n_buffers; ++b) {
+      if (!P.needData[b] || B.buffer_elems[b] <= 0)
         continue;
-      const size_t at = align16(blob.size());
-      const size_t bytes = 8 * static_cast<size_t>(B.buffer_elems[h]);
-      blob.resize(at + bytes);
-      if (B.buffer_data && B.buffer_data[h])
-        std::memcpy(blob.data() + at, B.buffer_data[h], bytes);
+      const size_t bytes = 8 * static_cast<size_t>(B.buffer_elems[b]);
+      if (B.buffer_data && B.buffer_data[b])
+        std::memcpy(h + at, B.buffer_data[b], bytes);
       else
-        std::memset(blob.data() + at, 0, bytes);
-      bufAt[h] = at;
+        std::memset(h + at, 0, bytes);
+      for (uint32_t p = 0; p < L.n_params; ++p)
+        if (P.params[p].handle == static_cast<int32_t>(b))
+          P.params[p].ptr = reinterpret_cast<int64_t *>(dev + at);
+      at = align16(at + bytes);
     }
-    dataAt[k].assign(P.params.size(), SIZE_MAX);
-    for (uint32_t p = 0; p < L.n_params; ++p)
-      if (P.params[p].handle >= 0)
-        dataAt[k][p] = bufAt[static_cast<size_t>(P.params[p].handle)];
-    fix[k].params = batchPut(blob, P.params.data(), P.params.size());
-    LaunchDev &D = bl[k].L;
-    D = LaunchDev{};
+    std::memcpy(h + f.params, P.params.data(), sizeof(ParamDev) * P.params.size());
+    BatchLaunch bl{};
+    LaunchDev &D = bl.L;
+    D.code = reinterpret_cast<const hgrd_gpu_insn *>(dev + f.code);
+    D.sites = reinterpret_cast<const SiteDev *>(dev + f.sites);
+    D.params = reinterpret_cast<const ParamDev *>(dev + f.params);
+    D.regInit = reinterpret_cast<const int64_t *>(dev + f.regs);
+    D.confInter = reinterpret_cast<const uint64_t *>(dev + f.cInter);
+    D.confIntra = reinterpret_cast<const uint64_t *>(dev + f.cIntra);
     D.nCode = static_cast<int>(L.n_code);
     D.nRegs = static_cast<int>(L.n_regs);
     D.nSites = static_cast<int>(L.n_sites);
@@ -2196,58 +2290,15 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     D.dGxGy = FastDiv::make(static_cast<uint32_t>(L.grid[0] * L.grid[1]));
     D.dWs = FastDiv::make(static_cast<uint32_t>(L.warp_size));
     D.threadEnd = D.nThreads;
-    const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
-    bl[k].nW = static_cast<int32_t>(P.wBase.size());
-    bl[k].nLocs = nLocs;
-    bl[k].R = P.R;
-    bl[k].raceOff = raceOff;
-    raceOff += static_cast<uint32_t>(3 * nLocs * nLocs);
-    maxKeys = std::max(maxKeys, 3 * nLocs * nLocs);
-    maxCode = std::max(maxCode, D.nCode);
-    maxSites = std::max(maxSites, std::max(D.nSites, 1));
-    maxParams = std::max(maxParams, std::max(D.nParams, 1));
-    maxW = std::max(maxW, bl[k].nW);
-  }
-  const size_t nextAt = batchPut(blob, &raceOff, 0);
-  blob.resize(nextAt + 16); // work counter, trap cursor
-  std::memset(blob.data() + nextAt, 0, 16);
-  const size_t h2d = blob.size();
-  const size_t outAt = align16(h2d);
-  const size_t racesAt = align16(outAt + sizeof(BatchOut) * m);
-  const size_t total = racesAt + sizeof(hgrd_gpu_race) * std::max<uint32_t>(raceOff, 1);
-  // trap area: every trap of the batch's launches (12 B each), read back only
-  // when the trap cursor is non-zero
-  const unsigned trapCap = static_cast<unsigned>(std::min<uint64_t>(uint64_t(m) * 256, 1u << 22));
-  const size_t trapKeyAt = align16(total);
-  const size_t trapSiteAt = align16(trapKeyAt + 8 * static_cast<size_t>(trapCap));
-  const size_t devTotal = trapSiteAt + 4 * static_cast<size_t>(trapCap);
-  NEED(c->batchBlob, devTotal);
-  unsigned char *dev = c->batchBlob.p;
-  for (uint32_t k = 0; k < m; ++k) {
-    LaunchDev &D = bl[k].L;
-    D.code = reinterpret_cast<const hgrd_gpu_insn *>(dev + fix[k].code);
-    D.sites = reinterpret_cast<const SiteDev *>(dev + fix[k].sites);
-    D.params = reinterpret_cast<const ParamDev *>(dev + fix[k].params);
-    D.regInit = reinterpret_cast<const int64_t *>(dev + fix[k].regs);
-    D.confInter = reinterpret_cast<const uint64_t *>(dev + fix[k].cInter);
-    D.confIntra = reinterpret_cast<const uint64_t *>(dev + fix[k].cIntra);
-    bl[k].wBase = reinterpret_cast<const uint64_t *>(dev + fix[k].wBase);
-    auto *pd = reinterpret_cast<ParamDev *>(blob.data() + fix[k].params);
-    for (size_t p = 0; p < dataAt[k].size(); ++p)
-      pd[p].ptr = dataAt[k][p] == SIZE_MAX ? nullptr
-                                           : reinterpret_cast<int64_t *>(dev + dataAt[k][p]);
-  }
-  std::memcpy(blob.data(), bl.data(), sizeof(BatchLaunch) * m);
-  if (c->hBatchCap < std::max(h2d, total - outAt)) {
-    if (c->hBatch)
-      CK(cudaFreeHost(c->hBatch));
-    c->hBatch = nullptr;
-    c->hBatchCap = std::max(std::max(h2d, total - outAt), size_t(1) << 20);
-    CK(cudaMallocHost(&c->hBatch, c->hBatchCap));
-  }
-  std::memcpy(c->hBatch, blob.data(), h2d);
+    bl.wBase = reinterpret_cast<const uint64_t *>(dev + f.wBase);
+    bl.nW = static_cast<int32_t>(P.wBase.size());
+    bl.nLocs = static_cast<int32_t>(std::max<uint32_t>(L.n_locs, 1));
+    bl.R = P.R;
+    bl.raceOff = raceOffs[k];
+    std::memcpy(h + sizeof(BatchLaunch) * k, &bl, sizeof(BatchLaunch));
+  });
   const auto t1 = std::chrono::steady_clock::now();
-  CK(cudaMemcpyAsync(dev, c->hBatch, h2d, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(dev, h, h2d, cudaMemcpyHostToDevice, c->st));
   c->h2dBytes += h2d;
 
   const int keysPad = (maxKeys + 3) & ~3;
@@ -2342,7 +2393,7 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     }
     const BatchPlan &P = plans[idx[k]];
     for (uint32_t q = 0; q < o.nRaces; ++q) {
-      hgrd_gpu_race x = races[bl[k].raceOff + q];
+      hgrd_gpu_race x = races[raceOffs[k] + q];
       x.handle = P.wHandle[static_cast<size_t>(x.handle)];
       r.races[q] = x;
     }

@@ -209,22 +209,31 @@ __device__ __forceinline__ uint64_t fieldMask(int bits) {
 
 constexpr uint32_t kOwnerMulti = 0xFFFFFu; // block+1 field of an ownership word
 
-// Ownership table: per element two words, hi = max(epoch:12 | block+1:20)
-// and lo = max(epoch:12 | (0xFFFFF - (block+1))) over the blocks whose
-// records reached it in this launch — the maximum and (complemented) the
-// minimum block with the launch's epoch on top, so words of earlier launches
-// lose every max (no memset between launches).  An element is MULTI (two
-// blocks reached it: INTER-BLOCK candidates, pass 2) iff both words carry
-// the epoch and min != max.  The joins are RED.MAX (no value returned).
+// Ownership table (the fused path's INTER-BLOCK filter), two layouts:
+// * exchange (one word per element): the block's first record of an
+//   element swaps in epoch:12 | block+1:20; whoever replaces another
+//   block's tag (or MULTI) stores MULTI (epoch | 0xFFFFF) — the final value
+//   is MULTI exactly for elements reached from two blocks;
+// * reduction (two words per element): hi = max(epoch | block+1) and
+//   lo = max(epoch | (0xFFFFF - (block+1))) — max and (complemented) min
+//   block, fire-and-forget RED.MAX with no round trip on the thread's
+//   critical path; MULTI iff both words carry the epoch and min != max.
+// Tables small enough for L2 use reductions; large ones the exchange (two
+// reductions per element on a table far larger than L2 cost more DRAM
+// round trips than they save).  Epoch tags: no memset between launches.
+// The filter tag tells the layouts apart: epoch << 20 | 0xFFFFF (exchange:
+// the MULTI value) or epoch << 20 (reduction).
 __device__ __forceinline__ void ownerJoin(uint32_t *owner, uint64_t e, uint32_t epochTag,
                                           uint32_t blockPlus1) {
   atomicMax(&owner[2 * e], epochTag | blockPlus1);
   atomicMax(&owner[2 * e + 1], epochTag | (kOwnerMulti - blockPlus1));
 }
 __device__ __forceinline__ bool ownerIsMulti(const uint32_t *owner, uint64_t e,
-                                             uint32_t epochTag) {
+                                             uint32_t filterTag) {
+  if (filterTag & kOwnerMulti)
+    return owner[e] == filterTag;
   const uint2 w = *reinterpret_cast<const uint2 *>(owner + 2 * e);
-  return (w.x >> 20) == (epochTag >> 20) && (w.y >> 20) == (epochTag >> 20) &&
+  return (w.x >> 20) == (filterTag >> 20) && (w.y >> 20) == (filterTag >> 20) &&
          (w.x & kOwnerMulti) != kOwnerMulti - (w.y & kOwnerMulti);
 }
 

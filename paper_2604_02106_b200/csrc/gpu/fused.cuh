@@ -55,8 +55,9 @@ struct FusedArgs {
   int interOnChip; // the whole launch is one iteration: INTER-BLOCK pairs found on chip too
   uint32_t R;           // records per MiniCU thread when static (0: allocate)
   int64_t nIters;
-  uint32_t *owner; // per element ownership word (see FusedSink)
+  uint32_t *owner; // per element ownership word(s) (device.cuh)
   uint32_t epoch;
+  int ownerRed;    // reduction layout (two words per element), else exchange
   unsigned long long *keyElem;
   Candidate *cand;
   uint32_t candCap;
@@ -261,9 +262,8 @@ __device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_
 // paired with the records of its element pushed before it (every pair is
 // seen exactly once: by whichever of the two was pushed second).  The
 // block's first record of an element also joins the element's block range
-// in the ownership table (the INTER-BLOCK filter, ownerJoin): two
-// fire-and-forget max reductions, no round trip to L2 on the thread's
-// critical path.  Sites whose parameter is provably block-private (host
+// in the ownership table (the INTER-BLOCK filter, device.cuh): an exchange,
+// or two fire-and-forget max reductions when the table fits L2.  Sites whose parameter is provably block-private (host
 // affine analysis, `own` = false) skip it: no other block can reach their
 // elements.
 template <class Smem> struct FusedSink : ParState {
@@ -282,6 +282,7 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t *owner;      // per element ownership words (nullptr: ablated)
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
+  bool ownerRed = false; // reduction layout of the ownership table (else exchange)
   // k_batch: every trap of the launch, keyed thread << 20 | n-th trap of the
   // thread (canonical order once sorted); nullptr in k_fused (any trap sends
   // the launch to the ordered path there)
@@ -342,8 +343,17 @@ template <class Smem> struct FusedSink : ParState {
       }
       noteKey(*S, keyMin, real, (la * nLocs + lb) * 3 + kind, e);
     }
-    if (own && first && owner) // the block's first record of e: the block joins e's block range
-      ownerJoin(owner, e, epochTag, mine);
+    if (own && first && owner) { // the block's first record of e (device.cuh ownership)
+      if (ownerRed) {
+        ownerJoin(owner, e, epochTag, mine);
+      } else {
+        const uint32_t old = atomicExch(&owner[e], epochTag | mine);
+        if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
+          atomicExch(&owner[e], epochTag | kOwnerMulti);
+          flags |= kFlagShared;
+        }
+      }
+    }
   }
 
   __device__ __forceinline__ void record(int site, const ParamDev *P, int64_t idx, bool own) {
@@ -584,6 +594,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.interOnChip = F.interOnChip != 0;
         s.owner = (F.ablate & 4) ? nullptr : F.owner;
         s.epochTag = F.epoch << 20;
+        s.ownerRed = F.ownerRed != 0;
         s.mine = static_cast<uint32_t>(firstBlock + s.myBlk + 1);
         if (streamed) {
           s.stage = sStage + sb * F.stageCap;

@@ -331,10 +331,12 @@ void sortRaces(std::vector<Race> &races) {
 
 class HostRun {
 public:
+  // lean: a sweep's run — only the races count (enumerateVerdict,
+  // :863-903), so launch records keep no defValues
   HostRun(CompiledProgram &cp, const ExecConfig &cfg, LaunchBackend &be,
-          bool conservative, std::vector<PendingLaunch> *spec = nullptr)
+          bool conservative, std::vector<PendingLaunch> *spec = nullptr, bool lean = false)
       : cp_(cp), prog_(*cp.program), cfg_(cfg), be_(be),
-        conservative_(conservative), spec_(spec) {}
+        conservative_(conservative), spec_(spec), lean_(lean) {}
 
   bool budgetAborted() const { return budgetAbort_; }
   int64_t steps() const { return steps_; }
@@ -388,6 +390,8 @@ private:
   }
 
   void setDef(int site, int aux, const std::string &name, int64_t v) {
+    if (lean_)
+      return;
     auto key = std::make_pair(site, aux);
     auto it = defs_.find(key);
     if (it == defs_.end())
@@ -851,6 +855,7 @@ private:
   LaunchBackend &be_;
   const bool conservative_;
   std::vector<PendingLaunch> *spec_;
+  const bool lean_;
   bool budgetAbort_ = false;
   RunResult res_;
   std::vector<Buf> bufs_;
@@ -864,14 +869,14 @@ private:
 } // namespace
 
 RunResult runConcrete(CompiledProgram &prog, const ExecConfig &cfg,
-                      LaunchBackend &backend) {
+                      LaunchBackend &backend, bool lean) {
   try {
-    return HostRun(prog, cfg, backend, false).run();
+    return HostRun(prog, cfg, backend, false, nullptr, lean).run();
   } catch (const NeedConservative &) {
   }
   RunResult r;
   try {
-    r = HostRun(prog, cfg, backend, true).run();
+    r = HostRun(prog, cfg, backend, true, nullptr, lean).run();
   } catch (const NeedConservative &) {
     r.error = HGRD_GPU_EINVAL;
     r.errorMessage = "stale buffer in conservative mode";
@@ -902,7 +907,7 @@ SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
       c.maxThreads = caps.maxThreads;
       for (int i = 0; i < inputs; ++i)
         c.inputs.push_back(caps.inputSet[cursor[static_cast<size_t>(i)]]);
-      RunResult r = runConcrete(prog, c, backend);
+      RunResult r = runConcrete(prog, c, backend, true);
       if (r.error) {
         out.error = r.error;
         out.errorMessage = r.errorMessage;
@@ -1003,7 +1008,7 @@ SpecRun speculate(CompiledProgram &prog, const ExecConfig &cfg) {
   SpecRun out;
   SpecBackend be;
   try {
-    HostRun run(prog, cfg, be, false, &out.launches);
+    HostRun run(prog, cfg, be, false, &out.launches, true);
     out.res = run.run();
     out.ok = !run.budgetAborted() && out.res.error == 0;
     out.hostSteps = run.steps();
@@ -1049,7 +1054,7 @@ struct ExactPool {
       threads.emplace_back([&, be] {
         for (size_t k; (k = next.fetch_add(1)) < which.size();) {
           const ConfigJob &j = jobs[which[k]];
-          RunResult r = runConcrete(*j.prog, j.cfg, *be);
+          RunResult r = runConcrete(*j.prog, j.cfg, *be, true);
           if (r.error) {
             error = r.error;
             err = r.errorMessage;
@@ -1065,7 +1070,7 @@ struct ExactPool {
              std::vector<RunResult> &out, LaunchBackend &be) {
     for (size_t k; (k = next.fetch_add(1)) < which.size();) {
       const ConfigJob &j = jobs[which[k]];
-      RunResult r = runConcrete(*j.prog, j.cfg, be);
+      RunResult r = runConcrete(*j.prog, j.cfg, be, true);
       if (r.error) {
         error = r.error;
         err = r.errorMessage;
@@ -1208,21 +1213,11 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
     }
     kernelSteps[i] += results[e].steps;
   }
-  // development: HGRD_SWEEP_TRACE=1 prints why configurations were re-run
-  static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
-  if (trace) {
-    auto us = [](auto a, auto b) {
-      return std::chrono::duration<double, std::micro>(b - a).count();
-    };
-    std::fprintf(stderr, "[hgrd sweep] %zu configs, %zu launches batched, %zu speculation "
-                 "failures, %zu with unchecked launches; speculate %.0f prepare %.0f batch %.0f "
-                 "(us)\n", nc, owner.size(), nSpecFail, nUnchecked, us(tA, tB), us(tB, tC),
-                 us(tC, tD));
-  }
   if (pool.finish(jobs, failed, outRuns, backend) < 0) {
     err = pool.err;
     return pool.error;
   }
+  const auto tE = std::chrono::steady_clock::now();
   size_t e = 0;
   for (size_t i = 0; i < nc; ++i) {
     RunResult &r = outRuns[i];
@@ -1234,7 +1229,7 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
     if (!exact[i] && spec[i].hostSteps + kernelSteps[i] > jobs[i].cfg.maxSteps)
       exact[i] = 1; // the budget runs out somewhere: the exact run finds where
     if (exact[i]) {
-      r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend);
+      r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend, true);
       if (r.error) {
         err = r.errorMessage;
         return r.error;
@@ -1268,7 +1263,7 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
         }
       }
       if (truncated) {
-        r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend);
+        r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend, true);
         if (r.error) {
           err = r.errorMessage;
           return r.error;
@@ -1294,6 +1289,19 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
       }
       sortRaces(r.races);
     }
+  }
+  // development: HGRD_SWEEP_TRACE=1 prints why configurations were re-run
+  // and where the time went
+  static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
+  if (trace) {
+    const auto tF = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    std::fprintf(stderr, "[hgrd sweep] %zu configs, %zu launches batched, %zu speculation "
+                 "failures, %zu with unchecked launches; speculate %.0f prepare %.0f batch %.0f "
+                 "exact-wait %.0f merge %.0f (us)\n", nc, owner.size(), nSpecFail, nUnchecked,
+                 us(tA, tB), us(tB, tC), us(tC, tD), us(tD, tE), us(tE, tF));
   }
   return 0;
 }
@@ -1406,7 +1414,7 @@ SweepShard sweepShard(CompiledProgram &prog, const SweepCaps &caps, int rank, in
         c.maxThreads = caps.maxThreads;
         for (int i = 0; i < inputs; ++i)
           c.inputs.push_back(caps.inputSet[cursor[static_cast<size_t>(i)]]);
-        RunResult r = runConcrete(prog, c, backend);
+        RunResult r = runConcrete(prog, c, backend, true);
         if (r.error) {
           out.error = r.error;
           out.errorMessage = r.errorMessage;
@@ -1968,6 +1976,8 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     uint64_t total = 0;
     size_t first = 0;             // first entry in the combined list
   };
+  static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   std::vector<Job> jobs;
   try {
     JVal arr = JParse(jobsJson ? jobsJson : "[]").value();
@@ -1999,6 +2009,7 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     out = errorJson({std::string("jobs: ") + e.what()});
     return HGRD_GPU_EINVAL;
   }
+  const auto t1 = std::chrono::steady_clock::now();
   // every job's configurations in one batched run
   std::vector<ConfigJob> all;
   for (Job &j : jobs) {
@@ -2018,7 +2029,7 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
   if (rc == HGRD_GPU_ENOTSUP) {
     runs.clear();
     for (const ConfigJob &c : all) {
-      runs.push_back(runConcrete(*c.prog, c.cfg, *b0));
+      runs.push_back(runConcrete(*c.prog, c.cfg, *b0, true));
       if (runs.back().error) {
         rc = runs.back().error;
         err = runs.back().errorMessage;
@@ -2032,6 +2043,7 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     out = errorJson({"backend: " + err});
     return rc;
   }
+  const auto t2 = std::chrono::steady_clock::now();
   out = "[";
   for (size_t q = 0; q < jobs.size(); ++q) {
     Job &j = jobs[q];
@@ -2078,6 +2090,14 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     }
   }
   out += "]";
+  if (trace) {
+    auto us = [](auto a, auto b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    std::fprintf(stderr, "[hgrd many] %zu jobs: parse+compile %.0f run %.0f report %.0f (us)\n",
+                 jobs.size(), us(t0, t1), us(t1, t2),
+                 us(t2, std::chrono::steady_clock::now()));
+  }
   return HGRD_GPU_OK;
 }
 

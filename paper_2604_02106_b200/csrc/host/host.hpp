@@ -133,8 +133,10 @@ struct CompiledProgram {
 
 std::unique_ptr<CompiledProgram> compileProgram(std::unique_ptr<Program> p);
 
+// lean: a sweep's run (launch records without defValues; races, traps and
+// counters as always)
 RunResult runConcrete(CompiledProgram &prog, const ExecConfig &cfg,
-                      LaunchBackend &backend);
+                      LaunchBackend &backend, bool lean = false);
 SweepResult enumerateVerdict(CompiledProgram &prog, const SweepCaps &caps,
                              LaunchBackend &backend);
 // One rank's share of enumerateVerdict's configuration lattice: the

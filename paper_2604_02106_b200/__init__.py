@@ -386,19 +386,29 @@ class GpuContext:
             raise RuntimeError(f"sweep_shard failed ({rc}): {s}")
         return json.loads(s)
 
+    @staticmethod
+    def sweep_jobs_payload(jobs) -> bytes:
+        """The C ABI's jobs JSON for enumerate_verdict_many_raw."""
+        return json.dumps([{"source": j["source"], "file": j.get("file", "prog.mcu"),
+                            "caps": j.get("caps") or {}} for j in jobs]).encode()
+
+    def enumerate_verdict_many_raw(self, payload: bytes, rank: int = 0, world: int = 1) -> str:
+        """hgrd_gpu_enumerate_verdict_many_json as is: jobs JSON in, report
+        JSON text out."""
+        out = ctypes.c_void_p()
+        rc = self._lib.hgrd_gpu_enumerate_verdict_many_json(self._ctx, payload, rank, world,
+                                                            ctypes.byref(out))
+        s = _take_string(self._lib, out)
+        if rc != 0:
+            raise RuntimeError(f"enumerate_verdict_many failed ({rc}): {s}")
+        return s
+
     def enumerate_verdict_many(self, jobs, rank: int = 0, world: int = 1) -> List[dict]:
         """Many programs' sweeps at once (BASELINE config 5): jobs is a list
         of {"source", "file", "caps"}; returns per job its enumerateVerdict
         result (world 1) or this rank's sweep shard (parallel.merge_shards)."""
-        out = ctypes.c_void_p()
-        payload = json.dumps([{"source": j["source"], "file": j.get("file", "prog.mcu"),
-                               "caps": j.get("caps") or {}} for j in jobs])
-        rc = self._lib.hgrd_gpu_enumerate_verdict_many_json(self._ctx, payload.encode(), rank,
-                                                            world, ctypes.byref(out))
-        s = _take_string(self._lib, out)
-        if rc != 0:
-            raise RuntimeError(f"enumerate_verdict_many failed ({rc}): {s}")
-        return json.loads(s)
+        return json.loads(self.enumerate_verdict_many_raw(self.sweep_jobs_payload(jobs), rank,
+                                                          world))
 
     def enumerate_verdict(self, source: str, caps=None, file_name: str = "prog.mcu") -> dict:
         out = ctypes.c_void_p()

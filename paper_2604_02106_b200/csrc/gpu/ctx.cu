@@ -12,6 +12,7 @@
 #include "batch.cuh"
 #include "affine.hpp"
 #include "jit.hpp"
+#include "parallel_for.hpp"
 
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -934,7 +935,8 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   // ownership table (epoch-tagged, no memset between launches, device.cuh):
   // reduction layout (two words per element) when it fits L2 comfortably,
   // else the exchange layout (one word)
-  const bool ownerRed = 8 * P.totalW <= (uint64_t(32) << 20);
+  static const char *redEnv = std::getenv("HGRD_OWNER_RED"); // A/B knob: 0 / 1 forces a layout
+  const bool ownerRed = redEnv ? std::atoi(redEnv) != 0 : 8 * P.totalW <= (uint64_t(32) << 20);
   const size_t ownerN = (ownerRed ? 2 : 1) * std::max<uint64_t>(P.totalW, 1);
   const bool fresh = c->owner.cap < ownerN;
   NEED(c->owner, ownerN);
@@ -1996,29 +1998,6 @@ int shardDetect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, const uint64_t *keys,
 // descriptor, one k_batch launch, one D2H of every launch's counters and
 // races.
 
-// fn(i) for i < n on up to the hardware's threads (chunks of 64).
-template <class F> void parallelFor(size_t n, F &&fn) {
-  const size_t hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  const size_t nt = std::min(hw, (n + 255) / 256);
-  if (nt <= 1) {
-    for (size_t i = 0; i < n; ++i)
-      fn(i);
-    return;
-  }
-  std::atomic<size_t> next{0};
-  auto work = [&] {
-    for (size_t b; (b = next.fetch_add(64)) < n;)
-      for (size_t i = b; i < std::min(n, b + 64); ++i)
-        fn(i);
-  };
-  std::vector<std::thread> pool;
-  for (size_t t = 1; t < nt; ++t)
-    pool.emplace_back(work);
-  work();
-  for (auto &t : pool)
-    t.join();
-}
-
 struct BatchPlan {
   bool ok = false;
   uint32_t R = 0;
@@ -2031,6 +2010,12 @@ struct BatchPlan {
 };
 
 void planBatchLaunch(const hgrd_gpu_batch_launch &B, BatchPlan &P) {
+  // (P may hold an earlier batch's plan: reused storage, no allocations)
+  P.ok = false;
+  P.R = 0;
+  P.totalW = 0;
+  P.wBase.clear();
+  P.wHandle.clear();
   const hgrd_gpu_launch &L = B.launch;
   std::string why;
   if (!validLaunch(L, why))
@@ -2050,12 +2035,15 @@ void planBatchLaunch(const hgrd_gpu_batch_launch &B, BatchPlan &P) {
     const int32_t h = L.param_handle[param];
     return (h >= 0 && static_cast<uint32_t>(h) < nb) ? h : -1;
   };
-  std::vector<char> written(nb, 0);
+  static thread_local std::vector<char> written; // (per-thread scratch, no allocations)
+  static thread_local std::vector<uint64_t> base;
+  static thread_local std::vector<int> windex;
+  written.assign(nb, 0);
+  base.assign(nb, 0);
+  windex.assign(nb, 0);
   for (uint32_t s = 0; s < L.n_sites; ++s)
     if (L.sites[s].kind != HGRD_SITE_LOAD && bufOf(L.sites[s].param) >= 0)
       written[static_cast<size_t>(bufOf(L.sites[s].param))] = 1;
-  std::vector<uint64_t> base(nb, 0);
-  std::vector<int> windex(nb, 0);
   for (uint32_t h = 0; h < nb; ++h)
     if (written[h]) {
       windex[h] = static_cast<int>(P.wBase.size()) + 1;
@@ -2149,9 +2137,12 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
     resetResult(&R[i]);
     R[i].mode = HGRD_RESULT_UNCHECKED;
   }
-  // 1. per-launch plans, on host threads
-  std::vector<BatchPlan> plans(n);
-  parallelFor(n, [&](size_t i) { planBatchLaunch(BL[i], plans[i]); });
+  // 1. per-launch plans, on host threads (storage kept across batches of
+  //    this host thread: a sweep's batches allocate nothing after the first)
+  static thread_local std::vector<BatchPlan> plans;
+  if (plans.size() < n)
+    plans.resize(n);
+  hgrdgpu::parallelFor(n, [&](size_t i) { planBatchLaunch(BL[i], plans[i]); });
   std::vector<uint32_t> idx; // batch entry -> launch
   for (uint32_t i = 0; i < n; ++i)
     if (plans[i].ok)
@@ -2229,7 +2220,7 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
   // 3. fill the pinned staging buffer (device addresses fixed up), on host threads
   unsigned char *h = c->hBatch;
   std::memset(h + nextAt, 0, 16);
-  parallelFor(m, [&](size_t k) {
+  hgrdgpu::parallelFor(m, [&](size_t k) {
     const hgrd_gpu_batch_launch &B = BL[idx[k]];
     const hgrd_gpu_launch &L = B.launch;
     BatchPlan &P = plans[idx[k]];

@@ -19,6 +19,7 @@
 // value matters, restarts the run in conservative mode, where every launch
 // that writes memory runs SEQUENTIAL, so buffers are always exact.
 #include "host.hpp"
+#include "parallel_for.hpp"
 
 #include <atomic>
 #include <thread>
@@ -1146,8 +1147,12 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
   constexpr uint32_t kTrapsPerLaunch = 64; // more: the configuration is re-run exactly
   std::unique_ptr<hgrd_gpu_trap[]> trapStore(
       new hgrd_gpu_trap[std::max<size_t>(owner.size(), 1) * kTrapsPerLaunch]);
-  size_t raceAt = 0;
+  std::vector<size_t> raceAt(owner.size() + 1, 0);
   for (size_t e = 0; e < owner.size(); ++e) {
+    const size_t nl = std::max<size_t>(spec[owner[e].first].launches[owner[e].second].lk->locs.size(), 1);
+    raceAt[e + 1] = raceAt[e] + 3 * nl * nl;
+  }
+  parallelFor(owner.size(), [&](size_t e) {
     const PendingLaunch &p = spec[owner[e].first].launches[owner[e].second];
     const LoweredKernel &lk = *p.lk;
     hgrd_gpu_launch &L = bl[e].launch;
@@ -1174,14 +1179,12 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
     bl[e].buffer_elems = p.bufElems.data();
     bl[e].buffer_data = dataPtrs[e].data();
     bl[e].n_buffers = static_cast<uint32_t>(p.bufElems.size());
-    const size_t nl = std::max<size_t>(lk.locs.size(), 1);
     results[e] = hgrd_gpu_result{};
-    results[e].races = raceStore.data() + raceAt;
-    results[e].race_cap = static_cast<uint32_t>(3 * nl * nl);
+    results[e].races = raceStore.data() + raceAt[e];
+    results[e].race_cap = static_cast<uint32_t>(raceAt[e + 1] - raceAt[e]);
     results[e].traps = trapStore.get() + e * kTrapsPerLaunch;
     results[e].trap_cap = kTrapsPerLaunch;
-    raceAt += 3 * nl * nl;
-  }
+  });
   const auto tC = std::chrono::steady_clock::now();
   if (!bl.empty()) {
     constexpr size_t kChunk = 1 << 16; // launches per batched check
@@ -1218,76 +1221,80 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
     return pool.error;
   }
   const auto tE = std::chrono::steady_clock::now();
-  size_t e = 0;
-  for (size_t i = 0; i < nc; ++i) {
-    RunResult &r = outRuns[i];
-    const size_t e0 = e;
-    while (e < owner.size() && owner[e].first == i)
-      ++e;
-    if (!spec[i].ok)
-      continue; // (run exactly by the pool)
-    if (!exact[i] && spec[i].hostSteps + kernelSteps[i] > jobs[i].cfg.maxSteps)
-      exact[i] = 1; // the budget runs out somewhere: the exact run finds where
-    if (exact[i]) {
-      r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend, true);
-      if (r.error) {
-        err = r.errorMessage;
-        return r.error;
-      }
-      ++r.stats.restarts;
-    } else {
-      // kernel traps go between the host traps recorded before and after
-      // their launch; the run keeps the first 256 (reference :125-130)
-      std::vector<std::string> traps;
-      const std::vector<std::string> &hostTraps = spec[i].res.traps;
-      size_t hostAt = 0;
-      bool truncated = false;
-      for (size_t q = e0; q < e && !truncated; ++q) {
-        const PendingLaunch &p = spec[i].launches[q - e0];
-        while (hostAt < p.trapPos && hostAt < hostTraps.size())
+  // the configurations' first batch entries (entries are in config order)
+  std::vector<size_t> firstEntry(nc + 1, owner.size());
+  for (size_t e = owner.size(); e-- > 0;)
+    firstEntry[owner[e].first] = e;
+  // 3a. the speculation's report per configuration (independent: host threads)
+  parallelFor(
+      nc,
+      [&](size_t i) {
+        if (!spec[i].ok)
+          return; // (run exactly by the pool)
+        if (!exact[i] && spec[i].hostSteps + kernelSteps[i] > jobs[i].cfg.maxSteps)
+          exact[i] = 1; // the budget runs out somewhere: the exact run finds where
+        if (exact[i])
+          return;
+        const size_t e0 = firstEntry[i], e = e0 + spec[i].launches.size();
+        // kernel traps go between the host traps recorded before and after
+        // their launch; the run keeps the first 256 (reference :125-130)
+        std::vector<std::string> traps;
+        const std::vector<std::string> &hostTraps = spec[i].res.traps;
+        size_t hostAt = 0;
+        for (size_t q = e0; q < e; ++q) {
+          const PendingLaunch &p = spec[i].launches[q - e0];
+          while (hostAt < p.trapPos && hostAt < hostTraps.size())
+            traps.push_back(hostTraps[hostAt++]);
+          const hgrd_gpu_result &kr = results[q];
+          const uint64_t want = std::min<uint64_t>(kr.n_traps_total,
+                                                   traps.size() < 256 ? 256 - traps.size() : 0);
+          if (want > kr.n_traps) {
+            exact[i] = 1; // more traps than the batch handed back
+            return;
+          }
+          for (uint64_t t = 0; t < want; ++t) {
+            const auto si = static_cast<size_t>(kr.traps[t].site);
+            traps.push_back(jobs[i].prog->program->file + ":" +
+                            std::to_string(p.lk->siteLoc[si].line) + ": " +
+                            (kr.traps[t].kind == HGRD_TRAP_OOB
+                                 ? "kernel access out of bounds on "
+                                 : "kernel access to unallocated array ") +
+                            p.lk->siteArray[si]);
+          }
+        }
+        while (hostAt < hostTraps.size())
           traps.push_back(hostTraps[hostAt++]);
-        const hgrd_gpu_result &kr = results[q];
-        const uint64_t want = std::min<uint64_t>(kr.n_traps_total,
-                                                 traps.size() < 256 ? 256 - traps.size() : 0);
-        if (want > kr.n_traps) {
-          truncated = true; // more traps than the batch handed back
-          break;
+        if (traps.size() > 256)
+          traps.resize(256);
+        RunResult &r = outRuns[i];
+        r = std::move(spec[i].res);
+        r.traps = std::move(traps);
+        SeenKeys keys;
+        for (size_t q = e0; q < e; ++q) {
+          const PendingLaunch &p = spec[i].launches[q - e0];
+          mergeLaunchRaces(r, keys, *p.lk, p.grid, p.block, results[q].races,
+                           results[q].n_races, p.launchIndex);
+          r.stats.instances += results[q].instances;
+          r.stats.records += results[q].records;
+          r.stats.kernelSteps += results[q].steps;
+          ++r.stats.batchedLaunches;
         }
-        for (uint64_t t = 0; t < want; ++t) {
-          const auto si = static_cast<size_t>(kr.traps[t].site);
-          traps.push_back(jobs[i].prog->program->file + ":" + std::to_string(p.lk->siteLoc[si].line) +
-                          ": " +
-                          (kr.traps[t].kind == HGRD_TRAP_OOB ? "kernel access out of bounds on "
-                                                             : "kernel access to unallocated array ") +
-                          p.lk->siteArray[si]);
-        }
-      }
-      if (truncated) {
-        r = runConcrete(*jobs[i].prog, jobs[i].cfg, backend, true);
-        if (r.error) {
-          err = r.errorMessage;
-          return r.error;
-        }
-        ++r.stats.restarts;
-        continue;
-      }
-      while (hostAt < hostTraps.size())
-        traps.push_back(hostTraps[hostAt++]);
-      if (traps.size() > 256)
-        traps.resize(256);
-      r = std::move(spec[i].res);
-      r.traps = std::move(traps);
-      SeenKeys keys;
-      for (size_t q = e0; q < e; ++q) {
-        const PendingLaunch &p = spec[i].launches[q - e0];
-        mergeLaunchRaces(r, keys, *p.lk, p.grid, p.block, results[q].races, results[q].n_races,
-                         p.launchIndex);
-        r.stats.instances += results[q].instances;
-        r.stats.records += results[q].records;
-        r.stats.kernelSteps += results[q].steps;
-        ++r.stats.batchedLaunches;
-      }
-      sortRaces(r.races);
+        sortRaces(r.races);
+      },
+      64);
+  // 3b. exact re-runs of what the batch could not decide (traps beyond the
+  //     batch's trap slots, the step budget, unchecked launches)
+  std::vector<size_t> redo;
+  for (size_t i = 0; i < nc; ++i)
+    if (spec[i].ok && exact[i])
+      redo.push_back(i);
+  if (!redo.empty()) {
+    ExactPool pool2{workers, workers ? nWorkers : 0};
+    if (workers)
+      pool2.start(jobs, redo, outRuns);
+    if (pool2.finish(jobs, redo, outRuns, backend) < 0) {
+      err = pool2.err;
+      return pool2.error;
     }
   }
   // development: HGRD_SWEEP_TRACE=1 prints why configurations were re-run
@@ -1763,16 +1770,43 @@ std::string runResultJson(const RunResult &r, const std::string &file) {
 }
 
 std::string sweepResultJson(const SweepResult &r, const std::string &file) {
-  std::ostringstream o;
-  o << "{\"races\":[";
+  // (direct appends: a config-5 sweep reports thousands of races per call)
+  const std::string fileJ = esc(file);
+  std::string o;
+  o.reserve(96 + r.races.size() * (112 + 2 * fileJ.size()));
+  o += "{\"races\":[";
+  char num[24];
+  auto put = [&](int64_t v) {
+    const int n = std::snprintf(num, sizeof num, "%" PRId64, v);
+    o.append(num, static_cast<size_t>(n));
+  };
+  auto loc = [&](const Loc &l) {
+    o += "{\"file\":";
+    o += fileJ;
+    o += ",\"line\":";
+    put(l.line);
+    o += ",\"column\":";
+    put(l.col);
+    o += "}";
+  };
   for (size_t i = 0; i < r.races.size(); ++i) {
     const SweepRace &x = r.races[i];
-    o << (i ? "," : "") << "{\"kind\":" << esc(raceKindName(x.kind))
-      << ",\"locA\":" << locJ(x.locA, file) << ",\"locB\":" << locJ(x.locB, file)
-      << ",\"warpSize\":" << x.warpSize << "}";
+    o += i ? ",{\"kind\":\"" : "{\"kind\":\"";
+    o += raceKindName(x.kind);
+    o += "\",\"locA\":";
+    loc(x.locA);
+    o += ",\"locB\":";
+    loc(x.locB);
+    o += ",\"warpSize\":";
+    put(x.warpSize);
+    o += "}";
   }
-  o << "],\"configs\":" << r.configs << ",\"stats\":" << statsJ(r.stats) << "}";
-  return o.str();
+  o += "],\"configs\":";
+  put(static_cast<int64_t>(r.configs));
+  o += ",\"stats\":";
+  o += statsJ(r.stats);
+  o += "}";
+  return o;
 }
 
 std::string sweepShardJson(const SweepShard &r, const std::string &file) {
@@ -1983,28 +2017,36 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     JVal arr = JParse(jobsJson ? jobsJson : "[]").value();
     if (arr.kind != JVal::Arr)
       throw std::runtime_error("jobs: expected an array");
-    for (const JVal &j : arr.arr) {
-      Job job;
-      const JVal *src = j.get("source");
-      const JVal *file = j.get("file");
-      job.file = file && file->kind == JVal::Str ? file->s : "prog.mcu";
-      if (const JVal *c = j.get("caps"))
-        capsFromJson(*c, job.caps);
-      ParseOutcome po = parseMiniCU(src && src->kind == JVal::Str ? src->s : "", job.file);
-      if (!po.program) {
-        job.error = errorJson(po.diagnostics);
-      } else {
-        job.cp = compileProgram(std::move(po.program));
-        const std::vector<ExecConfig> all = sweepConfigs(*job.cp, job.caps);
-        job.total = all.size();
-        for (size_t k = 0; k < all.size(); ++k)
-          if (static_cast<int>(k % static_cast<size_t>(world)) == rank) {
-            job.cfgs.push_back(all[k]);
-            job.index.push_back(k);
-          }
-      }
-      jobs.push_back(std::move(job));
+    jobs.resize(arr.arr.size());
+    for (size_t q = 0; q < arr.arr.size(); ++q) {
+      const JVal *file = arr.arr[q].get("file");
+      jobs[q].file = file && file->kind == JVal::Str ? file->s : "prog.mcu";
+      if (const JVal *c = arr.arr[q].get("caps"))
+        capsFromJson(*c, jobs[q].caps);
     }
+    // front end of every job (independent programs: host threads)
+    parallelFor(
+        jobs.size(),
+        [&](size_t q) {
+          Job &job = jobs[q];
+          const JVal *src = arr.arr[q].get("source");
+          ParseOutcome po = parseMiniCU(src && src->kind == JVal::Str ? src->s : "", job.file);
+          if (!po.program) {
+            job.error = errorJson(po.diagnostics);
+            return;
+          }
+          job.cp = compileProgram(std::move(po.program));
+          for (const Function &k : job.cp->program->kernels)
+            job.cp->kernel(&k); // lowered here, in parallel
+          const std::vector<ExecConfig> all = sweepConfigs(*job.cp, job.caps);
+          job.total = all.size();
+          for (size_t k = 0; k < all.size(); ++k)
+            if (static_cast<int>(k % static_cast<size_t>(world)) == rank) {
+              job.cfgs.push_back(all[k]);
+              job.index.push_back(k);
+            }
+        },
+        8);
   } catch (const std::exception &e) {
     out = errorJson({std::string("jobs: ") + e.what()});
     return HGRD_GPU_EINVAL;

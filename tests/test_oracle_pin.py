@@ -175,3 +175,20 @@ def test_batched_sweeps(cpu_oracle):
         restarts += got["stats"]["restarts"]
         configs += got["configs"]
     assert configs == 9695 and restarts < configs // 50  # most configurations batched
+
+
+def test_many_sweeps_and_shards(cpu_oracle):
+    """sweepManyJson (hgrd_gpu_enumerate_verdict_many_json's host side): all
+    229 config-5 programs in one call reproduce the reference's sweeps, and
+    per-rank shards (canonical index % world) merge back to them."""
+    from paper_2604_02106_b200.parallel import merge_shards
+    lat = load_golden("lattice")
+    jobs = [{"source": j["source"], "file": j["file"], "caps": j["caps"]} for j in lat]
+    got = cpu_oracle.enumerate_verdict_many(jobs)
+    assert [strip_extras(g) for g in got] == [j["sweep"] for j in lat]
+    world = 3
+    shards = [cpu_oracle.enumerate_verdict_many(jobs, r, world) for r in range(world)]
+    for q, j in enumerate(lat):
+        assert merge_shards([shards[r][q] for r in range(world)])["races"] == j["sweep"]["races"]
+    bad = cpu_oracle.enumerate_verdict_many([{"source": "int main(", "file": "x.mcu"}])
+    assert "error" in bad[0]

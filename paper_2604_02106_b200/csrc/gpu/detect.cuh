@@ -601,6 +601,80 @@ __device__ __forceinline__ bool crossed(const LockSet &x, const LockSet &y, bool
   return false;
 }
 
+// Exact lockOrdered (reference :678-728) straight from two threads' sync-op
+// lists, for events whose lock sets exceed LockSet's 8 entries (no limit;
+// quadratic in the ops, so only the fallback).  Scopes: 0 absent, 1 block,
+// 2 device; an acquire of lock (h, i) before event seq is a CAS on it
+// before a fence before seq (scope: the narrower of the two, the widest
+// such pair), a release an Exch after a fence after seq; a critical section
+// both, scope the narrower.
+__device__ int lockScopeOf(const LaunchDev &L, uint64_t thread, int32_t seq, int32_t h,
+                           int64_t idx, bool acquire) {
+  const uint64_t b = L.opStride ? thread * L.opStride : L.opStart[thread];
+  const uint64_t e = L.opStride ? b + L.opStride : L.opStart[thread + 1];
+  int best = 0;
+  for (uint64_t f = b; f < e; ++f) {
+    const int32_t mf = L.opMeta[f];
+    if ((mf & 15) != 2)
+      continue;
+    const int32_t fs = L.opSeq[f], fsc = (mf >> 4) & 15;
+    if (acquire ? !(fs < seq) : !(fs > seq))
+      continue;
+    for (uint64_t c = b; c < e; ++c) {
+      const int32_t mc = L.opMeta[c];
+      if ((mc & 15) != (acquire ? 0 : 1) || (mc >> 8) - 1 != h || L.opIndex[c] != idx)
+        continue;
+      if (acquire ? L.opSeq[c] >= fs : L.opSeq[c] <= fs)
+        continue;
+      best = max(best, min((mc >> 4) & 15, fsc));
+    }
+  }
+  return best;
+}
+
+__device__ bool lockOrderedDirect(const LaunchDev &L, uint64_t ta, int32_t sa, uint64_t tb,
+                                  int32_t sb, bool sameBlock) {
+  const uint64_t b = L.opStride ? ta * L.opStride : L.opStart[ta];
+  const uint64_t e = L.opStride ? b + L.opStride : L.opStart[ta + 1];
+  for (uint64_t o = b; o < e; ++o) { // every lock of a's sets is one of a's CAS / Exch
+    const int32_t m = L.opMeta[o];
+    if ((m & 15) > 1)
+      continue;
+    const int32_t h = (m >> 8) - 1;
+    const int64_t idx = L.opIndex[o];
+    const int acqA = lockScopeOf(L, ta, sa, h, idx, true);
+    const int relA = lockScopeOf(L, ta, sa, h, idx, false);
+    const int acqB = lockScopeOf(L, tb, sb, h, idx, true);
+    const int relB = lockScopeOf(L, tb, sb, h, idx, false);
+    const int csA = (acqA && relA) ? min(acqA, relA) : 0;
+    const int csB = (acqB && relB) ? min(acqB, relB) : 0;
+    if ((csA && csB && covers(min(csA, csB), sameBlock)) ||
+        (relA && acqB && covers(min(relA, acqB), sameBlock)) ||
+        (relB && acqA && covers(min(relB, acqA), sameBlock)))
+      return true;
+  }
+  return false;
+}
+
+// lockOrdered(a, b) from both events' lock facts (a's computed once per row);
+// the exact direct evaluation when a set overflowed LockSet.
+template <class E>
+__device__ bool lockPairOrdered(const LaunchDev &L, const E &a, const E &b, bool sameBlock,
+                                LockInfo &la, bool &laFull, bool &laWide, LockInfo &lb) {
+  if (!laFull) {
+    unsigned f = 0;
+    lockInfoOf(L, a.thread, a.seq, la, f);
+    laWide = (f & kFlagLockSet) != 0;
+    laFull = true;
+  }
+  unsigned f = 0;
+  lockInfoOf(L, b.thread, b.seq, lb, f);
+  if (laWide || (f & kFlagLockSet))
+    return lockOrderedDirect(L, a.thread, a.seq, b.thread, b.seq, sameBlock);
+  return crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
+         crossed(lb.rel, la.acq, sameBlock);
+}
+
 // Per-event lock facts precomputed once (k_lock_info) instead of per pair:
 // up to two entries per set, entry = (handle + 1) << 48 | scope << 46 |
 // index, 0 = empty.  Wider sets, handles or indices mark the event
@@ -672,13 +746,9 @@ __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
   const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
   const SiteDev sa = A.sites[a.site];
   LockC ca{};
-  bool laFull = false;
-  if (locks && lc) {
+  bool laFull = false, laWide = false;
+  if (locks && lc)
     ca = lc[x];
-  } else if (locks) {
-    lockInfoOf(L, a.thread, a.seq, la, flags);
-    laFull = true;
-  }
   for (uint64_t y = x + 1; y < e; ++y) {
     const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
     if (a.thread == b.thread)
@@ -702,13 +772,7 @@ __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
         ordered = crossedC(ca.cs, cb.cs, sameBlock) || crossedC(ca.rel, cb.acq, sameBlock) ||
                   crossedC(cb.rel, ca.acq, sameBlock);
       } else {
-        if (!laFull) {
-          lockInfoOf(L, a.thread, a.seq, la, flags);
-          laFull = true;
-        }
-        lockInfoOf(L, b.thread, b.seq, lb, flags);
-        ordered = crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
-                  crossed(lb.rel, la.acq, sameBlock);
+        ordered = lockPairOrdered(L, a, b, sameBlock, la, laFull, laWide, lb);
       }
       if (ordered)
         continue;
@@ -739,11 +803,12 @@ __global__ void k_lock_info(DetectArgs A, LaunchDev L, const uint32_t *order, Lo
   unsigned flags = 0;
   lockInfoOf(L, a.thread, a.seq, li, flags);
   LockC c;
-  if (!packSet(li.cs, c.cs) || !packSet(li.acq, c.acq) || !packSet(li.rel, c.rel))
+  // (wide: more than two entries, or a set past LockSet's capacity — the
+  // pair pass then evaluates lockOrdered exactly, lockPairOrdered)
+  if ((flags & kFlagLockSet) || !packSet(li.cs, c.cs) || !packSet(li.acq, c.acq) ||
+      !packSet(li.rel, c.rel))
     c.cs[0] = kLockWide;
   out[x] = c;
-  if (flags)
-    atomicOr(&L.ctr->flags, flags);
 }
 
 __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
@@ -868,7 +933,7 @@ __global__ void __launch_bounds__(256) k_detect_pairwise_big(DetectArgs A, Launc
       if (locks)
         ca = lc[x];
       LockInfo la, lb;
-      bool laFull = false;
+      bool laFull = false, laWide = false;
       const int jStart = rb == tb ? tid + 1 : 0;
       for (int j = jStart; j < nTile; ++j) {
         const EvT &b = tEv[j];
@@ -892,13 +957,7 @@ __global__ void __launch_bounds__(256) k_detect_pairwise_big(DetectArgs A, Launc
             ordered = crossedC(ca.cs, cb.cs, sameBlock) || crossedC(ca.rel, cb.acq, sameBlock) ||
                       crossedC(cb.rel, ca.acq, sameBlock);
           } else {
-            if (!laFull) {
-              lockInfoOf(L, a.thread, a.seq, la, flags);
-              laFull = true;
-            }
-            lockInfoOf(L, b.thread, b.seq, lb, flags);
-            ordered = crossed(la.cs, lb.cs, sameBlock) || crossed(la.rel, lb.acq, sameBlock) ||
-                      crossed(lb.rel, la.acq, sameBlock);
+            ordered = lockPairOrdered(L, a, b, sameBlock, la, laFull, laWide, lb);
           }
           if (ordered)
             continue;

@@ -428,3 +428,81 @@ def histogram_pow2_expected(n_threads: int, bins: int, update: str = "store"):
         return []
     i0 = (-HIST_SEED * pow(HIST_MULT, -1, bins)) % bins
     return [("INTER-BLOCK", 0, i0, i0 + bins)]
+
+
+def wide_lock_kernel(n_locks: int, variant: str, threads: int = 64, block: int = 16) -> str:
+    """Critical sections guarded by `n_locks` locks at once: lock sets wider
+    than the GPU detector's fixed sets (8), evaluated exactly
+    (detect.cuh lockOrderedDirect).  `clean`: every thread takes every lock;
+    `partial`: odd threads skip lock 0 (the others still order them);
+    `leaky`: threads of block 1 touch the cell without taking any lock;
+    `blockscope`: block-scope CAS on lock 0 (device-scope on the rest)."""
+    acq, rel = [], []
+    for i in range(n_locks):
+        cas = "atomicCAS_block" if (variant == "blockscope" and i == 0) else "atomicCAS"
+        guard = "if (t % 2 == 0) { " if (variant == "partial" and i == 0) else ""
+        close = " }" if guard else ""
+        acq.append(f"  {guard}{cas}(L[{i}], 0, 1);{close}\n")
+        rel.append(f"  {guard}atomicExch(L[{i}], 0);{close}\n")
+    body = "".join(acq) + "  __threadfence();\n"
+    cs = "  acc[t % 3] = acc[t % 3] + t;\n"
+    if variant == "leaky":
+        body = ("  if (blockIdx.x != 1) {\n" + "".join("  " + a for a in acq) +
+                "    __threadfence();\n  }\n")
+        cs = "  acc[t % 3] = acc[t % 3] + t;\n"
+        tail = ("  if (blockIdx.x != 1) {\n    __threadfence();\n" +
+                "".join("  " + r for r in rel) + "  }\n")
+    else:
+        tail = "  __threadfence();\n" + "".join(rel)
+    return ("__global__ void k(int *acc, lock *L) {\n"
+            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+            f"{body}{cs}{tail}"
+            "}\n"
+            f"void main() {{ int *acc; lock *L; cudaMalloc(&acc, 4); cudaMalloc(&L, {n_locks});\n"
+            f"  k<<<({threads // block},1,1),({block},1,1)>>>(acc, L); }}\n")
+
+
+WIDE_LOCK_CASES = [(n, v) for n in (9, 12) for v in ("clean", "partial", "leaky", "blockscope")]
+
+
+def _overflow_programs() -> Dict[str, str]:
+    """Launches past the fused kernel's fixed fields, which must fall back
+    to the general / pairwise paths exactly: more than 255 barrier phases in
+    a thread, more than 8 written buffers, more than 64 access sites."""
+    out = {}
+    out["barriers_300"] = (
+        "__global__ void k(int *A, int n) {\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  for (int i = 0; i < n; i++) {\n"
+        "    A[t] = i;\n"
+        "    __syncthreads();\n"
+        "  }\n"
+        "  A[(t + 1) % 64] = t;\n"
+        "  A[64 + t % 4] = t;\n"
+        "}\n"
+        "void main() { int *A; cudaMalloc(&A, 68);\n"
+        "  k<<<(2,1,1),(32,1,1)>>>(A, 300); }\n")
+    params = ", ".join(f"int *B{i}" for i in range(9))
+    stores = "".join(f"  B{i}[(t + {i}) % 5] = t;\n" for i in range(9))
+    decls = " ".join(f"int *B{i}; cudaMalloc(&B{i}, 16);" for i in range(9))
+    args = ", ".join(f"B{i}" for i in range(9))
+    out["written_9"] = (
+        f"__global__ void k({params}) {{\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        f"{stores}"
+        "}\n"
+        f"void main() {{ {decls}\n"
+        f"  k<<<(2,1,1),(8,1,1)>>>({args}); }}\n")
+    lines = "".join(f"  A[t * 34 + {i}] = A[t * 34 + {i + 1}];\n" for i in range(33))
+    out["sites_67"] = (
+        "__global__ void k(int *A) {\n"
+        "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+        f"{lines}"
+        "  A[t % 3] = t;\n"
+        "}\n"
+        "void main() { int *A; cudaMalloc(&A, 1100);\n"
+        "  k<<<(2,1,1),(16,1,1)>>>(A); }\n")
+    return out
+
+
+OVERFLOW_PROGRAMS = _overflow_programs()

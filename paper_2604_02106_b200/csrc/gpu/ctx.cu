@@ -2139,7 +2139,8 @@ int checkBatch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *BL, uint32_t n,
   }
   // 1. per-launch plans, on host threads (storage kept across batches of
   //    this host thread: a sweep's batches allocate nothing after the first)
-  static thread_local std::vector<BatchPlan> plans;
+  static thread_local std::vector<BatchPlan> tlPlans;
+  std::vector<BatchPlan> &plans = tlPlans; // (the caller's: lambdas on other threads use it)
   if (plans.size() < n)
     plans.resize(n);
   hgrdgpu::parallelFor(n, [&](size_t i) { planBatchLaunch(BL[i], plans[i]); });

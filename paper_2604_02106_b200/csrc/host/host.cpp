@@ -25,6 +25,7 @@
 #include <thread>
 
 #include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
@@ -1101,21 +1102,11 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
   }
   // 1. speculative host runs, spread over host threads
   std::vector<SpecRun> spec(nc);
-  {
-    const int nt = static_cast<int>(std::max<size_t>(
-        1, std::min<size_t>(static_cast<size_t>(std::max(hostThreads, 1)), (nc + 31) / 32)));
-    std::atomic<size_t> next{0};
-    auto work = [&] {
-      for (size_t i; (i = next.fetch_add(1)) < nc;)
-        spec[i] = speculate(*jobs[i].prog, jobs[i].cfg);
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nt; ++t)
-      pool.emplace_back(work);
-    work();
-    for (auto &th : pool)
-      th.join();
-  }
+  if (hostThreads > 1)
+    parallelFor(nc, [&](size_t i) { spec[i] = speculate(*jobs[i].prog, jobs[i].cfg); }, 16);
+  else
+    for (size_t i = 0; i < nc; ++i)
+      spec[i] = speculate(*jobs[i].prog, jobs[i].cfg);
   // configurations whose speculation failed (sequential or lock-idiom
   // launches, host reads of device results, the host's step budget) run
   // exactly on the worker backends while the batch is checked
@@ -1297,6 +1288,10 @@ int runConfigsBatched(const std::vector<ConfigJob> &jobs, LaunchBackend &backend
       return pool2.error;
     }
   }
+  // the speculation state (tens of thousands of small allocations) is freed
+  // off the caller's critical path
+  std::thread([s = std::move(spec), b = std::move(bl), d = std::move(dataPtrs),
+               r = std::move(results), rs = std::move(raceStore)]() mutable {}).detach();
   // development: HGRD_SWEEP_TRACE=1 prints why configurations were re-run
   // and where the time went
   static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
@@ -1777,8 +1772,8 @@ std::string sweepResultJson(const SweepResult &r, const std::string &file) {
   o += "{\"races\":[";
   char num[24];
   auto put = [&](int64_t v) {
-    const int n = std::snprintf(num, sizeof num, "%" PRId64, v);
-    o.append(num, static_cast<size_t>(n));
+    const auto res = std::to_chars(num, num + sizeof num, v);
+    o.append(num, static_cast<size_t>(res.ptr - num));
   };
   auto loc = [&](const Loc &l) {
     o += "{\"file\":";
@@ -2012,11 +2007,13 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
   };
   static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
+  auto tJson = t0;
   std::vector<Job> jobs;
   try {
     JVal arr = JParse(jobsJson ? jobsJson : "[]").value();
     if (arr.kind != JVal::Arr)
       throw std::runtime_error("jobs: expected an array");
+    tJson = std::chrono::steady_clock::now();
     jobs.resize(arr.arr.size());
     for (size_t q = 0; q < arr.arr.size(); ++q) {
       const JVal *file = arr.arr[q].get("file");
@@ -2136,8 +2133,8 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     auto us = [](auto a, auto b) {
       return std::chrono::duration<double, std::micro>(b - a).count();
     };
-    std::fprintf(stderr, "[hgrd many] %zu jobs: parse+compile %.0f run %.0f report %.0f (us)\n",
-                 jobs.size(), us(t0, t1), us(t1, t2),
+    std::fprintf(stderr, "[hgrd many] %zu jobs: json %.0f front end %.0f run %.0f report %.0f "
+                 "(us)\n", jobs.size(), us(t0, tJson), us(tJson, t1), us(t1, t2),
                  us(t2, std::chrono::steady_clock::now()));
   }
   return HGRD_GPU_OK;

@@ -765,6 +765,8 @@ def run_sweep_arm(args):
         t0 = time.perf_counter()
         got = step()
         times.append(time.perf_counter() - t0)
+        if os.environ.get("HGRD_SWEEP_TRACE"):
+            print(f"[bench step] {1e3 * times[-1]:.2f} ms", file=sys.stderr)
     clk = clocks.stop()
     got = parsed(got)
     assert [strip_extras(g)["races"] for g in got] == [w["races"] for w in want]

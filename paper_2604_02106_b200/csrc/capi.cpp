@@ -8,6 +8,8 @@
 #include "gpu_backend.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <memory>
 #include <vector>
@@ -63,10 +65,19 @@ int hgrd_gpu_enumerate_verdict_many_json(hgrd_gpu_ctx *ctx, const char *jobs_jso
                                          int world, char **out) {
   if (!ctx || !out)
     return HGRD_GPU_EINVAL;
-  SweepWorkers pool(ctx);
-  std::string s;
-  int rc = sweepManyJson(pool.getter(), pool.n, jobs_json, rank, world, s);
-  *out = dup(s);
+  static const bool trace = std::getenv("HGRD_SWEEP_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc;
+  {
+    SweepWorkers pool(ctx);
+    std::string s;
+    rc = sweepManyJson(pool.getter(), pool.n, jobs_json, rank, world, s);
+    *out = dup(s);
+  }
+  if (trace)
+    std::fprintf(stderr, "[hgrd many-call] %.0f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0)
+                     .count());
   return rc;
 }
 

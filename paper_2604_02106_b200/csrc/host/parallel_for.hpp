@@ -1,5 +1,5 @@
-// fn(i) for i < n on the host's threads (chunks of 64 indices; one thread
-// when n is small).  Host-side data parallelism of the sweep pipeline
+// fn(i) for i < n on the host's threads (chunks of up to 64 indices; one
+// thread when n < 2 x minPerThread).  Host-side data parallelism of the sweep pipeline
 // (speculated configurations, batch staging, merges).  The worker threads
 // persist for the process (thread creation would cost more than a sweep's
 // host phases); a call that finds the pool busy (another thread's
@@ -34,6 +34,8 @@ public:
       std::lock_guard<std::mutex> lk(mu_);
       body_ = &body;
       n_ = n;
+      // chunks small enough for every thread to get several
+      chunk_ = std::max<size_t>(1, std::min<size_t>(64, n / (4 * threads())));
       next_ = 0;
       active_ = workers_.size();
       ++gen_;
@@ -63,8 +65,8 @@ private:
       t.join();
   }
   void drain() {
-    for (size_t b; (b = next_.fetch_add(64)) < n_;)
-      for (size_t i = b; i < std::min(n_, b + 64); ++i)
+    for (size_t b; (b = next_.fetch_add(chunk_)) < n_;)
+      for (size_t i = b; i < std::min(n_, b + chunk_); ++i)
         (*body_)(i);
   }
   void loop() {
@@ -88,7 +90,7 @@ private:
   std::mutex busy_, mu_;
   std::condition_variable cv_, done_;
   const std::function<void(size_t)> *body_ = nullptr;
-  size_t n_ = 0;
+  size_t n_ = 0, chunk_ = 64;
   std::atomic<size_t> next_{0};
   size_t active_ = 0;
   uint64_t gen_ = 0;

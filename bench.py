@@ -1,26 +1,33 @@
 #!/usr/bin/env python
 """Race-check throughput on B200: access instances race-checked per second.
 
-Workload (BASELINE.json configs[1]): the synthetic 1D stencil with a
-per-block tile, 2^20 MiniCU threads in blocks of 256, warp size 32; one step
-checks BOTH variants of the config — the missing-barrier launch (4 racy keys)
-and the fixed one (clean) — i.e. 2 x 5 x 2^20 = 10,485,760 instances/step.
+Default workload: BASELINE.json configs[3], the largest config that fits one
+GPU — the global-memory histogram with data-dependent bins, 2^27 MiniCU
+threads (2^28 access instances per launch), 2^16 bins; one step checks the
+three update variants of SURVEY.md §8(d) row 4 (atomicAdd / atomicAdd_block /
+store) over the same 1 GiB data array.  --workload selects the other configs
+(stencil = configs[1], transpose = configs[2], permutation / histogram_2p24 =
+configs[3] variants, corpus = configs[0] and lattice = configs[4] sweeps).
 
-* ``value``: instances / device time of hgrd_gpu_check_launch with the launch
-  buffers already resident in HBM (CUDA events on the context's stream),
-  L2 flushed (256 MiB write) between steps.
-* ``e2e``: the same checks through the reference-facing entry point
-  (hgrd_gpu_run_concrete_json = hgrd::runConcrete): MiniCU source text in,
-  JSON race report out, wall clock; h2d/d2h bytes are the context's counted
-  host<->device copies per step (launch descriptors, counters, race records).
-* ``roofline``: dominant pipeline stage vs the measured HBM copy bandwidth,
-  algorithmic bytes = 32 B per instance.
+* ``value``: instances / device time of hgrd_gpu_check_launch (CUDA events on
+  the context's stream) with the inputs resident in HBM; L2 flushed (256 MiB
+  write) between steps (the data arrays exceed L2 too).
+* ``e2e``: the same checks through the C ABI with HOST buffers: every step
+  copies the host's input arrays from pinned memory (hgrd_gpu_buffer_write),
+  checks and reads the reports back (workloads without host data go through
+  hgrd_gpu_run_concrete_json: source text in, JSON out); wall clock.
+* ``roofline``: the dominant kernel vs the measured HBM copy bandwidth, with
+  SURVEY.md §8(d)'s algorithmic bytes (32 B per instance, +8 B per value-
+  consumed load: 36 B for the histogram) x the instances of one launch.
 * ``cpu_baseline``: the unmodified reference (oracle/_ref/libhgrd_ref.so,
-  hgrd::runConcrete) on this host's cores on a bounded sample.
+  hgrd::runConcrete) on every host thread on a bounded sample.
 
 --impl reference times that reference CPU implementation alone (rank 0).
-With --gpus N under torchrun every rank checks its own replica of the
-workload (weak scaling; the path has no cross-rank exchange for this config).
+--gpus N under torchrun: every rank checks its own independent launches (own
+data, no data-path collective: weak scaling); --shard-launch instead splits
+ONE launch of N x the per-GPU threads by whole-block ranges (INTER-BLOCK via
+an NCCL reduce-scatter, parallel.check_launch_sharded).  The sweep workloads
+shard their configurations by canonical index (strong scaling).
 """
 from __future__ import annotations
 
@@ -89,7 +96,7 @@ class Histogram(Workload):
     b_alg = 36  # 32 B per instance + 8 B per value-consumed load (1 per 2 instances)
     updates = ("atomic", "atomic_block", "store")
 
-    shardable = True  # --gpus N: one launch of N x n threads, whole-block ranges per rank
+    shardable = True  # --shard-launch: one launch of N x n threads, whole-block ranges per rank
 
     def __init__(self, n=1 << 27, bins=1 << 16):
         self.n, self.bins = n, bins
@@ -97,6 +104,12 @@ class Histogram(Workload):
                      f"block256_ws32_atomic+atomic_block+store")
         self.inst_per_launch = 2 * n
         self.world, self.rank = 1, 0
+        self.seed = programs.HIST_SEED
+
+    def independent(self, rank):
+        """--gpus N (default): rank r checks its own launches over its own
+        data (seed + r), independent units with no data-path collective."""
+        self.seed = programs.HIST_SEED + rank
 
     def shard(self, world, rank):
         """Weak scaling: the launch grows to world x n threads; this rank
@@ -107,17 +120,18 @@ class Histogram(Workload):
         self.inst_per_launch = 2 * self.n * world
 
     def program(self, n, upd, host_init):
-        return programs.histogram(n, self.bins, upd, host_init=host_init)
+        return programs.histogram(n, self.bins, upd, host_init=host_init, seed=self.seed)
 
     def data(self, n, lo=0, hi=None):
         """data[lo:hi] of an n-thread launch."""
         import numpy as np
         i = np.arange(lo, n if hi is None else hi, dtype=np.int64)
-        return (i * programs.HIST_MULT + programs.HIST_SEED) % self.bins
+        return (i * programs.HIST_MULT + self.seed) % self.bins
 
     def expected(self, upd):
         if self.bins & (self.bins - 1) == 0 and self.bins >= 256:
-            return programs.histogram_pow2_expected(self.n * self.world, self.bins, upd)
+            return programs.histogram_pow2_expected(self.n * self.world, self.bins, upd,
+                                                    self.seed)
         return None
 
     def table(self):
@@ -156,6 +170,9 @@ class Permutation(Histogram):
     hit once except the injected duplicates (programs.PERM_DUPS)."""
 
     updates = ("store", "atomic_block")
+
+    def independent(self, rank):
+        pass  # (one fixed permutation: every rank checks the same launches)
     shardable = False  # (the permutation spans the whole launch: replicas)
 
     def __init__(self, n=1 << 27):
@@ -424,11 +441,13 @@ def run_gpu_arm(args):
     # whole-block ranges per rank (INTRA kinds rank-local; INTER-BLOCK through
     # an NCCL reduce-scatter of the block summaries, parallel.py); otherwise
     # every rank checks its own replica of the workload
-    sharded = use_dist and wl.shardable
+    sharded = use_dist and wl.shardable and args.shard_launch
     if sharded:
         from paper_2604_02106_b200.parallel import TorchComm, check_launch_sharded
         wl.shard(ws, rank)
         comm = TorchComm()
+    elif use_dist and hasattr(wl, "independent"):
+        wl.independent(rank)
 
     def pinned(a):
         t = torch.empty(a.size, dtype=torch.int64, pin_memory=True).numpy()
@@ -568,7 +587,8 @@ def run_gpu_arm(args):
                    "launches_per_step": len(launches),
                    "instances_per_step": wl.inst_per_launch * len(launches),
                    "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"blockshard{ws}" if sharded else f"replicas{ws}"},
+                   "parallelism": (f"blockshard{ws}" if sharded else
+                                   f"independent-launches{ws}" if use_dist else "1")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": wl.e2e_api},
         "gpu_launches": n_launch,
@@ -851,6 +871,10 @@ def main():
     ap.add_argument("--workload", default="histogram",
                     choices=sorted(WORKLOADS) + list(SWEEP_WORKLOADS),
                     help="BASELINE config to time (default: configs[3], the largest)")
+    ap.add_argument("--shard-launch", action="store_true",
+                    help="--gpus N: split ONE launch of N x the per-GPU threads by whole-block "
+                         "ranges (INTER-BLOCK through NCCL reduce-scatter) instead of "
+                         "independent launches per rank")
     ap.add_argument("--paths", action="store_true",
                     help="time the lock-idiom, SEQUENTIAL and sweep paths against the reference")
     args = ap.parse_args()

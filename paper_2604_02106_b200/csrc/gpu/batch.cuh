@@ -114,12 +114,12 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
     for (int i = tid; i < nKeys; i += NT)
       sKeyMin[i] = ~0u;
     for (int i = tid; i < BatchSmem::kTable; i += NT)
-      S.u.ch.head[i] = BatchSmem::kEnd;
+      S.u.ch.head[i] = 0; // (tag 0: empty; this launch pushes with tag 1)
     const uint32_t nThreads = static_cast<uint32_t>(sL.nThreads);
     if (tid == 0) {
-      S.count = R ? nThreads * R : 0;
-      S.hot = 0;
-      S.nReal = 0;
+      S.ic[0].count = R ? nThreads * R : 0;
+      S.ic[0].hot = 0;
+      S.ic[0].nReal = 0;
       S.flags = 0;
       sFlags = 0;
       sNRaces = 0;
@@ -133,6 +133,8 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
     unsigned flags = 0;
     for (uint32_t tl = tid; tl < nThreads; tl += NT) {
       FusedSink<BatchSmem> s;
+      s.ic = &S.ic[0];
+      s.htag = 1u << kHeadPosBits;
       s.L = &sL;
       s.sites = sSites;
       s.params = sParams;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
     }
     __syncthreads();
     if (tid == 0) {
-      if (S.count > static_cast<unsigned>(BatchSmem::kCap) || S.hot)
+      if (S.ic[0].count > static_cast<unsigned>(BatchSmem::kCap) || S.ic[0].hot)
         sFlags |= kFlagFusedOverflow; // (a hot element needs radix grouping: the host re-checks)
       sFlags |= S.flags;
       sTrapOff = 0;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
 
     // 2. per realised key: the first (x, y) pair of its minimum element
     if (ok) {
-      const unsigned nReal = S.nReal;
+      const unsigned nReal = S.ic[0].nReal;
       for (unsigned r = tid; r < nReal; r += NT) {
         const int K = static_cast<int>(sReal[r]);
         const int kind = K % 3;
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
         const uint32_t ge = sKeyMin[K];
         uint32_t mem[kSmallGroup + 1];
         int cnt = 0;
-        for (uint32_t q = S.u.ch.head[hashSlot<BatchSmem>(ge)];
+        for (uint32_t q = headPos(S.u.ch.head[hashSlot<BatchSmem>(ge)], 1u << kHeadPosBits);
              q != BatchSmem::kEnd && cnt <= kSmallGroup; q = S.u.ch.next[q])
           if (rElem(S.r0[q]) == ge)
             mem[cnt++] = q;

@@ -154,6 +154,7 @@ struct hgrd_gpu_ctx {
   bool e1AtSync = false; // e1 recorded at readCountersAndRaces' synchronisation
   bool e1Done = false;   // ... and no GPU work since: the check's end
   bool fusedOrdered = false; // the fused attempt saw traps / the step budget
+  bool fusedShardTables = false; // the fused check filled the shard's INTER tables
   std::vector<std::pair<const char *, std::chrono::steady_clock::time_point>> trace;
   hgrdgpu::jit::Cache *jit = nullptr;
   std::string jitErr;
@@ -889,8 +890,10 @@ int launchFused(hgrd_gpu_ctx *c, const FusedArgs &F, size_t smem, const void *ji
 // (hgrd_gpu_shard_*).
 int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobOffsets &o,
              const Plan &P, hgrd_gpu_result *R, uint32_t recInsns, bool loops,
-             JitGetter &jk, int64_t b0 = 0, int64_t b1 = -1, bool shard = false) {
+             JitGetter &jk, int64_t b0 = 0, int64_t b1 = -1, bool shard = false,
+             uint32_t *shardLo = nullptr, uint32_t *shardHi = nullptr) {
   c->fusedOrdered = false;
+  c->fusedShardTables = false;
   if (b1 < 0)
     b1 = D.nBlocks;
   const int nLocs = static_cast<int>(std::max<uint32_t>(L.n_locs, 1));
@@ -965,6 +968,11 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     anyOwn |= sd.record && sd.own;
   F.owner = (shard || F.interOnChip || !anyOwn) ? nullptr : c->owner.p;
   F.ownerRed = ownerRed;
+  if (shard && shardLo) { // the shard's (element, site) block min / max, from the records
+    F.shardLo = shardLo;
+    F.shardHi = shardHi;
+    F.nSitesTab = static_cast<int>(L.n_sites);
+  }
   F.epoch = c->epoch;
   F.keyElem = c->curKeyElem;
   F.cand = c->cand.p;
@@ -1014,6 +1022,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   R->instances = h.instances;
   R->records = h.records;
   R->mode = L.flags & ~HGRD_LAUNCH_SEQUENTIAL;
+  c->fusedShardTables = F.shardLo != nullptr;
   if (shard || !(h.flags & kFlagShared)) {
     if (fetchRaces(c, R) < 0) // (races read from the same synchronisation)
       return -1;
@@ -1763,23 +1772,27 @@ int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
   if (rc < 0)
     return rc;
   JitGetter jk = shardJit(c, L, S);
+  bool anyOwn = false;
+  for (const auto &s : S.P.sites)
+    anyOwn |= s.record && s.own;
+  const uint64_t nTab = S.P.totalW * static_cast<uint64_t>(L.n_sites);
+  if (anyOwn) { // the shard's INTER summary tables, filled by k_fused's records
+    NEED(c->shardLo, nTab);
+    NEED(c->shardHi, nTab);
+    CK(cudaMemsetAsync(c->shardLo.p, 0x7f, nTab * sizeof(uint32_t), c->st)); // kShardEmpty
+    CK(cudaMemsetAsync(c->shardHi.p, 0, nTab * sizeof(uint32_t), c->st));
+  }
   rc = runFused(c, L, S.D, S.o, S.P, R, S.recInsns, S.loops, jk, Sh->block_begin,
-                Sh->block_end, true);
+                Sh->block_end, true, anyOwn ? c->shardLo.p : nullptr,
+                anyOwn ? c->shardHi.p : nullptr);
   if (rc < 0)
     return rc;
   if (rc == 0) { // traps, step budget, overflow: the canonical order is needed
     c->err = "shard needs the ordered path (traps / step budget / capacity)";
     return HGRD_GPU_ENOTSUP;
   }
-  bool anyOwn = false;
-  for (const auto &s : S.P.sites)
-    anyOwn |= s.record && s.own;
-  if (anyOwn) { // INTER summary of this shard's blocks
-    const uint64_t n = S.P.totalW * static_cast<uint64_t>(L.n_sites);
-    NEED(c->shardLo, n);
-    NEED(c->shardHi, n);
-    CK(cudaMemsetAsync(c->shardLo.p, 0x7f, n * sizeof(uint32_t), c->st)); // kShardEmpty
-    CK(cudaMemsetAsync(c->shardHi.p, 0, n * sizeof(uint32_t), c->st));
+  if (anyOwn && !c->fusedShardTables) { // INTER summary of this shard's blocks (separate pass)
+    const uint64_t n = nTab;
     NEED(c->ctr2, 1);
     CK(cudaMemsetAsync(c->ctr2.p, 0, sizeof(Counters), c->st));
     LaunchDev Ds = S.D;
@@ -1803,9 +1816,11 @@ int shardCheck(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_shard *Sh,
     if (rc < 0)
       return rc;
     CK(cudaStreamSynchronize(c->st));
+  }
+  if (anyOwn) {
     Sh->inter_lo = c->shardLo.p;
     Sh->inter_hi = c->shardHi.p;
-    Sh->inter_n = n;
+    Sh->inter_n = nTab;
   }
   float ms = 0;
   if (c->timing) {

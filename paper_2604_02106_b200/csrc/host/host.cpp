@@ -2083,6 +2083,7 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     return rc;
   }
   const auto t2 = std::chrono::steady_clock::now();
+  const size_t nJobs = jobs.size();
   out = "[";
   for (size_t q = 0; q < jobs.size(); ++q) {
     Job &j = jobs[q];
@@ -2129,12 +2130,15 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
     }
   }
   out += "]";
+  // the jobs' programs and runs are freed off the caller's critical path
+  std::thread([j = std::move(jobs), r = std::move(runs), a = std::move(all)]() mutable {})
+      .detach();
   if (trace) {
     auto us = [](auto a, auto b) {
       return std::chrono::duration<double, std::micro>(b - a).count();
     };
     std::fprintf(stderr, "[hgrd many] %zu jobs: json %.0f front end %.0f run %.0f report %.0f "
-                 "(us)\n", jobs.size(), us(t0, tJson), us(tJson, t1), us(t1, t2),
+                 "(us)\n", nJobs, us(t0, tJson), us(tJson, t1), us(t1, t2),
                  us(t2, std::chrono::steady_clock::now()));
   }
   return HGRD_GPU_OK;

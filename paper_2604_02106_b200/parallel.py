@@ -206,9 +206,9 @@ def check_launch_sharded(ctx, spec, comm, device: int = 0) -> dict:
                 "records": res["records"], "mode": res["mode"], "ms": res["deviceMs"]}
     except NotShardable:
         res, sh, mine, stages = None, None, {"ok": False}, []
-    stats = comm.allgather(mine)
-    steps = sum(s.get("steps", 0) for s in stats)
-    if not all(s["ok"] for s in stats) or steps > spec.launch.step_budget:
+    import numpy as np
+    # every rank shardable? (one small MIN all-reduce instead of a gather)
+    if int(comm.allreduce_min_u64(np.array([1 if mine["ok"] else 0], np.uint64), device)[0]) == 0:
         out = ctx.check_launch(spec)  # replicas: the ordered path on every rank
         out["path"] = "replicas"
         return out
@@ -228,7 +228,13 @@ def check_launch_sharded(ctx, spec, comm, device: int = 0) -> dict:
     else:
         import numpy as np
         keys, vals = np.zeros(0, np.uint64), np.zeros(0, np.uint32)
-    parts = comm.allgather({"races": res["races"], "keys": keys, "vals": vals})
+    parts = comm.allgather({"races": res["races"], "keys": keys, "vals": vals, "stats": mine})
+    stats = [p["stats"] for p in parts]
+    steps = sum(s.get("steps", 0) for s in stats)
+    if steps > spec.launch.step_budget:  # the budget runs out: the ordered path decides
+        out = ctx.check_launch(spec)
+        out["path"] = "replicas"
+        return out
     best: Dict[tuple, dict] = {}
     for p in parts:  # INTRA: per key the minimum (element, x, y)
         for r in p["races"]:
@@ -237,7 +243,6 @@ def check_launch_sharded(ctx, spec, comm, device: int = 0) -> dict:
             if k not in best or o < best[k][0]:
                 best[k] = (o, r)
     races = [v[1] for v in best.values()]
-    import numpy as np
     all_keys = np.concatenate([p["keys"] for p in parts]) if parts else keys
     all_vals = np.concatenate([p["vals"] for p in parts]) if parts else vals
     if len(all_keys):

@@ -61,12 +61,12 @@ HIST_SEED = 0x5EED
 
 
 def histogram(n_threads: int, bins: int, update: str = "store", block: int = 256,
-              host_init: bool = True) -> str:
+              host_init: bool = True, seed: int = HIST_SEED) -> str:
     """Global-memory histogram with data-dependent bins:
     data[i] = (i*2654435761 + 0x5eed) % bins filled by a host loop, then
     `b = data[t]` and one update per thread.  With host_init=False the host
     loop is omitted and the caller fills `data` through the buffer API."""
-    init = (f"  for (int i = 0; i < {n_threads}; i++) {{ data[i] = (i * {HIST_MULT} + {HIST_SEED})"
+    init = (f"  for (int i = 0; i < {n_threads}; i++) {{ data[i] = (i * {HIST_MULT} + {seed})"
             f" % {bins}; }}\n") if host_init else ""
     return (
         "__global__ void h(int *data, int *hist) {\n"
@@ -80,11 +80,11 @@ def histogram(n_threads: int, bins: int, update: str = "store", block: int = 256
         f"  h<<<({n_threads // block},1,1),({block},1,1)>>>(data, hist); }}\n")
 
 
-def histogram_data(n_threads: int, bins: int):
+def histogram_data(n_threads: int, bins: int, seed: int = HIST_SEED):
     """Host-side contents of `data` for histogram(host_init=False)."""
     import numpy as np
     i = np.arange(n_threads, dtype=np.int64)
-    return (i * HIST_MULT + HIST_SEED) % bins
+    return (i * HIST_MULT + seed) % bins
 
 
 def synthetic_config(**over) -> Dict:
@@ -415,7 +415,8 @@ def permutation_expected(n_threads: int, update: str = "store", block: int = 256
     return [(k, *best[k]) for k in order if k in best]
 
 
-def histogram_pow2_expected(n_threads: int, bins: int, update: str = "store"):
+def histogram_pow2_expected(n_threads: int, bins: int, update: str = "store",
+                            seed: int = HIST_SEED):
     """The report of histogram(n_threads, bins, update) for power-of-two
     bins >= 256 (one block of 256 never repeats a bin: the multiplier is
     odd) and n_threads >= 2 * bins: only INTER-BLOCK pairs exist, the
@@ -426,7 +427,7 @@ def histogram_pow2_expected(n_threads: int, bins: int, update: str = "store"):
     assert bins >= 256 and bins & (bins - 1) == 0 and n_threads >= 2 * bins
     if update == "atomic":
         return []
-    i0 = (-HIST_SEED * pow(HIST_MULT, -1, bins)) % bins
+    i0 = (-seed * pow(HIST_MULT, -1, bins)) % bins
     return [("INTER-BLOCK", 0, i0, i0 + bins)]
 
 

@@ -12,6 +12,7 @@
 // (include/hgrd_gpu.h) so results are compared field by field.
 #include "hgrd/oracle.hpp"
 #include "hgrd/parser.hpp"
+#include "hgrd/report.hpp"
 
 #include <nlohmann/json.hpp>
 
@@ -150,6 +151,40 @@ double hgrd_ref_time_parallel(const char *src, const char *file,
   if (nRaces)
     *nRaces = found;
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// The reference's STATIC analyzer (analyzeProgram, src/report.cpp:82-211),
+// for the static-verdict cross-check (tests/crosscheck.py): its race
+// entries {kind, locA, locB, status} under AnalyzeOptions
+// {hostAnalysis, warpSize, domainBound, maxGrid, maxBlock} from optsJson.
+char *hgrd_ref_analyze(const char *src, const char *file, const char *optsJson) {
+  hgrd::ParseResult parsed = hgrd::parseTranslationUnit(src, file);
+  if (!parsed.ok())
+    return dupString(parseErrorJson(parsed).dump());
+  ordered_json o = ordered_json::parse(optsJson && *optsJson ? optsJson : "{}");
+  hgrd::AnalyzeOptions opts;
+  if (o.contains("hostAnalysis"))
+    opts.hostAnalysis = o["hostAnalysis"].get<bool>();
+  if (o.contains("warpSize"))
+    opts.warpSize = o["warpSize"].get<long long>();
+  if (o.contains("domainBound"))
+    opts.domainBound = o["domainBound"].get<long long>();
+  if (o.contains("maxGrid"))
+    opts.maxGrid = o["maxGrid"].get<long long>();
+  if (o.contains("maxBlock"))
+    opts.maxBlock = o["maxBlock"].get<long long>();
+  hgrd::RaceReport rep = hgrd::analyzeProgram(*parsed.program, opts);
+  ordered_json j;
+  j["races"] = ordered_json::array();
+  for (const auto &r : rep.races)
+    j["races"].push_back(ordered_json{
+        {"kind", hgrd::raceKindName(r.kind)},
+        {"locA", locJson(r.locA)},
+        {"locB", locJson(r.locB)},
+        {"array", r.array},
+        {"status", r.status == hgrd::RaceStatus::Race ? "race" : "undecided"}});
+  j["hadErrors"] = rep.hadErrors;
+  return dupString(j.dump());
 }
 
 // Bench reference arm of the sweep workloads (BASELINE config 5): every

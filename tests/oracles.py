@@ -37,12 +37,19 @@ class RefOracle:
         self.lib.hgrd_ref_enumerate_verdict.restype = ctypes.c_void_p
         self.lib.hgrd_ref_enumerate_verdict.argtypes = [ctypes.c_char_p] * 3
         self.lib.hgrd_ref_free.argtypes = [ctypes.c_void_p]
+        self.lib.hgrd_ref_analyze.restype = ctypes.c_void_p
+        self.lib.hgrd_ref_analyze.argtypes = [ctypes.c_char_p] * 3
         self.lib.hgrd_ref_time_sweeps.restype = ctypes.c_double
         self.lib.hgrd_ref_time_sweeps.argtypes = [ctypes.c_void_p] * 3 + [
             ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         self.lib.hgrd_ref_time_parallel.restype = ctypes.c_double
         self.lib.hgrd_ref_time_parallel.argtypes = [ctypes.c_char_p] * 3 + [
             ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+
+    def analyze(self, source: str, opts=None, file_name: str = "prog.mcu") -> dict:
+        """The reference's static analyzer (analyzeProgram): race entries."""
+        return self._take(self.lib.hgrd_ref_analyze(source.encode(), file_name.encode(),
+                                                    _cfg(opts)))
 
     def time_sweeps(self, jobs, threads: int):
         """Wall seconds of enumerateVerdict over `jobs` [(source, file, caps)]

@@ -114,12 +114,12 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
     for (int i = tid; i < nKeys; i += NT)
       sKeyMin[i] = ~0u;
     for (int i = tid; i < BatchSmem::kTable; i += NT)
-      S.u.ch.head[i] = 0; // (tag 0: empty; this launch pushes with tag 1)
+      S.u.ch.head[i] = BatchSmem::kEnd;
     const uint32_t nThreads = static_cast<uint32_t>(sL.nThreads);
     if (tid == 0) {
-      S.ic[0].count = R ? nThreads * R : 0;
-      S.ic[0].hot = 0;
-      S.ic[0].nReal = 0;
+      S.count = R ? nThreads * R : 0;
+      S.hot = 0;
+      S.nReal = 0;
       S.flags = 0;
       sFlags = 0;
       sNRaces = 0;
@@ -133,8 +133,6 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
     unsigned flags = 0;
     for (uint32_t tl = tid; tl < nThreads; tl += NT) {
       FusedSink<BatchSmem> s;
-      s.ic = &S.ic[0];
-      s.htag = 1u << kHeadPosBits;
       s.L = &sL;
       s.sites = sSites;
       s.params = sParams;
@@ -161,7 +159,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
       InterpBody::run(sL, sCode, bi, s, regs);
       for (uint32_t j = s.nrec; j < R; ++j)
         if (j * nThreads + tl < static_cast<uint32_t>(BatchSmem::kCap))
-          S.r0[j * nThreads + tl] = kNoRec;
+          S.rec[j * nThreads + tl].x = kNoRec;
       steps += static_cast<unsigned long long>(s.steps);
       inst += s.inst;
       traps += s.traps;
@@ -190,7 +188,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
     }
     __syncthreads();
     if (tid == 0) {
-      if (S.ic[0].count > static_cast<unsigned>(BatchSmem::kCap) || S.ic[0].hot)
+      if (S.count > static_cast<unsigned>(BatchSmem::kCap) || S.hot)
         sFlags |= kFlagFusedOverflow; // (a hot element needs radix grouping: the host re-checks)
       sFlags |= S.flags;
       sTrapOff = 0;
@@ -212,7 +210,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
 
     // 2. per realised key: the first (x, y) pair of its minimum element
     if (ok) {
-      const unsigned nReal = S.ic[0].nReal;
+      const unsigned nReal = S.nReal;
       for (unsigned r = tid; r < nReal; r += NT) {
         const int K = static_cast<int>(sReal[r]);
         const int kind = K % 3;
@@ -220,9 +218,9 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
         const uint32_t ge = sKeyMin[K];
         uint32_t mem[kSmallGroup + 1];
         int cnt = 0;
-        for (uint32_t q = headPos(S.u.ch.head[hashSlot<BatchSmem>(ge)], 1u << kHeadPosBits);
+        for (uint32_t q = S.u.ch.head[hashSlot<BatchSmem>(ge)];
              q != BatchSmem::kEnd && cnt <= kSmallGroup; q = S.u.ch.next[q])
-          if (rElem(S.r0[q]) == ge)
+          if (rElem(S.rec[q].x) == ge)
             mem[cnt++] = q;
         uint64_t bestX = ~0ull, bestY = ~0ull;
         int sX = 0, sY = 0;
@@ -230,7 +228,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
           return (static_cast<uint64_t>(rTli(r1)) << kSeqBits) | rSeq(r0);
         };
         for (int a = 0; a < cnt; ++a) {
-          const uint64_t a0 = S.r0[mem[a]], a1 = S.r1[mem[a]];
+          const uint64_t a0 = S.rec[mem[a]].x, a1 = S.rec[mem[a]].y;
           const int sa = rSite(a0);
           const int loa = sSites[sa].loc;
           if (loa != la && loa != lb)
@@ -241,7 +239,7 @@ __global__ void __launch_bounds__(kBatchThreads, 2) k_batch(BatchArgs A) {
           for (int b = 0; b < cnt; ++b) {
             if (b == a)
               continue;
-            const uint64_t b0 = S.r0[mem[b]], b1 = S.r1[mem[b]];
+            const uint64_t b0 = S.rec[mem[b]].x, b1 = S.rec[mem[b]].y;
             const uint64_t ob = order(b0, b1);
             if (ob <= oa)
               continue; // y follows x in event order

@@ -211,31 +211,17 @@ template <int NT, int IPT> struct FusedSmem {
       uint32_t sidx[kCap];  // sorted position -> record index
     } rx;
   } u;
-  uint64_t r0[kCap]; // site | seq | elem, by record index
-  uint64_t r1[kCap]; // tli | blk | bp | wp | warp
+  // records by index, {r0, r1} interleaved so a record is one 16-byte
+  // shared-memory store: r0 = site | seq | elem, r1 = tli | blk | bp | wp | warp
+  ulonglong2 rec[kCap];
   uint32_t minE[kMaxWritten], maxE[kMaxWritten];
-  // per-iteration counters, double-buffered by iteration parity: the next
-  // iteration's set is reset while this one runs (no extra barrier)
-  struct Iter {
-    unsigned int count, maxBp, maxWp, nReal, hot;
-  } ic[2];
-  unsigned int flags, needReset;
+  unsigned int count, maxBp, maxWp, nReal, flags, hot;
   // radix mode: field start bits of the key  w|off|blk|bp|warp|wp|lane
   int fWp, fWarp, fBp, fBlk, fOff, fW, total;
 };
 
 template <class Smem> __device__ __forceinline__ uint32_t hashSlot(uint32_t e) {
   return (e * 0x9E3779B1u) >> (32 - Smem::kLogTable);
-}
-
-// Hash chain heads carry the iteration's tag: tag:19 | record:13.  A head
-// whose tag is not the current iteration's is an empty slot, so the table
-// needs no reset between iterations (only every kTagPeriod iterations, and
-// after a radix-mode iteration overwrote it).  Tag 0 marks a reset slot.
-constexpr uint32_t kHeadPosBits = 13, kHeadPosMask = (1u << kHeadPosBits) - 1;
-constexpr uint32_t kTagPeriod = (1u << (32 - kHeadPosBits)) - 1;
-__device__ __forceinline__ uint32_t headPos(uint32_t h, uint32_t htag) {
-  return (h & ~kHeadPosMask) == htag ? (h & kHeadPosMask) : 0xffffffffu;
 }
 
 __device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa, int sb, int kind) {
@@ -250,13 +236,14 @@ __device__ __forceinline__ int keyIndex(const SiteDev *sites, int nLocs, int sa,
 
 // Keep the minimum `v` (element in hash mode, sorted position in radix
 // mode) per key; the first setter appends the key to the realised list.
-__device__ __forceinline__ void noteKey(unsigned &nReal, uint32_t *sKeyMin, uint32_t *sReal,
-                                        int K, uint32_t v) {
+template <class Smem>
+__device__ __forceinline__ void noteKey(Smem &S, uint32_t *sKeyMin, uint32_t *sReal, int K,
+                                        uint32_t v) {
   if (sKeyMin[K] <= v)
     return;
   const uint32_t old = atomicMin(&sKeyMin[K], v);
   if (old == ~0u) {
-    const unsigned slot = atomicAdd(&nReal, 1u);
+    const unsigned slot = atomicAdd(&S.nReal, 1u);
     sReal[slot] = static_cast<uint32_t>(K);
   }
 }
@@ -286,8 +273,6 @@ __device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_
 // elements.
 template <class Smem> struct FusedSink : ParState {
   Smem *S;
-  typename Smem::Iter *ic; // this iteration's counters
-  uint32_t htag;           // this iteration's chain-head tag (<< kHeadPosBits)
   uint32_t tli;      // thread index within the iteration
   uint32_t stride;   // fixed-slot mode: threads in the iteration
   uint32_t nrec = 0; // records produced by this thread
@@ -334,13 +319,13 @@ template <class Smem> struct FusedSink : ParState {
     const int myLoc = sites[site].loc;
     for (; q != Smem::kEnd; q = S->u.ch.next[q]) {
       if (++len > kSmallGroup) { // a hot element: radix grouping instead
-        ic->hot = 1;
+        S->hot = 1;
         break;
       }
-      const uint64_t q0 = S->r0[q];
+      const uint64_t q0 = S->rec[q].x;
       if (rElem(q0) != e)
         continue;
-      const uint64_t q1 = S->r1[q];
+      const uint64_t q1 = S->rec[q].y;
       const uint64_t *cf = conf;
       int kind;
       if (rBlk(q1) == myBlk) {
@@ -363,7 +348,7 @@ template <class Smem> struct FusedSink : ParState {
         la = lb;
         lb = t;
       }
-      noteKey(ic->nReal, keyMin, real, (la * nLocs + lb) * 3 + kind, e);
+      noteKey(*S, keyMin, real, (la * nLocs + lb) * 3 + kind, e);
     }
     if (own && shardLo) { // sharded check: the block joins (e, site)'s block range
       const uint64_t i = static_cast<uint64_t>(e) * nSitesTab + site;
@@ -399,7 +384,7 @@ template <class Smem> struct FusedSink : ParState {
       const int leader = __ffs(act) - 1;
       unsigned base = 0;
       if (ln == leader)
-        base = atomicAdd(&ic->count, static_cast<unsigned>(__popc(act)));
+        base = atomicAdd(&S->count, static_cast<unsigned>(__popc(act)));
       base = __shfl_sync(act, base, leader);
       pos = base + __popc(act & ((1u << ln) - 1));
     }
@@ -407,18 +392,17 @@ template <class Smem> struct FusedSink : ParState {
     if (pos < static_cast<unsigned>(Smem::kCap)) {
       const uint32_t e = static_cast<uint32_t>(elem);
       const uint64_t r1 = packR1(tli, myBlk, bp, wp, static_cast<uint32_t>(warp));
-      S->r0[pos] = packR0(site, seq, e);
-      S->r1[pos] = r1;
+      S->rec[pos] = make_ulonglong2(packR0(site, seq, e), r1); // one STS.128
       uint32_t *head = &S->u.ch.head[hashSlot<Smem>(e)];
       uint32_t h = *reinterpret_cast<volatile uint32_t *>(head);
       for (;;) {
-        S->u.ch.next[pos] = headPos(h, htag);
-        const uint32_t o = casAcqRel(head, h, htag | pos);
+        S->u.ch.next[pos] = h;
+        const uint32_t o = casAcqRel(head, h, pos);
         if (o == h)
           break;
         h = o;
       }
-      pairWithEarlier(e, r1, site, headPos(h, htag), own);
+      pairWithEarlier(e, r1, site, h, own);
     } else {
       flags |= kFlagFusedOverflow;
     }
@@ -557,11 +541,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
     sKeyMin[i] = ~0u;
     sKeyBound[i] = ~0u;
   }
-  for (int i = tid; i < Smem::kTable; i += kFusedThreads)
-    S.u.ch.head[i] = 0; // (tag 0: empty for every iteration)
   if (tid == 0) {
+    S.nReal = 0;
     S.flags = 0;
-    S.needReset = 0;
   }
   const uint32_t tpb = static_cast<uint32_t>(L.tpb);
   const int64_t ws = L.ws;
@@ -579,45 +561,28 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       sStageBase[0] = stageIssue(F, blockIdx.x, sStage, &sBar[0]);
   }
 
-  // iteration counters of the first iteration (later ones: reset one
-  // iteration ahead, below)
-  auto resetIter = [&](typename Smem::Iter &c, int64_t itx) {
-    const int64_t nbx =
-        min(static_cast<int64_t>(F.bpi), F.blockEnd - (F.blockBase + itx * F.bpi));
-    c.count = fixedR ? static_cast<unsigned>(nbx * L.tpb) * fixedR : 0;
-    c.maxBp = 0;
-    c.maxWp = 0;
-    c.hot = 0;
-    c.nReal = 0;
-  };
-  if (tid == 0 && static_cast<int64_t>(blockIdx.x) < F.nIters)
-    resetIter(S.ic[0], blockIdx.x);
-
-  int64_t k = 0; // this CTA's iteration count (staging buffer and counter set k & 1)
+  int64_t k = 0; // this CTA's iteration count (staging buffer k & 1)
   for (int64_t it = blockIdx.x; it < F.nIters; it += gridDim.x, ++k) {
     const int64_t firstBlock = F.blockBase + it * F.bpi;
     const int64_t nb = min(static_cast<int64_t>(F.bpi), F.blockEnd - firstBlock);
     __syncthreads();
     const int sb = static_cast<int>(k & 1);
-    typename Smem::Iter &IC = S.ic[sb];
-    const uint32_t tagIdx = static_cast<uint32_t>(k % kTagPeriod);
-    if (S.needReset || (tagIdx == 0 && k > 0)) { // (uniform: read after the barrier)
-      // a radix-mode iteration overwrote the chain heads, or the tags wrap
-      for (int i = tid; i < Smem::kTable; i += kFusedThreads)
-        S.u.ch.head[i] = 0;
-      __syncthreads();
-      if (tid == 0)
-        S.needReset = 0;
-    }
-    const uint32_t htag = (tagIdx + 1) << kHeadPosBits;
-    if (tid == 0 && it + gridDim.x < F.nIters) // the next iteration's counters
-      resetIter(S.ic[sb ^ 1], it + gridDim.x); // (its previous users passed the barrier)
     if (streamed) { // prefetch the next iteration's values, then wait for this one's
       if (tid == 0 && it + gridDim.x < F.nIters)
         sStageBase[sb ^ 1] =
             stageIssue(F, it + gridDim.x, sStage + (sb ^ 1) * F.stageCap, &sBar[sb ^ 1]);
       mbarWait(&sBar[sb], static_cast<unsigned>((k >> 1) & 1));
     }
+    if (tid == 0) {
+      S.count = fixedR ? static_cast<unsigned>(nb * L.tpb) * fixedR : 0;
+      S.maxBp = 0;
+      S.maxWp = 0;
+      S.hot = 0;
+      S.nReal = 0; // (every thread read it after the previous iteration's barrier)
+    }
+    for (int i = tid; i < Smem::kTable; i += kFusedThreads)
+      S.u.ch.head[i] = Smem::kEnd;
+    __syncthreads();
     // 1. expansion of the iteration's whole MiniCU blocks: records pushed
     //    per hash slot and paired as they are produced (FusedSink)
     if (!(F.ablate & 8)) {
@@ -628,8 +593,6 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.sites = sSites;
         s.params = sParams;
         s.S = &S;
-        s.ic = &IC;
-        s.htag = htag;
         s.tli = static_cast<uint32_t>(tl);
         s.R = fixedR;
         s.stride = static_cast<uint32_t>(nb * L.tpb);
@@ -656,7 +619,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         Body::run(L, sCode, bi, s, regs);
         for (uint32_t j = s.nrec; j < s.R; ++j)
           if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))
-            S.r0[j * s.stride + s.tli] = kNoRec;
+            S.rec[j * s.stride + s.tli].x = kNoRec;
         tally.add(s);
         myBp = max(myBp, s.bp);
         myWp = max(myWp, s.wp);
@@ -667,19 +630,19 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         myWp = max(myWp, __shfl_down_sync(0xffffffffu, myWp, o));
       }
       if ((tid & 31) == 0 && (myBp | myWp)) {
-        atomicMax(&IC.maxBp, myBp);
-        atomicMax(&IC.maxWp, myWp);
+        atomicMax(&S.maxBp, myBp);
+        atomicMax(&S.maxWp, myWp);
       }
     }
     __syncthreads();
-    const unsigned n = min(IC.count, static_cast<unsigned>(Smem::kCap));
-    if (IC.count > static_cast<unsigned>(Smem::kCap))
+    const unsigned n = min(S.count, static_cast<unsigned>(Smem::kCap));
+    if (S.count > static_cast<unsigned>(Smem::kCap))
       myFlags |= kFlagFusedOverflow;
     if (n == 0)
       continue;
     if (F.ablate & 1)
       continue;
-    const bool hashed = IC.hot == 0;
+    const bool hashed = S.hot == 0;
     if (!hashed && F.interOnChip) { // radix grouping has no INTER level: general path
       myFlags |= kFlagFusedOverflow;
       continue;
@@ -687,19 +650,17 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
     if (!hashed) {
       // radix mode for this iteration: drop the hash-mode keys, sort by
       // w | off | blk | bp | warp | wp | lane and summarise per group
-      for (unsigned r = tid; r < IC.nReal; r += kFusedThreads)
+      for (unsigned r = tid; r < S.nReal; r += kFusedThreads)
         sKeyMin[sReal[r]] = ~0u;
       if (tid < kMaxWritten) {
         S.minE[tid] = ~0u;
         S.maxE[tid] = 0;
       }
       __syncthreads();
-      if (tid == 0) {
-        IC.nReal = 0;
-        S.needReset = 1; // the sort overwrites the chain heads (union)
-      }
+      if (tid == 0)
+        S.nReal = 0;
       for (unsigned i = tid; i < n; i += kFusedThreads) {
-        const uint64_t r0 = S.r0[i];
+        const uint64_t r0 = S.rec[i].x;
         if (r0 == kNoRec)
           continue;
         const int w = sParams[sSites[rSite(r0)].param].written - 1;
@@ -714,8 +675,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
             span = max(span, static_cast<uint64_t>(S.maxE[w] - S.minE[w]) + 1);
         const int bL = bitsForDev(static_cast<uint64_t>(ws < L.tpb ? ws : L.tpb));
         const int bW = bitsForDev(static_cast<uint64_t>((L.tpb + ws - 1) / ws));
-        const int bQ = bitsForDev(uint64_t(IC.maxWp) + 1);
-        const int bP = bitsForDev(uint64_t(IC.maxBp) + 1);
+        const int bQ = bitsForDev(uint64_t(S.maxWp) + 1);
+        const int bP = bitsForDev(uint64_t(S.maxBp) + 1);
         const int bBk = bitsForDev(static_cast<uint64_t>(F.bpi));
         const int bO = bitsForDev(span);
         const int bWr = bitsForDev(static_cast<uint64_t>(F.nW));
@@ -738,9 +699,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       for (int j = 0; j < IPT; ++j) {
         const unsigned i = static_cast<unsigned>(tid * IPT + j);
         vals[j] = i;
-        const uint64_t r0 = i < n ? S.r0[i] : kNoRec;
+        const uint64_t r0 = i < n ? S.rec[i].x : kNoRec;
         if (r0 != kNoRec) {
-          const uint64_t r1 = S.r1[i];
+          const uint64_t r1 = S.rec[i].y;
           const uint32_t blk = rBlk(r1), warp = rWarp(r1);
           const uint32_t tl = rTli(r1) - blk * tpb;
           const uint32_t lane = tl - warp * static_cast<uint32_t>(ws);
@@ -790,7 +751,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
               const int b = __ffsll(static_cast<long long>(mm)) - 1;
               mm &= mm - 1;
               if (min(mn[a], mn[b]) < max(mx[a], mx[b]))
-                noteKey(IC.nReal, sKeyMin, sReal, keyIndex(sSites, F.nLocs, a, b, kind),
+                noteKey(S, sKeyMin, sReal, keyIndex(sSites, F.nLocs, a, b, kind),
                         static_cast<uint32_t>(p));
             }
           }
@@ -808,8 +769,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
             g3 = k >> shLane;
           }
           const uint32_t ri = S.u.rx.sidx[q];
-          const int s = rSite(S.r0[ri]);
-          const uint64_t r1 = S.r1[ri];
+          const int s = rSite(S.rec[ri].x);
+          const uint64_t r1 = S.rec[ri].y;
           const uint32_t wq = rWarp(r1);
           const uint32_t tl = rTli(r1) - rBlk(r1) * tpb;
           note(p2, mn2, mx2, s, wq);
@@ -821,7 +782,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       __syncthreads();
     }
     // 2. witnesses of the keys realised in this iteration
-    const unsigned nReal = IC.nReal;
+    const unsigned nReal = S.nReal;
     for (unsigned r = tid; r < nReal; r += kFusedThreads) {
       const int K = static_cast<int>(sReal[r]);
       const int kind = K % 3;
@@ -836,7 +797,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         ge = v;
       } else {
         g0 = v;
-        ge = rElem(S.r0[S.u.rx.sidx[g0]]);
+        ge = rElem(S.rec[S.u.rx.sidx[g0]].x);
         const uint64_t g = S.u.rx.skey[g0] >> S.fOff;
         g1 = g0 + 1;
         while (g1 < n && (S.u.rx.skey[g1] >> S.fOff) == g)
@@ -854,10 +815,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       uint32_t mem[kSmallGroup + 1];
       int nm = 0;
       if (hashed) {
-        for (uint32_t q = headPos(S.u.ch.head[hashSlot<Smem>(ge)], htag);
-             q != Smem::kEnd && nm <= kSmallGroup;
+        for (uint32_t q = S.u.ch.head[hashSlot<Smem>(ge)]; q != Smem::kEnd && nm <= kSmallGroup;
              q = S.u.ch.next[q])
-          if (rElem(S.r0[q]) == ge)
+          if (rElem(S.rec[q].x) == ge)
             mem[nm++] = q;
       }
       const int cnt = hashed ? nm : static_cast<int>(g1 - g0);
@@ -870,7 +830,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       };
       // lexicographically first (x, y) over the element's racing pairs of K
       for (int a = 0; a < cnt; ++a) {
-        const uint64_t a0 = S.r0[rec(a)], a1 = S.r1[rec(a)];
+        const uint64_t a0 = S.rec[rec(a)].x, a1 = S.rec[rec(a)].y;
         const int sa = rSite(a0);
         const int loa = sSites[sa].loc;
         if (loa != la && loa != lb)
@@ -881,7 +841,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         for (int b = 0; b < cnt; ++b) {
           if (b == a)
             continue;
-          const uint64_t b0 = S.r0[rec(b)], b1 = S.r1[rec(b)];
+          const uint64_t b0 = S.rec[rec(b)].x, b1 = S.rec[rec(b)].y;
           const uint64_t ob = order(b0, b1);
           if (ob <= oa)
             continue; // y must follow x in event order

@@ -587,7 +587,12 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
     //    per hash slot and paired as they are produced (FusedSink)
     if (!(F.ablate & 8)) {
       unsigned myBp = 0, myWp = 0;
-      for (int64_t tl = tid; tl < nb * L.tpb; tl += kFusedThreads) {
+      // (iteration invariants hoisted; an iteration holds < 2^16 MiniCU threads)
+      const uint32_t nT = static_cast<uint32_t>(nb * L.tpb);
+      const int64_t *stageBuf = streamed ? sStage + sb * F.stageCap : nullptr;
+      const int64_t stageB = streamed ? sStageBase[sb] : 0;
+      const int64_t firstThread = firstBlock * L.tpb;
+      for (uint32_t tl = tid; tl < nT; tl += kFusedThreads) {
         FusedSink<Smem> s;
         s.L = &L;
         s.sites = sSites;
@@ -595,8 +600,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.S = &S;
         s.tli = static_cast<uint32_t>(tl);
         s.R = fixedR;
-        s.stride = static_cast<uint32_t>(nb * L.tpb);
-        s.myBlk = L.dTpb.div(static_cast<uint32_t>(tl));
+        s.stride = nT;
+        s.myBlk = L.dTpb.div(tl);
         s.nLocs = F.nLocs;
         s.keyMin = sKeyMin;
         s.real = sReal;
@@ -610,12 +615,10 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.shardHi = F.shardHi;
         s.nSitesTab = F.nSitesTab;
         s.mine = static_cast<uint32_t>(firstBlock + s.myBlk + 1);
-        if (streamed) {
-          s.stage = sStage + sb * F.stageCap;
-          s.stageBase = sStageBase[sb];
-        }
+        s.stage = stageBuf;
+        s.stageBase = stageB;
         Builtins bi;
-        Body::identity(L, firstBlock * L.tpb + tl, bi, s.block, s.warp, s.lane);
+        Body::identity(L, firstThread + tl, bi, s.block, s.warp, s.lane);
         Body::run(L, sCode, bi, s, regs);
         for (uint32_t j = s.nrec; j < s.R; ++j)
           if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))

@@ -2084,14 +2084,16 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
   }
   const auto t2 = std::chrono::steady_clock::now();
   const size_t nJobs = jobs.size();
-  out = "[";
-  for (size_t q = 0; q < jobs.size(); ++q) {
+  // each job's report on host threads, then concatenated in job order
+  std::vector<std::string> parts(nJobs);
+  parallelFor(
+      nJobs,
+      [&](size_t q) {
     Job &j = jobs[q];
-    if (q)
-      out += ",";
+    std::string &part = parts[q];
     if (!j.error.empty()) {
-      out += j.error;
-      continue;
+      part = j.error;
+      return;
     }
     if (world == 1) { // the job's enumerateVerdict result
       SweepResult sr;
@@ -2112,7 +2114,7 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
             sr.races.push_back(SweepRace{race.locA, race.locB, race.kind, j.cfgs[k].warpSize});
         }
       }
-      out += sweepResultJson(sr, j.file);
+      part = sweepResultJson(sr, j.file);
     } else { // this rank's share (parallel.merge_shards combines them)
       SweepShard sh;
       sh.total = j.total;
@@ -2126,8 +2128,20 @@ int sweepManyJson(const std::function<LaunchBackend *(int)> &workers, int n,
         sh.stats.batchedLaunches += r.stats.batchedLaunches;
         sh.configs.push_back(ShardConfig{j.index[k], j.cfgs[k].warpSize, std::move(r.races)});
       }
-      out += sweepShardJson(sh, j.file);
+      part = sweepShardJson(sh, j.file);
     }
+      },
+      8);
+  size_t bytes = 2;
+  for (const std::string &p : parts)
+    bytes += p.size() + 1;
+  out.clear();
+  out.reserve(bytes);
+  out += "[";
+  for (size_t q = 0; q < nJobs; ++q) {
+    if (q)
+      out += ",";
+    out += parts[q];
   }
   out += "]";
   // the jobs' programs and runs are freed off the caller's critical path

@@ -63,7 +63,7 @@ __global__ void k_elem_keys_canon(const uint64_t *keys, const uint32_t *vals, ui
   const uint64_t lane = k & fieldMask(kl.bL);
   const uint64_t thread =
       block * static_cast<uint64_t>(tpb) + warp * static_cast<uint64_t>(ws) + lane;
-  elem[i] = (e << (bT + bS)) | (thread << bS) | (vals[i] & kSeqMask);
+  elem[i] = (e << (bT + bS)) | (thread << bS) | (vals[i] & seqMask(kl));
 }
 
 __global__ void k_shift_keys(uint64_t *x, uint64_t n, int sh) {
@@ -325,7 +325,8 @@ void phaseBounds(const hgrd_gpu_launch &L, int &bP, int &bQ, bool &bounded,
   }
 }
 
-bool makeLayout(KeyLayout &k, int bE, int bB, int bP, int bW, int bQ, int bL) {
+bool makeLayout(KeyLayout &k, int bE, int bB, int bP, int bW, int bQ, int bL, int nSites) {
+  k.bS = 32 - std::max(1, bitsFor(static_cast<uint64_t>(nSites)));
   k.bE = bE;
   k.bB = bB;
   k.bP = bP;
@@ -605,9 +606,6 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
   if (!append)
     CK(cudaMemsetAsync(&c->cur->nRaces, 0, sizeof(unsigned), c->st));
   DetectArgs A = detectArgs(c, L, D, o, n, kindMask);
-  (void)A;
-  {
-  }
   if (n > 1) {
     if (!pairwise) {
       NEED(c->keysAlt, n);
@@ -701,8 +699,9 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
         k_shift_keys<<<g, 256, 0, c->st>>>(dk.Current(), n, canonBits);
         CK(cudaGetLastError());
       }
-      NEED(c->keyPair, static_cast<size_t>(nKeys));
-      CK(cudaMemsetAsync(c->keyPair.p, 0xff, sizeof(unsigned long long) * nKeys, c->st));
+      NEED(c->keyPair, 2 * static_cast<size_t>(nKeys)); // first rows, then their y
+      CK(cudaMemsetAsync(c->keyPair.p, 0xff, 2 * sizeof(unsigned long long) * nKeys, c->st));
+      unsigned long long *keyY = c->keyPair.p + nKeys;
       {
         const uint32_t bigCap = 1u << 16; // (group start, end) pairs
         NEED(c->hot, 2 * bigCap + 1);
@@ -723,11 +722,13 @@ int detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev &D, const BlobOf
                                                  c->keyPair.p);
         k_detect_pairwise_big<<<c->nSM * 4, 256, 0, c->st>>>(A, D, dk.Current(), dv.Current(),
                                                              locks, lc, c->keyPair.p);
-        ++c->kernelLaunches;
+        k_pair_first_y<<<nKeys, 128, 0, c->st>>>(A, D, dk.Current(), dv.Current(), locks, lc,
+                                                 c->keyPair.p, keyY);
+        c->kernelLaunches += 2;
       }
       CK(cudaGetLastError());
       k_decode_pairwise<<<(nKeys + 127) / 128, 128, 0, c->st>>>(
-          A, dk.Current(), dv.Current(), c->keyPair.p, nKeys, c->curRaces, c->cur);
+          A, dk.Current(), dv.Current(), c->keyPair.p, keyY, nKeys, c->curRaces, c->cur);
       CK(cudaGetLastError());
       c->kernelLaunches += 3;
     }
@@ -742,9 +743,7 @@ int fetchRaces(hgrd_gpu_ctx *c, hgrd_gpu_result *R) {
   if (c->hCtr->flags & (kFlagLockSet | kFlagSegment)) {
     c->err = (c->hCtr->flags & kFlagLockSet)
                  ? std::string("pairwise detector limit exceeded: a lock set of more than 8 locks")
-                 : "pairwise detector limit exceeded: an element of more than " +
-                       std::to_string(kPairGroupMax - 1) + " events or more than " +
-                       std::to_string(kPairEventsMax - 1) + " events in total";
+                 : std::string("pairwise detector limit exceeded: 2^32 or more events");
     return HGRD_GPU_ENOTSUP;
   }
   const unsigned nr = c->hCtr->nRaces;
@@ -1127,7 +1126,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   }
   int bP = D.kl.bP, bQ = D.kl.bQ;
   for (int attempt = 0; attempt < 8; ++attempt) {
-    if (!makeLayout(D2.kl, D.kl.bE, D.kl.bB, bP, D.kl.bW, bQ, D.kl.bL)) {
+    if (!makeLayout(D2.kl, D.kl.bE, D.kl.bB, bP, D.kl.bW, bQ, D.kl.bL, D.nSites)) {
       c->err = "packed record key wider than 64 bits";
       return HGRD_GPU_ENOTSUP;
     }
@@ -1435,7 +1434,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   for (const auto &s : P.sites) // bit 0: record, bit 1: ownership exchange
     jk.rec.push_back(static_cast<uint8_t>((s.record ? 1 : 0) | (s.own ? 2 : 0)));
   markStream(L, P.params, jk); // bit 2: streamed load
-  if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
+  if (fusedOk && makeLayout(D.kl, bE, bB, bP, bW, bQ, bL, D.nSites)) {
     rc = runFused(c, L, D, o, P, R, recInsns, loops, jk);
     if (rc < 0)
       return rc;
@@ -1446,7 +1445,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
   }
 
   for (int attempt = 0; attempt < 16; ++attempt) {
-    if (!makeLayout(D.kl, bE, bB, bP, bW, bQ, bL)) {
+    if (!makeLayout(D.kl, bE, bB, bP, bW, bQ, bL, D.nSites)) {
       c->err = "packed record key wider than 64 bits";
       return HGRD_GPU_ENOTSUP;
     }
@@ -1503,7 +1502,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
         continue;
       }
       if (h.flags & kFlagSeqSite) {
-        c->err = "more than 2^20 accesses in one thread";
+        c->err = "more than 2^" + std::to_string(D.kl.bS) + " accesses in one thread";
         return HGRD_GPU_ENOTSUP;
       }
       if (h.flags & kFlagOps) { // (cannot happen: static op count)
@@ -1619,7 +1618,7 @@ int checkLaunch(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, hgrd_gpu_result *R) {
       if (retry)
         continue;
       if (h.flags & kFlagSeqSite) {
-        c->err = "more than 2^20 accesses in one thread";
+        c->err = "more than 2^" + std::to_string(D.kl.bS) + " accesses in one thread";
         return HGRD_GPU_ENOTSUP;
       }
     }
@@ -1721,7 +1720,7 @@ int shardPrepare(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, int64_t b0, int64_t 
   const int bB = bitsFor(static_cast<uint64_t>(D.nBlocks));
   const int bW = bitsFor(static_cast<uint64_t>((D.tpb + D.ws - 1) / D.ws));
   const int bL = bitsFor(static_cast<uint64_t>(std::min<int64_t>(D.ws, D.tpb)));
-  if (!why && !makeLayout(D.kl, bE, bB, bP, bW, bQ, bL))
+  if (!why && !makeLayout(D.kl, bE, bB, bP, bW, bQ, bL, D.nSites))
     why = "packed record key wider than 64 bits";
   if (why) {
     c->err = std::string("not shardable: ") + why;

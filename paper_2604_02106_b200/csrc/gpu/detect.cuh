@@ -138,7 +138,7 @@ __global__ void k_detect_summary(DetectArgs A, uint32_t *keySeg) {
     const uint64_t k = A.keys[j];
     if ((k >> kl.shE) != elem)
       break;
-    const int s = static_cast<int>(A.vals[j] >> kSeqBits);
+    const int s = static_cast<int>(A.vals[j] >> kl.bS);
     if (!(lv2 | lv3)) { // INTER only (fused pass 2): the block level alone
       note(p1, mn1, mx1, s, static_cast<uint32_t>((k >> kl.shB) & mB));
       continue;
@@ -189,7 +189,7 @@ __global__ void k_detect_hot(DetectArgs A, uint32_t *keySeg) {
       const uint64_t k = A.keys[j];
       if ((k >> kl.shE) != elem)
         break;
-      note(p, mn, mx, static_cast<int>(A.vals[j] >> kSeqBits),
+      note(p, mn, mx, static_cast<int>(A.vals[j] >> kl.bS),
            static_cast<uint32_t>((k >> kl.shB) & mB));
     }
     uint64_t all = p;
@@ -234,7 +234,7 @@ __device__ __forceinline__ uint64_t eventOrder(const DetectArgs &A, uint64_t k, 
   const uint64_t lane = k & fieldMask(kl.bL);
   const uint64_t thread = block * static_cast<uint64_t>(A.tpb) +
                           warp * static_cast<uint64_t>(A.ws) + lane;
-  return (thread << kSeqBits) | (v & kSeqMask);
+  return (thread << kl.bS) | (v & seqMask(kl));
 }
 
 // Early stop of the prefix-wise INTER witness pass (fused pass 2b): for
@@ -259,7 +259,7 @@ __global__ void k_inter_done(const uint64_t *keys, const uint32_t *vals, uint64_
   auto order = [&](uint64_t k, uint32_t v) {
     const uint64_t thread = ((k >> kl.shB) & mB) * static_cast<uint64_t>(tpb) +
                             ((k >> kl.shW) & mW) * static_cast<uint64_t>(ws) + (k & mL);
-    return (thread << kSeqBits) | (v & kSeqMask);
+    return (thread << kl.bS) | (v & seqMask(kl));
   };
   uint64_t best = ~0ull; // earliest eligible event (order), its site and block
   int bs = -1;
@@ -268,7 +268,7 @@ __global__ void k_inter_done(const uint64_t *keys, const uint32_t *vals, uint64_
     const uint64_t k = keys[i];
     if (k == kl.sentinel || (k >> kl.shE) != e)
       continue;
-    const int s = static_cast<int>(vals[i] >> kSeqBits);
+    const int s = static_cast<int>(vals[i] >> kl.bS);
     const int loc = sites[s].loc;
     if (loc != la && loc != lb)
       continue;
@@ -298,7 +298,7 @@ __global__ void k_inter_done(const uint64_t *keys, const uint32_t *vals, uint64_
       const uint64_t k = keys[i];
       if (k == kl.sentinel || (k >> kl.shE) != e || ((k >> kl.shB) & mB) == bb)
         continue;
-      const int s = static_cast<int>(vals[i] >> kSeqBits);
+      const int s = static_cast<int>(vals[i] >> kl.bS);
       if (sites[s].loc != want || !((confInter[bs] >> s) & 1ull))
         continue;
       found = order(k, vals[i]) > best;
@@ -345,7 +345,7 @@ __global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
     uint64_t ge = j;
     uint64_t pres = 0;
     for (; ge < e && (A.keys[ge] >> gsh) == g; ++ge) {
-      const int st = static_cast<int>(A.vals[ge] >> kSeqBits);
+      const int st = static_cast<int>(A.vals[ge] >> kl.bS);
       const uint32_t id = levelId(kl, kind, A.keys[ge]);
       const uint64_t bit = 1ull << st;
       if (!(pres & bit)) {
@@ -356,7 +356,7 @@ __global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
       }
     }
     for (uint64_t x = j; x < ge; ++x) {
-      const int st = static_cast<int>(A.vals[x] >> kSeqBits);
+      const int st = static_cast<int>(A.vals[x] >> kl.bS);
       const int loc = A.sites[st].loc;
       if (loc != la && loc != lb)
         continue;
@@ -384,7 +384,7 @@ __global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
   const uint32_t idx = levelId(kl, kind, A.keys[bestI]);
   uint64_t bestY = ~0ull, yI = bestI;
   for (uint64_t y = bestG0; y < bestG1; ++y) {
-    const int st = static_cast<int>(A.vals[y] >> kSeqBits);
+    const int st = static_cast<int>(A.vals[y] >> kl.bS);
     if (!((bestPm >> st) & 1ull) || levelId(kl, kind, A.keys[y]) <= idx)
       continue;
     const uint64_t ord = eventOrder(A, A.keys[y], A.vals[y]);
@@ -398,13 +398,13 @@ __global__ void k_witness(DetectArgs A, const uint32_t *keySeg, int nKeys,
   o.loc_a = la;
   o.loc_b = lb;
   o.kind = kind;
-  o.site_x = static_cast<int32_t>(A.vals[bestI] >> kSeqBits);
-  o.site_y = static_cast<int32_t>(A.vals[yI] >> kSeqBits);
+  o.site_x = static_cast<int32_t>(A.vals[bestI] >> kl.bS);
+  o.site_y = static_cast<int32_t>(A.vals[yI] >> kl.bS);
   elementOf(A, elem, o.handle, o.index);
-  o.thread_x = static_cast<int64_t>(best >> kSeqBits);
-  o.seq_x = static_cast<int32_t>(best & kSeqMask);
-  o.thread_y = static_cast<int64_t>(bestY >> kSeqBits);
-  o.seq_y = static_cast<int32_t>(bestY & kSeqMask);
+  o.thread_x = static_cast<int64_t>(best >> kl.bS);
+  o.seq_x = static_cast<int32_t>(best & seqMask(kl));
+  o.thread_y = static_cast<int64_t>(bestY >> kl.bS);
+  o.seq_y = static_cast<int32_t>(bestY & seqMask(kl));
 }
 
 // INTER-BLOCK witness, one warp per key: the whole element segment is one
@@ -443,7 +443,7 @@ __global__ void k_witness_inter(DetectArgs A, const uint32_t *keySeg, int nKeys,
     mx[i] = 0;
   __syncwarp();
   for (uint64_t p = s + lane; p < e; p += 32) {
-    const int st = static_cast<int>(A.vals[p] >> kSeqBits);
+    const int st = static_cast<int>(A.vals[p] >> kl.bS);
     atomicMax(&mx[st], static_cast<uint32_t>((A.keys[p] >> kl.shB) & fieldMask(kl.bB)));
     atomicOr(&spres[wid], 1ull << st);
   }
@@ -452,7 +452,7 @@ __global__ void k_witness_inter(DetectArgs A, const uint32_t *keySeg, int nKeys,
   // x: earliest event with a partner in a later block
   uint64_t bx = ~0ull, bpm = 0, bxi = s;
   for (uint64_t p = s + lane; p < e; p += 32) {
-    const int st = static_cast<int>(A.vals[p] >> kSeqBits);
+    const int st = static_cast<int>(A.vals[p] >> kl.bS);
     const int loc = A.sites[st].loc;
     if (loc != la && loc != lb)
       continue;
@@ -489,7 +489,7 @@ __global__ void k_witness_inter(DetectArgs A, const uint32_t *keySeg, int nKeys,
   const uint32_t idx = static_cast<uint32_t>((A.keys[bxi] >> kl.shB) & fieldMask(kl.bB));
   uint64_t by = ~0ull, byi = bxi;
   for (uint64_t p = s + lane; p < e; p += 32) {
-    const int st = static_cast<int>(A.vals[p] >> kSeqBits);
+    const int st = static_cast<int>(A.vals[p] >> kl.bS);
     if (!((bpm >> st) & 1ull) ||
         static_cast<uint32_t>((A.keys[p] >> kl.shB) & fieldMask(kl.bB)) <= idx)
       continue;
@@ -514,13 +514,13 @@ __global__ void k_witness_inter(DetectArgs A, const uint32_t *keySeg, int nKeys,
   o.loc_a = la;
   o.loc_b = lb;
   o.kind = 0;
-  o.site_x = static_cast<int32_t>(A.vals[bxi] >> kSeqBits);
-  o.site_y = static_cast<int32_t>(A.vals[byi] >> kSeqBits);
+  o.site_x = static_cast<int32_t>(A.vals[bxi] >> kl.bS);
+  o.site_y = static_cast<int32_t>(A.vals[byi] >> kl.bS);
   elementOf(A, elem, o.handle, o.index);
-  o.thread_x = static_cast<int64_t>(bx >> kSeqBits);
-  o.seq_x = static_cast<int32_t>(bx & kSeqMask);
-  o.thread_y = static_cast<int64_t>(by >> kSeqBits);
-  o.seq_y = static_cast<int32_t>(by & kSeqMask);
+  o.thread_x = static_cast<int64_t>(bx >> kl.bS);
+  o.seq_x = static_cast<int32_t>(bx & seqMask(kl));
+  o.thread_y = static_cast<int64_t>(by >> kl.bS);
+  o.seq_y = static_cast<int32_t>(by & seqMask(kl));
 }
 
 // ---------------------------------------------------------------------------
@@ -726,70 +726,100 @@ __device__ __forceinline__ Ev decodeEv(const DetectArgs &A, uint64_t k, uint32_t
   e.wp = (k >> kl.shQ) & fieldMask(kl.bQ);
   e.lane = k & fieldMask(kl.bL);
   e.thread = e.block * static_cast<uint64_t>(A.tpb) + e.warp * static_cast<uint64_t>(A.ws) + e.lane;
-  e.site = static_cast<int>(v >> kSeqBits);
-  e.seq = static_cast<int>(v & kSeqMask);
+  e.site = static_cast<int>(v >> kl.bS);
+  e.seq = static_cast<int>(v & seqMask(kl));
   return e;
 }
 
 // Pairs of one element group (sorted by element, canonical order within),
 // the reference's detectRaces rule (:730-784) including lockOrdered.  The
-// first-found pair per key is the minimum of element | x | y, packed as
-// group start (24 bits) | x offset (20) | y offset (20).
-constexpr uint64_t kPairGroupMax = 1u << 20, kPairEventsMax = 1u << 24;
+// first-found pair per key is the minimum of (element, x, y): keyPair holds
+// the least group start << 32 | x offset (the group start orders elements),
+// and k_pair_first_y then finds the least y of that row with the key.
+constexpr uint64_t kPairEventsMax = 1ull << 32; // (u32 sort order)
 constexpr uint64_t kPairBig = 64; // larger groups: k_detect_pairwise_big
+
+// The key of pair (a = event x, b = event y), or -1 when it is no race:
+// one thread, two loads, covering atomics, separated phases or lock order.
+__device__ __forceinline__ int pairKey(const DetectArgs &A, const LaunchDev &L,
+                                       const uint32_t *order, bool locks, const LockC *lc,
+                                       const Ev &a, const SiteDev &sa, const LockC &ca,
+                                       uint64_t y, LockInfo &la, bool &laFull, bool &laWide,
+                                       LockInfo &lb) {
+  const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
+  if (a.thread == b.thread)
+    return -1;
+  const SiteDev sb = A.sites[b.site];
+  if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
+    return -1;
+  const bool sameBlock = a.block == b.block;
+  if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC &&
+      covers(sa.scope, sameBlock) && covers(sb.scope, sameBlock))
+    return -1;
+  if (sameBlock && a.bp != b.bp)
+    return -1;
+  const bool sameWarp = sameBlock && a.warp == b.warp;
+  if (sameWarp && a.wp != b.wp)
+    return -1;
+  if (locks) {
+    bool ordered;
+    const LockC cb = lc ? lc[y] : LockC{};
+    if (lc && ca.cs[0] != kLockWide && cb.cs[0] != kLockWide) {
+      ordered = crossedC(ca.cs, cb.cs, sameBlock) || crossedC(ca.rel, cb.acq, sameBlock) ||
+                crossedC(cb.rel, ca.acq, sameBlock);
+    } else {
+      ordered = lockPairOrdered(L, a, b, sameBlock, la, laFull, laWide, lb);
+    }
+    if (ordered)
+      return -1;
+  }
+  const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
+  int l0 = sa.loc, l1 = sb.loc;
+  if (l1 < l0) {
+    const int t = l0;
+    l0 = l1;
+    l1 = t;
+  }
+  return (l0 * A.nLocs + l1) * 3 + kind;
+}
 
 __device__ __forceinline__ void pairRow(const DetectArgs &A, const LaunchDev &L,
                                         const uint32_t *order, bool locks, const LockC *lc,
                                         uint64_t i, uint64_t e, uint64_t x,
-                                        unsigned long long *keyPair, unsigned &flags) {
+                                        unsigned long long *keyPair) {
   LockInfo la, lb;
   const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
   const SiteDev sa = A.sites[a.site];
-  LockC ca{};
+  const LockC ca = locks && lc ? lc[x] : LockC{};
   bool laFull = false, laWide = false;
-  if (locks && lc)
-    ca = lc[x];
+  const unsigned long long packed = (static_cast<unsigned long long>(i) << 32) | (x - i);
   for (uint64_t y = x + 1; y < e; ++y) {
-    const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
-    if (a.thread == b.thread)
-      continue;
-    const SiteDev sb = A.sites[b.site];
-    if (sa.kind == HGRD_SITE_LOAD && sb.kind == HGRD_SITE_LOAD)
-      continue;
-    const bool sameBlock = a.block == b.block;
-    if (sa.kind == HGRD_SITE_ATOMIC && sb.kind == HGRD_SITE_ATOMIC &&
-        covers(sa.scope, sameBlock) && covers(sb.scope, sameBlock))
-      continue;
-    if (sameBlock && a.bp != b.bp)
-      continue;
-    const bool sameWarp = sameBlock && a.warp == b.warp;
-    if (sameWarp && a.wp != b.wp)
-      continue;
-    if (locks) {
-      bool ordered;
-      const LockC cb = lc ? lc[y] : LockC{};
-      if (lc && ca.cs[0] != kLockWide && cb.cs[0] != kLockWide) {
-        ordered = crossedC(ca.cs, cb.cs, sameBlock) || crossedC(ca.rel, cb.acq, sameBlock) ||
-                  crossedC(cb.rel, ca.acq, sameBlock);
-      } else {
-        ordered = lockPairOrdered(L, a, b, sameBlock, la, laFull, laWide, lb);
-      }
-      if (ordered)
-        continue;
-    }
-    const int kind = !sameBlock ? 0 : !sameWarp ? 1 : 2;
-    int l0 = sa.loc, l1 = sb.loc;
-    if (l1 < l0) {
-      int t = l0;
-      l0 = l1;
-      l1 = t;
-    }
-    const int K = (l0 * A.nLocs + l1) * 3 + kind;
-    const unsigned long long packed =
-        (static_cast<unsigned long long>(i) << 40) | ((x - i) << 20) | (y - i);
-    if (keyPair[K] > packed)
+    const int K = pairKey(A, L, order, locks, lc, a, sa, ca, y, la, laFull, laWide, lb);
+    if (K >= 0 && keyPair[K] > packed)
       atomicMin(&keyPair[K], packed);
   }
+}
+
+// keyY[K] = the least y offset of key K's first row (one CTA per key).
+__global__ void k_pair_first_y(DetectArgs A, LaunchDev L, const uint64_t *elemSorted,
+                               const uint32_t *order, bool locks, const LockC *lc,
+                               const unsigned long long *keyPair, unsigned long long *keyY) {
+  const int K = blockIdx.x;
+  const unsigned long long p = keyPair[K];
+  if (p == ~0ull)
+    return;
+  const uint64_t i = p >> 32, x = i + (p & 0xffffffffull);
+  const uint64_t elem = elemSorted[i];
+  LockInfo la, lb;
+  const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
+  const SiteDev sa = A.sites[a.site];
+  const LockC ca = locks && lc ? lc[x] : LockC{};
+  bool laFull = false, laWide = false;
+  for (uint64_t y = x + 1 + threadIdx.x; y < A.n && elemSorted[y] == elem; y += blockDim.x)
+    if (pairKey(A, L, order, locks, lc, a, sa, ca, y, la, laFull, laWide, lb) == K) {
+      atomicMin(&keyY[K], static_cast<unsigned long long>(y - i));
+      break;
+    }
 }
 
 // Lock facts of every event (sorted position x), once: lockInfoOf per pair
@@ -827,14 +857,14 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
     ++e;
   if (e - i < 2)
     return;
-  if (e - i >= kPairGroupMax || A.n >= kPairEventsMax) {
+  if (A.n >= kPairEventsMax) {
     atomicOr(&L.ctr->flags, static_cast<unsigned>(kFlagSegment));
     return;
   }
   if (A.nSites <= 64) { // no statically conflicting pair of the group's sites: skip
     uint64_t pres = 0;
     for (uint64_t x = i; x < e; ++x)
-      pres |= 1ull << (A.vals[order[x]] >> kSeqBits);
+      pres |= 1ull << (A.vals[order[x]] >> A.kl.bS);
     bool any = false;
     for (uint64_t rem = pres; rem && !any; rem &= rem - 1) {
       const int s = __ffsll(static_cast<long long>(rem)) - 1;
@@ -851,11 +881,8 @@ __global__ void k_detect_pairwise(DetectArgs A, LaunchDev L, const uint64_t *ele
       return;
     }
   }
-  unsigned flags = 0;
   for (uint64_t x = i; x < e; ++x)
-    pairRow(A, L, order, locks, lc, i, e, x, keyPair, flags);
-  if (flags)
-    atomicOr(&L.ctr->flags, flags);
+    pairRow(A, L, order, locks, lc, i, e, x, keyPair);
 }
 
 // The large groups listed by k_detect_pairwise, tiled like an n-body pass:
@@ -970,8 +997,7 @@ __global__ void __launch_bounds__(256) k_detect_pairwise_big(DetectArgs A, Launc
           l1 = t;
         }
         const int K = (l0 * A.nLocs + l1) * 3 + kind;
-        const unsigned long long packed = (static_cast<unsigned long long>(i) << 40) |
-                                          ((x - i) << 20) | (y0 + j - i);
+        const unsigned long long packed = (static_cast<unsigned long long>(i) << 32) | (x - i);
         if (keyPair[K] > packed)
           atomicMin(&keyPair[K], packed);
       }
@@ -984,7 +1010,8 @@ __global__ void __launch_bounds__(256) k_detect_pairwise_big(DetectArgs A, Launc
 
 __global__ void k_decode_pairwise(DetectArgs A, const uint64_t *elemSorted,
                                   const uint32_t *order,
-                                  const unsigned long long *keyPair, int nKeys,
+                                  const unsigned long long *keyPair,
+                                  const unsigned long long *keyY, int nKeys,
                                   hgrd_gpu_race *races, Counters *ctr) {
   const int K = blockIdx.x * blockDim.x + threadIdx.x;
   if (K >= nKeys)
@@ -992,8 +1019,8 @@ __global__ void k_decode_pairwise(DetectArgs A, const uint64_t *elemSorted,
   const unsigned long long p = keyPair[K];
   if (p == ~0ull)
     return;
-  const uint64_t s = p >> 40;
-  const uint64_t x = s + ((p >> 20) & 0xfffff), y = s + (p & 0xfffff);
+  const uint64_t s = p >> 32;
+  const uint64_t x = s + (p & 0xffffffffull), y = s + keyY[K];
   const Ev a = decodeEv(A, A.keys[order[x]], A.vals[order[x]]);
   const Ev b = decodeEv(A, A.keys[order[y]], A.vals[order[y]]);
   const unsigned pos = atomicAdd(&ctr->nRaces, 1u);

@@ -30,17 +30,19 @@ constexpr int kMaxRegs = 64;    // PARALLEL per-lane register file
 constexpr int kMaxSites = 64;   // summary detector site masks (u64)
 constexpr int kLaneBuf = 16;    // records buffered per lane per batch
 constexpr uint32_t kChunk = 4096; // records reserved per warp refill
-constexpr int kSeqBits = 20;    // val = site << 20 | seq
+// fused records (r0 seq field) and their thread << 20 | seq orders; the
+// general path's record values are site << KeyLayout::bS | seq instead
+constexpr int kSeqBits = 20;
 constexpr uint32_t kSeqMask = (1u << kSeqBits) - 1;
 constexpr int kMaxSiteId = 4095;
 
 enum CounterFlags : uint32_t {
   kFlagCapacity = 1u,   // record buffer too small
   kFlagPhase = 2u,      // a phase counter exceeded its key field
-  kFlagSeqSite = 4u,    // seq >= 2^20
+  kFlagSeqSite = 4u,    // seq >= 2^KeyLayout::bS
   kFlagAbort = 8u,      // step budget exhausted
   kFlagLockSet = 16u,   // lock-set scratch overflow (pairwise)
-  kFlagSegment = 32u,   // pairwise segment longer than 65535
+  kFlagSegment = 32u,   // pairwise: 2^32 or more events
   kFlagOps = 64u        // sync-op buffer too small
 };
 
@@ -62,6 +64,7 @@ struct SiteDev {
 
 struct KeyLayout {
   int bL, bQ, bW, bP, bB, bE;
+  int bS; // record value = site << bS | seq (32 - bits of the site count)
   int shQ, shW, shP, shB, shE;
   int total;
   uint64_t sentinel; // all-ones in `total` bits: never a valid key
@@ -205,6 +208,10 @@ __device__ __forceinline__ int bitsForDev(uint64_t n) { // bits to hold 0 .. n-1
 
 __device__ __forceinline__ uint64_t fieldMask(int bits) {
   return bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+}
+
+__host__ __device__ __forceinline__ uint32_t seqMask(const KeyLayout &kl) {
+  return (1u << kl.bS) - 1;
 }
 
 constexpr uint32_t kOwnerMulti = 0xFFFFFu; // block+1 field of an ownership word

@@ -240,12 +240,12 @@ struct ParSink : ParState {
     const uint64_t maskP = fieldMask(kl.bP), maskQ = fieldMask(kl.bQ);
     if (bp > maskP || wp > maskQ)
       flags |= kFlagPhase;
-    if (seq > kSeqMask)
+    if (seq > seqMask(kl))
       flags |= kFlagSeqSite;
     const uint64_t key = packKey(kl, e, static_cast<uint64_t>(block), bp & maskP,
                                  static_cast<uint64_t>(warp), wp & maskQ,
                                  static_cast<uint64_t>(lane));
-    const uint32_t val = (static_cast<uint32_t>(site) << kSeqBits) | (seq & kSeqMask);
+    const uint32_t val = (static_cast<uint32_t>(site) << kl.bS) | (seq & seqMask(kl));
     if (out->n < kLaneBuf) {
       out->k[out->n] = key;
       out->v[out->n] = val;
@@ -478,14 +478,14 @@ struct SeqSink {
       const uint64_t maskP = fieldMask(kl.bP), maskQ = fieldMask(kl.bQ);
       if (bp > maskP || wp > maskQ)
         flags |= kFlagPhase;
-      if (seq > kSeqMask)
+      if (seq > seqMask(kl))
         flags |= kFlagSeqSite;
       if (cursor < L->capacity) {
         L->keys[cursor] = packKey(kl, P->elemBase + static_cast<uint64_t>(idx),
                                   static_cast<uint64_t>(block), bp & maskP,
                                   static_cast<uint64_t>(warp), wp & maskQ,
                                   static_cast<uint64_t>(lane));
-        L->vals[cursor] = (static_cast<uint32_t>(site) << kSeqBits) | (seq & kSeqMask);
+        L->vals[cursor] = (static_cast<uint32_t>(site) << kl.bS) | (seq & seqMask(kl));
       } else {
         flags |= kFlagCapacity;
       }
@@ -550,14 +550,14 @@ struct SeqSink {
       const uint64_t maskP = fieldMask(kl.bP), maskQ = fieldMask(kl.bQ);
       if (bp > maskP || wp > maskQ)
         flags |= kFlagPhase;
-      if (seq > kSeqMask)
+      if (seq > seqMask(kl))
         flags |= kFlagSeqSite;
       if (cursor < L->capacity) {
         L->keys[cursor] = packKey(kl, base + static_cast<uint64_t>(idx),
                                   static_cast<uint64_t>(block), bp & maskP,
                                   static_cast<uint64_t>(warp), wp & maskQ,
                                   static_cast<uint64_t>(lane));
-        L->vals[cursor] = (static_cast<uint32_t>(site) << kSeqBits) | (seq & kSeqMask);
+        L->vals[cursor] = (static_cast<uint32_t>(site) << kl.bS) | (seq & seqMask(kl));
       } else {
         flags |= kFlagCapacity;
       }

@@ -192,6 +192,25 @@ __global__ void k_owner_any(const uint32_t *owner, uint64_t nElems, uint32_t epo
     atomicOr(&ctr->flags, static_cast<unsigned>(kFlagShared));
 }
 
+// A thread's ownership exchange in flight (exchange layout): its old value is
+// compared when the thread issues its next exchange or at the kernel's end,
+// so the L2 / HBM round trip overlaps the next MiniCU thread's expansion
+// instead of stalling this one.  A late MULTI mark is still a MULTI mark: any
+// later exchange of the element sees MULTI or another block and re-marks it.
+struct OwnerPend {
+  uint32_t *addr = nullptr;
+  uint32_t old = 0, mine = 0;
+  __device__ __forceinline__ void settle(uint32_t epochTag, unsigned &flags) {
+    if (addr) {
+      if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
+        atomicExch(addr, epochTag | kOwnerMulti);
+        flags |= kFlagShared;
+      }
+      addr = nullptr;
+    }
+  }
+};
+
 // NT threads x IPT records per thread of shared-memory record capacity.
 template <int NT, int IPT> struct FusedSmem {
   static constexpr int kThreads = NT;
@@ -288,6 +307,7 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
   bool ownerRed = false; // reduction layout of the ownership table (else exchange)
+  OwnerPend *pend = nullptr; // (exchange layout) the thread's exchange in flight
   uint32_t *shardLo = nullptr, *shardHi = nullptr; // sharded: (element, site) block min / max
   int nSitesTab = 0;
   // k_batch: every trap of the launch, keyed thread << 20 | n-th trap of the
@@ -359,11 +379,10 @@ template <class Smem> struct FusedSink : ParState {
       if (ownerRed) {
         ownerJoin(owner, e, epochTag, mine);
       } else {
-        const uint32_t old = atomicExch(&owner[e], epochTag | mine);
-        if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
-          atomicExch(&owner[e], epochTag | kOwnerMulti);
-          flags |= kFlagShared;
-        }
+        pend->settle(epochTag, flags);
+        pend->old = atomicExch(&owner[e], epochTag | mine);
+        pend->addr = &owner[e];
+        pend->mine = mine;
       }
     }
   }
@@ -553,6 +572,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   unsigned myFlags = 0;
   bool wroteCand = false; // this thread stored a candidate (released before the done count)
   int64_t regs[kMaxRegs];
+  OwnerPend pend;
   if (streamed && tid == 0) {
     mbarInit(&sBar[0], 1);
     mbarInit(&sBar[1], 1);
@@ -611,6 +631,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.owner = (F.ablate & 4) ? nullptr : F.owner;
         s.epochTag = F.epoch << 20;
         s.ownerRed = F.ownerRed != 0;
+        s.pend = &pend;
         s.shardLo = F.shardLo;
         s.shardHi = F.shardHi;
         s.nSitesTab = F.nSitesTab;
@@ -879,6 +900,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       }
     }
   }
+  pend.settle(F.epoch << 20, myFlags);
   // counters
   __syncthreads();
   const int lane = tid & 31;

@@ -507,3 +507,46 @@ def _overflow_programs() -> Dict[str, str]:
 
 
 OVERFLOW_PROGRAMS = _overflow_programs()
+
+
+def long_thread(n_acc: int, sites: int = 2) -> str:
+    """Thread 0 of one warp stores A[0 .. n_acc) (n_acc accesses, one site),
+    thread 1 then stores A[n_acc - 1]: an INTRA-WARP race whose first
+    witness is thread 0's access number n_acc - 1.  sites > 64 adds
+    per-thread private stores so the pairwise detector runs (more sites than
+    the summary detector's masks)."""
+    extra = "".join(f"  P[t * {sites} + {i}] = {i};\n" for i in range(max(0, sites - 2)))
+    return ("__global__ void k(int *A, int *P, int n) {\n"
+            "  int t = threadIdx.x;\n"
+            f"{extra}"
+            "  if (t == 0) {\n"
+            "    for (int i = 0; i < n; i++) {\n"
+            "      A[i] = i;\n"
+            "    }\n"
+            "  }\n"
+            "  if (t == 1) {\n"
+            "    A[n - 1] = 5;\n"
+            "  }\n"
+            "}\n"
+            f"void main() {{ int *A; int *P; cudaMalloc(&A, {n_acc}); cudaMalloc(&P, {2 * sites});\n"
+            f"  k<<<(1,1,1),(2,1,1)>>>(A, P, {n_acc}); }}\n")
+
+
+def wide_group(n_threads: int, block: int = 256) -> str:
+    """Every thread reads B[0] after thread 0 wrote it (one element group of
+    n_threads + 1 events) and stores 65 private elements (more sites than
+    the summary detector's 64-bit masks: the pairwise detector runs, with
+    66 * n_threads events).  Races: B[0] write / read at INTRA-WARP,
+    INTRA-BLOCK and INTER-BLOCK, first witnesses thread 0 against threads
+    1, 32 and `block`."""
+    stores = "".join(f"  A[t * 65 + {i}] = {i};\n" for i in range(65))
+    return ("__global__ void k(int *A, int *B) {\n"
+            "  int t = blockIdx.x * blockDim.x + threadIdx.x;\n"
+            "  if (t == 0) {\n"
+            "    B[0] = 7;\n"
+            "  }\n"
+            "  int r = B[0];\n"
+            f"{stores}"
+            "}\n"
+            f"void main() {{ int *A; int *B; cudaMalloc(&A, {65 * n_threads}); cudaMalloc(&B, 1);\n"
+            f"  k<<<({n_threads // block},1,1),({block},1,1)>>>(A, B); }}\n")

@@ -68,6 +68,28 @@ def test_xlarge(gpu):
         _check(gpu, c)
 
 
+def test_envelope(gpu, mode):
+    """Round-1 ENOTSUP limits, now exact: a thread of more than 2^20
+    accesses (record values site << bS | seq with bS = 32 - site bits), in
+    the summary and the pairwise detector."""
+    for c in load_golden("envelope"):
+        _check(gpu, c, "env.mcu")
+
+
+def test_wide_group_past_old_caps(gpu):
+    """The pairwise detector (66 sites) on an element group of 2^20 + 257
+    events and 2^26+ events in total (round 1: ENOTSUP past 2^20 / 2^24).
+    Same program as the envelope golden's wide_group_4096, which pins the
+    report: the races, their witnesses (thread 0 against 1, 32 and 256)
+    and 66 instances per thread are size-independent."""
+    small = next(c for c in load_golden("envelope") if c["name"] == "wide_group_4096")
+    n = (1 << 20) + 256
+    got = gpu.run_concrete(programs.wide_group(n), small["config"], "env.mcu")
+    assert strip_extras(got)["races"] == small["result"]["races"]
+    assert got["witnesses"] == small["witnesses_restatement"]
+    assert got["stats"]["instances"] == 66 * n + 1
+
+
 def test_lattice_config5(gpu):
     """BASELINE config 5: the reference's enumerateVerdict output for every
     program of the 10k-configuration lattice, through the batched sweep

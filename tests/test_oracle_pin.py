@@ -131,6 +131,14 @@ def test_regress_tiny_blocks(cpu_oracle):
         assert got["witnesses"] == c["witnesses_restatement"]
 
 
+def test_envelope_goldens(cpu_oracle):
+    """Long threads (> 2^20 accesses) and a wide pairwise group."""
+    for c in load_golden("envelope"):
+        got = cpu_oracle.run_concrete(c["source"], c["config"], "env.mcu")
+        assert strip_extras(got) == c["result"], c["name"]
+        assert got["witnesses"] == c["witnesses_restatement"]
+
+
 def test_structural_predictors_pinned():
     """programs.permutation_expected / histogram_pow2_expected (used by the
     2^27 GPU tests) reproduce the reference's reports at 2^20 / 2^22."""

@@ -183,6 +183,15 @@ int hgrd_gpu_buffers_reset(hgrd_gpu_ctx *ctx);
 int hgrd_gpu_buffer_alloc(hgrd_gpu_ctx *ctx, int64_t elems, int32_t *handle);
 int hgrd_gpu_buffer_write(hgrd_gpu_ctx *ctx, int32_t handle, int64_t offset,
                           int64_t count, const int64_t *src);
+/* hgrd_gpu_buffer_write on the context's copy stream: returns once the copy
+   is queued.  The copy starts after the work already queued on the context
+   (which may still read the buffer); the next check, read or write that
+   touches the buffer waits for it on the device, so uploading the next
+   batch overlaps the current check (B200-side addition: the reference keeps
+   its buffers in host memory).  src must stay valid until that point and
+   be pinned for the copy to run asynchronously. */
+int hgrd_gpu_buffer_write_async(hgrd_gpu_ctx *ctx, int32_t handle, int64_t offset,
+                                int64_t count, const int64_t *src);
 int hgrd_gpu_buffer_read(hgrd_gpu_ctx *ctx, int32_t handle, int64_t offset,
                          int64_t count, int64_t *dst);
 

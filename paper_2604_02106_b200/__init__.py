@@ -160,6 +160,7 @@ def load_library() -> ctypes.CDLL:
     lib.hgrd_gpu_buffers_reset.argtypes = [P]
     lib.hgrd_gpu_buffer_alloc.argtypes = [P, c_int64, ctypes.POINTER(c_int32)]
     lib.hgrd_gpu_buffer_write.argtypes = [P, c_int32, c_int64, c_int64, P]
+    lib.hgrd_gpu_buffer_write_async.argtypes = [P, c_int32, c_int64, c_int64, P]
     lib.hgrd_gpu_buffer_read.argtypes = [P, c_int32, c_int64, c_int64, P]
     lib.hgrd_gpu_check_launch.argtypes = [P, ctypes.POINTER(Launch), ctypes.POINTER(Result)]
     for fn in ("hgrd_gpu_run_concrete_json", "hgrd_gpu_enumerate_verdict_json"):
@@ -470,6 +471,16 @@ class GpuContext:
                                              array.ctypes.data)
         if rc:
             self._err("buffer_write", rc)
+
+    def write_async(self, handle: int, array, offset: int = 0):
+        """write() on the context's copy stream (hgrd_gpu_buffer_write_async):
+        returns at once; the next check that uses the buffer waits for the
+        copy on the device.  Keep `array` alive (and pinned, for overlap)
+        until then."""
+        rc = self._lib.hgrd_gpu_buffer_write_async(self._ctx, handle, offset, int(array.size),
+                                                   array.ctypes.data)
+        if rc:
+            self._err("buffer_write_async", rc)
 
     def read(self, handle: int, out, offset: int = 0):
         rc = self._lib.hgrd_gpu_buffer_read(self._ctx, handle, offset, int(out.size),

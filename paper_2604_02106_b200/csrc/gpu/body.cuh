@@ -80,6 +80,7 @@ __device__ __forceinline__ uint64_t elementAt(uint64_t base, int32_t idx) {
 
 struct InterpBody {
   static constexpr int kFixedR = -1; // records per thread not known at compile time
+  static constexpr bool kPair = false; // (no run2: one MiniCU thread per call)
   __device__ static __forceinline__ void identity(const LaunchDev &L, int64_t t, Builtins &b,
                                                   int64_t &block, int64_t &warp, int64_t &lane) {
     threadIdentity(L, t, b, block, warp, lane);

@@ -103,12 +103,17 @@ struct hgrd_gpu_ctx {
   int nSM = 148;
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // asynchronous uploads: copy stream, one event per upload in flight
+  cudaStream_t up = nullptr;
+  std::vector<cudaEvent_t> upEvents;
+  std::vector<int> upFree;
   std::string err;
 
   struct Buf {
     int64_t *p;
     int64_t elems;
     bool zeroPending; // allocated, zero-initialisation not yet materialised
+    int upload = -1;  // hgrd_gpu_buffer_write_async in flight: its upEvents slot
   };
   std::vector<Buf> bufs;
   // small allocations: bump arena over 256 MiB chunks; large: size-keyed cache
@@ -131,6 +136,7 @@ struct hgrd_gpu_ctx {
   DevVec<uint64_t> opStart;
   DevVec<hgrd_gpu_trap> traps;
   DevVec<uint32_t> owner;              // fused path: per-element ownership
+  bool ownerBits = false;              // owner last held the bit-map layout
   DevVec<uint32_t> shardLo, shardHi;   // sharded launches: INTER summary (min / max block)
   DevVec<uint32_t> hot;                // INTER detection: [0] count, then hot element starts
   DevVec<int> doneKeys;                // pass 2b early stop: per INTER key done flag, key id
@@ -354,9 +360,38 @@ struct Plan {
   bool summaryOk = true;
 };
 
+// A buffer's upload in flight (hgrd_gpu_buffer_write_async): the context
+// stream waits for it on the device before the next work that touches the
+// buffer; the host does not block.
+void awaitUpload(hgrd_gpu_ctx *c, int32_t h) {
+  auto &b = c->bufs[static_cast<size_t>(h)];
+  if (b.upload >= 0) {
+    cudaStreamWaitEvent(c->st, c->upEvents[static_cast<size_t>(b.upload)], 0);
+    c->upFree.push_back(b.upload);
+    b.upload = -1;
+  }
+}
+
+// Every upload a launch's buffers wait for (all of them when L is null).
+void awaitUploads(hgrd_gpu_ctx *c, const hgrd_gpu_launch *L) {
+  if (c->upFree.size() == c->upEvents.size())
+    return; // none in flight
+  if (!L) {
+    for (size_t h = 0; h < c->bufs.size(); ++h)
+      awaitUpload(c, static_cast<int32_t>(h));
+    return;
+  }
+  for (uint32_t p = 0; p < L->n_params; ++p) {
+    const int32_t h = L->param_handle[p];
+    if (h >= 0 && static_cast<size_t>(h) < c->bufs.size())
+      awaitUpload(c, h);
+  }
+}
+
 // A buffer's pending zero-initialisation, done before anything reads its
 // values (host reads and writes, value-needed loads, sequential launches).
 int materialize(hgrd_gpu_ctx *c, int32_t h) {
+  awaitUpload(c, h);
   auto &b = c->bufs[static_cast<size_t>(h)];
   if (b.zeroPending) {
     CK(cudaMemsetAsync(b.p, 0, static_cast<size_t>(b.elems) * 8, c->st));
@@ -934,19 +969,27 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   if (smem > 227 * 1024)
     return 0;
 
-  // ownership table (epoch-tagged, no memset between launches, device.cuh):
-  // reduction layout (two words per element) when it fits L2 comfortably,
-  // else the exchange layout (one word)
+  // ownership table (device.cuh): the reduction layout (two words per
+  // element, epoch-tagged: no memset between launches) when it fits L2
+  // comfortably, else the bit map (two bits per element, cleared per launch)
   static const char *redEnv = std::getenv("HGRD_OWNER_RED"); // A/B knob: 0 / 1 forces a layout
   const bool ownerRed = redEnv ? std::atoi(redEnv) != 0 : 8 * P.totalW <= (uint64_t(32) << 20);
-  const size_t ownerN = (ownerRed ? 2 : 1) * std::max<uint64_t>(P.totalW, 1);
+  const uint64_t nOwn = std::max<uint64_t>(P.totalW, 1);
+  const size_t ownerN = ownerRed ? 2 * nOwn : (nOwn + 15) / 16;
   const bool fresh = c->owner.cap < ownerN;
   NEED(c->owner, ownerN);
-  if (fresh || c->epoch >= 4094) {
-    CK(cudaMemsetAsync(c->owner.p, 0, c->owner.cap * sizeof(uint32_t), c->st));
-    c->epoch = 0;
+  if (ownerRed) {
+    // (a bit map leaves words that are no valid epoch tags: clear after one)
+    if (fresh || c->epoch >= 4094 || c->ownerBits) {
+      CK(cudaMemsetAsync(c->owner.p, 0, c->owner.cap * sizeof(uint32_t), c->st));
+      c->epoch = 0;
+      c->ownerBits = false;
+    }
+    ++c->epoch;
+  } else {
+    CK(cudaMemsetAsync(c->owner.p, 0, ownerN * sizeof(uint32_t), c->st));
+    c->ownerBits = true;
   }
-  ++c->epoch;
   const uint32_t candCap = 1u << 16;
   NEED(c->cand, candCap);
 
@@ -2456,6 +2499,8 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
   for (hgrd_gpu_ctx *w : c->workers)
     hgrd_gpu_destroy(w);
   cudaSetDevice(c->device);
+  if (c->up)
+    cudaStreamSynchronize(c->up);
   cudaStreamSynchronize(c->st);
   auto f = [](auto &v) {
     if (v.p)
@@ -2489,6 +2534,12 @@ void hgrd_gpu_destroy(hgrd_gpu_ctx *c) {
     cudaFree(c->batchBlob.p);
   hgrdgpu::jit::destroy(c->jit);
   for (cudaEvent_t e : c->evPool)
+    cudaEventDestroy(e);
+  if (c->up) {
+    cudaStreamSynchronize(c->up);
+    cudaStreamDestroy(c->up);
+  }
+  for (cudaEvent_t e : c->upEvents)
     cudaEventDestroy(e);
   cudaEventDestroy(c->e0);
   cudaEventDestroy(c->e1);
@@ -2549,6 +2600,7 @@ int hgrd_gpu_transfer_bytes(hgrd_gpu_ctx *c, unsigned long long *h2d, unsigned l
 int hgrd_gpu_buffers_reset(hgrd_gpu_ctx *c) {
   if (!c)
     return HGRD_GPU_EINVAL;
+  awaitUploads(c, nullptr); // (the memory is reused by later work on c->st)
   c->bufs.clear();
   c->chunkIdx = 0;
   c->chunkUsed = 0;
@@ -2618,6 +2670,42 @@ int hgrd_gpu_buffer_write(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n,
   return 0;
 }
 
+// The copy runs on the context's copy stream, after the work already queued
+// on the context stream (which may still read the buffer) and any zeroing;
+// later work touching the buffer waits for it on the device.
+int hgrd_gpu_buffer_write_async(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n,
+                                const int64_t *src) {
+  if (!c || h < 0 || static_cast<size_t>(h) >= c->bufs.size() || off < 0 || n < 0 ||
+      off + n > c->bufs[static_cast<size_t>(h)].elems || (n && !src))
+    return HGRD_GPU_EINVAL;
+  if (n == 0)
+    return 0;
+  CK(cudaSetDevice(c->device));
+  if (!c->up)
+    CK(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking));
+  if (off == 0 && n == c->bufs[static_cast<size_t>(h)].elems)
+    c->bufs[static_cast<size_t>(h)].zeroPending = false; // fully overwritten
+  if (materialize(c, h) < 0) // (also orders a previous upload of h on c->st)
+    return HGRD_GPU_ECUDA;
+  if (c->upFree.empty()) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->upEvents.push_back(e);
+    c->upFree.push_back(static_cast<int>(c->upEvents.size()) - 1);
+  }
+  const int slot = c->upFree.back();
+  c->upFree.pop_back();
+  cudaEvent_t ev = c->upEvents[static_cast<size_t>(slot)];
+  CK(cudaEventRecord(ev, c->st)); // the copy follows the context stream's queued work
+  CK(cudaStreamWaitEvent(c->up, ev, 0));
+  CK(cudaMemcpyAsync(c->bufs[static_cast<size_t>(h)].p + off, src, static_cast<size_t>(n) * 8,
+                     cudaMemcpyHostToDevice, c->up));
+  CK(cudaEventRecord(ev, c->up));
+  c->bufs[static_cast<size_t>(h)].upload = slot;
+  c->h2dBytes += static_cast<size_t>(n) * 8;
+  return 0;
+}
+
 int hgrd_gpu_buffer_read(hgrd_gpu_ctx *c, int32_t h, int64_t off, int64_t n, int64_t *dst) {
   if (!c || h < 0 || static_cast<size_t>(h) >= c->bufs.size() || off < 0 || n < 0 ||
       off + n > c->bufs[static_cast<size_t>(h)].elems || (n && !dst))
@@ -2645,6 +2733,7 @@ int hgrd_gpu_check_launch(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
     return HGRD_GPU_EINVAL;
   }
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, launch);
   return checkLaunch(c, *launch, result);
 }
 
@@ -2658,6 +2747,7 @@ int hgrd_gpu_shard_check(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, hgrd_gp
     return HGRD_GPU_EINVAL;
   }
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, launch);
   return shardCheck(c, *launch, shard, result);
 }
 
@@ -2669,6 +2759,7 @@ int hgrd_gpu_check_batch(hgrd_gpu_ctx *c, const hgrd_gpu_batch_launch *launches,
     if (!launches[i].buffer_elems && launches[i].n_buffers)
       return HGRD_GPU_EINVAL;
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, nullptr);
   try {
     return checkBatch(c, launches, n, results);
   } catch (const std::exception &e) {
@@ -2690,6 +2781,7 @@ int hgrd_gpu_shard_inter_scan(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, co
     return HGRD_GPU_EINVAL;
   }
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, launch);
   return shardInterScan(c, *launch, static_cast<const uint32_t *>(lo),
                         static_cast<const uint32_t *>(hi), elem_begin, n_elems, key_elem, n_keys);
 }
@@ -2706,6 +2798,7 @@ int hgrd_gpu_shard_inter_records(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
     return HGRD_GPU_EINVAL;
   }
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, launch);
   return shardInterRecords(c, *launch, shard, key_elem, n_keys, keys, vals, cap, n);
 }
 
@@ -2720,6 +2813,7 @@ int hgrd_gpu_shard_inter(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch,
     return HGRD_GPU_EINVAL;
   }
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, launch);
   return shardInter(c, *launch, shard, keys, vals, cap, n);
 }
 
@@ -2734,6 +2828,7 @@ int hgrd_gpu_shard_detect(hgrd_gpu_ctx *c, const hgrd_gpu_launch *launch, const 
     return HGRD_GPU_EINVAL;
   }
   CK(cudaSetDevice(c->device));
+  awaitUploads(c, launch);
   return shardDetect(c, *launch, keys, vals, n, result);
 }
 

@@ -214,22 +214,27 @@ __host__ __device__ __forceinline__ uint32_t seqMask(const KeyLayout &kl) {
   return (1u << kl.bS) - 1;
 }
 
-constexpr uint32_t kOwnerMulti = 0xFFFFFu; // block+1 field of an ownership word
+constexpr uint32_t kOwnerMulti = 0xFFFFFu; // filter-tag marker of the bit-map layout
 
 // Ownership table (the fused path's INTER-BLOCK filter), two layouts:
-// * exchange (one word per element): the block's first record of an
-//   element swaps in epoch:12 | block+1:20; whoever replaces another
-//   block's tag (or MULTI) stores MULTI (epoch | 0xFFFFF) — the final value
-//   is MULTI exactly for elements reached from two blocks;
+// * bit map (two bits per element, 16 elements per word): the block's first
+//   record of element e ORs e's "touched" bit; finding it already set means
+//   another block touched e (each block records e's first access once:
+//   k_fused's `first`), and the thread then ORs e's MULTI bit.  2 bits per
+//   element keep a 2^27-element table at 32 MiB, resident in L2 (the
+//   32-bit exchange table it replaced was 512 MiB of random DRAM
+//   read-modify-writes).  Cleared per launch (a memset of n / 4 bytes).  A
+//   block that records e twice (a chain walk cut short by radix mode) can
+//   only add a false MULTI, which pass 2 — exact on any superset of the
+//   shared elements — filters out.
 // * reduction (two words per element): hi = max(epoch | block+1) and
 //   lo = max(epoch | (0xFFFFF - (block+1))) — max and (complemented) min
 //   block, fire-and-forget RED.MAX with no round trip on the thread's
 //   critical path; MULTI iff both words carry the epoch and min != max.
-// Tables small enough for L2 use reductions; large ones the exchange (two
-// reductions per element on a table far larger than L2 cost more DRAM
-// round trips than they save).  Epoch tags: no memset between launches.
-// The filter tag tells the layouts apart: epoch << 20 | 0xFFFFF (exchange:
-// the MULTI value) or epoch << 20 (reduction).
+//   Epoch tags: no memset between launches.
+// Tables up to 4 Mi elements use reductions, larger ones the bit map.  The
+// filter tag tells the layouts apart: kOwnerMulti (bit map) or epoch << 20
+// (reduction).
 __device__ __forceinline__ void ownerJoin(uint32_t *owner, uint64_t e, uint32_t epochTag,
                                           uint32_t blockPlus1) {
   atomicMax(&owner[2 * e], epochTag | blockPlus1);
@@ -238,7 +243,7 @@ __device__ __forceinline__ void ownerJoin(uint32_t *owner, uint64_t e, uint32_t 
 __device__ __forceinline__ bool ownerIsMulti(const uint32_t *owner, uint64_t e,
                                              uint32_t filterTag) {
   if (filterTag & kOwnerMulti)
-    return owner[e] == filterTag;
+    return (owner[e >> 4] >> (2 * (e & 15) + 1)) & 1u;
   const uint2 w = *reinterpret_cast<const uint2 *>(owner + 2 * e);
   return (w.x >> 20) == (filterTag >> 20) && (w.y >> 20) == (filterTag >> 20) &&
          (w.x & kOwnerMulti) != kOwnerMulti - (w.y & kOwnerMulti);

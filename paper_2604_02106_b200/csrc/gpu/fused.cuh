@@ -15,8 +15,8 @@
 //      inside that element, published as a candidate (global element via
 //      atomicMin, candidates filtered by it; the last CTA keeps the
 //      lexicographically first pair of the minimum element).
-// INTER-BLOCK pairs need a second block: every (element, block) also does
-// one ownership exchange on a per-element table; an element reached from
+// INTER-BLOCK pairs need a second block: every (element, block) also joins
+// the element in the ownership table (device.cuh); an element reached from
 // two blocks becomes MULTI and only MULTI elements go through pass 2
 // (ctx.cu).
 #pragma once
@@ -57,7 +57,7 @@ struct FusedArgs {
   int64_t nIters;
   uint32_t *owner; // per element ownership word(s) (device.cuh)
   uint32_t epoch;
-  int ownerRed;    // reduction layout (two words per element), else exchange
+  int ownerRed;    // reduction layout (two words per element), else the bit map
   unsigned long long *keyElem;
   Candidate *cand;
   uint32_t candCap;
@@ -192,18 +192,19 @@ __global__ void k_owner_any(const uint32_t *owner, uint64_t nElems, uint32_t epo
     atomicOr(&ctr->flags, static_cast<unsigned>(kFlagShared));
 }
 
-// A thread's ownership exchange in flight (exchange layout): its old value is
-// compared when the thread issues its next exchange or at the kernel's end,
-// so the L2 / HBM round trip overlaps the next MiniCU thread's expansion
-// instead of stalling this one.  A late MULTI mark is still a MULTI mark: any
-// later exchange of the element sees MULTI or another block and re-marks it.
+// A thread's ownership OR in flight (bit-map layout, device.cuh): the old
+// word is examined when the thread issues its next OR or at the kernel's
+// end, so the L2 round trip overlaps the next MiniCU thread's expansion
+// instead of stalling this one.  (A late MULTI bit is still set before the
+// kernel ends, and only pass 2 reads it.)
 struct OwnerPend {
   uint32_t *addr = nullptr;
-  uint32_t old = 0, mine = 0;
-  __device__ __forceinline__ void settle(uint32_t epochTag, unsigned &flags) {
+  uint32_t old = 0, sh = 0; // old word, e's bit pair offset
+  __device__ __forceinline__ void settle(unsigned &flags) {
     if (addr) {
-      if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine) {
-        atomicExch(addr, epochTag | kOwnerMulti);
+      if ((old >> sh) & 1u) { // touched before by another block
+        if (!((old >> sh) & 2u))
+          atomicOr(addr, 2u << sh);
         flags |= kFlagShared;
       }
       addr = nullptr;
@@ -286,10 +287,10 @@ __device__ __forceinline__ uint32_t casAcqRel(uint32_t *p, uint32_t cmp, uint32_
 // paired with the records of its element pushed before it (every pair is
 // seen exactly once: by whichever of the two was pushed second).  The
 // block's first record of an element also joins the element's block range
-// in the ownership table (the INTER-BLOCK filter, device.cuh): an exchange,
-// or two fire-and-forget max reductions when the table fits L2.  Sites whose parameter is provably block-private (host
-// affine analysis, `own` = false) skip it: no other block can reach their
-// elements.
+// in the ownership table (the INTER-BLOCK filter, device.cuh): an OR into
+// the bit map, or two fire-and-forget max reductions when the table fits
+// L2.  Sites whose parameter is provably block-private (host affine
+// analysis, `own` = false) skip it: no other block can reach their elements.
 template <class Smem> struct FusedSink : ParState {
   Smem *S;
   uint32_t tli;      // thread index within the iteration
@@ -306,8 +307,8 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t *owner;      // per element ownership words (nullptr: ablated)
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
-  bool ownerRed = false; // reduction layout of the ownership table (else exchange)
-  OwnerPend *pend = nullptr; // (exchange layout) the thread's exchange in flight
+  bool ownerRed = false; // reduction layout of the ownership table (else the bit map)
+  OwnerPend *pend = nullptr; // (bit-map layout) the thread's OR in flight
   uint32_t *shardLo = nullptr, *shardHi = nullptr; // sharded: (element, site) block min / max
   int nSitesTab = 0;
   // k_batch: every trap of the launch, keyed thread << 20 | n-th trap of the
@@ -355,7 +356,7 @@ template <class Smem> struct FusedSink : ParState {
         kind = 0;
         cf = confX;
       } else {
-        continue; // INTER: the ownership exchange and pass 2
+        continue; // INTER: the ownership table and pass 2
       }
       if (kind < 0)
         continue;
@@ -379,10 +380,10 @@ template <class Smem> struct FusedSink : ParState {
       if (ownerRed) {
         ownerJoin(owner, e, epochTag, mine);
       } else {
-        pend->settle(epochTag, flags);
-        pend->old = atomicExch(&owner[e], epochTag | mine);
-        pend->addr = &owner[e];
-        pend->mine = mine;
+        pend->settle(flags);
+        pend->addr = &owner[e >> 4];
+        pend->sh = 2 * (e & 15);
+        pend->old = atomicOr(pend->addr, 1u << pend->sh);
       }
     }
   }
@@ -442,6 +443,12 @@ template <class Smem> struct FusedSink : ParState {
       recordE(site, elementAt(base, idx), own);
     ++seq;
     return need ? __ldg(params[param].ptr + idx) : 0;
+  }
+  // The value half of a value-needed loadC (JitBody::run2 issues both
+  // threads' fetches before either records): 0 when out of range, as loadC.
+  template <class I>
+  __device__ __forceinline__ int64_t fetchC(int param, I idx, int64_t size) const {
+    return outOfRange(idx, size) ? 0 : __ldg(params[param].ptr + idx);
   }
   // S variant: a streamed load (affine.hpp streamSites): idx is the MiniCU
   // thread's dense id plus a constant, so the iteration's values were staged
@@ -572,7 +579,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   unsigned myFlags = 0;
   bool wroteCand = false; // this thread stored a candidate (released before the done count)
   int64_t regs[kMaxRegs];
-  OwnerPend pend;
+  OwnerPend pend, pend2; // (pend2: the second thread of a JitBody::run2 pair)
   if (streamed && tid == 0) {
     mbarInit(&sBar[0], 1);
     mbarInit(&sBar[1], 1);
@@ -612,8 +619,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       const int64_t *stageBuf = streamed ? sStage + sb * F.stageCap : nullptr;
       const int64_t stageB = streamed ? sStageBase[sb] : 0;
       const int64_t firstThread = firstBlock * L.tpb;
-      for (uint32_t tl = tid; tl < nT; tl += kFusedThreads) {
-        FusedSink<Smem> s;
+      auto begin = [&](FusedSink<Smem> &s, uint32_t tl, OwnerPend *pd, Builtins &bi) {
         s.L = &L;
         s.sites = sSites;
         s.params = sParams;
@@ -631,22 +637,46 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.owner = (F.ablate & 4) ? nullptr : F.owner;
         s.epochTag = F.epoch << 20;
         s.ownerRed = F.ownerRed != 0;
-        s.pend = &pend;
+        s.pend = pd;
         s.shardLo = F.shardLo;
         s.shardHi = F.shardHi;
         s.nSitesTab = F.nSitesTab;
         s.mine = static_cast<uint32_t>(firstBlock + s.myBlk + 1);
         s.stage = stageBuf;
         s.stageBase = stageB;
-        Builtins bi;
         Body::identity(L, firstThread + tl, bi, s.block, s.warp, s.lane);
-        Body::run(L, sCode, bi, s, regs);
+      };
+      auto finish = [&](FusedSink<Smem> &s) {
         for (uint32_t j = s.nrec; j < s.R; ++j)
           if (j * s.stride + s.tli < static_cast<uint32_t>(Smem::kCap))
             S.rec[j * s.stride + s.tli].x = kNoRec;
         tally.add(s);
         myBp = max(myBp, s.bp);
         myWp = max(myWp, s.wp);
+      };
+      if constexpr (Body::kPair) { // MiniCU threads tl and tl + NT together (JitBody::run2)
+        for (uint32_t tl = tid; tl < nT; tl += 2 * kFusedThreads) {
+          FusedSink<Smem> s0, s1;
+          Builtins b0, b1;
+          begin(s0, tl, &pend, b0);
+          if (tl + kFusedThreads < nT) {
+            begin(s1, tl + kFusedThreads, &pend2, b1);
+            Body::run2(b0, s0, b1, s1);
+            finish(s0);
+            finish(s1);
+          } else {
+            Body::run(L, sCode, b0, s0, regs);
+            finish(s0);
+          }
+        }
+      } else {
+        for (uint32_t tl = tid; tl < nT; tl += kFusedThreads) {
+          FusedSink<Smem> s;
+          Builtins bi;
+          begin(s, tl, &pend, bi);
+          Body::run(L, sCode, bi, s, regs);
+          finish(s);
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -900,7 +930,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       }
     }
   }
-  pend.settle(F.epoch << 20, myFlags);
+  pend.settle(myFlags);
+  pend2.settle(myFlags);
   // counters
   __syncthreads();
   const int lane = tid & 31;

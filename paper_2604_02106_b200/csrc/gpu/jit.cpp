@@ -261,17 +261,17 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
   auto rangeAt = [&](uint32_t pc, uint16_t r) -> Range {
     return pc < ranges.size() && r < ranges[pc].size() ? ranges[pc][r] : Range{};
   };
-  // the access's index register as a 32-bit value when it and the buffer
-  // size fit (one unsigned compare bounds-checks it)
-  auto idxArg = [&](uint32_t pc, uint16_t r, int64_t site) -> std::string {
+  // the access's index register (register prefix R) as a 32-bit value when
+  // it and the buffer size fit (one unsigned compare bounds-checks it)
+  auto idxArg = [&](uint32_t pc, uint16_t r, int64_t site, const char *R) -> std::string {
     const size_t i = static_cast<size_t>(site);
     const int32_t p = i < L.n_sites ? L.sites[i].param : -1;
     const int64_t size = (p >= 0 && static_cast<size_t>(p) < params.size())
                              ? params[static_cast<size_t>(p)].size
                              : 0;
     if (rangeAt(pc, r).fits32() && size <= INT32_MAX)
-      return "static_cast<int32_t>(r" + std::to_string(r) + ")";
-    return "r" + std::to_string(r);
+      return "static_cast<int32_t>(" + std::string(R) + std::to_string(r) + ")";
+    return R + std::to_string(r);
   };
   // access -> literal arguments of the sink's C accessors: site, param,
   // record, own (rec[s]: bit 0 record, bit 1 ownership exchange), ... , size,
@@ -290,40 +290,41 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                             : JitParam{0, 0};
     return ", " + lit(jp.size) + ", " + std::to_string(jp.base) + "ULL";
   };
-  std::ostringstream o;
-  o << "#include \"jit_kernels.cuh\"\n"
-       "namespace hgrdgpu {\nnamespace dev {\n"
-       "struct JitBody {\n";
-  o << "  static constexpr int kFixedR = " << (loops ? 0 : nRec) << ";\n";
-  emitIdentity(o, L);
-  o << "  template <class Sink>\n"
-       "  __device__ static __forceinline__ void run(const LaunchDev &, const hgrd_gpu_insn *,\n"
-       "                                             const Builtins &bi, Sink &s, int64_t *) {\n";
-  for (uint32_t i = 0; i < L.n_regs; ++i)
-    o << "    int64_t r" << i << " = " << lit(L.reg_init ? L.reg_init[i] : 0) << ";\n";
-  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+  auto sizeLit = [&](int64_t s) {
+    const size_t i = static_cast<size_t>(s);
+    const int32_t p = i < L.n_sites ? L.sites[i].param : -1;
+    return lit((p >= 0 && static_cast<size_t>(p) < params.size())
+                   ? params[static_cast<size_t>(p)].size
+                   : 0);
+  };
+  auto streamed = [&](const hgrd_gpu_insn &I) {
+    return (I.sub & 1) && static_cast<size_t>(I.imm) < rec.size() &&
+           (rec[static_cast<size_t>(I.imm)] & 4);
+  };
+  // One instruction for registers R, builtins B and sink S.
+  auto insn = [&](std::ostringstream &o, uint32_t pc, const char *R, const char *B,
+                  const char *S) {
     const auto &I = L.code[pc];
-    if (target[pc])
-      o << "  L" << pc << ":;\n";
-    o << "    ";
+    const std::string r = R, sk = S;
+    auto reg = [&](uint16_t x) { return r + std::to_string(x); };
     switch (I.op) {
     case HGRD_OP_END:
       o << "return;";
       break;
     case HGRD_OP_STEP:
       if (noStepChecks)
-        o << "s.stepNC();";
+        o << sk << ".stepNC();";
       else
-        o << "if (!s.step(" << I.imm << ")) return;";
+        o << "if (!" << sk << ".step(" << I.imm << ")) return;";
       break;
     case HGRD_OP_CONST:
-      o << "r" << I.a << " = " << lit(I.imm) << ";";
+      o << reg(I.a) << " = " << lit(I.imm) << ";";
       break;
     case HGRD_OP_MOV:
-      o << "r" << I.a << " = r" << I.b << ";";
+      o << reg(I.a) << " = " << reg(I.b) << ";";
       break;
     case HGRD_OP_BUILTIN:
-      o << "r" << I.a << " = bi.v[" << int(I.sub) << "];";
+      o << reg(I.a) << " = " << B << ".v[" << int(I.sub) << "];";
       break;
     case HGRD_OP_BIN: {
       const Range rl = rangeAt(pc, I.b), rr = rangeAt(pc, I.c);
@@ -334,40 +335,41 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                           ((I.sub != HGRD_DIV && I.sub != HGRD_MOD) ||
                            (rr.lo == rr.hi && rr.lo != 0 && rr.lo != -1));
       if (narrow)
-        o << "r" << I.a << " = static_cast<int64_t>(static_cast<int32_t>(r" << I.b << ") "
-          << ops[I.sub] << " static_cast<int32_t>(r" << I.c << "));";
+        o << reg(I.a) << " = static_cast<int64_t>(static_cast<int32_t>(" << reg(I.b) << ") "
+          << ops[I.sub] << " static_cast<int32_t>(" << reg(I.c) << "));";
       else
-        o << "r" << I.a << " = applyBin(" << int(I.sub) << ", r" << I.b << ", r" << I.c << ");";
+        o << reg(I.a) << " = applyBin(" << int(I.sub) << ", " << reg(I.b) << ", " << reg(I.c)
+          << ");";
       break;
     }
     case HGRD_OP_LOAD:
-      if ((I.sub & 1) && static_cast<size_t>(I.imm) < rec.size() &&
-          (rec[static_cast<size_t>(I.imm)] & 4)) // streamed (staged) value-needed load
-        o << "r" << I.a << " = s.loadS(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm)
-          << buf(I.imm) << ");";
+      if (streamed(I)) // streamed (staged) value-needed load
+        o << reg(I.a) << " = " << sk << ".loadS(" << site(I.imm) << ", "
+          << idxArg(pc, I.b, I.imm, R) << buf(I.imm) << ");";
       else
-        o << "r" << I.a << " = s.loadC(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm) << ", "
-          << ((I.sub & 1) ? "true" : "false") << buf(I.imm) << ");";
+        o << reg(I.a) << " = " << sk << ".loadC(" << site(I.imm) << ", "
+          << idxArg(pc, I.b, I.imm, R) << ", " << ((I.sub & 1) ? "true" : "false")
+          << buf(I.imm) << ");";
       break;
     case HGRD_OP_STORE:
-      o << "s.storeC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm) << ", r" << I.b
-        << buf(I.imm) << ");";
+      o << sk << ".storeC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm, R) << ", "
+        << reg(I.b) << buf(I.imm) << ");";
       break;
     case HGRD_OP_ATOMIC:
-      o << "s.atomicC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm) << ", r" << I.b
-        << ", r" << I.c << buf(I.imm) << ");";
+      o << sk << ".atomicC(" << site(I.imm) << ", " << idxArg(pc, I.a, I.imm, R) << ", "
+        << reg(I.b) << ", " << reg(I.c) << buf(I.imm) << ");";
       break;
     case HGRD_OP_SYNCTHREADS:
-      o << "s.syncthreads();";
+      o << sk << ".syncthreads();";
       break;
     case HGRD_OP_SYNCWARP:
-      o << "s.syncwarp();";
+      o << sk << ".syncwarp();";
       break;
     case HGRD_OP_FENCE:
-      o << "s.fence(" << int(I.sub) << ");";
+      o << sk << ".fence(" << int(I.sub) << ");";
       break;
     case HGRD_OP_JZ:
-      o << "if (r" << I.a << " == 0) goto L" << I.imm << ";";
+      o << "if (" << reg(I.a) << " == 0) goto L" << I.imm << ";";
       break;
     case HGRD_OP_JMP:
       o << "goto L" << I.imm << ";";
@@ -375,9 +377,71 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
     default:
       o << "return;";
     }
+  };
+  // Two MiniCU threads per call (k_fused): branch-free bodies with no step
+  // checks interleave the threads instruction by instruction, and a
+  // value-needed global load fetches both threads' values before either
+  // records its access, so the two loads are in flight together (memory-level
+  // parallelism the per-thread interpretation order would serialise).
+  bool pairable = !loops && noStepChecks;
+  for (uint32_t pc = 0; pc < L.n_code && pairable; ++pc)
+    pairable = L.code[pc].op != HGRD_OP_JZ && L.code[pc].op != HGRD_OP_JMP;
+
+  std::ostringstream o;
+  o << "#include \"jit_kernels.cuh\"\n"
+       "namespace hgrdgpu {\nnamespace dev {\n"
+       "struct JitBody {\n";
+  o << "  static constexpr int kFixedR = " << (loops ? 0 : nRec) << ";\n";
+  o << "  static constexpr bool kPair = " << (pairable ? "true" : "false") << ";\n";
+  emitIdentity(o, L);
+  o << "  template <class Sink>\n"
+       "  __device__ static __forceinline__ void run(const LaunchDev &, const hgrd_gpu_insn *,\n"
+       "                                             const Builtins &bi, Sink &s, int64_t *) {\n";
+  for (uint32_t i = 0; i < L.n_regs; ++i)
+    o << "    int64_t r" << i << " = " << lit(L.reg_init ? L.reg_init[i] : 0) << ";\n";
+  for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+    if (target[pc])
+      o << "  L" << pc << ":;\n";
+    o << "    ";
+    insn(o, pc, "r", "bi", "s");
     o << "\n";
   }
-  o << "  }\n};\n}\n}\n";
+  o << "  }\n";
+  o << "  template <class Sink>\n"
+       "  __device__ static __forceinline__ void run2(const Builtins &ba, Sink &sa,\n"
+       "                                              const Builtins &bb, Sink &sb) {\n";
+  if (pairable) {
+    for (uint32_t i = 0; i < L.n_regs; ++i) {
+      o << "    int64_t a" << i << " = " << lit(L.reg_init ? L.reg_init[i] : 0) << ";\n";
+      o << "    int64_t b" << i << " = " << lit(L.reg_init ? L.reg_init[i] : 0) << ";\n";
+    }
+    for (uint32_t pc = 0; pc < L.n_code; ++pc) {
+      const auto &I = L.code[pc];
+      if (I.op == HGRD_OP_END) {
+        o << "    return;\n";
+        break;
+      }
+      if (I.op == HGRD_OP_LOAD && (I.sub & 1) && !streamed(I)) {
+        const int32_t p = static_cast<size_t>(I.imm) < L.n_sites ? L.sites[I.imm].param : 0;
+        const std::string sz = sizeLit(I.imm);
+        o << "    { const int64_t va = sa.fetchC(" << p << ", " << idxArg(pc, I.b, I.imm, "a")
+          << ", " << sz << "), vb = sb.fetchC(" << p << ", " << idxArg(pc, I.b, I.imm, "b")
+          << ", " << sz << ");\n";
+        o << "      sa.loadC(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm, "a") << ", false"
+          << buf(I.imm) << "); a" << I.a << " = va;\n";
+        o << "      sb.loadC(" << site(I.imm) << ", " << idxArg(pc, I.b, I.imm, "b") << ", false"
+          << buf(I.imm) << "); b" << I.a << " = vb; }\n";
+        continue;
+      }
+      o << "    ";
+      insn(o, pc, "a", "ba", "sa");
+      o << "\n    ";
+      insn(o, pc, "b", "bb", "sb");
+      o << "\n";
+    }
+  }
+  o << "  }\n";
+  o << "};\n}\n}\n";
   return o.str();
 }
 

@@ -240,7 +240,7 @@ bool stepFree(const hgrd_gpu_launch &L, bool seq) {
 }
 
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
-                     const std::vector<JitParam> &params, bool seq) {
+                     const std::vector<JitParam> &params, bool seq, bool lowOccupancy) {
   std::vector<char> target(L.n_code + 1, 0);
   uint32_t nRec = 0;
   for (uint32_t pc = 0; pc < L.n_code; ++pc) {
@@ -382,10 +382,20 @@ std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
   // checks interleave the threads instruction by instruction, and a
   // value-needed global load fetches both threads' values before either
   // records its access, so the two loads are in flight together (memory-level
-  // parallelism the per-thread interpretation order would serialise).
-  bool pairable = !loops && noStepChecks;
-  for (uint32_t pc = 0; pc < L.n_code && pairable; ++pc)
-    pairable = L.code[pc].op != HGRD_OP_JZ && L.code[pc].op != HGRD_OP_JMP;
+  // parallelism the per-thread interpretation order would serialise).  Only
+  // bodies with such a load, or for the variants of at most two CTAs per SM
+  // (few resident warps: the second thread's independent record pushes fill
+  // the issue slots).  Otherwise the pair only adds code (A/B,
+  // profiles/r02/ab_pair_bits.txt: histogram 2.42 -> 2.52 ms; the x12
+  // transpose 1.67 -> 1.60 ms).
+  bool pairable = !loops && noStepChecks && !std::getenv("HGRD_JIT_NO_PAIR"); // (A/B knob)
+  bool globalValueLoad = false;
+  for (uint32_t pc = 0; pc < L.n_code && pairable; ++pc) {
+    const auto &I = L.code[pc];
+    pairable = I.op != HGRD_OP_JZ && I.op != HGRD_OP_JMP;
+    globalValueLoad |= I.op == HGRD_OP_LOAD && (I.sub & 1) && !streamed(I);
+  }
+  pairable = pairable && (globalValueLoad || lowOccupancy);
 
   std::ostringstream o;
   o << "#include \"jit_kernels.cuh\"\n"
@@ -546,7 +556,8 @@ const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &
   auto it = c->mods.find(key);
   if (it != c->mods.end())
     return it->second;
-  const std::string src = generate(L, rec, params, v == kExpandSeq);
+  const std::string src =
+      generate(L, rec, params, v == kExpandSeq, v == kFused12 || v == kFusedWide);
   const auto t0 = std::chrono::steady_clock::now();
   auto fail = [&](const std::string &why) -> const void * {
     err = why;
@@ -580,7 +591,8 @@ size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
   Cache *c = create();
   std::vector<char> cubin;
   std::string lowered;
-  const std::string src = generate(L, rec, params, v == kExpandSeq);
+  const std::string src =
+      generate(L, rec, params, v == kExpandSeq, v == kFused12 || v == kFusedWide);
   if (const char *dump = std::getenv("HGRD_JIT_DUMP")) { // development: keep the source
     if (FILE *f = std::fopen(dump, "w")) {
       std::fputs(src.c_str(), f);

@@ -39,8 +39,10 @@ void destroy(Cache *c);
 // bit 2: a streamed load (affine.hpp streamSites; k_fused stages its values).
 const void *get(Cache *c, const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                 const std::vector<JitParam> &params, Variant v, std::string &err);
+// lowOccupancy: the k_fused variant keeps at most two CTAs per SM (x12, x16)
 std::string generate(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
-                     const std::vector<JitParam> &params, bool seq = false);
+                     const std::vector<JitParam> &params, bool seq = false,
+                     bool lowOccupancy = false);
 // Compile without loading (no GPU needed): cubin size, 0 and err on failure.
 size_t compileOnly(const hgrd_gpu_launch &L, const std::vector<uint8_t> &rec,
                    const std::vector<JitParam> &params, Variant v, std::string &err);

@@ -961,19 +961,27 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   // 16-byte alignment slack), only with the JIT body that reads them
   const bool streamed = jitKernel && jk.streamSite >= 0;
   const int stageCap = streamed ? static_cast<int>(bpi * D.tpb) + 4 : 0;
-  const size_t smem = (ipt == 4    ? fusedSmemBytes<256, 4>(L, P, nKeys)
-                       : ipt == 8  ? fusedSmemBytes<256, 8>(L, P, nKeys)
-                       : ipt == 12 ? fusedSmemBytes<256, 12>(L, P, nKeys)
-                                   : fusedSmemBytes<256, 16>(L, P, nKeys)) +
-                      (streamed ? 16 + 16 * static_cast<size_t>(stageCap) : 0);
-  if (smem > 227 * 1024)
-    return 0;
-
   // ownership table (device.cuh): the reduction layout (two words per
   // element, epoch-tagged: no memset between launches) when it fits L2
   // comfortably, else the bit map (two bits per element, cleared per launch)
   static const char *redEnv = std::getenv("HGRD_OWNER_RED"); // A/B knob: 0 / 1 forces a layout
   const bool ownerRed = redEnv ? std::atoi(redEnv) != 0 : 8 * P.totalW <= (uint64_t(32) << 20);
+  // small reduction tables: each CTA keeps a bit map of the elements it has
+  // seen become MULTI and skips their joins (a hot 2^16-bin table is joined
+  // by every block; HGRD_NO_KNOWN=1 for A/B)
+  static const bool noKnown = std::getenv("HGRD_NO_KNOWN") != nullptr;
+  const uint32_t knownWords =
+      ownerRed && !noKnown && P.totalW <= kKnownMax ? static_cast<uint32_t>((P.totalW + 31) / 32)
+                                                    : 0;
+  const size_t smem = (ipt == 4    ? fusedSmemBytes<256, 4>(L, P, nKeys)
+                       : ipt == 8  ? fusedSmemBytes<256, 8>(L, P, nKeys)
+                       : ipt == 12 ? fusedSmemBytes<256, 12>(L, P, nKeys)
+                                   : fusedSmemBytes<256, 16>(L, P, nKeys)) +
+                      (streamed ? 16 + 16 * static_cast<size_t>(stageCap) : 0) +
+                      4 * static_cast<size_t>(knownWords);
+  if (smem > 227 * 1024)
+    return 0;
+
   const uint64_t nOwn = std::max<uint64_t>(P.totalW, 1);
   const size_t ownerN = ownerRed ? 2 * nOwn : (nOwn + 15) / 16;
   const bool fresh = c->owner.cap < ownerN;
@@ -1033,6 +1041,7 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
     F.streamSize = sp.size;
     F.stageCap = stageCap;
   }
+  F.knownWords = F.owner ? knownWords : 0;
   int rc = ipt == 4    ? launchFused<256, 4>(c, F, smem, jitKernel)
            : ipt == 8  ? launchFused<256, 8>(c, F, smem, jitKernel)
            : ipt == 12 ? launchFused<256, 12>(c, F, smem, jitKernel)

@@ -33,6 +33,7 @@ namespace dev {
 constexpr int kMaxWritten = 8;
 constexpr int kSmallGroup = 32; // hash slots up to this size, radix grouping above
 constexpr int kMaxIterBlocks = 256; // MiniCU blocks per iteration: the 8-bit blk field of r1
+constexpr uint64_t kKnownMax = 1u << 17; // elements of a CTA's known-MULTI map (16 KB)
 
 enum FusedFlags : uint32_t {
   kFlagShared = 128u,   // an element is accessed by two blocks (pass 2 needed)
@@ -75,6 +76,9 @@ struct FusedArgs {
   const int64_t *stream;
   int64_t streamOff, streamSize;
   int stageCap; // elements per staging buffer
+  // reduction layout, small tables: words of the CTA's shared bit map of
+  // elements it has seen become MULTI (their joins are skipped), else 0
+  uint32_t knownWords;
   // sharded checks: the shard's per-(element, site) min / max block + 1
   // (parallel.py's INTER summary), filled from the records (nullptr: none)
   uint32_t *shardLo, *shardHi;
@@ -192,19 +196,27 @@ __global__ void k_owner_any(const uint32_t *owner, uint64_t nElems, uint32_t epo
     atomicOr(&ctr->flags, static_cast<unsigned>(kFlagShared));
 }
 
-// A thread's ownership OR in flight (bit-map layout, device.cuh): the old
-// word is examined when the thread issues its next OR or at the kernel's
-// end, so the L2 round trip overlaps the next MiniCU thread's expansion
-// instead of stalling this one.  (A late MULTI bit is still set before the
-// kernel ends, and only pass 2 reads it.)
+// A thread's ownership atomic in flight: its old word is examined when the
+// thread issues its next one or at the kernel's end, so the L2 round trip
+// overlaps the next MiniCU thread's expansion instead of stalling this one.
+// * bit map (device.cuh): the touched bit was already set -> the thread
+//   sets e's MULTI bit (a late MULTI bit is still set before the kernel
+//   ends, and only pass 2 reads it);
+// * reduction layout with the CTA's known-MULTI map (`known`): the previous
+//   max(epoch | block+1) was another block's -> e is MULTI, and the CTA's
+//   later joins of e are skipped (MULTI is final within the launch: the
+//   joins already made keep min != max).
 struct OwnerPend {
   uint32_t *addr = nullptr;
-  uint32_t old = 0, sh = 0; // old word, e's bit pair offset
-  __device__ __forceinline__ void settle(unsigned &flags) {
+  uint32_t old = 0, aux = 0, mine = 0; // aux: bit-pair offset, or the element
+  __device__ __forceinline__ void settle(unsigned &flags, uint32_t *known, uint32_t epochTag) {
     if (addr) {
-      if ((old >> sh) & 1u) { // touched before by another block
-        if (!((old >> sh) & 2u))
-          atomicOr(addr, 2u << sh);
+      if (known) {
+        if ((old >> 20) == (epochTag >> 20) && (old & kOwnerMulti) != mine)
+          atomicOr(&known[aux >> 5], 1u << (aux & 31));
+      } else if ((old >> aux) & 1u) { // touched before by another block
+        if (!((old >> aux) & 2u))
+          atomicOr(addr, 2u << aux);
         flags |= kFlagShared;
       }
       addr = nullptr;
@@ -308,7 +320,8 @@ template <class Smem> struct FusedSink : ParState {
   uint32_t epochTag;    // epoch << 20
   uint32_t mine;        // this thread's block + 1
   bool ownerRed = false; // reduction layout of the ownership table (else the bit map)
-  OwnerPend *pend = nullptr; // (bit-map layout) the thread's OR in flight
+  OwnerPend *pend = nullptr; // the thread's ownership atomic in flight
+  uint32_t *known = nullptr;  // the CTA's known-MULTI elements (reduction layout)
   uint32_t *shardLo = nullptr, *shardHi = nullptr; // sharded: (element, site) block min / max
   int nSitesTab = 0;
   // k_batch: every trap of the launch, keyed thread << 20 | n-th trap of the
@@ -377,13 +390,20 @@ template <class Smem> struct FusedSink : ParState {
       atomicMax(&shardHi[i], mine);
     }
     if (own && first && owner) { // the block's first record of e (device.cuh ownership)
-      if (ownerRed) {
-        ownerJoin(owner, e, epochTag, mine);
-      } else {
-        pend->settle(flags);
+      if (!ownerRed) {
+        pend->settle(flags, nullptr, epochTag);
         pend->addr = &owner[e >> 4];
-        pend->sh = 2 * (e & 15);
-        pend->old = atomicOr(pend->addr, 1u << pend->sh);
+        pend->aux = 2 * (e & 15);
+        pend->old = atomicOr(pend->addr, 1u << pend->aux);
+      } else if (!known) {
+        ownerJoin(owner, e, epochTag, mine);
+      } else if (!((known[e >> 5] >> (e & 31)) & 1u)) { // (known MULTI: nothing to add)
+        pend->settle(flags, known, epochTag);
+        atomicMax(&owner[2 * e + 1], epochTag | (kOwnerMulti - mine));
+        pend->addr = &owner[2 * e];
+        pend->aux = e;
+        pend->mine = mine;
+        pend->old = atomicMax(pend->addr, epochTag | mine);
       }
     }
   }
@@ -548,6 +568,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   uint64_t *sConfX = sConf + F.L.nSites;
   int64_t *sStage = reinterpret_cast<int64_t *>(
       (reinterpret_cast<uintptr_t>(sConfX + F.L.nSites) + 15) & ~uintptr_t(15));
+  uint32_t *sKnown = F.knownWords ? reinterpret_cast<uint32_t *>(
+                                         sStage + (F.stream ? 2 * F.stageCap + 2 : 0))
+                                   : nullptr;
   // dynamic shared memory layout mirrored by fusedSmemBytes() in ctx.cu
   __shared__ __align__(8) uint64_t sBar[2];
   __shared__ int64_t sStageBase[2];
@@ -563,6 +586,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
   }
   for (int i = tid; i < L.nParams; i += kFusedThreads)
     sParams[i] = L.params[i];
+  for (uint32_t i = tid; i < F.knownWords; i += kFusedThreads)
+    sKnown[i] = 0;
   for (int i = tid; i < F.nKeys; i += kFusedThreads) {
     sKeyMin[i] = ~0u;
     sKeyBound[i] = ~0u;
@@ -638,6 +663,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
         s.epochTag = F.epoch << 20;
         s.ownerRed = F.ownerRed != 0;
         s.pend = pd;
+        s.known = sKnown;
         s.shardLo = F.shardLo;
         s.shardHi = F.shardHi;
         s.nSitesTab = F.nSitesTab;
@@ -930,8 +956,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       }
     }
   }
-  pend.settle(myFlags);
-  pend2.settle(myFlags);
+  pend.settle(myFlags, sKnown, F.epoch << 20);
+  pend2.settle(myFlags, sKnown, F.epoch << 20);
   // counters
   __syncthreads();
   const int lane = tid & 31;

@@ -23,7 +23,7 @@ void main() { int *A; int *B; int *C; cudaMalloc(&A, 997); cudaMalloc(&B, NT);
   g<<<(GRID,1,1),(BLOCK,1,1)>>>(A, B, C); }
 """
 
-UPDATES = {"store": "C[v % 50] = t;", "atomic": "atomicAdd(&C[v % 50], 1);",
+UPDATES = {"store": "C[v % 50] = t;", "atomic": "atomicAdd(C[v % 50], 1);",
            "none": "B[t] = B[t] + v;"}
 
 
@@ -34,6 +34,7 @@ def _src(grid, block, update, mod=997):
 
 
 def _same(got, want, what):
+    assert "error" not in want, want
     assert strip_extras(got) == strip_extras(want), what
     assert got["witnesses"] == want["witnesses"], what
     assert got["stats"]["instances"] == want["stats"]["instances"], what

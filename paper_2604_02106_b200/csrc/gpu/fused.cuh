@@ -632,8 +632,10 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
       S.hot = 0;
       S.nReal = 0; // (every thread read it after the previous iteration's barrier)
     }
-    for (int i = tid; i < Smem::kTable; i += kFusedThreads)
-      S.u.ch.head[i] = Smem::kEnd;
+    static_assert(Smem::kTable % 4 == 0, "chain heads are reset 16 bytes at a time");
+    for (int i = tid; i < Smem::kTable / 4; i += kFusedThreads) // (S: 16-byte aligned)
+      reinterpret_cast<uint4 *>(S.u.ch.head)[i] =
+          make_uint4(Smem::kEnd, Smem::kEnd, Smem::kEnd, Smem::kEnd);
     __syncthreads();
     // 1. expansion of the iteration's whole MiniCU blocks: records pushed
     //    per hash slot and paired as they are produced (FusedSink)
@@ -704,14 +706,16 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : HGRD_FUSED_MINB) k_fused(F
           finish(s);
         }
       }
+      if (__any_sync(0xffffffffu, myBp | myWp)) { // (barrier-free bodies: one vote)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        myBp = max(myBp, __shfl_down_sync(0xffffffffu, myBp, o));
-        myWp = max(myWp, __shfl_down_sync(0xffffffffu, myWp, o));
-      }
-      if ((tid & 31) == 0 && (myBp | myWp)) {
-        atomicMax(&S.maxBp, myBp);
-        atomicMax(&S.maxWp, myWp);
+        for (int o = 16; o > 0; o >>= 1) {
+          myBp = max(myBp, __shfl_down_sync(0xffffffffu, myBp, o));
+          myWp = max(myWp, __shfl_down_sync(0xffffffffu, myWp, o));
+        }
+        if ((tid & 31) == 0) {
+          atomicMax(&S.maxBp, myBp);
+          atomicMax(&S.maxWp, myWp);
+        }
       }
     }
     __syncthreads();

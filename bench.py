@@ -607,12 +607,12 @@ def run_gpu_arm(args):
     # (sharded: one rank's kernel processes its share of the launch)
     kernel_inst = wl.inst_per_launch // (ws if sharded else 1)
     achieved = wl.b_alg * kernel_inst / (dom_avg_ms / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None  # DRAM bytes per launch, from a committed ncu capture
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        tr = json.load(open(tpath))
-        traffic = tr.get(args.workload, {}).get(dom) if isinstance(tr.get(args.workload),
-                                                                   dict) else None
+        tr = json.load(open(tpath)).get(args.workload)
+        if isinstance(tr, dict) and dom in tr:
+            traffic, traffic_src = tr[dom], tr.get("source")
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -632,7 +632,12 @@ def run_gpu_arm(args):
                    if e2e_serial_s else {})},
         "gpu_launches": n_launch,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": dom,
+                     "frac": achieved / peak, "traffic": traffic,
+                     **({"traffic_unit": "DRAM bytes per launch (ncu)",
+                         "traffic_source": traffic_src,
+                         "alg_bytes_per_launch": wl.inst_per_launch * wl.b_alg}
+                        if traffic is not None else {}),
+                     "kernel": dom,
                      "kernel_avg_ms": dom_avg_ms, "b_alg_per_instance": wl.b_alg,
                      "peak_source": peak_kind,
                      "stage_share": {k: v / sum(stage_ms.values()) for k, v in stage_ms.items()}},

@@ -934,12 +934,21 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
   const int nKeys = 3 * nLocs * nLocs;
   static const int64_t kIterThreads = [] { // development knob: MiniCU threads per iteration
     const char *e = std::getenv("HGRD_FUSED_ITER");
-    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(512);
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
   }();
+  const uint64_t per = std::max<uint32_t>(recInsns, 1);
+  // MiniCU threads per iteration: 512, or 1024 when one record per thread
+  // still fills only the x4 record capacity and the launch is large enough
+  // (2^22+ threads) for the fewer iterations to keep every CTA busy — the
+  // per-iteration barriers and resets are then paid half as often
+  // (A/B: profiles/r02/ab_pair_bits.txt, histogram 1.29 -> 1.12 ms; the
+  // 2^20-thread stencil lost with larger iterations)
+  const int64_t iterThreads =
+      kIterThreads ? kIterThreads
+                   : (!loops && per == 1 && D.nThreads >= (int64_t(1) << 22) ? 1024 : 512);
   // (at most 256: a record keeps its MiniCU block within the iteration in
   // 8 bits, packR1 / rBlk in fused.cuh)
-  int64_t bpi = std::min<int64_t>(kMaxIterBlocks, std::max<int64_t>(1, kIterThreads / D.tpb));
-  const uint64_t per = std::max<uint32_t>(recInsns, 1);
+  int64_t bpi = std::min<int64_t>(kMaxIterBlocks, std::max<int64_t>(1, iterThreads / D.tpb));
   while (bpi > 1 && static_cast<uint64_t>(bpi * D.tpb) * per > 4096)
     bpi /= 2;
   const uint64_t perIter = static_cast<uint64_t>(bpi * D.tpb) * per;

@@ -987,7 +987,9 @@ int runFused(hgrd_gpu_ctx *c, const hgrd_gpu_launch &L, LaunchDev D, const BlobO
                        : ipt == 12 ? fusedSmemBytes<256, 12>(L, P, nKeys)
                                    : fusedSmemBytes<256, 16>(L, P, nKeys)) +
                       (streamed ? 16 + 16 * static_cast<size_t>(stageCap) : 0) +
-                      4 * static_cast<size_t>(knownWords);
+                      (knownWords ? 16 + 4 * static_cast<size_t>(knownWords) : 0);
+  // (+16: the device places the stage and the known map after a 16-byte
+  // alignment of the layout above, which this sum does not round up)
   if (smem > 227 * 1024)
     return 0;
 

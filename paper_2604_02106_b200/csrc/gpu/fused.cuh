@@ -228,9 +228,7 @@ struct OwnerPend {
 template <int NT, int IPT> struct FusedSmem {
   static constexpr int kThreads = NT;
   static constexpr int kCap = NT * IPT;
-  // hash slots: x4 capacity records get four per record (a 1024-record
-  // iteration of one-record threads fills the capacity), the larger ones two
-  static constexpr int kTable = (IPT == 4 ? 4 : 2) * kCap;
+  static constexpr int kTable = 2 * kCap; // hash slots (power of two)
   static constexpr int kLogTable = ilog2(kTable);
   static constexpr uint32_t kEnd = 0xffffffffu;
   using Sort = cub::BlockRadixSort<uint64_t, NT, IPT, uint32_t, 5>;
